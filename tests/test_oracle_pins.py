@@ -1,0 +1,385 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix (not against itself).
+
+Each test names the passage it checks.  Runs on CPU (-m "not gpu").
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+from pfinputs import CONFIGS, reduced, cfg1_problem, cfg1_noise
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+def _rand_sym(n, seed, spec=None):
+    rng = np.random.default_rng(seed)
+    q, r = np.linalg.qr(rng.standard_normal((n, n)))
+    q = q * np.sign(np.diag(r))
+    lam = rng.standard_normal(n) if spec is None else np.asarray(spec, float)
+    return (q * lam) @ q.T, q, lam
+
+
+# ------------------------------------------------------------------ Chebyshev (eq:cheb)
+def test_cheb_golden_values():
+    for g in GOLD["cheb_values"]:
+        assert O.cheb_T(g["d"], g["t"]) == pytest.approx(g["T"], rel=1e-14, abs=1e-14), g["cite"]
+
+
+def test_cheb_closed_form_matches_three_term_recurrence():
+    # T_0 = 1, T_1 = t, T_{k+1} = 2 t T_k - T_{k-1}: the defining recurrence, written here
+    for t in np.concatenate([np.linspace(-3, 3, 61), [-1.0, 1.0, 1.0 + 1e-9]]):
+        t0, t1 = 1.0, t
+        for d in range(0, 20):
+            ref = t0 if d == 0 else t1
+            if d >= 1:
+                t0, t1 = t1, 2 * t * t1 - t0
+            got = O.cheb_T(d, t)
+            assert got == pytest.approx(ref, rel=1e-10, abs=1e-10), (d, t)
+            if d == 0:
+                t0, t1 = 1.0, t
+
+
+def test_cheb_composition_identity():
+    # T_2d(x) = T_d(2x^2 - 1) (used by reading R6)
+    for x in np.linspace(-2.5, 2.5, 41):
+        for d in range(1, 9):
+            assert O.cheb_T(2 * d, x) == pytest.approx(O.cheb_T(d, 2 * x * x - 1), rel=1e-10, abs=1e-10)
+
+
+def test_lemma_cheb_growth_grid():
+    # Lemma lem:cheb-est on the S:610 grid
+    for g in GOLD["growth_bound"]:
+        assert O.growth_lower_bound(g["d"], g["eps"]) == pytest.approx(g["bound"]), g["cite"]
+    for d in range(1, 65):
+        for eps in (1e-4, 1e-3, 1e-2, 0.1, 0.25, 1.0):
+            lb = O.growth_lower_bound(d, eps)
+            assert O.cheb_T(d, 1 + eps) >= lb
+            assert abs(O.cheb_T(d, -(1 + eps))) >= lb
+
+
+# ------------------------------------------------------------------ interval
+def test_interval_rules():
+    for g in GOLD["interval"]:
+        if g["mode"] == "all_positive":
+            assert O.interval_psd(g["a"], g["eta"]) == pytest.approx((g["a"], g["b"])), g["cite"]
+        else:
+            assert O.interval_top_r(g["a"], g["lam_r"], g["eta"]) == pytest.approx((g["a"], g["b"]))
+    with pytest.raises(ValueError):
+        O.interval_psd(1.0, 0.1)
+    with pytest.raises(ValueError):
+        O.interval_map(1.0, 1.0)
+    assert O.interval_map(-10.0, -1.0) == pytest.approx((-5.5, 4.5))
+    assert O.interval_soft(4.0, 0.1) == pytest.approx((-3.6, 3.6))
+
+
+# ------------------------------------------------------------------ filter
+def test_filter_diagonal_golden():
+    g = GOLD["filter_diag"]
+    A = np.diag(g["A_diag"])
+    U = np.array(g["U"])[:, None] / math.sqrt(3)
+    Y = O.chebyshev_filter(A, U, g["a"], g["b"], g["d"])
+    np.testing.assert_allclose(Y[:, 0], np.array(g["Y"]) / math.sqrt(3), rtol=1e-14, atol=1e-14)
+
+
+def test_filter_commutes_with_known_evd():
+    # rho(A) = Q diag(rho(lambda)) Q^T, rho = T_d(L(.)) evaluated by eq:cheb closed form
+    n, p = 40, 5
+    A, Q, lam = _rand_sym(n, 1, spec=np.linspace(-3, 6, n))
+    U = np.random.default_rng(2).standard_normal((n, p))
+    a, b = -3.1, 1.0
+    c, e = (a + b) / 2, (b - a) / 2
+    for d in (1, 2, 5, 9):
+        rho = np.array([O.cheb_T(d, (l - c) / e) for l in lam])
+        ref = (Q * rho) @ (Q.T @ U)
+        Y = O.chebyshev_filter(A, U, a, b, d)
+        assert np.linalg.norm(Y - ref) <= 1e-11 * np.linalg.norm(ref)
+
+
+def test_filter_rebase_preserves_span():
+    # re-basing is right-multiplication of (Y_j, Y_{j-1}) by R^-1: Range(Y_d) unchanged (R7)
+    n, p, d = 60, 6, 10
+    rng = np.random.default_rng(4)
+    # (i) mild growth: the un-rebased recurrence is accurate, all plans agree to rounding
+    A, Q, lam = _rand_sym(n, 3, spec=np.concatenate([np.linspace(1.2, 2.0, 6), np.linspace(-1, 1, n - 6)]))
+    U = np.linalg.qr(rng.standard_normal((n, p)))[0]
+    Y0 = O.orth(O.chebyshev_filter(A, U, -1.1, 1.1, d))
+    for plan in ([2, 5, 7], [1, 2, 3, 4, 5, 6, 7, 8, 9]):
+        Y1 = O.orth(O.chebyshev_filter(A, U, -1.1, 1.1, d, rebase_after=plan))
+        assert np.max(O.sin_theta(Y0, Y1)) < 1e-12
+    # (ii) large growth (kappa(Y_d) ~ 1e9): re-based filters agree with each other and with the
+    # exact filtered span Q diag(T_d) Q^T U to its own distance from the top eigenspace
+    A, Q, lam = _rand_sym(n, 3, spec=np.concatenate([np.linspace(5, 40, 6), np.linspace(-1, 1, n - 6)]))
+    Ya = O.orth(O.chebyshev_filter(A, U, -1.1, 1.1, d, rebase_after=[2, 5, 7]))
+    Yb = O.orth(O.chebyshev_filter(A, U, -1.1, 1.1, d, rebase_after=list(range(1, d))))
+    assert np.max(O.sin_theta(Ya, Yb)) < 1e-12
+    top = Q[:, np.argsort(-lam)[:p]]
+    bound = 1.0 / O.cheb_T(d, 5 / 1.1)     # eq:err-oi shape: max inside [-1,1] is 1
+    assert np.max(O.sin_theta(top, Ya)) < 10 * bound * np.linalg.norm(np.linalg.pinv(top.T @ U))
+    plan = O.rebase_plan(-1.1, 1.1, 40.0, d, 1e6)
+    assert plan and all(1 <= j < d for j in plan)
+
+
+def test_orth_properties():
+    Y = np.random.default_rng(5).standard_normal((50, 7)) @ np.diag(10.0 ** np.arange(7))
+    Q = O.orth(Y)
+    assert np.linalg.norm(Q.T @ Q - np.eye(7)) < 1e-14 * 7
+    assert np.linalg.norm(Y - Q @ (Q.T @ Y)) < 1e-13 * np.linalg.norm(Y)
+
+
+# ------------------------------------------------------------------ Rayleigh-Ritz (eqn:RR)
+def test_rayleigh_ritz_golden_and_interlacing():
+    g = GOLD["rayleigh_ritz_invariant"]
+    A = np.diag(g["A_diag"])
+    th, V = O.rayleigh_ritz(A, np.eye(3)[:, g["U_cols"]])
+    np.testing.assert_allclose(th, g["values"], atol=1e-15)
+    g2 = GOLD["small_eig"]
+    th, _ = O.rayleigh_ritz(np.array(g2["H"]), np.eye(2))
+    np.testing.assert_allclose(th, g2["values"], atol=1e-14)
+    A, _, lam = _rand_sym(6, 7)
+    U = np.linalg.qr(np.random.default_rng(8).standard_normal((6, 3)))[0]
+    th, _ = O.rayleigh_ritz(A, U)
+    assert th.min() >= lam.min() - 1e-12 and th.max() <= lam.max() + 1e-12
+    assert np.all(np.diff(th) <= 0)
+
+
+def test_jacobi_against_lapack_and_closed_forms():
+    lam, V = O.jacobi_eig(np.array(GOLD["small_eig"]["H"]))
+    np.testing.assert_allclose(lam, [3.0, 1.0], atol=1e-15)
+    np.testing.assert_allclose(np.abs(V[:, 0]), [2 ** -0.5] * 2, atol=1e-15)
+    for n, seed in ((8, 1), (33, 2)):
+        H, _, _ = _rand_sym(n, seed)
+        lam, V = O.jacobi_eig(H)
+        assert np.linalg.norm(H @ V - V * lam) <= 1e-13 * np.linalg.norm(H)
+        assert np.linalg.norm(V.T @ V - np.eye(n)) <= 1e-13 * n
+        np.testing.assert_allclose(lam, np.sort(np.linalg.eigvalsh(H))[::-1], atol=1e-12)
+
+
+def test_invariant_subspace_exactness():
+    n = 30
+    A, Q, lam = _rand_sym(n, 9, spec=np.linspace(-5, 5, n))
+    U = Q[:, :4] @ np.linalg.qr(np.random.default_rng(1).standard_normal((4, 4)))[0]
+    th, V = O.rayleigh_ritz(A, U)
+    np.testing.assert_allclose(np.sort(th), np.sort(lam[:4]), atol=1e-13)
+    assert np.linalg.norm(A @ V - V * th) < 1e-12
+
+
+# ------------------------------------------------------------------ spectral operators
+def test_project_and_map_golden():
+    for g in GOLD["project_and_map"]:
+        th = np.array(g["theta"])
+        f = O.spectral_psd(th) if g["op"] == "psd" else O.spectral_soft(th, g["thr"])
+        np.testing.assert_allclose(f, g["f"], atol=1e-15)
+    np.testing.assert_allclose(O.spectral_soft(np.array([-3.0, 0.2]), 0.5), [-2.5, 0.0])
+
+
+@pytest.mark.parametrize("op", ["psd", "soft"])
+def test_p_equals_n_special_case(op):
+    # Range(U) = R^n => P_U(A) = A and the filtered step is the exact spectral operator,
+    # for any interval and degree.  Reference: brute-force Jacobi EVD (independent of LAPACK).
+    n = 14
+    A, _, _ = _rand_sym(n, 11)
+    U = np.random.default_rng(12).standard_normal((n, n))
+    U = O.filter_update(A, U, -0.8, 0.8, 3)
+    th, V = O.rayleigh_ritz(A, U)
+    thr = 0.4
+    f = O.spectral_psd(th) if op == "psd" else O.spectral_soft(th, thr)
+    X = (V * f) @ V.T
+    Xe = O.exact_spectral(A, op, thr)
+    assert np.linalg.norm(X - Xe) <= 1e-12 * max(1.0, np.linalg.norm(Xe))
+
+
+def test_moreau_and_soft_threshold_optimality():
+    A, _, _ = _rand_sym(20, 13)
+    P = O.exact_spectral(A, "psd")
+    assert np.linalg.norm(O.exact_spectral(P, "psd") - P) < 1e-12            # idempotent
+    assert np.linalg.eigvalsh(P).min() > -1e-12                             # PSD
+    assert np.linalg.eigvalsh(A - P).max() < 1e-12                          # A - P_+(A) NSD
+    assert abs(np.sum(P * (A - P))) < 1e-12                                 # complementarity
+    thr = 0.5
+    X = O.exact_spectral(A, "soft", thr)
+    assert np.linalg.norm(A - X, 2) <= thr + 1e-12
+    nuc = np.sum(np.abs(np.linalg.eigvalsh(X)))
+    assert np.sum((A - X) * X) == pytest.approx(thr * nuc, rel=1e-11, abs=1e-11)
+
+
+def test_convergence_in_degree_on_config1_spectrum():
+    # eq:err-oi: error of P_+(P_U(A)) vs exact P_+(A) decreases as d grows (one sweep
+    # from the same random block; config-1 A_0, well separated spectrum)
+    cfg = CONFIGS[1]
+    A = cfg1_problem(cfg)
+    lam, Q = np.linalg.eigh(A)
+    Xe = (Q * np.maximum(lam, 0)) @ Q.T
+    U0 = np.linalg.qr(np.random.default_rng(0).standard_normal((cfg.n, cfg.p)))[0]
+    a, b = O.interval_psd(lam.min() * 1.001, 0.1)
+    errs = []
+    for d in (1, 2, 4, 8, 16):
+        U = O.filter_update(A, U0, a, b, d, rebase_after=O.rebase_plan(a, b, 10.0, d, 1e6))
+        th, V = O.rayleigh_ritz(A, U)
+        f = O.spectral_psd(th)
+        errs.append(np.linalg.norm((V * f) @ V.T - Xe) / np.linalg.norm(Xe))
+    assert all(errs[i + 1] < errs[i] for i in range(len(errs) - 1)), errs
+    assert errs[-1] < 1e-12
+
+
+def test_lanczos_extremes_known_spectrum():
+    n = 300
+    spec = np.concatenate([[-7.0], np.linspace(-3, 2, n - 2), [4.0]])
+    A, _, _ = _rand_sym(n, 14, spec=spec)
+    lo, hi = O.lanczos_extremes(A, np.random.default_rng(15).standard_normal(n), 20)
+    assert lo <= -7.0 + 1e-10 and lo > -7.0 - 0.5
+    assert hi >= 4.0 - 1e-10 and hi < 4.5
+    lo, hi = O.lanczos_extremes(np.diag([1.0, 2.0, 3.0]), np.ones(3), 20)   # breakdown at 3 steps
+    assert lo == pytest.approx(1.0) and hi == pytest.approx(3.0)
+
+
+# ------------------------------------------------------------------ PFAM
+def test_prox_affine_golden_and_feasibility():
+    out = O.prox_tG_diag(np.zeros((3, 3)), np.zeros((3, 3)), 1.0)
+    np.testing.assert_array_equal(out, np.eye(3))
+    rng = np.random.default_rng(3)
+    Y = rng.standard_normal((6, 6)); Y = Y + Y.T
+    C = rng.standard_normal((6, 6)); C = C + C.T
+    P = O.prox_tG_diag(Y, C, 0.7)
+    np.testing.assert_allclose(np.diag(P), 1.0, atol=1e-15)
+    # prox optimality: P - (Y - tC) is in Range(A^*) = diagonal matrices
+    D = P - (Y - 0.7 * C)
+    assert np.linalg.norm(D - np.diag(np.diag(D))) < 1e-14
+
+
+def _exact_drs(C, t, iters, n):
+    Z = np.zeros((n, n))
+    for _ in range(iters):
+        th, V = O.rayleigh_ritz(Z, np.eye(n))         # p = n: exact P_+
+        f = O.spectral_psd(th)
+        Z, cw, res = O.pfam_next(V, f, Z, C, t)
+    th, V = O.rayleigh_ritz(Z, np.eye(n))
+    f = O.spectral_psd(th)
+    return (V * f) @ V.T, cw, res
+
+
+def test_pfam_two_node_maxcut():
+    g = GOLD["maxcut_2node"]
+    adj = np.array(g["adj"], bool)
+    C = O.maxcut_C(adj, adj.sum(1))
+    X, cw, res = _exact_drs(C, 1.0, 200, 2)
+    assert cw == pytest.approx(g["opt_value"], abs=1e-9)
+    np.testing.assert_allclose(X, g["X_opt"], atol=1e-8)
+
+
+def test_pfam_five_cycle_closed_form():
+    # corrected prox sign (reading R1) reaches the C5 max-cut SDP value -(25+5 sqrt5)/8
+    n = 5
+    adj = np.zeros((n, n), bool)
+    for i in range(n):
+        adj[i, (i + 1) % n] = adj[(i + 1) % n, i] = True
+    C = O.maxcut_C(adj, adj.sum(1))
+    X, cw, res = _exact_drs(C, 1.0, 3000, n)
+    assert cw == pytest.approx(-(25 + 5 * math.sqrt(5)) / 8, abs=1e-7)
+    assert res < 1e-7
+    np.testing.assert_allclose(np.diag(X), 1.0, atol=1e-7)
+
+
+def test_pfam_literal_paper_sign_fails():
+    # the sign printed at P:381 converges to a different point (documents reading R1)
+    n = 5
+    adj = np.zeros((n, n), bool)
+    for i in range(n):
+        adj[i, (i + 1) % n] = adj[(i + 1) % n, i] = True
+    C = O.maxcut_C(adj, adj.sum(1))
+    Z = np.zeros((n, n))
+    for _ in range(2000):
+        lam, Q = np.linalg.eigh(Z)
+        W = (Q * np.maximum(lam, 0)) @ Q.T
+        Y = 2 * W - Z
+        Yc = Y + C                                  # literal (Y + tC)
+        P = Yc - np.diag(np.diag(Yc) - 1)
+        Z = P - W + Z
+    assert np.sum(C * W) > -4.0
+
+
+def test_pfam_fixed_point():
+    n = 5
+    adj = np.zeros((n, n), bool)
+    for i in range(n):
+        adj[i, (i + 1) % n] = adj[(i + 1) % n, i] = True
+    C = O.maxcut_C(adj, adj.sum(1))
+    Z = np.zeros((n, n))
+    for _ in range(4000):
+        th, V = O.rayleigh_ritz(Z, np.eye(n))
+        Z, _, _ = O.pfam_next(V, O.spectral_psd(th), Z, C, 1.0)
+    th, V = O.rayleigh_ritz(Z, np.eye(n))
+    Z2, _, res = O.pfam_next(V, O.spectral_psd(th), Z, C, 1.0)
+    assert np.linalg.norm(Z2 - Z) < 1e-9
+
+
+# ------------------------------------------------------------------ PFPG
+def test_pfpg_p_equals_n_is_exact_prox_gradient():
+    # with p = n the driver is exact PG: X+ = soft(X - tau Omega o (X - M), tau mu); compare
+    # step by step with a brute-force (Jacobi EVD) prox-gradient, and objective non-increasing
+    cfg = reduced(CONFIGS[2], n=24, p=24, d=3, iters=8, r=2, omega_prob=0.5, warmup=1)
+    res = O.run(cfg)
+    from pfinputs import pfpg_problem, unpack_bitmask
+    prob = pfpg_problem(cfg)
+    Om = unpack_bitmask(prob["omega_bits"], cfg.n).astype(float)
+    M = prob["W"] @ prob["W"].T
+    X = np.zeros((cfg.n, cfg.n))
+    objs = []
+    for rec in res["records"]:
+        A = X - cfg.tau * Om * (X - M)
+        X = O.exact_spectral(A, "soft", cfg.tau * prob["mu"])
+        Xf = (rec["V"] * rec["f"]) @ rec["V"].T
+        assert np.linalg.norm(Xf - X) <= 1e-11 * max(1.0, np.linalg.norm(X))
+        fit = 0.5 * np.sum((Om * (X - M)) ** 2)
+        nuc = np.sum(np.abs(np.linalg.eigvalsh(X)))
+        assert rec["objective"] == pytest.approx(fit + prob["mu"] * nuc, rel=1e-10)
+        objs.append(rec["objective"])
+    assert all(objs[i + 1] <= objs[i] * (1 + 1e-12) for i in range(len(objs) - 1))
+
+
+def test_config1_k0_equals_exact_projection():
+    cfg = CONFIGS[1]
+    res = O.run(cfg, iters=1)
+    A = cfg1_problem(cfg)
+    lam, Q = np.linalg.eigh(A)
+    rec = res["records"][0]
+    err = O.lowrank_diff_fro(rec["V"], rec["f"], Q[:, lam > 0], lam[lam > 0])
+    assert err <= 1e-12 * np.linalg.norm(lam[lam > 0])
+
+
+def test_sweep_p_equals_n_tracks_exact_projection():
+    cfg = reduced(CONFIGS[1], n=16, p=16, iters=5, lanczos_steps=8)
+    res = O.run(cfg)
+    A = cfg1_problem(cfg)
+    for rec in res["records"]:
+        Xe = O.exact_spectral(A, "psd")
+        assert O.lowrank_diff_fro(rec["V"], rec["f"], np.eye(16), np.zeros(16)) == pytest.approx(
+            np.linalg.norm(Xe), rel=1e-12)
+        assert np.linalg.norm((rec["V"] * rec["f"]) @ rec["V"].T - Xe) < 1e-12 * np.linalg.norm(Xe)
+        A = A + cfg1_noise(cfg, rec["k"])
+
+
+# ------------------------------------------------------------------ metrics
+def test_sin_theta_golden_and_identity():
+    g = GOLD["sin_theta_half"]
+    assert O.sin_theta(np.array(g["X"]), np.array(g["Y"])).max() == pytest.approx(g["max"])
+    rng = np.random.default_rng(21)
+    for _ in range(20):
+        X = np.linalg.qr(rng.standard_normal((12, 3)))[0]
+        Y = np.linalg.qr(rng.standard_normal((12, 3)))[0]
+        s = O.sin_theta(X, Y).max()
+        assert s == pytest.approx(np.linalg.norm(X @ X.T - Y @ Y.T, 2), abs=1e-12)
+        assert O.sin_theta(X, Y) == pytest.approx(O.sin_theta(Y, X), abs=1e-12)
+
+
+def test_lowrank_diff_fro_brute_force():
+    rng = np.random.default_rng(22)
+    V1, V2 = rng.standard_normal((40, 5)), rng.standard_normal((40, 3))
+    f1, f2 = rng.standard_normal(5), rng.standard_normal(3)
+    ref = np.linalg.norm((V1 * f1) @ V1.T - (V2 * f2) @ V2.T)
+    assert O.lowrank_diff_fro(V1, f1, V2, f2) == pytest.approx(ref, rel=1e-13)
+    assert O.lowrank_fro(V1, f1) == pytest.approx(np.linalg.norm((V1 * f1) @ V1.T), rel=1e-13)
+    assert O.lowrank_diff_fro(V1, f1, V1, f1) < 1e-12
