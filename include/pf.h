@@ -1,0 +1,150 @@
+/*
+ * pf.h -- C ABI of the B200 hot path of the polynomial-filtered first-order methods PFPG / PFAM
+ * (Liu, Wen, Zhang et al., arXiv 1904.10585).  Citations "P:n" are lines of the paper's LaTeX
+ * source with the equation label; DESIGN.md lists the readings R1..R14.
+ *
+ * Conventions (all entry points)
+ *  - Every matrix argument is a DEVICE pointer to fp64 data, ROW-MAJOR, with leading dimension
+ *    (elements between consecutive rows) given next to it.  ld must be >= the row length, even
+ *    (TMA needs 16-byte row pitch) and the base 16-byte aligned.
+ *  - n is the matrix order, p the block width (p % 8 == 0, 8 <= p <= 128, p <= n).
+ *  - With world > 1 (pf_create_dist) rank g owns rows [row0, row0 + n_local) of every n-row
+ *    object (A, Z, U, V) where row0 = g*n/world (integer division); those row blocks are what
+ *    the caller passes.  Small objects (theta, f, rank, obj, interval) are replicated.
+ *  - Scalar outputs are device pointers so a whole iteration can be captured in a CUDA graph.
+ *  - The caller allocates all arguments; the context owns only scratch allocated in pf_create.
+ *    No call allocates device memory.  One context is used by one host thread at a time; calls
+ *    are stream-ordered on the stream argument and never synchronise the host (except
+ *    pf_get_device_status, which synchronises `stream`).
+ *  - Argument errors are returned synchronously (nothing is enqueued).  Numerical events
+ *    (Cholesky shift used, non-finite values, degenerate interval, saturation) set bits in a
+ *    device status word read by pf_get_device_status.
+ */
+#ifndef PF_H_
+#define PF_H_
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pf_ctx_s* pf_ctx;
+typedef void* pf_stream; /* a cudaStream_t; NULL = legacy default stream */
+
+typedef enum { PF_FP64 = 0 } pf_dtype; /* fp64 storage + fp64 DMMA tensor cores */
+
+typedef enum { PF_OP_PSD = 0, PF_OP_SOFT_THRESHOLD = 1 } pf_op;
+
+typedef enum {
+  PF_OK = 0,
+  PF_ERR_ARG = 1,       /* invalid argument (null pointer, q or degree out of range, bad op) */
+  PF_ERR_DIM = 2,       /* dimension / leading-dimension / alignment mismatch */
+  PF_ERR_INTERVAL = 3,  /* b <= a */
+  PF_ERR_CUDA = 4,      /* a CUDA runtime call failed (message in pf_last_error) */
+  PF_ERR_NOMEM = 5,     /* scratch allocation failed in pf_create */
+  PF_ERR_NCCL = 6,      /* NCCL initialisation / collective failed */
+  PF_ERR_UNSUPPORTED = 7
+} pf_status;
+
+/* device status word bits (pf_get_device_status) */
+#define PF_FLAG_CHOL_SHIFT 0x1u      /* CholeskyQR fell back to the shifted variant (3 passes) */
+#define PF_FLAG_NONFINITE 0x2u       /* a non-finite value reached the Gram / H matrix */
+#define PF_FLAG_DEGENERATE_INT 0x4u  /* PSD interval needed a < 0 but the estimate was >= 0 */
+#define PF_FLAG_SATURATED 0x8u       /* rank == p after the spectral operator */
+#define PF_FLAG_JACOBI_MAXSWEEP 0x10u /* Jacobi hit its sweep limit before the tolerance */
+#define PF_FLAG_LANCZOS_BREAK 0x20u  /* Lanczos stopped early (invariant subspace found) */
+
+/* ---------------------------------------------------------------------------- lifetime */
+/* Create a single-GPU context for order-n problems with block width p and Chebyshev degree
+ * `degree` (1 <= degree <= 64) on the current CUDA device.  Allocates all scratch. */
+pf_status pf_create(int64_t n, int32_t p, int32_t degree, pf_dtype dtype, pf_ctx* out);
+
+/* Same, for rank `rank` of `world` processes (one per GPU) sharing the NCCL unique id
+ * `nccl_id` (128 bytes, from ncclGetUniqueId on one rank, broadcast by the caller).
+ * Row block of this rank: rows [rank*n/world, (rank+1)*n/world). */
+pf_status pf_create_dist(int64_t n, int32_t p, int32_t degree, pf_dtype dtype,
+                         const void* nccl_id, int32_t rank, int32_t world, pf_ctx* out);
+
+pf_status pf_destroy(pf_ctx ctx);
+const char* pf_status_string(pf_status s);
+const char* pf_last_error(pf_ctx ctx);      /* last CUDA/NCCL error text of this context */
+int64_t pf_local_rows(pf_ctx ctx);          /* n_local of this rank */
+int64_t pf_row0(pf_ctx ctx);                /* first global row of this rank */
+
+/* Synchronises `stream`, then returns (and clears) the device status word, the number of
+ * re-basing steps executed since the last call and the last Lanczos extremes estimate. */
+pf_status pf_get_device_status(pf_ctx ctx, pf_stream stream, uint32_t* flags, int32_t* rebases,
+                               double* lanczos_lo_hi /* [2], may be NULL */);
+
+/* ---------------------------------------------------------------------------- interval
+ * The suppression interval [a, b] lives in device memory (double[2]) so it can be computed
+ * on the device.  Every pf_filter call reads it from `interval`.                         */
+
+/* m-step Lanczos with full re-orthogonalisation on the symmetric A (reading R5):
+ * writes lo_hi[0] = theta_min - |r_min|, lo_hi[1] = theta_max + |r_max| (device double[2]),
+ * and remembers them in the context.  v0: device start vector (n_local entries, any norm).
+ * 1 <= m <= 64. */
+pf_status pf_lanczos(pf_ctx ctx, const double* A, int64_t lda, const double* v0, int32_t m,
+                     double* lo_hi, pf_stream stream);
+
+/* PSD / all-positive interval: a = lo_hi[0], b = eta * a.  Writes interval[2]. */
+pf_status pf_interval_psd(pf_ctx ctx, const double* lo_hi, double eta, double* interval,
+                          pf_stream stream);
+
+/* Two-sided soft-threshold interval [-beta, beta], beta = (1 - eta) * thr (reading R6). */
+pf_status pf_interval_soft(pf_ctx ctx, double thr, double eta, double* interval,
+                           pf_stream stream);
+
+/* ---------------------------------------------------------------------------- hot path */
+/* U <- orth(rho^q(A) U) with rho(t) = T_d(L(t)), L(t) = (t - (a+b)/2)/((b-a)/2)
+ * (eq:cheb P:185-191, eqn:cheb-linear-map P:216-218, eqn:subspace-update P:225-227).
+ * Three-term recurrence Y_1 = (A Y_0 - c Y_0)/e, Y_{j+1} = (2/e)(A Y_j - c Y_j) - Y_{j-1};
+ * span-exact re-basing when the predicted amplification exceeds rho_max (reading R7);
+ * orth = CholeskyQR2 with a shifted CholeskyQR3 fallback ("a single QR" -> any
+ * span-exact orthonormalisation).  A: n_local x n (lda), U: n_local x p (ldu), in place.
+ * interval: device double[2] {a, b}.  1 <= q <= 10. */
+pf_status pf_filter(pf_ctx ctx, const double* A, int64_t lda, double* U, int64_t ldu,
+                    const double* interval, int32_t q, double rho_max, pf_stream stream);
+
+/* U <- orth(U) (CholeskyQR2 + shifted fallback).  U: n_local x p. */
+pf_status pf_orth(pf_ctx ctx, double* U, int64_t ldu, pf_stream stream);
+
+/* Rayleigh-Ritz (eqn:RR P:269-286): H = U^T A U (symmetrised), H = Y Lambda Y^T by an on-device
+ * parallel cyclic Jacobi, theta = Ritz values DESCENDING (device double[p]), V = U Y
+ * (n_local x p, ldv).  U must be orthonormal (output of pf_filter / pf_orth). */
+pf_status pf_rayleigh_ritz(pf_ctx ctx, const double* A, int64_t lda, const double* U,
+                           int64_t ldu, double* V, int64_t ldv, double* theta, pf_stream stream);
+
+/* Spectral operator on the Ritz values: PSD f = max(theta, 0) or soft threshold
+ * f = sign(theta) max(|theta| - thr, 0) (shrink).  f: device double[p];
+ * rank: device int32 = #{f != 0}. */
+pf_status pf_spectral_op(pf_ctx ctx, pf_op op, double thr, const double* theta, double* f,
+                         int32_t* rank, pf_stream stream);
+
+/* PFPG update for F = 1/2 ||P_Omega(X - M)||_F^2, M = W W^T (eq:pfpg1 P:338-341):
+ * X = V diag(f) V^T, A_out = X - tau * Omega o (X - M)  (n_local x n, lda_out).
+ * omega: packed row-major symmetric bitmask, uint32 words, bit (j & 31) of word [i][j >> 5],
+ * row pitch ldo words (>= ceil(n/32)), local rows.  W: n x r FULL (all rows), ldw >= r,
+ * 0 <= r <= 64.  obj: device double[2] = {1/2 ||P_Omega(X - M)||_F^2, sum_i |f_i|}. */
+pf_status pf_prox_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f, double tau,
+                       const uint32_t* omega, int64_t ldo, const double* W, int64_t ldw,
+                       int32_t r, double* A_out, int64_t lda_out, double* obj,
+                       pf_stream stream);
+
+/* PFAM update for the max-cut SDP min <C,X> s.t. diag(X) = 1, X PSD, C = -L/4 (eq:PFAM1 P:389
+ * with the prox sign corrected, reading R1): W = V diag(f) V^T,
+ * Z <- prox_tG(2W - Z) - W + Z = offdiag(W - tC) + Diag(1 - W_ii + Z_ii), in place.
+ * adj: packed adjacency bitmask (as omega above, local rows, no self loops); deg: device
+ * double[n] FULL degree vector.  obj: device double[2] = {<C, W>, ||Z_new - Z_old||_F}. */
+pf_status pf_admm_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f, double t,
+                       const uint32_t* adj, int64_t ldadj, const double* deg, double* Z,
+                       int64_t ldz, double* obj, pf_stream stream);
+
+/* Workload helper (not the method): A <- A + E (config 1 noise, BASELINE configs[0]). */
+pf_status pf_perturb(pf_ctx ctx, double* A, int64_t lda, const double* E, int64_t lde,
+                     pf_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PF_H_ */

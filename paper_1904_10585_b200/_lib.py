@@ -1,0 +1,178 @@
+"""ctypes binding of libpf.so (include/pf.h).  Argument marshalling only: every step of the
+hot path runs in the CUDA kernels behind the C ABI.  There is no CPU fallback -- if the shared
+library is missing or fails to load, importing the binding raises."""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libpf.so")
+
+PF_FP64 = 0
+PF_OP_PSD = 0
+PF_OP_SOFT_THRESHOLD = 1
+STATUS = {0: "PF_OK", 1: "PF_ERR_ARG", 2: "PF_ERR_DIM", 3: "PF_ERR_INTERVAL", 4: "PF_ERR_CUDA",
+          5: "PF_ERR_NOMEM", 6: "PF_ERR_NCCL", 7: "PF_ERR_UNSUPPORTED"}
+FLAGS = {0x1: "CHOL_SHIFT", 0x2: "NONFINITE", 0x4: "DEGENERATE_INTERVAL", 0x8: "SATURATED",
+         0x10: "JACOBI_MAXSWEEP", 0x20: "LANCZOS_BREAK"}
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load libpf.so (raises if it was not built -- no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: run __graft_entry__.build() (no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, I64, I32, D, U32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double, ctypes.c_uint32
+    sig = {
+        "pf_create": [I64, I32, I32, I32, ctypes.POINTER(P)],
+        "pf_create_dist": [I64, I32, I32, I32, P, I32, I32, ctypes.POINTER(P)],
+        "pf_destroy": [P],
+        "pf_status_string": [I32],
+        "pf_last_error": [P],
+        "pf_local_rows": [P],
+        "pf_row0": [P],
+        "pf_get_device_status": [P, P, ctypes.POINTER(U32), ctypes.POINTER(I32), P],
+        "pf_lanczos": [P, P, I64, P, I32, P, P],
+        "pf_interval_psd": [P, P, D, P, P],
+        "pf_interval_soft": [P, D, D, P, P],
+        "pf_filter": [P, P, I64, P, I64, P, I32, D, P],
+        "pf_orth": [P, P, I64, P],
+        "pf_rayleigh_ritz": [P, P, I64, P, I64, P, I64, P, P],
+        "pf_spectral_op": [P, I32, D, P, P, P, P],
+        "pf_prox_step": [P, P, I64, P, D, P, I64, P, I64, I32, P, I64, P, P],
+        "pf_admm_step": [P, P, I64, P, D, P, I64, P, P, I64, P, P],
+        "pf_perturb": [P, P, I64, P, I64, P],
+    }
+    for name, args in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = ctypes.c_int32
+    lib.pf_status_string.restype = ctypes.c_char_p
+    lib.pf_last_error.restype = ctypes.c_char_p
+    lib.pf_local_rows.restype = ctypes.c_int64
+    lib.pf_row0.restype = ctypes.c_int64
+    _lib = lib
+    return lib
+
+
+class PFError(RuntimeError):
+    pass
+
+
+def _ptr(t) -> int | None:
+    if t is None:
+        return None
+    if isinstance(t, torch.Tensor):
+        if not t.is_cuda:
+            raise PFError("pf: tensors must live on the GPU (no CPU fallback)")
+        return t.data_ptr()
+    return int(t)
+
+
+def _ld(t: torch.Tensor) -> int:
+    if t.dim() != 2 or t.stride(1) != 1:
+        raise PFError("pf: matrices must be 2-D row-major with unit column stride")
+    return t.stride(0)
+
+
+def _stream(stream) -> int | None:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+class Context:
+    """One pf_ctx: scratch for order-n problems with block width p and degree d."""
+
+    def __init__(self, n: int, p: int, d: int, nccl_id: bytes | None = None, rank: int = 0,
+                 world: int = 1):
+        self.lib = load()
+        self.n, self.p, self.d = n, p, d
+        h = ctypes.c_void_p()
+        if world == 1:
+            st = self.lib.pf_create(n, p, d, PF_FP64, ctypes.byref(h))
+        else:
+            buf = ctypes.create_string_buffer(nccl_id, 128)
+            st = self.lib.pf_create_dist(n, p, d, PF_FP64, buf, rank, world, ctypes.byref(h))
+        if st != 0:
+            raise PFError(f"pf_create failed: {STATUS.get(st, st)}")
+        self.h = h
+        self.n_local = self.lib.pf_local_rows(h)
+        self.row0 = self.lib.pf_row0(h)
+
+    def _check(self, st: int, what: str):
+        if st != 0:
+            msg = self.lib.pf_last_error(self.h).decode()
+            raise PFError(f"{what}: {STATUS.get(st, st)} {msg}")
+
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            self.lib.pf_destroy(self.h)
+            self.h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------ ABI wrappers
+    def status(self, stream=None):
+        fl, rb = ctypes.c_uint32(), ctypes.c_int32()
+        lohi = (ctypes.c_double * 2)()
+        self._check(self.lib.pf_get_device_status(self.h, _stream(stream), ctypes.byref(fl),
+                                                  ctypes.byref(rb), lohi), "pf_get_device_status")
+        names = [v for k, v in FLAGS.items() if fl.value & k]
+        return {"flags": fl.value, "names": names, "rebases": rb.value, "lanczos": (lohi[0], lohi[1])}
+
+    def lanczos(self, A, v0, m, lo_hi, stream=None):
+        self._check(self.lib.pf_lanczos(self.h, _ptr(A), _ld(A), _ptr(v0), m, _ptr(lo_hi),
+                                        _stream(stream)), "pf_lanczos")
+
+    def interval_psd(self, lo_hi, eta, interval, stream=None):
+        self._check(self.lib.pf_interval_psd(self.h, _ptr(lo_hi), eta, _ptr(interval),
+                                             _stream(stream)), "pf_interval_psd")
+
+    def interval_soft(self, thr, eta, interval, stream=None):
+        self._check(self.lib.pf_interval_soft(self.h, thr, eta, _ptr(interval), _stream(stream)),
+                    "pf_interval_soft")
+
+    def filter(self, A, U, interval, q=1, rho_max=1e6, stream=None):
+        self._check(self.lib.pf_filter(self.h, _ptr(A), _ld(A), _ptr(U), _ld(U), _ptr(interval),
+                                       q, rho_max, _stream(stream)), "pf_filter")
+
+    def orth(self, U, stream=None):
+        self._check(self.lib.pf_orth(self.h, _ptr(U), _ld(U), _stream(stream)), "pf_orth")
+
+    def rayleigh_ritz(self, A, U, V, theta, stream=None):
+        self._check(self.lib.pf_rayleigh_ritz(self.h, _ptr(A), _ld(A), _ptr(U), _ld(U), _ptr(V),
+                                              _ld(V), _ptr(theta), _stream(stream)),
+                    "pf_rayleigh_ritz")
+
+    def spectral_op(self, op, thr, theta, f, rank, stream=None):
+        self._check(self.lib.pf_spectral_op(self.h, op, thr, _ptr(theta), _ptr(f), _ptr(rank),
+                                            _stream(stream)), "pf_spectral_op")
+
+    def prox_step(self, V, f, tau, omega, W, A_out, obj, stream=None):
+        r = 0 if W is None else W.shape[1]
+        ldw = 0 if W is None else _ld(W)
+        self._check(self.lib.pf_prox_step(self.h, _ptr(V), _ld(V), _ptr(f), tau, _ptr(omega),
+                                          _ld(omega), _ptr(W), ldw, r, _ptr(A_out), _ld(A_out),
+                                          _ptr(obj), _stream(stream)), "pf_prox_step")
+
+    def admm_step(self, V, f, t, adj, deg, Z, obj, stream=None):
+        self._check(self.lib.pf_admm_step(self.h, _ptr(V), _ld(V), _ptr(f), t, _ptr(adj),
+                                          _ld(adj), _ptr(deg), _ptr(Z), _ld(Z), _ptr(obj),
+                                          _stream(stream)), "pf_admm_step")
+
+    def perturb(self, A, E, stream=None):
+        self._check(self.lib.pf_perturb(self.h, _ptr(A), _ld(A), _ptr(E), _ld(E),
+                                        _stream(stream)), "pf_perturb")

@@ -1,0 +1,373 @@
+// pf_gemm.cu -- the Chebyshev-step filter GEMM (hot loop of eq:cheb / eqn:subspace-update,
+// P:185-227): out = s1 * (A B) + s2 * Ycur + s3 * Yprev, with A the n_rows x n_k row block of the
+// dense symmetric iterate and B = Y_j (n_k x p).  One launch per Chebyshev step; the same
+// kernel computes W = A Q for Rayleigh-Ritz (s1 = 1, s2 = s3 = 0).
+//
+// B200 design (DESIGN.md §4 K1):
+//  * fp64 tensor cores: mma.sync.m16n8k4.f64 (SASS DMMA.8x8x4) -- tcgen05 has no f64 kind.
+//  * A and B tiles staged by TMA (cp.async.bulk.tensor.2d) into a STAGES-deep smem ring guarded
+//    by mbarriers; A uses the 128-byte swizzle so the m16n8k4 fragment loads are conflict-free.
+//  * one producer warp (TMA) + 8 consumer warps; 1 CTA per SM.
+//  * stream-K: the (m-tile, k-block) iteration space is split evenly over `grid` = #SMs CTAs, so
+//    the 128-256 m-tiles of the filter shapes do not leave SMs idle.  Partial tiles are written
+//    to a workspace and the LAST contributor (atomic tile counter) sums all partials in fixed
+//    CTA order -> deterministic results, no co-residency assumption.
+//  * the Chebyshev recurrence's scale-shift-subtract is applied in the epilogue of the owner.
+#include <algorithm>
+
+#include "pf_kernels.cuh"
+
+namespace pf {
+
+template <int P>
+struct GemmCfg {
+  // 9 warps per CTA -> one SMSP hosts 3 warps -> <= 168 registers per thread (16K regs/SMSP),
+  // so every warp tile is kept at <= 32 x 32 doubles of accumulator: BM = 64 for P = 128.
+  static constexpr int BM = (P >= 128) ? 64 : 128, BK = 16;
+  static constexpr int NCW = 8;  // consumer warps
+  static constexpr int NCT = NCW * 32;
+  static constexpr int THREADS = NCT + 32;
+  static constexpr int WARPS_M = (P >= 128) ? 2 : ((P >= 64) ? 4 : 8);
+  static constexpr int WARPS_N = NCW / WARPS_M;
+  static constexpr int WM = BM / WARPS_M;
+  static constexpr int WN = P / WARPS_N;
+  static constexpr int MT = WM / 16;
+  static constexpr int NT = WN / 8;
+  static constexpr int NACC = MT * NT * 4;
+  static constexpr int A_BYTES = BM * BK * 8;
+  static constexpr int B_BYTES = BK * P * 8;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_RAW > 10 ? 10 : STAGES_RAW;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align slack*/ + 2 * STAGES * 8 + 64;
+  static_assert(WN % 8 == 0 && WM % 16 == 0, "warp tile");
+  static_assert(A_BYTES % 1024 == 0, "A tiles must stay 1024-byte aligned for SWIZZLE_128B");
+};
+
+struct ChebArgs {
+  const double* ycur;
+  const double* yprev;
+  double* out;
+  const double* coef;
+  double* ws;
+  int* counters;
+  int n_rows;
+  int kblocks;
+  long long total;
+};
+
+// owner of iteration i: largest q with floor(T q / G) <= i
+__device__ __forceinline__ int cta_of(long long i, long long T, int G) {
+  return (int)(((i + 1) * (long long)G + T - 1) / T) - 1;
+}
+
+template <int P>
+__global__ void __launch_bounds__(GemmCfg<P>::THREADS, 1)
+    cheb_gemm_kernel(const __grid_constant__ CUtensorMap mapA,
+                     const __grid_constant__ CUtensorMap mapB, ChebArgs args) {
+  using C = GemmCfg<P>;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  double* sA = reinterpret_cast<double*>(smem);
+  double* sB = reinterpret_cast<double*>(smem + C::STAGES * C::A_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  volatile int* sflag = reinterpret_cast<volatile int*>(empty + C::STAGES);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], C::NCW);
+    }
+    fence_mbar_init();
+  }
+  if (warp == C::NCW && lane == 0) {
+    tma_prefetch_desc(&mapA);
+    tma_prefetch_desc(&mapB);
+  }
+  __syncthreads();
+
+  const long long T = args.total;
+  const int G = gridDim.x, g = blockIdx.x;
+  const int KB = args.kblocks;
+  const long long it_begin = T * g / G, it_end = T * (g + 1) / G;
+
+  if (warp == C::NCW) {
+    // ------------------------------------------------------------ TMA producer (one lane)
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (long long it = it_begin; it < it_end; ++it) {
+        const int tile = (int)(it / KB), kb = (int)(it % KB);
+        mbar_wait(&empty[stage], phase ^ 1u);
+        mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+        tma_load_2d(sA + stage * (C::BM * C::BK), &mapA, &full[stage], kb * C::BK, tile * C::BM);
+        tma_load_2d(sB + stage * (C::BK * P), &mapB, &full[stage], 0, kb * C::BK);
+        if (++stage == C::STAGES) {
+          stage = 0;
+          phase ^= 1u;
+        }
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers (8 warps)
+  const int ctid = threadIdx.x;  // 0 .. NCT-1
+  const int wm = warp % C::WARPS_M, wn = warp / C::WARPS_M;
+  const int g8 = lane >> 2, t4 = lane & 3;
+  int stage = 0;
+  uint32_t phase = 0;
+
+  // per-thread constant parts of the swizzled A fragment address (in doubles)
+  // element (r, k) of a BM x 16 tile with SWIZZLE_128B: r*16 + (((k>>1) ^ (r&7)) << 1) + (k&1)
+  int a_off[C::MT][4];
+#pragma unroll
+  for (int mt = 0; mt < C::MT; ++mt) {
+    const int r = wm * C::WM + mt * 16 + g8;
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      const int k = ks * 4 + t4;
+      a_off[mt][ks] = r * 16 + ((((k >> 1) ^ (r & 7))) << 1) + (k & 1);
+    }
+  }
+  const int b_off = t4 * P + wn * C::WN + g8;
+
+  long long it = it_begin;
+  while (it < it_end) {
+    const int tile = (int)(it / KB);
+    const int kb0 = (int)(it % KB);
+    const long long seg_end = min(it_end, (long long)(tile + 1) * KB);
+    const int kb1 = kb0 + (int)(seg_end - it);
+
+    double acc[C::MT][C::NT][4];
+#pragma unroll
+    for (int mt = 0; mt < C::MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < C::NT; ++nt)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[mt][nt][i] = 0.0;
+
+    for (int kb = kb0; kb < kb1; ++kb) {
+      mbar_wait(&full[stage], phase);
+      const double* a = sA + stage * (C::BM * C::BK);
+      const double* b = sB + stage * (C::BK * P);
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        double af[C::MT][2], bf[C::NT];
+#pragma unroll
+        for (int mt = 0; mt < C::MT; ++mt) {
+          af[mt][0] = a[a_off[mt][ks]];
+          af[mt][1] = a[a_off[mt][ks] + 8 * 16];
+        }
+#pragma unroll
+        for (int nt = 0; nt < C::NT; ++nt) bf[nt] = b[ks * 4 * P + b_off + nt * 8];
+#pragma unroll
+        for (int mt = 0; mt < C::MT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < C::NT; ++nt) dmma16884(acc[mt][nt], af[mt][0], af[mt][1], bf[nt]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == C::STAGES) {
+        stage = 0;
+        phase ^= 1u;
+      }
+    }
+
+    bool do_epilogue = true;
+    if (!(kb0 == 0 && kb1 == KB)) {
+      // ---------------------------------------------------- stream-K partial tile
+      const int slot = (it == it_begin) ? 0 : 1;
+      double* mine = args.ws + (size_t)(g * 2 + slot) * (C::NCT * C::NACC);
+#pragma unroll
+      for (int mt = 0; mt < C::MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < C::NT; ++nt)
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            __stcg(mine + ((mt * C::NT + nt) * 4 + i) * C::NCT + ctid, acc[mt][nt][i]);
+      __threadfence();
+      named_bar_sync(1, C::NCT);
+      if (ctid == 0) {
+        const int add = kb1 - kb0;
+        const int prev = atomicAdd(&args.counters[tile], add);
+        *sflag = (prev + add == KB) ? 1 : 0;
+      }
+      named_bar_sync(1, C::NCT);
+      do_epilogue = (*sflag != 0);
+      named_bar_sync(1, C::NCT);  // sflag reused by the next segment
+      if (do_epilogue) {
+        __threadfence();
+        const long long t0 = (long long)tile * KB;
+        const int gf = cta_of(t0, T, G), gl = cta_of(t0 + KB - 1, T, G);
+#pragma unroll
+        for (int mt = 0; mt < C::MT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < C::NT; ++nt)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[mt][nt][i] = 0.0;
+        for (int q = gf; q <= gl; ++q) {
+          const long long qb = T * q / G;
+          const int qslot = (qb >= t0) ? 0 : 1;
+          const double* src = args.ws + (size_t)(q * 2 + qslot) * (C::NCT * C::NACC);
+#pragma unroll
+          for (int mt = 0; mt < C::MT; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < C::NT; ++nt)
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                acc[mt][nt][i] += __ldcg(src + ((mt * C::NT + nt) * 4 + i) * C::NCT + ctid);
+        }
+        if (ctid == 0) args.counters[tile] = 0;  // ready for the next launch
+      }
+    }
+
+    if (do_epilogue) {
+      // ------------------------------------------------------ fused Chebyshev epilogue
+      const double s1 = args.coef[0], s2 = args.coef[1], s3 = args.coef[2];
+#pragma unroll
+      for (int mt = 0; mt < C::MT; ++mt) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int row = tile * C::BM + wm * C::WM + mt * 16 + g8 + h * 8;
+          if (row >= args.n_rows) continue;
+#pragma unroll
+          for (int nt = 0; nt < C::NT; ++nt) {
+            const int col = wn * C::WN + nt * 8 + 2 * t4;
+            const size_t o = (size_t)row * P + col;
+            double2 v;
+            v.x = s1 * acc[mt][nt][2 * h];
+            v.y = s1 * acc[mt][nt][2 * h + 1];
+            if (s2 != 0.0) {
+              const double2 y = *reinterpret_cast<const double2*>(args.ycur + o);
+              v.x += s2 * y.x;
+              v.y += s2 * y.y;
+            }
+            if (s3 != 0.0) {
+              const double2 y = *reinterpret_cast<const double2*>(args.yprev + o);
+              v.x += s3 * y.x;
+              v.y += s3 * y.y;
+            }
+            *reinterpret_cast<double2*>(args.out + o) = v;
+          }
+        }
+      }
+    }
+    it = seg_end;
+  }
+}
+
+// ------------------------------------------------------------------------------ host side
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  }
+  return fn;
+}
+
+bool encode_map_A(CUtensorMap* map, const double* A, int64_t lda, int n_rows, int n_k, int p) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)n_k, (cuuint64_t)n_rows};
+  cuuint64_t strides[1] = {(cuuint64_t)lda * 8};
+  cuuint32_t box[2] = {16, (cuuint32_t)((p >= 128) ? 64 : 128)};
+  cuuint32_t es[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(A), dims, strides, box,
+             es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool encode_map_B(CUtensorMap* map, const double* B, int p, int n_k) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)p, (cuuint64_t)n_k};
+  cuuint64_t strides[1] = {(cuuint64_t)p * 8};
+  cuuint32_t box[2] = {(cuuint32_t)p, 16};
+  cuuint32_t es[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(B), dims, strides, box,
+             es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int P>
+static size_t ws_per_cta() {
+  return (size_t)2 * GemmCfg<P>::NCT * GemmCfg<P>::NACC;
+}
+
+ChebGemmPlan cheb_gemm_plan(int p, int n_rows, int n_k, int num_sms) {
+  ChebGemmPlan pl;
+  pl.p = p;
+  pl.n_rows = n_rows;
+  pl.n_k = n_k;
+  const int bm = (p >= 128) ? 64 : 128;
+  pl.mtiles = (n_rows + bm - 1) / bm;
+  pl.kblocks = (n_k + 15) / 16;
+  const long long T = (long long)pl.mtiles * pl.kblocks;
+  // at least 8 k-blocks per CTA so the fixup stays amortised
+  long long g = std::min<long long>(num_sms, std::max<long long>(1, T / 8));
+  pl.grid = (int)g;
+  size_t per = 0;
+  switch (p) {
+    case 16: per = ws_per_cta<16>(); break;
+    case 32: per = ws_per_cta<32>(); break;
+    case 64: per = ws_per_cta<64>(); break;
+    case 128: per = ws_per_cta<128>(); break;
+    default: per = ws_per_cta<128>(); break;
+  }
+  pl.ws_doubles = per * (size_t)num_sms;
+  return pl;
+}
+
+template <int P>
+static cudaError_t launch_p(const ChebGemmPlan& pl, const CUtensorMap& mapA,
+                            const CUtensorMap& mapB, const ChebArgs& a, cudaStream_t st) {
+  using C = GemmCfg<P>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(cheb_gemm_kernel<P>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  cheb_gemm_kernel<P><<<pl.grid, C::THREADS, C::SMEM, st>>>(mapA, mapB, a);
+  return cudaGetLastError();
+}
+
+cudaError_t cheb_gemm_launch(const ChebGemmPlan& pl, const CUtensorMap& mapA,
+                             const CUtensorMap& mapB, const double* ycur, const double* yprev,
+                             double* out, const double* coef, double* ws, int* counters,
+                             cudaStream_t st) {
+  ChebArgs a;
+  a.ycur = ycur;
+  a.yprev = yprev;
+  a.out = out;
+  a.coef = coef;
+  a.ws = ws;
+  a.counters = counters;
+  a.n_rows = pl.n_rows;
+  a.kblocks = pl.kblocks;
+  a.total = (long long)pl.mtiles * pl.kblocks;
+  switch (pl.p) {
+    case 16: return launch_p<16>(pl, mapA, mapB, a, st);
+    case 32: return launch_p<32>(pl, mapA, mapB, a, st);
+    case 64: return launch_p<64>(pl, mapA, mapB, a, st);
+    case 128: return launch_p<128>(pl, mapA, mapB, a, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace pf

@@ -1,0 +1,79 @@
+// pf_kernels.cuh -- host-side launchers of the PF kernels (internal to libpf.so).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "pf_common.cuh"
+
+namespace pf {
+
+// ---- Chebyshev-step GEMM (pf_gemm.cu): out = s1*(A B) + s2*Ycur + s3*Yprev (rows of A local)
+struct ChebGemmPlan {
+  int p;
+  int n_rows;         // rows of A (local block)
+  int n_k;            // columns of A == rows of B
+  int grid;           // stream-K CTAs
+  int mtiles, kblocks;
+  size_t ws_doubles;  // partial workspace size needed
+};
+ChebGemmPlan cheb_gemm_plan(int p, int n_rows, int n_k, int num_sms);
+// Encode the TMA descriptors (host only, no device work).
+bool encode_map_A(CUtensorMap* map, const double* A, int64_t lda, int n_rows, int n_k, int p);
+bool encode_map_B(CUtensorMap* map, const double* B, int p, int n_k);
+cudaError_t cheb_gemm_launch(const ChebGemmPlan& pl, const CUtensorMap& mapA,
+                             const CUtensorMap& mapB, const double* ycur, const double* yprev,
+                             double* out, const double* coef, double* ws, int* counters,
+                             cudaStream_t st);
+
+// ---- small dense kernels (pf_small.cu); all p x p objects are row-major, ld = p
+// G = X^T Y over rows [0, n_rows) (X, Y: n_rows x p, ld p).  Deterministic two-level sum:
+// per-CTA partials then the last CTA reduces in CTA order.  If `cond` != NULL the kernel is a
+// no-op unless *cond != 0.  Returns the grid used (<= max_blocks).
+int gram_blocks(int n_rows, int p);
+cudaError_t gram_launch(const double* X, const double* Y, int n_rows, int p, double* G,
+                        double* partials, int* counter, const int* cond, cudaStream_t st);
+// Cholesky G = L L^T (shifted on breakdown) and Rinv = L^{-T}; n_global for the shift.
+cudaError_t chol_inv_launch(const double* G, int p, int64_t n_global, double* Rinv,
+                            DevState* state, int* shift_flag_out, const int* cond,
+                            cudaStream_t st);
+// out(n_rows x p, ldo) = in(n_rows x p, ldi) * R (p x p); in place allowed (in == out, ldi == ldo)
+cudaError_t rmul_launch(const double* in, int64_t ldi, const double* R, double* out, int64_t ldo,
+                        int n_rows, int p, const int* cond, cudaStream_t st);
+// two-sided parallel cyclic Jacobi: H (p x p symmetric, only read) -> theta desc, Y (p x p)
+cudaError_t jacobi_launch(const double* H, int p, const int* p_dev, double* theta, double* Y,
+                          DevState* state, double tol, int max_sweeps, cudaStream_t st);
+cudaError_t spectral_launch(int op, double thr, const double* theta, int p, double* f,
+                            int* rank, DevState* state, cudaStream_t st);
+// plan kernel: interval -> per-step coefficients + re-base flags
+cudaError_t plan_launch(const double* interval, int d, double rho_max, int p, DevState* state,
+                        cudaStream_t st);
+cudaError_t interval_psd_launch(const double* lo_hi, double eta, double* interval,
+                                DevState* state, cudaStream_t st);
+cudaError_t interval_soft_launch(double thr, double eta, double* interval, DevState* state,
+                                 cudaStream_t st);
+cudaError_t copy_theta_launch(const double* theta, int p, DevState* state, cudaStream_t st);
+// Lanczos
+int lanczos_blocks(int n_rows);
+cudaError_t lanczos_init_launch(const double* v0, int n, double* Qcols, double* partials,
+                                int* counter, DevState* state, cudaStream_t st);
+cudaError_t lanczos_step_launch(const double* A, int64_t lda, int n, int64_t ldq, int j,
+                                double* Qcols, double* w, double* h, double* partials,
+                                int* counter, DevState* state, cudaStream_t st);
+cudaError_t lanczos_finish_launch(int m, double* T, double* theta, double* S, double* lo_hi,
+                                  DevState* state, cudaStream_t st);
+cudaError_t perturb_launch(double* A, int64_t lda, const double* E, int64_t lde, int rows,
+                           int cols, cudaStream_t st);
+
+// ---- rebuild + update (pf_rebuild.cu)
+int rebuild_blocks(int n_rows, int n);
+cudaError_t prox_launch(const double* V, int64_t ldv, const double* f, double tau,
+                        const uint32_t* omega, int64_t ldo, const double* W, int64_t ldw, int r,
+                        double* Aout, int64_t lda, int n_rows, int n, int row0, int p,
+                        double* obj, double* partials, int* counter, cudaStream_t st);
+cudaError_t admm_launch(const double* V, int64_t ldv, const double* f, double t,
+                        const uint32_t* adj, int64_t ldadj, const double* deg, double* Z,
+                        int64_t ldz, int n_rows, int n, int row0, int p, double* obj,
+                        double* partials, int* counter, cudaStream_t st);
+
+}  // namespace pf

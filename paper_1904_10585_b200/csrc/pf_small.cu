@@ -1,0 +1,879 @@
+// pf_small.cu -- the p x p side of the hot path and the tall-skinny n x p kernels:
+//   Gram / cross-Gram (fp64 DMMA) for CholeskyQR2 and H = Q^T (A Q)
+//   Cholesky + triangular inverse, shifted on breakdown                       (reading R10)
+//   right multiplication Y <- Y R (fp64 DMMA): Q = Y R^-1, V = Q Y_eig, re-basing
+//   two-sided parallel cyclic Jacobi eigensolver (single CTA)                  (eqn:RR)
+//   spectral operator, interval / re-base plan, Lanczos, perturbation helper.
+#include <algorithm>
+
+#include "pf_kernels.cuh"
+#include "../../include/pf.h"
+
+namespace pf {
+
+// =============================================================================== Gram
+// partials[blk] = X[rows of blk]^T Y[rows of blk]; then gram_reduce sums blocks in order.
+constexpr int kGramRows = 32;       // rows per block are a multiple of this
+constexpr int kGramMaxBlocks = 148;
+
+template <int P>
+struct GramCfg {
+  static constexpr int WTN = P < 32 ? P : 32;        // warp tile 16 x WTN
+  static constexpr int NT = WTN / 8;
+  static constexpr int NWT = (P / 16) * (P / WTN);   // warp tiles
+  static constexpr int PER_WARP = (NWT + 7) / 8;
+  static constexpr int LD = P + 4;                   // padded smem row (conflict-free frags)
+  static constexpr int R = P >= 128 ? 16 : 32;       // rows per smem sub-chunk (static smem)
+};
+
+template <int P>
+__global__ void __launch_bounds__(256) gram_partial_kernel(const double* __restrict__ X,
+                                                          const double* __restrict__ Y,
+                                                          int n_rows, int rows_per_block,
+                                                          double* __restrict__ partials,
+                                                          const int* cond) {
+  using C = GramCfg<P>;
+  if (cond && *cond == 0) return;
+  __shared__ __align__(16) double Xs[C::R * C::LD];
+  __shared__ __align__(16) double Ys[C::R * C::LD];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g8 = lane >> 2, t4 = lane & 3;
+  const int r0 = blockIdx.x * rows_per_block;
+  const int r1 = min(n_rows, r0 + rows_per_block);
+  double acc[C::PER_WARP][C::NT][4];
+#pragma unroll
+  for (int w = 0; w < C::PER_WARP; ++w)
+#pragma unroll
+    for (int nt = 0; nt < C::NT; ++nt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[w][nt][i] = 0.0;
+
+  for (int rb = r0; rb < r1; rb += C::R) {
+    for (int e = threadIdx.x; e < C::R * P / 2; e += 256) {
+      const int rr = e / (P / 2), cc = (e % (P / 2)) * 2;
+      const int row = rb + rr;
+      double2 x = make_double2(0.0, 0.0), y = make_double2(0.0, 0.0);
+      if (row < r1) {
+        x = *reinterpret_cast<const double2*>(X + (size_t)row * P + cc);
+        y = *reinterpret_cast<const double2*>(Y + (size_t)row * P + cc);
+      }
+      *reinterpret_cast<double2*>(Xs + rr * C::LD + cc) = x;
+      *reinterpret_cast<double2*>(Ys + rr * C::LD + cc) = y;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < C::PER_WARP; ++w) {
+      const int wt = warp + 8 * w;
+      if (wt < C::NWT) {
+        const int m0 = (wt % (P / 16)) * 16, n0 = (wt / (P / 16)) * C::WTN;
+#pragma unroll
+        for (int ks = 0; ks < C::R / 4; ++ks) {
+          const int k = ks * 4 + t4;
+          const double a0 = Xs[k * C::LD + m0 + g8];
+          const double a1 = Xs[k * C::LD + m0 + g8 + 8];
+#pragma unroll
+          for (int nt = 0; nt < C::NT; ++nt)
+            dmma16884(acc[w][nt], a0, a1, Ys[k * C::LD + n0 + nt * 8 + g8]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  double* out = partials + (size_t)blockIdx.x * P * P;
+#pragma unroll
+  for (int w = 0; w < C::PER_WARP; ++w) {
+    const int wt = warp + 8 * w;
+    if (wt < C::NWT) {
+      const int m0 = (wt % (P / 16)) * 16, n0 = (wt / (P / 16)) * C::WTN;
+#pragma unroll
+      for (int nt = 0; nt < C::NT; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int m = m0 + g8 + 8 * h, n = n0 + nt * 8 + 2 * t4;
+          *reinterpret_cast<double2*>(out + m * P + n) =
+              make_double2(acc[w][nt][2 * h], acc[w][nt][2 * h + 1]);
+        }
+    }
+  }
+}
+
+__global__ void gram_reduce_kernel(const double* __restrict__ partials, int nblk, int pp,
+                                   double* __restrict__ G, const int* cond) {
+  if (cond && *cond == 0) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= pp) return;
+  double s = 0.0;
+  for (int b = 0; b < nblk; ++b) s += partials[(size_t)b * pp + i];
+  G[i] = s;
+}
+
+static int gram_rows_per_block(int n_rows) {
+  int nb = std::min(kGramMaxBlocks, std::max(1, (n_rows + 63) / 64));
+  int rpb = (n_rows + nb - 1) / nb;
+  rpb = ((rpb + kGramRows - 1) / kGramRows) * kGramRows;
+  return std::max(rpb, kGramRows);
+}
+
+int gram_blocks(int n_rows, int p) {
+  (void)p;
+  const int rpb = gram_rows_per_block(n_rows);
+  return std::max(1, (n_rows + rpb - 1) / rpb);
+}
+
+cudaError_t gram_launch(const double* X, const double* Y, int n_rows, int p, double* G,
+                        double* partials, int* counter, const int* cond, cudaStream_t st) {
+  (void)counter;
+  const int rpb = gram_rows_per_block(n_rows);
+  const int nb = std::max(1, (n_rows + rpb - 1) / rpb);
+  switch (p) {
+    case 16: gram_partial_kernel<16><<<nb, 256, 0, st>>>(X, Y, n_rows, rpb, partials, cond); break;
+    case 32: gram_partial_kernel<32><<<nb, 256, 0, st>>>(X, Y, n_rows, rpb, partials, cond); break;
+    case 64: gram_partial_kernel<64><<<nb, 256, 0, st>>>(X, Y, n_rows, rpb, partials, cond); break;
+    case 128: gram_partial_kernel<128><<<nb, 256, 0, st>>>(X, Y, n_rows, rpb, partials, cond); break;
+    default: return cudaErrorInvalidValue;
+  }
+  const int pp = p * p;
+  gram_reduce_kernel<<<(pp + 255) / 256, 256, 0, st>>>(partials, nb, pp, G, cond);
+  return cudaGetLastError();
+}
+
+// =============================================================================== Cholesky
+// One CTA.  M (p x (p+1), smem): lower triangle incl. diagonal = L, X = L^{-1} stored
+// transposed in the strict upper part: X[i][c] (i >= c) at M[c][i+1].  Output Rinv = L^{-T}.
+__global__ void __launch_bounds__(512) chol_inv_kernel(const double* __restrict__ G, int p,
+                                                     double shift_scale, double* __restrict__ Rinv,
+                                                     DevState* state, int* shift_flag_out,
+                                                     const int* cond) {
+  if (cond && *cond == 0) return;
+  extern __shared__ double M[];
+  __shared__ double sdiag;
+  __shared__ int sfail;
+  __shared__ double red[32];
+  const int P1 = p + 1;
+  const int tid = threadIdx.x, nt = blockDim.x;
+
+  // finiteness + trace
+  double tr = 0.0;
+  int bad = 0;
+  for (int e = tid; e < p * p; e += nt) {
+    const double v = G[e];
+    if (!isfinite(v)) bad = 1;
+    if (e / p == e % p) tr += v;
+  }
+  bad = __syncthreads_or(bad);
+  tr = block_sum(tr, red);
+  if (bad && tid == 0) atomicOr(&state->flags, PF_FLAG_NONFINITE);
+
+  double shift = 0.0;
+  int attempt = 0;
+  for (;;) {
+    for (int e = tid; e < p * p; e += nt) {
+      const int i = e / p, j = e % p;
+      if (j <= i) M[i * P1 + j] = G[e] + ((i == j) ? shift : 0.0);
+    }
+    if (tid == 0) sfail = 0;
+    __syncthreads();
+    for (int j = 0; j < p; ++j) {
+      if (tid == 0) {
+        const double d = M[j * P1 + j];
+        const double g = G[j * p + j];
+        if (!(d > 1e-12 * g) || !(d > 0.0)) {
+          sfail = 1;
+          sdiag = 1.0;
+        } else {
+          sdiag = sqrt(d);
+        }
+        M[j * P1 + j] = sdiag;
+      }
+      __syncthreads();
+      if (sfail) break;
+      const double dj = sdiag;
+      for (int i = j + 1 + tid; i < p; i += nt) M[i * P1 + j] /= dj;
+      __syncthreads();
+      // trailing update of the lower triangle: rows i > j, cols k in (j, i]
+      const int m = p - j - 1;
+      for (int e = tid; e < m * m; e += nt) {
+        const int ii = e / m, kk = e % m;
+        if (kk <= ii) {
+          const int i = j + 1 + ii, k = j + 1 + kk;
+          M[i * P1 + k] -= M[i * P1 + j] * M[k * P1 + j];
+        }
+      }
+      __syncthreads();
+    }
+    if (!sfail) break;
+    if (attempt == 1) {
+      if (tid == 0) atomicOr(&state->flags, PF_FLAG_NONFINITE);
+      break;
+    }
+    attempt = 1;
+    shift = shift_scale * (tr > 0.0 ? tr : 1.0);
+    __syncthreads();
+  }
+  if (tid == 0) {
+    if (attempt) atomicOr(&state->flags, PF_FLAG_CHOL_SHIFT);
+    if (shift_flag_out && attempt) *shift_flag_out = 1;
+  }
+  // X = L^{-1}, right-looking: X = I; for j: X[j][:] /= L[j][j]; X[i][:] -= L[i][j] X[j][:]
+  for (int e = tid; e < p * p; e += nt) {
+    const int i = e / p, c = e % p;
+    if (i >= c) M[c * P1 + i + 1] = (i == c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int j = 0; j < p; ++j) {
+    const double ljj = M[j * P1 + j];
+    for (int c = tid; c <= j; c += nt) M[c * P1 + j + 1] /= ljj;
+    __syncthreads();
+    const int m = p - j - 1;
+    for (int e = tid; e < m * (j + 1); e += nt) {
+      const int i = j + 1 + e / (j + 1), c = e % (j + 1);
+      M[c * P1 + i + 1] -= M[i * P1 + j] * M[c * P1 + j + 1];
+    }
+    __syncthreads();
+  }
+  // Rinv = L^{-T}: Rinv[c][i] = X[i][c] (upper triangular)
+  for (int e = tid; e < p * p; e += nt) {
+    const int c = e / p, i = e % p;
+    Rinv[e] = (i >= c) ? M[c * P1 + i + 1] : 0.0;
+  }
+}
+
+cudaError_t chol_inv_launch(const double* G, int p, int64_t n_global, double* Rinv,
+                            DevState* state, int* shift_flag_out, const int* cond,
+                            cudaStream_t st) {
+  const double u = 1.1102230246251565e-16;
+  const double scale = 11.0 * ((double)n_global * p + (double)p * (p + 1)) * u;
+  const size_t smem = (size_t)p * (p + 1) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(128 * 129 * sizeof(double)));
+    attr = true;
+  }
+  chol_inv_kernel<<<1, 512, smem, st>>>(G, p, scale, Rinv, state, shift_flag_out, cond);
+  return cudaGetLastError();
+}
+
+// =============================================================================== Y R
+template <int P>
+struct RmulCfg {
+  static constexpr int BM = 64;
+  static constexpr int LD = P + 4;
+  static constexpr int WN = P / 2;                  // warps 4 (M) x 2 (N), warp tile 16 x WN
+  static constexpr int NT = WN / 8;
+  static constexpr int SMEM = (P * LD + BM * LD) * 8;
+};
+
+template <int P>
+__global__ void __launch_bounds__(256) rmul_kernel(const double* in, int64_t ldi,
+                                                  const double* __restrict__ R, double* out,
+                                                  int64_t ldo, int n_rows, const int* cond) {
+  using C = RmulCfg<P>;
+  if (cond && *cond == 0) return;
+  extern __shared__ __align__(16) double sm[];
+  double* Rs = sm;
+  double* Ys = sm + P * C::LD;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g8 = lane >> 2, t4 = lane & 3;
+  const int row0 = blockIdx.x * C::BM;
+  for (int e = threadIdx.x; e < P * P / 2; e += 256) {
+    const int r = e / (P / 2), c = (e % (P / 2)) * 2;
+    *reinterpret_cast<double2*>(Rs + r * C::LD + c) =
+        *reinterpret_cast<const double2*>(R + r * P + c);
+  }
+  for (int e = threadIdx.x; e < C::BM * P / 2; e += 256) {
+    const int r = e / (P / 2), c = (e % (P / 2)) * 2;
+    double2 v = make_double2(0.0, 0.0);
+    if (row0 + r < n_rows) v = *reinterpret_cast<const double2*>(in + (size_t)(row0 + r) * ldi + c);
+    *reinterpret_cast<double2*>(Ys + r * C::LD + c) = v;
+  }
+  __syncthreads();
+  const int wm = warp & 3, wn = warp >> 2;
+  double acc[C::NT][4];
+#pragma unroll
+  for (int nt = 0; nt < C::NT; ++nt)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[nt][i] = 0.0;
+#pragma unroll 4
+  for (int ks = 0; ks < P / 4; ++ks) {
+    const int k = ks * 4 + t4;
+    const double a0 = Ys[(wm * 16 + g8) * C::LD + k];
+    const double a1 = Ys[(wm * 16 + g8 + 8) * C::LD + k];
+#pragma unroll
+    for (int nt = 0; nt < C::NT; ++nt)
+      dmma16884(acc[nt], a0, a1, Rs[k * C::LD + wn * C::WN + nt * 8 + g8]);
+  }
+#pragma unroll
+  for (int nt = 0; nt < C::NT; ++nt)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int row = row0 + wm * 16 + g8 + 8 * h;
+      if (row < n_rows) {
+        const int col = wn * C::WN + nt * 8 + 2 * t4;
+        *reinterpret_cast<double2*>(out + (size_t)row * ldo + col) =
+            make_double2(acc[nt][2 * h], acc[nt][2 * h + 1]);
+      }
+    }
+}
+
+template <int P>
+static cudaError_t rmul_p(const double* in, int64_t ldi, const double* R, double* out,
+                          int64_t ldo, int n_rows, const int* cond, cudaStream_t st) {
+  using C = RmulCfg<P>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(rmul_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    attr = true;
+  }
+  const int grid = std::max(1, (n_rows + C::BM - 1) / C::BM);
+  rmul_kernel<P><<<grid, 256, C::SMEM, st>>>(in, ldi, R, out, ldo, n_rows, cond);
+  return cudaGetLastError();
+}
+
+cudaError_t rmul_launch(const double* in, int64_t ldi, const double* R, double* out, int64_t ldo,
+                        int n_rows, int p, const int* cond, cudaStream_t st) {
+  switch (p) {
+    case 16: return rmul_p<16>(in, ldi, R, out, ldo, n_rows, cond, st);
+    case 32: return rmul_p<32>(in, ldi, R, out, ldo, n_rows, cond, st);
+    case 64: return rmul_p<64>(in, ldi, R, out, ldo, n_rows, cond, st);
+    case 128: return rmul_p<128>(in, ldi, R, out, ldo, n_rows, cond, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// =============================================================================== Jacobi
+// Two-sided cyclic Jacobi with the round-robin (tournament) parallel ordering: in each round the
+// Pe/2 disjoint pairs are rotated simultaneously; every 2x2 block (pair a, pair b) of H is
+// updated by exactly one thread as B' = J_a^T B J_b (J = [[c, s], [-s, c]], Golub & Van Loan
+// sym.schur2), so no row/column phasing is needed.  H is kept as a packed upper triangle
+// (Pe(Pe+1)/2 doubles) and V = prod J as a dense Pe x Pe matrix, both in shared memory.
+__device__ __forceinline__ int pk(int i, int j, int Pe) {
+  if (i > j) {
+    const int t = i;
+    i = j;
+    j = t;
+  }
+  return i * Pe - (i * (i - 1)) / 2 + (j - i);
+}
+
+__global__ void __launch_bounds__(1024) jacobi_kernel(const double* __restrict__ H, int p_static,
+                                                    const int* p_dev, double* __restrict__ theta,
+                                                    double* __restrict__ Yout, DevState* state,
+                                                    double tol, int max_sweeps) {
+  extern __shared__ double js[];
+  __shared__ double red[32];
+  __shared__ int s_cnt;
+  const int p = p_dev ? *p_dev : p_static;
+  if (p <= 0) return;
+  const int Pe = p + (p & 1);
+  const int half = Pe / 2;
+  double* Hp = js;                                  // Pe(Pe+1)/2
+  double* V = Hp + (Pe * (Pe + 1)) / 2;             // Pe x Pe
+  double* cs = V + Pe * Pe;                         // [half][3] = c, s, t
+  int* pi = reinterpret_cast<int*>(cs + 3 * half);  // [half]
+  int* pj = pi + half;
+  const int tid = threadIdx.x, nt = blockDim.x;
+
+  for (int i = tid; i < Pe; i += nt)
+    for (int j = i; j < Pe; ++j) {
+      double v = 0.0;
+      if (i < p && j < p) v = 0.5 * (H[i * p + j] + H[j * p + i]);
+      Hp[pk(i, j, Pe)] = v;
+    }
+  for (int e = tid; e < Pe * Pe; e += nt) V[e] = (e / Pe == e % Pe) ? 1.0 : 0.0;
+  __syncthreads();
+
+  int sweep = 0;
+  bool converged = false;
+  for (; sweep < max_sweeps; ++sweep) {
+    double off = 0.0, tot = 0.0;
+    for (int e = tid; e < Pe * Pe; e += nt) {
+      const int i = e / Pe, j = e % Pe;
+      const double v = Hp[pk(i, j, Pe)];
+      tot += v * v;
+      if (i != j) off += v * v;
+    }
+    off = block_sum(off, red);
+    tot = block_sum(tot, red);
+    if (off <= tol * tol * tot || off == 0.0) {
+      converged = true;
+      break;
+    }
+    if (tid == 0) s_cnt = 0;
+    __syncthreads();
+    for (int r = 0; r < Pe - 1; ++r) {
+      // pairs of this round and their rotations
+      for (int m = tid; m < half; m += nt) {
+        int a, b;
+        if (m == 0) {
+          a = Pe - 1;
+          b = r;
+        } else {
+          a = (r + m) % (Pe - 1);
+          b = (r - m + (Pe - 1)) % (Pe - 1);
+        }
+        const int i = a < b ? a : b, j = a < b ? b : a;
+        pi[m] = i;
+        pj[m] = j;
+        double c = 1.0, s = 0.0, t = 0.0;
+        if (j < p) {
+          const double hij = Hp[pk(i, j, Pe)];
+          const double hii = Hp[pk(i, i, Pe)], hjj = Hp[pk(j, j, Pe)];
+          if (fabs(hij) > 1e-300 && fabs(hij) > 1e-17 * sqrt(fabs(hii * hjj))) {
+            const double tau = (hjj - hii) / (2.0 * hij);
+            t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+            c = 1.0 / sqrt(1.0 + t * t);
+            s = t * c;
+            atomicAdd(&s_cnt, 1);
+          }
+        }
+        cs[3 * m] = c;
+        cs[3 * m + 1] = s;
+        cs[3 * m + 2] = t;
+      }
+      __syncthreads();
+      // 2x2 block updates: blocks (a, b), a <= b, enumerated linearly
+      const int nblk = half * (half + 1) / 2;
+      for (int e = tid; e < nblk; e += nt) {
+        // invert e -> (a, b) with a <= b: row a has (half - a) blocks
+        int a = 0, rem = e;
+        while (rem >= half - a) {
+          rem -= half - a;
+          ++a;
+        }
+        const int b = a + rem;
+        const int ia = pi[a], ja = pj[a];
+        const double ca = cs[3 * a], sa = cs[3 * a + 1];
+        if (a == b) {
+          const double ta = cs[3 * a + 2];
+          if (sa != 0.0) {
+            const double hij = Hp[pk(ia, ja, Pe)];
+            Hp[pk(ia, ia, Pe)] -= ta * hij;
+            Hp[pk(ja, ja, Pe)] += ta * hij;
+            Hp[pk(ia, ja, Pe)] = 0.0;
+          }
+        } else {
+          const int ib = pi[b], jb = pj[b];
+          const double cb = cs[3 * b], sb = cs[3 * b + 1];
+          if (sa != 0.0 || sb != 0.0) {
+            const int k11 = pk(ia, ib, Pe), k12 = pk(ia, jb, Pe), k21 = pk(ja, ib, Pe),
+                      k22 = pk(ja, jb, Pe);
+            const double b11 = Hp[k11], b12 = Hp[k12], b21 = Hp[k21], b22 = Hp[k22];
+            const double t11 = ca * b11 - sa * b21, t12 = ca * b12 - sa * b22;
+            const double t21 = sa * b11 + ca * b21, t22 = sa * b12 + ca * b22;
+            Hp[k11] = t11 * cb - t12 * sb;
+            Hp[k12] = t11 * sb + t12 * cb;
+            Hp[k21] = t21 * cb - t22 * sb;
+            Hp[k22] = t21 * sb + t22 * cb;
+          }
+        }
+      }
+      // V <- V J (columns i, j of every row)
+      for (int e = tid; e < Pe * half; e += nt) {
+        const int row = e / half, m = e % half;
+        const double c = cs[3 * m], s = cs[3 * m + 1];
+        if (s != 0.0) {
+          const int i = pi[m], j = pj[m];
+          const double vi = V[row * Pe + i], vj = V[row * Pe + j];
+          V[row * Pe + i] = c * vi - s * vj;
+          V[row * Pe + j] = s * vi + c * vj;
+        }
+      }
+      __syncthreads();
+    }
+    if (s_cnt == 0) {
+      converged = true;
+      ++sweep;
+      break;
+    }
+  }
+  if (!converged && tid == 0) atomicOr(&state->flags, PF_FLAG_JACOBI_MAXSWEEP);
+  // sort descending (stable by index) and emit
+  for (int i = tid; i < p; i += nt) {
+    const double li = Hp[pk(i, i, Pe)];
+    int rank = 0;
+    for (int k = 0; k < p; ++k) {
+      const double lk = Hp[pk(k, k, Pe)];
+      if (lk > li || (lk == li && k < i)) ++rank;
+    }
+    theta[rank] = li;
+    for (int row = 0; row < p; ++row) Yout[row * p + rank] = V[row * Pe + i];
+  }
+}
+
+cudaError_t jacobi_launch(const double* H, int p, const int* p_dev, double* theta, double* Y,
+                          DevState* state, double tol, int max_sweeps, cudaStream_t st) {
+  const int Pe = p + (p & 1), half = Pe / 2;
+  const size_t smem = ((size_t)Pe * (Pe + 1) / 2 + (size_t)Pe * Pe + 3 * half) * 8 + 2 * half * 4;
+  static bool attr = false;
+  if (!attr) {
+    const size_t mx = ((size_t)128 * 129 / 2 + 128 * 128 + 3 * 64) * 8 + 2 * 64 * 4;
+    cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+    attr = true;
+  }
+  jacobi_kernel<<<1, 1024, smem, st>>>(H, p, p_dev, theta, Y, state, tol, max_sweeps);
+  return cudaGetLastError();
+}
+
+// =============================================================================== spectral op
+__global__ void spectral_kernel(int op, double thr, const double* __restrict__ theta, int p,
+                                double* __restrict__ f, int* rank, DevState* state) {
+  const int i = threadIdx.x;
+  int nz = 0;
+  if (i < p) {
+    const double t = theta[i];
+    double v;
+    if (op == PF_OP_PSD)
+      v = t > 0.0 ? t : 0.0;  // P_+ 
+    else
+      v = (t > thr) ? (t - thr) : ((t < -thr) ? (t + thr) : 0.0);  // shrink
+    f[i] = v;
+    nz = (v != 0.0);
+  }
+  const int cnt = __syncthreads_count(nz);
+  if (i == 0) {
+    *rank = cnt;
+    if (cnt == p) atomicOr(&state->flags, PF_FLAG_SATURATED);
+  }
+}
+
+cudaError_t spectral_launch(int op, double thr, const double* theta, int p, double* f, int* rank,
+                            DevState* state, cudaStream_t st) {
+  spectral_kernel<<<1, 128, 0, st>>>(op, thr, theta, p, f, rank, state);
+  return cudaGetLastError();
+}
+
+// =============================================================================== plan
+// Per pf_filter call: coefficients of the recurrence and the re-base schedule (reading R7).
+__global__ void plan_kernel(const double* __restrict__ interval, int d, double rho_max, int p,
+                            DevState* state) {
+  if (threadIdx.x != 0) return;
+  double a = interval[0], b = interval[1];
+  if (!(b > a)) {
+    atomicOr(&state->flags, PF_FLAG_DEGENERATE_INT);
+    b = a + 1.0;
+  }
+  const double c = 0.5 * (b + a), e = 0.5 * (b - a);
+  state->interval[0] = a;
+  state->interval[1] = b;
+  double spread;
+  if (state->have_theta) {
+    spread = 0.0;
+    for (int i = 0; i < p; ++i) spread = fmax(spread, fabs(state->theta[i]));
+  } else if (state->have_lanczos) {
+    spread = fmax(fabs(state->lanczos[0]), fabs(state->lanczos[1]));
+  } else {
+    spread = fmax(fabs(a), fabs(b));
+  }
+  const double that = fmax(1.0, fmax(fabs((1.1 * spread - c) / e), fabs((-1.1 * spread - c) / e)));
+  for (int j = 0; j < d; ++j) {
+    if (j == 0) {
+      state->coef[0][0] = 1.0 / e;
+      state->coef[0][1] = -c / e;
+      state->coef[0][2] = 0.0;
+    } else {
+      state->coef[j][0] = 2.0 / e;
+      state->coef[j][1] = -2.0 * c / e;
+      state->coef[j][2] = -1.0;
+    }
+  }
+  int base = 0;
+  for (int j = 1; j <= d; ++j) {
+    int rb = 0;
+    if (j < d && cheb_T(j, that) / cheb_T(base, that) > rho_max) {
+      rb = 1;
+      base = j;
+    }
+    state->rebase[j - 1] = rb;
+    state->rebases += rb;
+  }
+}
+
+cudaError_t plan_launch(const double* interval, int d, double rho_max, int p, DevState* state,
+                        cudaStream_t st) {
+  plan_kernel<<<1, 32, 0, st>>>(interval, d, rho_max, p, state);
+  return cudaGetLastError();
+}
+
+__global__ void interval_psd_kernel(const double* lo_hi, double eta, double* interval,
+                                    DevState* state) {
+  double a = lo_hi[0];
+  if (!(a < 0.0)) {
+    atomicOr(&state->flags, PF_FLAG_DEGENERATE_INT);
+    a = -(fabs(a) + 1.0);
+  }
+  interval[0] = a;
+  interval[1] = eta * a;  // b = eta a
+}
+
+cudaError_t interval_psd_launch(const double* lo_hi, double eta, double* interval,
+                                DevState* state, cudaStream_t st) {
+  interval_psd_kernel<<<1, 1, 0, st>>>(lo_hi, eta, interval, state);
+  return cudaGetLastError();
+}
+
+__global__ void interval_soft_kernel(double thr, double eta, double* interval) {
+  const double beta = (1.0 - eta) * thr;
+  interval[0] = -beta;
+  interval[1] = beta;
+}
+
+cudaError_t interval_soft_launch(double thr, double eta, double* interval, DevState* state,
+                                 cudaStream_t st) {
+  (void)state;
+  interval_soft_kernel<<<1, 1, 0, st>>>(thr, eta, interval);
+  return cudaGetLastError();
+}
+
+__global__ void copy_theta_kernel(const double* theta, int p, DevState* state) {
+  const int i = threadIdx.x;
+  if (i < p) state->theta[i] = theta[i];
+  if (i == 0) state->have_theta = 1;
+}
+
+cudaError_t copy_theta_launch(const double* theta, int p, DevState* state, cudaStream_t st) {
+  copy_theta_kernel<<<1, 128, 0, st>>>(theta, p, state);
+  return cudaGetLastError();
+}
+
+// =============================================================================== Lanczos
+// Q: (m+1) Lanczos vectors stored column by column (vector j at Q + j*n).
+constexpr int kLzThreads = 256;
+
+int lanczos_blocks(int n_rows) { return std::max(1, std::min(296, (n_rows + 7) / 8)); }
+
+// last-block reduction helper: partials[blk * stride + i], i < cnt -> out[i] (block order)
+__device__ bool last_block_done(int* counter, int* s_last) {
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int prev = atomicAdd(counter, 1);
+    *s_last = (prev == (int)gridDim.x - 1);
+  }
+  __syncthreads();
+  return *s_last != 0;
+}
+
+__global__ void lanczos_init_kernel(const double* __restrict__ v0, int n, double* Q,
+                                    DevState* state) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += v0[i] * v0[i];
+  s = block_sum(s, red);
+  const double inv = 1.0 / sqrt(s);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) Q[i] = v0[i] * inv;
+  if (threadIdx.x == 0) {
+    state->lanczos_steps = -1;  // running
+  }
+}
+
+cudaError_t lanczos_init_launch(const double* v0, int n, double* Qcols, double* partials,
+                                int* counter, DevState* state, cudaStream_t st) {
+  (void)partials;
+  (void)counter;
+  lanczos_init_kernel<<<1, 1024, 0, st>>>(v0, n, Qcols, state);
+  return cudaGetLastError();
+}
+
+// phase 0: w = A q_j and partial h_i = Q_i . w (i <= j); last block reduces -> h
+__global__ void __launch_bounds__(kLzThreads) lanczos_gemv_kernel(
+    const double* __restrict__ A, int64_t lda, int n, int64_t ldq, int j, const double* __restrict__ Q,
+    double* __restrict__ w, double* __restrict__ h, double* __restrict__ partials, int* counter,
+    DevState* state) {
+  if (state->lanczos_steps >= 0) return;  // stopped
+  __shared__ double ws[64];
+  __shared__ int s_last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = kLzThreads / 32;
+  const int rows_per = (n + gridDim.x - 1) / gridDim.x;
+  const int r0 = blockIdx.x * rows_per, r1 = min(n, r0 + rows_per);
+  const double* q = Q + (size_t)j * ldq;
+  for (int r = r0 + warp; r < r1; r += nw) {
+    const double* a = A + (size_t)r * lda;
+    double s0 = 0.0, s1 = 0.0;
+    int c = lane * 2;
+    for (; c + 64 * 3 + 1 < n; c += 64 * 4) {
+      const double2 x0 = __ldg(reinterpret_cast<const double2*>(a + c));
+      const double2 x1 = __ldg(reinterpret_cast<const double2*>(a + c + 64));
+      const double2 x2 = __ldg(reinterpret_cast<const double2*>(a + c + 128));
+      const double2 x3 = __ldg(reinterpret_cast<const double2*>(a + c + 192));
+      const double2 y0 = *reinterpret_cast<const double2*>(q + c);
+      const double2 y1 = *reinterpret_cast<const double2*>(q + c + 64);
+      const double2 y2 = *reinterpret_cast<const double2*>(q + c + 128);
+      const double2 y3 = *reinterpret_cast<const double2*>(q + c + 192);
+      s0 += x0.x * y0.x + x1.x * y1.x + x2.x * y2.x + x3.x * y3.x;
+      s1 += x0.y * y0.y + x1.y * y1.y + x2.y * y2.y + x3.y * y3.y;
+    }
+    for (; c < n; c += 64) {
+      s0 += a[c] * q[c];
+      if (c + 1 < n) s1 += a[c + 1] * q[c + 1];
+    }
+    const double s = warp_sum(s0 + s1);
+    if (lane == 0) {
+      w[r] = s;
+      if (r - r0 < 64) ws[r - r0] = s;
+    }
+  }
+  __syncthreads();
+  // partial dots with Q_0..Q_j over this block's rows (one warp per vector)
+  for (int i = warp; i <= j; i += nw) {
+    const double* qi = Q + (size_t)i * ldq;
+    double s = 0.0;
+    for (int r = r0 + lane; r < r1; r += 32) s += qi[r] * ((r - r0 < 64) ? ws[r - r0] : w[r]);
+    s = warp_sum(s);
+    if (lane == 0) partials[(size_t)blockIdx.x * kMaxLanczos + i] = s;
+  }
+  if (last_block_done(counter, &s_last)) {
+    __threadfence();
+    for (int i = threadIdx.x; i <= j; i += blockDim.x) {
+      double s = 0.0;
+      for (int b = 0; b < (int)gridDim.x; ++b) s += __ldcg(partials + (size_t)b * kMaxLanczos + i);
+      h[i] = s;
+    }
+    if (threadIdx.x == 0) *counter = 0;
+  }
+}
+
+// phase 1/2: w -= Q h (rows of this block), then partial dots (phase 1) or partial |w|^2 (phase 2)
+__global__ void __launch_bounds__(kLzThreads) lanczos_orth_kernel(
+    int n, int64_t ldq, int j, const double* __restrict__ Q, double* __restrict__ w, double* __restrict__ h,
+    double* __restrict__ h_next, double* __restrict__ partials, int* counter, DevState* state,
+    int phase) {
+  if (state->lanczos_steps >= 0) return;
+  __shared__ double hs[kMaxLanczos];
+  __shared__ int s_last;
+  __shared__ double red[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = kLzThreads / 32;
+  for (int i = threadIdx.x; i <= j; i += blockDim.x) hs[i] = h[i];
+  if (phase == 1 && threadIdx.x == 0) state->lanczos_alpha[j] = h[j];  // alpha_j = q_j . A q_j
+  __syncthreads();
+  const int rows_per = (n + gridDim.x - 1) / gridDim.x;
+  const int r0 = blockIdx.x * rows_per, r1 = min(n, r0 + rows_per);
+  for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+    double v = w[r];
+    for (int i = 0; i <= j; ++i) v -= Q[(size_t)i * ldq + r] * hs[i];
+    w[r] = v;
+  }
+  __syncthreads();
+  if (phase == 1) {
+    for (int i = warp; i <= j; i += nw) {
+      const double* qi = Q + (size_t)i * ldq;
+      double s = 0.0;
+      for (int r = r0 + lane; r < r1; r += 32) s += qi[r] * w[r];
+      s = warp_sum(s);
+      if (lane == 0) partials[(size_t)blockIdx.x * kMaxLanczos + i] = s;
+    }
+  } else {
+    double s = 0.0;
+    for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) s += w[r] * w[r];
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) partials[(size_t)blockIdx.x * kMaxLanczos] = s;
+  }
+  if (last_block_done(counter, &s_last)) {
+    __threadfence();
+    if (phase == 1) {
+      for (int i = threadIdx.x; i <= j; i += blockDim.x) {
+        double s = 0.0;
+        for (int b = 0; b < (int)gridDim.x; ++b)
+          s += __ldcg(partials + (size_t)b * kMaxLanczos + i);
+        h_next[i] = s;
+      }
+    } else if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int b = 0; b < (int)gridDim.x; ++b) s += __ldcg(partials + (size_t)b * kMaxLanczos);
+      const double beta = sqrt(s);
+      double amax = 1.0;
+      for (int i = 0; i <= j; ++i) amax = fmax(amax, fabs(state->lanczos_alpha[i]));
+      if (beta <= 1e-12 * amax) {
+        state->lanczos_beta[j] = 0.0;
+        state->lanczos_steps = j + 1;  // breakdown: stop
+        atomicOr(&state->flags, PF_FLAG_LANCZOS_BREAK);
+      } else {
+        state->lanczos_beta[j] = beta;
+      }
+    }
+    if (threadIdx.x == 0) *counter = 0;
+  }
+}
+
+__global__ void lanczos_next_kernel(int n, int64_t ldq, int j, double* Q, const double* w,
+                                    DevState* state) {
+  if (state->lanczos_steps >= 0) return;
+  const double inv = 1.0 / state->lanczos_beta[j];
+  double* q = Q + (size_t)(j + 1) * ldq;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
+    q[r] = w[r] * inv;
+}
+
+cudaError_t lanczos_step_launch(const double* A, int64_t lda, int n, int64_t ldq, int j,
+                                double* Qcols, double* w, double* h, double* partials,
+                                int* counter, DevState* state, cudaStream_t st) {
+  const int nb = lanczos_blocks(n);
+  double* h1 = h;
+  double* h2 = h + kMaxLanczos;
+  lanczos_gemv_kernel<<<nb, kLzThreads, 0, st>>>(A, lda, n, ldq, j, Qcols, w, h1, partials,
+                                                 counter, state);
+  lanczos_orth_kernel<<<nb, kLzThreads, 0, st>>>(n, ldq, j, Qcols, w, h1, h2, partials, counter,
+                                                 state, 1);
+  lanczos_orth_kernel<<<nb, kLzThreads, 0, st>>>(n, ldq, j, Qcols, w, h2, nullptr, partials,
+                                                 counter, state, 2);
+  lanczos_next_kernel<<<std::max(1, std::min(148, (n + 255) / 256)), 256, 0, st>>>(n, ldq, j,
+                                                                                  Qcols, w, state);
+  return cudaGetLastError();
+}
+
+// build T (m_eff x m_eff) from alpha/beta; m_eff is written to scratch int for the Jacobi
+__global__ void lanczos_T_kernel(int m, double* T, DevState* state, int* m_out) {
+  int me = state->lanczos_steps;
+  if (me < 0) me = m;  // ran all m steps
+  if (threadIdx.x == 0) {
+    *m_out = me;
+    state->lanczos_steps = me;
+  }
+  for (int e = threadIdx.x; e < me * me; e += blockDim.x) {
+    const int i = e / me, k = e % me;
+    double v = 0.0;
+    if (i == k) v = state->lanczos_alpha[i];
+    else if (k == i + 1) v = state->lanczos_beta[i];
+    else if (i == k + 1) v = state->lanczos_beta[k];
+    T[e] = v;
+  }
+}
+
+__global__ void lanczos_extremes_kernel(const double* theta, const double* S, const int* m_dev,
+                                        double* lo_hi, DevState* state) {
+  const int me = *m_dev;
+  const double bl = state->lanczos_beta[me - 1];
+  const double rmin = fabs(bl * S[(me - 1) * me + (me - 1)]);
+  const double rmax = fabs(bl * S[(me - 1) * me + 0]);
+  const double lo = theta[me - 1] - rmin, hi = theta[0] + rmax;
+  lo_hi[0] = lo;
+  lo_hi[1] = hi;
+  state->lanczos[0] = lo;
+  state->lanczos[1] = hi;
+  state->have_lanczos = 1;
+}
+
+cudaError_t lanczos_finish_launch(int m, double* T, double* theta, double* S, double* lo_hi,
+                                  DevState* state, cudaStream_t st) {
+  int* m_dev = reinterpret_cast<int*>(&state->scratch[0]);
+  lanczos_T_kernel<<<1, 256, 0, st>>>(m, T, state, m_dev);
+  cudaError_t e = jacobi_launch(T, m, m_dev, theta, S, state, 1e-15, 40, st);
+  if (e != cudaSuccess) return e;
+  lanczos_extremes_kernel<<<1, 1, 0, st>>>(theta, S, m_dev, lo_hi, state);
+  return cudaGetLastError();
+}
+
+// =============================================================================== perturb
+__global__ void perturb_kernel(double* A, int64_t lda, const double* E, int64_t lde, int rows,
+                               int cols) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = blockIdx.y;
+  if (c < cols && r < rows) A[(size_t)r * lda + c] += E[(size_t)r * lde + c];
+}
+
+cudaError_t perturb_launch(double* A, int64_t lda, const double* E, int64_t lde, int rows,
+                           int cols, cudaStream_t st) {
+  dim3 grid((cols + 255) / 256, rows);
+  perturb_kernel<<<grid, 256, 0, st>>>(A, lda, E, lde, rows, cols);
+  return cudaGetLastError();
+}
+
+}  // namespace pf

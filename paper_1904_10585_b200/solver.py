@@ -1,0 +1,130 @@
+"""GPU driver of the PFPG / PFAM / sweep iteration (SURVEY §8(c) order) over the C ABI.
+
+Python only sequences C-ABI calls and moves inputs to device memory; the interval, filter,
+orthonormalisation, Rayleigh-Ritz, spectral operator and update all run in libpf.so kernels.
+The per-iteration order matches the paper: eq:pfpg1/eq:pfpg2 and
+eq:PFAM1/eq:PFAM2, shifted so each iteration is filter -> orth -> RR -> f -> update.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from pfinputs import (Config, initial_block, lanczos_start, cfg1_problem, cfg1_noise, pfpg_problem,
+                      pfam_problem)
+
+from ._lib import Context, PF_OP_PSD, PF_OP_SOFT_THRESHOLD
+
+
+def _dev(x, dtype=torch.float64):
+    return torch.as_tensor(x, dtype=dtype).cuda()
+
+
+def _bits(b: np.ndarray) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(b).view(np.int32)).cuda()
+
+
+class Solver:
+    """Holds the device state of one run: iterate A/Z (n x n), block U, factors V, f."""
+
+    def __init__(self, cfg: Config, problem: dict | None = None, stream=None):
+        self.cfg = cfg
+        n, p, d = cfg.n, cfg.p, cfg.d
+        self.stream = stream
+        self.ctx = Context(n, p, d)
+        self.psd = cfg.mode in ("sweep_psd", "pfam")
+        self.op = PF_OP_PSD if self.psd else PF_OP_SOFT_THRESHOLD
+        self.U = _dev(initial_block(cfg))
+        self.V = torch.empty((n, p), dtype=torch.float64, device="cuda")
+        self.theta = torch.empty(p, dtype=torch.float64, device="cuda")
+        self.f = torch.zeros(p, dtype=torch.float64, device="cuda")
+        self.rank = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.obj = torch.zeros(2, dtype=torch.float64, device="cuda")
+        self.lohi = torch.zeros(2, dtype=torch.float64, device="cuda")
+        self.interval = torch.zeros(2, dtype=torch.float64, device="cuda")
+        self.k = 0
+        self.thr = 0.0
+        if cfg.mode in ("sweep_psd", "sweep_soft"):
+            A0 = cfg1_problem(cfg) if problem is None else problem["A0"]
+            self.A = _dev(A0)
+            self.thr = cfg.theta
+        elif cfg.mode == "pfpg":
+            prob = pfpg_problem(cfg) if problem is None else problem
+            self.prob = prob
+            self.omega = _bits(prob["omega_bits"])
+            self.W = _dev(prob["W"])
+            self.mu = prob["mu"]
+            self.thr = cfg.tau * prob["mu"]
+            self.A = torch.empty((n, n), dtype=torch.float64, device="cuda")
+            # X_0 = 0: A_0 = 0 - tau Omega o (0 - M)  (the update kernel with zero factors)
+            self.ctx.prox_step(self.V.zero_(), self.f, cfg.tau, self.omega, self.W, self.A,
+                               self.obj, stream)
+        elif cfg.mode == "pfam":
+            prob = pfam_problem(cfg) if problem is None else problem
+            self.prob = prob
+            self.adj = _bits(prob["adj_bits"])
+            self.deg = _dev(prob["deg"])
+            self.A = torch.zeros((n, n), dtype=torch.float64, device="cuda")
+            # Z_0 = 0 -> Z_1 = prox_tG(0) = offdiag(-tC) + I  (reading R9)
+            self.ctx.admm_step(self.V.zero_(), self.f, cfg.t, self.adj, self.deg, self.A,
+                               self.obj, stream)
+        else:
+            raise ValueError(cfg.mode)
+        self.ctx.orth(self.U, stream)
+        self._v0 = {}
+
+    def lanczos_vector(self, k: int) -> torch.Tensor:
+        if k not in self._v0:
+            self._v0[k] = _dev(lanczos_start(self.cfg, k))
+        return self._v0[k]
+
+    def step(self):
+        """One iteration k: interval -> filter (+warm-up at k = 0) -> RR -> f -> update."""
+        cfg, ctx, st, k = self.cfg, self.ctx, self.stream, self.k
+        if k == 0 or (self.psd and k % cfg.lanczos_every == 0):
+            ctx.lanczos(self.A, self.lanczos_vector(k), cfg.lanczos_steps, self.lohi, st)
+        if self.psd:
+            ctx.interval_psd(self.lohi, cfg.eta, self.interval, st)
+        else:
+            ctx.interval_soft(self.thr, cfg.eta, self.interval, st)
+        for _ in range(cfg.warmup if k == 0 else 1):
+            ctx.filter(self.A, self.U, self.interval, 1, cfg.rho_max, st)
+        ctx.rayleigh_ritz(self.A, self.U, self.V, self.theta, st)
+        ctx.spectral_op(self.op, self.thr, self.theta, self.f, self.rank, st)
+        if cfg.mode == "pfpg":
+            ctx.prox_step(self.V, self.f, cfg.tau, self.omega, self.W, self.A, self.obj, st)
+        elif cfg.mode == "pfam":
+            ctx.admm_step(self.V, self.f, cfg.t, self.adj, self.deg, self.A, self.obj, st)
+        self.k += 1
+
+    def perturb(self, E: torch.Tensor):
+        self.ctx.perturb(self.A, E, self.stream)
+
+    def objective(self) -> tuple[float, float]:
+        """(objective, aux) on the host: PFPG (fit + mu sum|f|, fit); PFAM (<C,W>, ||dZ||_F)."""
+        o = self.obj.cpu().numpy()
+        if self.cfg.mode == "pfpg":
+            return float(o[0] + self.mu * o[1]), float(o[0])
+        return float(o[0]), float(o[1])
+
+
+def run(cfg: Config, iters: int | None = None, record: bool = True, problem=None) -> dict:
+    """Run K iterations on the GPU, recording per-iteration factors / objectives on the host."""
+    K = cfg.iters if iters is None else iters
+    s = Solver(cfg, problem)
+    recs = []
+    for k in range(K):
+        s.step()
+        rec = {"k": k}
+        if record:
+            f = s.f.cpu().numpy()
+            keep = f != 0.0
+            rec.update(theta=s.theta.cpu().numpy(), rank=int(s.rank.item()),
+                       V=s.V.cpu().numpy()[:, keep], f=f[keep])
+            if cfg.mode in ("pfpg", "pfam"):
+                rec["objective"], rec["aux"] = s.objective()
+        if cfg.mode in ("sweep_psd", "sweep_soft") and k + 1 < K:
+            s.perturb(_dev(cfg1_noise(cfg, k)))
+        recs.append(rec)
+    torch.cuda.synchronize()
+    return {"records": recs, "status": s.ctx.status(), "solver": s}

