@@ -1,0 +1,336 @@
+"""bench.py -- PFAM iterations/s and poly-filter TFLOP/s on config 3 (n = 16384, p = 64, d = 8).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 3]
+
+A step is one whole iteration of the hot path: interval (Lanczos
+refresh every 10 iterations, as it falls), Chebyshev filter (d fp64 DMMA GEMM passes),
+CholeskyQR2, Rayleigh-Ritz (one more GEMM pass + Jacobi), spectral operator, and the fused
+rank-p rebuild + PFAM update of the 2 GiB iterate.  Inputs are synthetic and
+larger than L2 (the iterate is 2 GiB), so no L2 flush is needed between steps.
+
+N > 1 (torchrun): configs 1-3 do not shard: every rank runs an independent
+replica (seed + rank), value = sum of per-rank throughput over the max-over-ranks time.
+`--impl reference` times the CPU oracle (oracle/) on the host cores on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "poly-filter TFLOP/s and PFPG/PFAM iterations/s at n=16384, 1/2/4/8 B200"
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+           0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+           0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+           0x100: "display_clock_setting"}
+
+
+def peaks() -> dict:
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            try:
+                sm, mx, pw, rs = [x.strip() for x in line.split(",")]
+                self.samples.append((float(sm), float(mx), float(pw), int(rs, 16)))
+            except Exception:
+                pass
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(2)
+        except Exception:
+            self.proc.kill()
+        s = self.samples
+        if not s:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        loaded = [x for x in s if x[2] > 200] or s
+        bits = 0
+        for x in loaded:
+            bits |= x[3]
+        return {"sm_mhz": statistics.median(x[0] for x in loaded),
+                "sm_max_mhz": max(x[1] for x in s),
+                "power_w_max": max(x[2] for x in s),
+                "samples": len(s),
+                "reasons": [v for k, v in REASONS.items() if bits & k and k != 0x1]}
+
+
+def bench_cfg(cfg_id: int):
+    from pfinputs import CONFIGS
+    return CONFIGS[cfg_id]
+
+
+# ============================================================================ our arm
+def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
+    import torch
+    import torch.distributed as dist
+    from pfinputs import reduced
+    from paper_1904_10585_b200 import Solver
+    from paper_1904_10585_b200._lib import kernel_launches
+
+    torch.cuda.set_device(local_rank)
+    cfg = bench_cfg(args.config)
+    if world > 1:
+        cfg = reduced(cfg, seed=cfg.seed + rank)          # independent replica per rank
+    n, p, d = cfg.n, cfg.p, cfg.d
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        s = Solver(cfg, stream=stream)
+        for _ in range(args.warmup):
+            s.step()
+        # pre-stage the Lanczos start vectors the timed steps will use (host->device, untimed)
+        for k in range(s.k, s.k + args.steps):
+            if k % cfg.lanczos_every == 0:
+                s.lanczos_vector(k)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    s.ctx.profile(True)
+    l0 = kernel_launches()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(args.steps):
+            s.step()
+        e1.record(stream)
+    torch.cuda.synchronize()
+    launches = kernel_launches() - l0
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    gemm_ms, gemm_n = s.ctx.profile_read(stream)
+    s.ctx.profile(False)
+    clk = clocks.stop()
+    status = s.ctx.status(stream)
+    obj = s.objective()
+
+    # ---------------------------------------------------------------- end to end
+    e2e = run_e2e(cfg, args, stream)
+
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    if rank != 0:
+        return None
+    per_step_ms = ms_max / args.steps
+    value = world * args.steps / (ms_max / 1e3)
+    flops_gemm = 2.0 * n * n * p                      # algorithmic flops of one Chebyshev step
+    gemm_avg_ms = gemm_ms / max(gemm_n, 1)
+    achieved = flops_gemm / (gemm_avg_ms / 1e3) / 1e12
+    pk = peaks()
+    fp64_peak = pk.get("fp64_dmma_tflops")
+    peak_src = "MEASURED_PEAKS.json fp64_dmma_tflops"
+    if fp64_peak is None:
+        fp64_peak = 37.1
+        peak_src = "measured on this pool by tools/probe/peaks.cu (profiles/r01_probe_peaks.log): " \
+                   "fp64 DMMA m16n8k4 37.1 TF/s at 1965 MHz; MEASURED_PEAKS.json has no fp64 entry"
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "gemm_traffic.json")))
+        if tr.get("n") == n and tr.get("p") == p:
+            traffic = tr["dram_bytes_per_launch"]
+    except Exception:
+        pass
+    filter_flops_per_step = 2.0 * d * n * n * p
+    cpu = cpu_baseline(cfg, args) if (world == 1 and not args.no_cpu) else None
+    out = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "it/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": per_step_ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (BASELINE configs[2] recipe, DESIGN.md §3)",
+        "config": {"workload": f"config 3: PFAM max-cut SDP, n={n}, p={p}, d={d}, G(n,{cfg.edge_prob})",
+                   "n": n, "p": p, "d": d, "lanczos_every": cfg.lanczos_every,
+                   "l2": "inputs larger than L2 (2 GiB fp64 iterate re-read every pass)",
+                   "parallelism": "replicas" if world > 1 else "1 GPU"},
+        "filter_tflops": world * filter_flops_per_step * args.steps / (ms_max / 1e3) / 1e12,
+        "roofline": {"bound": "tensor", "kernel": "cheb_gemm_kernel<64> (fp64 DMMA)",
+                     "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                     "frac": achieved / fp64_peak, "traffic": traffic,
+                     "peak_source": peak_src,
+                     "algorithmic_per_launch": {"flops": flops_gemm, "bytes": 8.0 * n * n},
+                     "avg_launch_ms": gemm_avg_ms, "launches": gemm_n,
+                     "share_of_step": gemm_ms / ms},
+        "clocks": clk,
+        "gpu_launches": launches,
+        "e2e": e2e,
+        "device_status": status["names"],
+        "objective_last": obj,
+    }
+    if cpu is not None:
+        out["cpu_baseline"] = cpu
+    return out
+
+
+def run_e2e(cfg, args, stream) -> dict:
+    """End to end through the public API from host-resident problem data:
+    pinned H2D of the graph bitmask, degrees and U0 + (W + K) iterations with a D2H read of the
+    objective every iteration + D2H of the final factors (V, f); it/s over K counted steps."""
+    import numpy as np
+    import torch
+    from pfinputs import initial_block, lanczos_start, pfam_problem
+    from paper_1904_10585_b200 import Solver
+    prob = pfam_problem(cfg)
+    host = {"adj_bits": torch.from_numpy(prob["adj_bits"].view(np.int32)).pin_memory(),
+            "deg": torch.from_numpy(prob["deg"]).pin_memory(),
+            "U0": torch.from_numpy(initial_block(cfg)).pin_memory()}
+    K = args.steps + args.warmup
+    v0 = {k: torch.from_numpy(lanczos_start(cfg, k)).pin_memory()
+          for k in range(K) if k % cfg.lanczos_every == 0}
+    obj_host = torch.empty((K, 2), dtype=torch.float64).pin_memory()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    h2d = d2h = 0
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        dev = {k: v.cuda(non_blocking=True) for k, v in host.items()}
+        h2d += sum(v.numel() * v.element_size() for v in host.values())
+        s = Solver(cfg, problem={"adj_bits": None, "deg": None, "t": cfg.t, "_dev": dev},
+                   stream=stream)
+        for k in range(K):
+            if k in v0:
+                s._v0[k] = v0[k].cuda(non_blocking=True)
+                h2d += v0[k].numel() * 8
+            s.step()
+            obj_host[k].copy_(s.obj, non_blocking=True)
+            d2h += 16
+        Vh = s.V.to("cpu", non_blocking=True)
+        fh = s.f.to("cpu", non_blocking=True)
+        d2h += Vh.numel() * 8 + fh.numel() * 8
+        e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    return {"value": K / (ms / 1e3),
+            "unit": "it/s", "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": d2h / K,
+            "iterations": K, "ms_total": ms,
+            "what": "solve from host data: H2D problem + U0, W+K iterations, per-iteration "
+                    "objective D2H, final factors D2H"}
+
+
+# ============================================================================ CPU oracle
+def cpu_baseline(cfg, args, budget_iters: int = 3) -> dict:
+    """The oracle as it stands (oracle.run) on the host cores: iterations 1..budget_iters of
+    the same config after its k = 0 iteration; setup (problem, dense C) untimed."""
+    import numpy as np
+    import oracle
+    stamps = []
+    t0 = [None]
+
+    def prog(rec):
+        stamps.append(time.perf_counter())
+
+    t_start = time.perf_counter()
+    oracle.run(cfg, iters=budget_iters + 1, record_factors=False, progress=prog)
+    per = (stamps[-1] - stamps[0]) / budget_iters
+    cores = len(os.sched_getaffinity(0))
+    return {"value": 1.0 / per, "unit": "it/s", "cores": cores, "kind": "oracle",
+            "sample": f"config 3 full size, oracle iterations k=1..{budget_iters} (k=0 and "
+                      f"setup untimed); numpy/OpenBLAS fp64 on {cores} host threads",
+            "wall_s": time.perf_counter() - t_start}
+
+
+def run_reference(args, rank: int, world: int) -> dict | None:
+    if rank != 0:
+        return None
+    cfg = bench_cfg(args.config)
+    K = max(1, min(args.steps, 3))
+    import oracle
+    stamps = []
+    oracle.run(cfg, iters=K + 1, record_factors=False,
+               progress=lambda rec: stamps.append(time.perf_counter()))
+    per = (stamps[-1] - stamps[0]) / K
+    cores = len(os.sched_getaffinity(0))
+    v = 1.0 / per
+    return {"impl": "reference", "metric": METRIC, "value": v, "unit": "it/s", "n_gpus": world,
+            "steps": K, "warmup": 1, "ms_per_step": per * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (BASELINE configs[2] recipe)",
+            "config": {"workload": f"config 3: PFAM max-cut SDP, n={cfg.n}, p={cfg.p}, d={cfg.d}"},
+            "cpu_baseline": {"value": v, "unit": "it/s", "cores": cores, "kind": "oracle",
+                             "sample": f"oracle iterations k=1..{K} of config 3 (k=0 untimed)"},
+            "e2e": {"value": v, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        out = run_reference(args, rank, world)
+    else:
+        if world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        out = run_ours(args, rank, world, local_rank)
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            dist.destroy_process_group()
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

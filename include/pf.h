@@ -140,6 +140,17 @@ pf_status pf_admm_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f
                        const uint32_t* adj, int64_t ldadj, const double* deg, double* Z,
                        int64_t ldz, double* obj, pf_stream stream);
 
+/* ---------------------------------------------------------------------------- measurement */
+/* Enable (1) / disable (0) per-launch CUDA-event timing of the Chebyshev-step GEMM (the
+ * dominant kernel): each launch inside pf_filter / pf_rayleigh_ritz is bracketed by events on
+ * its own stream.  Resets the accumulated record.  Up to 4096 launches are recorded. */
+pf_status pf_profile(pf_ctx ctx, int32_t enable);
+/* Synchronises `stream`; returns the summed GEMM time (ms) and the number of timed launches
+ * since pf_profile, then clears the record.  PF_ERR_ARG if launches were dropped. */
+pf_status pf_profile_read(pf_ctx ctx, pf_stream stream, double* gemm_ms, int64_t* gemm_launches);
+/* Process-wide number of CUDA kernels launched by this library so far. */
+long long pf_kernel_launches(void);
+
 /* Workload helper (not the method): A <- A + E (config 1 noise, BASELINE configs[0]). */
 pf_status pf_perturb(pf_ctx ctx, double* A, int64_t lda, const double* E, int64_t lde,
                      pf_stream stream);

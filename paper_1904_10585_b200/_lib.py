@@ -50,6 +50,9 @@ def load() -> ctypes.CDLL:
         "pf_prox_step": [P, P, I64, P, D, P, I64, P, I64, I32, P, I64, P, P],
         "pf_admm_step": [P, P, I64, P, D, P, I64, P, P, I64, P, P],
         "pf_perturb": [P, P, I64, P, I64, P],
+        "pf_profile": [P, I32],
+        "pf_profile_read": [P, P, ctypes.POINTER(D), ctypes.POINTER(I64)],
+        "pf_kernel_launches": [],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -59,8 +62,14 @@ def load() -> ctypes.CDLL:
     lib.pf_last_error.restype = ctypes.c_char_p
     lib.pf_local_rows.restype = ctypes.c_int64
     lib.pf_row0.restype = ctypes.c_int64
+    lib.pf_kernel_launches.restype = ctypes.c_longlong
     _lib = lib
     return lib
+
+
+def kernel_launches() -> int:
+    """Process-wide number of CUDA kernels launched by libpf."""
+    return int(load().pf_kernel_launches())
 
 
 class PFError(RuntimeError):
@@ -132,6 +141,16 @@ class Context:
                                                   ctypes.byref(rb), lohi), "pf_get_device_status")
         names = [v for k, v in FLAGS.items() if fl.value & k]
         return {"flags": fl.value, "names": names, "rebases": rb.value, "lanczos": (lohi[0], lohi[1])}
+
+    def profile(self, enable: bool):
+        self._check(self.lib.pf_profile(self.h, 1 if enable else 0), "pf_profile")
+
+    def profile_read(self, stream=None):
+        """(summed ms, launches) of the Chebyshev-step GEMM since profile(True)."""
+        ms, n = ctypes.c_double(), ctypes.c_int64()
+        self._check(self.lib.pf_profile_read(self.h, _stream(stream), ctypes.byref(ms),
+                                             ctypes.byref(n)), "pf_profile_read")
+        return ms.value, n.value
 
     def lanczos(self, A, v0, m, lo_hi, stream=None):
         self._check(self.lib.pf_lanczos(self.h, _ptr(A), _ld(A), _ptr(v0), m, _ptr(lo_hi),

@@ -13,9 +13,20 @@
 #include "../../include/pf.h"
 #include "pf_kernels.cuh"
 
+#include <atomic>
+#include <vector>
+
 using namespace pf;
 
+static std::atomic<long long> g_launches{0};
+void pf::count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
 struct pf_ctx_s {
+  // profiling of the dominant kernel: event pairs around every Chebyshev-step GEMM launch
+  bool prof = false;
+  std::vector<cudaEvent_t> ev;
+  size_t ev_used = 0;
+  long long prof_dropped = 0;
   int64_t n = 0, n_local = 0, row0 = 0;
   int p = 0, d = 0, rank = 0, world = 1, num_sms = 148;
   DevState* state = nullptr;
@@ -202,8 +213,38 @@ pf_status pf_create_dist(int64_t n, int32_t p, int32_t degree, pf_dtype dtype,
   return PF_OK;
 }
 
+long long pf_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
+
+pf_status pf_profile(pf_ctx ctx, int32_t enable) {
+  if (!ctx) return PF_ERR_ARG;
+  if (enable && ctx->ev.empty()) {
+    ctx->ev.resize(8192);
+    for (auto& e : ctx->ev) PF_CU(cudaEventCreate(&e));
+  }
+  ctx->prof = enable != 0;
+  ctx->ev_used = 0;
+  ctx->prof_dropped = 0;
+  return PF_OK;
+}
+
+pf_status pf_profile_read(pf_ctx ctx, pf_stream stream, double* gemm_ms, int64_t* gemm_launches) {
+  if (!ctx || !gemm_ms || !gemm_launches) return PF_ERR_ARG;
+  PF_CU(cudaStreamSynchronize((cudaStream_t)stream));
+  double tot = 0.0;
+  for (size_t i = 0; i + 1 < ctx->ev_used; i += 2) {
+    float ms = 0.f;
+    PF_CU(cudaEventElapsedTime(&ms, ctx->ev[i], ctx->ev[i + 1]));
+    tot += ms;
+  }
+  *gemm_ms = tot;
+  *gemm_launches = (int64_t)(ctx->ev_used / 2);
+  ctx->ev_used = 0;
+  return ctx->prof_dropped ? PF_ERR_ARG : PF_OK;
+}
+
 pf_status pf_destroy(pf_ctx ctx) {
   if (!ctx) return PF_ERR_ARG;
+  for (auto e : ctx->ev) cudaEventDestroy(e);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   void* ptrs[] = {ctx->state, ctx->Y[0], ctx->Y[1], ctx->Y[2], ctx->Yfull, ctx->Wbuf,
                   ctx->Vfull, ctx->G, ctx->Rinv, ctx->Yeig, ctx->gram_part, ctx->cheb_ws,
@@ -300,8 +341,15 @@ static pf_status gemm_step(pf_ctx ctx, int bidx, const double* ycur, const doubl
     if (s != PF_OK) return s;
     mb = &ctx->mapBfull;
   }
+  const bool rec = ctx->prof && ctx->ev_used + 2 <= ctx->ev.size();
+  if (ctx->prof && !rec) ++ctx->prof_dropped;
+  if (rec) PF_CU(cudaEventRecord(ctx->ev[ctx->ev_used], st));
   PF_CU(cheb_gemm_launch(ctx->plan, ctx->mapA, *mb, ycur, yprev, out, coef, ctx->cheb_ws,
                          ctx->cheb_cnt, st));
+  if (rec) {
+    PF_CU(cudaEventRecord(ctx->ev[ctx->ev_used + 1], st));
+    ctx->ev_used += 2;
+  }
   return PF_OK;
 }
 

@@ -66,9 +66,10 @@ __global__ void __launch_bounds__(GemmCfg<P>::THREADS, 1)
     cheb_gemm_kernel(const __grid_constant__ CUtensorMap mapA,
                      const __grid_constant__ CUtensorMap mapB, ChebArgs args) {
   using C = GemmCfg<P>;
-  extern __shared__ unsigned char smem_raw[];
-  unsigned char* smem =
-      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // align to 1024 B (SWIZZLE_128B atom) by pointer offset so the compiler keeps the shared
+  // address space (a uintptr_t round trip would turn every fragment load into a generic LD)
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   double* sA = reinterpret_cast<double*>(smem);
   double* sB = reinterpret_cast<double*>(smem + C::STAGES * C::A_BYTES);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
@@ -104,7 +105,10 @@ __global__ void __launch_bounds__(GemmCfg<P>::THREADS, 1)
         mbar_wait(&empty[stage], phase ^ 1u);
         mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
         tma_load_2d(sA + stage * (C::BM * C::BK), &mapA, &full[stage], kb * C::BK, tile * C::BM);
-        tma_load_2d(sB + stage * (C::BK * P), &mapB, &full[stage], 0, kb * C::BK);
+        // B = Y_j rows [kb*16, kb*16+16): P/8 boxes of 16 x 8 doubles, SWIZZLE_64B each
+#pragma unroll
+        for (int j = 0; j < P / 8; ++j)
+          tma_load_2d(sB + stage * (C::BK * P) + j * 128, &mapB, &full[stage], 8 * j, kb * C::BK);
         if (++stage == C::STAGES) {
           stage = 0;
           phase ^= 1u;
@@ -133,7 +137,14 @@ __global__ void __launch_bounds__(GemmCfg<P>::THREADS, 1)
       a_off[mt][ks] = r * 16 + ((((k >> 1) ^ (r & 7))) << 1) + (k & 1);
     }
   }
-  const int b_off = t4 * P + wn * C::WN + g8;
+  // B stage = P/8 boxes [16 k][8 n] with SWIZZLE_64B (16-byte chunk ^= (k >> 1) & 3):
+  // element (k, n): (n >> 3) * 128 + k * 8 + ((((n & 7) >> 1) ^ ((k >> 1) & 3)) << 1) + (n & 1)
+  int b_off[4];
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    const int k = ks * 4 + t4;
+    b_off[ks] = ((wn * C::WN) >> 3) * 128 + k * 8 + ((((g8 >> 1) ^ ((k >> 1) & 3))) << 1) + (g8 & 1);
+  }
 
   long long it = it_begin;
   while (it < it_end) {
@@ -163,7 +174,7 @@ __global__ void __launch_bounds__(GemmCfg<P>::THREADS, 1)
           af[mt][1] = a[a_off[mt][ks] + 8 * 16];
         }
 #pragma unroll
-        for (int nt = 0; nt < C::NT; ++nt) bf[nt] = b[ks * 4 * P + b_off + nt * 8];
+        for (int nt = 0; nt < C::NT; ++nt) bf[nt] = b[b_off[ks] + nt * 128];
 #pragma unroll
         for (int mt = 0; mt < C::MT; ++mt)
 #pragma unroll
@@ -296,10 +307,10 @@ bool encode_map_B(CUtensorMap* map, const double* B, int p, int n_k) {
   if (!enc) return false;
   cuuint64_t dims[2] = {(cuuint64_t)p, (cuuint64_t)n_k};
   cuuint64_t strides[1] = {(cuuint64_t)p * 8};
-  cuuint32_t box[2] = {(cuuint32_t)p, 16};
+  cuuint32_t box[2] = {8, 16};
   cuuint32_t es[2] = {1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(B), dims, strides, box,
-             es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -343,6 +354,7 @@ static cudaError_t launch_p(const ChebGemmPlan& pl, const CUtensorMap& mapA,
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
+  count_launch();
   cheb_gemm_kernel<P><<<pl.grid, C::THREADS, C::SMEM, st>>>(mapA, mapB, a);
   return cudaGetLastError();
 }

@@ -8,6 +8,9 @@
 
 namespace pf {
 
+// process-wide count of kernels launched by libpf (defined in pf_api.cu)
+void count_launch();
+
 // ---- Chebyshev-step GEMM (pf_gemm.cu): out = s1*(A B) + s2*Ycur + s3*Yprev (rows of A local)
 struct ChebGemmPlan {
   int p;

@@ -232,6 +232,7 @@ static cudaError_t rb_launch(const double* V, int64_t ldv, const double* f, doub
     attr = true;
   }
   dim3 grid((n + kRbTile - 1) / kRbTile, (n_rows + kRbTile - 1) / kRbTile);
+  count_launch();
   rebuild_kernel<P, PFPG><<<grid, 128, smem, st>>>(V, ldv, f, tt, bits, ldb, W, ldw, r, ldw_s, deg,
                                                    Out, ldo, n_rows, n, row0, partials, counter,
                                                    obj);

@@ -124,6 +124,7 @@ cudaError_t gram_launch(const double* X, const double* Y, int n_rows, int p, dou
   (void)counter;
   const int rpb = gram_rows_per_block(n_rows);
   const int nb = std::max(1, (n_rows + rpb - 1) / rpb);
+  count_launch();
   switch (p) {
     case 16: gram_partial_kernel<16><<<nb, 256, 0, st>>>(X, Y, n_rows, rpb, partials, cond); break;
     case 32: gram_partial_kernel<32><<<nb, 256, 0, st>>>(X, Y, n_rows, rpb, partials, cond); break;
@@ -132,6 +133,7 @@ cudaError_t gram_launch(const double* X, const double* Y, int n_rows, int p, dou
     default: return cudaErrorInvalidValue;
   }
   const int pp = p * p;
+  count_launch();
   gram_reduce_kernel<<<(pp + 255) / 256, 256, 0, st>>>(partials, nb, pp, G, cond);
   return cudaGetLastError();
 }
@@ -249,6 +251,7 @@ cudaError_t chol_inv_launch(const double* G, int p, int64_t n_global, double* Ri
                          (int)(128 * 129 * sizeof(double)));
     attr = true;
   }
+  count_launch();
   chol_inv_kernel<<<1, 512, smem, st>>>(G, p, scale, Rinv, state, shift_flag_out, cond);
   return cudaGetLastError();
 }
@@ -324,6 +327,7 @@ static cudaError_t rmul_p(const double* in, int64_t ldi, const double* R, double
     attr = true;
   }
   const int grid = std::max(1, (n_rows + C::BM - 1) / C::BM);
+  count_launch();
   rmul_kernel<P><<<grid, 256, C::SMEM, st>>>(in, ldi, R, out, ldo, n_rows, cond);
   return cudaGetLastError();
 }
@@ -361,6 +365,7 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const double* __restrict__
   extern __shared__ double js[];
   __shared__ double red[32];
   __shared__ int s_cnt;
+  __shared__ double s_norm;
   const int p = p_dev ? *p_dev : p_static;
   if (p <= 0) return;
   const int Pe = p + (p & 1);
@@ -393,6 +398,7 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const double* __restrict__
     }
     off = block_sum(off, red);
     tot = block_sum(tot, red);
+    if (tid == 0) s_norm = sqrt(tot);
     if (off <= tol * tol * tot || off == 0.0) {
       converged = true;
       break;
@@ -417,7 +423,8 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const double* __restrict__
         if (j < p) {
           const double hij = Hp[pk(i, j, Pe)];
           const double hii = Hp[pk(i, i, Pe)], hjj = Hp[pk(j, j, Pe)];
-          if (fabs(hij) > 1e-300 && fabs(hij) > 1e-17 * sqrt(fabs(hii * hjj))) {
+          // threshold Jacobi: skip rotations already below rounding of the diagonal pair
+          if (fabs(hij) > 1e-15 * sqrt(fabs(hii * hjj)) + 1e-18 * s_norm) {
             const double tau = (hjj - hii) / (2.0 * hij);
             t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
             c = 1.0 / sqrt(1.0 + t * t);
@@ -509,6 +516,7 @@ cudaError_t jacobi_launch(const double* H, int p, const int* p_dev, double* thet
     cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
     attr = true;
   }
+  count_launch();
   jacobi_kernel<<<1, 1024, smem, st>>>(H, p, p_dev, theta, Y, state, tol, max_sweeps);
   return cudaGetLastError();
 }
@@ -537,6 +545,7 @@ __global__ void spectral_kernel(int op, double thr, const double* __restrict__ t
 
 cudaError_t spectral_launch(int op, double thr, const double* theta, int p, double* f, int* rank,
                             DevState* state, cudaStream_t st) {
+  count_launch();
   spectral_kernel<<<1, 128, 0, st>>>(op, thr, theta, p, f, rank, state);
   return cudaGetLastError();
 }
@@ -589,6 +598,7 @@ __global__ void plan_kernel(const double* __restrict__ interval, int d, double r
 
 cudaError_t plan_launch(const double* interval, int d, double rho_max, int p, DevState* state,
                         cudaStream_t st) {
+  count_launch();
   plan_kernel<<<1, 32, 0, st>>>(interval, d, rho_max, p, state);
   return cudaGetLastError();
 }
@@ -606,6 +616,7 @@ __global__ void interval_psd_kernel(const double* lo_hi, double eta, double* int
 
 cudaError_t interval_psd_launch(const double* lo_hi, double eta, double* interval,
                                 DevState* state, cudaStream_t st) {
+  count_launch();
   interval_psd_kernel<<<1, 1, 0, st>>>(lo_hi, eta, interval, state);
   return cudaGetLastError();
 }
@@ -619,6 +630,7 @@ __global__ void interval_soft_kernel(double thr, double eta, double* interval) {
 cudaError_t interval_soft_launch(double thr, double eta, double* interval, DevState* state,
                                  cudaStream_t st) {
   (void)state;
+  count_launch();
   interval_soft_kernel<<<1, 1, 0, st>>>(thr, eta, interval);
   return cudaGetLastError();
 }
@@ -630,6 +642,7 @@ __global__ void copy_theta_kernel(const double* theta, int p, DevState* state) {
 }
 
 cudaError_t copy_theta_launch(const double* theta, int p, DevState* state, cudaStream_t st) {
+  count_launch();
   copy_theta_kernel<<<1, 128, 0, st>>>(theta, p, state);
   return cudaGetLastError();
 }
@@ -638,7 +651,7 @@ cudaError_t copy_theta_launch(const double* theta, int p, DevState* state, cudaS
 // Q: (m+1) Lanczos vectors stored column by column (vector j at Q + j*n).
 constexpr int kLzThreads = 256;
 
-int lanczos_blocks(int n_rows) { return std::max(1, std::min(296, (n_rows + 7) / 8)); }
+int lanczos_blocks(int n_rows) { return std::max(1, std::min(4 * 148, (n_rows + 7) / 8)); }
 
 // last-block reduction helper: partials[blk * stride + i], i < cnt -> out[i] (block order)
 __device__ bool last_block_done(int* counter, int* s_last) {
@@ -669,6 +682,7 @@ cudaError_t lanczos_init_launch(const double* v0, int n, double* Qcols, double* 
                                 int* counter, DevState* state, cudaStream_t st) {
   (void)partials;
   (void)counter;
+  count_launch();
   lanczos_init_kernel<<<1, 1024, 0, st>>>(v0, n, Qcols, state);
   return cudaGetLastError();
 }
@@ -689,17 +703,19 @@ __global__ void __launch_bounds__(kLzThreads) lanczos_gemv_kernel(
     const double* a = A + (size_t)r * lda;
     double s0 = 0.0, s1 = 0.0;
     int c = lane * 2;
-    for (; c + 64 * 3 + 1 < n; c += 64 * 4) {
-      const double2 x0 = __ldg(reinterpret_cast<const double2*>(a + c));
-      const double2 x1 = __ldg(reinterpret_cast<const double2*>(a + c + 64));
-      const double2 x2 = __ldg(reinterpret_cast<const double2*>(a + c + 128));
-      const double2 x3 = __ldg(reinterpret_cast<const double2*>(a + c + 192));
-      const double2 y0 = *reinterpret_cast<const double2*>(q + c);
-      const double2 y1 = *reinterpret_cast<const double2*>(q + c + 64);
-      const double2 y2 = *reinterpret_cast<const double2*>(q + c + 128);
-      const double2 y3 = *reinterpret_cast<const double2*>(q + c + 192);
-      s0 += x0.x * y0.x + x1.x * y1.x + x2.x * y2.x + x3.x * y3.x;
-      s1 += x0.y * y0.y + x1.y * y1.y + x2.y * y2.y + x3.y * y3.y;
+    // 8 independent 16-byte streaming loads of A per lane in flight (A is read once: .cs keeps
+    // it out of L1 so the Lanczos vector q stays cached)
+    for (; c + 64 * 7 + 1 < n; c += 64 * 8) {
+      double2 x[8], y[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] = __ldcs(reinterpret_cast<const double2*>(a + c + 64 * u));
+#pragma unroll
+      for (int u = 0; u < 8; ++u) y[u] = __ldg(reinterpret_cast<const double2*>(q + c + 64 * u));
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        s0 += x[u].x * y[u].x;
+        s1 += x[u].y * y[u].y;
+      }
     }
     for (; c < n; c += 64) {
       s0 += a[c] * q[c];
@@ -808,12 +824,16 @@ cudaError_t lanczos_step_launch(const double* A, int64_t lda, int n, int64_t ldq
   const int nb = lanczos_blocks(n);
   double* h1 = h;
   double* h2 = h + kMaxLanczos;
+  count_launch();
   lanczos_gemv_kernel<<<nb, kLzThreads, 0, st>>>(A, lda, n, ldq, j, Qcols, w, h1, partials,
                                                  counter, state);
+  count_launch();
   lanczos_orth_kernel<<<nb, kLzThreads, 0, st>>>(n, ldq, j, Qcols, w, h1, h2, partials, counter,
                                                  state, 1);
+  count_launch();
   lanczos_orth_kernel<<<nb, kLzThreads, 0, st>>>(n, ldq, j, Qcols, w, h2, nullptr, partials,
                                                  counter, state, 2);
+  count_launch();
   lanczos_next_kernel<<<std::max(1, std::min(148, (n + 255) / 256)), 256, 0, st>>>(n, ldq, j,
                                                                                   Qcols, w, state);
   return cudaGetLastError();
@@ -854,9 +874,11 @@ __global__ void lanczos_extremes_kernel(const double* theta, const double* S, co
 cudaError_t lanczos_finish_launch(int m, double* T, double* theta, double* S, double* lo_hi,
                                   DevState* state, cudaStream_t st) {
   int* m_dev = reinterpret_cast<int*>(&state->scratch[0]);
+  count_launch();
   lanczos_T_kernel<<<1, 256, 0, st>>>(m, T, state, m_dev);
   cudaError_t e = jacobi_launch(T, m, m_dev, theta, S, state, 1e-15, 40, st);
   if (e != cudaSuccess) return e;
+  count_launch();
   lanczos_extremes_kernel<<<1, 1, 0, st>>>(theta, S, m_dev, lo_hi, state);
   return cudaGetLastError();
 }
@@ -872,6 +894,7 @@ __global__ void perturb_kernel(double* A, int64_t lda, const double* E, int64_t 
 cudaError_t perturb_launch(double* A, int64_t lda, const double* E, int64_t lde, int rows,
                            int cols, cudaStream_t st) {
   dim3 grid((cols + 255) / 256, rows);
+  count_launch();
   perturb_kernel<<<grid, 256, 0, st>>>(A, lda, E, lde, rows, cols);
   return cudaGetLastError();
 }

@@ -34,7 +34,9 @@ class Solver:
         self.ctx = Context(n, p, d)
         self.psd = cfg.mode in ("sweep_psd", "pfam")
         self.op = PF_OP_PSD if self.psd else PF_OP_SOFT_THRESHOLD
-        self.U = _dev(initial_block(cfg))
+        # problem["_dev"]: inputs already on the device (the e2e path uploads them itself)
+        devp = (problem or {}).get("_dev") or {}
+        self.U = devp["U0"] if "U0" in devp else _dev(initial_block(cfg))
         self.V = torch.empty((n, p), dtype=torch.float64, device="cuda")
         self.theta = torch.empty(p, dtype=torch.float64, device="cuda")
         self.f = torch.zeros(p, dtype=torch.float64, device="cuda")
@@ -60,10 +62,13 @@ class Solver:
             self.ctx.prox_step(self.V.zero_(), self.f, cfg.tau, self.omega, self.W, self.A,
                                self.obj, stream)
         elif cfg.mode == "pfam":
-            prob = pfam_problem(cfg) if problem is None else problem
-            self.prob = prob
-            self.adj = _bits(prob["adj_bits"])
-            self.deg = _dev(prob["deg"])
+            if "adj_bits" in devp:
+                self.adj, self.deg = devp["adj_bits"], devp["deg"]
+            else:
+                prob = pfam_problem(cfg) if problem is None else problem
+                self.prob = prob
+                self.adj = _bits(prob["adj_bits"])
+                self.deg = _dev(prob["deg"])
             self.A = torch.zeros((n, n), dtype=torch.float64, device="cuda")
             # Z_0 = 0 -> Z_1 = prox_tG(0) = offdiag(-tC) + I  (reading R9)
             self.ctx.admm_step(self.V.zero_(), self.f, cfg.t, self.adj, self.deg, self.A,

@@ -140,8 +140,8 @@ def sym_bernoulli_bitmask(n: int, prob: float, rng: np.random.Generator,
 
 
 def unpack_bitmask(bits: np.ndarray, n: int) -> np.ndarray:
-    """Inverse of the packing above: bool [n, n]."""
-    b8 = np.ascontiguousarray(bits).view(np.uint8).reshape(n, -1)
+    """Inverse of the packing above: bool [rows, n] (rows = bits.shape[0])."""
+    b8 = np.ascontiguousarray(bits).view(np.uint8).reshape(bits.shape[0], -1)
     return np.unpackbits(b8, axis=1, bitorder="little")[:, :n].astype(bool)
 
 

@@ -8,7 +8,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _declared():
     src = open(os.path.join(ROOT, "include", "pf.h")).read()
-    return sorted(set(re.findall(r"^(?:pf_status|const char\*|int64_t)\s+(pf_\w+)\(", src, re.M)))
+    return sorted(set(re.findall(r"^(?:pf_status|const char\*|int64_t|long long)\s+(pf_\w+)\(", src, re.M)))
 
 
 def test_header_declares_the_north_star_calls():
@@ -45,5 +45,5 @@ def test_product_does_not_import_oracle():
     subprocess.check_call([sys.executable, "-c", code])
     for f in os.listdir(os.path.join(ROOT, "paper_1904_10585_b200")):
         if f.endswith(".py"):
-            assert "oracle" not in open(os.path.join(ROOT, "paper_1904_10585_b200", f)).read().replace(
-                "no CPU fallback", "").split("import")[0] or True
+            src = open(os.path.join(ROOT, "paper_1904_10585_b200", f)).read()
+            assert "import oracle" not in src and "from oracle" not in src, f
