@@ -135,7 +135,9 @@ pf_status pf_prox_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f
  * with the prox sign corrected, reading R1): W = V diag(f) V^T,
  * Z <- prox_tG(2W - Z) - W + Z = offdiag(W - tC) + Diag(1 - W_ii + Z_ii), in place.
  * adj: packed adjacency bitmask (as omega above, local rows, no self loops); deg: device
- * double[n] FULL degree vector.  obj: device double[2] = {<C, W>, ||Z_new - Z_old||_F}. */
+ * double[n] FULL degree vector.  obj: device double[2] = {<C, W>, ||Z_new - Z_old||_F}.
+ * Z must be symmetric (it is the DRS iterate on S^n): with world = 1 only its upper triangle
+ * is read and the lower triangle is written as the exact mirror of the upper one. */
 pf_status pf_admm_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f, double t,
                        const uint32_t* adj, int64_t ldadj, const double* deg, double* Z,
                        int64_t ldz, double* obj, pf_stream stream);

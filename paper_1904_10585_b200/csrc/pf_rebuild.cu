@@ -5,79 +5,161 @@
 //                                W = V diag(f) V^T,
 //                                Z+ = offdiag(W - tC) + Diag(1 - W_ii + Z_ii),  C = -L/4,
 //                                obj = {<C, W>, ||Z+ - Z||_F}
-// The low-rank products run on fp64 DMMA with the f scaling folded into the smem load; the
-// masks (Omega / adjacency) are read as packed bits, so C and Omega cost n^2/8 bytes.
-// Reductions are deterministic: per-CTA partials, summed in CTA order by the last CTA.
+// B200 design (DESIGN.md §4 K7):
+//  * 64 x 64 output tiles on fp64 DMMA (K = p), f folded into the A-fragment loads;
+//  * single GPU (whole rows): only tiles I <= J are computed; the (J, I) tile is written as the
+//    transpose through shared memory -> n^2 p flops instead of 2 n^2 p, and the old iterate is
+//    read only on the upper half (PFAM; Z is symmetric by contract), none at all for PFPG;
+//  * V panels staged with cp.async, the old-iterate tile prefetched into registers before the
+//    MMA loop so its HBM latency overlaps the math; masks (Omega / adjacency) are packed bits.
+//  * reductions are deterministic: per-CTA partials summed in CTA order by the last CTA.
 #include <algorithm>
+#include <cmath>
 
 #include "pf_kernels.cuh"
 
 namespace pf {
 
-constexpr int kRbTile = 64;  // 64 x 64 output tile, 4 warps (2 x 2), warp tile 32 x 32
+constexpr int kRb = 64;  // tile edge; 4 warps (2 x 2), warp tile 32 x 32
+
+struct RbArgs {
+  const double* V;
+  int64_t ldv;
+  const double* f;
+  double tt;  // tau (PFPG) or t (PFAM)
+  const uint32_t* bits;
+  int64_t ldb;
+  const double* W;
+  int64_t ldw;
+  int r, rpad;
+  const double* deg;
+  double* Out;
+  int64_t ldo;
+  int n_rows, n, row0;
+  int sym, T;
+  double* partials;
+  int* counter;
+  double* obj;
+};
 
 template <int P, bool PFPG>
 struct RbCfg {
   static constexpr int LD = P + 4;
-  static constexpr int SMEM_V = 2 * kRbTile * LD * 8;
+  static constexpr int LDS = kRb + 1;  // transpose staging row pitch
 };
 
-__device__ __forceinline__ bool mask_bit(const uint32_t* bits, int64_t ld, int i, int j) {
-  return (__ldg(bits + (size_t)i * ld + (j >> 5)) >> (j & 31)) & 1u;
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+// decode pair index e (0 <= e < T(T+1)/2) into (I, J), I <= J, row-major over the upper triangle
+__device__ __forceinline__ void pair_of(int e, int T, int& I, int& J) {
+  // number of pairs before row I: I*T - I*(I-1)/2
+  double b = 2.0 * T + 1.0;
+  int i = (int)floor((b - sqrt(b * b - 8.0 * e)) * 0.5);
+  if (i < 0) i = 0;
+  while (i > 0 && (long long)i * T - (long long)i * (i - 1) / 2 > e) --i;
+  while ((long long)(i + 1) * T - (long long)(i + 1) * i / 2 <= e) ++i;
+  I = i;
+  J = i + (e - (int)((long long)i * T - (long long)i * (i - 1) / 2));
 }
 
 template <int P, bool PFPG>
-__global__ void __launch_bounds__(128) rebuild_kernel(
-    const double* __restrict__ V, int64_t ldv, const double* __restrict__ f, double tau_or_t,
-    const uint32_t* __restrict__ bits, int64_t ldb, const double* __restrict__ W, int64_t ldw,
-    int r, int ldw_s, const double* __restrict__ deg, double* Out, int64_t ldo, int n_rows, int n,
-    int row0, double* __restrict__ partials, int* counter, double* __restrict__ obj) {
+__global__ void __launch_bounds__(128) rebuild_kernel(const RbArgs a) {
   using C = RbCfg<P, PFPG>;
   extern __shared__ __align__(16) double sm[];
   __shared__ double red[32];
+  __shared__ double fs[P];
   __shared__ int s_last;
-  double* VFi = sm;                       // 64 x LD   f-scaled rows I (local rows -> global row0+i)
-  double* Vj = sm + kRbTile * C::LD;      // 64 x LD   rows J
-  double* Wi = Vj + kRbTile * C::LD;      // 64 x ldw_s (PFPG)
-  double* Wj = Wi + kRbTile * ldw_s;
+  const int ldw_s = a.rpad + 4;
+  double* Vi = sm;                  // 64 x LD  rows I (local row block)
+  double* Vj = sm + kRb * C::LD;    // 64 x LD  rows J
+  double* Wi = Vj + kRb * C::LD;    // 64 x ldw_s (PFPG)
+  double* Wj = Wi + kRb * ldw_s;
+  double* Ts = sm;                  // 64 x 65 transpose staging (reuses the panels)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g8 = lane >> 2, t4 = lane & 3;
-  const int i0 = blockIdx.y * kRbTile;  // local row tile
-  const int j0 = blockIdx.x * kRbTile;  // global column tile
-
-  for (int e = tid; e < kRbTile * P; e += 128) {
-    const int rr = e / P, c = e % P;
-    const int gi = row0 + i0 + rr, gj = j0 + rr;
-    VFi[rr * C::LD + c] = (i0 + rr < n_rows) ? V[(size_t)gi * ldv + c] * f[c] : 0.0;
-    Vj[rr * C::LD + c] = (gj < n) ? V[(size_t)gj * ldv + c] : 0.0;
+  int I, J;
+  if (a.sym) {
+    pair_of(blockIdx.x, a.T, I, J);
+  } else {
+    I = blockIdx.y;
+    J = blockIdx.x;
   }
+  const int i0 = I * kRb, j0 = J * kRb;  // local row tile start, global column tile start
+  const bool mirror = a.sym && I < J;
+  const double wgt = mirror ? 2.0 : 1.0;
+
+  // ---- stage V panels (cp.async 16 B), f, W panels
+  for (int e = tid; e < kRb * (P / 2); e += 128) {
+    const int rr = e / (P / 2), c = (e % (P / 2)) * 2;
+    double* di = Vi + rr * C::LD + c;
+    double* dj = Vj + rr * C::LD + c;
+    if (i0 + rr < a.n_rows) cp_async16(di, a.V + (size_t)(a.row0 + i0 + rr) * a.ldv + c);
+    else *reinterpret_cast<double2*>(di) = make_double2(0.0, 0.0);
+    if (j0 + rr < a.n) cp_async16(dj, a.V + (size_t)(j0 + rr) * a.ldv + c);
+    else *reinterpret_cast<double2*>(dj) = make_double2(0.0, 0.0);
+  }
+  for (int c = tid; c < P; c += 128) fs[c] = a.f[c];
   if (PFPG) {
-    for (int e = tid; e < kRbTile * ldw_s; e += 128) {
+    for (int e = tid; e < kRb * ldw_s; e += 128) {
       const int rr = e / ldw_s, c = e % ldw_s;
-      const int gi = row0 + i0 + rr, gj = j0 + rr;
-      Wi[e] = (c < r && i0 + rr < n_rows) ? W[(size_t)gi * ldw + c] : 0.0;
-      Wj[e] = (c < r && gj < n) ? W[(size_t)gj * ldw + c] : 0.0;
+      Wi[e] = (c < a.r && i0 + rr < a.n_rows) ? a.W[(size_t)(a.row0 + i0 + rr) * a.ldw + c] : 0.0;
+      Wj[e] = (c < a.r && j0 + rr < a.n) ? a.W[(size_t)(j0 + rr) * a.ldw + c] : 0.0;
     }
   }
-  __syncthreads();
 
   const int wm = warp & 1, wn = warp >> 1;
+  // ---- PFAM: prefetch the old iterate at this thread's fragment positions (overlaps the MMA)
+  double zo[2][2][4][2];
+  if (!PFPG) {
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int li = i0 + wm * 32 + mt * 16 + g8 + 8 * h;
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          const int j = j0 + wn * 32 + nt * 8 + 2 * t4;
+          zo[mt][h][nt][0] = zo[mt][h][nt][1] = 0.0;
+          if (li < a.n_rows && j < a.n) {
+            const double* zp = a.Out + (size_t)li * a.ldo + j;
+            if (j + 1 < a.n && ((reinterpret_cast<uintptr_t>(zp) & 15) == 0)) {
+              const double2 z2 = __ldcs(reinterpret_cast<const double2*>(zp));
+              zo[mt][h][nt][0] = z2.x;
+              zo[mt][h][nt][1] = z2.y;
+            } else {
+              zo[mt][h][nt][0] = zp[0];
+              if (j + 1 < a.n) zo[mt][h][nt][1] = zp[1];
+            }
+          }
+        }
+      }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+
+  // ---- X tile = (V_I diag(f)) V_J^T on DMMA
   double acc[2][4][4];
-  double accm[PFPG ? 2 : 1][PFPG ? 4 : 1][4];
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
+  for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-    for (int b = 0; b < 4; ++b)
+    for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
-      for (int k = 0; k < 4; ++k) acc[a][b][k] = 0.0;
-#pragma unroll 2
+      for (int k = 0; k < 4; ++k) acc[mt][nt][k] = 0.0;
+#pragma unroll 4
   for (int ks = 0; ks < P / 4; ++ks) {
     const int k = ks * 4 + t4;
+    const double fk = fs[k];
     double a0[2], a1[2], b0[4];
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
-      a0[mt] = VFi[(wm * 32 + mt * 16 + g8) * C::LD + k];
-      a1[mt] = VFi[(wm * 32 + mt * 16 + g8 + 8) * C::LD + k];
+      a0[mt] = Vi[(wm * 32 + mt * 16 + g8) * C::LD + k] * fk;
+      a1[mt] = Vi[(wm * 32 + mt * 16 + g8 + 8) * C::LD + k] * fk;
     }
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) b0[nt] = Vj[(wn * 32 + nt * 8 + g8) * C::LD + k];
@@ -86,14 +168,15 @@ __global__ void __launch_bounds__(128) rebuild_kernel(
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt) dmma16884(acc[mt][nt], a0[mt], a1[mt], b0[nt]);
   }
+  double accm[PFPG ? 2 : 1][PFPG ? 4 : 1][4];
   if (PFPG) {
 #pragma unroll
-    for (int a = 0; a < (PFPG ? 2 : 1); ++a)
+    for (int mt = 0; mt < (PFPG ? 2 : 1); ++mt)
 #pragma unroll
-      for (int b = 0; b < (PFPG ? 4 : 1); ++b)
+      for (int nt = 0; nt < (PFPG ? 4 : 1); ++nt)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) accm[a][b][k] = 0.0;
-    for (int ks = 0; ks < (ldw_s - 4) / 4; ++ks) {
+        for (int k = 0; k < 4; ++k) accm[mt][nt][k] = 0.0;
+    for (int ks = 0; ks < a.rpad / 4; ++ks) {
       const int k = ks * 4 + t4;
       double a0[2], a1[2], b0[4];
 #pragma unroll
@@ -110,158 +193,178 @@ __global__ void __launch_bounds__(128) rebuild_kernel(
           dmma16884(accm[mt][nt], a0[mt], a1[mt], b0[nt]);
     }
   }
+  if (mirror) __syncthreads();  // panels are about to be overwritten by the staging tile
 
-  // ------------------------------------------------------------------ elementwise update
+  // ---- elementwise update + reductions
   double s0 = 0.0, s1 = 0.0;
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int li = i0 + wm * 32 + mt * 16 + g8 + 8 * h;  // local row
-      if (li >= n_rows) continue;
-      const int gi = row0 + li;
+      const int rt = wm * 32 + mt * 16 + g8 + 8 * h;  // row within tile
+      const int li = i0 + rt;
+      if (li >= a.n_rows) continue;
+      const int gi = a.row0 + li;
+      const uint32_t word = __ldg(a.bits + (size_t)li * a.ldb + ((j0 + wn * 32) >> 5));
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt) {
-        const int j = j0 + wn * 32 + nt * 8 + 2 * t4;
-        if (j >= n) continue;
-        const bool two = (j + 1 < n);
-        double* op = Out + (size_t)li * ldo + j;
+        const int ct = wn * 32 + nt * 8 + 2 * t4;  // column within tile
+        const int j = j0 + ct;
+        if (j >= a.n) continue;
+        const bool two = (j + 1 < a.n);
         double o[2];
-        if (PFPG) {
 #pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            const double x = acc[mt][nt][2 * h + c];
+        for (int c = 0; c < 2; ++c) {
+          const int jj = j + c;
+          const bool bit = (c == 0 || two) ? ((word >> (jj & 31)) & 1u) : false;
+          const double x = acc[mt][nt][2 * h + c];
+          if (PFPG) {
             const double m = accm[PFPG ? mt : 0][PFPG ? nt : 0][2 * h + c];
-            const bool om = (c == 0 || two) ? mask_bit(bits, ldb, li, j + c) : false;
             const double dxm = x - m;
-            o[c] = om ? x - tau_or_t * dxm : x;
-            if (om) s0 += dxm * dxm;
-          }
-        } else {
-          double zold[2];
-          if (two && ((reinterpret_cast<uintptr_t>(op) & 15) == 0)) {
-            const double2 z2 = *reinterpret_cast<const double2*>(op);
-            zold[0] = z2.x;
-            zold[1] = z2.y;
+            o[c] = bit ? x - a.tt * dxm : x;
+            if (bit) s0 += wgt * dxm * dxm;
           } else {
-            zold[0] = op[0];
-            zold[1] = two ? op[1] : 0.0;
-          }
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            if (c == 1 && !two) break;
-            const int jj = j + c;
-            const double w = acc[mt][nt][2 * h + c];
+            const double zold = zo[mt][h][nt][c];
             double znew;
             if (jj == gi) {
-              znew = 1.0 - w + zold[c];            // Diag(1 - W_ii + Z_ii)
-              s0 += -0.25 * deg[gi] * w;           // C_ii = -deg_i / 4
+              znew = 1.0 - x + zold;               // Diag(1 - W_ii + Z_ii)
+              s0 += -0.25 * a.deg[gi] * x;         // C_ii = -deg_i / 4
             } else {
-              const bool a = mask_bit(bits, ldb, li, jj);
-              znew = a ? w - 0.25 * tau_or_t : w;  // W_ij - t C_ij, C_ij = adj_ij / 4
-              if (a) s0 += 0.25 * w;
+              znew = bit ? x - 0.25 * a.tt : x;    // W_ij - t C_ij, C_ij = adj_ij / 4
+              if (bit) s0 += wgt * 0.25 * x;
             }
-            const double dz = znew - zold[c];
-            s1 += dz * dz;
+            if (c == 0 || two) {
+              const double dz = znew - zold;
+              s1 += wgt * dz * dz;
+            }
             o[c] = znew;
           }
         }
+        double* op = a.Out + (size_t)li * a.ldo + j;
         if (two && ((reinterpret_cast<uintptr_t>(op) & 15) == 0)) {
-          *reinterpret_cast<double2*>(op) = make_double2(o[0], o[1]);
+          __stcs(reinterpret_cast<double2*>(op), make_double2(o[0], o[1]));
         } else {
           op[0] = o[0];
           if (two) op[1] = o[1];
         }
+        if (mirror) {
+          Ts[rt * C::LDS + ct] = o[0];
+          Ts[rt * C::LDS + ct + 1] = o[1];
+        }
       }
     }
+  if (mirror) {
+    __syncthreads();
+    // (J, I) tile = transpose: row b of the mirrored tile = column b of Ts
+    for (int e = tid; e < kRb * (kRb / 2); e += 128) {
+      const int b = e / (kRb / 2), a2 = (e % (kRb / 2)) * 2;
+      const int row = j0 + b, col = i0 + a2;
+      if (row < a.n && col < a.n) {
+        double* op = a.Out + (size_t)row * a.ldo + col;
+        const double v0 = Ts[a2 * C::LDS + b], v1 = Ts[(a2 + 1) * C::LDS + b];
+        if (col + 1 < a.n && ((reinterpret_cast<uintptr_t>(op) & 15) == 0)) {
+          __stcs(reinterpret_cast<double2*>(op), make_double2(v0, v1));
+        } else {
+          op[0] = v0;
+          if (col + 1 < a.n) op[1] = v1;
+        }
+      }
+    }
+  }
+
+  // ---- deterministic reduction: block tree, then the last CTA sums CTA partials in order
   s0 = block_sum(s0, red);
   s1 = block_sum(s1, red);
   const int bid = blockIdx.y * gridDim.x + blockIdx.x;
   const int nb = gridDim.x * gridDim.y;
   if (tid == 0) {
-    partials[2 * (size_t)bid] = s0;
-    partials[2 * (size_t)bid + 1] = s1;
+    a.partials[2 * (size_t)bid] = s0;
+    a.partials[2 * (size_t)bid + 1] = s1;
   }
   __threadfence();
   __syncthreads();
-  if (tid == 0) s_last = (atomicAdd(counter, 1) == nb - 1);
+  if (tid == 0) s_last = (atomicAdd(a.counter, 1) == nb - 1);
   __syncthreads();
   if (s_last) {
     __threadfence();
     double t0 = 0.0, t1 = 0.0;
-    // fixed assignment of blocks to threads + fixed tree -> deterministic
     for (int b = tid; b < nb; b += 128) {
-      t0 += __ldcg(partials + 2 * (size_t)b);
-      t1 += __ldcg(partials + 2 * (size_t)b + 1);
+      t0 += __ldcg(a.partials + 2 * (size_t)b);
+      t1 += __ldcg(a.partials + 2 * (size_t)b + 1);
     }
     t0 = block_sum(t0, red);
     t1 = block_sum(t1, red);
     if (tid == 0) {
       if (PFPG) {
         double sf = 0.0;
-        for (int c = 0; c < P; ++c) sf += fabs(f[c]);
-        obj[0] = 0.5 * t0;
-        obj[1] = sf;
+        for (int c = 0; c < P; ++c) sf += fabs(a.f[c]);
+        a.obj[0] = 0.5 * t0;
+        a.obj[1] = sf;
       } else {
-        obj[0] = t0;
-        obj[1] = sqrt(t1);
+        a.obj[0] = t0;
+        a.obj[1] = sqrt(t1);
       }
-      *counter = 0;
+      *a.counter = 0;
     }
   }
 }
 
 int rebuild_blocks(int n_rows, int n) {
-  return ((n + kRbTile - 1) / kRbTile) * ((n_rows + kRbTile - 1) / kRbTile);
+  return ((n + kRb - 1) / kRb) * ((n_rows + kRb - 1) / kRb);
 }
 
 template <int P, bool PFPG>
-static cudaError_t rb_launch(const double* V, int64_t ldv, const double* f, double tt,
-                             const uint32_t* bits, int64_t ldb, const double* W, int64_t ldw,
-                             int r, const double* deg, double* Out, int64_t ldo, int n_rows,
-                             int n, int row0, double* obj, double* partials, int* counter,
-                             cudaStream_t st) {
+static cudaError_t rb_launch(RbArgs a, cudaStream_t st) {
   using C = RbCfg<P, PFPG>;
-  const int rpad = PFPG ? ((r + 3) / 4) * 4 : 0;
-  const int ldw_s = PFPG ? (rpad + 4) : 0;
-  const size_t smem = C::SMEM_V + (PFPG ? (size_t)2 * kRbTile * ldw_s * 8 : 0);
+  a.rpad = PFPG ? ((a.r + 3) / 4) * 4 : 0;
+  const int ldw_s = a.rpad + 4;
+  const size_t panels = (size_t)2 * kRb * C::LD * 8 + (PFPG ? (size_t)2 * kRb * ldw_s * 8 : 0);
+  const size_t stage = (size_t)kRb * C::LDS * 8;
+  const size_t smem = std::max(panels, stage);
   static bool attr = false;
   if (!attr) {
-    const int mx = C::SMEM_V + (PFPG ? 2 * kRbTile * (64 + 4) * 8 : 0);
-    cudaFuncSetAttribute(rebuild_kernel<P, PFPG>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    const size_t mx =
+        std::max((size_t)2 * kRb * C::LD * 8 + (PFPG ? (size_t)2 * kRb * 68 * 8 : 0), stage);
+    cudaFuncSetAttribute(rebuild_kernel<P, PFPG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)mx);
     attr = true;
   }
-  dim3 grid((n + kRbTile - 1) / kRbTile, (n_rows + kRbTile - 1) / kRbTile);
+  const int tr = (a.n_rows + kRb - 1) / kRb, tc = (a.n + kRb - 1) / kRb;
+  a.sym = (a.row0 == 0 && a.n_rows == a.n) ? 1 : 0;
+  a.T = tc;
+  dim3 grid = a.sym ? dim3((unsigned)((long long)tc * (tc + 1) / 2), 1) : dim3(tc, tr);
   count_launch();
-  rebuild_kernel<P, PFPG><<<grid, 128, smem, st>>>(V, ldv, f, tt, bits, ldb, W, ldw, r, ldw_s, deg,
-                                                   Out, ldo, n_rows, n, row0, partials, counter,
-                                                   obj);
+  rebuild_kernel<P, PFPG><<<grid, 128, smem, st>>>(a);
   return cudaGetLastError();
 }
 
-#define PF_RB_DISPATCH(PFPG_, ...)                                        \
-  switch (p) {                                                            \
-    case 16: return rb_launch<16, PFPG_>(__VA_ARGS__);                    \
-    case 32: return rb_launch<32, PFPG_>(__VA_ARGS__);                    \
-    case 64: return rb_launch<64, PFPG_>(__VA_ARGS__);                    \
-    case 128: return rb_launch<128, PFPG_>(__VA_ARGS__);                  \
-    default: return cudaErrorInvalidValue;                                \
+template <bool PFPG>
+static cudaError_t rb_dispatch(int p, const RbArgs& a, cudaStream_t st) {
+  switch (p) {
+    case 16: return rb_launch<16, PFPG>(a, st);
+    case 32: return rb_launch<32, PFPG>(a, st);
+    case 64: return rb_launch<64, PFPG>(a, st);
+    case 128: return rb_launch<128, PFPG>(a, st);
+    default: return cudaErrorInvalidValue;
   }
+}
 
 cudaError_t prox_launch(const double* V, int64_t ldv, const double* f, double tau,
                         const uint32_t* omega, int64_t ldo, const double* W, int64_t ldw, int r,
                         double* Aout, int64_t lda, int n_rows, int n, int row0, int p,
                         double* obj, double* partials, int* counter, cudaStream_t st) {
-  PF_RB_DISPATCH(true, V, ldv, f, tau, omega, ldo, W, ldw, r, nullptr, Aout, lda, n_rows, n, row0,
-                 obj, partials, counter, st)
+  RbArgs a{V, ldv, f, tau, omega, ldo, W, ldw, r, 0, nullptr, Aout, lda, n_rows, n, row0,
+           0, 0, partials, counter, obj};
+  return rb_dispatch<true>(p, a, st);
 }
 
 cudaError_t admm_launch(const double* V, int64_t ldv, const double* f, double t,
                         const uint32_t* adj, int64_t ldadj, const double* deg, double* Z,
                         int64_t ldz, int n_rows, int n, int row0, int p, double* obj,
                         double* partials, int* counter, cudaStream_t st) {
-  PF_RB_DISPATCH(false, V, ldv, f, t, adj, ldadj, nullptr, 0, 0, deg, Z, ldz, n_rows, n, row0,
-                 obj, partials, counter, st)
+  RbArgs a{V, ldv, f, t, adj, ldadj, nullptr, 0, 0, 0, deg, Z, ldz, n_rows, n, row0,
+           0, 0, partials, counter, obj};
+  return rb_dispatch<false>(p, a, st);
 }
 
 }  // namespace pf
