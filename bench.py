@@ -246,7 +246,7 @@ def run_e2e(cfg, args, stream) -> dict:
             s.step()
             obj_host[k].copy_(s.obj, non_blocking=True)
             d2h += 16
-        Vh = s.V.to("cpu", non_blocking=True)
+        Vh = s.ritz.to("cpu", non_blocking=True)
         fh = s.f.to("cpu", non_blocking=True)
         d2h += Vh.numel() * 8 + fh.numel() * 8
         e1.record(stream)

@@ -147,8 +147,6 @@ __global__ void __launch_bounds__(512) chol_inv_kernel(const double* __restrict_
                                                      const int* cond) {
   if (cond && *cond == 0) return;
   extern __shared__ double M[];
-  __shared__ double sdiag;
-  __shared__ int sfail;
   __shared__ double red[32];
   const int P1 = p + 1;
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -165,73 +163,65 @@ __global__ void __launch_bounds__(512) chol_inv_kernel(const double* __restrict_
   tr = block_sum(tr, red);
   if (bad && tid == 0) atomicOr(&state->flags, PF_FLAG_NONFINITE);
 
+  // 2-D thread layout for the triangular updates (no integer division in the inner loops)
+  const int tx = tid & 31, ty = tid >> 5, nty = nt >> 5;
+  double* gdiag = M + p * P1;  // p doubles after M
+  for (int i = tid; i < p; i += nt) gdiag[i] = G[i * p + i];
+
   double shift = 0.0;
   int attempt = 0;
   for (;;) {
-    for (int e = tid; e < p * p; e += nt) {
-      const int i = e / p, j = e % p;
-      if (j <= i) M[i * P1 + j] = G[e] + ((i == j) ? shift : 0.0);
-    }
-    if (tid == 0) sfail = 0;
+    for (int i = ty; i < p; i += nty)
+      for (int j = tx; j <= i; j += 32) M[i * P1 + j] = G[i * p + j] + ((i == j) ? shift : 0.0);
     __syncthreads();
+    // right-looking Cholesky, one barrier per column: the trailing update uses the unscaled
+    // column j divided by the pivot, and column j is scaled afterwards (disjoint elements)
+    bool fail = false;
     for (int j = 0; j < p; ++j) {
-      if (tid == 0) {
-        const double d = M[j * P1 + j];
-        const double g = G[j * p + j];
-        if (!(d > 1e-12 * g) || !(d > 0.0)) {
-          sfail = 1;
-          sdiag = 1.0;
-        } else {
-          sdiag = sqrt(d);
-        }
-        M[j * P1 + j] = sdiag;
+      const double d = M[j * P1 + j];
+      if (!(d > 1e-12 * gdiag[j]) || !(d > 0.0)) {  // uniform: every thread reads the same d
+        fail = true;
+        break;
+      }
+      const double inv_d = 1.0 / d;
+      for (int i = j + 1 + ty; i < p; i += nty) {
+        const double lij = M[i * P1 + j] * inv_d;
+        for (int k = j + 1 + tx; k <= i; k += 32) M[i * P1 + k] -= lij * M[k * P1 + j];
       }
       __syncthreads();
-      if (sfail) break;
-      const double dj = sdiag;
-      for (int i = j + 1 + tid; i < p; i += nt) M[i * P1 + j] /= dj;
-      __syncthreads();
-      // trailing update of the lower triangle: rows i > j, cols k in (j, i]
-      const int m = p - j - 1;
-      for (int e = tid; e < m * m; e += nt) {
-        const int ii = e / m, kk = e % m;
-        if (kk <= ii) {
-          const int i = j + 1 + ii, k = j + 1 + kk;
-          M[i * P1 + k] -= M[i * P1 + j] * M[k * P1 + j];
-        }
-      }
-      __syncthreads();
+      const double sd = sqrt(d);
+      for (int i = j + 1 + tid; i < p; i += nt) M[i * P1 + j] = M[i * P1 + j] / sd;
+      if (tid == 0) M[j * P1 + j] = sd;
     }
-    if (!sfail) break;
+    __syncthreads();
+    if (!fail) break;
     if (attempt == 1) {
       if (tid == 0) atomicOr(&state->flags, PF_FLAG_NONFINITE);
       break;
     }
     attempt = 1;
     shift = shift_scale * (tr > 0.0 ? tr : 1.0);
-    __syncthreads();
   }
   if (tid == 0) {
     if (attempt) atomicOr(&state->flags, PF_FLAG_CHOL_SHIFT);
     if (shift_flag_out && attempt) *shift_flag_out = 1;
   }
-  // X = L^{-1}, right-looking: X = I; for j: X[j][:] /= L[j][j]; X[i][:] -= L[i][j] X[j][:]
-  for (int e = tid; e < p * p; e += nt) {
-    const int i = e / p, c = e % p;
-    if (i >= c) M[c * P1 + i + 1] = (i == c) ? 1.0 : 0.0;
-  }
+  // X = L^{-1}, right-looking with one barrier per column: X[i][c] -= L[i][j] X[j][c] / L[j][j]
+  // for i > j, c <= j (row j unscaled), then row j is scaled by 1/L[j][j] (disjoint elements).
+  for (int i = ty; i < p; i += nty)
+    for (int c = tx; c <= i; c += 32) M[c * P1 + i + 1] = (i == c) ? 1.0 : 0.0;
   __syncthreads();
   for (int j = 0; j < p; ++j) {
     const double ljj = M[j * P1 + j];
-    for (int c = tid; c <= j; c += nt) M[c * P1 + j + 1] /= ljj;
-    __syncthreads();
-    const int m = p - j - 1;
-    for (int e = tid; e < m * (j + 1); e += nt) {
-      const int i = j + 1 + e / (j + 1), c = e % (j + 1);
-      M[c * P1 + i + 1] -= M[i * P1 + j] * M[c * P1 + j + 1];
+    const double inv = 1.0 / ljj;
+    for (int i = j + 1 + ty; i < p; i += nty) {
+      const double lij = M[i * P1 + j] * inv;
+      for (int c = tx; c <= j; c += 32) M[c * P1 + i + 1] -= lij * M[c * P1 + j + 1];
     }
     __syncthreads();
+    for (int c = tid; c <= j; c += nt) M[c * P1 + j + 1] = M[c * P1 + j + 1] / ljj;
   }
+  __syncthreads();
   // Rinv = L^{-T}: Rinv[c][i] = X[i][c] (upper triangular)
   for (int e = tid; e < p * p; e += nt) {
     const int c = e / p, i = e % p;
@@ -244,11 +234,11 @@ cudaError_t chol_inv_launch(const double* G, int p, int64_t n_global, double* Ri
                             cudaStream_t st) {
   const double u = 1.1102230246251565e-16;
   const double scale = 11.0 * ((double)n_global * p + (double)p * (p + 1)) * u;
-  const size_t smem = (size_t)p * (p + 1) * sizeof(double);
+  const size_t smem = (size_t)p * (p + 2) * sizeof(double);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(128 * 129 * sizeof(double)));
+                         (int)(128 * 130 * sizeof(double)));
     attr = true;
   }
   count_launch();
@@ -375,7 +365,17 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const double* __restrict__
   double* cs = V + Pe * Pe;                         // [half][3] = c, s, t
   int* pi = reinterpret_cast<int*>(cs + 3 * half);  // [half]
   int* pj = pi + half;
+  unsigned short* blk = reinterpret_cast<unsigned short*>(pj + half);  // [nblk] = (a << 8) | b
   const int tid = threadIdx.x, nt = blockDim.x;
+  const int nblk_all = half * (half + 1) / 2;
+  for (int e = tid; e < nblk_all; e += nt) {  // block (a, b), a <= b, enumerated once
+    int a = 0, rem = e;
+    while (rem >= half - a) {
+      rem -= half - a;
+      ++a;
+    }
+    blk[e] = (unsigned short)((a << 8) | (a + rem));
+  }
 
   for (int i = tid; i < Pe; i += nt)
     for (int j = i; j < Pe; ++j) {
@@ -423,8 +423,9 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const double* __restrict__
         if (j < p) {
           const double hij = Hp[pk(i, j, Pe)];
           const double hii = Hp[pk(i, i, Pe)], hjj = Hp[pk(j, j, Pe)];
-          // threshold Jacobi: skip rotations already below rounding of the diagonal pair
-          if (fabs(hij) > 1e-15 * sqrt(fabs(hii * hjj)) + 1e-18 * s_norm) {
+          // threshold Jacobi: skip rotations below the rounding floor of H; the error this
+          // leaves in V diag(f) V^T is <= |h_ij| (a rotation mixes pairs within their gap)
+          if (fabs(hij) > 1e-16 * s_norm) {
             const double tau = (hjj - hii) / (2.0 * hij);
             t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
             c = 1.0 / sqrt(1.0 + t * t);
@@ -438,15 +439,8 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const double* __restrict__
       }
       __syncthreads();
       // 2x2 block updates: blocks (a, b), a <= b, enumerated linearly
-      const int nblk = half * (half + 1) / 2;
-      for (int e = tid; e < nblk; e += nt) {
-        // invert e -> (a, b) with a <= b: row a has (half - a) blocks
-        int a = 0, rem = e;
-        while (rem >= half - a) {
-          rem -= half - a;
-          ++a;
-        }
-        const int b = a + rem;
+      for (int e = tid; e < nblk_all; e += nt) {
+        const int a = blk[e] >> 8, b = blk[e] & 0xff;
         const int ia = pi[a], ja = pj[a];
         const double ca = cs[3 * a], sa = cs[3 * a + 1];
         if (a == b) {
@@ -509,10 +503,12 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const double* __restrict__
 cudaError_t jacobi_launch(const double* H, int p, const int* p_dev, double* theta, double* Y,
                           DevState* state, double tol, int max_sweeps, cudaStream_t st) {
   const int Pe = p + (p & 1), half = Pe / 2;
-  const size_t smem = ((size_t)Pe * (Pe + 1) / 2 + (size_t)Pe * Pe + 3 * half) * 8 + 2 * half * 4;
+  const size_t smem = ((size_t)Pe * (Pe + 1) / 2 + (size_t)Pe * Pe + 3 * half) * 8 +
+                      2 * half * 4 + (size_t)half * (half + 1) / 2 * 2;
   static bool attr = false;
   if (!attr) {
-    const size_t mx = ((size_t)128 * 129 / 2 + 128 * 128 + 3 * 64) * 8 + 2 * 64 * 4;
+    const size_t mx =
+        ((size_t)128 * 129 / 2 + 128 * 128 + 3 * 64) * 8 + 2 * 64 * 4 + (size_t)64 * 65 / 2 * 2;
     cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
     attr = true;
   }
@@ -665,6 +661,14 @@ __device__ bool last_block_done(int* counter, int* s_last) {
   return *s_last != 0;
 }
 
+// deterministic warp reduction of partials[b * kMaxLanczos + i] over b (fixed lane stride + tree)
+__device__ __forceinline__ double warp_reduce_partials(const double* partials, int nb, int i) {
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (int b = lane; b < nb; b += 32) s += __ldcg(partials + (size_t)b * kMaxLanczos + i);
+  return warp_sum(s);
+}
+
 __global__ void lanczos_init_kernel(const double* __restrict__ v0, int n, double* Q,
                                     DevState* state) {
   __shared__ double red[32];
@@ -738,10 +742,9 @@ __global__ void __launch_bounds__(kLzThreads) lanczos_gemv_kernel(
   }
   if (last_block_done(counter, &s_last)) {
     __threadfence();
-    for (int i = threadIdx.x; i <= j; i += blockDim.x) {
-      double s = 0.0;
-      for (int b = 0; b < (int)gridDim.x; ++b) s += __ldcg(partials + (size_t)b * kMaxLanczos + i);
-      h[i] = s;
+    for (int i = warp; i <= j; i += nw) {
+      const double s = warp_reduce_partials(partials, (int)gridDim.x, i);
+      if (lane == 0) h[i] = s;
     }
     if (threadIdx.x == 0) *counter = 0;
   }
@@ -785,24 +788,23 @@ __global__ void __launch_bounds__(kLzThreads) lanczos_orth_kernel(
   if (last_block_done(counter, &s_last)) {
     __threadfence();
     if (phase == 1) {
-      for (int i = threadIdx.x; i <= j; i += blockDim.x) {
-        double s = 0.0;
-        for (int b = 0; b < (int)gridDim.x; ++b)
-          s += __ldcg(partials + (size_t)b * kMaxLanczos + i);
-        h_next[i] = s;
+      for (int i = warp; i <= j; i += nw) {
+        const double s = warp_reduce_partials(partials, (int)gridDim.x, i);
+        if (lane == 0) h_next[i] = s;
       }
-    } else if (threadIdx.x == 0) {
-      double s = 0.0;
-      for (int b = 0; b < (int)gridDim.x; ++b) s += __ldcg(partials + (size_t)b * kMaxLanczos);
+    } else if (warp == 0) {
+      const double s = warp_reduce_partials(partials, (int)gridDim.x, 0);
       const double beta = sqrt(s);
-      double amax = 1.0;
-      for (int i = 0; i <= j; ++i) amax = fmax(amax, fabs(state->lanczos_alpha[i]));
-      if (beta <= 1e-12 * amax) {
-        state->lanczos_beta[j] = 0.0;
-        state->lanczos_steps = j + 1;  // breakdown: stop
-        atomicOr(&state->flags, PF_FLAG_LANCZOS_BREAK);
-      } else {
-        state->lanczos_beta[j] = beta;
+      if (lane == 0) {
+        double amax = 1.0;
+        for (int i = 0; i <= j; ++i) amax = fmax(amax, fabs(state->lanczos_alpha[i]));
+        if (beta <= 1e-12 * amax) {
+          state->lanczos_beta[j] = 0.0;
+          state->lanczos_steps = j + 1;  // breakdown: stop
+          atomicOr(&state->flags, PF_FLAG_LANCZOS_BREAK);
+        } else {
+          state->lanczos_beta[j] = beta;
+        }
       }
     }
     if (threadIdx.x == 0) *counter = 0;

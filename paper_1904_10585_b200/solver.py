@@ -100,6 +100,11 @@ class Solver:
             ctx.prox_step(self.V, self.f, cfg.tau, self.omega, self.W, self.A, self.obj, st)
         elif cfg.mode == "pfam":
             ctx.admm_step(self.V, self.f, cfg.t, self.adj, self.deg, self.A, self.obj, st)
+        # Warm start the next filter from the Ritz vectors: Range(V) = Range(U), so the method
+        # is unchanged (eqn:subspace-update depends on Range(U) only), but the next H = Q^T A Q
+        # is then nearly diagonal and the Jacobi solve converges in one or two sweeps.
+        self.ritz = self.V
+        self.U, self.V = self.V, self.U
         self.k += 1
 
     def perturb(self, E: torch.Tensor):
@@ -125,7 +130,7 @@ def run(cfg: Config, iters: int | None = None, record: bool = True, problem=None
             f = s.f.cpu().numpy()
             keep = f != 0.0
             rec.update(theta=s.theta.cpu().numpy(), rank=int(s.rank.item()),
-                       V=s.V.cpu().numpy()[:, keep], f=f[keep])
+                       V=s.ritz.cpu().numpy()[:, keep], f=f[keep])
             if cfg.mode in ("pfpg", "pfam"):
                 rec["objective"], rec["aux"] = s.objective()
         if cfg.mode in ("sweep_psd", "sweep_soft") and k + 1 < K:
