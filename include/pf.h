@@ -152,6 +152,9 @@ pf_status pf_profile(pf_ctx ctx, int32_t enable);
 pf_status pf_profile_read(pf_ctx ctx, pf_stream stream, double* gemm_ms, int64_t* gemm_launches);
 /* Process-wide number of CUDA kernels launched by this library so far. */
 long long pf_kernel_launches(void);
+/* Synchronises `stream`; diag[0] = Jacobi sweeps of the last Rayleigh-Ritz solve,
+ * diag[1] = Lanczos steps of the last refresh. */
+pf_status pf_diagnostics(pf_ctx ctx, pf_stream stream, double* diag /* [2] */);
 
 /* Workload helper (not the method): A <- A + E (config 1 noise, BASELINE configs[0]). */
 pf_status pf_perturb(pf_ctx ctx, double* A, int64_t lda, const double* E, int64_t lde,

@@ -53,6 +53,7 @@ def load() -> ctypes.CDLL:
         "pf_profile": [P, I32],
         "pf_profile_read": [P, P, ctypes.POINTER(D), ctypes.POINTER(I64)],
         "pf_kernel_launches": [],
+        "pf_diagnostics": [P, P, ctypes.POINTER(D)],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -141,6 +142,11 @@ class Context:
                                                   ctypes.byref(rb), lohi), "pf_get_device_status")
         names = [v for k, v in FLAGS.items() if fl.value & k]
         return {"flags": fl.value, "names": names, "rebases": rb.value, "lanczos": (lohi[0], lohi[1])}
+
+    def diagnostics(self, stream=None) -> dict:
+        d = (ctypes.c_double * 2)()
+        self._check(self.lib.pf_diagnostics(self.h, _stream(stream), d), "pf_diagnostics")
+        return {"jacobi_sweeps": int(d[0]), "lanczos_steps": int(d[1])}
 
     def profile(self, enable: bool):
         self._check(self.lib.pf_profile(self.h, 1 if enable else 0), "pf_profile")

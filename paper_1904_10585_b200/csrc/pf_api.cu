@@ -215,6 +215,16 @@ pf_status pf_create_dist(int64_t n, int32_t p, int32_t degree, pf_dtype dtype,
 
 long long pf_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
+pf_status pf_diagnostics(pf_ctx ctx, pf_stream stream, double* diag) {
+  if (!ctx || !diag) return PF_ERR_ARG;
+  PF_CU(cudaStreamSynchronize((cudaStream_t)stream));
+  DevState h;
+  PF_CU(cudaMemcpy(&h, ctx->state, sizeof(DevState), cudaMemcpyDeviceToHost));
+  diag[0] = h.scratch[1];
+  diag[1] = (double)h.lanczos_steps;
+  return PF_OK;
+}
+
 pf_status pf_profile(pf_ctx ctx, int32_t enable) {
   if (!ctx) return PF_ERR_ARG;
   if (enable && ctx->ev.empty()) {

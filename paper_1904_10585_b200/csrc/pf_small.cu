@@ -183,15 +183,15 @@ __global__ void __launch_bounds__(512) chol_inv_kernel(const double* __restrict_
         fail = true;
         break;
       }
-      const double inv_d = 1.0 / d;
+      const double rsd = rsqrt(d);      // 1 / sqrt(d): one MUFU + refinement, no division
+      const double inv_d = rsd * rsd;
       for (int i = j + 1 + ty; i < p; i += nty) {
         const double lij = M[i * P1 + j] * inv_d;
         for (int k = j + 1 + tx; k <= i; k += 32) M[i * P1 + k] -= lij * M[k * P1 + j];
       }
       __syncthreads();
-      const double sd = sqrt(d);
-      for (int i = j + 1 + tid; i < p; i += nt) M[i * P1 + j] = M[i * P1 + j] / sd;
-      if (tid == 0) M[j * P1 + j] = sd;
+      for (int i = j + 1 + tid; i < p; i += nt) M[i * P1 + j] *= rsd;
+      if (tid == 0) M[j * P1 + j] = d * rsd;
     }
     __syncthreads();
     if (!fail) break;
@@ -210,16 +210,16 @@ __global__ void __launch_bounds__(512) chol_inv_kernel(const double* __restrict_
   // for i > j, c <= j (row j unscaled), then row j is scaled by 1/L[j][j] (disjoint elements).
   for (int i = ty; i < p; i += nty)
     for (int c = tx; c <= i; c += 32) M[c * P1 + i + 1] = (i == c) ? 1.0 : 0.0;
+  for (int i = tid; i < p; i += nt) gdiag[i] = 1.0 / M[i * P1 + i];  // reciprocals of diag(L)
   __syncthreads();
   for (int j = 0; j < p; ++j) {
-    const double ljj = M[j * P1 + j];
-    const double inv = 1.0 / ljj;
+    const double inv = gdiag[j];
     for (int i = j + 1 + ty; i < p; i += nty) {
       const double lij = M[i * P1 + j] * inv;
       for (int c = tx; c <= j; c += 32) M[c * P1 + i + 1] -= lij * M[c * P1 + j + 1];
     }
     __syncthreads();
-    for (int c = tid; c <= j; c += nt) M[c * P1 + j + 1] = M[c * P1 + j + 1] / ljj;
+    for (int c = tid; c <= j; c += nt) M[c * P1 + j + 1] *= inv;
   }
   __syncthreads();
   // Rinv = L^{-T}: Rinv[c][i] = X[i][c] (upper triangular)
@@ -335,101 +335,147 @@ cudaError_t rmul_launch(const double* in, int64_t ldi, const double* R, double* 
 
 // =============================================================================== Jacobi
 // Two-sided cyclic Jacobi with the round-robin (tournament) parallel ordering: in each round the
-// Pe/2 disjoint pairs are rotated simultaneously; every 2x2 block (pair a, pair b) of H is
+// PE/2 disjoint pairs are rotated simultaneously; every 2x2 block (pair a, pair b) of H is
 // updated by exactly one thread as B' = J_a^T B J_b (J = [[c, s], [-s, c]], Golub & Van Loan
-// sym.schur2), so no row/column phasing is needed.  H is kept as a packed upper triangle
-// (Pe(Pe+1)/2 doubles) and V = prod J as a dense Pe x Pe matrix, both in shared memory.
-__device__ __forceinline__ int pk(int i, int j, int Pe) {
-  if (i > j) {
-    const int t = i;
-    i = j;
-    j = t;
+// sym.schur2), so no row/column phasing is needed.  PE (compile time) >= p is the padded even
+// order; indices >= p are inert dummies (identity rotations, zero rows).  H is stored full for
+// PE <= 64 and as a packed upper triangle for PE = 128 (so H + V fit in 227 KB of smem).
+template <int PE>
+struct JacCfg {
+  static constexpr bool PACKED = PE > 64;
+  static constexpr int HALF = PE / 2;
+  static constexpr int NBLK = HALF * (HALF + 1) / 2;
+  static constexpr int HSIZE = PACKED ? PE * (PE + 1) / 2 : PE * PE;
+  static constexpr int THREADS = PE <= 32 ? 256 : 1024;
+  static constexpr size_t SMEM =
+      (size_t)(HSIZE + PE * PE + 6 * HALF) * 8 + 4 * HALF * 4 + NBLK * 2;
+};
+
+template <int PE>
+__device__ __forceinline__ int hix(int i, int j) {
+  if (JacCfg<PE>::PACKED) {
+    if (i > j) {
+      const int t = i;
+      i = j;
+      j = t;
+    }
+    return i * PE - (i * (i - 1)) / 2 + (j - i);
   }
-  return i * Pe - (i * (i - 1)) / 2 + (j - i);
+  return i * PE + j;
 }
 
-__global__ void __launch_bounds__(1024) jacobi_kernel(const double* __restrict__ H, int p_static,
-                                                    const int* p_dev, double* __restrict__ theta,
-                                                    double* __restrict__ Yout, DevState* state,
-                                                    double tol, int max_sweeps) {
+template <int PE>
+__global__ void __launch_bounds__(JacCfg<PE>::THREADS) jacobi_kernel(
+    const double* __restrict__ H, int p_static, const int* p_dev, double* __restrict__ theta,
+    double* __restrict__ Yout, DevState* state, double tol, int max_sweeps) {
+  using C = JacCfg<PE>;
   extern __shared__ double js[];
   __shared__ double red[32];
   __shared__ int s_cnt;
   __shared__ double s_norm;
   const int p = p_dev ? *p_dev : p_static;
   if (p <= 0) return;
-  const int Pe = p + (p & 1);
-  const int half = Pe / 2;
-  double* Hp = js;                                  // Pe(Pe+1)/2
-  double* V = Hp + (Pe * (Pe + 1)) / 2;             // Pe x Pe
-  double* cs = V + Pe * Pe;                         // [half][3] = c, s, t
-  int* pi = reinterpret_cast<int*>(cs + 3 * half);  // [half]
-  int* pj = pi + half;
-  unsigned short* blk = reinterpret_cast<unsigned short*>(pj + half);  // [nblk] = (a << 8) | b
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int nblk_all = half * (half + 1) / 2;
-  for (int e = tid; e < nblk_all; e += nt) {  // block (a, b), a <= b, enumerated once
+  double* Hs = js;                                       // HSIZE
+  double* V = Hs + C::HSIZE;                             // PE x PE
+  double* cs2 = V + PE * PE;                             // [2][HALF][3] = c, s, t
+  int* pi2 = reinterpret_cast<int*>(cs2 + 6 * C::HALF);  // [2][HALF]
+  int* pj2 = pi2 + 2 * C::HALF;                          // [2][HALF]
+  unsigned short* blk = reinterpret_cast<unsigned short*>(pj2 + 2 * C::HALF);  // (a << 8) | b
+  const int tid = threadIdx.x;
+  constexpr int NT = C::THREADS;
+
+  for (int e = tid; e < C::NBLK; e += NT) {
     int a = 0, rem = e;
-    while (rem >= half - a) {
-      rem -= half - a;
+    while (rem >= C::HALF - a) {
+      rem -= C::HALF - a;
       ++a;
     }
     blk[e] = (unsigned short)((a << 8) | (a + rem));
   }
-
-  for (int i = tid; i < Pe; i += nt)
-    for (int j = i; j < Pe; ++j) {
-      double v = 0.0;
-      if (i < p && j < p) v = 0.5 * (H[i * p + j] + H[j * p + i]);
-      Hp[pk(i, j, Pe)] = v;
-    }
-  for (int e = tid; e < Pe * Pe; e += nt) V[e] = (e / Pe == e % Pe) ? 1.0 : 0.0;
+  for (int e = tid; e < PE * PE; e += NT) {
+    const int i = e / PE, j = e % PE;
+    V[e] = (i == j) ? 1.0 : 0.0;
+    if (!C::PACKED || i <= j)
+      Hs[hix<PE>(i, j)] = (i < p && j < p) ? 0.5 * (H[i * p + j] + H[j * p + i]) : 0.0;
+  }
   __syncthreads();
 
   int sweep = 0;
   bool converged = false;
   for (; sweep < max_sweeps; ++sweep) {
     double off = 0.0, tot = 0.0;
-    for (int e = tid; e < Pe * Pe; e += nt) {
-      const int i = e / Pe, j = e % Pe;
-      const double v = Hp[pk(i, j, Pe)];
+    for (int e = tid; e < PE * PE; e += NT) {
+      const int i = e / PE, j = e % PE;
+      const double v = Hs[hix<PE>(i, j)];
       tot += v * v;
       if (i != j) off += v * v;
     }
     off = block_sum(off, red);
     tot = block_sum(tot, red);
-    if (tid == 0) s_norm = sqrt(tot);
     if (off <= tol * tol * tot || off == 0.0) {
       converged = true;
       break;
     }
-    if (tid == 0) s_cnt = 0;
+    if (tid == 0) {
+      s_cnt = 0;
+      s_norm = sqrt(tot);
+    }
     __syncthreads();
-    for (int r = 0; r < Pe - 1; ++r) {
-      // pairs of this round and their rotations
-      for (int m = tid; m < half; m += nt) {
+    for (int r = 0; r <= PE - 1; ++r) {
+      // phase 1: the first warp computes the rotations of round r (double-buffered) while the
+      // other warps apply the V update of round r - 1 (V is not read inside a sweep)
+      double* cs = cs2 + (r & 1) * 3 * C::HALF;
+      int* pi = pi2 + (r & 1) * C::HALF;
+      int* pj = pj2 + (r & 1) * C::HALF;
+      if (r > 0 && tid >= 32) {
+        const double* csp = cs2 + ((r - 1) & 1) * 3 * C::HALF;
+        const int* pip = pi2 + ((r - 1) & 1) * C::HALF;
+        const int* pjp = pj2 + ((r - 1) & 1) * C::HALF;
+        for (int e = tid - 32; e < PE * C::HALF; e += NT - 32) {
+          const int row = e / C::HALF, m = e % C::HALF;
+          const double c = csp[3 * m], s = csp[3 * m + 1];
+          if (s != 0.0) {
+            const int i = pip[m], j = pjp[m];
+            const double vi = V[row * PE + i], vj = V[row * PE + j];
+            V[row * PE + i] = c * vi - s * vj;
+            V[row * PE + j] = s * vi + c * vj;
+          }
+        }
+      }
+      if (r == PE - 1) {  // flush of the last round's V update done above
+        __syncthreads();
+        break;
+      }
+      if (tid < C::HALF) {
+        const int m = tid;
         int a, b;
         if (m == 0) {
-          a = Pe - 1;
+          a = PE - 1;
           b = r;
         } else {
-          a = (r + m) % (Pe - 1);
-          b = (r - m + (Pe - 1)) % (Pe - 1);
+          a = (r + m) % (PE - 1);
+          b = (r - m + (PE - 1)) % (PE - 1);
         }
         const int i = a < b ? a : b, j = a < b ? b : a;
         pi[m] = i;
         pj[m] = j;
         double c = 1.0, s = 0.0, t = 0.0;
         if (j < p) {
-          const double hij = Hp[pk(i, j, Pe)];
-          const double hii = Hp[pk(i, i, Pe)], hjj = Hp[pk(j, j, Pe)];
+          const double hij = Hs[hix<PE>(i, j)];
           // threshold Jacobi: skip rotations below the rounding floor of H; the error this
           // leaves in V diag(f) V^T is <= |h_ij| (a rotation mixes pairs within their gap)
           if (fabs(hij) > 1e-16 * s_norm) {
-            const double tau = (hjj - hii) / (2.0 * hij);
-            t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-            c = 1.0 / sqrt(1.0 + t * t);
-            s = t * c;
+            const double hii = Hs[hix<PE>(i, i)], hjj = Hs[hix<PE>(j, j)];
+            // sym.schur2 via cot(2 phi) = (h_jj - h_ii) / (2 h_ij), |phi| <= pi/4, written with
+            // two reciprocal square roots instead of the div/sqrt/div chain:
+            // cos 2phi = |d|/r, c = sqrt((1 + cos 2phi)/2), s = sign(d) e / (2 r c), t = s / c
+            const double dd = hjj - hii, ee = 2.0 * hij;
+            const double ir = rsqrt(dd * dd + ee * ee);
+            const double hh = 0.5 + 0.5 * fabs(dd) * ir;
+            const double rc = rsqrt(hh);
+            c = hh * rc;
+            s = (dd >= 0.0 ? 0.5 : -0.5) * ee * ir * rc;
+            t = s * rc;
             atomicAdd(&s_cnt, 1);
           }
         }
@@ -438,44 +484,41 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const double* __restrict__
         cs[3 * m + 2] = t;
       }
       __syncthreads();
-      // 2x2 block updates: blocks (a, b), a <= b, enumerated linearly
-      for (int e = tid; e < nblk_all; e += nt) {
+      for (int e = tid; e < C::NBLK; e += NT) {
         const int a = blk[e] >> 8, b = blk[e] & 0xff;
         const int ia = pi[a], ja = pj[a];
         const double ca = cs[3 * a], sa = cs[3 * a + 1];
         if (a == b) {
-          const double ta = cs[3 * a + 2];
           if (sa != 0.0) {
-            const double hij = Hp[pk(ia, ja, Pe)];
-            Hp[pk(ia, ia, Pe)] -= ta * hij;
-            Hp[pk(ja, ja, Pe)] += ta * hij;
-            Hp[pk(ia, ja, Pe)] = 0.0;
+            const double ta = cs[3 * a + 2];
+            const double hij = Hs[hix<PE>(ia, ja)];
+            Hs[hix<PE>(ia, ia)] -= ta * hij;
+            Hs[hix<PE>(ja, ja)] += ta * hij;
+            Hs[hix<PE>(ia, ja)] = 0.0;
+            if (!C::PACKED) Hs[hix<PE>(ja, ia)] = 0.0;
           }
         } else {
           const int ib = pi[b], jb = pj[b];
           const double cb = cs[3 * b], sb = cs[3 * b + 1];
           if (sa != 0.0 || sb != 0.0) {
-            const int k11 = pk(ia, ib, Pe), k12 = pk(ia, jb, Pe), k21 = pk(ja, ib, Pe),
-                      k22 = pk(ja, jb, Pe);
-            const double b11 = Hp[k11], b12 = Hp[k12], b21 = Hp[k21], b22 = Hp[k22];
+            const int k11 = hix<PE>(ia, ib), k12 = hix<PE>(ia, jb), k21 = hix<PE>(ja, ib),
+                      k22 = hix<PE>(ja, jb);
+            const double b11 = Hs[k11], b12 = Hs[k12], b21 = Hs[k21], b22 = Hs[k22];
             const double t11 = ca * b11 - sa * b21, t12 = ca * b12 - sa * b22;
             const double t21 = sa * b11 + ca * b21, t22 = sa * b12 + ca * b22;
-            Hp[k11] = t11 * cb - t12 * sb;
-            Hp[k12] = t11 * sb + t12 * cb;
-            Hp[k21] = t21 * cb - t22 * sb;
-            Hp[k22] = t21 * sb + t22 * cb;
+            const double n11 = t11 * cb - t12 * sb, n12 = t11 * sb + t12 * cb;
+            const double n21 = t21 * cb - t22 * sb, n22 = t21 * sb + t22 * cb;
+            Hs[k11] = n11;
+            Hs[k12] = n12;
+            Hs[k21] = n21;
+            Hs[k22] = n22;
+            if (!C::PACKED) {  // mirror into the lower triangle
+              Hs[hix<PE>(ib, ia)] = n11;
+              Hs[hix<PE>(jb, ia)] = n12;
+              Hs[hix<PE>(ib, ja)] = n21;
+              Hs[hix<PE>(jb, ja)] = n22;
+            }
           }
-        }
-      }
-      // V <- V J (columns i, j of every row)
-      for (int e = tid; e < Pe * half; e += nt) {
-        const int row = e / half, m = e % half;
-        const double c = cs[3 * m], s = cs[3 * m + 1];
-        if (s != 0.0) {
-          const int i = pi[m], j = pj[m];
-          const double vi = V[row * Pe + i], vj = V[row * Pe + j];
-          V[row * Pe + i] = c * vi - s * vj;
-          V[row * Pe + j] = s * vi + c * vj;
         }
       }
       __syncthreads();
@@ -486,36 +529,48 @@ __global__ void __launch_bounds__(1024) jacobi_kernel(const double* __restrict__
       break;
     }
   }
-  if (!converged && tid == 0) atomicOr(&state->flags, PF_FLAG_JACOBI_MAXSWEEP);
+  if (tid == 0) {
+    state->scratch[1] = (double)sweep;
+    if (!converged) atomicOr(&state->flags, PF_FLAG_JACOBI_MAXSWEEP);
+  }
   // sort descending (stable by index) and emit
-  for (int i = tid; i < p; i += nt) {
-    const double li = Hp[pk(i, i, Pe)];
+  for (int i = tid; i < p; i += NT) {
+    const double li = Hs[hix<PE>(i, i)];
     int rank = 0;
     for (int k = 0; k < p; ++k) {
-      const double lk = Hp[pk(k, k, Pe)];
+      const double lk = Hs[hix<PE>(k, k)];
       if (lk > li || (lk == li && k < i)) ++rank;
     }
     theta[rank] = li;
-    for (int row = 0; row < p; ++row) Yout[row * p + rank] = V[row * Pe + i];
+    for (int row = 0; row < p; ++row) Yout[row * p + rank] = V[row * PE + i];
   }
 }
 
-cudaError_t jacobi_launch(const double* H, int p, const int* p_dev, double* theta, double* Y,
-                          DevState* state, double tol, int max_sweeps, cudaStream_t st) {
-  const int Pe = p + (p & 1), half = Pe / 2;
-  const size_t smem = ((size_t)Pe * (Pe + 1) / 2 + (size_t)Pe * Pe + 3 * half) * 8 +
-                      2 * half * 4 + (size_t)half * (half + 1) / 2 * 2;
+template <int PE>
+static cudaError_t jacobi_pe(const double* H, int p, const int* p_dev, double* theta, double* Y,
+                             DevState* state, double tol, int max_sweeps, cudaStream_t st) {
+  using C = JacCfg<PE>;
   static bool attr = false;
   if (!attr) {
-    const size_t mx =
-        ((size_t)128 * 129 / 2 + 128 * 128 + 3 * 64) * 8 + 2 * 64 * 4 + (size_t)64 * 65 / 2 * 2;
-    cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+    cudaFuncSetAttribute(jacobi_kernel<PE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)C::SMEM);
     attr = true;
   }
   count_launch();
-  jacobi_kernel<<<1, 1024, smem, st>>>(H, p, p_dev, theta, Y, state, tol, max_sweeps);
+  jacobi_kernel<PE><<<1, C::THREADS, C::SMEM, st>>>(H, p, p_dev, theta, Y, state, tol, max_sweeps);
   return cudaGetLastError();
 }
+
+// p: order (runtime bound when p_dev != NULL: the kernel reads *p_dev <= p)
+cudaError_t jacobi_launch(const double* H, int p, const int* p_dev, double* theta, double* Y,
+                          DevState* state, double tol, int max_sweeps, cudaStream_t st) {
+  if (p <= 16) return jacobi_pe<16>(H, p, p_dev, theta, Y, state, tol, max_sweeps, st);
+  if (p <= 32) return jacobi_pe<32>(H, p, p_dev, theta, Y, state, tol, max_sweeps, st);
+  if (p <= 64) return jacobi_pe<64>(H, p, p_dev, theta, Y, state, tol, max_sweeps, st);
+  if (p <= 128) return jacobi_pe<128>(H, p, p_dev, theta, Y, state, tol, max_sweeps, st);
+  return cudaErrorInvalidValue;
+}
+
 
 // =============================================================================== spectral op
 __global__ void spectral_kernel(int op, double thr, const double* __restrict__ theta, int p,
@@ -703,35 +758,57 @@ __global__ void __launch_bounds__(kLzThreads) lanczos_gemv_kernel(
   const int rows_per = (n + gridDim.x - 1) / gridDim.x;
   const int r0 = blockIdx.x * rows_per, r1 = min(n, r0 + rows_per);
   const double* q = Q + (size_t)j * ldq;
-  for (int r = r0 + warp; r < r1; r += nw) {
-    const double* a = A + (size_t)r * lda;
+  // All 8 warps cooperate on each pair of rows (warp w owns the column segment w): every warp
+  // has the same work, 8 independent 16-byte streaming loads of A per lane are in flight, and
+  // the warp's segment of q stays in L1 (A is read once with .cs).
+  __shared__ double red2[2][kLzThreads / 32];
+  const int seg = (((n + nw - 1) / nw) + 1) & ~1;
+  const int c0 = min(n, warp * seg), c1 = min(n, c0 + seg);
+  for (int r = r0; r < r1; r += 2) {
+    const bool two = (r + 1 < r1);
+    const double* a0 = A + (size_t)r * lda;
+    const double* a1 = A + (size_t)(two ? r + 1 : r) * lda;
     double s0 = 0.0, s1 = 0.0;
-    int c = lane * 2;
-    // 8 independent 16-byte streaming loads of A per lane in flight (A is read once: .cs keeps
-    // it out of L1 so the Lanczos vector q stays cached)
-    for (; c + 64 * 7 + 1 < n; c += 64 * 8) {
-      double2 x[8], y[8];
+    int c = c0 + lane * 2;
+    for (; c + 64 * 3 + 1 < c1; c += 64 * 4) {
+      double2 x0[4], x1[4], y[4];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) x[u] = __ldcs(reinterpret_cast<const double2*>(a + c + 64 * u));
+      for (int u = 0; u < 4; ++u) {
+        x0[u] = __ldcs(reinterpret_cast<const double2*>(a0 + c + 64 * u));
+        x1[u] = __ldcs(reinterpret_cast<const double2*>(a1 + c + 64 * u));
+      }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) y[u] = __ldg(reinterpret_cast<const double2*>(q + c + 64 * u));
+      for (int u = 0; u < 4; ++u) y[u] = __ldg(reinterpret_cast<const double2*>(q + c + 64 * u));
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        s0 += x[u].x * y[u].x;
-        s1 += x[u].y * y[u].y;
+      for (int u = 0; u < 4; ++u) {
+        s0 += x0[u].x * y[u].x + x0[u].y * y[u].y;
+        s1 += x1[u].x * y[u].x + x1[u].y * y[u].y;
       }
     }
-    for (; c < n; c += 64) {
-      s0 += a[c] * q[c];
-      if (c + 1 < n) s1 += a[c + 1] * q[c + 1];
+    for (; c < c1; c += 64) {
+      s0 += a0[c] * q[c];
+      s1 += a1[c] * q[c];
+      if (c + 1 < c1) {
+        s0 += a0[c + 1] * q[c + 1];
+        s1 += a1[c + 1] * q[c + 1];
+      }
     }
-    const double s = warp_sum(s0 + s1);
+    s0 = warp_sum(s0);
+    s1 = warp_sum(s1);
     if (lane == 0) {
-      w[r] = s;
-      if (r - r0 < 64) ws[r - r0] = s;
+      red2[0][warp] = s0;
+      red2[1][warp] = s1;
     }
+    __syncthreads();
+    if (threadIdx.x < 2 && (threadIdx.x == 0 || two)) {
+      double s = 0.0;
+      for (int u = 0; u < nw; ++u) s += red2[threadIdx.x][u];  // fixed order: deterministic
+      const int rr = r + threadIdx.x;
+      w[rr] = s;
+      if (rr - r0 < 64) ws[rr - r0] = s;
+    }
+    __syncthreads();
   }
-  __syncthreads();
   // partial dots with Q_0..Q_j over this block's rows (one warp per vector)
   for (int i = warp; i <= j; i += nw) {
     const double* qi = Q + (size_t)i * ldq;
