@@ -59,11 +59,16 @@ typedef enum {
  * `degree` (1 <= degree <= 64) on the current CUDA device.  Allocates all scratch. */
 pf_status pf_create(int64_t n, int32_t p, int32_t degree, pf_dtype dtype, pf_ctx* out);
 
-/* Same, for rank `rank` of `world` processes (one per GPU) sharing the NCCL unique id
- * `nccl_id` (128 bytes, from ncclGetUniqueId on one rank, broadcast by the caller).
- * Row block of this rank: rows [rank*n/world, (rank+1)*n/world). */
+/* Same, for rank `rank` of `world` processes (one per GPU, current device) sharing the NCCL
+ * unique id `nccl_id` (128 bytes from pf_nccl_unique_id on one rank, broadcast by the caller).
+ * Row block of this rank: rows [rank*n/world, (rank+1)*n/world).  Collective: every rank must
+ * call it.  Per Chebyshev step the context all-gathers Y_j over NCCL; Gram / H matrices and
+ * scalar objectives are all-reduced; Jacobi and the spectral operator run replicated.
+ * world = 1 is allowed (single-rank communicator, same code path). */
 pf_status pf_create_dist(int64_t n, int32_t p, int32_t degree, pf_dtype dtype,
                          const void* nccl_id, int32_t rank, int32_t world, pf_ctx* out);
+/* Writes a fresh NCCL unique id (ncclGetUniqueId) into out[0 .. bytes); bytes >= 128. */
+pf_status pf_nccl_unique_id(void* out, int32_t bytes);
 
 pf_status pf_destroy(pf_ctx ctx);
 const char* pf_status_string(pf_status s);

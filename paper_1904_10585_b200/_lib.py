@@ -54,6 +54,7 @@ def load() -> ctypes.CDLL:
         "pf_profile_read": [P, P, ctypes.POINTER(D), ctypes.POINTER(I64)],
         "pf_kernel_launches": [],
         "pf_diagnostics": [P, P, ctypes.POINTER(D)],
+        "pf_nccl_unique_id": [P, I32],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -75,6 +76,15 @@ def kernel_launches() -> int:
 
 class PFError(RuntimeError):
     pass
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh NCCL unique id (128 bytes) for pf_create_dist; broadcast it to every rank."""
+    buf = ctypes.create_string_buffer(128)
+    st = load().pf_nccl_unique_id(buf, 128)
+    if st != 0:
+        raise PFError(f"pf_nccl_unique_id: {STATUS.get(st, st)}")
+    return buf.raw
 
 
 def _ptr(t) -> int | None:
@@ -107,7 +117,7 @@ class Context:
         self.lib = load()
         self.n, self.p, self.d = n, p, d
         h = ctypes.c_void_p()
-        if world == 1:
+        if nccl_id is None:
             st = self.lib.pf_create(n, p, d, PF_FP64, ctypes.byref(h))
         else:
             buf = ctypes.create_string_buffer(nccl_id, 128)

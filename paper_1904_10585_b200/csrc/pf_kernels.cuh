@@ -56,13 +56,20 @@ cudaError_t interval_psd_launch(const double* lo_hi, double eta, double* interva
 cudaError_t interval_soft_launch(double thr, double eta, double* interval, DevState* state,
                                  cudaStream_t st);
 cudaError_t copy_theta_launch(const double* theta, int p, DevState* state, cudaStream_t st);
-// Lanczos
+// Lanczos (pf_lanczos.cu): vectors are local row blocks with pitch ldq; every phase leaves
+// LOCAL sums that the host all-reduces between phases when the context is distributed.
 int lanczos_blocks(int n_rows);
-cudaError_t lanczos_init_launch(const double* v0, int n, double* Qcols, double* partials,
-                                int* counter, DevState* state, cudaStream_t st);
-cudaError_t lanczos_step_launch(const double* A, int64_t lda, int n, int64_t ldq, int j,
-                                double* Qcols, double* w, double* h, double* partials,
-                                int* counter, DevState* state, cudaStream_t st);
+// norm_only: s[0] = |v0|^2 (local); else q0 = v0 / sqrt(s[0]) and the run is marked active
+cudaError_t lz_start_launch(const double* v0, int n_local, double* s, double* q0,
+                            DevState* state, cudaStream_t st, bool norm_only);
+cudaError_t lz_gemv_launch(const double* A, int64_t lda, int n_local, int n, const double* q,
+                           const double* Q, int64_t ldq, int j, double* w, double* h,
+                           double* partials, int* counter, DevState* state, cudaStream_t st);
+cudaError_t lz_orth_launch(int n_local, const double* Q, int64_t ldq, int j, double* w,
+                           const double* h, double* out, double* partials, int* counter,
+                           DevState* state, int phase, cudaStream_t st);
+cudaError_t lz_next_launch(int n_local, double* Q, int64_t ldq, int j, const double* w,
+                           const double* s, DevState* state, cudaStream_t st);
 cudaError_t lanczos_finish_launch(int m, double* T, double* theta, double* S, double* lo_hi,
                                   DevState* state, cudaStream_t st);
 cudaError_t perturb_launch(double* A, int64_t lda, const double* E, int64_t lde, int rows,
@@ -77,6 +84,7 @@ cudaError_t prox_launch(const double* V, int64_t ldv, const double* f, double ta
 cudaError_t admm_launch(const double* V, int64_t ldv, const double* f, double t,
                         const uint32_t* adj, int64_t ldadj, const double* deg, double* Z,
                         int64_t ldz, int n_rows, int n, int row0, int p, double* obj,
-                        double* partials, int* counter, cudaStream_t st);
+                        double* partials, int* counter, int raw, cudaStream_t st);
+cudaError_t sqrt_inplace_launch(double* x, cudaStream_t st);
 
 }  // namespace pf

@@ -1,0 +1,305 @@
+// pf_lanczos.cu -- m-step Lanczos with full re-orthogonalisation (CGS2) for the interval end a
+// (the paper's `eigs` for lambda_n; reading R5).  Vectors are row blocks of n_local
+// rows (pitch ldq); the matrix-vector product reads the local rows of A against the full
+// (all-gathered) Lanczos vector, so every step is one HBM pass over the local block of A.
+// Each phase produces LOCAL partial sums (dots, norms) reduced deterministically inside the
+// kernel; the host all-reduces them between phases when the context is distributed.
+#include <algorithm>
+
+#include "pf_kernels.cuh"
+#include "../../include/pf.h"
+
+namespace pf {
+
+constexpr int kLzThreads = 256;
+
+int lanczos_blocks(int n_rows) { return std::max(1, std::min(4 * 148, (n_rows + 7) / 8)); }
+
+__device__ bool last_block_done(int* counter, int* s_last) {
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int prev = atomicAdd(counter, 1);
+    *s_last = (prev == (int)gridDim.x - 1);
+  }
+  __syncthreads();
+  return *s_last != 0;
+}
+
+// deterministic warp reduction of partials[b * kMaxLanczos + i] over b (fixed lane stride + tree)
+__device__ __forceinline__ double warp_reduce_partials(const double* partials, int nb, int i) {
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (int b = lane; b < nb; b += 32) s += __ldcg(partials + (size_t)b * kMaxLanczos + i);
+  return warp_sum(s);
+}
+
+// s[0] = sum of squares of the local rows of v
+__global__ void lz_norm2_kernel(const double* __restrict__ v, int n_local, double* s) {
+  __shared__ double red[32];
+  double a = 0.0;
+  for (int i = threadIdx.x; i < n_local; i += blockDim.x) a += v[i] * v[i];
+  a = block_sum(a, red);
+  if (threadIdx.x == 0) s[0] = a;
+}
+
+// q0 = v0 / sqrt(s[0]) (s = global sum of squares); marks the Lanczos run as active
+__global__ void lz_start_kernel(const double* __restrict__ v0, int n_local, const double* s,
+                                double* q, DevState* state) {
+  const double inv = 1.0 / sqrt(s[0]);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_local; i += gridDim.x * blockDim.x)
+    q[i] = v0[i] * inv;
+  if (blockIdx.x == 0 && threadIdx.x == 0) state->lanczos_steps = -1;  // running
+}
+
+cudaError_t lz_start_launch(const double* v0, int n_local, double* s, double* q0,
+                            DevState* state, cudaStream_t st, bool norm_only) {
+  if (norm_only) {
+    count_launch();
+    lz_norm2_kernel<<<1, 1024, 0, st>>>(v0, n_local, s);
+  } else {
+    count_launch();
+    lz_start_kernel<<<std::max(1, std::min(148, (n_local + 255) / 256)), 256, 0, st>>>(
+        v0, n_local, s, q0, state);
+  }
+  return cudaGetLastError();
+}
+
+// w = A_local q_full (one HBM pass over the local rows of A), then local partial dots
+// h_i = Q_i . w (i <= j) reduced in block order by the last block.
+__global__ void __launch_bounds__(kLzThreads, 4) lz_gemv_kernel(
+    const double* __restrict__ A, int64_t lda, int n_local, int n, const double* __restrict__ q,
+    const double* __restrict__ Q, int64_t ldq, int j, double* __restrict__ w,
+    double* __restrict__ h, double* __restrict__ partials, int* counter, DevState* state) {
+  if (state->lanczos_steps >= 0) return;  // stopped (breakdown)
+  __shared__ double ws[64];
+  __shared__ int s_last;
+  __shared__ double red2[2][kLzThreads / 32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = kLzThreads / 32;
+  const int rows_per = (n_local + gridDim.x - 1) / gridDim.x;
+  const int r0 = blockIdx.x * rows_per, r1 = min(n_local, r0 + rows_per);
+  // All 8 warps cooperate on each pair of rows (warp w owns the column segment w): every warp
+  // has the same work, 8 independent 16-byte streaming loads of A per lane are in flight, and
+  // the warp's segment of q stays in L1 (A is read once with .cs).
+  const int seg = (((n + nw - 1) / nw) + 1) & ~1;
+  const int c0 = min(n, warp * seg), c1 = min(n, c0 + seg);
+  for (int r = r0; r < r1; r += 2) {
+    const bool two = (r + 1 < r1);
+    const double* a0 = A + (size_t)r * lda;
+    const double* a1 = A + (size_t)(two ? r + 1 : r) * lda;
+    double s0 = 0.0, s1 = 0.0;
+    int c = c0 + lane * 2;
+    for (; c + 64 * 3 + 1 < c1; c += 64 * 4) {
+      double2 x0[4], x1[4], y[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        x0[u] = __ldcs(reinterpret_cast<const double2*>(a0 + c + 64 * u));
+        x1[u] = __ldcs(reinterpret_cast<const double2*>(a1 + c + 64 * u));
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) y[u] = __ldg(reinterpret_cast<const double2*>(q + c + 64 * u));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        s0 += x0[u].x * y[u].x + x0[u].y * y[u].y;
+        s1 += x1[u].x * y[u].x + x1[u].y * y[u].y;
+      }
+    }
+    for (; c < c1; c += 64) {
+      s0 += a0[c] * q[c];
+      s1 += a1[c] * q[c];
+      if (c + 1 < c1) {
+        s0 += a0[c + 1] * q[c + 1];
+        s1 += a1[c + 1] * q[c + 1];
+      }
+    }
+    s0 = warp_sum(s0);
+    s1 = warp_sum(s1);
+    if (lane == 0) {
+      red2[0][warp] = s0;
+      red2[1][warp] = s1;
+    }
+    __syncthreads();
+    if (threadIdx.x < 2 && (threadIdx.x == 0 || two)) {
+      double s = 0.0;
+      for (int u = 0; u < nw; ++u) s += red2[threadIdx.x][u];  // fixed order: deterministic
+      const int rr = r + threadIdx.x;
+      w[rr] = s;
+      if (rr - r0 < 64) ws[rr - r0] = s;
+    }
+    __syncthreads();
+  }
+  // partial dots with Q_0..Q_j over this block's rows (one warp per vector)
+  for (int i = warp; i <= j; i += nw) {
+    const double* qi = Q + (size_t)i * ldq;
+    double s = 0.0;
+    for (int r = r0 + lane; r < r1; r += 32) s += qi[r] * ((r - r0 < 64) ? ws[r - r0] : w[r]);
+    s = warp_sum(s);
+    if (lane == 0) partials[(size_t)blockIdx.x * kMaxLanczos + i] = s;
+  }
+  if (last_block_done(counter, &s_last)) {
+    __threadfence();
+    for (int i = warp; i <= j; i += nw) {
+      const double s = warp_reduce_partials(partials, (int)gridDim.x, i);
+      if (lane == 0) h[i] = s;
+    }
+    if (threadIdx.x == 0) *counter = 0;
+  }
+}
+
+// w -= Q h (local rows); phase 1: local partial dots -> out[0..j]; phase 2: local |w|^2 -> out[0]
+__global__ void __launch_bounds__(kLzThreads) lz_orth_kernel(
+    int n_local, const double* __restrict__ Q, int64_t ldq, int j, double* __restrict__ w,
+    const double* __restrict__ h, double* __restrict__ out, double* __restrict__ partials,
+    int* counter, DevState* state, int phase) {
+  if (state->lanczos_steps >= 0) return;
+  __shared__ double hs[kMaxLanczos];
+  __shared__ int s_last;
+  __shared__ double red[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = kLzThreads / 32;
+  for (int i = threadIdx.x; i <= j; i += blockDim.x) hs[i] = h[i];
+  if (phase == 1 && blockIdx.x == 0 && threadIdx.x == 0)
+    state->lanczos_alpha[j] = h[j];  // alpha_j = q_j . A q_j (global after the all-reduce)
+  __syncthreads();
+  const int rows_per = (n_local + gridDim.x - 1) / gridDim.x;
+  const int r0 = blockIdx.x * rows_per, r1 = min(n_local, r0 + rows_per);
+  for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+    double v = w[r];
+    for (int i = 0; i <= j; ++i) v -= Q[(size_t)i * ldq + r] * hs[i];
+    w[r] = v;
+  }
+  __syncthreads();
+  if (phase == 1) {
+    for (int i = warp; i <= j; i += nw) {
+      const double* qi = Q + (size_t)i * ldq;
+      double s = 0.0;
+      for (int r = r0 + lane; r < r1; r += 32) s += qi[r] * w[r];
+      s = warp_sum(s);
+      if (lane == 0) partials[(size_t)blockIdx.x * kMaxLanczos + i] = s;
+    }
+  } else {
+    double s = 0.0;
+    for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) s += w[r] * w[r];
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) partials[(size_t)blockIdx.x * kMaxLanczos] = s;
+  }
+  if (last_block_done(counter, &s_last)) {
+    __threadfence();
+    if (phase == 1) {
+      for (int i = warp; i <= j; i += nw) {
+        const double s = warp_reduce_partials(partials, (int)gridDim.x, i);
+        if (lane == 0) out[i] = s;
+      }
+    } else if (warp == 0) {
+      const double s = warp_reduce_partials(partials, (int)gridDim.x, 0);
+      if (lane == 0) out[0] = s;
+    }
+    if (threadIdx.x == 0) *counter = 0;
+  }
+}
+
+// beta_j = sqrt(s) with the breakdown test of reading R5, then q_{j+1} = w / beta_j
+__global__ void lz_next_kernel(int n_local, double* Q, int64_t ldq, int j, const double* w,
+                               const double* s, DevState* state) {
+  __shared__ int s_stop;
+  if (state->lanczos_steps >= 0) return;
+  const double beta = sqrt(s[0]);
+  if (threadIdx.x == 0) {
+    double amax = 1.0;
+    for (int i = 0; i <= j; ++i) amax = fmax(amax, fabs(state->lanczos_alpha[i]));
+    s_stop = (beta <= 1e-12 * amax);
+  }
+  __syncthreads();
+  if (s_stop) {
+    // every block reaches the same decision from the same (all-reduced) s; block 0 records it
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      state->lanczos_beta[j] = 0.0;
+      atomicOr(&state->flags, PF_FLAG_LANCZOS_BREAK);
+    }
+    return;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) state->lanczos_beta[j] = beta;
+  const double inv = 1.0 / beta;
+  double* q = Q + (size_t)(j + 1) * ldq;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n_local; r += gridDim.x * blockDim.x)
+    q[r] = w[r] * inv;
+}
+
+// the stop flag is applied after the step in a separate single-thread kernel so no block of
+// lz_next reads a half-updated lanczos_steps
+__global__ void lz_commit_kernel(int j, DevState* state) {
+  if (state->lanczos_steps >= 0) return;
+  if (state->lanczos_beta[j] == 0.0) state->lanczos_steps = j + 1;
+}
+
+cudaError_t lz_gemv_launch(const double* A, int64_t lda, int n_local, int n, const double* q,
+                           const double* Q, int64_t ldq, int j, double* w, double* h,
+                           double* partials, int* counter, DevState* state, cudaStream_t st) {
+  count_launch();
+  lz_gemv_kernel<<<lanczos_blocks(n_local), kLzThreads, 0, st>>>(A, lda, n_local, n, q, Q, ldq, j,
+                                                                 w, h, partials, counter, state);
+  return cudaGetLastError();
+}
+
+cudaError_t lz_orth_launch(int n_local, const double* Q, int64_t ldq, int j, double* w,
+                           const double* h, double* out, double* partials, int* counter,
+                           DevState* state, int phase, cudaStream_t st) {
+  count_launch();
+  lz_orth_kernel<<<lanczos_blocks(n_local), kLzThreads, 0, st>>>(n_local, Q, ldq, j, w, h, out,
+                                                                 partials, counter, state, phase);
+  return cudaGetLastError();
+}
+
+cudaError_t lz_next_launch(int n_local, double* Q, int64_t ldq, int j, const double* w,
+                           const double* s, DevState* state, cudaStream_t st) {
+  count_launch();
+  lz_next_kernel<<<std::max(1, std::min(148, (n_local + 255) / 256)), 256, 0, st>>>(n_local, Q, ldq,
+                                                                                   j, w, s, state);
+  count_launch();
+  lz_commit_kernel<<<1, 1, 0, st>>>(j, state);
+  return cudaGetLastError();
+}
+
+// build T (m_eff x m_eff) from alpha/beta; m_eff is written to a device int for the Jacobi
+__global__ void lanczos_T_kernel(int m, double* T, DevState* state, int* m_out) {
+  int me = state->lanczos_steps;
+  if (me < 0) me = m;  // ran all m steps
+  if (threadIdx.x == 0) *m_out = me;
+  for (int e = threadIdx.x; e < me * me; e += blockDim.x) {
+    const int i = e / me, k = e % me;
+    double v = 0.0;
+    if (i == k) v = state->lanczos_alpha[i];
+    else if (k == i + 1) v = state->lanczos_beta[i];
+    else if (i == k + 1) v = state->lanczos_beta[k];
+    T[e] = v;
+  }
+}
+
+// lo = theta_min - |beta_last s_{last,min}|, hi = theta_max + |beta_last s_{last,max}|
+__global__ void lanczos_extremes_kernel(const double* theta, const double* S, const int* m_dev,
+                                        double* lo_hi, DevState* state) {
+  const int me = *m_dev;
+  const double bl = state->lanczos_beta[me - 1];
+  const double rmin = fabs(bl * S[(me - 1) * me + (me - 1)]);
+  const double rmax = fabs(bl * S[(me - 1) * me + 0]);
+  const double lo = theta[me - 1] - rmin, hi = theta[0] + rmax;
+  lo_hi[0] = lo;
+  lo_hi[1] = hi;
+  state->lanczos[0] = lo;
+  state->lanczos[1] = hi;
+  state->have_lanczos = 1;
+  state->lanczos_steps = me;
+}
+
+cudaError_t lanczos_finish_launch(int m, double* T, double* theta, double* S, double* lo_hi,
+                                  DevState* state, cudaStream_t st) {
+  int* m_dev = reinterpret_cast<int*>(&state->scratch[0]);
+  count_launch();
+  lanczos_T_kernel<<<1, 256, 0, st>>>(m, T, state, m_dev);
+  cudaError_t e = jacobi_launch(T, m, m_dev, theta, S, state, 1e-15, 40, st);
+  if (e != cudaSuccess) return e;
+  count_launch();
+  lanczos_extremes_kernel<<<1, 1, 0, st>>>(theta, S, m_dev, lo_hi, state);
+  return cudaGetLastError();
+}
+
+}  // namespace pf

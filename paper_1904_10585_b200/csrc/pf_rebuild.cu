@@ -37,6 +37,7 @@ struct RbArgs {
   int64_t ldo;
   int n_rows, n, row0;
   int sym, T;
+  int raw;  // 1: obj[1] (PFAM) is left as the raw sum of squares for a cross-rank all-reduce
   double* partials;
   int* counter;
   double* obj;
@@ -302,7 +303,7 @@ __global__ void __launch_bounds__(128) rebuild_kernel(const RbArgs a) {
         a.obj[1] = sf;
       } else {
         a.obj[0] = t0;
-        a.obj[1] = sqrt(t1);
+        a.obj[1] = a.raw ? t1 : sqrt(t1);
       }
       *a.counter = 0;
     }
@@ -354,17 +355,25 @@ cudaError_t prox_launch(const double* V, int64_t ldv, const double* f, double ta
                         double* Aout, int64_t lda, int n_rows, int n, int row0, int p,
                         double* obj, double* partials, int* counter, cudaStream_t st) {
   RbArgs a{V, ldv, f, tau, omega, ldo, W, ldw, r, 0, nullptr, Aout, lda, n_rows, n, row0,
-           0, 0, partials, counter, obj};
+           0, 0, 0, partials, counter, obj};
   return rb_dispatch<true>(p, a, st);
 }
 
 cudaError_t admm_launch(const double* V, int64_t ldv, const double* f, double t,
                         const uint32_t* adj, int64_t ldadj, const double* deg, double* Z,
                         int64_t ldz, int n_rows, int n, int row0, int p, double* obj,
-                        double* partials, int* counter, cudaStream_t st) {
+                        double* partials, int* counter, int raw, cudaStream_t st) {
   RbArgs a{V, ldv, f, t, adj, ldadj, nullptr, 0, 0, 0, deg, Z, ldz, n_rows, n, row0,
-           0, 0, partials, counter, obj};
+           0, 0, raw, partials, counter, obj};
   return rb_dispatch<false>(p, a, st);
+}
+
+__global__ void sqrt_inplace_kernel(double* x) { x[0] = sqrt(x[0]); }
+
+cudaError_t sqrt_inplace_launch(double* x, cudaStream_t st) {
+  count_launch();
+  sqrt_inplace_kernel<<<1, 1, 0, st>>>(x);
+  return cudaGetLastError();
 }
 
 }  // namespace pf

@@ -698,270 +698,6 @@ cudaError_t copy_theta_launch(const double* theta, int p, DevState* state, cudaS
   return cudaGetLastError();
 }
 
-// =============================================================================== Lanczos
-// Q: (m+1) Lanczos vectors stored column by column (vector j at Q + j*n).
-constexpr int kLzThreads = 256;
-
-int lanczos_blocks(int n_rows) { return std::max(1, std::min(4 * 148, (n_rows + 7) / 8)); }
-
-// last-block reduction helper: partials[blk * stride + i], i < cnt -> out[i] (block order)
-__device__ bool last_block_done(int* counter, int* s_last) {
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const int prev = atomicAdd(counter, 1);
-    *s_last = (prev == (int)gridDim.x - 1);
-  }
-  __syncthreads();
-  return *s_last != 0;
-}
-
-// deterministic warp reduction of partials[b * kMaxLanczos + i] over b (fixed lane stride + tree)
-__device__ __forceinline__ double warp_reduce_partials(const double* partials, int nb, int i) {
-  const int lane = threadIdx.x & 31;
-  double s = 0.0;
-  for (int b = lane; b < nb; b += 32) s += __ldcg(partials + (size_t)b * kMaxLanczos + i);
-  return warp_sum(s);
-}
-
-__global__ void lanczos_init_kernel(const double* __restrict__ v0, int n, double* Q,
-                                    DevState* state) {
-  __shared__ double red[32];
-  double s = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) s += v0[i] * v0[i];
-  s = block_sum(s, red);
-  const double inv = 1.0 / sqrt(s);
-  for (int i = threadIdx.x; i < n; i += blockDim.x) Q[i] = v0[i] * inv;
-  if (threadIdx.x == 0) {
-    state->lanczos_steps = -1;  // running
-  }
-}
-
-cudaError_t lanczos_init_launch(const double* v0, int n, double* Qcols, double* partials,
-                                int* counter, DevState* state, cudaStream_t st) {
-  (void)partials;
-  (void)counter;
-  count_launch();
-  lanczos_init_kernel<<<1, 1024, 0, st>>>(v0, n, Qcols, state);
-  return cudaGetLastError();
-}
-
-// phase 0: w = A q_j and partial h_i = Q_i . w (i <= j); last block reduces -> h
-__global__ void __launch_bounds__(kLzThreads) lanczos_gemv_kernel(
-    const double* __restrict__ A, int64_t lda, int n, int64_t ldq, int j, const double* __restrict__ Q,
-    double* __restrict__ w, double* __restrict__ h, double* __restrict__ partials, int* counter,
-    DevState* state) {
-  if (state->lanczos_steps >= 0) return;  // stopped
-  __shared__ double ws[64];
-  __shared__ int s_last;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = kLzThreads / 32;
-  const int rows_per = (n + gridDim.x - 1) / gridDim.x;
-  const int r0 = blockIdx.x * rows_per, r1 = min(n, r0 + rows_per);
-  const double* q = Q + (size_t)j * ldq;
-  // All 8 warps cooperate on each pair of rows (warp w owns the column segment w): every warp
-  // has the same work, 8 independent 16-byte streaming loads of A per lane are in flight, and
-  // the warp's segment of q stays in L1 (A is read once with .cs).
-  __shared__ double red2[2][kLzThreads / 32];
-  const int seg = (((n + nw - 1) / nw) + 1) & ~1;
-  const int c0 = min(n, warp * seg), c1 = min(n, c0 + seg);
-  for (int r = r0; r < r1; r += 2) {
-    const bool two = (r + 1 < r1);
-    const double* a0 = A + (size_t)r * lda;
-    const double* a1 = A + (size_t)(two ? r + 1 : r) * lda;
-    double s0 = 0.0, s1 = 0.0;
-    int c = c0 + lane * 2;
-    for (; c + 64 * 3 + 1 < c1; c += 64 * 4) {
-      double2 x0[4], x1[4], y[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        x0[u] = __ldcs(reinterpret_cast<const double2*>(a0 + c + 64 * u));
-        x1[u] = __ldcs(reinterpret_cast<const double2*>(a1 + c + 64 * u));
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) y[u] = __ldg(reinterpret_cast<const double2*>(q + c + 64 * u));
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        s0 += x0[u].x * y[u].x + x0[u].y * y[u].y;
-        s1 += x1[u].x * y[u].x + x1[u].y * y[u].y;
-      }
-    }
-    for (; c < c1; c += 64) {
-      s0 += a0[c] * q[c];
-      s1 += a1[c] * q[c];
-      if (c + 1 < c1) {
-        s0 += a0[c + 1] * q[c + 1];
-        s1 += a1[c + 1] * q[c + 1];
-      }
-    }
-    s0 = warp_sum(s0);
-    s1 = warp_sum(s1);
-    if (lane == 0) {
-      red2[0][warp] = s0;
-      red2[1][warp] = s1;
-    }
-    __syncthreads();
-    if (threadIdx.x < 2 && (threadIdx.x == 0 || two)) {
-      double s = 0.0;
-      for (int u = 0; u < nw; ++u) s += red2[threadIdx.x][u];  // fixed order: deterministic
-      const int rr = r + threadIdx.x;
-      w[rr] = s;
-      if (rr - r0 < 64) ws[rr - r0] = s;
-    }
-    __syncthreads();
-  }
-  // partial dots with Q_0..Q_j over this block's rows (one warp per vector)
-  for (int i = warp; i <= j; i += nw) {
-    const double* qi = Q + (size_t)i * ldq;
-    double s = 0.0;
-    for (int r = r0 + lane; r < r1; r += 32) s += qi[r] * ((r - r0 < 64) ? ws[r - r0] : w[r]);
-    s = warp_sum(s);
-    if (lane == 0) partials[(size_t)blockIdx.x * kMaxLanczos + i] = s;
-  }
-  if (last_block_done(counter, &s_last)) {
-    __threadfence();
-    for (int i = warp; i <= j; i += nw) {
-      const double s = warp_reduce_partials(partials, (int)gridDim.x, i);
-      if (lane == 0) h[i] = s;
-    }
-    if (threadIdx.x == 0) *counter = 0;
-  }
-}
-
-// phase 1/2: w -= Q h (rows of this block), then partial dots (phase 1) or partial |w|^2 (phase 2)
-__global__ void __launch_bounds__(kLzThreads) lanczos_orth_kernel(
-    int n, int64_t ldq, int j, const double* __restrict__ Q, double* __restrict__ w, double* __restrict__ h,
-    double* __restrict__ h_next, double* __restrict__ partials, int* counter, DevState* state,
-    int phase) {
-  if (state->lanczos_steps >= 0) return;
-  __shared__ double hs[kMaxLanczos];
-  __shared__ int s_last;
-  __shared__ double red[32];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = kLzThreads / 32;
-  for (int i = threadIdx.x; i <= j; i += blockDim.x) hs[i] = h[i];
-  if (phase == 1 && threadIdx.x == 0) state->lanczos_alpha[j] = h[j];  // alpha_j = q_j . A q_j
-  __syncthreads();
-  const int rows_per = (n + gridDim.x - 1) / gridDim.x;
-  const int r0 = blockIdx.x * rows_per, r1 = min(n, r0 + rows_per);
-  for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
-    double v = w[r];
-    for (int i = 0; i <= j; ++i) v -= Q[(size_t)i * ldq + r] * hs[i];
-    w[r] = v;
-  }
-  __syncthreads();
-  if (phase == 1) {
-    for (int i = warp; i <= j; i += nw) {
-      const double* qi = Q + (size_t)i * ldq;
-      double s = 0.0;
-      for (int r = r0 + lane; r < r1; r += 32) s += qi[r] * w[r];
-      s = warp_sum(s);
-      if (lane == 0) partials[(size_t)blockIdx.x * kMaxLanczos + i] = s;
-    }
-  } else {
-    double s = 0.0;
-    for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) s += w[r] * w[r];
-    s = block_sum(s, red);
-    if (threadIdx.x == 0) partials[(size_t)blockIdx.x * kMaxLanczos] = s;
-  }
-  if (last_block_done(counter, &s_last)) {
-    __threadfence();
-    if (phase == 1) {
-      for (int i = warp; i <= j; i += nw) {
-        const double s = warp_reduce_partials(partials, (int)gridDim.x, i);
-        if (lane == 0) h_next[i] = s;
-      }
-    } else if (warp == 0) {
-      const double s = warp_reduce_partials(partials, (int)gridDim.x, 0);
-      const double beta = sqrt(s);
-      if (lane == 0) {
-        double amax = 1.0;
-        for (int i = 0; i <= j; ++i) amax = fmax(amax, fabs(state->lanczos_alpha[i]));
-        if (beta <= 1e-12 * amax) {
-          state->lanczos_beta[j] = 0.0;
-          state->lanczos_steps = j + 1;  // breakdown: stop
-          atomicOr(&state->flags, PF_FLAG_LANCZOS_BREAK);
-        } else {
-          state->lanczos_beta[j] = beta;
-        }
-      }
-    }
-    if (threadIdx.x == 0) *counter = 0;
-  }
-}
-
-__global__ void lanczos_next_kernel(int n, int64_t ldq, int j, double* Q, const double* w,
-                                    DevState* state) {
-  if (state->lanczos_steps >= 0) return;
-  const double inv = 1.0 / state->lanczos_beta[j];
-  double* q = Q + (size_t)(j + 1) * ldq;
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
-    q[r] = w[r] * inv;
-}
-
-cudaError_t lanczos_step_launch(const double* A, int64_t lda, int n, int64_t ldq, int j,
-                                double* Qcols, double* w, double* h, double* partials,
-                                int* counter, DevState* state, cudaStream_t st) {
-  const int nb = lanczos_blocks(n);
-  double* h1 = h;
-  double* h2 = h + kMaxLanczos;
-  count_launch();
-  lanczos_gemv_kernel<<<nb, kLzThreads, 0, st>>>(A, lda, n, ldq, j, Qcols, w, h1, partials,
-                                                 counter, state);
-  count_launch();
-  lanczos_orth_kernel<<<nb, kLzThreads, 0, st>>>(n, ldq, j, Qcols, w, h1, h2, partials, counter,
-                                                 state, 1);
-  count_launch();
-  lanczos_orth_kernel<<<nb, kLzThreads, 0, st>>>(n, ldq, j, Qcols, w, h2, nullptr, partials,
-                                                 counter, state, 2);
-  count_launch();
-  lanczos_next_kernel<<<std::max(1, std::min(148, (n + 255) / 256)), 256, 0, st>>>(n, ldq, j,
-                                                                                  Qcols, w, state);
-  return cudaGetLastError();
-}
-
-// build T (m_eff x m_eff) from alpha/beta; m_eff is written to scratch int for the Jacobi
-__global__ void lanczos_T_kernel(int m, double* T, DevState* state, int* m_out) {
-  int me = state->lanczos_steps;
-  if (me < 0) me = m;  // ran all m steps
-  if (threadIdx.x == 0) {
-    *m_out = me;
-    state->lanczos_steps = me;
-  }
-  for (int e = threadIdx.x; e < me * me; e += blockDim.x) {
-    const int i = e / me, k = e % me;
-    double v = 0.0;
-    if (i == k) v = state->lanczos_alpha[i];
-    else if (k == i + 1) v = state->lanczos_beta[i];
-    else if (i == k + 1) v = state->lanczos_beta[k];
-    T[e] = v;
-  }
-}
-
-__global__ void lanczos_extremes_kernel(const double* theta, const double* S, const int* m_dev,
-                                        double* lo_hi, DevState* state) {
-  const int me = *m_dev;
-  const double bl = state->lanczos_beta[me - 1];
-  const double rmin = fabs(bl * S[(me - 1) * me + (me - 1)]);
-  const double rmax = fabs(bl * S[(me - 1) * me + 0]);
-  const double lo = theta[me - 1] - rmin, hi = theta[0] + rmax;
-  lo_hi[0] = lo;
-  lo_hi[1] = hi;
-  state->lanczos[0] = lo;
-  state->lanczos[1] = hi;
-  state->have_lanczos = 1;
-}
-
-cudaError_t lanczos_finish_launch(int m, double* T, double* theta, double* S, double* lo_hi,
-                                  DevState* state, cudaStream_t st) {
-  int* m_dev = reinterpret_cast<int*>(&state->scratch[0]);
-  count_launch();
-  lanczos_T_kernel<<<1, 256, 0, st>>>(m, T, state, m_dev);
-  cudaError_t e = jacobi_launch(T, m, m_dev, theta, S, state, 1e-15, 40, st);
-  if (e != cudaSuccess) return e;
-  count_launch();
-  lanczos_extremes_kernel<<<1, 1, 0, st>>>(theta, S, m_dev, lo_hi, state);
-  return cudaGetLastError();
-}
-
 // =============================================================================== perturb
 __global__ void perturb_kernel(double* A, int64_t lda, const double* E, int64_t lde, int rows,
                                int cols) {

@@ -24,20 +24,33 @@ def _bits(b: np.ndarray) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(b).view(np.int32)).cuda()
 
 
-class Solver:
-    """Holds the device state of one run: iterate A/Z (n x n), block U, factors V, f."""
+def rows_of(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Row block [r0, r1) owned by `rank` (the C library's split: floor(g n / world))."""
+    return rank * n // world, (rank + 1) * n // world
 
-    def __init__(self, cfg: Config, problem: dict | None = None, stream=None):
+
+class Solver:
+    """Holds the device state of one run: iterate A/Z (local rows x n), block U, factors V, f.
+
+    Distributed (nccl_id given): this process owns rows [r0, r1) = rows_of(n, rank, world) of
+    A/Z, U, V and of the row-wise masks; small objects are replicated (include/pf.h)."""
+
+    def __init__(self, cfg: Config, problem: dict | None = None, stream=None,
+                 nccl_id: bytes | None = None, rank: int = 0, world: int = 1):
         self.cfg = cfg
         n, p, d = cfg.n, cfg.p, cfg.d
         self.stream = stream
-        self.ctx = Context(n, p, d)
+        self.ctx = Context(n, p, d, nccl_id=nccl_id, rank=rank, world=world)
+        r0, r1 = rows_of(n, rank, world) if nccl_id is not None else (0, n)
+        self.r0, self.r1, self.n_local = r0, r1, r1 - r0
+        assert self.n_local == self.ctx.n_local
+        nl = self.n_local
         self.psd = cfg.mode in ("sweep_psd", "pfam")
         self.op = PF_OP_PSD if self.psd else PF_OP_SOFT_THRESHOLD
         # problem["_dev"]: inputs already on the device (the e2e path uploads them itself)
         devp = (problem or {}).get("_dev") or {}
-        self.U = devp["U0"] if "U0" in devp else _dev(initial_block(cfg))
-        self.V = torch.empty((n, p), dtype=torch.float64, device="cuda")
+        self.U = devp["U0"] if "U0" in devp else _dev(initial_block(cfg)[r0:r1])
+        self.V = torch.empty((nl, p), dtype=torch.float64, device="cuda")
         self.theta = torch.empty(p, dtype=torch.float64, device="cuda")
         self.f = torch.zeros(p, dtype=torch.float64, device="cuda")
         self.rank = torch.zeros(1, dtype=torch.int32, device="cuda")
@@ -48,16 +61,16 @@ class Solver:
         self.thr = 0.0
         if cfg.mode in ("sweep_psd", "sweep_soft"):
             A0 = cfg1_problem(cfg) if problem is None else problem["A0"]
-            self.A = _dev(A0)
+            self.A = _dev(A0[r0:r1])
             self.thr = cfg.theta
         elif cfg.mode == "pfpg":
             prob = pfpg_problem(cfg) if problem is None else problem
             self.prob = prob
-            self.omega = _bits(prob["omega_bits"])
+            self.omega = _bits(prob["omega_bits"][r0:r1])
             self.W = _dev(prob["W"])
             self.mu = prob["mu"]
             self.thr = cfg.tau * prob["mu"]
-            self.A = torch.empty((n, n), dtype=torch.float64, device="cuda")
+            self.A = torch.empty((nl, n), dtype=torch.float64, device="cuda")
             # X_0 = 0: A_0 = 0 - tau Omega o (0 - M)  (the update kernel with zero factors)
             self.ctx.prox_step(self.V.zero_(), self.f, cfg.tau, self.omega, self.W, self.A,
                                self.obj, stream)
@@ -67,9 +80,9 @@ class Solver:
             else:
                 prob = pfam_problem(cfg) if problem is None else problem
                 self.prob = prob
-                self.adj = _bits(prob["adj_bits"])
+                self.adj = _bits(prob["adj_bits"][r0:r1])
                 self.deg = _dev(prob["deg"])
-            self.A = torch.zeros((n, n), dtype=torch.float64, device="cuda")
+            self.A = torch.zeros((nl, n), dtype=torch.float64, device="cuda")
             # Z_0 = 0 -> Z_1 = prox_tG(0) = offdiag(-tC) + I  (reading R9)
             self.ctx.admm_step(self.V.zero_(), self.f, cfg.t, self.adj, self.deg, self.A,
                                self.obj, stream)
@@ -80,7 +93,7 @@ class Solver:
 
     def lanczos_vector(self, k: int) -> torch.Tensor:
         if k not in self._v0:
-            self._v0[k] = _dev(lanczos_start(self.cfg, k))
+            self._v0[k] = _dev(lanczos_start(self.cfg, k)[self.r0:self.r1])
         return self._v0[k]
 
     def step(self):
@@ -118,10 +131,11 @@ class Solver:
         return float(o[0]), float(o[1])
 
 
-def run(cfg: Config, iters: int | None = None, record: bool = True, problem=None) -> dict:
-    """Run K iterations on the GPU, recording per-iteration factors / objectives on the host."""
+def run(cfg: Config, iters: int | None = None, record: bool = True, problem=None,
+        nccl_id: bytes | None = None, rank: int = 0, world: int = 1) -> dict:
+    """Run K iterations on the GPU, recording per-iteration factors (local rows) / objectives."""
     K = cfg.iters if iters is None else iters
-    s = Solver(cfg, problem)
+    s = Solver(cfg, problem, nccl_id=nccl_id, rank=rank, world=world)
     recs = []
     for k in range(K):
         s.step()
@@ -134,7 +148,7 @@ def run(cfg: Config, iters: int | None = None, record: bool = True, problem=None
             if cfg.mode in ("pfpg", "pfam"):
                 rec["objective"], rec["aux"] = s.objective()
         if cfg.mode in ("sweep_psd", "sweep_soft") and k + 1 < K:
-            s.perturb(_dev(cfg1_noise(cfg, k)))
+            s.perturb(_dev(cfg1_noise(cfg, k)[s.r0:s.r1]))
         recs.append(rec)
     torch.cuda.synchronize()
     return {"records": recs, "status": s.ctx.status(), "solver": s}
