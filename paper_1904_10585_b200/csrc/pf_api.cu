@@ -33,6 +33,7 @@ struct pf_ctx_s {
   double* Y[3] = {nullptr, nullptr, nullptr};  // n_local x p, ld p
   double* Yfull = nullptr;                     // n x p gathered block (dist)
   double* Wbuf = nullptr;                      // n_local x p (A Q)
+  double* VFbuf = nullptr;                     // n_local x p (V diag(f) for the rebuild)
   double* Vfull = nullptr;                     // n x p (dist)
   double* G = nullptr;                         // p x p
   double* Rinv = nullptr;
@@ -124,6 +125,7 @@ static pf_status alloc_all(pf_ctx ctx) {
   ok &= A((void**)&ctx->state, sizeof(DevState));
   for (int i = 0; i < 3; ++i) ok &= A((void**)&ctx->Y[i], (size_t)nl * p * 8);
   ok &= A((void**)&ctx->Wbuf, (size_t)nl * p * 8);
+  ok &= A((void**)&ctx->VFbuf, (size_t)nl * p * 8);
   if (ctx->dist) {
     ok &= A((void**)&ctx->Yfull, (size_t)n * p * 8);
     ok &= A((void**)&ctx->Vfull, (size_t)n * p * 8);
@@ -274,7 +276,7 @@ pf_status pf_destroy(pf_ctx ctx) {
   for (auto e : ctx->ev) cudaEventDestroy(e);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   void* ptrs[] = {ctx->state,  ctx->Y[0],     ctx->Y[1],      ctx->Y[2],    ctx->Yfull,
-                  ctx->Wbuf,   ctx->Vfull,    ctx->G,         ctx->Rinv,    ctx->Yeig,
+                  ctx->Wbuf,   ctx->VFbuf,    ctx->Vfull,    ctx->G,         ctx->Rinv,    ctx->Yeig,
                   ctx->gram_part, ctx->cheb_ws, ctx->cheb_cnt, ctx->lz_Q,   ctx->lz_qfull,
                   ctx->lz_w,   ctx->lz_h,     ctx->lz_part,   ctx->lz_cnt,  ctx->lz_T,
                   ctx->lz_theta, ctx->lz_S,   ctx->rb_part,   ctx->rb_cnt,  ctx->shift_flag};
@@ -546,14 +548,16 @@ pf_status pf_prox_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f
                        pf_stream stream) {
   if (!ctx || !V || !f || !omega || !A_out || !obj) return PF_ERR_ARG;
   if (r < 0 || r > 64 || (r > 0 && !W)) return PF_ERR_ARG;
-  if (ldv < ctx->p || ldo < (ctx->n + 31) / 32 || lda_out < ctx->n || (r > 0 && ldw < r))
+  if (ldv < ctx->p || (ldv & 1) || !aligned16(V) || ldo < (ctx->n + 31) / 32 ||
+      lda_out < ctx->n || (r > 0 && ldw < r))
     return PF_ERR_DIM;
   cudaStream_t st = (cudaStream_t)stream;
   const double* Vf;
   int64_t ldf;
   PF_TRY(full_V(ctx, V, ldv, &Vf, &ldf, st));
-  PF_CU(prox_launch(Vf, ldf, f, tau, omega, ldo, W, ldw, r, A_out, lda_out, (int)ctx->n_local,
-                    (int)ctx->n, (int)ctx->row0, ctx->p, obj, ctx->rb_part, ctx->rb_cnt, st));
+  PF_CU(prox_launch(Vf, ldf, V, ldv, f, tau, omega, ldo, W, ldw, r, A_out, lda_out,
+                    (int)ctx->n_local, (int)ctx->n, (int)ctx->row0, ctx->p, obj, ctx->rb_part,
+                    ctx->rb_cnt, ctx->VFbuf, st));
   // obj[0] is a sum over row blocks; obj[1] = sum |f| is replicated
   return allreduce(ctx, obj, 1, st);
 }
@@ -562,13 +566,15 @@ pf_status pf_admm_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f
                        const uint32_t* adj, int64_t ldadj, const double* deg, double* Z,
                        int64_t ldz, double* obj, pf_stream stream) {
   if (!ctx || !V || !f || !adj || !deg || !Z || !obj) return PF_ERR_ARG;
-  if (ldv < ctx->p || ldadj < (ctx->n + 31) / 32 || ldz < ctx->n) return PF_ERR_DIM;
+  if (ldv < ctx->p || (ldv & 1) || !aligned16(V) || ldadj < (ctx->n + 31) / 32 || ldz < ctx->n)
+    return PF_ERR_DIM;
   cudaStream_t st = (cudaStream_t)stream;
   const double* Vf;
   int64_t ldf;
   PF_TRY(full_V(ctx, V, ldv, &Vf, &ldf, st));
-  PF_CU(admm_launch(Vf, ldf, f, t, adj, ldadj, deg, Z, ldz, (int)ctx->n_local, (int)ctx->n,
-                    (int)ctx->row0, ctx->p, obj, ctx->rb_part, ctx->rb_cnt, ctx->dist ? 1 : 0, st));
+  PF_CU(admm_launch(Vf, ldf, V, ldv, f, t, adj, ldadj, deg, Z, ldz, (int)ctx->n_local,
+                    (int)ctx->n, (int)ctx->row0, ctx->p, obj, ctx->rb_part, ctx->rb_cnt,
+                    ctx->dist ? 1 : 0, ctx->VFbuf, st));
   if (ctx->dist) {
     // <C, W> and the squared residual are sums over row blocks; sqrt after the reduction
     PF_TRY(allreduce(ctx, obj, 2, st));

@@ -77,14 +77,17 @@ cudaError_t perturb_launch(double* A, int64_t lda, const double* E, int64_t lde,
 
 // ---- rebuild + update (pf_rebuild.cu)
 int rebuild_blocks(int n_rows, int n);
-cudaError_t prox_launch(const double* V, int64_t ldv, const double* f, double tau,
-                        const uint32_t* omega, int64_t ldo, const double* W, int64_t ldw, int r,
-                        double* Aout, int64_t lda, int n_rows, int n, int row0, int p,
-                        double* obj, double* partials, int* counter, cudaStream_t st);
-cudaError_t admm_launch(const double* V, int64_t ldv, const double* f, double t,
-                        const uint32_t* adj, int64_t ldadj, const double* deg, double* Z,
-                        int64_t ldz, int n_rows, int n, int row0, int p, double* obj,
-                        double* partials, int* counter, int raw, cudaStream_t st);
+// V: all n rows (ldv); Vloc: this rank's rows (ldvl); vf: scratch n_local x p for V diag(f)
+cudaError_t prox_launch(const double* V, int64_t ldv, const double* Vloc, int64_t ldvl,
+                        const double* f, double tau, const uint32_t* omega, int64_t ldo,
+                        const double* W, int64_t ldw, int r, double* Aout, int64_t lda,
+                        int n_rows, int n, int row0, int p, double* obj, double* partials,
+                        int* counter, double* vf, cudaStream_t st);
+cudaError_t admm_launch(const double* V, int64_t ldv, const double* Vloc, int64_t ldvl,
+                        const double* f, double t, const uint32_t* adj, int64_t ldadj,
+                        const double* deg, double* Z, int64_t ldz, int n_rows, int n, int row0,
+                        int p, double* obj, double* partials, int* counter, int raw, double* vf,
+                        cudaStream_t st);
 cudaError_t sqrt_inplace_launch(double* x, cudaStream_t st);
 
 }  // namespace pf

@@ -6,7 +6,8 @@
 //                                Z+ = offdiag(W - tC) + Diag(1 - W_ii + Z_ii),  C = -L/4,
 //                                obj = {<C, W>, ||Z+ - Z||_F}
 // B200 design (DESIGN.md §4 K7):
-//  * 64 x 64 output tiles on fp64 DMMA (K = p), f folded into the A-fragment loads;
+//  * 64 x 64 output tiles on fp64 DMMA (K = p); the I panel is V diag(f) (scaled once per
+//    call by scale_cols_kernel), the J panel V;
 //  * single GPU (whole rows): only tiles I <= J are computed; the (J, I) tile is written as the
 //    transpose through shared memory -> n^2 p flops instead of 2 n^2 p, and the old iterate is
 //    read only on the upper half (PFAM; Z is symmetric by contract), none at all for PFPG;
@@ -23,8 +24,10 @@ namespace pf {
 constexpr int kRb = 64;  // tile edge; 4 warps (2 x 2), warp tile 32 x 32
 
 struct RbArgs {
-  const double* V;
+  const double* V;   // all n rows (J panels)
   int64_t ldv;
+  const double* VF;  // local rows of V diag(f) (I panels), pitch p
+
   const double* f;
   double tt;  // tau (PFPG) or t (PFAM)
   const uint32_t* bits;
@@ -70,7 +73,7 @@ __device__ __forceinline__ void pair_of(int e, int T, int& I, int& J) {
 }
 
 template <int P, bool PFPG>
-__global__ void __launch_bounds__(128) rebuild_kernel(const RbArgs a) {
+__global__ void __launch_bounds__(128, 3) rebuild_kernel(const RbArgs a) {
   using C = RbCfg<P, PFPG>;
   extern __shared__ __align__(16) double sm[];
   __shared__ double red[32];
@@ -84,28 +87,35 @@ __global__ void __launch_bounds__(128) rebuild_kernel(const RbArgs a) {
   double* Ts = sm;                  // 64 x 65 transpose staging (reuses the panels)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g8 = lane >> 2, t4 = lane & 3;
+  const int wm = warp & 1, wn = warp >> 1;
+  const int tc = (a.n + kRb - 1) / kRb, tr = (a.n_rows + kRb - 1) / kRb;
+  const int ntiles = a.sym ? (tc * (tc + 1)) / 2 : tr * tc;
+  for (int c = tid; c < P; c += 128) fs[c] = a.f[c];
+  double s0 = 0.0, s1 = 0.0;
+  // persistent CTAs: fixed strided tile assignment (deterministic sums), one reduction at the end
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
   int I, J;
   if (a.sym) {
-    pair_of(blockIdx.x, a.T, I, J);
+    pair_of(tile, a.T, I, J);
   } else {
-    I = blockIdx.y;
-    J = blockIdx.x;
+    I = tile / tc;
+    J = tile % tc;
   }
   const int i0 = I * kRb, j0 = J * kRb;  // local row tile start, global column tile start
   const bool mirror = a.sym && I < J;
   const double wgt = mirror ? 2.0 : 1.0;
+  __syncthreads();  // the previous tile's readers of the panels / staging tile are done
 
   // ---- stage V panels (cp.async 16 B), f, W panels
   for (int e = tid; e < kRb * (P / 2); e += 128) {
     const int rr = e / (P / 2), c = (e % (P / 2)) * 2;
     double* di = Vi + rr * C::LD + c;
     double* dj = Vj + rr * C::LD + c;
-    if (i0 + rr < a.n_rows) cp_async16(di, a.V + (size_t)(a.row0 + i0 + rr) * a.ldv + c);
+    if (i0 + rr < a.n_rows) cp_async16(di, a.VF + (size_t)(i0 + rr) * P + c);
     else *reinterpret_cast<double2*>(di) = make_double2(0.0, 0.0);
     if (j0 + rr < a.n) cp_async16(dj, a.V + (size_t)(j0 + rr) * a.ldv + c);
     else *reinterpret_cast<double2*>(dj) = make_double2(0.0, 0.0);
   }
-  for (int c = tid; c < P; c += 128) fs[c] = a.f[c];
   if (PFPG) {
     for (int e = tid; e < kRb * ldw_s; e += 128) {
       const int rr = e / ldw_s, c = e % ldw_s;
@@ -114,7 +124,6 @@ __global__ void __launch_bounds__(128) rebuild_kernel(const RbArgs a) {
     }
   }
 
-  const int wm = warp & 1, wn = warp >> 1;
   // ---- PFAM: prefetch the old iterate at this thread's fragment positions (overlaps the MMA)
   double zo[2][2][4][2];
   if (!PFPG) {
@@ -155,12 +164,11 @@ __global__ void __launch_bounds__(128) rebuild_kernel(const RbArgs a) {
 #pragma unroll 4
   for (int ks = 0; ks < P / 4; ++ks) {
     const int k = ks * 4 + t4;
-    const double fk = fs[k];
     double a0[2], a1[2], b0[4];
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
-      a0[mt] = Vi[(wm * 32 + mt * 16 + g8) * C::LD + k] * fk;
-      a1[mt] = Vi[(wm * 32 + mt * 16 + g8 + 8) * C::LD + k] * fk;
+      a0[mt] = Vi[(wm * 32 + mt * 16 + g8) * C::LD + k];
+      a1[mt] = Vi[(wm * 32 + mt * 16 + g8 + 8) * C::LD + k];
     }
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) b0[nt] = Vj[(wn * 32 + nt * 8 + g8) * C::LD + k];
@@ -197,7 +205,6 @@ __global__ void __launch_bounds__(128) rebuild_kernel(const RbArgs a) {
   if (mirror) __syncthreads();  // panels are about to be overwritten by the staging tile
 
   // ---- elementwise update + reductions
-  double s0 = 0.0, s1 = 0.0;
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -273,6 +280,8 @@ __global__ void __launch_bounds__(128) rebuild_kernel(const RbArgs a) {
     }
   }
 
+  }  // tile loop
+
   // ---- deterministic reduction: block tree, then the last CTA sums CTA partials in order
   s0 = block_sum(s0, red);
   s1 = block_sum(s1, red);
@@ -333,7 +342,13 @@ static cudaError_t rb_launch(RbArgs a, cudaStream_t st) {
   const int tr = (a.n_rows + kRb - 1) / kRb, tc = (a.n + kRb - 1) / kRb;
   a.sym = (a.row0 == 0 && a.n_rows == a.n) ? 1 : 0;
   a.T = tc;
-  dim3 grid = a.sym ? dim3((unsigned)((long long)tc * (tc + 1) / 2), 1) : dim3(tc, tr);
+  const long long ntiles = a.sym ? (long long)tc * (tc + 1) / 2 : (long long)tr * tc;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rebuild_kernel<P, PFPG>, 128, smem);
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  dim3 grid((unsigned)std::max<long long>(1, std::min<long long>(ntiles, (long long)std::max(per_sm, 1) * sms)));
   count_launch();
   rebuild_kernel<P, PFPG><<<grid, 128, smem, st>>>(a);
   return cudaGetLastError();
@@ -350,20 +365,47 @@ static cudaError_t rb_dispatch(int p, const RbArgs& a, cudaStream_t st) {
   }
 }
 
-cudaError_t prox_launch(const double* V, int64_t ldv, const double* f, double tau,
-                        const uint32_t* omega, int64_t ldo, const double* W, int64_t ldw, int r,
-                        double* Aout, int64_t lda, int n_rows, int n, int row0, int p,
-                        double* obj, double* partials, int* counter, cudaStream_t st) {
-  RbArgs a{V, ldv, f, tau, omega, ldo, W, ldw, r, 0, nullptr, Aout, lda, n_rows, n, row0,
+__global__ void scale_cols_kernel(const double* __restrict__ V, int64_t ldv,
+                                  const double* __restrict__ f, int n_rows, int p,
+                                  double* __restrict__ out) {
+  // p is a multiple of 16: each thread scales 2 adjacent columns of one row (no 64-bit division)
+  const int half = p >> 1;
+  for (int i = blockIdx.x; i < n_rows; i += gridDim.x)
+    for (int c2 = threadIdx.x; c2 < half; c2 += blockDim.x) {
+      const int c = 2 * c2;
+      const double2 v = *reinterpret_cast<const double2*>(V + (size_t)i * ldv + c);
+      *reinterpret_cast<double2*>(out + (size_t)i * p + c) = make_double2(v.x * f[c], v.y * f[c + 1]);
+    }
+}
+
+static cudaError_t scale_cols(const double* V, int64_t ldv, const double* f, int n_rows, int p,
+                              double* out, cudaStream_t st) {
+  count_launch();
+  scale_cols_kernel<<<std::max(1, std::min(n_rows, 16 * 148)), std::max(32, p / 2), 0, st>>>(
+      V, ldv, f, n_rows, p, out);
+  return cudaGetLastError();
+}
+
+cudaError_t prox_launch(const double* V, int64_t ldv, const double* Vloc, int64_t ldvl,
+                        const double* f, double tau, const uint32_t* omega, int64_t ldo,
+                        const double* W, int64_t ldw, int r, double* Aout, int64_t lda,
+                        int n_rows, int n, int row0, int p, double* obj, double* partials,
+                        int* counter, double* vf, cudaStream_t st) {
+  cudaError_t e = scale_cols(Vloc, ldvl, f, n_rows, p, vf, st);
+  if (e != cudaSuccess) return e;
+  RbArgs a{V, ldv, vf, f, tau, omega, ldo, W, ldw, r, 0, nullptr, Aout, lda, n_rows, n, row0,
            0, 0, 0, partials, counter, obj};
   return rb_dispatch<true>(p, a, st);
 }
 
-cudaError_t admm_launch(const double* V, int64_t ldv, const double* f, double t,
-                        const uint32_t* adj, int64_t ldadj, const double* deg, double* Z,
-                        int64_t ldz, int n_rows, int n, int row0, int p, double* obj,
-                        double* partials, int* counter, int raw, cudaStream_t st) {
-  RbArgs a{V, ldv, f, t, adj, ldadj, nullptr, 0, 0, 0, deg, Z, ldz, n_rows, n, row0,
+cudaError_t admm_launch(const double* V, int64_t ldv, const double* Vloc, int64_t ldvl,
+                        const double* f, double t, const uint32_t* adj, int64_t ldadj,
+                        const double* deg, double* Z, int64_t ldz, int n_rows, int n, int row0,
+                        int p, double* obj, double* partials, int* counter, int raw, double* vf,
+                        cudaStream_t st) {
+  cudaError_t e = scale_cols(Vloc, ldvl, f, n_rows, p, vf, st);
+  if (e != cudaSuccess) return e;
+  RbArgs a{V, ldv, vf, f, t, adj, ldadj, nullptr, 0, 0, 0, deg, Z, ldz, n_rows, n, row0,
            0, 0, raw, partials, counter, obj};
   return rb_dispatch<false>(p, a, st);
 }
