@@ -23,7 +23,8 @@ template <int P>
 struct GemmCfg {
   // 9 warps per CTA -> one SMSP hosts 3 warps -> <= 168 registers per thread (16K regs/SMSP),
   // so every warp tile is kept at <= 32 x 32 doubles of accumulator: BM = 64 for P = 128.
-  static constexpr int BM = (P >= 128) ? 64 : 128, BK = 16;
+  // BK = 32: two 16-column SWIZZLE_128B A sub-tiles per stage (8 k4-steps between barriers)
+  static constexpr int BM = (P >= 128) ? 64 : 128, BK = 32;
   static constexpr int NCW = 8;  // consumer warps
   static constexpr int NCT = NCW * 32;
   static constexpr int THREADS = NCT + 32;
@@ -105,10 +106,13 @@ __global__ void __launch_bounds__(GemmCfg<P>::THREADS, 1)
         mbar_wait(&empty[stage], phase ^ 1u);
         mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
         tma_load_2d(sA + stage * (C::BM * C::BK), &mapA, &full[stage], kb * C::BK, tile * C::BM);
-        // B = Y_j rows [kb*16, kb*16+16): P/8 boxes of 16 x 8 doubles, SWIZZLE_64B each
+        tma_load_2d(sA + stage * (C::BM * C::BK) + C::BM * 16, &mapA, &full[stage], kb * C::BK + 16,
+                    tile * C::BM);
+        // B = Y_j rows [kb*BK, (kb+1)*BK): P/8 boxes of BK x 8 doubles, SWIZZLE_64B each
 #pragma unroll
         for (int j = 0; j < P / 8; ++j)
-          tma_load_2d(sB + stage * (C::BK * P) + j * 128, &mapB, &full[stage], 8 * j, kb * C::BK);
+          tma_load_2d(sB + stage * (C::BK * P) + j * (C::BK * 8), &mapB, &full[stage], 8 * j,
+                      kb * C::BK);
         if (++stage == C::STAGES) {
           stage = 0;
           phase ^= 1u;
@@ -137,13 +141,14 @@ __global__ void __launch_bounds__(GemmCfg<P>::THREADS, 1)
       a_off[mt][ks] = r * 16 + ((((k >> 1) ^ (r & 7))) << 1) + (k & 1);
     }
   }
-  // B stage = P/8 boxes [16 k][8 n] with SWIZZLE_64B (16-byte chunk ^= (k >> 1) & 3):
-  // element (k, n): (n >> 3) * 128 + k * 8 + ((((n & 7) >> 1) ^ ((k >> 1) & 3)) << 1) + (n & 1)
-  int b_off[4];
+  // B stage = P/8 boxes [BK k][8 n] with SWIZZLE_64B (16-byte chunk ^= (k >> 1) & 3):
+  // element (k, n): (n >> 3) * 8 BK + k * 8 + ((((n & 7) >> 1) ^ ((k >> 1) & 3)) << 1) + (n & 1)
+  int b_off[C::BK / 4];
 #pragma unroll
-  for (int ks = 0; ks < 4; ++ks) {
+  for (int ks = 0; ks < C::BK / 4; ++ks) {
     const int k = ks * 4 + t4;
-    b_off[ks] = ((wn * C::WN) >> 3) * 128 + k * 8 + ((((g8 >> 1) ^ ((k >> 1) & 3))) << 1) + (g8 & 1);
+    b_off[ks] = ((wn * C::WN) >> 3) * (C::BK * 8) + k * 8 +
+                ((((g8 >> 1) ^ ((k >> 1) & 3))) << 1) + (g8 & 1);
   }
 
   long long it = it_begin;
@@ -166,15 +171,16 @@ __global__ void __launch_bounds__(GemmCfg<P>::THREADS, 1)
       const double* a = sA + stage * (C::BM * C::BK);
       const double* b = sB + stage * (C::BK * P);
 #pragma unroll
-      for (int ks = 0; ks < 4; ++ks) {
+      for (int ks = 0; ks < C::BK / 4; ++ks) {
         double af[C::MT][2], bf[C::NT];
+        const int sub = (ks >> 2) * (C::BM * 16);  // A sub-tile of this k-step
 #pragma unroll
         for (int mt = 0; mt < C::MT; ++mt) {
-          af[mt][0] = a[a_off[mt][ks]];
-          af[mt][1] = a[a_off[mt][ks] + 8 * 16];
+          af[mt][0] = a[sub + a_off[mt][ks & 3]];
+          af[mt][1] = a[sub + a_off[mt][ks & 3] + 8 * 16];
         }
 #pragma unroll
-        for (int nt = 0; nt < C::NT; ++nt) bf[nt] = b[b_off[ks] + nt * 128];
+        for (int nt = 0; nt < C::NT; ++nt) bf[nt] = b[b_off[ks] + nt * (C::BK * 8)];
 #pragma unroll
         for (int mt = 0; mt < C::MT; ++mt)
 #pragma unroll
@@ -307,7 +313,7 @@ bool encode_map_B(CUtensorMap* map, const double* B, int p, int n_k) {
   if (!enc) return false;
   cuuint64_t dims[2] = {(cuuint64_t)p, (cuuint64_t)n_k};
   cuuint64_t strides[1] = {(cuuint64_t)p * 8};
-  cuuint32_t box[2] = {8, 16};
+  cuuint32_t box[2] = {8, 32};
   cuuint32_t es[2] = {1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(B), dims, strides, box,
              es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
@@ -326,7 +332,7 @@ ChebGemmPlan cheb_gemm_plan(int p, int n_rows, int n_k, int num_sms) {
   pl.n_k = n_k;
   const int bm = (p >= 128) ? 64 : 128;
   pl.mtiles = (n_rows + bm - 1) / bm;
-  pl.kblocks = (n_k + 15) / 16;
+  pl.kblocks = (n_k + 31) / 32;
   const long long T = (long long)pl.mtiles * pl.kblocks;
   // at least 8 k-blocks per CTA so the fixup stays amortised
   long long g = std::min<long long>(num_sms, std::max<long long>(1, T / 8));
