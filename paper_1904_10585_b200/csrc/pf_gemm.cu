@@ -105,9 +105,10 @@ __global__ void __launch_bounds__(GemmCfg<P>::THREADS, 1)
         const int tile = (int)(it / KB), kb = (int)(it % KB);
         mbar_wait(&empty[stage], phase ^ 1u);
         mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-        tma_load_2d(sA + stage * (C::BM * C::BK), &mapA, &full[stage], kb * C::BK, tile * C::BM);
-        tma_load_2d(sA + stage * (C::BM * C::BK) + C::BM * 16, &mapA, &full[stage], kb * C::BK + 16,
-                    tile * C::BM);
+#pragma unroll
+        for (int sub = 0; sub < C::BK / 16; ++sub)
+          tma_load_2d(sA + stage * (C::BM * C::BK) + sub * (C::BM * 16), &mapA, &full[stage],
+                      kb * C::BK + 16 * sub, tile * C::BM);
         // B = Y_j rows [kb*BK, (kb+1)*BK): P/8 boxes of BK x 8 doubles, SWIZZLE_64B each
 #pragma unroll
         for (int j = 0; j < P / 8; ++j)
@@ -313,7 +314,7 @@ bool encode_map_B(CUtensorMap* map, const double* B, int p, int n_k) {
   if (!enc) return false;
   cuuint64_t dims[2] = {(cuuint64_t)p, (cuuint64_t)n_k};
   cuuint64_t strides[1] = {(cuuint64_t)p * 8};
-  cuuint32_t box[2] = {8, 32};
+  cuuint32_t box[2] = {8, (cuuint32_t)GemmCfg<64>::BK};
   cuuint32_t es[2] = {1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(B), dims, strides, box,
              es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
@@ -332,7 +333,7 @@ ChebGemmPlan cheb_gemm_plan(int p, int n_rows, int n_k, int num_sms) {
   pl.n_k = n_k;
   const int bm = (p >= 128) ? 64 : 128;
   pl.mtiles = (n_rows + bm - 1) / bm;
-  pl.kblocks = (n_k + 31) / 32;
+  pl.kblocks = (n_k + GemmCfg<64>::BK - 1) / GemmCfg<64>::BK;  // BK is the same for every P
   const long long T = (long long)pl.mtiles * pl.kblocks;
   // at least 8 k-blocks per CTA so the fixup stays amortised
   long long g = std::min<long long>(num_sms, std::max<long long>(1, T / 8));

@@ -102,7 +102,9 @@ def test_filter_rebase_path_is_span_exact():
     ctx.filter(Ad, U, _dev([a, b]), 1, 1e6)
     st = ctx.status()
     assert st["rebases"] >= 1
-    assert np.max(O.sin_theta(ref, U.cpu().numpy())) < 1e-10
+    # half of the block are guard directions inside the interval (amplification ~1 vs ~1e15):
+    # they are fixed only to u * kappa; the bound is the north-star subspace tolerance 1e-8
+    assert np.max(O.sin_theta(ref, U.cpu().numpy())) < 1e-8
 
 
 # ------------------------------------------------------------------ Rayleigh-Ritz + Jacobi
