@@ -513,7 +513,10 @@ pf_status pf_rayleigh_ritz(pf_ctx ctx, const double* A, int64_t lda, const doubl
   PF_CU(cudaMemcpy2DAsync(ctx->Y[0], row, U, ldu * 8, row, nl, cudaMemcpyDeviceToDevice, st));
   PF_TRY(gemm_step(ctx, 0, ctx->Y[0], ctx->Y[0], ctx->Wbuf, &ctx->state->coef_rr[0], st));
   PF_TRY(gram_all(ctx, ctx->Y[0], ctx->Wbuf, ctx->G, nullptr, st));  // H = Q^T (A Q)
-  PF_CU(jacobi_launch(ctx->G, p, nullptr, theta, ctx->Yeig, ctx->state, 1e-15, 40, st));
+  // stop once off(H) <= p * 1e-16 ||H||_F: the rotation threshold leaves every off-diagonal entry
+  // below 1e-16 ||H||_F, so this is reached without a final rotation-free confirmation sweep
+  PF_CU(jacobi_launch(ctx->G, p, nullptr, theta, ctx->Yeig, ctx->state,
+                      std::max(1e-15, 1e-16 * p), 40, st));
   PF_CU(copy_theta_launch(theta, p, ctx->state, st));
   PF_CU(rmul_launch(ctx->Y[0], p, ctx->Yeig, V, ldv, nl, p, nullptr, st));
   return PF_OK;
