@@ -321,6 +321,22 @@ bool encode_map_B(CUtensorMap* map, const double* B, int p, int n_k) {
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// fp32 2-D map for the TF32 filter GEMM: rows x cols (cols contiguous, pitch in elements),
+// box = box_cols (16 -> 64 bytes, SWIZZLE_64B) x box_rows; unswizzled boxes are L2 prefetches.
+bool encode_map_f32(CUtensorMap* map, const float* base, int64_t pitch, int rows, int cols,
+                    int box_rows, int box_cols, bool swizzle) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)pitch * 4};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
+             box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             swizzle ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int P>
 static size_t ws_per_cta() {
   return (size_t)2 * GemmCfg<P>::NCT * GemmCfg<P>::NACC;

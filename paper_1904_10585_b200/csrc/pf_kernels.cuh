@@ -29,6 +29,28 @@ cudaError_t cheb_gemm_launch(const ChebGemmPlan& pl, const CUtensorMap& mapA,
                              double* out, const double* coef, double* ws, int* counters,
                              cudaStream_t st);
 
+// ---- fp32-storage filter GEMM on tcgen05 TF32 tensor cores (pf_gemm_tf32.cu).  Blocks are
+// p-major (transposed): element (i, c) of an n x p block at Y[c * ldy + i].
+struct Tf32Plan {
+  int p;
+  int n_rows, n_k;
+  int mtiles, kblocks;  // 256-row pair tiles, 16-wide k-blocks
+  int pairs;            // launched CTA pairs
+  int split;            // K-split of the leftover (tail) tiles
+  size_t ws_floats;     // partial workspace
+  size_t counters;      // tile counters (ints)
+};
+Tf32Plan tf32_plan(int p, int n_rows, int n_k, int num_sms);
+// map: 16 x 128 SWIZZLE_64B load boxes; map_pf: 32 x 128 L2-prefetch boxes
+bool tf32_encode_A(CUtensorMap* map, CUtensorMap* map_pf, const float* A, int64_t lda,
+                   int n_rows, int n_k);
+bool tf32_encode_B(CUtensorMap* map, const float* Yt, int64_t ldy, int p, int n_k);
+cudaError_t tf32_gemm_launch(const Tf32Plan& pl, const CUtensorMap& mapA, const CUtensorMap& mapB,
+                             const CUtensorMap& mapApf,
+                             const float* ycur, const float* yprev, float* out, int64_t ldy,
+                             const double* coef, float* ws, int* counters, int npass,
+                             cudaStream_t st);
+
 // ---- small dense kernels (pf_small.cu); all p x p objects are row-major, ld = p
 // G = X^T Y over rows [0, n_rows) (X, Y: n_rows x p, ld p).  Deterministic two-level sum:
 // per-CTA partials then the last CTA reduces in CTA order.  If `cond` != NULL the kernel is a
