@@ -33,7 +33,7 @@ import math
 import numpy as np
 
 from pfinputs import (Config, initial_block, lanczos_start, cfg1_problem, cfg1_noise,
-                      pfpg_problem, pfam_problem, unpack_bitmask)
+                      pfpg_problem, pfam_problem, unpack_bitmask, cfg5_problem, cfg5_perturb)
 
 __all__ = [
     "cheb_T", "growth_lower_bound", "interval_map", "interval_psd", "interval_top_r",
@@ -330,8 +330,13 @@ def run(cfg: Config, iters: int | None = None, record_factors: bool = True,
     """
     K = cfg.iters if iters is None else iters
     U = orth(initial_block(cfg))
-    M = omega = C = None
-    if cfg.mode in ("sweep_psd", "sweep_soft"):
+    M = omega = C = A32 = None
+    if cfg.mode in ("sweep_psd", "sweep_soft") and cfg.gen == "cfg5":
+        # config 5 stores the iterate in fp32 (BASELINE configs[4]); the oracle computes in fp64
+        # on exactly those fp32 values, and the workload's noise update is the fp32 add
+        A32 = cfg5_problem(cfg) if problem is None else np.array(problem["A0"], dtype=np.float32)
+        A = A32.astype(np.float64)
+    elif cfg.mode in ("sweep_psd", "sweep_soft"):
         A = cfg1_problem(cfg) if problem is None else problem["A0"]
     elif cfg.mode == "pfpg":
         prob = pfpg_problem(cfg) if problem is None else problem
@@ -372,7 +377,10 @@ def run(cfg: Config, iters: int | None = None, record_factors: bool = True,
             rec["V"], rec["f"] = V[:, keep], f[keep]
         # a6
         if cfg.mode in ("sweep_psd", "sweep_soft"):
-            if k + 1 < K:
+            if k + 1 < K and A32 is not None:
+                cfg5_perturb(cfg, A32, k)                         # A_{k+1} = fl32(A_k + E_k)
+                A = A32.astype(np.float64)
+            elif k + 1 < K:
                 A = A + cfg1_noise(cfg, k)
         elif cfg.mode == "pfpg":
             A, fit = pfpg_next(V[:, keep], f[keep], omega, M, cfg.tau)

@@ -11,6 +11,13 @@ oracle and the GPU path see bit-identical inputs.  Stream ids:
     6  ground-truth factor W (M = W W^T) for configs 2/4
     7  sampling mask Omega for configs 2/4
     8  Erdos-Renyi edges for config 3
+    9  config-5 spectrum (large eigenvalues, semicircle bulk, positions)
+   10  config-5 Householder vectors
+
+Config-5 noise is NOT drawn from a numpy stream: at n = 65536 it is 2^31 Gaussians per
+iteration, generated on the device by the library's workload helper.  Both sides implement the
+same counter-based generator (`hash_gauss` below, pf_perturb_hash in libpf): entry (i, j) of
+E_k depends only on (seed, k, min(i,j), max(i,j)).
 
 Masks (Omega, graph adjacency) are delivered as a packed row-major bitmask of uint32
 words: bit (j & 31) of word [i, j >> 5] is entry (i, j); row stride = ceil(n/32) words.
@@ -50,8 +57,11 @@ class Config:
     # PFAM (config 3): max-cut SDP on G(n, edge_prob)
     edge_prob: float = 0.0
     t: float = 1.0
-    # config 5 soft threshold (reading R11)
+    # config 5 soft threshold (reading R11) and workload shape
     theta: float = 3.0
+    gen: str = "cfg1"         # sweep workload: "cfg1" (Haar basis) | "cfg5" (Householder basis)
+    nbig: int = 256           # config 5: eigenvalues drawn from U[5, 50]
+    nrefl: int = 64           # config 5: Householder reflectors in the basis
 
 
 CONFIGS = {
@@ -63,7 +73,7 @@ CONFIGS = {
     4: Config("cfg4_pfpg_n32768", n=32768, p=128, d=10, iters=100, mode="pfpg",
               r=50, omega_prob=0.05),
     5: Config("cfg5_soft_sweep_n65536", n=65536, p=512, d=8, iters=30, mode="sweep_soft",
-              dtype="tf32", rho_max=1e3),
+              dtype="tf32", rho_max=1e3, gen="cfg5"),
 }
 
 
@@ -194,3 +204,129 @@ def pfam_problem(cfg: Config) -> dict:
     for i0 in range(0, n, chunk):
         deg[i0:i0 + chunk] = unpack_bitmask(adj[i0:i0 + chunk], n).sum(axis=1)
     return {"adj_bits": adj, "deg": deg, "t": cfg.t}
+
+
+# ----------------------------------------------------------------------------- config 5
+def cfg5_spectrum(cfg: Config) -> np.ndarray:
+    """lambda: nbig entries U[5, 50] and n - nbig from the Wigner semicircle on [-1, 1]
+    (x = sqrt(u1) cos(2 pi u2): the abscissa of a uniform point of the unit disk), placed at
+    seeded random positions (BASELINE.json configs[4]; reading R16)."""
+    n, nb = cfg.n, min(cfg.nbig, cfg.n)
+    rs = _rng(cfg.seed, 9)
+    big = rs.uniform(5.0, 50.0, nb)
+    u1 = rs.random(n - nb)
+    u2 = rs.random(n - nb)
+    bulk = np.sqrt(u1) * np.cos(2.0 * np.pi * u2)
+    lam = np.concatenate([big, bulk])
+    return lam[rs.permutation(n)]
+
+
+def cfg5_reflectors(cfg: Config) -> tuple[np.ndarray, np.ndarray]:
+    """Q = H_1 H_2 ... H_m, H_i = I - 2 v_i v_i^T, v_i = w_i / |w_i|, w_i iid N(0, I_n), in the
+    compact WY form Q = I - V T V^T (T upper triangular): appending H_j to Q_{j-1} =
+    I - V T V^T gives T' = [[T, -2 T V^T v_j], [0, 2]].  Returns (V, T)."""
+    n, m = cfg.n, cfg.nrefl
+    W = _rng(cfg.seed, 10).standard_normal((n, m))
+    V = W / np.linalg.norm(W, axis=0)[None, :]
+    T = np.zeros((m, m))
+    for j in range(m):
+        T[j, j] = 2.0
+        if j:
+            T[:j, j] = -2.0 * T[:j, :j] @ (V[:, :j].T @ V[:, j])
+    return V, T
+
+
+def cfg5_basis_columns(V: np.ndarray, T: np.ndarray, idx: np.ndarray) -> np.ndarray:
+    """Columns idx of Q = I - V T V^T (n x len(idx))."""
+    n = V.shape[0]
+    cols = -(V @ (T @ V[idx].T))
+    cols[idx, np.arange(len(idx))] += 1.0
+    return cols
+
+
+class Cfg5Matrix:
+    """A_0 = Q diag(lambda) Q^T for config 5, formed row block by row block in fp64 from the
+    compact WY factors: A_0 = Lam - V T P^T - P T^T V^T + V (T V^T P T^T) V^T with P = Lam V."""
+
+    def __init__(self, cfg: Config):
+        self.n = cfg.n
+        self.lam = cfg5_spectrum(cfg)
+        self.V, self.T = cfg5_reflectors(cfg)
+        self.P = self.lam[:, None] * self.V
+        self.K = self.T @ (self.V.T @ self.P) @ self.T.T
+        self.VT_T = self.V @ self.T            # n x m
+        self.P_Tt = self.P @ self.T.T          # n x m
+
+    def rows(self, i0: int, i1: int, j0: int = 0) -> np.ndarray:
+        """fp64 entries [i0, i1) x [j0, n) of A_0."""
+        V, P = self.V[j0:], self.P[j0:]
+        out = -(self.VT_T[i0:i1] @ P.T) - (self.P_Tt[i0:i1] @ V.T) + (self.V[i0:i1] @ self.K) @ V.T
+        r = np.arange(i0, i1)
+        on = (r >= j0)
+        out[np.arange(i1 - i0)[on], r[on] - j0] += self.lam[i0:i1][on]
+        return out
+
+
+def cfg5_problem(cfg: Config, chunk: int = 2048) -> np.ndarray:
+    """A_0 rounded once to fp32 (the stored iterate of config 5), n x n float32.  The upper
+    triangle (fp64 rows rounded to fp32) defines the matrix; the lower triangle is its exact
+    mirror, so the stored matrix is exactly symmetric."""
+    M = Cfg5Matrix(cfg)
+    n = cfg.n
+    A = np.empty((n, n), dtype=np.float32)
+    for i0 in range(0, n, chunk):
+        i1 = min(n, i0 + chunk)
+        A[i0:i1, i0:] = M.rows(i0, i1, i0)
+        blk = A[i0:i1, i0:i1]
+        lower = np.tril_indices(i1 - i0, -1)
+        blk[lower] = blk.T[lower]
+        if i0:
+            A[i0:i1, :i0] = A[:i0, i0:i1].T
+    return A
+
+
+_M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def _mix64(x: np.ndarray) -> np.ndarray:
+    """splitmix64 step on uint64 arrays (wrapping arithmetic)."""
+    with np.errstate(over="ignore"):
+        x = x + np.uint64(0x9E3779B97F4A7C15)
+        x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return x ^ (x >> np.uint64(31))
+
+
+def hash_gauss(seed: int, k: int, i: np.ndarray, j: np.ndarray) -> np.ndarray:
+    """Counter-based N(0,1) for the symmetric pair {i, j} of noise draw k:
+    c = min(i,j) * 2^32 + max(i,j); z1 = mix(c ^ mix(seed * 2^32 + k)); z2 = mix(z1);
+    u1 = ((z1 >> 11) + 1) 2^-53 in (0, 1], u2 = (z2 >> 11) 2^-53; g = sqrt(-2 ln u1) cos(2 pi u2)
+    (Box-Muller), all in fp64.  pf_perturb_hash implements the same function."""
+    lo = np.minimum(i, j).astype(np.uint64)
+    hi = np.maximum(i, j).astype(np.uint64)
+    key = _mix64(np.uint64(seed) * np.uint64(1 << 32) + np.uint64(k))
+    z1 = _mix64(((lo << np.uint64(32)) | hi) ^ key)
+    z2 = _mix64(z1)
+    u1 = ((z1 >> np.uint64(11)) + np.uint64(1)).astype(np.float64) * (2.0 ** -53)
+    u2 = (z2 >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
+    return np.sqrt(-2.0 * np.log(u1)) * np.cos((2.0 * np.pi) * u2)
+
+
+def cfg5_noise_rows(cfg: Config, k: int, i0: int, i1: int) -> np.ndarray:
+    """Rows [i0, i1) of E_k in fp32: E_ij = fl32(noise * g_ij * s_ij), s = 1 on the diagonal and
+    1/sqrt(2) off it -- the law of noise * (G + G^T)/2 with G iid N(0,1) ("1e-3 Gaussian
+    symmetric noise", BASELINE.json configs[4]).  The product is evaluated as
+    (noise * g) * s in fp64, then rounded once to fp32."""
+    rows = np.arange(i0, i1)[:, None]
+    cols = np.arange(cfg.n)[None, :]
+    g = hash_gauss(cfg.seed, k, rows, cols)
+    e = cfg.noise * g
+    e = np.where(rows == cols, e, e * 0.7071067811865476)
+    return e.astype(np.float32)
+
+
+def cfg5_perturb(cfg: Config, A32: np.ndarray, k: int, chunk: int = 1024) -> None:
+    """In place: A_{k+1} = fl32(A_k + E_k) (fp32 add, round to nearest) on an fp32 array."""
+    for i0 in range(0, cfg.n, chunk):
+        i1 = min(cfg.n, i0 + chunk)
+        A32[i0:i1] += cfg5_noise_rows(cfg, k, i0, i1)

@@ -383,3 +383,22 @@ def test_lowrank_diff_fro_brute_force():
     assert O.lowrank_diff_fro(V1, f1, V2, f2) == pytest.approx(ref, rel=1e-13)
     assert O.lowrank_fro(V1, f1) == pytest.approx(np.linalg.norm((V1 * f1) @ V1.T), rel=1e-13)
     assert O.lowrank_diff_fro(V1, f1, V1, f1) < 1e-12
+
+
+def test_config5_k0_closed_form():
+    """Config-5 sweep at k = 0 against the closed form: A_0 = Q diag(lambda) Q^T with Q and
+    lambda known from the generator, so the exact soft threshold is
+    Q[:, big] diag(sign(l)(|l| - theta)) Q[:, big]^T.  The oracle runs on the fp32-rounded A_0
+    (relative perturbation ~1e-7) and must land within 1e-6 of it; a wrong interval, recurrence
+    coefficient or shrink sign fails this."""
+    from pfinputs import cfg5_spectrum, cfg5_reflectors, cfg5_basis_columns
+    cfg = reduced(CONFIGS[5], n=640, p=48, nbig=20, nrefl=12, iters=1)
+    r = O.run(cfg)["records"][0]
+    lam = cfg5_spectrum(cfg)
+    V, T = cfg5_reflectors(cfg)
+    big = np.where(np.abs(lam) > cfg.theta)[0]
+    Qb = cfg5_basis_columns(V, T, big)
+    fex = np.sign(lam[big]) * (np.abs(lam[big]) - cfg.theta)
+    assert r["rank"] == len(big) == 20
+    err = O.lowrank_diff_fro(r["V"], r["f"], Qb, fex) / O.lowrank_fro(Qb, fex)
+    assert err < 1e-6, err
