@@ -4,10 +4,17 @@
  * source with the equation label; DESIGN.md lists the readings R1..R14.
  *
  * Conventions (all entry points)
- *  - Every matrix argument is a DEVICE pointer to fp64 data, ROW-MAJOR, with leading dimension
- *    (elements between consecutive rows) given next to it.  ld must be >= the row length, even
- *    (TMA needs 16-byte row pitch) and the base 16-byte aligned.
- *  - n is the matrix order, p the block width (p % 8 == 0, 8 <= p <= 128, p <= n).
+ *  - The context's dtype fixes the storage of the n-row objects:
+ *      PF_FP64: A/Z and the blocks U, V are fp64 ROW-MAJOR (block element (i, c) at U[i*ldu + c]);
+ *               ld even (16-byte TMA row pitch), base 16-byte aligned; p in {16, 32, 64, 128}.
+ *      PF_TF32: A is fp32 ROW-MAJOR (lda % 4 == 0, base 16-byte aligned) and the blocks U, V are
+ *               fp32 P-MAJOR: block element (i, c) at U[c*ldu + i], ldu >= n_local (the block's
+ *               transpose, row-major); p in {64, 128, 256, 512}.  The filter GEMM runs on the
+ *               tcgen05 TF32 tensor cores in 3xTF32 (hi/lo split, fp32 accumulation); Gram, H and
+ *               every p x p object are fp64.  BASELINE configs[4] ("fp32/TF32").
+ *    Every matrix argument is a DEVICE pointer with its leading dimension (elements between
+ *    consecutive rows of the stored array) given next to it.
+ *  - n is the matrix order, p the block width (p <= n).
  *  - With world > 1 (pf_create_dist) rank g owns rows [row0, row0 + n_local) of every n-row
  *    object (A, Z, U, V) where row0 = g*n/world (integer division); those row blocks are what
  *    the caller passes.  Small objects (theta, f, rank, obj, interval) are replicated.
@@ -31,7 +38,11 @@ extern "C" {
 typedef struct pf_ctx_s* pf_ctx;
 typedef void* pf_stream; /* a cudaStream_t; NULL = legacy default stream */
 
-typedef enum { PF_FP64 = 0 } pf_dtype; /* fp64 storage + fp64 DMMA tensor cores */
+typedef enum {
+  PF_FP64 = 0, /* fp64 storage + fp64 DMMA tensor cores (mma.sync .f64)                    */
+  PF_FP32 = 1, /* reserved (plain fp32 SIMT filter): not built, PF_ERR_UNSUPPORTED          */
+  PF_TF32 = 2  /* fp32 storage, tcgen05 kind::tf32 filter GEMM (3xTF32), fp64 small objects */
+} pf_dtype;
 
 typedef enum { PF_OP_PSD = 0, PF_OP_SOFT_THRESHOLD = 1 } pf_op;
 
@@ -89,7 +100,7 @@ pf_status pf_get_device_status(pf_ctx ctx, pf_stream stream, uint32_t* flags, in
  * writes lo_hi[0] = theta_min - |r_min|, lo_hi[1] = theta_max + |r_max| (device double[2]),
  * and remembers them in the context.  v0: device start vector (n_local entries, any norm).
  * 1 <= m <= 64. */
-pf_status pf_lanczos(pf_ctx ctx, const double* A, int64_t lda, const double* v0, int32_t m,
+pf_status pf_lanczos(pf_ctx ctx, const void* A, int64_t lda, const double* v0, int32_t m,
                      double* lo_hi, pf_stream stream);
 
 /* PSD / all-positive interval: a = lo_hi[0], b = eta * a.  Writes interval[2]. */
@@ -108,17 +119,17 @@ pf_status pf_interval_soft(pf_ctx ctx, double thr, double eta, double* interval,
  * orth = CholeskyQR2 with a shifted CholeskyQR3 fallback ("a single QR" -> any
  * span-exact orthonormalisation).  A: n_local x n (lda), U: n_local x p (ldu), in place.
  * interval: device double[2] {a, b}.  1 <= q <= 10. */
-pf_status pf_filter(pf_ctx ctx, const double* A, int64_t lda, double* U, int64_t ldu,
+pf_status pf_filter(pf_ctx ctx, const void* A, int64_t lda, void* U, int64_t ldu,
                     const double* interval, int32_t q, double rho_max, pf_stream stream);
 
 /* U <- orth(U) (CholeskyQR2 + shifted fallback).  U: n_local x p. */
-pf_status pf_orth(pf_ctx ctx, double* U, int64_t ldu, pf_stream stream);
+pf_status pf_orth(pf_ctx ctx, void* U, int64_t ldu, pf_stream stream);
 
 /* Rayleigh-Ritz (eqn:RR P:269-286): H = U^T A U (symmetrised), H = Y Lambda Y^T by an on-device
  * parallel cyclic Jacobi, theta = Ritz values DESCENDING (device double[p]), V = U Y
  * (n_local x p, ldv).  U must be orthonormal (output of pf_filter / pf_orth). */
-pf_status pf_rayleigh_ritz(pf_ctx ctx, const double* A, int64_t lda, const double* U,
-                           int64_t ldu, double* V, int64_t ldv, double* theta, pf_stream stream);
+pf_status pf_rayleigh_ritz(pf_ctx ctx, const void* A, int64_t lda, const void* U,
+                           int64_t ldu, void* V, int64_t ldv, double* theta, pf_stream stream);
 
 /* Spectral operator on the Ritz values: PSD f = max(theta, 0) or soft threshold
  * f = sign(theta) max(|theta| - thr, 0) (shrink).  f: device double[p];
@@ -161,9 +172,21 @@ long long pf_kernel_launches(void);
  * diag[1] = Lanczos steps of the last refresh. */
 pf_status pf_diagnostics(pf_ctx ctx, pf_stream stream, double* diag /* [2] */);
 
-/* Workload helper (not the method): A <- A + E (config 1 noise, BASELINE configs[0]). */
+/* Workload helper (not the method): A <- A + E (config 1 noise, BASELINE configs[0]).
+ * PF_FP64 contexts only. */
 pf_status pf_perturb(pf_ctx ctx, double* A, int64_t lda, const double* E, int64_t lde,
                      pf_stream stream);
+
+/* Workload helper (not the method), PF_TF32 contexts: config-5 noise (BASELINE configs[4])
+ * A_ij <- fl32(A_ij + fl32((noise * g) * s)), s = 1 on the diagonal, 1/sqrt(2) off it, and
+ * g = Box-Muller N(0,1) from the counter-based hash of (seed, k, min(i,j), max(i,j)) --
+ * the same function as pfinputs.generators.hash_gauss.  Local rows of A (n_local x n, fp32). */
+pf_status pf_perturb_hash(pf_ctx ctx, float* A, int64_t lda, uint64_t seed, int32_t k,
+                          double noise, pf_stream stream);
+
+/* Number of TF32 MMA passes of the filter GEMM (PF_TF32 contexts): 3 (default, 3xTF32: error
+ * ~ fp32) or 1 (plain TF32, operator rounded to 10 mantissa bits).  PF_ERR_ARG otherwise. */
+pf_status pf_set_tf32_passes(pf_ctx ctx, int32_t passes);
 
 #ifdef __cplusplus
 }

@@ -4,5 +4,6 @@
 The CUDA extension is required: importing `Context` / `Solver` loads libpf.so and raises if it
 is missing.  There is no CPU fallback in this package.
 """
-from ._lib import Context, PFError, PF_OP_PSD, PF_OP_SOFT_THRESHOLD, load  # noqa: F401
+from ._lib import (Context, PFError, PF_FP64, PF_TF32, PF_OP_PSD, PF_OP_SOFT_THRESHOLD,  # noqa: F401
+                   load)
 from .solver import Solver, run  # noqa: F401

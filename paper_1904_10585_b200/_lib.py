@@ -12,6 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libpf.so")
 
 PF_FP64 = 0
+PF_TF32 = 2
 PF_OP_PSD = 0
 PF_OP_SOFT_THRESHOLD = 1
 STATUS = {0: "PF_OK", 1: "PF_ERR_ARG", 2: "PF_ERR_DIM", 3: "PF_ERR_INTERVAL", 4: "PF_ERR_CUDA",
@@ -50,6 +51,8 @@ def load() -> ctypes.CDLL:
         "pf_prox_step": [P, P, I64, P, D, P, I64, P, I64, I32, P, I64, P, P],
         "pf_admm_step": [P, P, I64, P, D, P, I64, P, P, I64, P, P],
         "pf_perturb": [P, P, I64, P, I64, P],
+        "pf_perturb_hash": [P, P, I64, ctypes.c_uint64, I32, D, P],
+        "pf_set_tf32_passes": [P, I32],
         "pf_profile": [P, I32],
         "pf_profile_read": [P, P, ctypes.POINTER(D), ctypes.POINTER(I64)],
         "pf_kernel_launches": [],
@@ -110,18 +113,21 @@ def _stream(stream) -> int | None:
 
 
 class Context:
-    """One pf_ctx: scratch for order-n problems with block width p and degree d."""
+    """One pf_ctx: scratch for order-n problems with block width p and degree d.
+
+    dtype PF_FP64: A and the n x p blocks are fp64 row-major tensors.
+    dtype PF_TF32: A is fp32 row-major, blocks are fp32 p-major tensors of shape (p, n_local)."""
 
     def __init__(self, n: int, p: int, d: int, nccl_id: bytes | None = None, rank: int = 0,
-                 world: int = 1):
+                 world: int = 1, dtype: int = PF_FP64):
         self.lib = load()
-        self.n, self.p, self.d = n, p, d
+        self.n, self.p, self.d, self.dtype = n, p, d, dtype
         h = ctypes.c_void_p()
         if nccl_id is None:
-            st = self.lib.pf_create(n, p, d, PF_FP64, ctypes.byref(h))
+            st = self.lib.pf_create(n, p, d, dtype, ctypes.byref(h))
         else:
             buf = ctypes.create_string_buffer(nccl_id, 128)
-            st = self.lib.pf_create_dist(n, p, d, PF_FP64, buf, rank, world, ctypes.byref(h))
+            st = self.lib.pf_create_dist(n, p, d, dtype, buf, rank, world, ctypes.byref(h))
         if st != 0:
             raise PFError(f"pf_create failed: {STATUS.get(st, st)}")
         self.h = h
@@ -211,3 +217,10 @@ class Context:
     def perturb(self, A, E, stream=None):
         self._check(self.lib.pf_perturb(self.h, _ptr(A), _ld(A), _ptr(E), _ld(E),
                                         _stream(stream)), "pf_perturb")
+
+    def perturb_hash(self, A, seed: int, k: int, noise: float, stream=None):
+        self._check(self.lib.pf_perturb_hash(self.h, _ptr(A), _ld(A), seed, k, noise,
+                                             _stream(stream)), "pf_perturb_hash")
+
+    def set_tf32_passes(self, passes: int):
+        self._check(self.lib.pf_set_tf32_passes(self.h, passes), "pf_set_tf32_passes")

@@ -28,6 +28,7 @@ void pf::count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 struct pf_ctx_s {
   int64_t n = 0, n_local = 0, row0 = 0;
   int p = 0, d = 0, rank = 0, world = 1, num_sms = 148;
+  pf_dtype dtype = PF_FP64;
   bool dist = false;                           // NCCL communicator present
   DevState* state = nullptr;
   double* Y[3] = {nullptr, nullptr, nullptr};  // n_local x p, ld p
@@ -66,6 +67,27 @@ struct pf_ctx_s {
   std::vector<cudaEvent_t> ev;
   size_t ev_used = 0;
   long long prof_dropped = 0;
+  // ---- fp32 storage / TF32 tensor-core path (dtype PF_TF32): p-major fp32 blocks
+  int64_t ldy32 = 0;                           // pitch of the internal blocks (>= n_local, %4)
+  float* Yf[3] = {nullptr, nullptr, nullptr};  // p x ldy32
+  float* Wf = nullptr;                         // A Q
+  double* g32_part = nullptr;
+  int g32_slices = 1;
+  double* chol_W = nullptr;                    // p x p
+  double* chol_D = nullptr;                    // p x 32
+  double* jac_H = nullptr;                     // 2 p x p
+  double* jac_V = nullptr;                     // p x p
+  double* jac_red = nullptr;
+  int* jac_cnt = nullptr;
+  float* tf_ws = nullptr;
+  float* tf_acc = nullptr;
+  int* tf_cnt = nullptr;
+  int tf_npass = 3;
+  Tf32Plan tplan;
+  CUtensorMap mapBf[3];
+  CUtensorMap mapAf, mapApf;
+  const float* mapAf_ptr = nullptr;
+  int64_t mapAf_lda = 0;
   char err[512] = {0};
 };
 
@@ -84,7 +106,10 @@ static pf_status cuda_fail(pf_ctx c, cudaError_t e, const char* where) {
     if (s_ != PF_OK) return s_;      \
   } while (0)
 
-static bool p_supported(int p) { return p == 16 || p == 32 || p == 64 || p == 128; }
+static bool p_supported(int p, pf_dtype dt) {
+  if (dt == PF_TF32) return p == 64 || p == 128 || p == 256 || p == 512;
+  return p == 16 || p == 32 || p == 64 || p == 128;
+}
 static bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }
 
 extern "C" {
@@ -122,10 +147,28 @@ static pf_status alloc_all(pf_ctx ctx) {
     return cudaMalloc(ptr, std::max<size_t>(bytes, 16)) == cudaSuccess;
   };
   bool ok = true;
+  const bool f32 = ctx->dtype == PF_TF32;
   ok &= A((void**)&ctx->state, sizeof(DevState));
-  for (int i = 0; i < 3; ++i) ok &= A((void**)&ctx->Y[i], (size_t)nl * p * 8);
-  ok &= A((void**)&ctx->Wbuf, (size_t)nl * p * 8);
-  ok &= A((void**)&ctx->VFbuf, (size_t)nl * p * 8);
+  if (f32) {
+    ctx->ldy32 = (nl + 3) / 4 * 4;
+    for (int i = 0; i < 3; ++i) ok &= A((void**)&ctx->Yf[i], (size_t)p * ctx->ldy32 * 4);
+    ok &= A((void**)&ctx->Wf, (size_t)p * ctx->ldy32 * 4);
+    ctx->g32_slices = gram32_slices((int)nl, p, ctx->num_sms);
+    ok &= A((void**)&ctx->g32_part, (size_t)ctx->g32_slices * p * p * 8);
+    ok &= A((void**)&ctx->chol_W, (size_t)p * p * 8);
+    ok &= A((void**)&ctx->chol_D, (size_t)p * 32 * 8);
+    ok &= A((void**)&ctx->jac_H, (size_t)2 * p * p * 8);
+    ok &= A((void**)&ctx->jac_V, (size_t)p * p * 8);
+    ok &= A((void**)&ctx->jac_red, (size_t)2 * jacobi_big_grid() * 8);
+    ok &= A((void**)&ctx->jac_cnt, 16);
+    ok &= A((void**)&ctx->tf_ws, ctx->tplan.ws_floats * 4);
+    ok &= A((void**)&ctx->tf_acc, ctx->tplan.acc_floats * 4);
+    ok &= A((void**)&ctx->tf_cnt, ctx->tplan.counters * 4);
+  } else {
+    for (int i = 0; i < 3; ++i) ok &= A((void**)&ctx->Y[i], (size_t)nl * p * 8);
+    ok &= A((void**)&ctx->Wbuf, (size_t)nl * p * 8);
+    ok &= A((void**)&ctx->VFbuf, (size_t)nl * p * 8);
+  }
   if (ctx->dist) {
     ok &= A((void**)&ctx->Yfull, (size_t)n * p * 8);
     ok &= A((void**)&ctx->Vfull, (size_t)n * p * 8);
@@ -134,9 +177,11 @@ static pf_status alloc_all(pf_ctx ctx) {
   ok &= A((void**)&ctx->G, (size_t)p * p * 8);
   ok &= A((void**)&ctx->Rinv, (size_t)p * p * 8);
   ok &= A((void**)&ctx->Yeig, (size_t)p * p * 8);
-  ok &= A((void**)&ctx->gram_part, (size_t)gram_blocks((int)nl, p) * p * p * 8);
-  ok &= A((void**)&ctx->cheb_ws, ctx->plan.ws_doubles * 8);
-  ok &= A((void**)&ctx->cheb_cnt, (size_t)(ctx->plan.mtiles + 1) * 4);
+  if (!f32) {
+    ok &= A((void**)&ctx->gram_part, (size_t)gram_blocks((int)nl, p) * p * p * 8);
+    ok &= A((void**)&ctx->cheb_ws, ctx->plan.ws_doubles * 8);
+    ok &= A((void**)&ctx->cheb_cnt, (size_t)(ctx->plan.mtiles + 1) * 4);
+  }
   ctx->lz_ldq = ((nl + 31) / 32) * 32;
   ok &= A((void**)&ctx->lz_Q, (size_t)ctx->lz_ldq * (kMaxLanczos + 1) * 8);
   ok &= A((void**)&ctx->lz_w, (size_t)nl * 8);
@@ -154,14 +199,21 @@ static pf_status alloc_all(pf_ctx ctx) {
     return PF_ERR_NOMEM;
   }
   PF_CU(cudaMemset(ctx->state, 0, sizeof(DevState)));
-  PF_CU(cudaMemset(ctx->cheb_cnt, 0, (size_t)(ctx->plan.mtiles + 1) * 4));
+  if (f32) PF_CU(cudaMemset(ctx->tf_cnt, 0, ctx->tplan.counters * 4));
+  else PF_CU(cudaMemset(ctx->cheb_cnt, 0, (size_t)(ctx->plan.mtiles + 1) * 4));
   PF_CU(cudaMemset(ctx->lz_cnt, 0, 16));
   PF_CU(cudaMemset(ctx->rb_cnt, 0, 16));
   PF_CU(cudaMemset(ctx->shift_flag, 0, 16));
   const double rr[3] = {1.0, 0.0, 0.0};
   PF_CU(cudaMemcpy(&ctx->state->coef_rr[0], rr, sizeof(rr), cudaMemcpyHostToDevice));
   // TMA descriptors of the internal B operands
-  if (!ctx->dist) {
+  if (f32) {
+    for (int i = 0; i < 3; ++i)
+      if (!tf32_encode_B(&ctx->mapBf[i], ctx->Yf[i], ctx->ldy32, p, (int)n)) {
+        snprintf(ctx->err, sizeof(ctx->err), "cuTensorMapEncodeTiled(B, fp32) failed");
+        return PF_ERR_CUDA;
+      }
+  } else if (!ctx->dist) {
     for (int i = 0; i < 3; ++i)
       if (!encode_map_B(&ctx->mapB[i], ctx->Y[i], p, (int)n)) {
         snprintf(ctx->err, sizeof(ctx->err), "cuTensorMapEncodeTiled(B) failed");
@@ -179,15 +231,19 @@ static pf_status create_common(int64_t n, int32_t p, int32_t degree, pf_dtype dt
                                int world, const void* nccl_id, pf_ctx* out) {
   if (!out) return PF_ERR_ARG;
   *out = nullptr;
-  if (dtype != PF_FP64) return PF_ERR_UNSUPPORTED;
+  if (dtype != PF_FP64 && dtype != PF_TF32) return PF_ERR_UNSUPPORTED;
+  // the fp32 path is single-GPU in this build (its row-block all-gather is not wired)
+  if (dtype == PF_TF32 && nccl_id != nullptr) return PF_ERR_UNSUPPORTED;
   if (degree < 1 || degree > kMaxDeg) return PF_ERR_ARG;
   if (world < 1 || rank < 0 || rank >= world) return PF_ERR_ARG;
-  if (!p_supported(p) || n < p || n > (int64_t)1 << 30 || n < world * (int64_t)p) return PF_ERR_DIM;
+  if (!p_supported(p, dtype) || n < p || n > (int64_t)1 << 30 || n < world * (int64_t)p)
+    return PF_ERR_DIM;
   pf_ctx ctx = new (std::nothrow) pf_ctx_s();
   if (!ctx) return PF_ERR_NOMEM;
   ctx->n = n;
   ctx->p = p;
   ctx->d = degree;
+  ctx->dtype = dtype;
   ctx->rank = rank;
   ctx->world = world;
   ctx->dist = (nccl_id != nullptr);
@@ -202,7 +258,8 @@ static pf_status create_common(int64_t n, int32_t p, int32_t degree, pf_dtype dt
     delete ctx;
     return s;
   }
-  ctx->plan = cheb_gemm_plan(p, (int)ctx->n_local, (int)n, ctx->num_sms);
+  if (dtype == PF_TF32) ctx->tplan = tf32_plan(p, (int)ctx->n_local, (int)n, ctx->num_sms);
+  else ctx->plan = cheb_gemm_plan(p, (int)ctx->n_local, (int)n, ctx->num_sms);
   pf_status s = alloc_all(ctx);
   if (s == PF_OK && ctx->dist) {
     ncclUniqueId id;
@@ -279,7 +336,10 @@ pf_status pf_destroy(pf_ctx ctx) {
                   ctx->Wbuf,   ctx->VFbuf,    ctx->Vfull,    ctx->G,         ctx->Rinv,    ctx->Yeig,
                   ctx->gram_part, ctx->cheb_ws, ctx->cheb_cnt, ctx->lz_Q,   ctx->lz_qfull,
                   ctx->lz_w,   ctx->lz_h,     ctx->lz_part,   ctx->lz_cnt,  ctx->lz_T,
-                  ctx->lz_theta, ctx->lz_S,   ctx->rb_part,   ctx->rb_cnt,  ctx->shift_flag};
+                  ctx->lz_theta, ctx->lz_S,   ctx->rb_part,   ctx->rb_cnt,  ctx->shift_flag,
+                  ctx->Yf[0],  ctx->Yf[1],    ctx->Yf[2],     ctx->Wf,      ctx->g32_part,
+                  ctx->chol_W, ctx->chol_D,   ctx->jac_H,     ctx->jac_V,   ctx->jac_red,
+                  ctx->jac_cnt, ctx->tf_ws,   ctx->tf_cnt,    ctx->tf_acc};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete ctx;
@@ -398,12 +458,137 @@ static pf_status orth_internal(pf_ctx ctx, double* Y, cudaStream_t st) {
   return chol_pass(ctx, Y, nullptr, ctx->shift_flag, st);
 }
 
+
+// ------------------------------------------------------------------------------ fp32 internals
+static pf_status check_A32(pf_ctx ctx, const float* A, int64_t lda) {
+  if (!A) return PF_ERR_ARG;
+  if (lda < ctx->n || (lda & 3) || !aligned16(A)) return PF_ERR_DIM;
+  return PF_OK;
+}
+
+static pf_status map_A32(pf_ctx ctx, const float* A, int64_t lda) {
+  if (A != ctx->mapAf_ptr || lda != ctx->mapAf_lda) {
+    if (!tf32_encode_A(&ctx->mapAf, &ctx->mapApf, A, lda, (int)ctx->n_local, (int)ctx->n)) {
+      snprintf(ctx->err, sizeof(ctx->err), "cuTensorMapEncodeTiled(A, fp32) failed");
+      return PF_ERR_CUDA;
+    }
+    ctx->mapAf_ptr = A;
+    ctx->mapAf_lda = lda;
+  }
+  return PF_OK;
+}
+
+// user p-major block (pitch ld) <-> internal block (pitch ldy32)
+static pf_status copy_block32(pf_ctx ctx, float* dst, int64_t ldd, const float* src, int64_t lds,
+                              cudaStream_t st) {
+  PF_CU(cudaMemcpy2DAsync(dst, ldd * 4, src, lds * 4, (size_t)ctx->n_local * 4, ctx->p,
+                          cudaMemcpyDeviceToDevice, st));
+  return PF_OK;
+}
+
+static pf_status gemm_step32(pf_ctx ctx, int bidx, const float* ycur, const float* yprev,
+                             float* out, const double* coef, cudaStream_t st) {
+  const bool rec = ctx->prof && ctx->ev_used + 2 <= ctx->ev.size();
+  if (ctx->prof && !rec) ++ctx->prof_dropped;
+  if (rec) PF_CU(cudaEventRecord(ctx->ev[ctx->ev_used], st));
+  PF_CU(tf32_gemm_launch(ctx->tplan, ctx->mapAf, ctx->mapBf[bidx], ctx->mapApf, ycur, yprev, out,
+                         ctx->ldy32, coef, ctx->tf_ws, ctx->tf_acc, ctx->tf_cnt, ctx->tf_npass,
+                         st));
+  if (rec) {
+    PF_CU(cudaEventRecord(ctx->ev[ctx->ev_used + 1], st));
+    ctx->ev_used += 2;
+  }
+  return PF_OK;
+}
+
+static pf_status gram32_all(pf_ctx ctx, const float* X, const float* Y, double* G, const int* cond,
+                            cudaStream_t st) {
+  PF_CU(gram32_launch(X, ctx->ldy32, Y, ctx->ldy32, (int)ctx->n_local, ctx->p, G, ctx->g32_part,
+                      ctx->g32_slices, cond, st));
+  return PF_OK;
+}
+
+static pf_status chol32(pf_ctx ctx, int* shift_out, const int* cond, cudaStream_t st) {
+  PF_CU(chol_inv_big_launch(ctx->G, ctx->p, ctx->n, ctx->chol_W, ctx->chol_D, ctx->Rinv,
+                            ctx->state, shift_out, cond, st));
+  return PF_OK;
+}
+
+static pf_status chol_pass32(pf_ctx ctx, float* Y, int* shift_out, const int* cond,
+                             cudaStream_t st) {
+  PF_TRY(gram32_all(ctx, Y, Y, ctx->G, cond, st));
+  PF_TRY(chol32(ctx, shift_out, cond, st));
+  PF_CU(rmul32_launch(Y, ctx->ldy32, ctx->Rinv, Y, ctx->ldy32, (int)ctx->n_local, ctx->p, cond, st));
+  return PF_OK;
+}
+
+static pf_status orth_internal32(pf_ctx ctx, float* Y, cudaStream_t st) {
+  PF_CU(cudaMemsetAsync(ctx->shift_flag, 0, sizeof(int), st));
+  PF_TRY(chol_pass32(ctx, Y, ctx->shift_flag, nullptr, st));
+  PF_TRY(chol_pass32(ctx, Y, ctx->shift_flag, nullptr, st));
+  return chol_pass32(ctx, Y, nullptr, ctx->shift_flag, st);
+}
+
+static pf_status filter32(pf_ctx ctx, const float* A, int64_t lda, float* U, int64_t ldu,
+                          const double* interval, int32_t q, double rho_max, cudaStream_t st) {
+  if (ldu < ctx->n_local) return PF_ERR_DIM;
+  PF_TRY(check_A32(ctx, A, lda));
+  PF_TRY(map_A32(ctx, A, lda));
+  const int p = ctx->p, d = ctx->d, nl = (int)ctx->n_local;
+  PF_CU(plan_launch(interval, d, rho_max, p, ctx->state, st));
+  PF_TRY(copy_block32(ctx, ctx->Yf[0], ctx->ldy32, U, ldu, st));
+  int cur = 0, prev = -1;
+  for (int rep = 0; rep < q; ++rep) {
+    prev = -1;
+    for (int j = 0; j < d; ++j) {
+      const int out = (prev < 0) ? (cur + 1) % 3 : 3 - cur - prev;
+      const double* coef = &ctx->state->coef[j][0];
+      PF_TRY(gemm_step32(ctx, cur, ctx->Yf[cur], prev < 0 ? ctx->Yf[cur] : ctx->Yf[prev],
+                         ctx->Yf[out], coef, st));
+      prev = cur;
+      cur = out;
+      if (j + 1 < d) {
+        const int* cond = &ctx->state->rebase[j];
+        PF_TRY(gram32_all(ctx, ctx->Yf[cur], ctx->Yf[cur], ctx->G, cond, st));
+        PF_TRY(chol32(ctx, nullptr, cond, st));
+        PF_CU(rmul32_launch(ctx->Yf[cur], ctx->ldy32, ctx->Rinv, ctx->Yf[cur], ctx->ldy32, nl, p,
+                            cond, st));
+        PF_CU(rmul32_launch(ctx->Yf[prev], ctx->ldy32, ctx->Rinv, ctx->Yf[prev], ctx->ldy32, nl, p,
+                            cond, st));
+      }
+    }
+  }
+  PF_TRY(orth_internal32(ctx, ctx->Yf[cur], st));
+  return copy_block32(ctx, U, ldu, ctx->Yf[cur], ctx->ldy32, st);
+}
+
+static pf_status rayleigh_ritz32(pf_ctx ctx, const float* A, int64_t lda, const float* U,
+                                 int64_t ldu, float* V, int64_t ldv, double* theta,
+                                 cudaStream_t st) {
+  if (ldu < ctx->n_local || ldv < ctx->n_local) return PF_ERR_DIM;
+  PF_TRY(check_A32(ctx, A, lda));
+  PF_TRY(map_A32(ctx, A, lda));
+  const int p = ctx->p, nl = (int)ctx->n_local;
+  PF_TRY(copy_block32(ctx, ctx->Yf[0], ctx->ldy32, U, ldu, st));
+  PF_TRY(gemm_step32(ctx, 0, ctx->Yf[0], ctx->Yf[0], ctx->Wf, &ctx->state->coef_rr[0], st));
+  PF_TRY(gram32_all(ctx, ctx->Yf[0], ctx->Wf, ctx->G, nullptr, st));  // H = Q^T (A Q)
+  PF_CU(jacobi_big_launch(ctx->G, p, theta, ctx->Yeig, ctx->jac_H, ctx->jac_V, ctx->jac_red,
+                          ctx->jac_cnt, ctx->state, std::max(1e-15, 1e-16 * p), 40, st));
+  PF_CU(copy_theta_launch(theta, p, ctx->state, st));
+  PF_CU(rmul32_launch(ctx->Yf[0], ctx->ldy32, ctx->Yeig, V, ldv, nl, p, nullptr, st));
+  return PF_OK;
+}
+
 // ------------------------------------------------------------------------------ ABI
-pf_status pf_lanczos(pf_ctx ctx, const double* A, int64_t lda, const double* v0, int32_t m,
+pf_status pf_lanczos(pf_ctx ctx, const void* Av, int64_t lda, const double* v0, int32_t m,
                      double* lo_hi, pf_stream stream) {
   if (!ctx || !v0 || !lo_hi) return PF_ERR_ARG;
   if (m < 1 || m > kMaxLanczos) return PF_ERR_ARG;
-  PF_TRY(check_A(ctx, A, lda));
+  const bool f32 = ctx->dtype == PF_TF32;
+  const double* A = static_cast<const double*>(Av);
+  const float* A32 = static_cast<const float*>(Av);
+  if (f32) PF_TRY(check_A32(ctx, A32, lda));
+  else PF_TRY(check_A(ctx, A, lda));
   cudaStream_t st = (cudaStream_t)stream;
   const int nl = (int)ctx->n_local, n = (int)ctx->n;
   m = (int32_t)std::min<int64_t>(m, ctx->n);
@@ -420,8 +605,12 @@ pf_status pf_lanczos(pf_ctx ctx, const double* A, int64_t lda, const double* v0,
       PF_TRY(gather(ctx, qj, ctx->lz_qfull, 1, st));
       qfull = ctx->lz_qfull;
     }
-    PF_CU(lz_gemv_launch(A, lda, nl, n, qfull, ctx->lz_Q, ctx->lz_ldq, j, ctx->lz_w, h1,
-                         ctx->lz_part, ctx->lz_cnt, ctx->state, st));
+    if (f32)
+      PF_CU(lz_gemv_f32_launch(A32, lda, nl, n, qfull, ctx->lz_Q, ctx->lz_ldq, j, ctx->lz_w, h1,
+                               ctx->lz_part, ctx->lz_cnt, ctx->state, st));
+    else
+      PF_CU(lz_gemv_launch(A, lda, nl, n, qfull, ctx->lz_Q, ctx->lz_ldq, j, ctx->lz_w, h1,
+                           ctx->lz_part, ctx->lz_cnt, ctx->state, st));
     PF_TRY(allreduce(ctx, h1, (size_t)j + 1, st));
     PF_CU(lz_orth_launch(nl, ctx->lz_Q, ctx->lz_ldq, j, ctx->lz_w, h1, h2, ctx->lz_part,
                          ctx->lz_cnt, ctx->state, 1, st));
@@ -452,10 +641,18 @@ pf_status pf_interval_soft(pf_ctx ctx, double thr, double eta, double* interval,
   return PF_OK;
 }
 
-pf_status pf_orth(pf_ctx ctx, double* U, int64_t ldu, pf_stream stream) {
-  if (!ctx || !U) return PF_ERR_ARG;
-  if (ldu < ctx->p) return PF_ERR_DIM;
+pf_status pf_orth(pf_ctx ctx, void* Uv, int64_t ldu, pf_stream stream) {
+  if (!ctx || !Uv) return PF_ERR_ARG;
   cudaStream_t st = (cudaStream_t)stream;
+  if (ctx->dtype == PF_TF32) {
+    float* U = static_cast<float*>(Uv);
+    if (ldu < ctx->n_local) return PF_ERR_DIM;
+    PF_TRY(copy_block32(ctx, ctx->Yf[0], ctx->ldy32, U, ldu, st));
+    PF_TRY(orth_internal32(ctx, ctx->Yf[0], st));
+    return copy_block32(ctx, U, ldu, ctx->Yf[0], ctx->ldy32, st);
+  }
+  double* U = static_cast<double*>(Uv);
+  if (ldu < ctx->p) return PF_ERR_DIM;
   const size_t row = (size_t)ctx->p * 8;
   PF_CU(cudaMemcpy2DAsync(ctx->Y[0], row, U, ldu * 8, row, ctx->n_local, cudaMemcpyDeviceToDevice, st));
   PF_TRY(orth_internal(ctx, ctx->Y[0], st));
@@ -463,10 +660,15 @@ pf_status pf_orth(pf_ctx ctx, double* U, int64_t ldu, pf_stream stream) {
   return PF_OK;
 }
 
-pf_status pf_filter(pf_ctx ctx, const double* A, int64_t lda, double* U, int64_t ldu,
+pf_status pf_filter(pf_ctx ctx, const void* Av, int64_t lda, void* Uv, int64_t ldu,
                     const double* interval, int32_t q, double rho_max, pf_stream stream) {
-  if (!ctx || !U || !interval) return PF_ERR_ARG;
+  if (!ctx || !Uv || !interval) return PF_ERR_ARG;
   if (q < 1 || q > 10 || !(rho_max > 1.0)) return PF_ERR_ARG;
+  if (ctx->dtype == PF_TF32)
+    return filter32(ctx, static_cast<const float*>(Av), lda, static_cast<float*>(Uv), ldu,
+                    interval, q, rho_max, (cudaStream_t)stream);
+  const double* A = static_cast<const double*>(Av);
+  double* U = static_cast<double*>(Uv);
   if (ldu < ctx->p) return PF_ERR_DIM;
   PF_TRY(check_A(ctx, A, lda));
   PF_TRY(map_A(ctx, A, lda));
@@ -501,9 +703,15 @@ pf_status pf_filter(pf_ctx ctx, const double* A, int64_t lda, double* U, int64_t
   return PF_OK;
 }
 
-pf_status pf_rayleigh_ritz(pf_ctx ctx, const double* A, int64_t lda, const double* U,
-                           int64_t ldu, double* V, int64_t ldv, double* theta, pf_stream stream) {
-  if (!ctx || !U || !V || !theta) return PF_ERR_ARG;
+pf_status pf_rayleigh_ritz(pf_ctx ctx, const void* Av, int64_t lda, const void* Uv,
+                           int64_t ldu, void* Vv, int64_t ldv, double* theta, pf_stream stream) {
+  if (!ctx || !Uv || !Vv || !theta) return PF_ERR_ARG;
+  if (ctx->dtype == PF_TF32)
+    return rayleigh_ritz32(ctx, static_cast<const float*>(Av), lda, static_cast<const float*>(Uv),
+                           ldu, static_cast<float*>(Vv), ldv, theta, (cudaStream_t)stream);
+  const double* A = static_cast<const double*>(Av);
+  const double* U = static_cast<const double*>(Uv);
+  double* V = static_cast<double*>(Vv);
   if (ldu < ctx->p || ldv < ctx->p || (ldv & 1) || !aligned16(V)) return PF_ERR_DIM;
   PF_TRY(check_A(ctx, A, lda));
   PF_TRY(map_A(ctx, A, lda));
@@ -550,6 +758,7 @@ pf_status pf_prox_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f
                        int32_t r, double* A_out, int64_t lda_out, double* obj,
                        pf_stream stream) {
   if (!ctx || !V || !f || !omega || !A_out || !obj) return PF_ERR_ARG;
+  if (ctx->dtype != PF_FP64) return PF_ERR_UNSUPPORTED;
   if (r < 0 || r > 64 || (r > 0 && !W)) return PF_ERR_ARG;
   if (ldv < ctx->p || (ldv & 1) || !aligned16(V) || ldo < (ctx->n + 31) / 32 ||
       lda_out < ctx->n || (r > 0 && ldw < r))
@@ -569,6 +778,7 @@ pf_status pf_admm_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f
                        const uint32_t* adj, int64_t ldadj, const double* deg, double* Z,
                        int64_t ldz, double* obj, pf_stream stream) {
   if (!ctx || !V || !f || !adj || !deg || !Z || !obj) return PF_ERR_ARG;
+  if (ctx->dtype != PF_FP64) return PF_ERR_UNSUPPORTED;
   if (ldv < ctx->p || (ldv & 1) || !aligned16(V) || ldadj < (ctx->n + 31) / 32 || ldz < ctx->n)
     return PF_ERR_DIM;
   cudaStream_t st = (cudaStream_t)stream;
@@ -589,8 +799,26 @@ pf_status pf_admm_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f
 pf_status pf_perturb(pf_ctx ctx, double* A, int64_t lda, const double* E, int64_t lde,
                      pf_stream stream) {
   if (!ctx || !A || !E) return PF_ERR_ARG;
+  if (ctx->dtype != PF_FP64) return PF_ERR_UNSUPPORTED;
   if (lda < ctx->n || lde < ctx->n) return PF_ERR_DIM;
   PF_CU(perturb_launch(A, lda, E, lde, (int)ctx->n_local, (int)ctx->n, (cudaStream_t)stream));
+  return PF_OK;
+}
+
+pf_status pf_perturb_hash(pf_ctx ctx, float* A, int64_t lda, uint64_t seed, int32_t k,
+                          double noise, pf_stream stream) {
+  if (!ctx || !A) return PF_ERR_ARG;
+  if (ctx->dtype != PF_TF32) return PF_ERR_UNSUPPORTED;
+  if (lda < ctx->n) return PF_ERR_DIM;
+  PF_CU(perturb_hash32_launch(A, lda, (int)ctx->n_local, (int)ctx->n, (int)ctx->row0,
+                              (unsigned long long)seed, k, noise, (cudaStream_t)stream));
+  return PF_OK;
+}
+
+pf_status pf_set_tf32_passes(pf_ctx ctx, int32_t passes) {
+  if (!ctx || (passes != 1 && passes != 3)) return PF_ERR_ARG;
+  if (ctx->dtype != PF_TF32) return PF_ERR_UNSUPPORTED;
+  ctx->tf_npass = passes;
   return PF_OK;
 }
 

@@ -10,7 +10,7 @@
 
 namespace pf {
 
-constexpr int kMaxP = 128;
+constexpr int kMaxP = 512;
 constexpr int kMaxDeg = 64;
 constexpr int kMaxLanczos = 64;
 

@@ -56,8 +56,8 @@ struct Tf32Cfg {
   static constexpr int TMEM_COLS = P < 32 ? 32 : P;
   static constexpr int PF_DIST = 32;              // L2 prefetch distance (k-blocks) for A
   static constexpr int NCONV_WARPS = 6;           // warps 2..7
-  static constexpr int NEPI_WARPS = 4;            // warps 8..11 (TMEM lane quarters 0..3)
-  static constexpr int THREADS = 12 * 32;
+  static constexpr int NEPI_WARPS = 8;            // warps 8..15: lane quarter x column half
+  static constexpr int THREADS = 16 * 32;
   static constexpr int BAR_BYTES = 8 * (2 * NT + 2 * NL + 2) + 16;
   static constexpr int SMEM = (NT + NL) * STAGE_BYTES + 1024 + BAR_BYTES;
   static_assert(P % 32 == 0 && P >= 64 && P <= 512, "p");
@@ -78,6 +78,8 @@ struct Tf32Args {
   int mtiles;
   int split;           // K-split of the tail wave
   int npass;
+  int chunk_kb;        // k-blocks accumulated in TMEM before folding into `acc` (0: no limit)
+  float* acc;          // fp32 chunk accumulators: [pair][2 ctas][P][128]
 };
 
 // Work schedule of pair g among G pairs: F = M / G full waves in which every pair runs a whole
@@ -218,12 +220,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tf32Cfg<P>::THREADS,
       const uint32_t idesc = tc::idesc_tf32(256, C::NMMA);
       Ring rt(C::NT), rl(C::NL);
       uint32_t tphase = 0;
+      const int kch = args.chunk_kb > 0 ? args.chunk_kb : (1 << 30);
       for (int w = 0; w < nitems; ++w) {
         int tile, kb0, kb1;
         sch.item(w, tile, kb0, kb1);
+        for (int s0 = kb0; s0 < kb1; s0 += kch) {
+        const int s1 = min(kb1, s0 + kch);
         tc::mbar_wait_cluster(tempty, tphase ^ 1u);  // both epilogues drained the accumulator
         tc::fence_after_sync();
-        for (int kb = kb0; kb < kb1; ++kb, rt.next(), rl.next()) {
+        for (int kb = s0; kb < s1; ++kb, rt.next(), rl.next()) {
           // the converters of BOTH CTAs saw this raw stage land and wrote its lo copy
           TRACE(3, w, kb - kb0);
           tc::mbar_wait_cluster(&ready[rl.s], rl.ph);
@@ -238,7 +243,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tf32Cfg<P>::THREADS,
             for (int h = 0; h < C::NH; ++h) {
               const uint32_t d = tmem + h * C::NMMA;
               const uint32_t boff = h * (C::NMMA / 2) * 64 + ks * 32;
-              const uint32_t acc = (kb == kb0 && ks == 0) ? 0u : 1u;
+              const uint32_t acc = (kb == s0 && ks == 0) ? 0u : 1u;
               tc::mma_tf32_pair(d, tc::sdesc_k_sw64(a_hi + ks * 32),
                                 tc::sdesc_k_sw64(b_hi + boff), idesc, acc);
               if (args.npass == 3) {
@@ -254,6 +259,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tf32Cfg<P>::THREADS,
         }
         tc::mma_commit_pair(tfull);  // accumulator complete -> both epilogues
         tphase ^= 1u;
+        }
       }
     }
   } else if (warp < 2 + C::NCONV_WARPS) {
@@ -291,68 +297,81 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tf32Cfg<P>::THREADS,
       }
     }
   } else {
-    // ------------------------------------------------------------ epilogue (4 warps)
-    const int q = warp & 3;  // TMEM lane quarter
-    const int et = threadIdx.x - 256;  // 0..127 == row within this CTA's 128 rows
+    // ------------------------------------------------------------ epilogue (8 warps)
+    // warp 8 + 4h + q drains TMEM lanes 32q..32q+31 (rows) and columns [h P/2, (h+1) P/2).
+    // The tensor core's fp32 accumulation truncates (tools/probe: one-signed data drifts by
+    // -3e-4 relative over K = 65536), so at most chunk_kb k-blocks are accumulated in TMEM;
+    // chunk results are folded into `acc` with round-to-nearest fp32 adds (same thread, same
+    // order every launch: deterministic).
+    const int q = warp & 3, hc = (warp - 8) >> 2;
+    const int et = 32 * q + lane;  // row within this CTA's 128 rows
+    const int cb = hc * (P / 2), ce = cb + P / 2;
     const uint32_t tempty_leader = tc::mapa(smem_u32(tempty), 0);
     const float s1 = (float)args.coef[0], s2 = (float)args.coef[1], s3 = (float)args.coef[2];
+    const int kch = args.chunk_kb > 0 ? args.chunk_kb : (1 << 30);
+    float* accp = args.acc + ((size_t)g * 2 + crank) * (size_t)(P * 128) + et;
     uint32_t tphase = 0;
     for (int w = 0; w < nitems; ++w) {
       int tile, kb0, kb1;
       sch.item(w, tile, kb0, kb1);
       const int row = tile * 256 + (int)crank * C::BM + et;
       const bool row_ok = row < args.n_rows;
+      const bool whole = (kb0 == 0 && kb1 == KB);
       const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16);
-      mbar_wait(tfull, tphase);
-      tphase ^= 1u;
-      tc::fence_after_sync();
-      if (kb0 == 0 && kb1 == KB) {
+      float* mine = args.ws + ((size_t)g * 2 + crank) * (size_t)(P * 128) + et;
+      for (int s0 = kb0; s0 < kb1; s0 += kch) {
+        const bool first = (s0 == kb0), last = (s0 + kch >= kb1);
+        mbar_wait(tfull, tphase);
+        tphase ^= 1u;
+        tc::fence_after_sync();
 #pragma unroll 1
-        for (int c0 = 0; c0 < P; c0 += 32) {
+        for (int c0 = cb; c0 < ce; c0 += 32) {
           float v[32];
           tc::tmem_ld32(taddr + c0, v);
-          if (row_ok) {
+          if (!first) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const size_t o = (size_t)(c0 + j) * args.ldy + row;
-              float y = s1 * v[j];
-              if (s2 != 0.f) y = fmaf(s2, args.ycur[o], y);
-              if (s3 != 0.f) y = fmaf(s3, args.yprev[o], y);
-              args.out[o] = y;
+            for (int j = 0; j < 32; ++j) v[j] += __ldcg(accp + (size_t)(c0 + j) * 128);
+          }
+          if (!last) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) __stcg(accp + (size_t)(c0 + j) * 128, v[j]);
+          } else if (whole) {
+            if (row_ok) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const size_t o = (size_t)(c0 + j) * args.ldy + row;
+                float y = s1 * v[j];
+                if (s2 != 0.f) y = fmaf(s2, args.ycur[o], y);
+                if (s3 != 0.f) y = fmaf(s3, args.yprev[o], y);
+                args.out[o] = y;
+              }
             }
+          } else {  // split-K partial of a tail tile
+#pragma unroll
+            for (int j = 0; j < 32; ++j) __stcg(mine + (size_t)(c0 + j) * 128, v[j]);
           }
         }
         tc::fence_before_sync();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive_cluster(tempty_leader);
-      } else {
-        // -------------------------------------------------- split-K partial tile
-        float* mine = args.ws + ((size_t)g * 2 + crank) * (size_t)(P * 128);
-#pragma unroll 1
-        for (int c0 = 0; c0 < P; c0 += 32) {
-          float v[32];
-          tc::tmem_ld32(taddr + c0, v);
-#pragma unroll
-          for (int j = 0; j < 32; ++j) __stcg(mine + (size_t)(c0 + j) * 128 + et, v[j]);
-        }
-        tc::fence_before_sync();
-        __syncwarp();
         if (lane == 0) tc::mbar_arrive_cluster(tempty_leader);  // TMEM free: MMA may go on
+      }
+      if (!whole) {
+        // -------------------------------------------------- split-K fixup (last contributor)
         __threadfence();
-        named_bar_sync(1, 128);
-        if (et == 0) {
+        named_bar_sync(1, 256);
+        if (threadIdx.x == 256) {
           const int add = kb1 - kb0;
           const int prev = atomicAdd(&args.counters[tile * 2 + crank], add);
           *sflag = (prev + add == KB) ? 1 : 0;
         }
-        named_bar_sync(1, 128);
-        const bool last = (*sflag != 0);
-        named_bar_sync(1, 128);
-        if (last) {
+        named_bar_sync(1, 256);
+        const bool lastc = (*sflag != 0);
+        named_bar_sync(1, 256);
+        if (lastc) {
           __threadfence();
           const int u0 = (tile - sch.F * G) * sch.S;  // first contributing pair
 #pragma unroll 1
-          for (int c0 = 0; c0 < P; c0 += 32) {
+          for (int c0 = cb; c0 < ce; c0 += 32) {
             float acc[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) acc[j] = 0.f;
@@ -374,7 +393,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tf32Cfg<P>::THREADS,
               }
             }
           }
-          if (et == 0) args.counters[tile * 2 + crank] = 0;  // ready for the next launch
+          named_bar_sync(1, 256);
+          if (threadIdx.x == 256) args.counters[tile * 2 + crank] = 0;  // ready for next launch
         }
       }
     }
@@ -407,6 +427,8 @@ Tf32Plan tf32_plan(int p, int n_rows, int n_k, int num_sms) {
   pl.pairs = G;
   pl.split = R ? std::max(1, std::min(smax, G / R)) : 1;
   pl.ws_floats = (size_t)G * 2 * (size_t)p * 128;
+  pl.acc_floats = pl.ws_floats;
+  pl.chunk_kb = 128;  // K_c = 2048 per TMEM accumulation (truncating accumulator, see kernel)
   pl.counters = (size_t)pl.mtiles * 2;
   return pl;
 }
@@ -440,8 +462,8 @@ static cudaError_t tf32_launch_p(const Tf32Plan& pl, const CUtensorMap& mapA,
 cudaError_t tf32_gemm_launch(const Tf32Plan& pl, const CUtensorMap& mapA, const CUtensorMap& mapB,
                              const CUtensorMap& mapApf,
                              const float* ycur, const float* yprev, float* out, int64_t ldy,
-                             const double* coef, float* ws, int* counters, int npass,
-                             cudaStream_t st) {
+                             const double* coef, float* ws, float* acc, int* counters,
+                             int npass, cudaStream_t st) {
   Tf32Args a;
   a.ycur = ycur;
   a.yprev = yprev;
@@ -455,6 +477,8 @@ cudaError_t tf32_gemm_launch(const Tf32Plan& pl, const CUtensorMap& mapA, const 
   a.mtiles = pl.mtiles;
   a.split = pl.split;
   a.npass = npass;
+  a.chunk_kb = pl.chunk_kb;
+  a.acc = acc;
   switch (pl.p) {
     case 64: return tf32_launch_p<64>(pl, mapA, mapB, mapApf, a, st);
     case 128: return tf32_launch_p<128>(pl, mapA, mapB, mapApf, a, st);

@@ -38,6 +38,8 @@ struct Tf32Plan {
   int pairs;            // launched CTA pairs
   int split;            // K-split of the leftover (tail) tiles
   size_t ws_floats;     // partial workspace
+  size_t acc_floats;    // chunk accumulators
+  int chunk_kb;         // k-blocks per TMEM accumulation chunk
   size_t counters;      // tile counters (ints)
 };
 Tf32Plan tf32_plan(int p, int n_rows, int n_k, int num_sms);
@@ -48,8 +50,32 @@ bool tf32_encode_B(CUtensorMap* map, const float* Yt, int64_t ldy, int p, int n_
 cudaError_t tf32_gemm_launch(const Tf32Plan& pl, const CUtensorMap& mapA, const CUtensorMap& mapB,
                              const CUtensorMap& mapApf,
                              const float* ycur, const float* yprev, float* out, int64_t ldy,
-                             const double* coef, float* ws, int* counters, int npass,
-                             cudaStream_t st);
+                             const double* coef, float* ws, float* acc, int* counters,
+                             int npass, cudaStream_t st);
+
+// ---- fp32-path kernels (pf_f32.cu); blocks fp32 p-major, p x p objects fp64 row-major
+int gram32_slices(int n_rows, int p, int num_sms);
+// G = X Y^T over the n_rows columns of the p-major blocks; partials: nslices * p * p doubles
+cudaError_t gram32_launch(const float* X, int64_t ldx, const float* Y, int64_t ldy, int n_rows,
+                          int p, double* G, double* partials, int nslices, const int* cond,
+                          cudaStream_t st);
+// out = in R (block view), in place allowed
+cudaError_t rmul32_launch(const float* in, int64_t ldi, const double* R, float* out, int64_t ldo,
+                          int n_rows, int p, const int* cond, cudaStream_t st);
+// W: p*p doubles scratch, Dinv: p*32 doubles scratch
+cudaError_t chol_inv_big_launch(const double* G, int p, int64_t n_global, double* W, double* Dinv,
+                                double* Rinv, DevState* state, int* shift_flag_out,
+                                const int* cond, cudaStream_t st);
+int jacobi_big_grid();
+cudaError_t jacobi_big_launch(const double* H, int p, double* theta, double* Y, double* Hw,
+                              double* Vw, double* red_ws, int* cnt_ws, DevState* state, double tol,
+                              int max_sweeps, cudaStream_t st);
+cudaError_t perturb_hash32_launch(float* A, int64_t lda, int rows, int cols, int row0,
+                                  unsigned long long seed, int k, double noise, cudaStream_t st);
+// Lanczos GEMV on an fp32 iterate (fp64 accumulation), same contract as lz_gemv_launch
+cudaError_t lz_gemv_f32_launch(const float* A, int64_t lda, int n_local, int n, const double* q,
+                               const double* Q, int64_t ldq, int j, double* w, double* h,
+                               double* partials, int* counter, DevState* state, cudaStream_t st);
 
 // ---- small dense kernels (pf_small.cu); all p x p objects are row-major, ld = p
 // G = X^T Y over rows [0, n_rows) (X, Y: n_rows x p, ld p).  Deterministic two-level sum:

@@ -67,8 +67,18 @@ cudaError_t lz_start_launch(const double* v0, int n_local, double* s, double* q0
 
 // w = A_local q_full (one HBM pass over the local rows of A), then local partial dots
 // h_i = Q_i . w (i <= j) reduced in block order by the last block.
+// two consecutive entries of a row of A as doubles (streaming load: A is read once per step)
+__device__ __forceinline__ double2 lz_ld2(const double* p) {
+  return __ldcs(reinterpret_cast<const double2*>(p));
+}
+__device__ __forceinline__ double2 lz_ld2(const float* p) {
+  const float2 f = __ldcs(reinterpret_cast<const float2*>(p));
+  return make_double2((double)f.x, (double)f.y);
+}
+
+template <typename TA>
 __global__ void __launch_bounds__(kLzThreads, 4) lz_gemv_kernel(
-    const double* __restrict__ A, int64_t lda, int n_local, int n, const double* __restrict__ q,
+    const TA* __restrict__ A, int64_t lda, int n_local, int n, const double* __restrict__ q,
     const double* __restrict__ Q, int64_t ldq, int j, double* __restrict__ w,
     double* __restrict__ h, double* __restrict__ partials, int* counter, DevState* state) {
   if (state->lanczos_steps >= 0) return;  // stopped (breakdown)
@@ -85,16 +95,16 @@ __global__ void __launch_bounds__(kLzThreads, 4) lz_gemv_kernel(
   const int c0 = min(n, warp * seg), c1 = min(n, c0 + seg);
   for (int r = r0; r < r1; r += 2) {
     const bool two = (r + 1 < r1);
-    const double* a0 = A + (size_t)r * lda;
-    const double* a1 = A + (size_t)(two ? r + 1 : r) * lda;
+    const TA* a0 = A + (size_t)r * lda;
+    const TA* a1 = A + (size_t)(two ? r + 1 : r) * lda;
     double s0 = 0.0, s1 = 0.0;
     int c = c0 + lane * 2;
     for (; c + 64 * 3 + 1 < c1; c += 64 * 4) {
       double2 x0[4], x1[4], y[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        x0[u] = __ldcs(reinterpret_cast<const double2*>(a0 + c + 64 * u));
-        x1[u] = __ldcs(reinterpret_cast<const double2*>(a1 + c + 64 * u));
+        x0[u] = lz_ld2(a0 + c + 64 * u);
+        x1[u] = lz_ld2(a1 + c + 64 * u);
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) y[u] = __ldg(reinterpret_cast<const double2*>(q + c + 64 * u));
@@ -105,11 +115,11 @@ __global__ void __launch_bounds__(kLzThreads, 4) lz_gemv_kernel(
       }
     }
     for (; c < c1; c += 64) {
-      s0 += a0[c] * q[c];
-      s1 += a1[c] * q[c];
+      s0 += (double)a0[c] * q[c];
+      s1 += (double)a1[c] * q[c];
       if (c + 1 < c1) {
-        s0 += a0[c + 1] * q[c + 1];
-        s1 += a1[c + 1] * q[c + 1];
+        s0 += (double)a0[c + 1] * q[c + 1];
+        s1 += (double)a1[c + 1] * q[c + 1];
       }
     }
     s0 = warp_sum(s0);
@@ -235,8 +245,17 @@ cudaError_t lz_gemv_launch(const double* A, int64_t lda, int n_local, int n, con
                            const double* Q, int64_t ldq, int j, double* w, double* h,
                            double* partials, int* counter, DevState* state, cudaStream_t st) {
   count_launch();
-  lz_gemv_kernel<<<lanczos_blocks(n_local), kLzThreads, 0, st>>>(A, lda, n_local, n, q, Q, ldq, j,
-                                                                 w, h, partials, counter, state);
+  lz_gemv_kernel<double><<<lanczos_blocks(n_local), kLzThreads, 0, st>>>(
+      A, lda, n_local, n, q, Q, ldq, j, w, h, partials, counter, state);
+  return cudaGetLastError();
+}
+
+cudaError_t lz_gemv_f32_launch(const float* A, int64_t lda, int n_local, int n, const double* q,
+                               const double* Q, int64_t ldq, int j, double* w, double* h,
+                               double* partials, int* counter, DevState* state, cudaStream_t st) {
+  count_launch();
+  lz_gemv_kernel<float><<<lanczos_blocks(n_local), kLzThreads, 0, st>>>(
+      A, lda, n_local, n, q, Q, ldq, j, w, h, partials, counter, state);
   return cudaGetLastError();
 }
 

@@ -597,7 +597,7 @@ __global__ void spectral_kernel(int op, double thr, const double* __restrict__ t
 cudaError_t spectral_launch(int op, double thr, const double* theta, int p, double* f, int* rank,
                             DevState* state, cudaStream_t st) {
   count_launch();
-  spectral_kernel<<<1, 128, 0, st>>>(op, thr, theta, p, f, rank, state);
+  spectral_kernel<<<1, kMaxP, 0, st>>>(op, thr, theta, p, f, rank, state);
   return cudaGetLastError();
 }
 
@@ -694,7 +694,7 @@ __global__ void copy_theta_kernel(const double* theta, int p, DevState* state) {
 
 cudaError_t copy_theta_launch(const double* theta, int p, DevState* state, cudaStream_t st) {
   count_launch();
-  copy_theta_kernel<<<1, 128, 0, st>>>(theta, p, state);
+  copy_theta_kernel<<<1, kMaxP, 0, st>>>(theta, p, state);
   return cudaGetLastError();
 }
 

@@ -11,9 +11,9 @@ import numpy as np
 import torch
 
 from pfinputs import (Config, initial_block, lanczos_start, cfg1_problem, cfg1_noise, pfpg_problem,
-                      pfam_problem)
+                      pfam_problem, cfg5_problem)
 
-from ._lib import Context, PF_OP_PSD, PF_OP_SOFT_THRESHOLD
+from ._lib import Context, PF_FP64, PF_TF32, PF_OP_PSD, PF_OP_SOFT_THRESHOLD
 
 
 def _dev(x, dtype=torch.float64):
@@ -40,7 +40,9 @@ class Solver:
         self.cfg = cfg
         n, p, d = cfg.n, cfg.p, cfg.d
         self.stream = stream
-        self.ctx = Context(n, p, d, nccl_id=nccl_id, rank=rank, world=world)
+        self.f32 = cfg.dtype == "tf32"   # fp32 storage, TF32 tensor-core filter (config 5)
+        self.ctx = Context(n, p, d, nccl_id=nccl_id, rank=rank, world=world,
+                           dtype=PF_TF32 if self.f32 else PF_FP64)
         r0, r1 = rows_of(n, rank, world) if nccl_id is not None else (0, n)
         self.r0, self.r1, self.n_local = r0, r1, r1 - r0
         assert self.n_local == self.ctx.n_local
@@ -49,8 +51,13 @@ class Solver:
         self.op = PF_OP_PSD if self.psd else PF_OP_SOFT_THRESHOLD
         # problem["_dev"]: inputs already on the device (the e2e path uploads them itself)
         devp = (problem or {}).get("_dev") or {}
-        self.U = devp["U0"] if "U0" in devp else _dev(initial_block(cfg)[r0:r1])
-        self.V = torch.empty((nl, p), dtype=torch.float64, device="cuda")
+        if self.f32:  # p-major fp32 blocks: tensors of shape (p, n_local)
+            self.U = devp["U0"] if "U0" in devp else \
+                _dev(np.ascontiguousarray(initial_block(cfg)[r0:r1].T), torch.float32)
+            self.V = torch.empty((p, nl), dtype=torch.float32, device="cuda")
+        else:
+            self.U = devp["U0"] if "U0" in devp else _dev(initial_block(cfg)[r0:r1])
+            self.V = torch.empty((nl, p), dtype=torch.float64, device="cuda")
         self.theta = torch.empty(p, dtype=torch.float64, device="cuda")
         self.f = torch.zeros(p, dtype=torch.float64, device="cuda")
         self.rank = torch.zeros(1, dtype=torch.int32, device="cuda")
@@ -59,7 +66,17 @@ class Solver:
         self.interval = torch.zeros(2, dtype=torch.float64, device="cuda")
         self.k = 0
         self.thr = 0.0
-        if cfg.mode in ("sweep_psd", "sweep_soft"):
+        if cfg.mode in ("sweep_psd", "sweep_soft") and cfg.gen == "cfg5":
+            if "A0" in devp:
+                self.A = devp["A0"]
+            else:
+                A0 = cfg5_problem(cfg) if problem is None else problem["A0"]
+                # 16-byte row pitch for the TMA descriptors (include/pf.h: lda % 4 == 0)
+                buf = torch.empty((nl, (n + 3) // 4 * 4), dtype=torch.float32, device="cuda")
+                buf[:, :n].copy_(torch.from_numpy(np.ascontiguousarray(A0[r0:r1])))
+                self.A = buf[:, :n]
+            self.thr = cfg.theta
+        elif cfg.mode in ("sweep_psd", "sweep_soft"):
             A0 = cfg1_problem(cfg) if problem is None else problem["A0"]
             self.A = _dev(A0[r0:r1])
             self.thr = cfg.theta
@@ -123,6 +140,15 @@ class Solver:
     def perturb(self, E: torch.Tensor):
         self.ctx.perturb(self.A, E, self.stream)
 
+    def perturb_hash(self, k: int):
+        """Config-5 workload noise E_k generated on the device (pfinputs.hash_gauss)."""
+        self.ctx.perturb_hash(self.A, self.cfg.seed, k, self.cfg.noise, self.stream)
+
+    def ritz_factors(self) -> np.ndarray:
+        """Ritz vectors of the last iteration as an (n_local x p) fp64 host array."""
+        v = self.ritz.cpu().numpy()
+        return (v.T if self.f32 else v).astype(np.float64)
+
     def objective(self) -> tuple[float, float]:
         """(objective, aux) on the host: PFPG (fit + mu sum|f|, fit); PFAM (<C,W>, ||dZ||_F)."""
         o = self.obj.cpu().numpy()
@@ -144,11 +170,14 @@ def run(cfg: Config, iters: int | None = None, record: bool = True, problem=None
             f = s.f.cpu().numpy()
             keep = f != 0.0
             rec.update(theta=s.theta.cpu().numpy(), rank=int(s.rank.item()),
-                       V=s.ritz.cpu().numpy()[:, keep], f=f[keep])
+                       V=s.ritz_factors()[:, keep], f=f[keep])
             if cfg.mode in ("pfpg", "pfam"):
                 rec["objective"], rec["aux"] = s.objective()
         if cfg.mode in ("sweep_psd", "sweep_soft") and k + 1 < K:
-            s.perturb(_dev(cfg1_noise(cfg, k)[s.r0:s.r1]))
+            if cfg.gen == "cfg5":
+                s.perturb_hash(k)
+            else:
+                s.perturb(_dev(cfg1_noise(cfg, k)[s.r0:s.r1]))
         recs.append(rec)
     torch.cuda.synchronize()
     return {"records": recs, "status": s.ctx.status(), "solver": s}

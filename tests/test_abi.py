@@ -35,6 +35,14 @@ def test_argument_errors_are_synchronous_without_gpu():
     assert lib.pf_create(10, 16, 4, 0, ctypes.byref(h)) == 2       # n < p -> DIM
     assert lib.pf_create(100, 16, 0, 0, ctypes.byref(h)) == 1      # degree < 1 -> ARG
     assert lib.pf_create(100, 16, 4, 3, ctypes.byref(h)) == 7      # dtype -> UNSUPPORTED
+    assert lib.pf_create(100, 16, 4, 1, ctypes.byref(h)) == 7      # PF_FP32 reserved
+    # PF_TF32 (config 5): p in {64, 128, 256, 512}
+    assert lib.pf_create(1000, 16, 4, 2, ctypes.byref(h)) == 2
+    assert lib.pf_create(1000, 96, 4, 2, ctypes.byref(h)) == 2
+    assert lib.pf_create(300, 512, 4, 2, ctypes.byref(h)) == 2     # n < p
+    nid = ctypes.create_string_buffer(128)
+    assert lib.pf_create_dist(1000, 64, 4, 2, nid, 0, 1, ctypes.byref(h)) == 7  # single-GPU only
+    assert lib.pf_set_tf32_passes(None, 3) == 1
     assert lib.pf_status_string(3) == b"PF_ERR_INTERVAL"
 
 

@@ -26,14 +26,15 @@ void tf32_trace_read(unsigned long long* host);
     }                                                                               \
   } while (0)
 
-__global__ void fill(float* x, size_t n, unsigned long long seed) {
+__global__ void fill(float* x, size_t n, unsigned long long seed, int positive) {
   size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   for (; i < n; i += (size_t)gridDim.x * blockDim.x) {
     unsigned long long z = seed + i * 0x9E3779B97F4A7C15ull;
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
     z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
     z ^= z >> 31;
-    x[i] = (float)((double)(z >> 11) * (1.0 / 9007199254740992.0) * 2.0 - 1.0);
+    const double u = (double)(z >> 11) * (1.0 / 9007199254740992.0);
+    x[i] = (float)(positive ? u : u * 2.0 - 1.0);
   }
 }
 
@@ -60,6 +61,7 @@ int main(int argc, char** argv) {
   int reps = argc > 5 ? atoi(argv[5]) : 0;
   int row_stride = argc > 6 ? atoi(argv[6]) : 1;
   int dbg = argc > 7 ? atoi(argv[7]) : 0;
+  int positive = argc > 8 ? atoi(argv[8]) : 0;
   int64_t lda = (nk + 3) / 4 * 4, ldy = (std::max(rows, nk) + 3) / 4 * 4;
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
@@ -73,16 +75,19 @@ int main(int argc, char** argv) {
   CK(cudaMalloc(&out, sizeof(float) * p * ldy));
   CK(cudaMalloc(&ref, sizeof(double) * p * ldy));
   CK(cudaMalloc(&bound, sizeof(double) * p * ldy));
-  fill<<<1024, 256>>>(A, (size_t)rows * lda, 1);
-  fill<<<1024, 256>>>(Y, (size_t)p * ldy, 2);
-  fill<<<1024, 256>>>(yc, (size_t)p * ldy, 3);
-  fill<<<1024, 256>>>(yp, (size_t)p * ldy, 4);
+  fill<<<1024, 256>>>(A, (size_t)rows * lda, 1, positive);
+  fill<<<1024, 256>>>(Y, (size_t)p * ldy, 2, positive);
+  fill<<<1024, 256>>>(yc, (size_t)p * ldy, 3, positive);
+  fill<<<1024, 256>>>(yp, (size_t)p * ldy, 4, positive);
   CK(cudaMemset(out, 0, sizeof(float) * p * ldy));
   double hc[3] = {0.75, -0.5, -1.0};
   CK(cudaMalloc(&coef, sizeof(hc)));
   CK(cudaMemcpy(coef, hc, sizeof(hc), cudaMemcpyHostToDevice));
   pf::Tf32Plan pl = pf::tf32_plan(p, rows, nk, sms);
   CK(cudaMalloc(&ws, sizeof(float) * pl.ws_floats));
+  float* accb;
+  CK(cudaMalloc(&accb, sizeof(float) * pl.acc_floats));
+  if (getenv("CHUNK_KB")) pl.chunk_kb = atoi(getenv("CHUNK_KB"));
   CK(cudaMalloc(&cnt, sizeof(int) * pl.counters));
   CK(cudaMemset(cnt, 0, sizeof(int) * pl.counters));
   CUtensorMap mA, mB, mApf;
@@ -92,7 +97,7 @@ int main(int argc, char** argv) {
   }
   printf("rows %d nk %d p %d npass %d: pairs %d split %d mtiles %d kblocks %d\n", rows, nk, p, npass, pl.pairs,
          pl.split, pl.mtiles, pl.kblocks);
-  CK(pf::tf32_gemm_launch(pl, mA, mB, mApf, yc, yp, out, ldy, coef, ws, cnt, npass, 0));
+  CK(pf::tf32_gemm_launch(pl, mA, mB, mApf, yc, yp, out, ldy, coef, ws, accb, cnt, npass, 0));
   CK(cudaDeviceSynchronize());
   dim3 rg((rows / row_stride + 127) / 128, p);
   ref_kernel<<<rg, 128>>>(A, lda, Y, ldy, rows, nk, p, yc, yp, hc[0], hc[1], hc[2], ref, bound,
@@ -117,16 +122,24 @@ int main(int argc, char** argv) {
         ++bad;
       }
     }
-  printf("max |err|/bound = %.3e  max |err| = %.3e  bad = %ld\n", maxrel, maxabs, bad);
+  double bias = 0, nb = 0;
+  for (int c = 0; c < p; ++c)
+    for (int i = 0; i < rows; i += row_stride) {
+      size_t o = (size_t)c * ldy + i;
+      bias += ((double)ho[o] - hr[o]) / (hb[o] > 0 ? hb[o] : 1.0);
+      nb += 1;
+    }
+  printf("max |err|/bound = %.3e  max |err| = %.3e  mean signed err/bound = %.3e  bad = %ld\n",
+         maxrel, maxabs, bias / nb, bad);
   if (reps > 0) {
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
     for (int w = 0; w < 2; ++w)
-      CK(pf::tf32_gemm_launch(pl, mA, mB, mApf, yc, yp, out, ldy, coef, ws, cnt, npass, 0));
+      CK(pf::tf32_gemm_launch(pl, mA, mB, mApf, yc, yp, out, ldy, coef, ws, accb, cnt, npass, 0));
     CK(cudaEventRecord(e0));
     for (int r = 0; r < reps; ++r)
-      CK(pf::tf32_gemm_launch(pl, mA, mB, mApf, yc, yp, out, ldy, coef, ws, cnt, npass, 0));
+      CK(pf::tf32_gemm_launch(pl, mA, mB, mApf, yc, yp, out, ldy, coef, ws, accb, cnt, npass, 0));
     CK(cudaEventRecord(e1));
     CK(cudaEventSynchronize(e1));
     float ms;
@@ -138,7 +151,7 @@ int main(int argc, char** argv) {
   }
 #ifdef PF_TRACE
   {
-    CK(pf::tf32_gemm_launch(pl, mA, mB, mApf, yc, yp, out, ldy, coef, ws, cnt, npass, 0));
+    CK(pf::tf32_gemm_launch(pl, mA, mB, mApf, yc, yp, out, ldy, coef, ws, accb, cnt, npass, 0));
     CK(cudaDeviceSynchronize());
     static unsigned long long tr[12][512];
     pf::tf32_trace_read(&tr[0][0]);
