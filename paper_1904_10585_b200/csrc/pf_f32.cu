@@ -575,8 +575,8 @@ __host__ __device__ __forceinline__ unsigned long long mix64(unsigned long long 
 
 __global__ void perturb_hash32_kernel(float* A, int64_t lda, int rows, int cols, int row0,
                                       unsigned long long key, double noise) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  const int r = blockIdx.y;
+  const int j = blockIdx.y * blockDim.x + threadIdx.x;  // rows on x: gridDim.y <= 65535
+  const int r = blockIdx.x;
   if (j >= cols || r >= rows) return;
   const unsigned long long i = (unsigned long long)(row0 + r), jj = (unsigned long long)j;
   const unsigned long long lo = i < jj ? i : jj, hi = i < jj ? jj : i;
@@ -594,7 +594,7 @@ __global__ void perturb_hash32_kernel(float* A, int64_t lda, int rows, int cols,
 cudaError_t perturb_hash32_launch(float* A, int64_t lda, int rows, int cols, int row0,
                                   unsigned long long seed, int k, double noise, cudaStream_t st) {
   const unsigned long long key = mix64(seed * (1ull << 32) + (unsigned long long)k);
-  dim3 grid((cols + 255) / 256, rows);
+  dim3 grid(rows, (cols + 255) / 256);
   count_launch();
   perturb_hash32_kernel<<<grid, 256, 0, st>>>(A, lda, rows, cols, row0, key, noise);
   return cudaGetLastError();

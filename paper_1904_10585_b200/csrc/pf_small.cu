@@ -701,14 +701,14 @@ cudaError_t copy_theta_launch(const double* theta, int p, DevState* state, cudaS
 // =============================================================================== perturb
 __global__ void perturb_kernel(double* A, int64_t lda, const double* E, int64_t lde, int rows,
                                int cols) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  const int r = blockIdx.y;
+  const int c = blockIdx.y * blockDim.x + threadIdx.x;  // rows on x: gridDim.y <= 65535
+  const int r = blockIdx.x;
   if (c < cols && r < rows) A[(size_t)r * lda + c] += E[(size_t)r * lde + c];
 }
 
 cudaError_t perturb_launch(double* A, int64_t lda, const double* E, int64_t lde, int rows,
                            int cols, cudaStream_t st) {
-  dim3 grid((cols + 255) / 256, rows);
+  dim3 grid(rows, (cols + 255) / 256);
   count_launch();
   perturb_kernel<<<grid, 256, 0, st>>>(A, lda, E, lde, rows, cols);
   return cudaGetLastError();
