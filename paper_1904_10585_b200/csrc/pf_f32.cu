@@ -30,8 +30,9 @@ __global__ void __launch_bounds__(256) gram32_kernel(const float* __restrict__ X
                                                      double* __restrict__ partials,
                                                      const int* cond) {
   if (cond && *cond == 0) return;
-  __shared__ double Xs[G32_T][G32_LD];
-  __shared__ double Ys[G32_T][G32_LD];
+  extern __shared__ __align__(16) unsigned char g32_smem[];
+  double(*Xs)[G32_T][G32_LD] = reinterpret_cast<double(*)[G32_T][G32_LD]>(g32_smem);
+  double(*Ys)[G32_T][G32_LD] = Xs + 2;
   const int nt = p / G32_T;
   int tile = blockIdx.x, ta = 0, tb = 0;
   if (sym) {  // upper-triangular tile pairs ta <= tb
@@ -58,31 +59,52 @@ __global__ void __launch_bounds__(256) gram32_kernel(const float* __restrict__ X
       for (int e = 0; e < 4; ++e) acc[a][b][e] = 0.0;
   const float* xb = X + (size_t)(ta * G32_T) * ldx;
   const float* yb = Y + (size_t)(tb * G32_T) * ldy;
-  for (int k = k0; k < k1; k += G32_KC) {
+  constexpr int PER = (G32_T * G32_KC) / 256;  // 8 elements of X and of Y per thread
+  float rx[PER], ry[PER];
+  auto fetch = [&](int k) {
 #pragma unroll
-    for (int u = 0; u < (G32_T * G32_KC) / 256; ++u) {
+    for (int u = 0; u < PER; ++u) {
       const int e = tid + 256 * u, r = e / G32_KC, c = e % G32_KC;
       const bool ok = k + c < k1;
-      Xs[r][c] = ok ? (double)xb[(size_t)r * ldx + k + c] : 0.0;
-      Ys[r][c] = ok ? (double)yb[(size_t)r * ldy + k + c] : 0.0;
+      rx[u] = ok ? xb[(size_t)r * ldx + k + c] : 0.f;
+      ry[u] = ok ? yb[(size_t)r * ldy + k + c] : 0.f;
     }
-    __syncthreads();
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = tid + 256 * u, r = e / G32_KC, c = e % G32_KC;
+      Xs[buf][r][c] = (double)rx[u];
+      Ys[buf][r][c] = (double)ry[u];
+    }
+  };
+  if (k0 < k1) {
+    fetch(k0);
+    stash(0);
+  }
+  __syncthreads();
+  int buf = 0;
+  for (int k = k0; k < k1; k += G32_KC) {
+    const bool more = k + G32_KC < k1;
+    if (more) fetch(k + G32_KC);  // global loads in flight during the DMMAs below
 #pragma unroll
     for (int kk = 0; kk < G32_KC; kk += 4) {
       double af[2][2], bf[2];
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) {
-        af[mt][0] = Xs[wm * 32 + mt * 16 + g8][kk + t4];
-        af[mt][1] = Xs[wm * 32 + mt * 16 + g8 + 8][kk + t4];
+        af[mt][0] = Xs[buf][wm * 32 + mt * 16 + g8][kk + t4];
+        af[mt][1] = Xs[buf][wm * 32 + mt * 16 + g8 + 8][kk + t4];
       }
 #pragma unroll
-      for (int nt2 = 0; nt2 < 2; ++nt2) bf[nt2] = Ys[wn * 16 + nt2 * 8 + g8][kk + t4];
+      for (int nt2 = 0; nt2 < 2; ++nt2) bf[nt2] = Ys[buf][wn * 16 + nt2 * 8 + g8][kk + t4];
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
         for (int nt2 = 0; nt2 < 2; ++nt2) dmma16884(acc[mt][nt2], af[mt][0], af[mt][1], bf[nt2]);
     }
+    if (more) stash(buf ^ 1);
     __syncthreads();
+    buf ^= 1;
   }
   double* out = partials + (size_t)slice * p * p;
 #pragma unroll
@@ -129,8 +151,14 @@ cudaError_t gram32_launch(const float* X, int64_t ldx, const float* Y, int64_t l
   const int nt = p / G32_T;
   const int sym = (X == Y && ldx == ldy) ? 1 : 0;
   dim3 grid(sym ? nt * (nt + 1) / 2 : nt * nt, nslices);
+  const int smem = 4 * G32_T * G32_LD * (int)sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gram32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
   count_launch();
-  gram32_kernel<<<grid, 256, 0, st>>>(X, ldx, Y, ldy, n_rows, p, nslices, sym, partials, cond);
+  gram32_kernel<<<grid, 256, smem, st>>>(X, ldx, Y, ldy, n_rows, p, nslices, sym, partials, cond);
   count_launch();
   gram32_reduce_kernel<<<(p * p + 255) / 256, 256, 0, st>>>(partials, nslices, p, sym, G, cond);
   return cudaGetLastError();
@@ -150,7 +178,7 @@ __global__ void __launch_bounds__(256) rmul32_kernel(const float* in, int64_t ld
   extern __shared__ __align__(16) unsigned char rm_smem[];
   const int LDI = RM_BI + 4;  // fp32 row pitch of the staged block
   float* Ins = reinterpret_cast<float*>(rm_smem);                                  // p x LDI
-  double* Rs = reinterpret_cast<double*>(rm_smem + (size_t)p * LDI * 4);           // KC x 68
+  double* Rs = reinterpret_cast<double*>(rm_smem + (size_t)p * LDI * 4);           // 2 x KC x 68
   const int i0 = blockIdx.x * RM_BI;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wm = warp >> 2, wn = warp & 3, g8 = lane >> 2, t4 = lane & 3;
@@ -158,60 +186,83 @@ __global__ void __launch_bounds__(256) rmul32_kernel(const float* in, int64_t ld
     const int r = e / RM_BI, c = e % RM_BI;
     Ins[r * LDI + c] = (i0 + c < n_rows) ? in[(size_t)r * ldi + i0 + c] : 0.f;
   }
-  __syncthreads();
-  for (int c0 = 0; c0 < p; c0 += 64) {
-    double acc[2][2][4];
+  // chunk t = (c-tile ct, a-chunk ac): R[ac*KC .. +KC][ct*64 .. +64], 8 doubles per thread,
+  // prefetched into registers one chunk ahead (one barrier per chunk)
+  const int nac = p / RM_KC, nch = (p / 64) * nac;
+  double rr[8];
+  auto fetch = [&](int t) {
+    const int c0 = (t / nac) * 64, a0 = (t % nac) * RM_KC;
 #pragma unroll
-    for (int a = 0; a < 2; ++a)
-#pragma unroll
-      for (int b = 0; b < 2; ++b)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) acc[a][b][e] = 0.0;
-    for (int a0 = 0; a0 < p; a0 += RM_KC) {
-      for (int e = tid; e < RM_KC * 64; e += 256) {
-        const int r = e / 64, c = e % 64;
-        Rs[r * 68 + c] = R[(size_t)(a0 + r) * p + c0 + c];
-      }
-      __syncthreads();
-#pragma unroll
-      for (int kk = 0; kk < RM_KC; kk += 4) {
-        double af[2][2], bf[2];
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {  // A(m = c, k = a) = R[a][c]
-          af[mt][0] = Rs[(kk + t4) * 68 + wm * 32 + mt * 16 + g8];
-          af[mt][1] = Rs[(kk + t4) * 68 + wm * 32 + mt * 16 + g8 + 8];
-        }
-#pragma unroll
-        for (int nt2 = 0; nt2 < 2; ++nt2)  // B(k = a, n = i) = in[a][i]
-          bf[nt2] = (double)Ins[(a0 + kk + t4) * LDI + wn * 16 + nt2 * 8 + g8];
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-          for (int nt2 = 0; nt2 < 2; ++nt2) dmma16884(acc[mt][nt2], af[mt][0], af[mt][1], bf[nt2]);
-      }
-      __syncthreads();
+    for (int u = 0; u < 8; ++u) {
+      const int e = tid + 256 * u, r = e / 64, c = e % 64;
+      rr[u] = R[(size_t)(a0 + r) * p + c0 + c];
     }
+  };
+  auto stash = [&](int buf) {
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
+    for (int u = 0; u < 8; ++u) {
+      const int e = tid + 256 * u, r = e / 64, c = e % 64;
+      Rs[buf * RM_KC * 68 + r * 68 + c] = rr[u];
+    }
+  };
+  fetch(0);
+  stash(0);
+  __syncthreads();
+  double acc[2][2][4];
+  for (int t = 0; t < nch; ++t) {
+    const int buf = t & 1, ac = t % nac, c0 = (t / nac) * 64, a0 = ac * RM_KC;
+    if (ac == 0) {
 #pragma unroll
-      for (int nt2 = 0; nt2 < 2; ++nt2)
+      for (int a = 0; a < 2; ++a)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int c = c0 + wm * 32 + mt * 16 + g8 + 8 * h;
-          const int i = i0 + wn * 16 + nt2 * 8 + 2 * t4;
-          if (i < n_rows) out[(size_t)c * ldo + i] = (float)acc[mt][nt2][2 * h];
-          if (i + 1 < n_rows) out[(size_t)c * ldo + i + 1] = (float)acc[mt][nt2][2 * h + 1];
-        }
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[a][b][e] = 0.0;
+    }
+    const bool more = t + 1 < nch;
+    if (more) fetch(t + 1);
+    const double* Rb = Rs + buf * RM_KC * 68;
+#pragma unroll
+    for (int kk = 0; kk < RM_KC; kk += 4) {
+      double af[2][2], bf[2];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {  // A(m = c, k = a) = R[a][c]
+        af[mt][0] = Rb[(kk + t4) * 68 + wm * 32 + mt * 16 + g8];
+        af[mt][1] = Rb[(kk + t4) * 68 + wm * 32 + mt * 16 + g8 + 8];
+      }
+#pragma unroll
+      for (int nt2 = 0; nt2 < 2; ++nt2)  // B(k = a, n = i) = in[a][i]
+        bf[nt2] = (double)Ins[(a0 + kk + t4) * LDI + wn * 16 + nt2 * 8 + g8];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt2 = 0; nt2 < 2; ++nt2) dmma16884(acc[mt][nt2], af[mt][0], af[mt][1], bf[nt2]);
+    }
+    if (more) stash(buf ^ 1);
+    if (ac == nac - 1) {
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt2 = 0; nt2 < 2; ++nt2)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = c0 + wm * 32 + mt * 16 + g8 + 8 * h;
+            const int i = i0 + wn * 16 + nt2 * 8 + 2 * t4;
+            if (i < n_rows) out[(size_t)c * ldo + i] = (float)acc[mt][nt2][2 * h];
+            if (i + 1 < n_rows) out[(size_t)c * ldo + i + 1] = (float)acc[mt][nt2][2 * h + 1];
+          }
+    }
+    __syncthreads();
   }
 }
 
 cudaError_t rmul32_launch(const float* in, int64_t ldi, const double* R, float* out, int64_t ldo,
                           int n_rows, int p, const int* cond, cudaStream_t st) {
-  const size_t smem = (size_t)p * (RM_BI + 4) * 4 + (size_t)RM_KC * 68 * 8;
+  const size_t smem = (size_t)p * (RM_BI + 4) * 4 + (size_t)2 * RM_KC * 68 * 8;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(rmul32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(512 * (RM_BI + 4) * 4 + RM_KC * 68 * 8));
+                         (int)(512 * (RM_BI + 4) * 4 + 2 * RM_KC * 68 * 8));
     attr = true;
   }
   count_launch();
@@ -290,15 +341,42 @@ __global__ void __launch_bounds__(1024) chol_inv_big_kernel(const double* __rest
         const int r = e / CB, c = e % CB;
         if (c <= r) W[(size_t)(J + r) * p + J + c] = cs[r * CB_LD + c];
       }
-      // trailing update of the lower triangle: W[i][k] -= sum_c P[i][c] P[k][c], J+32 <= k <= i
-      for (int i = J + CB + ty; i < p; i += 32) {
-        const double* pi = cs + (i - J) * CB_LD;
-        for (int k = J + CB + tx; k <= i; k += 32) {
-          const double* pk = cs + (k - J) * CB_LD;
-          double s = 0.0;
+      // trailing update of the lower triangle: W[i][k] -= sum_c P[i][c] P[k][c], J+32 <= k <= i,
+      // in 4 x 4 register tiles (8 shared loads per 16 FMAs instead of 2 per FMA)
+      {
+        const int R4 = (p - J - CB) / 4;  // p - J - CB is a multiple of 32
+        const int ntile = R4 * (R4 + 1) / 2;
+        for (int e = tid; e < ntile; e += 1024) {
+          int ti = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+          while (ti * (ti + 1) / 2 > e) --ti;
+          while ((ti + 1) * (ti + 2) / 2 <= e) ++ti;
+          const int tk = e - ti * (ti + 1) / 2;  // tk <= ti
+          const double* pi = cs + (CB + 4 * ti) * CB_LD;
+          const double* pk = cs + (CB + 4 * tk) * CB_LD;
+          double acc[4][4];
 #pragma unroll
-          for (int c = 0; c < CB; ++c) s += pi[c] * pk[c];
-          W[(size_t)i * p + k] -= s;
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+#pragma unroll 8
+          for (int c = 0; c < CB; ++c) {
+            double xi[4], xk[4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+              xi[a] = pi[a * CB_LD + c];
+              xk[a] = pk[a * CB_LD + c];
+            }
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+              for (int b = 0; b < 4; ++b) acc[a][b] += xi[a] * xk[b];
+          }
+          const int i0 = J + CB + 4 * ti, k0 = J + CB + 4 * tk;
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+              if (k0 + b <= i0 + a) W[(size_t)(i0 + a) * p + k0 + b] -= acc[a][b];
         }
       }
       __syncthreads();
@@ -341,9 +419,17 @@ __global__ void __launch_bounds__(1024) chol_inv_big_kernel(const double* __rest
   for (int C = 0; C < p; C += CB) {
     for (int I = C; I < p; I += CB) {
       // s = E[I, C] - L[I, C:I] X[C:I, C]  (thread (ty, tx) = element (I + ty, C + tx))
+      // warp ty owns row I + ty of L: 32 consecutive entries per coalesced load, broadcast by
+      // shuffles (the old per-thread walk along the row was L2-latency bound)
       double s = (I == C && ty == tx) ? 1.0 : 0.0;
       const double* lrow = W + (size_t)(I + ty) * p;
-      for (int k = C; k < I; ++k) s -= lrow[k] * cs[(k - C) * CB_LD + tx];
+#pragma unroll 2
+      for (int k0 = C; k0 < I; k0 += 32) {
+        const double lv = lrow[k0 + tx];
+#pragma unroll
+        for (int q = 0; q < 32; ++q)
+          s -= __shfl_sync(0xffffffffu, lv, q) * cs[(k0 + q - C) * CB_LD + tx];
+      }
       T[ty * CB_LD + tx] = s;
       __syncthreads();
       const double* di = Dinv + (size_t)(I / CB) * CB * CB + ty * CB;
@@ -390,9 +476,21 @@ cudaError_t chol_inv_big_launch(const double* G, int p, int64_t n_global, double
 // in place, then one grid barrier per round.
 constexpr int JB_THREADS = 512;
 
+// block e of the packed upper triangle of pairs (a <= b) over `half` pairs
+__device__ __forceinline__ void jb_decode(int e, int half, int& a, int& b) {
+  // a = largest a with S(a) = a*half - a(a-1)/2 <= e
+  const double h = (double)half + 0.5;
+  int aa = (int)floor(h - sqrt(h * h - 2.0 * (double)e));
+  aa = max(0, min(half - 1, aa));
+  while (aa > 0 && aa * half - aa * (aa - 1) / 2 > e) --aa;
+  while (aa + 1 < half && (aa + 1) * half - (aa + 1) * aa / 2 <= e) ++aa;
+  a = aa;
+  b = aa + (e - (aa * half - aa * (aa - 1) / 2));
+}
+
 __global__ void __launch_bounds__(JB_THREADS) jacobi_big_kernel(
     const double* __restrict__ Hin, int p, double* __restrict__ theta, double* __restrict__ Yout,
-    double* H0, double* V, double* red_ws, int* cnt_ws, DevState* state, double tol,
+    double* H0, double* Vt_, double* red_ws, int* cnt_ws, DevState* state, double tol,
     int max_sweeps) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double csv[3 * 256];
@@ -401,11 +499,14 @@ __global__ void __launch_bounds__(JB_THREADS) jacobi_big_kernel(
   __shared__ int s_cnt;
   const int tid = threadIdx.x, half = p / 2;
   const int gtid = blockIdx.x * JB_THREADS + tid, gthreads = gridDim.x * JB_THREADS;
+  const int nblk = half * (half + 1) / 2;
   double* Hb[2] = {H0, H0 + (size_t)p * p};
+  double* __restrict__ Vt = Vt_;  // Vt[i][row] = V[row][i]: rotating columns i, j of V
+                                  // rotates two contiguous rows of Vt (coalesced)
   for (int e = gtid; e < p * p; e += gthreads) {
     const int i = e / p, j = e % p;
     Hb[0][e] = 0.5 * (Hin[(size_t)i * p + j] + Hin[(size_t)j * p + i]);
-    V[e] = (i == j) ? 1.0 : 0.0;
+    Vt[e] = (i == j) ? 1.0 : 0.0;
   }
   grid.sync();
   int cur = 0;
@@ -413,7 +514,6 @@ __global__ void __launch_bounds__(JB_THREADS) jacobi_big_kernel(
   bool converged = false;
   for (; sweep < max_sweeps; ++sweep) {
     const double* H = Hb[cur];
-    // ||H||_F^2 and off(H)^2: per-CTA partials, summed by every CTA in CTA order
     double off = 0.0, tot = 0.0;
     for (int e = gtid; e < p * p; e += gthreads) {
       const double v = H[e];
@@ -441,8 +541,8 @@ __global__ void __launch_bounds__(JB_THREADS) jacobi_big_kernel(
     if (tid == 0) s_cnt = 0;
     __syncthreads();
     for (int r = 0; r < p - 1; ++r) {
-      const double* Hc = Hb[cur];
-      double* Hn = Hb[cur ^ 1];
+      const double* __restrict__ Hc = Hb[cur];
+      double* __restrict__ Hn = Hb[cur ^ 1];
       if (tid < half) {
         const int m = tid;
         int a, b;
@@ -456,10 +556,10 @@ __global__ void __launch_bounds__(JB_THREADS) jacobi_big_kernel(
         const int i = a < b ? a : b, j = a < b ? b : a;
         pii[m] = i;
         pjj[m] = j;
-        double c = 1.0, s = 0.0, t = 0.0;
         const double hij = Hc[(size_t)i * p + j];
+        const double hii = Hc[(size_t)i * p + i], hjj = Hc[(size_t)j * p + j];
+        double c = 1.0, s = 0.0, t = 0.0;
         if (fabs(hij) > 1e-16 * s_norm) {
-          const double hii = Hc[(size_t)i * p + i], hjj = Hc[(size_t)j * p + j];
           const double dd = hjj - hii, ee = 2.0 * hij;
           const double ir = rsqrt(dd * dd + ee * ee);
           const double hh = 0.5 + 0.5 * fabs(dd) * ir;
@@ -474,9 +574,9 @@ __global__ void __launch_bounds__(JB_THREADS) jacobi_big_kernel(
         csv[3 * m + 2] = t;
       }
       __syncthreads();
-      for (int e = gtid; e < half * half; e += gthreads) {
-        const int a = e / half, b = e % half;
-        if (a > b) continue;
+      for (int e = gtid; e < nblk; e += gthreads) {
+        int a, b;
+        jb_decode(e, half, a, b);
         const int ia = pii[a], ja = pjj[a];
         const double ca = csv[3 * a], sa = csv[3 * a + 1];
         if (a == b) {
@@ -507,18 +607,26 @@ __global__ void __launch_bounds__(JB_THREADS) jacobi_big_kernel(
           Hn[(size_t)jb * p + ja] = n22;
         }
       }
-      for (int e = gtid; e < p * half; e += gthreads) {
-        const int row = e / half, m = e % half;
+      // V <- V J: rows i, j of Vt, 4 consecutive entries per thread (loads before stores)
+      for (int e = gtid; e < half * (p / 4); e += gthreads) {
+        const int m = e / (p / 4), c4 = (e % (p / 4)) * 4;
         const double c = csv[3 * m], s = csv[3 * m + 1];
         if (s != 0.0) {
-          const int i = pii[m], j = pjj[m];
-          const double vi = V[(size_t)row * p + i], vj = V[(size_t)row * p + j];
-          V[(size_t)row * p + i] = c * vi - s * vj;
-          V[(size_t)row * p + j] = s * vi + c * vj;
+          double* vi = Vt + (size_t)pii[m] * p + c4;
+          double* vj = Vt + (size_t)pjj[m] * p + c4;
+          const double4 xi = *reinterpret_cast<const double4*>(vi);
+          const double4 xj = *reinterpret_cast<const double4*>(vj);
+          double4 yi, yj;
+          yi.x = c * xi.x - s * xj.x; yj.x = s * xi.x + c * xj.x;
+          yi.y = c * xi.y - s * xj.y; yj.y = s * xi.y + c * xj.y;
+          yi.z = c * xi.z - s * xj.z; yj.z = s * xi.z + c * xj.z;
+          yi.w = c * xi.w - s * xj.w; yj.w = s * xi.w + c * xj.w;
+          *reinterpret_cast<double4*>(vi) = yi;
+          *reinterpret_cast<double4*>(vj) = yj;
         }
       }
       cur ^= 1;
-      grid.sync();  // also orders this round's smem pairs/rotations before the next overwrite
+      grid.sync();
     }
     if (blockIdx.x == 0 && tid == 0) cnt_ws[0] = s_cnt;
     grid.sync();
@@ -534,21 +642,22 @@ __global__ void __launch_bounds__(JB_THREADS) jacobi_big_kernel(
     state->scratch[1] = (double)sweep;
     if (!converged) atomicOr(&state->flags, PF_FLAG_JACOBI_MAXSWEEP);
   }
-  // sort descending (stable by index) and emit theta, Y[:, rank] = V[:, i]
+  // sort descending (stable by index); theta[rank] = H_ii, Y[:, rank] = V[:, i] = Vt[i][:]
   const double* H = Hb[cur];
-  for (int i = gtid; i < p; i += gthreads) {
+  for (int e = gtid; e < p * p; e += gthreads) {
+    const int i = e / p, row = e % p;
     const double li = H[(size_t)i * p + i];
     int rank = 0;
     for (int k = 0; k < p; ++k) {
       const double lk = H[(size_t)k * p + k];
       if (lk > li || (lk == li && k < i)) ++rank;
     }
-    theta[rank] = li;
-    for (int row = 0; row < p; ++row) Yout[(size_t)row * p + rank] = V[(size_t)row * p + i];
+    if (row == 0) theta[rank] = li;
+    Yout[(size_t)row * p + rank] = Vt[(size_t)i * p + row];
   }
 }
 
-int jacobi_big_grid() { return 32; }
+int jacobi_big_grid() { return 64; }
 
 // Hw: 2 p^2 doubles, Vw: p^2, red_ws: 2 * jacobi_big_grid() doubles, cnt_ws: 4 ints
 cudaError_t jacobi_big_launch(const double* H, int p, double* theta, double* Y, double* Hw,
