@@ -184,9 +184,17 @@ pf_status pf_perturb(pf_ctx ctx, double* A, int64_t lda, const double* E, int64_
 pf_status pf_perturb_hash(pf_ctx ctx, float* A, int64_t lda, uint64_t seed, int32_t k,
                           double noise, pf_stream stream);
 
-/* Number of TF32 MMA passes of the filter GEMM (PF_TF32 contexts): 3 (default, 3xTF32: error
- * ~ fp32) or 1 (plain TF32, operator rounded to 10 mantissa bits).  PF_ERR_ARG otherwise. */
+/* TF32 MMA passes of every filter / Rayleigh-Ritz GEMM (PF_TF32 contexts): 3 = 3xTF32
+ * (A_hi B_hi + A_lo B_hi + A_hi B_lo, error ~ fp32; the default), 2 = A_hi B_hi + A_lo B_hi (exact
+ * operator, iterate rounded to tf32), 1 = plain TF32 (operator rounded to 10 mantissa bits).
+ * PF_ERR_ARG outside 1..3. */
 pf_status pf_set_tf32_passes(pf_ctx ctx, int32_t passes);
+
+/* Precision schedule of pf_filter (PF_TF32 contexts): the first degree - exact_tail Chebyshev
+ * steps run at early_passes (1..3), the last exact_tail steps and the Rayleigh-Ritz product in
+ * 3xTF32.  Errors injected by the cheaper early steps are damped by the exact tail steps
+ * (reading R18). */
+pf_status pf_set_tf32_schedule(pf_ctx ctx, int32_t early_passes, int32_t exact_tail);
 
 #ifdef __cplusplus
 }

@@ -53,6 +53,7 @@ def load() -> ctypes.CDLL:
         "pf_perturb": [P, P, I64, P, I64, P],
         "pf_perturb_hash": [P, P, I64, ctypes.c_uint64, I32, D, P],
         "pf_set_tf32_passes": [P, I32],
+        "pf_set_tf32_schedule": [P, I32, I32],
         "pf_profile": [P, I32],
         "pf_profile_read": [P, P, ctypes.POINTER(D), ctypes.POINTER(I64)],
         "pf_kernel_launches": [],
@@ -224,3 +225,7 @@ class Context:
 
     def set_tf32_passes(self, passes: int):
         self._check(self.lib.pf_set_tf32_passes(self.h, passes), "pf_set_tf32_passes")
+
+    def set_tf32_schedule(self, early_passes: int, exact_tail: int):
+        self._check(self.lib.pf_set_tf32_schedule(self.h, early_passes, exact_tail),
+                    "pf_set_tf32_schedule")

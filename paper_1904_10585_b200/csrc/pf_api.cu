@@ -82,7 +82,9 @@ struct pf_ctx_s {
   float* tf_ws = nullptr;
   float* tf_acc = nullptr;
   int* tf_cnt = nullptr;
-  int tf_npass = 3;
+  int tf_early = 3;  // TF32 passes of the Chebyshev steps before the exact tail
+  int tf_tail = 0;   // number of final Chebyshev steps run in 3xTF32
+  int tf_rr = 3;     // passes of the Rayleigh-Ritz product A Q
   Tf32Plan tplan;
   CUtensorMap mapBf[3];
   CUtensorMap mapAf, mapApf;
@@ -487,13 +489,12 @@ static pf_status copy_block32(pf_ctx ctx, float* dst, int64_t ldd, const float* 
 }
 
 static pf_status gemm_step32(pf_ctx ctx, int bidx, const float* ycur, const float* yprev,
-                             float* out, const double* coef, cudaStream_t st) {
+                             float* out, const double* coef, int npass, cudaStream_t st) {
   const bool rec = ctx->prof && ctx->ev_used + 2 <= ctx->ev.size();
   if (ctx->prof && !rec) ++ctx->prof_dropped;
   if (rec) PF_CU(cudaEventRecord(ctx->ev[ctx->ev_used], st));
   PF_CU(tf32_gemm_launch(ctx->tplan, ctx->mapAf, ctx->mapBf[bidx], ctx->mapApf, ycur, yprev, out,
-                         ctx->ldy32, coef, ctx->tf_ws, ctx->tf_acc, ctx->tf_cnt, ctx->tf_npass,
-                         st));
+                         ctx->ldy32, coef, ctx->tf_ws, ctx->tf_acc, ctx->tf_cnt, npass, st));
   if (rec) {
     PF_CU(cudaEventRecord(ctx->ev[ctx->ev_used + 1], st));
     ctx->ev_used += 2;
@@ -543,8 +544,11 @@ static pf_status filter32(pf_ctx ctx, const float* A, int64_t lda, float* U, int
     for (int j = 0; j < d; ++j) {
       const int out = (prev < 0) ? (cur + 1) % 3 : 3 - cur - prev;
       const double* coef = &ctx->state->coef[j][0];
+      // precision schedule: early steps at tf_early passes, the last tf_tail steps in 3xTF32
+      // (errors injected by the early steps are damped by the exact tail, reading R18)
+      const int npass = (j >= d - ctx->tf_tail) ? 3 : ctx->tf_early;
       PF_TRY(gemm_step32(ctx, cur, ctx->Yf[cur], prev < 0 ? ctx->Yf[cur] : ctx->Yf[prev],
-                         ctx->Yf[out], coef, st));
+                         ctx->Yf[out], coef, npass, st));
       prev = cur;
       cur = out;
       if (j + 1 < d) {
@@ -570,7 +574,8 @@ static pf_status rayleigh_ritz32(pf_ctx ctx, const float* A, int64_t lda, const 
   PF_TRY(map_A32(ctx, A, lda));
   const int p = ctx->p, nl = (int)ctx->n_local;
   PF_TRY(copy_block32(ctx, ctx->Yf[0], ctx->ldy32, U, ldu, st));
-  PF_TRY(gemm_step32(ctx, 0, ctx->Yf[0], ctx->Yf[0], ctx->Wf, &ctx->state->coef_rr[0], st));
+  PF_TRY(gemm_step32(ctx, 0, ctx->Yf[0], ctx->Yf[0], ctx->Wf, &ctx->state->coef_rr[0], ctx->tf_rr,
+                     st));
   PF_TRY(gram32_all(ctx, ctx->Yf[0], ctx->Wf, ctx->G, nullptr, st));  // H = Q^T (A Q)
   // H is formed from fp32 blocks (relative accuracy ~1e-7): diagonalise to off(H) <= 1e-12 ||H||
   // (fp64 storage of H; eigenvector error ~1e-12 / gap, far below the fp32 data error)
@@ -818,9 +823,20 @@ pf_status pf_perturb_hash(pf_ctx ctx, float* A, int64_t lda, uint64_t seed, int3
 }
 
 pf_status pf_set_tf32_passes(pf_ctx ctx, int32_t passes) {
-  if (!ctx || (passes != 1 && passes != 3)) return PF_ERR_ARG;
+  if (!ctx || passes < 1 || passes > 3) return PF_ERR_ARG;
   if (ctx->dtype != PF_TF32) return PF_ERR_UNSUPPORTED;
-  ctx->tf_npass = passes;
+  ctx->tf_early = passes;
+  ctx->tf_tail = 0;
+  ctx->tf_rr = passes;
+  return PF_OK;
+}
+
+pf_status pf_set_tf32_schedule(pf_ctx ctx, int32_t early_passes, int32_t exact_tail) {
+  if (!ctx || early_passes < 1 || early_passes > 3 || exact_tail < 0) return PF_ERR_ARG;
+  if (ctx->dtype != PF_TF32) return PF_ERR_UNSUPPORTED;
+  ctx->tf_early = early_passes;
+  ctx->tf_tail = exact_tail;
+  ctx->tf_rr = 3;
   return PF_OK;
 }
 

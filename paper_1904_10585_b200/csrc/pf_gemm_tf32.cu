@@ -12,7 +12,8 @@
 // ~1e-3 relative -- too much for the 1e-4 parity bar.  Each fp32 operand is split
 // x = hi + lo with hi = trunc13(x) (tf32) and lo = x - hi (exact in fp32), and the product is
 // A_hi B_hi + A_hi B_lo + A_lo B_hi (dropped A_lo B_lo ~ 2^-22 relative), fp32 accumulation
-// in TMEM.  npass = 1 runs the single A_hi B_hi product (plain TF32).
+// in TMEM.  npass = 2 drops A_hi B_lo (exact operator, iterate rounded to tf32), npass = 1 runs
+// the single A_hi B_hi product (plain TF32).
 //
 // B200 design (DESIGN.md §4 K1-tf32):
 //  * CTA pair (cluster 2x1, tcgen05 cta_group::2): the pair owns a 256-row tile of A; each CTA
@@ -31,6 +32,7 @@
 //    them in fixed order (deterministic) before the Chebyshev scale-shift-subtract epilogue.
 //  * epilogue warps drain TMEM with tcgen05.ld (32 lanes x 32 columns per instruction).
 #include <algorithm>
+#include <cstdlib>
 
 #include "pf_kernels.cuh"
 #include "pf_tc.cuh"
@@ -246,12 +248,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tf32Cfg<P>::THREADS,
               const uint32_t acc = (kb == s0 && ks == 0) ? 0u : 1u;
               tc::mma_tf32_pair(d, tc::sdesc_k_sw64(a_hi + ks * 32),
                                 tc::sdesc_k_sw64(b_hi + boff), idesc, acc);
-              if (args.npass == 3) {
-                tc::mma_tf32_pair(d, tc::sdesc_k_sw64(a_hi + ks * 32),
-                                  tc::sdesc_k_sw64(b_lo + boff), idesc, 1u);
+              if (args.npass >= 2)  // exact operator: + A_lo B_hi
                 tc::mma_tf32_pair(d, tc::sdesc_k_sw64(a_lo + ks * 32),
                                   tc::sdesc_k_sw64(b_hi + boff), idesc, 1u);
-              }
+              if (args.npass == 3)  // exact iterate: + A_hi B_lo
+                tc::mma_tf32_pair(d, tc::sdesc_k_sw64(a_hi + ks * 32),
+                                  tc::sdesc_k_sw64(b_lo + boff), idesc, 1u);
             }
           }
           tc::mma_commit_pair(&empty[rt.s]);  // raw stage free in both CTAs
@@ -275,11 +277,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tf32Cfg<P>::THREADS,
         if (ct == 0) TRACE(1 + 6 * crank, w, kb - kb0);
         mbar_wait(&full[rt.s], rt.ph);
         if (ct == 0) TRACE(2 + 6 * crank, w, kb - kb0);
-        if (args.npass == 3) {
+        if (args.npass >= 2) {  // npass 2: lo of A only; npass 3: lo of A and B
           const float4* src = reinterpret_cast<const float4*>(raw + rt.s * C::STAGE_BYTES);
           float4* dst = reinterpret_cast<float4*>(low + rl.s * C::STAGE_BYTES);
+          const int nvec = (args.npass == 3 ? C::STAGE_BYTES : C::A_BYTES) / 16;
 #pragma unroll 4
-          for (int i = ct; i < C::STAGE_BYTES / 16; i += 32 * C::NCONV_WARPS) {
+          for (int i = ct; i < nvec; i += 32 * C::NCONV_WARPS) {
             const float4 x = src[i];
             float4 l;
             l.x = x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
@@ -429,6 +432,7 @@ Tf32Plan tf32_plan(int p, int n_rows, int n_k, int num_sms) {
   pl.ws_floats = (size_t)G * 2 * (size_t)p * 128;
   pl.acc_floats = pl.ws_floats;
   pl.chunk_kb = 128;  // K_c = 2048 per TMEM accumulation (truncating accumulator, see kernel)
+  if (const char* e = getenv("PF_TF32_CHUNK_KB")) pl.chunk_kb = atoi(e);  // development knob
   pl.counters = (size_t)pl.mtiles * 2;
   return pl;
 }

@@ -43,6 +43,8 @@ class Solver:
         self.f32 = cfg.dtype == "tf32"   # fp32 storage, TF32 tensor-core filter (config 5)
         self.ctx = Context(n, p, d, nccl_id=nccl_id, rank=rank, world=world,
                            dtype=PF_TF32 if self.f32 else PF_FP64)
+        if self.f32:
+            self.ctx.set_tf32_schedule(cfg.tf32_early, cfg.tf32_tail)
         r0, r1 = rows_of(n, rank, world) if nccl_id is not None else (0, n)
         self.r0, self.r1, self.n_local = r0, r1, r1 - r0
         assert self.n_local == self.ctx.n_local

@@ -60,6 +60,10 @@ class Config:
     # config 5 soft threshold (reading R11) and workload shape
     theta: float = 3.0
     gen: str = "cfg1"         # sweep workload: "cfg1" (Haar basis) | "cfg5" (Householder basis)
+    # TF32 precision schedule of the GPU filter (reading R18; the fp64 oracle ignores it):
+    # the first d - tf32_tail Chebyshev steps at tf32_early MMA passes, the rest in 3xTF32
+    tf32_early: int = 3
+    tf32_tail: int = 0
     nbig: int = 256           # config 5: eigenvalues drawn from U[5, 50]
     nrefl: int = 64           # config 5: Householder reflectors in the basis
 
@@ -73,7 +77,7 @@ CONFIGS = {
     4: Config("cfg4_pfpg_n32768", n=32768, p=128, d=10, iters=100, mode="pfpg",
               r=50, omega_prob=0.05),
     5: Config("cfg5_soft_sweep_n65536", n=65536, p=512, d=8, iters=30, mode="sweep_soft",
-              dtype="tf32", rho_max=1e3, gen="cfg5"),
+              dtype="tf32", rho_max=1e3, gen="cfg5", tf32_early=1, tf32_tail=2),
 }
 
 

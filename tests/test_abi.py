@@ -43,6 +43,7 @@ def test_argument_errors_are_synchronous_without_gpu():
     nid = ctypes.create_string_buffer(128)
     assert lib.pf_create_dist(1000, 64, 4, 2, nid, 0, 1, ctypes.byref(h)) == 7  # single-GPU only
     assert lib.pf_set_tf32_passes(None, 3) == 1
+    assert lib.pf_set_tf32_schedule(None, 1, 3) == 1
     assert lib.pf_status_string(3) == b"PF_ERR_INTERVAL"
 
 

@@ -27,7 +27,8 @@ def main():
     ap.add_argument("--p", type=int, default=512)
     ap.add_argument("--d", type=int, nargs="+", default=[4, 8, 16])
     ap.add_argument("--steps", type=int, default=3)
-    ap.add_argument("--passes", type=int, default=3)
+    ap.add_argument("--passes", type=int, default=0,
+                    help="uniform TF32 passes (1..3); 0 = the config's schedule (reading R18)")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -50,7 +51,8 @@ def main():
                 Adev = buf[:, :cfg.n]
             A = Adev.clone() if False else Adev
             s = Solver(cfg, problem={"_dev": {"A0": A}}, stream=stream)
-            s.ctx.set_tf32_passes(args.passes)
+            if args.passes:
+                s.ctx.set_tf32_passes(args.passes)
             s.step()                      # k = 0: Lanczos + warm-up sweeps (untimed)
             s.perturb_hash(0)
         torch.cuda.synchronize()
@@ -79,13 +81,15 @@ def main():
         flops_pass = 2.0 * n * n * p
         rank = int(s.rank.item())
         out = {
-            "config": f"config 5 sweep, n={n}, p={p}, d={d}, fp32 storage, "
-                      f"{args.passes}xTF32 tcgen05 filter, 1 GPU",
+            "config": f"config 5 sweep, n={n}, p={p}, d={d}, fp32 storage, tcgen05 TF32 filter "
+                      + (f"{args.passes}xTF32 every pass" if args.passes else
+                         f"schedule: {cfg.tf32_early}xTF32 steps 1..{d - cfg.tf32_tail}, "
+                         f"3xTF32 last {cfg.tf32_tail} steps + RR") + ", 1 GPU",
             "it_per_s": 1e3 / ms, "ms_per_step": ms, "step_ms": step_ms,
             "filter_tflops": 2.0 * d * n * n * p / (ms / 1e3) / 1e12,
             "gemm_avg_ms": gemm_avg, "gemm_launches": gemm_n,
             "gemm_algorithmic_tflops": flops_pass / (gemm_avg / 1e3) / 1e12,
-            "gemm_tensor_tflops": args.passes * flops_pass / (gemm_avg / 1e3) / 1e12,
+            "gemm_passes_per_step": None if not args.passes else args.passes,
             "gemm_share_of_step": gemm_ms / sum(step_ms),
             "perturb_ms": float(np.mean(pert_ms)),
             "perturb_gbps": 2 * 4.0 * n * n / (np.mean(pert_ms) / 1e3) / 1e9,
