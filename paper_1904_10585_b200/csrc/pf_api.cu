@@ -71,6 +71,8 @@ struct pf_ctx_s {
   int64_t ldy32 = 0;                           // pitch of the internal blocks (>= n_local, %4)
   float* Yf[3] = {nullptr, nullptr, nullptr};  // p x ldy32
   float* Wf = nullptr;                         // A Q
+  float* Yfull32 = nullptr;                    // dist: rank-major all-gather [world][p][n_local]
+  CUtensorMap mapBfull32;
   double* g32_part = nullptr;
   int g32_slices = 1;
   double* chol_W = nullptr;                    // p x p
@@ -152,7 +154,10 @@ static pf_status alloc_all(pf_ctx ctx) {
   const bool f32 = ctx->dtype == PF_TF32;
   ok &= A((void**)&ctx->state, sizeof(DevState));
   if (f32) {
-    ctx->ldy32 = (nl + 3) / 4 * 4;
+    // distributed: n_local % 16 == 0, so the blocks are contiguous p x n_local slabs that
+    // ncclAllGather concatenates rank-major; the B operand is then read through a 3-D map
+    ctx->ldy32 = ctx->dist ? nl : (nl + 3) / 4 * 4;
+    if (ctx->dist) ok &= A((void**)&ctx->Yfull32, (size_t)p * n * 4);
     for (int i = 0; i < 3; ++i) ok &= A((void**)&ctx->Yf[i], (size_t)p * ctx->ldy32 * 4);
     ok &= A((void**)&ctx->Wf, (size_t)p * ctx->ldy32 * 4);
     ctx->g32_slices = gram32_slices((int)nl, p, ctx->num_sms);
@@ -209,7 +214,12 @@ static pf_status alloc_all(pf_ctx ctx) {
   const double rr[3] = {1.0, 0.0, 0.0};
   PF_CU(cudaMemcpy(&ctx->state->coef_rr[0], rr, sizeof(rr), cudaMemcpyHostToDevice));
   // TMA descriptors of the internal B operands
-  if (f32) {
+  if (f32 && ctx->dist) {
+    if (!tf32_encode_B_dist(&ctx->mapBfull32, ctx->Yfull32, p, (int)nl, ctx->world)) {
+      snprintf(ctx->err, sizeof(ctx->err), "cuTensorMapEncodeTiled(B, fp32, 3-D) failed");
+      return PF_ERR_CUDA;
+    }
+  } else if (f32) {
     for (int i = 0; i < 3; ++i)
       if (!tf32_encode_B(&ctx->mapBf[i], ctx->Yf[i], ctx->ldy32, p, (int)n)) {
         snprintf(ctx->err, sizeof(ctx->err), "cuTensorMapEncodeTiled(B, fp32) failed");
@@ -234,8 +244,10 @@ static pf_status create_common(int64_t n, int32_t p, int32_t degree, pf_dtype dt
   if (!out) return PF_ERR_ARG;
   *out = nullptr;
   if (dtype != PF_FP64 && dtype != PF_TF32) return PF_ERR_UNSUPPORTED;
-  // the fp32 path is single-GPU in this build (its row-block all-gather is not wired)
-  if (dtype == PF_TF32 && nccl_id != nullptr) return PF_ERR_UNSUPPORTED;
+  // fp32 path, distributed: equal row blocks with n_local % 16 == 0 (a 16-wide TMA K box never
+  // straddles two ranks' slabs of the gathered block)
+  if (dtype == PF_TF32 && nccl_id != nullptr && (n % (16 * (int64_t)world)) != 0)
+    return PF_ERR_DIM;
   if (degree < 1 || degree > kMaxDeg) return PF_ERR_ARG;
   if (world < 1 || rank < 0 || rank >= world) return PF_ERR_ARG;
   if (!p_supported(p, dtype) || n < p || n > (int64_t)1 << 30 || n < world * (int64_t)p)
@@ -341,7 +353,7 @@ pf_status pf_destroy(pf_ctx ctx) {
                   ctx->lz_theta, ctx->lz_S,   ctx->rb_part,   ctx->rb_cnt,  ctx->shift_flag,
                   ctx->Yf[0],  ctx->Yf[1],    ctx->Yf[2],     ctx->Wf,      ctx->g32_part,
                   ctx->chol_W, ctx->chol_D,   ctx->jac_H,     ctx->jac_V,   ctx->jac_red,
-                  ctx->jac_cnt, ctx->tf_ws,   ctx->tf_cnt,    ctx->tf_acc};
+                  ctx->jac_cnt, ctx->tf_ws,   ctx->tf_cnt,    ctx->tf_acc,  ctx->Yfull32};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete ctx;
@@ -490,11 +502,21 @@ static pf_status copy_block32(pf_ctx ctx, float* dst, int64_t ldd, const float* 
 
 static pf_status gemm_step32(pf_ctx ctx, int bidx, const float* ycur, const float* yprev,
                              float* out, const double* coef, int npass, cudaStream_t st) {
+  const CUtensorMap* mb = &ctx->mapBf[bidx];
+  int bdist_kb = 0;
+  if (ctx->dist) {
+    // all-gather the p-major blocks rank-major: [world][p][n_local] (one NCCL call per step)
+    ncclResult_t r = ncclAllGather(ctx->Yf[bidx], ctx->Yfull32, (size_t)ctx->p * ctx->n_local,
+                                   ncclFloat, ctx->comm, st);
+    if (r != ncclSuccess) return nccl_fail(ctx, r, "ncclAllGather(fp32 block)");
+    mb = &ctx->mapBfull32;
+    bdist_kb = (int)(ctx->n_local / 16);
+  }
   const bool rec = ctx->prof && ctx->ev_used + 2 <= ctx->ev.size();
   if (ctx->prof && !rec) ++ctx->prof_dropped;
   if (rec) PF_CU(cudaEventRecord(ctx->ev[ctx->ev_used], st));
-  PF_CU(tf32_gemm_launch(ctx->tplan, ctx->mapAf, ctx->mapBf[bidx], ctx->mapApf, ycur, yprev, out,
-                         ctx->ldy32, coef, ctx->tf_ws, ctx->tf_acc, ctx->tf_cnt, npass, st));
+  PF_CU(tf32_gemm_launch(ctx->tplan, ctx->mapAf, *mb, ctx->mapApf, ycur, yprev, out, ctx->ldy32,
+                         coef, ctx->tf_ws, ctx->tf_acc, ctx->tf_cnt, npass, st, bdist_kb));
   if (rec) {
     PF_CU(cudaEventRecord(ctx->ev[ctx->ev_used + 1], st));
     ctx->ev_used += 2;
@@ -506,7 +528,10 @@ static pf_status gram32_all(pf_ctx ctx, const float* X, const float* Y, double* 
                             cudaStream_t st) {
   PF_CU(gram32_launch(X, ctx->ldy32, Y, ctx->ldy32, (int)ctx->n_local, ctx->p, G, ctx->g32_part,
                       ctx->g32_slices, cond, st));
-  return PF_OK;
+  // p x p sum over the row blocks.  Under a re-base condition the all-reduce runs regardless
+  // (collectives cannot be skipped per rank); every rank evaluates the same plan, so either all
+  // ranks consume the sum or none does.
+  return allreduce(ctx, G, (size_t)ctx->p * ctx->p, st);
 }
 
 static pf_status chol32(pf_ctx ctx, int* shift_out, const int* cond, cudaStream_t st) {

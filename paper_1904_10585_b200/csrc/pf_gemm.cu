@@ -337,6 +337,19 @@ bool encode_map_f32(CUtensorMap* map, const float* base, int64_t pitch, int rows
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Rank-major all-gather of p-major blocks: [world][p][n_local] contiguous (n_local % 16 == 0).
+bool tf32_encode_B_dist(CUtensorMap* map, const float* Yg, int p, int n_local, int world) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)n_local, (cuuint64_t)p, (cuuint64_t)world};
+  cuuint64_t strides[2] = {(cuuint64_t)n_local * 4, (cuuint64_t)n_local * 4 * p};
+  cuuint32_t box[3] = {16, (cuuint32_t)(std::min(p, 256) / 2), 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(Yg), dims, strides, box,
+             es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int P>
 static size_t ws_per_cta() {
   return (size_t)2 * GemmCfg<P>::NCT * GemmCfg<P>::NACC;

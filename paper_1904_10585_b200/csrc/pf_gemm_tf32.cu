@@ -81,6 +81,8 @@ struct Tf32Args {
   int split;           // K-split of the tail wave
   int npass;
   int chunk_kb;        // k-blocks accumulated in TMEM before folding into `acc` (0: no limit)
+  int bdist_kb;        // > 0: B is the rank-major all-gather [world][p][n_local] read through a
+                       // 3-D map; k-blocks per rank (n_local / 16)
   float* acc;          // fp32 chunk accumulators: [pair][2 ctas][P][128]
 };
 
@@ -209,10 +211,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tf32Cfg<P>::THREADS,
           unsigned char* st = raw + rt.s * C::STAGE_BYTES;
           mbar_arrive_expect_tx(&full[rt.s], C::STAGE_BYTES);
           tma_load_2d(st, &mapA, &full[rt.s], kb * C::BK, arow);
+          if (args.bdist_kb > 0) {
+            // global k-block kb lives in rank kb / bdist_kb's slab at local k-block kb % bdist_kb
+            const int rk = kb / args.bdist_kb, lk = kb - rk * args.bdist_kb;
 #pragma unroll
-          for (int h = 0; h < C::NH; ++h)
-            tma_load_2d(st + C::A_BYTES + h * (C::NMMA / 2) * 64, &mapB, &full[rt.s], kb * C::BK,
-                        h * C::NMMA + (int)crank * (C::NMMA / 2));
+            for (int h = 0; h < C::NH; ++h)
+              tc::tma_load_3d(st + C::A_BYTES + h * (C::NMMA / 2) * 64, &mapB, &full[rt.s],
+                              lk * C::BK, h * C::NMMA + (int)crank * (C::NMMA / 2), rk);
+          } else {
+#pragma unroll
+            for (int h = 0; h < C::NH; ++h)
+              tma_load_2d(st + C::A_BYTES + h * (C::NMMA / 2) * 64, &mapB, &full[rt.s],
+                          kb * C::BK, h * C::NMMA + (int)crank * (C::NMMA / 2));
+          }
         }
       }
     }
@@ -446,6 +457,7 @@ bool tf32_encode_B(CUtensorMap* map, const float* Yt, int64_t ldy, int p, int n_
   return encode_map_f32(map, Yt, ldy, p, n_k, std::min(p, 256) / 2);
 }
 
+
 template <int P>
 static cudaError_t tf32_launch_p(const Tf32Plan& pl, const CUtensorMap& mapA,
                                  const CUtensorMap& mapB, const CUtensorMap& mapApf,
@@ -467,7 +479,7 @@ cudaError_t tf32_gemm_launch(const Tf32Plan& pl, const CUtensorMap& mapA, const 
                              const CUtensorMap& mapApf,
                              const float* ycur, const float* yprev, float* out, int64_t ldy,
                              const double* coef, float* ws, float* acc, int* counters,
-                             int npass, cudaStream_t st) {
+                             int npass, cudaStream_t st, int bdist_kb) {
   Tf32Args a;
   a.ycur = ycur;
   a.yprev = yprev;
@@ -482,6 +494,7 @@ cudaError_t tf32_gemm_launch(const Tf32Plan& pl, const CUtensorMap& mapA, const 
   a.split = pl.split;
   a.npass = npass;
   a.chunk_kb = pl.chunk_kb;
+  a.bdist_kb = bdist_kb;
   a.acc = acc;
   switch (pl.p) {
     case 64: return tf32_launch_p<64>(pl, mapA, mapB, mapApf, a, st);

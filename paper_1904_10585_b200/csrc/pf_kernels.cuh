@@ -47,11 +47,13 @@ Tf32Plan tf32_plan(int p, int n_rows, int n_k, int num_sms);
 bool tf32_encode_A(CUtensorMap* map, CUtensorMap* map_pf, const float* A, int64_t lda,
                    int n_rows, int n_k);
 bool tf32_encode_B(CUtensorMap* map, const float* Yt, int64_t ldy, int p, int n_k);
+// B as the rank-major all-gather [world][p][n_local] of p-major blocks (3-D map)
+bool tf32_encode_B_dist(CUtensorMap* map, const float* Yg, int p, int n_local, int world);
 cudaError_t tf32_gemm_launch(const Tf32Plan& pl, const CUtensorMap& mapA, const CUtensorMap& mapB,
                              const CUtensorMap& mapApf,
                              const float* ycur, const float* yprev, float* out, int64_t ldy,
                              const double* coef, float* ws, float* acc, int* counters,
-                             int npass, cudaStream_t st);
+                             int npass, cudaStream_t st, int bdist_kb = 0);
 
 // ---- fp32-path kernels (pf_f32.cu); blocks fp32 p-major, p x p objects fp64 row-major
 int gram32_slices(int n_rows, int p, int num_sms);

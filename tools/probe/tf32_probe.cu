@@ -95,9 +95,26 @@ int main(int argc, char** argv) {
     printf("encode failed\n");
     return 1;
   }
+  // VWORLD=W: read B through the 3-D map of a rank-major "all-gather" [W][p][nk/W] assembled
+  // here from Y (exercises the distributed addressing on one GPU)
+  int vworld = getenv("VWORLD") ? atoi(getenv("VWORLD")) : 0, bdist_kb = 0;
+  if (vworld > 0) {
+    const int nl = nk / vworld;
+    float* Yg;
+    CK(cudaMalloc(&Yg, sizeof(float) * (size_t)p * nk));
+    for (int r = 0; r < vworld; ++r)
+      CK(cudaMemcpy2D(Yg + (size_t)r * p * nl, nl * 4, Y + (size_t)r * nl, ldy * 4, nl * 4, p,
+                      cudaMemcpyDeviceToDevice));
+    if (!pf::tf32_encode_B_dist(&mB, Yg, p, nl, vworld)) {
+      printf("encode 3-D failed\n");
+      return 1;
+    }
+    bdist_kb = nl / 16;
+    printf("virtual world %d, n_local %d (3-D B map)\n", vworld, nl);
+  }
   printf("rows %d nk %d p %d npass %d: pairs %d split %d mtiles %d kblocks %d\n", rows, nk, p, npass, pl.pairs,
          pl.split, pl.mtiles, pl.kblocks);
-  CK(pf::tf32_gemm_launch(pl, mA, mB, mApf, yc, yp, out, ldy, coef, ws, accb, cnt, npass, 0));
+  CK(pf::tf32_gemm_launch(pl, mA, mB, mApf, yc, yp, out, ldy, coef, ws, accb, cnt, npass, 0, bdist_kb));
   CK(cudaDeviceSynchronize());
   dim3 rg((rows / row_stride + 127) / 128, p);
   ref_kernel<<<rg, 128>>>(A, lda, Y, ldy, rows, nk, p, yc, yp, hc[0], hc[1], hc[2], ref, bound,
@@ -136,10 +153,10 @@ int main(int argc, char** argv) {
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
     for (int w = 0; w < 2; ++w)
-      CK(pf::tf32_gemm_launch(pl, mA, mB, mApf, yc, yp, out, ldy, coef, ws, accb, cnt, npass, 0));
+      CK(pf::tf32_gemm_launch(pl, mA, mB, mApf, yc, yp, out, ldy, coef, ws, accb, cnt, npass, 0, bdist_kb));
     CK(cudaEventRecord(e0));
     for (int r = 0; r < reps; ++r)
-      CK(pf::tf32_gemm_launch(pl, mA, mB, mApf, yc, yp, out, ldy, coef, ws, accb, cnt, npass, 0));
+      CK(pf::tf32_gemm_launch(pl, mA, mB, mApf, yc, yp, out, ldy, coef, ws, accb, cnt, npass, 0, bdist_kb));
     CK(cudaEventRecord(e1));
     CK(cudaEventSynchronize(e1));
     float ms;
@@ -151,7 +168,7 @@ int main(int argc, char** argv) {
   }
 #ifdef PF_TRACE
   {
-    CK(pf::tf32_gemm_launch(pl, mA, mB, mApf, yc, yp, out, ldy, coef, ws, accb, cnt, npass, 0));
+    CK(pf::tf32_gemm_launch(pl, mA, mB, mApf, yc, yp, out, ldy, coef, ws, accb, cnt, npass, 0, bdist_kb));
     CK(cudaDeviceSynchronize());
     static unsigned long long tr[12][512];
     pf::tf32_trace_read(&tr[0][0]);
