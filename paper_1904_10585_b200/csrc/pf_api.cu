@@ -87,6 +87,7 @@ struct pf_ctx_s {
   int tf_early = 3;  // TF32 passes of the Chebyshev steps before the exact tail
   int tf_tail = 0;   // number of final Chebyshev steps run in 3xTF32
   int tf_rr = 3;     // passes of the Rayleigh-Ritz product A Q
+  bool filtered = false;  // a pf_filter ran: state->interval holds its damped interval
   Tf32Plan tplan;
   CUtensorMap mapBf[3];
   CUtensorMap mapAf, mapApf;
@@ -562,6 +563,7 @@ static pf_status filter32(pf_ctx ctx, const float* A, int64_t lda, float* U, int
   PF_TRY(map_A32(ctx, A, lda));
   const int p = ctx->p, d = ctx->d, nl = (int)ctx->n_local;
   PF_CU(plan_launch(interval, d, rho_max, p, ctx->state, st));
+  ctx->filtered = true;
   PF_TRY(copy_block32(ctx, ctx->Yf[0], ctx->ldy32, U, ldu, st));
   int cur = 0, prev = -1;
   for (int rep = 0; rep < q; ++rep) {
@@ -604,8 +606,11 @@ static pf_status rayleigh_ritz32(pf_ctx ctx, const float* A, int64_t lda, const 
   PF_TRY(gram32_all(ctx, ctx->Yf[0], ctx->Wf, ctx->G, nullptr, st));  // H = Q^T (A Q)
   // H is formed from fp32 blocks (relative accuracy ~1e-7): diagonalise to off(H) <= 1e-12 ||H||
   // (fp64 storage of H; eigenvector error ~1e-12 / gap, far below the fp32 data error)
+  // partial diagonalisation (reading R19): the damped interval of the last pf_filter call
+  // (state->interval, set by its plan) bounds the Ritz values whose f is 0
   PF_CU(jacobi_big_launch(ctx->G, p, theta, ctx->Yeig, ctx->jac_H, ctx->jac_V, ctx->jac_red,
-                          ctx->jac_cnt, ctx->state, 1e-12, 40, st));
+                          ctx->jac_cnt, ctx->state, 1e-12, 40,
+                          ctx->filtered ? &ctx->state->interval[0] : nullptr, st));
   PF_CU(copy_theta_launch(theta, p, ctx->state, st));
   PF_CU(rmul32_launch(ctx->Yf[0], ctx->ldy32, ctx->Yeig, V, ldv, nl, p, nullptr, st));
   return PF_OK;

@@ -491,15 +491,21 @@ __device__ __forceinline__ void jb_decode(int e, int half, int& a, int& b) {
 __global__ void __launch_bounds__(JB_THREADS) jacobi_big_kernel(
     const double* __restrict__ Hin, int p, double* __restrict__ theta, double* __restrict__ Yout,
     double* H0, double* Vt_, double* red_ws, int* cnt_ws, DevState* state, double tol,
-    int max_sweeps) {
+    int max_sweeps, const double* damped) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double csv[3 * 256];
   __shared__ int pii[256], pjj[256];
   __shared__ double red[32];
   __shared__ int s_cnt;
+  __shared__ unsigned char inside[512];  // diagonal entry strictly inside the damped interval
   const int tid = threadIdx.x, half = p / 2;
   const int gtid = blockIdx.x * JB_THREADS + tid, gthreads = gridDim.x * JB_THREADS;
   const int nblk = half * (half + 1) / 2;
+  // Damped interval [a, b] of the last filter (reading R19): f(theta) = 0 there for both
+  // spectral operators, so pairs with BOTH diagonal entries inside are never rotated -- the
+  // block of H they span is left undiagonalised; everything else converges as usual.
+  const double da = damped ? damped[0] : 0.0, db = damped ? damped[1] : 0.0;
+  const bool skip = damped != nullptr && db > da;
   double* Hb[2] = {H0, H0 + (size_t)p * p};
   double* __restrict__ Vt = Vt_;  // Vt[i][row] = V[row][i]: rotating columns i, j of V
                                   // rotates two contiguous rows of Vt (coalesced)
@@ -514,11 +520,17 @@ __global__ void __launch_bounds__(JB_THREADS) jacobi_big_kernel(
   bool converged = false;
   for (; sweep < max_sweeps; ++sweep) {
     const double* H = Hb[cur];
+    for (int i = tid; i < p; i += JB_THREADS) {
+      const double hii = H[(size_t)i * p + i];
+      inside[i] = (skip && hii > da && hii < db) ? 1 : 0;
+    }
+    __syncthreads();
     double off = 0.0, tot = 0.0;
     for (int e = gtid; e < p * p; e += gthreads) {
       const double v = H[e];
       tot += v * v;
-      if (e / p != e % p) off += v * v;
+      const int i = e / p, j = e % p;
+      if (i != j && !(inside[i] && inside[j])) off += v * v;
     }
     off = block_sum(off, red);
     tot = block_sum(tot, red);
@@ -559,7 +571,8 @@ __global__ void __launch_bounds__(JB_THREADS) jacobi_big_kernel(
         const double hij = Hc[(size_t)i * p + j];
         const double hii = Hc[(size_t)i * p + i], hjj = Hc[(size_t)j * p + j];
         double c = 1.0, s = 0.0, t = 0.0;
-        if (fabs(hij) > 1e-16 * s_norm) {
+        const bool both_in = skip && hii > da && hii < db && hjj > da && hjj < db;
+        if (!both_in && fabs(hij) > 1e-16 * s_norm) {
           const double dd = hjj - hii, ee = 2.0 * hij;
           const double ir = rsqrt(dd * dd + ee * ee);
           const double hh = 0.5 + 0.5 * fabs(dd) * ir;
@@ -662,10 +675,10 @@ int jacobi_big_grid() { return 64; }
 // Hw: 2 p^2 doubles, Vw: p^2, red_ws: 2 * jacobi_big_grid() doubles, cnt_ws: 4 ints
 cudaError_t jacobi_big_launch(const double* H, int p, double* theta, double* Y, double* Hw,
                               double* Vw, double* red_ws, int* cnt_ws, DevState* state, double tol,
-                              int max_sweeps, cudaStream_t st) {
+                              int max_sweeps, const double* damped, cudaStream_t st) {
   void* args[] = {(void*)&H,      (void*)&p,     (void*)&theta,  (void*)&Y,
                   (void*)&Hw,     (void*)&Vw,    (void*)&red_ws, (void*)&cnt_ws,
-                  (void*)&state,  (void*)&tol,   (void*)&max_sweeps};
+                  (void*)&state,  (void*)&tol,   (void*)&max_sweeps, (void*)&damped};
   count_launch();
   return cudaLaunchCooperativeKernel((const void*)jacobi_big_kernel, dim3(jacobi_big_grid()),
                                      dim3(JB_THREADS), args, 0, st);

@@ -69,9 +69,11 @@ cudaError_t chol_inv_big_launch(const double* G, int p, int64_t n_global, double
                                 double* Rinv, DevState* state, int* shift_flag_out,
                                 const int* cond, cudaStream_t st);
 int jacobi_big_grid();
+// damped: device double[2] {a, b} (may be NULL): pairs whose two diagonal entries both lie in
+// (a, b) are not rotated (their eigenpairs have f = 0)
 cudaError_t jacobi_big_launch(const double* H, int p, double* theta, double* Y, double* Hw,
                               double* Vw, double* red_ws, int* cnt_ws, DevState* state, double tol,
-                              int max_sweeps, cudaStream_t st);
+                              int max_sweeps, const double* damped, cudaStream_t st);
 cudaError_t perturb_hash32_launch(float* A, int64_t lda, int rows, int cols, int row0,
                                   unsigned long long seed, int k, double noise, cudaStream_t st);
 // Lanczos GEMV on an fp32 iterate (fp64 accumulation), same contract as lz_gemv_launch
