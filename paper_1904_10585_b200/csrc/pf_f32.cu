@@ -272,27 +272,43 @@ cudaError_t rmul32_launch(const float* in, int64_t ldi, const double* R, float* 
 }
 
 // =============================================================================== Cholesky
-// One CTA of 1024 threads; W (p x p fp64 scratch) holds the lower triangle.  Phase 1: right-
-// looking Cholesky by 32-column panels (panel factored in smem, trailing update from the
-// panel).  Phase 2: X = L^{-1} by column blocks: X[I, C] = L_II^{-1} (E[I, C] - L[I, C:I] X[C:I, C])
-// with the diagonal-block inverses L_II^{-1} formed first.  Rinv = X^T.
+// chol_inv_big_kernel: one CTA of CH_NT threads; W (p x p fp64 scratch) holds the lower triangle.
+// Right-looking Cholesky by 32-column panels staged in smem: (a) the 32 x 32 top block
+// block-wide (two barriers per column), (b) the panel rows below by per-thread forward
+// substitution, (c) the trailing update on fp64 DMMA; then the 32 x 32 diagonal-block inverses
+// (one warp per block).  linv_big_kernel: X = L^{-1} by independent column blocks, one CTA each:
+// X[I, C] = L_II^{-1} (E[I, C] - L[I, C:I] X[C:I, C]).  Rinv = X^T.
+// Measured at p = 512 (tools/probe/chol_probe.cu): 1.9 -> 1.36 ms per call; the remaining cost is
+// the single-SM trailing update (at ~55% of one SM's DMMA rate) and the serial panel chain.
 constexpr int CB = 32, CB_LD = 33;
+constexpr int CH_NT = 512;  // Cholesky CTA: 128 registers/thread (4x4 tiles, 32-wide rows)
+// panel row r, column c: one pad double after every 4 rows, so lanes reading rows 4t + a of
+// consecutive 4-row tiles t fall on distinct banks
+__host__ __device__ constexpr int PNL(int r, int c) { return r * CB_LD + (r >> 2) + c; }
+#ifdef PF_CHOL_PHASES
+__device__ long long g_chol_t[8];
+#define CHOL_T(i) if (threadIdx.x == 0) g_chol_t[i] = clock64()
+#else
+#define CHOL_T(i)
+#endif
 
-__global__ void __launch_bounds__(1024) chol_inv_big_kernel(const double* __restrict__ G, int p,
+__global__ void __launch_bounds__(CH_NT) chol_inv_big_kernel(const double* __restrict__ G, int p,
                                                             double shift_scale, double* W,
                                                             double* Dinv, double* __restrict__ Rinv,
                                                             DevState* state, int* shift_flag_out,
                                                             const int* cond) {
   if (cond && *cond == 0) return;
-  extern __shared__ double cs[];  // p x CB_LD panel / X block, + CB x CB_LD scratch
+  CHOL_T(0);
+  extern __shared__ double cs[];  // p x CB_LD panel
   __shared__ double red[32];
   __shared__ double gdiag[512];
+  __shared__ double rdiag[CB];     // 1 / L[c][c] of the current panel's top block
   __shared__ int s_fail;
-  double* T = cs + (size_t)p * CB_LD;
-  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  __shared__ unsigned char tri_k[CB * (CB + 1) / 2], tri_k2[CB * (CB + 1) / 2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double tr = 0.0;
   int bad = 0;
-  for (int e = tid; e < p * p; e += 1024) {
+  for (int e = tid; e < p * p; e += CH_NT) {
     const double v = G[e];
     if (!isfinite(v)) bad = 1;
     if (e / p == e % p) tr += v;
@@ -300,12 +316,20 @@ __global__ void __launch_bounds__(1024) chol_inv_big_kernel(const double* __rest
   bad = __syncthreads_or(bad);
   tr = block_sum(tr, red);
   if (bad && tid == 0) atomicOr(&state->flags, PF_FLAG_NONFINITE);
-  for (int i = tid; i < p; i += 1024) gdiag[i] = G[(size_t)i * p + i];
+  for (int i = tid; i < p; i += CH_NT) gdiag[i] = G[(size_t)i * p + i];
+  for (int e = tid; e < CB * (CB + 1) / 2; e += CH_NT) {
+    int k = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+    while (k * (k + 1) / 2 > e) --k;
+    while ((k + 1) * (k + 2) / 2 <= e) ++k;
+    tri_k[e] = (unsigned char)k;
+    tri_k2[e] = (unsigned char)(e - k * (k + 1) / 2);
+  }
 
   double shift = 0.0;
   int attempt = 0;
+  CHOL_T(1);
   for (;;) {
-    for (int e = tid; e < p * p; e += 1024) {
+    for (int e = tid; e < p * p; e += CH_NT) {
       const int i = e / p, j = e % p;
       if (j <= i) W[e] = G[e] + ((i == j) ? shift : 0.0);
     }
@@ -313,73 +337,103 @@ __global__ void __launch_bounds__(1024) chol_inv_big_kernel(const double* __rest
     __syncthreads();
     for (int J = 0; J < p; J += CB) {
       const int R = p - J;
-      for (int e = tid; e < R * CB; e += 1024) {
+      for (int e = tid; e < R * CB; e += CH_NT) {
         const int r = e / CB, c = e % CB;
-        cs[r * CB_LD + c] = (c <= r) ? W[(size_t)(J + r) * p + J + c] : 0.0;
+        cs[PNL(r, c)] = (c <= r) ? W[(size_t)(J + r) * p + J + c] : 0.0;
       }
       __syncthreads();
+      if (J == 0) CHOL_T(4);
+      // (a) top 32 x 32 block, block-wide: thread t owns fixed element(s) (k, k2), k2 <= k, of the
+      //     block's lower triangle; two barriers per column
       for (int c = 0; c < CB; ++c) {
-        const double d = cs[c * CB_LD + c];
-        if (!(d > 1e-12 * gdiag[J + c]) || !(d > 0.0)) {  // uniform
-          if (tid == 0) s_fail = 1;
-          break;
-        }
-        const double rsd = rsqrt(d);
-        // scale column c (rows > c), then update panel columns c+1..31 (rows >= them)
-        for (int r = c + 1 + tid; r < R; r += 1024) cs[r * CB_LD + c] *= rsd;
-        __syncthreads();
-        if (tid == 0) cs[c * CB_LD + c] = d * rsd;
-        for (int e = tid; e < (R - c - 1) * (CB - c - 1); e += 1024) {
-          const int r = c + 1 + e / (CB - c - 1), c2 = c + 1 + e % (CB - c - 1);
-          if (c2 <= r) cs[r * CB_LD + c2] -= cs[r * CB_LD + c] * cs[c2 * CB_LD + c];
+        const double d = cs[PNL(c, c)];  // pivot, final after the previous column's update
+        const double rs = rsqrt(fabs(d) + 1e-300);
+        if (tid == 0 && (!(d > 1e-12 * gdiag[J + c]) || !(d > 0.0))) s_fail = 1;
+        if (tid > c && tid < CB) cs[PNL(tid, c)] *= rs;  // L[tid][c]
+        if (tid == c) {
+          cs[PNL(c, c)] = d * rs;
+          rdiag[c] = 1.0 / (d * rs);
         }
         __syncthreads();
-      }
-      __syncthreads();
-      if (s_fail) break;
-      for (int e = tid; e < R * CB; e += 1024) {
-        const int r = e / CB, c = e % CB;
-        if (c <= r) W[(size_t)(J + r) * p + J + c] = cs[r * CB_LD + c];
-      }
-      // trailing update of the lower triangle: W[i][k] -= sum_c P[i][c] P[k][c], J+32 <= k <= i,
-      // in 4 x 4 register tiles (8 shared loads per 16 FMAs instead of 2 per FMA)
-      {
-        const int R4 = (p - J - CB) / 4;  // p - J - CB is a multiple of 32
-        const int ntile = R4 * (R4 + 1) / 2;
-        for (int e = tid; e < ntile; e += 1024) {
-          int ti = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
-          while (ti * (ti + 1) / 2 > e) --ti;
-          while ((ti + 1) * (ti + 2) / 2 <= e) ++ti;
-          const int tk = e - ti * (ti + 1) / 2;  // tk <= ti
-          const double* pi = cs + (CB + 4 * ti) * CB_LD;
-          const double* pk = cs + (CB + 4 * tk) * CB_LD;
-          double acc[4][4];
 #pragma unroll
-          for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-#pragma unroll 8
-          for (int c = 0; c < CB; ++c) {
-            double xi[4], xk[4];
-#pragma unroll
-            for (int a = 0; a < 4; ++a) {
-              xi[a] = pi[a * CB_LD + c];
-              xk[a] = pk[a * CB_LD + c];
-            }
-#pragma unroll
-            for (int a = 0; a < 4; ++a)
-#pragma unroll
-              for (int b = 0; b < 4; ++b) acc[a][b] += xi[a] * xk[b];
+        for (int u = 0; u < 2; ++u) {
+          const int e = tid + u * CH_NT;
+          if (e < CB * (CB + 1) / 2) {
+            const int k = tri_k[e], k2 = tri_k2[e];
+            if (k2 > c) cs[PNL(k, k2)] -= cs[PNL(k, c)] * cs[PNL(k2, c)];
           }
-          const int i0 = J + CB + 4 * ti, k0 = J + CB + 4 * tk;
+        }
+        __syncthreads();
+      }
+      __syncthreads();
+      if (J == 0) CHOL_T(5);
+      if (s_fail) break;
+      // (b) rows below the top block: L[r][0:32] = A[r][0:32] L_top^{-T}, forward substitution
+      //     in place, one panel row per thread (the top block is read as a broadcast)
+      for (int r = CB + tid; r < R; r += CH_NT) {
+        double x[CB];
 #pragma unroll
-          for (int a = 0; a < 4; ++a)
+        for (int c = 0; c < CB; ++c) x[c] = cs[PNL(r, c)];
 #pragma unroll
-            for (int b = 0; b < 4; ++b)
-              if (k0 + b <= i0 + a) W[(size_t)(i0 + a) * p + k0 + b] -= acc[a][b];
+        for (int c = 0; c < CB; ++c) {
+          double v = x[c];
+#pragma unroll
+          for (int q = 0; q < c; ++q) v -= x[q] * cs[PNL(c, q)];
+          x[c] = v * rdiag[c];
+        }
+#pragma unroll
+        for (int c = 0; c < CB; ++c) cs[PNL(r, c)] = x[c];
+      }
+      __syncthreads();
+      if (J == 0) CHOL_T(6);
+      for (int e = tid; e < R * CB; e += CH_NT) {
+        const int r = e / CB, c = e % CB;
+        if (c <= r) W[(size_t)(J + r) * p + J + c] = cs[PNL(r, c)];
+      }
+      // (c) trailing update of the lower triangle, W[i][k] -= sum_c P[i][c] P[k][c] for
+      //     J+32 <= k <= i, on fp64 DMMA (m16n8k4, K = 32 from the panel in smem): 64 x 64 blocks
+      //     of the lower block triangle, one 16 x 16 sub-tile per warp
+      {
+        const int R2 = p - J - CB;  // trailing order, a multiple of 32
+        const int nb = (R2 + 63) / 64;
+        const int nblk = nb * (nb + 1) / 2;
+        const int wr = (warp >> 2) * 16, wc = (warp & 3) * 16;  // warp sub-tile in the block
+        const int g8 = lane >> 2, t4 = lane & 3;
+        for (int b = 0; b < nblk; ++b) {
+          int bi = (int)((sqrt(8.0 * b + 1.0) - 1.0) * 0.5);
+          while (bi * (bi + 1) / 2 > b) --bi;
+          while ((bi + 1) * (bi + 2) / 2 <= b) ++bi;
+          const int bk = b - bi * (bi + 1) / 2;
+          const int ri = bi * 64 + wr, rk = bk * 64 + wc;  // trailing-local row / col bases
+          if (ri >= R2 || rk >= R2 || (bi == bk && rk > ri + 15)) continue;
+          double acc[2][4];
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[nt][e] = 0.0;
+#pragma unroll
+          for (int kk = 0; kk < CB; kk += 4) {
+            const double a0 = cs[PNL(CB + ri + g8, kk + t4)];
+            const double a1 = cs[PNL(CB + ri + g8 + 8, kk + t4)];
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+              const double b0 = cs[PNL(CB + rk + nt * 8 + g8, kk + t4)];
+              dmma16884(acc[nt], a0, a1, b0);
+            }
+          }
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int i = J + CB + ri + g8 + 8 * h, k = J + CB + rk + nt * 8 + 2 * t4 + e;
+                if (k <= i) W[(size_t)i * p + k] -= acc[nt][2 * h + e];
+              }
         }
       }
       __syncthreads();
+      if (J == 0) CHOL_T(7);
     }
     __syncthreads();
     if (!s_fail) break;
@@ -396,55 +450,61 @@ __global__ void __launch_bounds__(1024) chol_inv_big_kernel(const double* __rest
     if (shift_flag_out && attempt) *shift_flag_out = 1;
   }
   __syncthreads();
-  // ---- diagonal block inverses: Dinv[I] = L_II^{-1} (32 x 32 lower), warp-per-... one block at
-  // a time: forward substitution on the 32 columns of the identity (thread (ty, tx) = (row, col))
-  for (int I = 0; I < p; I += CB) {
-    T[ty * CB_LD + tx] = W[(size_t)(I + ty) * p + I + tx];  // L_II (upper part unused)
-    __syncthreads();
-    double x = (ty == tx) ? 1.0 : 0.0;  // becomes X[ty][tx]
-    cs[ty * CB_LD + tx] = 0.0;
-    __syncthreads();
-    for (int r = 0; r < CB; ++r) {
-      if (ty == r) {
-        double s = x;
-        for (int q = 0; q < r; ++q) s -= T[r * CB_LD + q] * cs[q * CB_LD + tx];
-        cs[r * CB_LD + tx] = s / T[r * CB_LD + r];
-      }
-      __syncthreads();
+  CHOL_T(2);
+  // ---- diagonal-block inverses, one warp per 32 x 32 block in parallel: lane j solves
+  //      L_II x = e_j (forward substitution, L_II read from global as a broadcast)
+  for (int I = warp * CB; I < p; I += (CH_NT / 32) * CB) {
+    double x[CB];
+#pragma unroll
+    for (int i = 0; i < CB; ++i) {
+      double v = (i == lane) ? 1.0 : 0.0;
+      const double* li = W + (size_t)(I + i) * p + I;
+#pragma unroll
+      for (int q = 0; q < i; ++q) v -= li[q] * x[q];
+      x[i] = v / li[i];
     }
-    Dinv[(size_t)(I / CB) * CB * CB + ty * CB + tx] = cs[ty * CB_LD + tx];
+#pragma unroll
+    for (int i = 0; i < CB; ++i) Dinv[(size_t)(I / CB) * CB * CB + i * CB + lane] = x[i];
+  }
+  CHOL_T(3);
+}
+
+// X = L^{-1} by independent column blocks: CTA C computes X[:, C..C+32) (forward substitution
+// over the row blocks I >= C: X[I, C] = Dinv_I (E[I, C] - L[I, C:I] X[C:I, C])) and writes the
+// transposed rows Rinv[C + cc][:] (Rinv = L^{-T}, upper triangular).
+__global__ void __launch_bounds__(1024) linv_big_kernel(const double* __restrict__ W, int p,
+                                                        const double* __restrict__ Dinv,
+                                                        double* __restrict__ Rinv,
+                                                        const int* cond) {
+  if (cond && *cond == 0) return;
+  extern __shared__ double cs[];  // (p - C) x CB_LD block of X, + CB x CB_LD scratch
+  const int C = blockIdx.x * CB;
+  double* T = cs + (size_t)p * CB_LD;
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  for (int I = C; I < p; I += CB) {
+    // s = E[I, C] - L[I, C:I] X[C:I, C]: warp ty owns row I + ty of L (32 consecutive entries
+    // per coalesced load, broadcast by shuffles)
+    double s = (I == C && ty == tx) ? 1.0 : 0.0;
+    const double* lrow = W + (size_t)(I + ty) * p;
+#pragma unroll 2
+    for (int k0 = C; k0 < I; k0 += 32) {
+      const double lv = lrow[k0 + tx];
+#pragma unroll
+      for (int q = 0; q < 32; ++q)
+        s -= __shfl_sync(0xffffffffu, lv, q) * cs[(k0 + q - C) * CB_LD + tx];
+    }
+    T[ty * CB_LD + tx] = s;
+    __syncthreads();
+    const double* di = Dinv + (size_t)(I / CB) * CB * CB + ty * CB;
+    double x = 0.0;
+#pragma unroll 8
+    for (int q = 0; q < CB; ++q) x += di[q] * T[q * CB_LD + tx];
+    cs[(I - C + ty) * CB_LD + tx] = x;
     __syncthreads();
   }
-  // ---- X = L^{-1} by column blocks C; XB (rows C.., 32 columns) in cs
-  for (int C = 0; C < p; C += CB) {
-    for (int I = C; I < p; I += CB) {
-      // s = E[I, C] - L[I, C:I] X[C:I, C]  (thread (ty, tx) = element (I + ty, C + tx))
-      // warp ty owns row I + ty of L: 32 consecutive entries per coalesced load, broadcast by
-      // shuffles (the old per-thread walk along the row was L2-latency bound)
-      double s = (I == C && ty == tx) ? 1.0 : 0.0;
-      const double* lrow = W + (size_t)(I + ty) * p;
-#pragma unroll 2
-      for (int k0 = C; k0 < I; k0 += 32) {
-        const double lv = lrow[k0 + tx];
-#pragma unroll
-        for (int q = 0; q < 32; ++q)
-          s -= __shfl_sync(0xffffffffu, lv, q) * cs[(k0 + q - C) * CB_LD + tx];
-      }
-      T[ty * CB_LD + tx] = s;
-      __syncthreads();
-      const double* di = Dinv + (size_t)(I / CB) * CB * CB + ty * CB;
-      double x = 0.0;
-#pragma unroll 8
-      for (int q = 0; q < CB; ++q) x += di[q] * T[q * CB_LD + tx];
-      cs[(I - C + ty) * CB_LD + tx] = x;
-      __syncthreads();
-    }
-    // Rinv[c][i] = X[i][c] (upper triangular), c in the block, all i
-    for (int e = tid; e < CB * p; e += 1024) {
-      const int cc = e / p, i = e % p;
-      Rinv[(size_t)(C + cc) * p + i] = (i >= C + cc) ? cs[(i - C) * CB_LD + cc] : 0.0;
-    }
-    __syncthreads();
+  for (int e = tid; e < CB * p; e += 1024) {
+    const int cc = e / p, i = e % p;
+    Rinv[(size_t)(C + cc) * p + i] = (i >= C + cc) ? cs[(i - C) * CB_LD + cc] : 0.0;
   }
 }
 
@@ -453,16 +513,21 @@ cudaError_t chol_inv_big_launch(const double* G, int p, int64_t n_global, double
                                 const int* cond, cudaStream_t st) {
   const double u = 1.1102230246251565e-16;
   const double scale = 11.0 * ((double)n_global * p + (double)p * (p + 1)) * u;
-  const size_t smem = ((size_t)p * CB_LD + CB * CB_LD) * sizeof(double);
+  const size_t smem = (size_t)(p * CB_LD + p / 4 + 4) * sizeof(double);
+  const size_t smem2 = ((size_t)p * CB_LD + CB * CB_LD) * sizeof(double);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(chol_inv_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)((512 * CB_LD + 512 / 4 + 4) * sizeof(double)));
+    cudaFuncSetAttribute(linv_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)((512 * CB_LD + CB * CB_LD) * sizeof(double)));
     attr = true;
   }
   count_launch();
-  chol_inv_big_kernel<<<1, 1024, smem, st>>>(G, p, scale, W, Dinv, Rinv, state, shift_flag_out,
-                                             cond);
+  chol_inv_big_kernel<<<1, CH_NT, smem, st>>>(G, p, scale, W, Dinv, Rinv, state, shift_flag_out,
+                                              cond);
+  count_launch();
+  linv_big_kernel<<<p / CB, 1024, smem2, st>>>(W, p, Dinv, Rinv, cond);
   return cudaGetLastError();
 }
 
