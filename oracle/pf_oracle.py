@@ -33,13 +33,14 @@ import math
 import numpy as np
 
 from pfinputs import (Config, initial_block, lanczos_start, cfg1_problem, cfg1_noise,
-                      pfpg_problem, pfam_problem, unpack_bitmask, cfg5_problem, cfg5_perturb)
+                      pfpg_problem, pfam_problem, unpack_bitmask, cfg5_problem, cfg5_perturb,
+                      nce_problem)
 
 __all__ = [
     "cheb_T", "growth_lower_bound", "interval_map", "interval_psd", "interval_top_r",
     "interval_soft", "lanczos_extremes", "rebase_plan", "spread_estimate", "chebyshev_filter",
     "orth", "filter_update", "rayleigh_ritz", "spectral_psd", "spectral_soft", "jacobi_eig",
-    "exact_spectral", "maxcut_C", "prox_tG_diag", "pfam_next", "pfpg_next", "run",
+    "exact_spectral", "maxcut_C", "prox_tG_diag", "pfam_next", "pfpg_next", "nce_next", "run",
     "lowrank_diff_fro", "lowrank_fro", "sin_theta",
 ]
 
@@ -276,6 +277,19 @@ def pfpg_next(V, f, omega: np.ndarray, M: np.ndarray, tau: float):
     return X - tau * R, float(0.5 * np.sum(R * R))
 
 
+def nce_next(V, f, x, G, tau):
+    """Dual gradient step of nearest correlation estimation (eqn:NCE-dual, eqn:NCE-gradient,
+    P:910-923): with B = G + Diag(x), Pi_+(B) ~ V diag(f) V^T (f = max(theta, 0)),
+    F(x) = 1/2 sum f_i^2 - 1^T x, grad F(x) = diag(Pi_+(B)) - 1, x+ = x - tau grad F(x).
+    Returns (x+, B+ = G + Diag(x+), F(x), ||grad F(x)||)."""
+    d = np.sum((V * V) * f[None, :], axis=1)          # diag(V diag(f) V^T)
+    g = d - 1.0
+    F = 0.5 * float(np.sum(f * f)) - float(np.sum(x))
+    xn = x - tau * g
+    B = G + np.diag(xn)
+    return xn, B, F, float(np.linalg.norm(g))
+
+
 # ============================================================================ metrics
 def lowrank_fro(V, f) -> float:
     """||V diag(f) V^T||_F = ||R diag(f) R^T||_F with V = Q R (thin QR; no n x n buffer)."""
@@ -347,9 +361,14 @@ def run(cfg: Config, iters: int | None = None, record_factors: bool = True,
         prob = pfam_problem(cfg) if problem is None else problem
         C = maxcut_C(unpack_bitmask(prob["adj_bits"], cfg.n), prob["deg"])
         A = prox_tG_diag(np.zeros((cfg.n, cfg.n)), C, cfg.t)      # Z_1 (reading R9)
+    elif cfg.mode == "nce":
+        prob = nce_problem(cfg) if problem is None else problem
+        Gn = prob["G"]
+        xn = 1.0 - np.diag(Gn)                                    # x^0 = 1 - diag(G)
+        A = Gn + np.diag(xn)
     else:
         raise ValueError(cfg.mode)
-    psd = cfg.mode in ("sweep_psd", "pfam")
+    psd = cfg.mode in ("sweep_psd", "pfam", "nce")
     thr = None if psd else _threshold(cfg, prob if cfg.mode == "pfpg" else None)
 
     recs = []
@@ -386,6 +405,11 @@ def run(cfg: Config, iters: int | None = None, record_factors: bool = True,
             A, fit = pfpg_next(V[:, keep], f[keep], omega, M, cfg.tau)
             rec["objective"] = fit + prob["mu"] * float(np.sum(np.abs(f)))
             rec["fit"] = fit
+        elif cfg.mode == "nce":
+            xn, A, F, gn = nce_next(V[:, keep], f[keep], xn, Gn, cfg.tau)
+            rec["objective"] = F
+            rec["grad_norm"] = gn
+            rec["x"] = xn
         else:
             A, cw, res = pfam_next(V[:, keep], f[keep], A, C, cfg.t)
             rec["objective"] = cw

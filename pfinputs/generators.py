@@ -13,6 +13,7 @@ oracle and the GPU path see bit-identical inputs.  Stream ids:
     8  Erdos-Renyi edges for config 3
     9  config-5 spectrum (large eigenvalues, semicircle bulk, positions)
    10  config-5 Householder vectors
+   11  NCE data matrix G (Examples 5.2 / 5.3 of the paper)
 
 Config-5 noise is NOT drawn from a numpy stream: at n = 65536 it is 2^31 Gaussians per
 iteration, generated on the device by the library's workload helper.  Both sides implement the
@@ -64,6 +65,8 @@ class Config:
     # the first d - tf32_tail Chebyshev steps at tf32_early MMA passes, the rest in 3xTF32
     tf32_early: int = 3
     tf32_tail: int = 0
+    # nearest correlation estimation (mode "nce"): paper Example eg:5.6 (6) or eg:5.7 (7)
+    nce_example: int = 7
     nbig: int = 256           # config 5: eigenvalues drawn from U[5, 50]
     nrefl: int = 64           # config 5: Householder reflectors in the basis
 
@@ -78,6 +81,14 @@ CONFIGS = {
               r=50, omega_prob=0.05),
     5: Config("cfg5_soft_sweep_n65536", n=65536, p=512, d=8, iters=30, mode="sweep_soft",
               dtype="tf32", rho_max=1e3, gen="cfg5", tf32_early=1, tf32_tail=2),
+}
+
+
+# Beyond BASELINE.json: the dual gradient method for nearest correlation
+# estimation, paper §5.1 (eqn:NCE-dual, Examples eg:5.6 / eg:5.7, Table tab:ncm).
+NEXT_CONFIGS = {
+    "nce7": Config("nce_ex57_n4000", n=4000, p=64, d=8, iters=300, mode="nce", nce_example=7),
+    "nce6": Config("nce_ex56_n2000", n=2000, p=128, d=8, iters=200, mode="nce", nce_example=6),
 }
 
 
@@ -334,3 +345,19 @@ def cfg5_perturb(cfg: Config, A32: np.ndarray, k: int, chunk: int = 1024) -> Non
     for i0 in range(0, cfg.n, chunk):
         i1 = min(cfg.n, i0 + chunk)
         A32[i0:i1] += cfg5_noise_rows(cfg, k, i0, i1)
+
+
+# ----------------------------------------------------------------------------- NCE (NEXT-1)
+def nce_problem(cfg: Config) -> dict:
+    """G of Examples eg:5.6 / eg:5.7: G_ij iid uniform in [-1, 1] (5.6) or [0, 2]
+    (5.7) for i < j, mirrored, G_ii = 1.  Upper triangle drawn row by row from stream 11."""
+    n = cfg.n
+    lo, hi = (-1.0, 1.0) if cfg.nce_example == 6 else (0.0, 2.0)
+    rs = _rng(cfg.seed, 11)
+    G = np.empty((n, n))
+    for i in range(n):
+        G[i, i:] = rs.uniform(lo, hi, n - i)
+    iu = np.triu_indices(n, 1)
+    G[(iu[1], iu[0])] = G[iu]
+    np.fill_diagonal(G, 1.0)
+    return {"G": G}
