@@ -158,6 +158,18 @@ pf_status pf_admm_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f
                        const uint32_t* adj, int64_t ldadj, const double* deg, double* Z,
                        int64_t ldz, double* obj, pf_stream stream);
 
+/* Nearest correlation estimation, dual gradient step (eqn:NCE-dual and
+ * eqn:NCE-gradient), PF_FP64 contexts: with Pi_+(B) ~ V diag(f) V^T for the iterate
+ * B = G + Diag(x) (f = max(theta, 0) from pf_spectral_op PF_OP_PSD):
+ *   grad_i = diag(V diag(f) V^T)_i - 1,  x <- x - tau grad,  B_ii <- G_ii + x_i.
+ * V: local rows (n_local x p, ldv); gdiag: device double[n] (full diag(G)); x: device
+ * double[n_local] (this rank's slice), in/out; B: local rows (n_local x n, ldb) -- only its
+ * diagonal entries (i, row0 + i) are written.  obj: device double[2] = {F(x_old),
+ * ||grad F(x_old)||}, F(x) = 1/2 sum f_i^2 - 1^T x.  tau > 0 (the paper uses tau = 1). */
+pf_status pf_nce_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f, double tau,
+                      const double* gdiag, double* x, double* B, int64_t ldb, double* obj,
+                      pf_stream stream);
+
 /* ---------------------------------------------------------------------------- measurement */
 /* Enable (1) / disable (0) per-launch CUDA-event timing of the Chebyshev-step GEMM (the
  * dominant kernel): each launch inside pf_filter / pf_rayleigh_ritz is bracketed by events on

@@ -833,6 +833,21 @@ pf_status pf_admm_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f
   return PF_OK;
 }
 
+pf_status pf_nce_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f, double tau,
+                      const double* gdiag, double* x, double* B, int64_t ldb, double* obj,
+                      pf_stream stream) {
+  if (!ctx || !V || !f || !gdiag || !x || !B || !obj) return PF_ERR_ARG;
+  if (ctx->dtype != PF_FP64) return PF_ERR_UNSUPPORTED;
+  if (ldv < ctx->p || ldb < ctx->n) return PF_ERR_DIM;
+  if (!(tau > 0.0)) return PF_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  PF_CU(nce_launch(V, ldv, f, ctx->p, tau, gdiag, x, B, ldb, (int)ctx->n_local, (int)ctx->row0,
+                   ctx->rb_part, ctx->rb_cnt, obj, st));
+  PF_TRY(allreduce(ctx, obj, 2, st));  // raw sums over the row blocks
+  PF_CU(nce_finish_launch(f, ctx->p, obj, st));
+  return PF_OK;
+}
+
 pf_status pf_perturb(pf_ctx ctx, double* A, int64_t lda, const double* E, int64_t lde,
                      pf_stream stream) {
   if (!ctx || !A || !E) return PF_ERR_ARG;

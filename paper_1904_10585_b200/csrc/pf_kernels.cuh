@@ -141,5 +141,10 @@ cudaError_t admm_launch(const double* V, int64_t ldv, const double* Vloc, int64_
                         int p, double* obj, double* partials, int* counter, int raw, double* vf,
                         cudaStream_t st);
 cudaError_t sqrt_inplace_launch(double* x, cudaStream_t st);
+// NCE dual gradient update (NEXT-1): partials >= 2 * 256 doubles; obj gets raw sums
+cudaError_t nce_launch(const double* V, int64_t ldv, const double* f, int p, double tau,
+                       const double* gdiag, double* x, double* B, int64_t ldb, int n_rows,
+                       int row0, double* partials, int* counter, double* obj, cudaStream_t st);
+cudaError_t nce_finish_launch(const double* f, int p, double* obj, cudaStream_t st);
 
 }  // namespace pf

@@ -419,3 +419,91 @@ cudaError_t sqrt_inplace_launch(double* x, cudaStream_t st) {
 }
 
 }  // namespace pf
+
+namespace pf {
+
+// ============================================================================== NCE update
+// Dual gradient step of nearest correlation estimation (eqn:NCE-dual,
+// eqn:NCE-gradient): with Pi_+(G + Diag x) ~ V diag(f) V^T on the local rows,
+//   d_i = sum_c f_c V_ic^2,  g_i = d_i - 1,  x_i <- x_i - tau g_i,  B_{i, row0 + i} = G_ii + x_i.
+// Only the diagonal of the iterate changes, so the update is O(n p) -- the filter dominates even
+// more than in PFPG / PFAM.  One warp per row (coalesced row of V); raw sums {sum x_old,
+// sum g^2} reduced deterministically (per-CTA partials, last CTA sums in CTA order); the
+// objective is finished by nce_finish_kernel after the (optional) cross-rank all-reduce.
+constexpr int kNceThreads = 256;
+
+__global__ void __launch_bounds__(kNceThreads) nce_kernel(
+    const double* __restrict__ V, int64_t ldv, const double* __restrict__ f, int p, double tau,
+    const double* __restrict__ gdiag, double* __restrict__ x, double* __restrict__ B, int64_t ldb,
+    int n_rows, int row0, double* partials, int* counter, double* obj) {
+  __shared__ double red[32];
+  __shared__ int s_last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wpb = kNceThreads / 32;
+  double sx = 0.0, sg = 0.0;
+  for (int i = blockIdx.x * wpb + warp; i < n_rows; i += gridDim.x * wpb) {
+    double d = 0.0;
+    for (int c = lane; c < p; c += 32) {
+      const double v = V[(size_t)i * ldv + c];
+      d += f[c] * v * v;
+    }
+    d = warp_sum(d);
+    if (lane == 0) {
+      const double g = d - 1.0, xo = x[i], xn = xo - tau * g;
+      x[i] = xn;
+      B[(size_t)i * ldb + row0 + i] = gdiag[row0 + i] + xn;
+      sx += xo;
+      sg += g * g;
+    }
+  }
+  sx = block_sum(sx, red);
+  sg = block_sum(sg, red);
+  if (threadIdx.x == 0) {
+    partials[2 * (size_t)blockIdx.x] = sx;
+    partials[2 * (size_t)blockIdx.x + 1] = sg;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(counter, 1) == (int)gridDim.x - 1);
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    if (threadIdx.x == 0) {
+      double tx = 0.0, tg = 0.0;
+      for (int b = 0; b < (int)gridDim.x; ++b) {
+        tx += __ldcg(partials + 2 * (size_t)b);
+        tg += __ldcg(partials + 2 * (size_t)b + 1);
+      }
+      obj[0] = tx;  // raw: sum x_old (local rows)
+      obj[1] = tg;  // raw: sum g^2
+      *counter = 0;
+    }
+  }
+}
+
+// obj <- {1/2 sum f^2 - sum x_old, sqrt(sum g^2)}  (F(x_old), ||grad F(x_old)||)
+__global__ void nce_finish_kernel(const double* f, int p, double* obj) {
+  if (threadIdx.x != 0) return;
+  double s = 0.0;
+  for (int c = 0; c < p; ++c) s += f[c] * f[c];
+  obj[0] = 0.5 * s - obj[0];
+  obj[1] = sqrt(obj[1]);
+}
+
+cudaError_t nce_launch(const double* V, int64_t ldv, const double* f, int p, double tau,
+                       const double* gdiag, double* x, double* B, int64_t ldb, int n_rows,
+                       int row0, double* partials, int* counter, double* obj, cudaStream_t st) {
+  const int blocks = std::max(1, std::min(256, (n_rows + 7) / 8));
+  count_launch();
+  nce_kernel<<<blocks, kNceThreads, 0, st>>>(V, ldv, f, p, tau, gdiag, x, B, ldb, n_rows, row0,
+                                             partials, counter, obj);
+  return cudaGetLastError();
+}
+
+cudaError_t nce_finish_launch(const double* f, int p, double* obj, cudaStream_t st) {
+  count_launch();
+  nce_finish_kernel<<<1, 32, 0, st>>>(f, p, obj);
+  return cudaGetLastError();
+}
+
+}  // namespace pf

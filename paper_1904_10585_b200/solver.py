@@ -11,7 +11,7 @@ import numpy as np
 import torch
 
 from pfinputs import (Config, initial_block, lanczos_start, cfg1_problem, cfg1_noise, pfpg_problem,
-                      pfam_problem, cfg5_problem)
+                      pfam_problem, cfg5_problem, nce_problem)
 
 from ._lib import Context, PF_FP64, PF_TF32, PF_OP_PSD, PF_OP_SOFT_THRESHOLD
 
@@ -49,7 +49,7 @@ class Solver:
         self.r0, self.r1, self.n_local = r0, r1, r1 - r0
         assert self.n_local == self.ctx.n_local
         nl = self.n_local
-        self.psd = cfg.mode in ("sweep_psd", "pfam")
+        self.psd = cfg.mode in ("sweep_psd", "pfam", "nce")
         self.op = PF_OP_PSD if self.psd else PF_OP_SOFT_THRESHOLD
         # problem["_dev"]: inputs already on the device (the e2e path uploads them itself)
         devp = (problem or {}).get("_dev") or {}
@@ -105,6 +105,19 @@ class Solver:
             # Z_0 = 0 -> Z_1 = prox_tG(0) = offdiag(-tC) + I  (reading R9)
             self.ctx.admm_step(self.V.zero_(), self.f, cfg.t, self.adj, self.deg, self.A,
                                self.obj, stream)
+        elif cfg.mode == "nce":
+            # nearest correlation estimation (NEXT-1): B = G + Diag(x), x^0 = 1 - diag(G)
+            prob = nce_problem(cfg) if problem is None else problem
+            self.prob = prob
+            G = prob["G"]
+            self.gdiag = _dev(np.ascontiguousarray(np.diag(G)))
+            self.x = _dev((1.0 - np.diag(G))[r0:r1])
+            B0 = G[r0:r1].copy()
+            B0[np.arange(nl), r0 + np.arange(nl)] = 1.0           # G_ii + x^0_i = 1
+            # even row pitch (16-byte TMA rows, include/pf.h) for any n
+            buf = torch.zeros((nl, (n + 1) // 2 * 2), dtype=torch.float64, device="cuda")
+            buf[:, :n].copy_(torch.from_numpy(B0))
+            self.A = buf[:, :n]
         else:
             raise ValueError(cfg.mode)
         self.ctx.orth(self.U, stream)
@@ -132,6 +145,8 @@ class Solver:
             ctx.prox_step(self.V, self.f, cfg.tau, self.omega, self.W, self.A, self.obj, st)
         elif cfg.mode == "pfam":
             ctx.admm_step(self.V, self.f, cfg.t, self.adj, self.deg, self.A, self.obj, st)
+        elif cfg.mode == "nce":
+            ctx.nce_step(self.V, self.f, cfg.tau, self.gdiag, self.x, self.A, self.obj, st)
         # Warm start the next filter from the Ritz vectors: Range(V) = Range(U), so the method
         # is unchanged (eqn:subspace-update depends on Range(U) only), but the next H = Q^T A Q
         # is then nearly diagonal and the Jacobi solve converges in one or two sweeps.
@@ -156,6 +171,8 @@ class Solver:
         o = self.obj.cpu().numpy()
         if self.cfg.mode == "pfpg":
             return float(o[0] + self.mu * o[1]), float(o[0])
+        if self.cfg.mode == "nce":
+            return float(o[0]), float(o[1])            # F(x_k), ||grad F(x_k)||
         return float(o[0]), float(o[1])
 
 
@@ -173,8 +190,10 @@ def run(cfg: Config, iters: int | None = None, record: bool = True, problem=None
             keep = f != 0.0
             rec.update(theta=s.theta.cpu().numpy(), rank=int(s.rank.item()),
                        V=s.ritz_factors()[:, keep], f=f[keep])
-            if cfg.mode in ("pfpg", "pfam"):
+            if cfg.mode in ("pfpg", "pfam", "nce"):
                 rec["objective"], rec["aux"] = s.objective()
+            if cfg.mode == "nce":
+                rec["x"] = s.x.cpu().numpy()
         if cfg.mode in ("sweep_psd", "sweep_soft") and k + 1 < K:
             if cfg.gen == "cfg5":
                 s.perturb_hash(k)
