@@ -1,0 +1,68 @@
+"""Nearest correlation estimation (paper §5.1 / Table tab:ncm) on one B200:
+the filtered dual gradient method run to the paper's stopping rule ||grad F|| <= 1e-7
+||grad F(x0)||.  Reports iterations, time (CUDA events around the whole solve,
+problem upload excluded) and the objective; the paper's CPU numbers (2 x 12-core Xeon E5-2680
+v3, MATLAB) are printed beside them as context, not as a target.
+
+  python tools/bench_nce.py [--example 7] [--n 4000] [--p 64] [--d 8] [--max-iters 600]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+PAPER = {  # tab:ncm, PFPG columns: (time s, iterations, f)
+    (6, 2000): (4.8, 22, 7.8e4), (6, 4000): (27.2, 25, 2.3e5),
+    (7, 2000): (5.0, 76, 2.0e6), (7, 4000): (32.8, 142, 8.0e6),
+}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--example", type=int, default=7)
+    ap.add_argument("--n", type=int, default=4000)
+    ap.add_argument("--p", type=int, default=64)
+    ap.add_argument("--d", type=int, default=8)
+    ap.add_argument("--max-iters", type=int, default=600)
+    a = ap.parse_args()
+    import torch
+    from pfinputs import NEXT_CONFIGS, reduced, nce_problem
+    from paper_1904_10585_b200 import Solver
+    cfg = reduced(NEXT_CONFIGS["nce%d" % a.example], n=a.n, p=a.p, d=a.d)
+    prob = nce_problem(cfg)
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        s = Solver(cfg, problem=prob, stream=st)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g0 = None
+    it = 0
+    with torch.cuda.stream(st):
+        e0.record(st)
+        while it < a.max_iters:
+            s.step()
+            it += 1
+            F, g = s.objective()          # F(x_{k}), ||grad F(x_k)|| (one 16-byte D2H per step)
+            if g0 is None:
+                g0 = g
+            if g <= 1e-7 * g0:
+                break
+        e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    ref = PAPER.get((a.example, a.n))
+    print(json.dumps({
+        "problem": f"NCE Example 5.{a.example - 4} (label eg:5.{a.example}), n={a.n}, "
+                   f"p={a.p}, d={a.d}, tau=1, x0 = 1 - diag(G), fp64, 1 B200",
+        "iterations": it, "time_s": ms / 1e3, "ms_per_iter": ms / it, "objective": F,
+        "rel_grad": g / g0, "rank_last": int(s.rank.item()), "status": s.ctx.status(st)["names"],
+        "paper_pfpg_cpu": None if ref is None else
+        {"time_s": ref[0], "iterations": ref[1], "f": ref[2],
+         "machine": "2 x Xeon E5-2680 v3 (24 cores), MATLAB; context only"}}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
