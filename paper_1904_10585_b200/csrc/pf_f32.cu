@@ -11,6 +11,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "../../include/pf.h"
 #include "pf_kernels.cuh"
@@ -645,11 +646,13 @@ __global__ void __launch_bounds__(JB_THREADS) jacobi_big_kernel(
           c = hh * rc;
           s = (dd >= 0.0 ? 0.5 : -0.5) * ee * ir * rc;
           t = s * rc;
-          if (blockIdx.x == 0) atomicAdd(&s_cnt, 1);
         }
         csv[3 * m] = c;
         csv[3 * m + 1] = s;
         csv[3 * m + 2] = t;
+        // rotation count by ballot (one shared atomic per warp, CTA 0 only)
+        const unsigned rot = __ballot_sync(0xffffffffu, s != 0.0);  // half = p/2 >= 32
+        if (blockIdx.x == 0 && (m & 31) == 0) atomicAdd(&s_cnt, __popc(rot));
       }
       __syncthreads();
       for (int e = gtid; e < nblk; e += gthreads) {
@@ -735,7 +738,14 @@ __global__ void __launch_bounds__(JB_THREADS) jacobi_big_kernel(
   }
 }
 
-int jacobi_big_grid() { return 64; }
+int jacobi_big_grid() {
+  static int g = 0;
+  if (!g) {  // development knob PF_JB_GRID (cooperative grid size), default 64
+    const char* e = getenv("PF_JB_GRID");
+    g = e ? atoi(e) : 64;
+  }
+  return g;
+}
 
 // Hw: 2 p^2 doubles, Vw: p^2, red_ws: 2 * jacobi_big_grid() doubles, cnt_ws: 4 ints
 cudaError_t jacobi_big_launch(const double* H, int p, double* theta, double* Y, double* Hw,

@@ -476,12 +476,15 @@ __global__ void __launch_bounds__(JacCfg<PE>::THREADS) jacobi_kernel(
             c = hh * rc;
             s = (dd >= 0.0 ? 0.5 : -0.5) * ee * ir * rc;
             t = s * rc;
-            atomicAdd(&s_cnt, 1);
           }
         }
         cs[3 * m] = c;
         cs[3 * m + 1] = s;
         cs[3 * m + 2] = t;
+        // count rotations with a ballot (a shared atomic per rotating pair serialises the round)
+        const unsigned wmask = C::HALF >= 32 ? 0xffffffffu : ((1u << C::HALF) - 1u);
+        const unsigned rot = __ballot_sync(wmask, s != 0.0);
+        if ((m & 31) == 0) atomicAdd(&s_cnt, __popc(rot));
       }
       __syncthreads();
       for (int e = tid; e < C::NBLK; e += NT) {
