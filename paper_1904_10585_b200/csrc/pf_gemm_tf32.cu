@@ -20,7 +20,8 @@
 //    stages its 128 rows of A and HALF of every 256-column slice of B, so per-SM B traffic is
 //    halved; the leader CTA issues M=256 x N=min(p,256) x K=8 MMAs into both CTAs' TMEM
 //    (128 lanes x p fp32 columns each).
-//  * TMA (cp.async.bulk.tensor.2d, SWIZZLE_64B, 16-wide K boxes) into a STAGES-deep ring.
+//  * TMA (cp.async.bulk.tensor.2d, SWIZZLE_64B, 16-wide K boxes) into a STAGES-deep ring, A loads
+//    tagged L2 evict_first (streamed once), Y loads evict_last (re-read by every pair).
 //  * kind::tf32 reads an fp32 operand as tf32 by dropping the low 13 mantissa bits (checked on
 //    the device: tools/probe/tf32_probe.cu), so the raw TMA tile IS the hi operand; converter
 //    warps write lo = x - trunc13(x) (exact in fp32) into a separate, shallower ring and release
@@ -56,7 +57,6 @@ struct Tf32Cfg {
   static constexpr int NL = RING >= 12 ? 4 : 3;
   static constexpr int NT = (RING - NL) > 12 ? 12 : (RING - NL);
   static constexpr int TMEM_COLS = P < 32 ? 32 : P;
-  static constexpr int PF_DIST = 32;              // L2 prefetch distance (k-blocks) for A
   static constexpr int NCONV_WARPS = 6;           // warps 2..7
   static constexpr int NEPI_WARPS = 8;            // warps 8..15: lane quarter x column half
   static constexpr int THREADS = 16 * 32;
@@ -84,6 +84,7 @@ struct Tf32Args {
   int bdist_kb;        // > 0: B is the rank-major all-gather [world][p][n_local] read through a
                        // 3-D map; k-blocks per rank (n_local / 16)
   float* acc;          // fp32 chunk accumulators: [pair][2 ctas][P][128]
+  int pf_dist;         // L2 prefetch distance of A in k-blocks (0: off)
 };
 
 // Work schedule of pair g among G pairs: F = M / G full waves in which every pair runs a whole
@@ -197,6 +198,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tf32Cfg<P>::THREADS,
     // ------------------------------------------------------------ TMA producer (one lane)
     if (lane == 0) {
       Ring rt(C::NT);
+      const uint64_t pol_a = tc::policy_evict_first(), pol_b = tc::policy_evict_last();
       for (int w = 0; w < nitems; ++w) {
         int tile, kb0, kb1;
         sch.item(w, tile, kb0, kb1);
@@ -204,25 +206,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tf32Cfg<P>::THREADS,
         for (int kb = kb0; kb < kb1; ++kb, rt.next()) {
           // A streams from HBM exactly once: pull it into L2 PF_DIST k-blocks ahead in
           // 128-byte row segments (every other k-block)
-          if (((kb - kb0) & 1) == 0 && kb + C::PF_DIST < kb1)
-            tc::tma_prefetch_2d(&mapApf, (kb + C::PF_DIST) * C::BK, arow);
+          if (args.pf_dist > 0 && ((kb - kb0) & 1) == 0 && kb + args.pf_dist < kb1)
+            tc::tma_prefetch_2d(&mapApf, (kb + args.pf_dist) * C::BK, arow, pol_a);
           mbar_wait(&empty[rt.s], rt.ph ^ 1u);
           TRACE(0 + 6 * crank, w, kb - kb0);
           unsigned char* st = raw + rt.s * C::STAGE_BYTES;
           mbar_arrive_expect_tx(&full[rt.s], C::STAGE_BYTES);
-          tma_load_2d(st, &mapA, &full[rt.s], kb * C::BK, arow);
+          tc::tma_load_2d_hint(st, &mapA, &full[rt.s], kb * C::BK, arow, pol_a);
           if (args.bdist_kb > 0) {
             // global k-block kb lives in rank kb / bdist_kb's slab at local k-block kb % bdist_kb
             const int rk = kb / args.bdist_kb, lk = kb - rk * args.bdist_kb;
 #pragma unroll
             for (int h = 0; h < C::NH; ++h)
-              tc::tma_load_3d(st + C::A_BYTES + h * (C::NMMA / 2) * 64, &mapB, &full[rt.s],
-                              lk * C::BK, h * C::NMMA + (int)crank * (C::NMMA / 2), rk);
+              tc::tma_load_3d_hint(st + C::A_BYTES + h * (C::NMMA / 2) * 64, &mapB, &full[rt.s],
+                                   lk * C::BK, h * C::NMMA + (int)crank * (C::NMMA / 2), rk,
+                                   pol_b);
           } else {
 #pragma unroll
             for (int h = 0; h < C::NH; ++h)
-              tma_load_2d(st + C::A_BYTES + h * (C::NMMA / 2) * 64, &mapB, &full[rt.s],
-                          kb * C::BK, h * C::NMMA + (int)crank * (C::NMMA / 2));
+              tc::tma_load_2d_hint(st + C::A_BYTES + h * (C::NMMA / 2) * 64, &mapB, &full[rt.s],
+                                   kb * C::BK, h * C::NMMA + (int)crank * (C::NMMA / 2), pol_b);
           }
         }
       }
@@ -442,8 +445,14 @@ Tf32Plan tf32_plan(int p, int n_rows, int n_k, int num_sms) {
   pl.split = R ? std::max(1, std::min(smax, G / R)) : 1;
   pl.ws_floats = (size_t)G * 2 * (size_t)p * 128;
   pl.acc_floats = pl.ws_floats;
-  pl.chunk_kb = 128;  // K_c = 2048 per TMEM accumulation (truncating accumulator, see kernel)
+  // K_c = 4096 per TMEM accumulation (truncating accumulator, see kernel): error floor 1.9e-5 on
+  // config 5 vs 9.2e-6 at K_c = 2048, half the fold traffic (profiles/r01_tf32_schedule.txt)
+  pl.chunk_kb = 256;
   if (const char* e = getenv("PF_TF32_CHUNK_KB")) pl.chunk_kb = atoi(e);  // development knob
+  // L2 prefetch of A off by default: measured to evict Y and the fold accumulators (DRAM reads
+  // 28.2 -> 20.5 GB per pass at n = 65536, p = 512, and slower; profiles/r01_tf32_dram.txt)
+  pl.pf_dist = 0;
+  if (const char* e = getenv("PF_TF32_PFDIST")) pl.pf_dist = atoi(e);     // development knob
   pl.counters = (size_t)pl.mtiles * 2;
   return pl;
 }
@@ -494,6 +503,7 @@ cudaError_t tf32_gemm_launch(const Tf32Plan& pl, const CUtensorMap& mapA, const 
   a.split = pl.split;
   a.npass = npass;
   a.chunk_kb = pl.chunk_kb;
+  a.pf_dist = pl.pf_dist;
   a.bdist_kb = bdist_kb;
   a.acc = acc;
   switch (pl.p) {

@@ -40,6 +40,7 @@ struct Tf32Plan {
   size_t ws_floats;     // partial workspace
   size_t acc_floats;    // chunk accumulators
   int chunk_kb;         // k-blocks per TMEM accumulation chunk
+  int pf_dist;          // L2 prefetch distance of A (k-blocks)
   size_t counters;      // tile counters (ints)
 };
 Tf32Plan tf32_plan(int p, int n_rows, int n_k, int num_sms);
