@@ -71,3 +71,38 @@ def test_rows_of_matches_c_split():
             for g in range(world):
                 assert cuts[g][0] == g * n // world          # pf_api.cu: row0 = rank * n / world
                 assert cuts[g][1] - cuts[g][0] in (n // world, n // world + 1)
+
+
+def _worker_tf32(rank, world, port, out):
+    """TF32 row-block layout: each rank holds the p-major slab Y^T[:, r0:r1] (p x n_local); the
+    NCCL all-gather concatenates slabs rank-major ([world][p][n_local]) and the filter GEMM
+    addresses column k of Y^T as slab k // n_local, offset k % n_local (3-D TMA coordinates
+    (k % n_local, c, k // n_local), pf_gemm_tf32.cu)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import torch
+    from paper_1904_10585_b200.solver import rows_of
+    cfg = reduced(CONFIGS[5], n=16 * world * 7, p=64)
+    r0, r1 = rows_of(cfg.n, rank, world)
+    slab = torch.from_numpy(np.ascontiguousarray(initial_block(cfg)[r0:r1].T)).float()
+    gathered = [torch.empty_like(slab) for _ in range(world)]
+    dist.all_gather(gathered, slab)                  # rank-major, as ncclAllGather lays it out
+    out[rank] = (r1 - r0, torch.stack(gathered).numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_tf32_gathered_layout_addressing():
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker_tf32, args=(world, _free_port(), out), nprocs=world, join=True)
+    cfg = reduced(CONFIGS[5], n=16 * world * 7, p=64)
+    Yt = initial_block(cfg).T.astype(np.float32)     # p x n
+    for rank in range(world):
+        nl, g = out[rank]
+        assert nl % 16 == 0 and g.shape == (world, cfg.p, nl)
+        k = np.arange(cfg.n)
+        # the kernel's 3-D coordinates: (k % n_local, c, k // n_local)
+        np.testing.assert_array_equal(g[k // nl, :, k % nl].T, Yt)
