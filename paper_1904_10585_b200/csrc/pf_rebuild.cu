@@ -9,8 +9,11 @@
 //  * 64 x 64 output tiles on fp64 DMMA (K = p); the I panel is V diag(f) (scaled once per
 //    call by scale_cols_kernel), the J panel V;
 //  * single GPU (whole rows): only tiles I <= J are computed; the (J, I) tile is written as the
-//    transpose through shared memory -> n^2 p flops instead of 2 n^2 p, and the old iterate is
-//    read only on the upper half (PFAM; Z is symmetric by contract), none at all for PFPG;
+//    transpose straight from the accumulator fragments -> n^2 p flops instead of 2 n^2 p, and the
+//    old iterate is read only on the upper half (PFAM; Z is symmetric by contract), none at all
+//    for PFPG;
+//  * each persistent CTA owns a contiguous range of tile pairs, so consecutive tiles share the
+//    row block I and its staged V diag(f) panel is reused;
 //  * V panels staged with cp.async, the old-iterate tile prefetched into registers before the
 //    MMA loop so its HBM latency overlaps the math; masks (Omega / adjacency) are packed bits.
 //  * reductions are deterministic: per-CTA partials summed in CTA order by the last CTA.
@@ -21,7 +24,10 @@
 
 namespace pf {
 
-constexpr int kRb = 64;  // tile edge; 4 warps (2 x 2), warp tile 32 x 32
+constexpr int kRb = 64;          // tile edge
+constexpr int kRbThreads = 256;  // 8 warps (2 x 4), warp tile 32 x 16: ~half the accumulator and
+                                 // prefetch registers of a 32 x 32 warp tile -> 16 warps / SM
+constexpr int kWn = 16, kNt = kWn / 8;
 
 struct RbArgs {
   const double* V;   // all n rows (J panels)
@@ -73,7 +79,7 @@ __device__ __forceinline__ void pair_of(int e, int T, int& I, int& J) {
 }
 
 template <int P, bool PFPG>
-__global__ void __launch_bounds__(128, 3) rebuild_kernel(const RbArgs a) {
+__global__ void __launch_bounds__(kRbThreads, 2) rebuild_kernel(const RbArgs a) {
   using C = RbCfg<P, PFPG>;
   extern __shared__ __align__(16) double sm[];
   __shared__ double red[32];
@@ -84,16 +90,21 @@ __global__ void __launch_bounds__(128, 3) rebuild_kernel(const RbArgs a) {
   double* Vj = sm + kRb * C::LD;    // 64 x LD  rows J
   double* Wi = Vj + kRb * C::LD;    // 64 x ldw_s (PFPG)
   double* Wj = Wi + kRb * ldw_s;
-  double* Ts = sm;                  // 64 x 65 transpose staging (reuses the panels)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g8 = lane >> 2, t4 = lane & 3;
-  const int wm = warp & 1, wn = warp >> 1;
+  const int wm = warp & 1, wn = warp >> 1;  // 2 (rows) x 4 (cols) warps, 32 x 16 each
   const int tc = (a.n + kRb - 1) / kRb, tr = (a.n_rows + kRb - 1) / kRb;
   const int ntiles = a.sym ? (tc * (tc + 1)) / 2 : tr * tc;
-  for (int c = tid; c < P; c += 128) fs[c] = a.f[c];
+  for (int c = tid; c < P; c += kRbThreads) fs[c] = a.f[c];
   double s0 = 0.0, s1 = 0.0;
-  // persistent CTAs: fixed strided tile assignment (deterministic sums), one reduction at the end
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  // persistent CTAs: each owns a CONTIGUOUS range of tiles (deterministic sums; in the row-major
+  // upper-triangle order consecutive tiles share the row block I, so the staged I panel is
+  // reused), one reduction at the end
+  const long long nt_all = ntiles;
+  const int t_begin = (int)(nt_all * blockIdx.x / gridDim.x);
+  const int t_end = (int)(nt_all * (blockIdx.x + 1) / gridDim.x);
+  int curI = -1;
+  for (int tile = t_begin; tile < t_end; ++tile) {
   int I, J;
   if (a.sym) {
     pair_of(tile, a.T, I, J);
@@ -104,28 +115,33 @@ __global__ void __launch_bounds__(128, 3) rebuild_kernel(const RbArgs a) {
   const int i0 = I * kRb, j0 = J * kRb;  // local row tile start, global column tile start
   const bool mirror = a.sym && I < J;
   const double wgt = mirror ? 2.0 : 1.0;
-  __syncthreads();  // the previous tile's readers of the panels / staging tile are done
+  const bool newI = (I != curI);
+  curI = I;
+  __syncthreads();  // the previous tile's readers of the panels are done
 
-  // ---- stage V panels (cp.async 16 B), f, W panels
-  for (int e = tid; e < kRb * (P / 2); e += 128) {
+  // ---- stage V panels (cp.async 16 B), f, W panels; the I panel only when I changed
+  for (int e = tid; e < kRb * (P / 2); e += kRbThreads) {
     const int rr = e / (P / 2), c = (e % (P / 2)) * 2;
     double* di = Vi + rr * C::LD + c;
     double* dj = Vj + rr * C::LD + c;
-    if (i0 + rr < a.n_rows) cp_async16(di, a.VF + (size_t)(i0 + rr) * P + c);
-    else *reinterpret_cast<double2*>(di) = make_double2(0.0, 0.0);
+    if (newI) {
+      if (i0 + rr < a.n_rows) cp_async16(di, a.VF + (size_t)(i0 + rr) * P + c);
+      else *reinterpret_cast<double2*>(di) = make_double2(0.0, 0.0);
+    }
     if (j0 + rr < a.n) cp_async16(dj, a.V + (size_t)(j0 + rr) * a.ldv + c);
     else *reinterpret_cast<double2*>(dj) = make_double2(0.0, 0.0);
   }
   if (PFPG) {
-    for (int e = tid; e < kRb * ldw_s; e += 128) {
+    for (int e = tid; e < kRb * ldw_s; e += kRbThreads) {
       const int rr = e / ldw_s, c = e % ldw_s;
-      Wi[e] = (c < a.r && i0 + rr < a.n_rows) ? a.W[(size_t)(a.row0 + i0 + rr) * a.ldw + c] : 0.0;
+      if (newI)
+        Wi[e] = (c < a.r && i0 + rr < a.n_rows) ? a.W[(size_t)(a.row0 + i0 + rr) * a.ldw + c] : 0.0;
       Wj[e] = (c < a.r && j0 + rr < a.n) ? a.W[(size_t)(j0 + rr) * a.ldw + c] : 0.0;
     }
   }
 
   // ---- PFAM: prefetch the old iterate at this thread's fragment positions (overlaps the MMA)
-  double zo[2][2][4][2];
+  double zo[2][2][kNt][2];
   if (!PFPG) {
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
@@ -133,8 +149,8 @@ __global__ void __launch_bounds__(128, 3) rebuild_kernel(const RbArgs a) {
       for (int h = 0; h < 2; ++h) {
         const int li = i0 + wm * 32 + mt * 16 + g8 + 8 * h;
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt) {
-          const int j = j0 + wn * 32 + nt * 8 + 2 * t4;
+        for (int nt = 0; nt < kNt; ++nt) {
+          const int j = j0 + wn * kWn + nt * 8 + 2 * t4;
           zo[mt][h][nt][0] = zo[mt][h][nt][1] = 0.0;
           if (li < a.n_rows && j < a.n) {
             const double* zp = a.Out + (size_t)li * a.ldo + j;
@@ -154,55 +170,54 @@ __global__ void __launch_bounds__(128, 3) rebuild_kernel(const RbArgs a) {
   __syncthreads();
 
   // ---- X tile = (V_I diag(f)) V_J^T on DMMA
-  double acc[2][4][4];
+  double acc[2][kNt][4];
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt)
+    for (int nt = 0; nt < kNt; ++nt)
 #pragma unroll
       for (int k = 0; k < 4; ++k) acc[mt][nt][k] = 0.0;
 #pragma unroll 4
   for (int ks = 0; ks < P / 4; ++ks) {
     const int k = ks * 4 + t4;
-    double a0[2], a1[2], b0[4];
+    double a0[2], a1[2], b0[kNt];
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
       a0[mt] = Vi[(wm * 32 + mt * 16 + g8) * C::LD + k];
       a1[mt] = Vi[(wm * 32 + mt * 16 + g8 + 8) * C::LD + k];
     }
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt) b0[nt] = Vj[(wn * 32 + nt * 8 + g8) * C::LD + k];
+    for (int nt = 0; nt < kNt; ++nt) b0[nt] = Vj[(wn * kWn + nt * 8 + g8) * C::LD + k];
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) dmma16884(acc[mt][nt], a0[mt], a1[mt], b0[nt]);
+      for (int nt = 0; nt < kNt; ++nt) dmma16884(acc[mt][nt], a0[mt], a1[mt], b0[nt]);
   }
-  double accm[PFPG ? 2 : 1][PFPG ? 4 : 1][4];
+  double accm[PFPG ? 2 : 1][PFPG ? kNt : 1][4];
   if (PFPG) {
 #pragma unroll
     for (int mt = 0; mt < (PFPG ? 2 : 1); ++mt)
 #pragma unroll
-      for (int nt = 0; nt < (PFPG ? 4 : 1); ++nt)
+      for (int nt = 0; nt < (PFPG ? kNt : 1); ++nt)
 #pragma unroll
         for (int k = 0; k < 4; ++k) accm[mt][nt][k] = 0.0;
     for (int ks = 0; ks < a.rpad / 4; ++ks) {
       const int k = ks * 4 + t4;
-      double a0[2], a1[2], b0[4];
+      double a0[2], a1[2], b0[kNt];
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) {
         a0[mt] = Wi[(wm * 32 + mt * 16 + g8) * ldw_s + k];
         a1[mt] = Wi[(wm * 32 + mt * 16 + g8 + 8) * ldw_s + k];
       }
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) b0[nt] = Wj[(wn * 32 + nt * 8 + g8) * ldw_s + k];
+      for (int nt = 0; nt < kNt; ++nt) b0[nt] = Wj[(wn * kWn + nt * 8 + g8) * ldw_s + k];
 #pragma unroll
       for (int mt = 0; mt < (PFPG ? 2 : 1); ++mt)
 #pragma unroll
-        for (int nt = 0; nt < (PFPG ? 4 : 1); ++nt)
+        for (int nt = 0; nt < (PFPG ? kNt : 1); ++nt)
           dmma16884(accm[mt][nt], a0[mt], a1[mt], b0[nt]);
     }
   }
-  if (mirror) __syncthreads();  // panels are about to be overwritten by the staging tile
 
   // ---- elementwise update + reductions
 #pragma unroll
@@ -213,10 +228,10 @@ __global__ void __launch_bounds__(128, 3) rebuild_kernel(const RbArgs a) {
       const int li = i0 + rt;
       if (li >= a.n_rows) continue;
       const int gi = a.row0 + li;
-      const uint32_t word = __ldg(a.bits + (size_t)li * a.ldb + ((j0 + wn * 32) >> 5));
+      const uint32_t word = __ldg(a.bits + (size_t)li * a.ldb + ((j0 + wn * kWn) >> 5));
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) {
-        const int ct = wn * 32 + nt * 8 + 2 * t4;  // column within tile
+      for (int nt = 0; nt < kNt; ++nt) {
+        const int ct = wn * kWn + nt * 8 + 2 * t4;  // column within tile
         const int j = j0 + ct;
         if (j >= a.n) continue;
         const bool two = (j + 1 < a.n);
@@ -256,29 +271,13 @@ __global__ void __launch_bounds__(128, 3) rebuild_kernel(const RbArgs a) {
           if (two) op[1] = o[1];
         }
         if (mirror) {
-          Ts[rt * C::LDS + ct] = o[0];
-          Ts[rt * C::LDS + ct + 1] = o[1];
+          // (J, I) tile = transpose, stored straight from the fragment: for a fixed (nt, c)
+          // the warp writes 4 rows x 8 consecutive doubles (full 32-byte sectors), no smem pass
+          __stcs(a.Out + (size_t)j * a.ldo + li, o[0]);
+          if (two) __stcs(a.Out + (size_t)(j + 1) * a.ldo + li, o[1]);
         }
       }
     }
-  if (mirror) {
-    __syncthreads();
-    // (J, I) tile = transpose: row b of the mirrored tile = column b of Ts
-    for (int e = tid; e < kRb * (kRb / 2); e += 128) {
-      const int b = e / (kRb / 2), a2 = (e % (kRb / 2)) * 2;
-      const int row = j0 + b, col = i0 + a2;
-      if (row < a.n && col < a.n) {
-        double* op = a.Out + (size_t)row * a.ldo + col;
-        const double v0 = Ts[a2 * C::LDS + b], v1 = Ts[(a2 + 1) * C::LDS + b];
-        if (col + 1 < a.n && ((reinterpret_cast<uintptr_t>(op) & 15) == 0)) {
-          __stcs(reinterpret_cast<double2*>(op), make_double2(v0, v1));
-        } else {
-          op[0] = v0;
-          if (col + 1 < a.n) op[1] = v1;
-        }
-      }
-    }
-  }
 
   }  // tile loop
 
@@ -298,7 +297,7 @@ __global__ void __launch_bounds__(128, 3) rebuild_kernel(const RbArgs a) {
   if (s_last) {
     __threadfence();
     double t0 = 0.0, t1 = 0.0;
-    for (int b = tid; b < nb; b += 128) {
+    for (int b = tid; b < nb; b += kRbThreads) {
       t0 += __ldcg(a.partials + 2 * (size_t)b);
       t1 += __ldcg(a.partials + 2 * (size_t)b + 1);
     }
@@ -344,13 +343,14 @@ static cudaError_t rb_launch(RbArgs a, cudaStream_t st) {
   a.T = tc;
   const long long ntiles = a.sym ? (long long)tc * (tc + 1) / 2 : (long long)tr * tc;
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rebuild_kernel<P, PFPG>, 128, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rebuild_kernel<P, PFPG>, kRbThreads,
+                                                smem);
   int sms = 148, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   dim3 grid((unsigned)std::max<long long>(1, std::min<long long>(ntiles, (long long)std::max(per_sm, 1) * sms)));
   count_launch();
-  rebuild_kernel<P, PFPG><<<grid, 128, smem, st>>>(a);
+  rebuild_kernel<P, PFPG><<<grid, kRbThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
 
