@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -758,10 +759,16 @@ pf_status pf_rayleigh_ritz(pf_ctx ctx, const void* Av, int64_t lda, const void* 
   PF_CU(cudaMemcpy2DAsync(ctx->Y[0], row, U, ldu * 8, row, nl, cudaMemcpyDeviceToDevice, st));
   PF_TRY(gemm_step(ctx, 0, ctx->Y[0], ctx->Y[0], ctx->Wbuf, &ctx->state->coef_rr[0], st));
   PF_TRY(gram_all(ctx, ctx->Y[0], ctx->Wbuf, ctx->G, nullptr, st));  // H = Q^T (A Q)
-  // stop once off(H) <= p * 1e-16 ||H||_F: the rotation threshold leaves every off-diagonal entry
-  // below 1e-16 ||H||_F, so this is reached without a final rotation-free confirmation sweep
+  // stop once off(H) <= tol ||H||_F.  X = V f(Lambda) V^T is a 1-Lipschitz spectral function of
+  // H, so the residual off-diagonal moves X by O(tol ||H||); PF_JACOBI_TOL (development knob)
+  // defaults to p * 1e-16 (the rounding floor of H)
+  static double jtol = -1.0;
+  if (jtol < 0.0) {
+    const char* e = getenv("PF_JACOBI_TOL");
+    jtol = e ? atof(e) : 0.0;
+  }
   PF_CU(jacobi_launch(ctx->G, p, nullptr, theta, ctx->Yeig, ctx->state,
-                      std::max(1e-15, 1e-16 * p), 40, st));
+                      jtol > 0.0 ? jtol : std::max(1e-15, 1e-16 * p), 40, st));
   PF_CU(copy_theta_launch(theta, p, ctx->state, st));
   PF_CU(rmul_launch(ctx->Y[0], p, ctx->Yeig, V, ldv, nl, p, nullptr, st));
   return PF_OK;
