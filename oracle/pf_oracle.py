@@ -40,7 +40,8 @@ __all__ = [
     "cheb_T", "growth_lower_bound", "interval_map", "interval_psd", "interval_top_r",
     "interval_soft", "lanczos_extremes", "rebase_plan", "spread_estimate", "chebyshev_filter",
     "orth", "filter_update", "rayleigh_ritz", "spectral_psd", "spectral_soft", "jacobi_eig",
-    "exact_spectral", "maxcut_C", "prox_tG_diag", "pfam_next", "pfpg_next", "nce_next", "run",
+    "exact_spectral", "maxcut_C", "prox_tG_diag", "pfam_next", "pfpg_next", "nce_next",
+    "rna_extrapolate", "run",
     "lowrank_diff_fro", "lowrank_fro", "sin_theta",
 ]
 
@@ -290,6 +291,21 @@ def nce_next(V, f, x, G, tau):
     return xn, B, F, float(np.linalg.norm(g))
 
 
+def rna_extrapolate(X: np.ndarray, lam_rel: float) -> tuple[np.ndarray, np.ndarray]:
+    """Regularized extrapolation (§4.3, Scieur et al.): X = [x^{k-l}, ..., x^{k+1}]
+    (n x (l+2), oldest first); U = [x^{k-l+1} - x^{k-l}, ..., x^{k+1} - x^k];
+    c = argmin_{1^T c = 1} c^T (U^T U + lambda I) c = (U^T U + lambda I)^{-1} 1 / (1^T (.)^{-1} 1),
+    lambda = lam_rel ||U^T U||_F (reading R21); returns (x~ = sum_i c_i x^{k-l+i}, c)."""
+    U = X[:, 1:] - X[:, :-1]
+    M = U.T @ U
+    lam = lam_rel * np.linalg.norm(M)
+    if lam == 0.0:
+        lam = lam_rel
+    z = np.linalg.solve(M + lam * np.eye(M.shape[0]), np.ones(M.shape[0]))
+    c = z / z.sum()
+    return X[:, :-1] @ c, c
+
+
 # ============================================================================ metrics
 def lowrank_fro(V, f) -> float:
     """||V diag(f) V^T||_F = ||R diag(f) R^T||_F with V = Q R (thin QR; no n x n buffer)."""
@@ -366,6 +382,7 @@ def run(cfg: Config, iters: int | None = None, record_factors: bool = True,
         Gn = prob["G"]
         xn = 1.0 - np.diag(Gn)                                    # x^0 = 1 - diag(G)
         A = Gn + np.diag(xn)
+        hist = [xn.copy()]                                        # extrapolation window (R21)
     else:
         raise ValueError(cfg.mode)
     psd = cfg.mode in ("sweep_psd", "pfam", "nce")
@@ -409,6 +426,13 @@ def run(cfg: Config, iters: int | None = None, record_factors: bool = True,
             xn, A, F, gn = nce_next(V[:, keep], f[keep], xn, Gn, cfg.tau)
             rec["objective"] = F
             rec["grad_norm"] = gn
+            if cfg.accel_l > 0:
+                # every l+2 iterates: x <- sum c_i x^{k-l+i} (§4.3), window restarts at x~ (R21)
+                hist.append(xn.copy())
+                if len(hist) == cfg.accel_l + 2:
+                    xn, rec["accel_c"] = rna_extrapolate(np.stack(hist, axis=1), cfg.accel_lam)
+                    A = Gn + np.diag(xn)
+                    hist = [xn.copy()]
             rec["x"] = xn
         else:
             A, cw, res = pfam_next(V[:, keep], f[keep], A, C, cfg.t)

@@ -67,6 +67,10 @@ class Config:
     tf32_tail: int = 0
     # nearest correlation estimation (mode "nce"): paper Example eg:5.6 (6) or eg:5.7 (7)
     nce_example: int = 7
+    # regularized extrapolation of the iterates (§4.3; NEXT-4): window l (0 = off)
+    # and lambda = accel_lam * ||U^T U||_2 (SPEC defaults l = 5, 1e-8; reading R21)
+    accel_l: int = 0
+    accel_lam: float = 1e-8
     nbig: int = 256           # config 5: eigenvalues drawn from U[5, 50]
     nrefl: int = 64           # config 5: Householder reflectors in the basis
 
@@ -89,6 +93,11 @@ CONFIGS = {
 NEXT_CONFIGS = {
     "nce7": Config("nce_ex57_n4000", n=4000, p=64, d=8, iters=300, mode="nce", nce_example=7),
     "nce6": Config("nce_ex56_n2000", n=2000, p=128, d=8, iters=200, mode="nce", nce_example=6),
+    # with the paper's acceleration (§4.3): the configuration tab:ncm's PFPG column is run with
+    "nce7a": Config("nce_ex57_n4000_accel", n=4000, p=64, d=8, iters=300, mode="nce",
+                    nce_example=7, accel_l=5),
+    "nce6a": Config("nce_ex56_n2000_accel", n=2000, p=128, d=8, iters=200, mode="nce",
+                    nce_example=6, accel_l=5),
 }
 
 

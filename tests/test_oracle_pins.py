@@ -467,3 +467,64 @@ def test_nce_objective_matches_table_ncm(ex, paper_f, iters, p):
     F = O.run(cfg, record_factors=False)["records"][-1]["objective"]
     half_ulp = 0.5 * 10 ** (np.floor(np.log10(paper_f)) - 1)
     assert abs(F - paper_f) <= half_ulp + 0.01 * paper_f, F
+
+
+# ------------------------------------------------------------------ regularized extrapolation
+def test_rna_trivial_cases():
+    """SPEC S:322-324: equal history -> the point itself; lambda -> infinity -> uniform weights;
+    coefficients always sum to 1."""
+    rng = np.random.default_rng(4)
+    xbar = rng.standard_normal(30)
+    xt, c = O.rna_extrapolate(np.tile(xbar[:, None], (1, 7)), 1e-8)
+    np.testing.assert_allclose(xt, xbar, atol=1e-15)
+    X = rng.standard_normal((30, 7))
+    xt, c = O.rna_extrapolate(X, 1e12)
+    np.testing.assert_allclose(c, np.full(6, 1 / 6), atol=1e-9)
+    assert abs(c.sum() - 1.0) < 1e-12
+
+
+def test_rna_l1_closed_form():
+    """l = 1: with U = [u1 u2], c minimises c^T (U^T U + lam I) c on c1 + c2 = 1:
+    c1 = (m22 + lam - m12) / (m11 + m22 + 2 lam - 2 m12) (hand-solved 2 x 2 KKT system)."""
+    X = np.array([[0.0, 1.0, 1.5], [0.0, 2.0, 2.5]])
+    U = X[:, 1:] - X[:, :-1]
+    m11, m12, m22 = U[:, 0] @ U[:, 0], U[:, 0] @ U[:, 1], U[:, 1] @ U[:, 1]
+    lam = 0.3 * np.sqrt(m11 ** 2 + 2 * m12 ** 2 + m22 ** 2)
+    c1 = (m22 + lam - m12) / (m11 + m22 + 2 * lam - 2 * m12)
+    xt, c = O.rna_extrapolate(X, 0.3)
+    np.testing.assert_allclose(c, [c1, 1 - c1], atol=1e-14)
+    np.testing.assert_allclose(xt, c1 * X[:, 0] + (1 - c1) * X[:, 1], atol=1e-14)
+
+
+def test_rna_recovers_fixed_point_of_linear_iteration():
+    """x+ = x - tau (A x - b) with A having 3 distinct eigenvalues: the differences span a
+    3-dimensional Krylov space, so with l + 1 = 4 > 3 the affine combination with U c = 0 is the
+    fixed point A^{-1} b (minimal-polynomial argument), up to the small regularisation."""
+    rng = np.random.default_rng(5)
+    Q = np.linalg.qr(rng.standard_normal((40, 40)))[0]
+    lam = np.repeat([1.0, 2.0, 4.0], [10, 15, 15])
+    A = (Q * lam) @ Q.T
+    b = rng.standard_normal(40)
+    xs = [np.zeros(40)]
+    for _ in range(4):
+        xs.append(xs[-1] - 0.2 * (A @ xs[-1] - b))
+    xt, _ = O.rna_extrapolate(np.stack(xs, axis=1), 1e-14)
+    xstar = np.linalg.solve(A, b)
+    assert np.linalg.norm(xt - xstar) <= 1e-6 * np.linalg.norm(xstar)
+    assert np.linalg.norm(xs[-1] - xstar) > 1e-2 * np.linalg.norm(xstar)   # plain iterate is far
+
+
+def test_nce_accelerated_reaches_tolerance_faster():
+    """§4.3: the extrapolated PFPG reaches ||grad F|| <= 1e-7 ||grad F(x0)|| in fewer iterations
+    than the plain method on eg:5.6, n = 500 (measured 30 vs 111), at the same objective."""
+    from pfinputs import NEXT_CONFIGS
+    out = {}
+    for key in ("nce6", "nce6a"):
+        cfg = reduced(NEXT_CONFIGS[key], n=500, p=128, d=8, iters=150)
+        recs = O.run(cfg, record_factors=False)["records"]
+        g0 = recs[0]["grad_norm"]
+        k = next((r["k"] for r in recs if r["grad_norm"] <= 1e-7 * g0), None)
+        out[key] = (k, recs[k if k is not None else -1]["objective"])
+    assert out["nce6a"][0] is not None and out["nce6a"][0] <= 45
+    assert out["nce6"][0] is None or out["nce6"][0] > 2 * out["nce6a"][0]
+    assert out["nce6a"][1] == pytest.approx(8.9e3, rel=0.01)
