@@ -162,13 +162,24 @@ pf_status pf_admm_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f
  * eqn:NCE-gradient), PF_FP64 contexts: with Pi_+(B) ~ V diag(f) V^T for the iterate
  * B = G + Diag(x) (f = max(theta, 0) from pf_spectral_op PF_OP_PSD):
  *   grad_i = diag(V diag(f) V^T)_i - 1,  x <- x - tau grad,  B_ii <- G_ii + x_i.
- * V: local rows (n_local x p, ldv); gdiag: device double[n] (full diag(G)); x: device
- * double[n_local] (this rank's slice), in/out; B: local rows (n_local x n, ldb) -- only its
+ * V: local rows (n_local x p, ldv); gdiag: device double[n] (full diag(G)); x_in / x_out:
+ * device double[n_local] (this rank's slice; may alias); B: local rows (n_local x n, ldb) -- only its
  * diagonal entries (i, row0 + i) are written.  obj: device double[2] = {F(x_old),
  * ||grad F(x_old)||}, F(x) = 1/2 sum f_i^2 - 1^T x.  tau > 0 (the paper uses tau = 1). */
 pf_status pf_nce_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f, double tau,
-                      const double* gdiag, double* x, double* B, int64_t ldb, double* obj,
-                      pf_stream stream);
+                      const double* gdiag, const double* x_in, double* x_out, double* B,
+                      int64_t ldb, double* obj, pf_stream stream);
+
+/* Regularized extrapolation of the iterates (paper §4.3),
+ * PF_FP64 contexts, for the NCE dual variable: hist[0..l+1] are l+2 device vectors (this rank's
+ * n_local entries, OLDEST FIRST; host array of device pointers), U = [h_1 - h_0, ..., h_{l+1} - h_l],
+ * c = (U^T U + lam I)^{-1} 1 / (1^T (U^T U + lam I)^{-1} 1), lam = lam_rel ||U^T U||_F (U^T U summed
+ * over all ranks), x_out = sum_{i<=l} c_i h_i (may alias any h_i), B_ii <- G_ii + x_out_i.
+ * coef: device double[l+1] or NULL.  0 <= l <= 7, lam_rel > 0 (the SPEC default is l = 5,
+ * lam_rel = 1e-8; reading R21). */
+pf_status pf_extrapolate(pf_ctx ctx, const double* const* hist, int32_t l, double lam_rel,
+                         const double* gdiag, double* x_out, double* B, int64_t ldb, double* coef,
+                         pf_stream stream);
 
 /* ---------------------------------------------------------------------------- measurement */
 /* Enable (1) / disable (0) per-launch CUDA-event timing of the Chebyshev-step GEMM (the

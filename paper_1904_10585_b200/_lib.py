@@ -52,7 +52,8 @@ def load() -> ctypes.CDLL:
         "pf_admm_step": [P, P, I64, P, D, P, I64, P, P, I64, P, P],
         "pf_perturb": [P, P, I64, P, I64, P],
         "pf_perturb_hash": [P, P, I64, ctypes.c_uint64, I32, D, P],
-        "pf_nce_step": [P, P, I64, P, D, P, P, P, I64, P, P],
+        "pf_nce_step": [P, P, I64, P, D, P, P, P, P, I64, P, P],
+        "pf_extrapolate": [P, P, I32, D, P, P, P, I64, P, P],
         "pf_set_tf32_passes": [P, I32],
         "pf_set_tf32_schedule": [P, I32, I32],
         "pf_profile": [P, I32],
@@ -220,10 +221,17 @@ class Context:
         self._check(self.lib.pf_perturb(self.h, _ptr(A), _ld(A), _ptr(E), _ld(E),
                                         _stream(stream)), "pf_perturb")
 
-    def nce_step(self, V, f, tau, gdiag, x, B, obj, stream=None):
+    def nce_step(self, V, f, tau, gdiag, x_in, x_out, B, obj, stream=None):
         self._check(self.lib.pf_nce_step(self.h, _ptr(V), _ld(V), _ptr(f), tau, _ptr(gdiag),
-                                         _ptr(x), _ptr(B), _ld(B), _ptr(obj), _stream(stream)),
-                    "pf_nce_step")
+                                         _ptr(x_in), _ptr(x_out), _ptr(B), _ld(B), _ptr(obj),
+                                         _stream(stream)), "pf_nce_step")
+
+    def extrapolate(self, hist, lam_rel, gdiag, x_out, B, coef=None, stream=None):
+        """hist: list of l+2 device vectors, oldest first."""
+        arr = (ctypes.c_void_p * len(hist))(*[_ptr(h) for h in hist])
+        self._check(self.lib.pf_extrapolate(self.h, arr, len(hist) - 2, lam_rel, _ptr(gdiag),
+                                            _ptr(x_out), _ptr(B), _ld(B), _ptr(coef),
+                                            _stream(stream)), "pf_extrapolate")
 
     def perturb_hash(self, A, seed: int, k: int, noise: float, stream=None):
         self._check(self.lib.pf_perturb_hash(self.h, _ptr(A), _ld(A), seed, k, noise,

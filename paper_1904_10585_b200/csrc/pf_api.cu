@@ -200,7 +200,9 @@ static pf_status alloc_all(pf_ctx ctx) {
   ok &= A((void**)&ctx->lz_T, (size_t)kMaxLanczos * kMaxLanczos * 8);
   ok &= A((void**)&ctx->lz_theta, (size_t)kMaxLanczos * 8);
   ok &= A((void**)&ctx->lz_S, (size_t)kMaxLanczos * kMaxLanczos * 8);
-  ok &= A((void**)&ctx->rb_part, (size_t)rebuild_blocks((int)nl, (int)n) * 2 * 8);
+  // shared by the rebuild (2 per tile CTA), NCE (2 x 256) and extrapolation (128 x 36) reductions
+  ok &= A((void**)&ctx->rb_part,
+          std::max<size_t>((size_t)rebuild_blocks((int)nl, (int)n) * 2, 128 * 36) * 8);
   ok &= A((void**)&ctx->rb_cnt, 16);
   ok &= A((void**)&ctx->shift_flag, 16);
   if (!ok) {
@@ -841,17 +843,36 @@ pf_status pf_admm_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f
 }
 
 pf_status pf_nce_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f, double tau,
-                      const double* gdiag, double* x, double* B, int64_t ldb, double* obj,
-                      pf_stream stream) {
-  if (!ctx || !V || !f || !gdiag || !x || !B || !obj) return PF_ERR_ARG;
+                      const double* gdiag, const double* x_in, double* x_out, double* B,
+                      int64_t ldb, double* obj, pf_stream stream) {
+  if (!ctx || !V || !f || !gdiag || !x_in || !x_out || !B || !obj) return PF_ERR_ARG;
   if (ctx->dtype != PF_FP64) return PF_ERR_UNSUPPORTED;
   if (ldv < ctx->p || ldb < ctx->n) return PF_ERR_DIM;
   if (!(tau > 0.0)) return PF_ERR_ARG;
   cudaStream_t st = (cudaStream_t)stream;
-  PF_CU(nce_launch(V, ldv, f, ctx->p, tau, gdiag, x, B, ldb, (int)ctx->n_local, (int)ctx->row0,
-                   ctx->rb_part, ctx->rb_cnt, obj, st));
+  PF_CU(nce_launch(V, ldv, f, ctx->p, tau, gdiag, x_in, x_out, B, ldb, (int)ctx->n_local,
+                   (int)ctx->row0, ctx->rb_part, ctx->rb_cnt, obj, st));
   PF_TRY(allreduce(ctx, obj, 2, st));  // raw sums over the row blocks
   PF_CU(nce_finish_launch(f, ctx->p, obj, st));
+  return PF_OK;
+}
+
+pf_status pf_extrapolate(pf_ctx ctx, const double* const* hist, int32_t l, double lam_rel,
+                         const double* gdiag, double* x_out, double* B, int64_t ldb, double* coef,
+                         pf_stream stream) {
+  if (!ctx || !hist || !gdiag || !x_out || !B) return PF_ERR_ARG;
+  if (ctx->dtype != PF_FP64) return PF_ERR_UNSUPPORTED;
+  if (l < 0 || l + 1 > 8 || !(lam_rel > 0.0)) return PF_ERR_ARG;
+  if (ldb < ctx->n) return PF_ERR_DIM;
+  for (int i = 0; i <= l + 1; ++i)
+    if (!hist[i]) return PF_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int L = l + 1;
+  // partials: rna_blocks * L(L+1)/2 <= 128 * 36 doubles fit the rebuild partials buffer
+  PF_CU(rna_gram_launch(hist, L, (int)ctx->n_local, ctx->rb_part, ctx->rb_cnt, ctx->G, st));
+  PF_TRY(allreduce(ctx, ctx->G, (size_t)L * L, st));
+  PF_CU(rna_combine_launch(hist, L, (int)ctx->n_local, ctx->G, lam_rel, gdiag, x_out, B, ldb,
+                           (int)ctx->row0, coef, st));
   return PF_OK;
 }
 

@@ -144,8 +144,16 @@ cudaError_t admm_launch(const double* V, int64_t ldv, const double* Vloc, int64_
 cudaError_t sqrt_inplace_launch(double* x, cudaStream_t st);
 // NCE dual gradient update (NEXT-1): partials >= 2 * 256 doubles; obj gets raw sums
 cudaError_t nce_launch(const double* V, int64_t ldv, const double* f, int p, double tau,
-                       const double* gdiag, double* x, double* B, int64_t ldb, int n_rows,
-                       int row0, double* partials, int* counter, double* obj, cudaStream_t st);
+                       const double* gdiag, const double* x_in, double* x_out, double* B,
+                       int64_t ldb, int n_rows, int row0, double* partials, int* counter,
+                       double* obj, cudaStream_t st);
+// regularized extrapolation (NEXT-4): L = l + 1 <= 8 differences; partials >= 128 * 36 doubles
+int rna_blocks(int n_rows);
+cudaError_t rna_gram_launch(const double* const* hist, int L, int n_rows, double* partials,
+                            int* counter, double* M, cudaStream_t st);
+cudaError_t rna_combine_launch(const double* const* hist, int L, int n_rows, const double* M,
+                               double lam_rel, const double* gdiag, double* x_out, double* B,
+                               int64_t ldb, int row0, double* coef, cudaStream_t st);
 cudaError_t nce_finish_launch(const double* f, int p, double* obj, cudaStream_t st);
 
 }  // namespace pf

@@ -434,8 +434,8 @@ constexpr int kNceThreads = 256;
 
 __global__ void __launch_bounds__(kNceThreads) nce_kernel(
     const double* __restrict__ V, int64_t ldv, const double* __restrict__ f, int p, double tau,
-    const double* __restrict__ gdiag, double* __restrict__ x, double* __restrict__ B, int64_t ldb,
-    int n_rows, int row0, double* partials, int* counter, double* obj) {
+    const double* __restrict__ gdiag, const double* x_in, double* x_out, double* __restrict__ B,
+    int64_t ldb, int n_rows, int row0, double* partials, int* counter, double* obj) {
   __shared__ double red[32];
   __shared__ int s_last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -449,8 +449,8 @@ __global__ void __launch_bounds__(kNceThreads) nce_kernel(
     }
     d = warp_sum(d);
     if (lane == 0) {
-      const double g = d - 1.0, xo = x[i], xn = xo - tau * g;
-      x[i] = xn;
+      const double g = d - 1.0, xo = x_in[i], xn = xo - tau * g;
+      x_out[i] = xn;
       B[(size_t)i * ldb + row0 + i] = gdiag[row0 + i] + xn;
       sx += xo;
       sg += g * g;
@@ -491,18 +491,162 @@ __global__ void nce_finish_kernel(const double* f, int p, double* obj) {
 }
 
 cudaError_t nce_launch(const double* V, int64_t ldv, const double* f, int p, double tau,
-                       const double* gdiag, double* x, double* B, int64_t ldb, int n_rows,
-                       int row0, double* partials, int* counter, double* obj, cudaStream_t st) {
+                       const double* gdiag, const double* x_in, double* x_out, double* B,
+                       int64_t ldb, int n_rows, int row0, double* partials, int* counter,
+                       double* obj, cudaStream_t st) {
   const int blocks = std::max(1, std::min(256, (n_rows + 7) / 8));
   count_launch();
-  nce_kernel<<<blocks, kNceThreads, 0, st>>>(V, ldv, f, p, tau, gdiag, x, B, ldb, n_rows, row0,
-                                             partials, counter, obj);
+  nce_kernel<<<blocks, kNceThreads, 0, st>>>(V, ldv, f, p, tau, gdiag, x_in, x_out, B, ldb, n_rows,
+                                             row0, partials, counter, obj);
   return cudaGetLastError();
 }
 
 cudaError_t nce_finish_launch(const double* f, int p, double* obj, cudaStream_t st) {
   count_launch();
   nce_finish_kernel<<<1, 32, 0, st>>>(f, p, obj);
+  return cudaGetLastError();
+}
+
+}  // namespace pf
+
+namespace pf {
+
+// ============================================================================== extrapolation
+// Regularized extrapolation of the iterates (paper §4.3; NEXT-4): history
+// h_0..h_L (L = l + 1 <= kRnaMax, oldest first), U = [h_1 - h_0, ..., h_L - h_{L-1}],
+// M = U^T U (all-reduced over row blocks), c = (M + lam I)^{-1} 1 / (1^T (M + lam I)^{-1} 1) with
+// lam = lam_rel ||M||_F (reading R21), x~ = sum_{i<L} c_i h_i.
+constexpr int kRnaMax = 8;
+struct RnaHist {
+  const double* h[kRnaMax + 1];
+};
+
+__global__ void __launch_bounds__(256) rna_gram_kernel(RnaHist hs, int L, int n_rows,
+                                                       double* partials, int* counter,
+                                                       double* M) {
+  __shared__ double red[32];
+  __shared__ int s_last;
+  double acc[kRnaMax * (kRnaMax + 1) / 2];
+#pragma unroll
+  for (int e = 0; e < kRnaMax * (kRnaMax + 1) / 2; ++e) acc[e] = 0.0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n_rows; r += gridDim.x * blockDim.x) {
+    double u[kRnaMax];
+#pragma unroll
+    for (int i = 0; i < kRnaMax; ++i) u[i] = (i < L) ? hs.h[i + 1][r] - hs.h[i][r] : 0.0;
+    int e = 0;
+#pragma unroll
+    for (int i = 0; i < kRnaMax; ++i)
+#pragma unroll
+      for (int j = i; j < kRnaMax; ++j) acc[e++] += u[i] * u[j];
+  }
+  const int ne = L * (L + 1) / 2;
+  int e = 0;
+  for (int i = 0; i < L; ++i)
+    for (int j = i; j < L; ++j) {
+      // packed index over kRnaMax for the accumulator, over L for the partials
+      const int ek = i * kRnaMax - i * (i - 1) / 2 + (j - i);
+      const double v = block_sum(acc[ek], red);
+      if (threadIdx.x == 0) partials[(size_t)blockIdx.x * ne + e] = v;
+      ++e;
+    }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(counter, 1) == (int)gridDim.x - 1);
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    if (threadIdx.x < ne) {
+      double t = 0.0;
+      for (int b = 0; b < (int)gridDim.x; ++b) t += __ldcg(partials + (size_t)b * ne + threadIdx.x);
+      int i = 0, rem = threadIdx.x;
+      while (rem >= L - i) {
+        rem -= L - i;
+        ++i;
+      }
+      const int j = i + rem;
+      M[i * L + j] = t;
+      M[j * L + i] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *counter = 0;
+  }
+}
+
+// every block solves the L x L system redundantly (L <= 8), then combines its rows
+__global__ void __launch_bounds__(256) rna_combine_kernel(RnaHist hs, int L, int n_rows,
+                                                          const double* M, double lam_rel,
+                                                          const double* gdiag, double* x_out,
+                                                          double* B, int64_t ldb, int row0,
+                                                          double* coef) {
+  __shared__ double c[kRnaMax];
+  if (threadIdx.x == 0) {
+    double a[kRnaMax][kRnaMax], z[kRnaMax];
+    double fro = 0.0;
+    for (int i = 0; i < L; ++i)
+      for (int j = 0; j < L; ++j) fro += M[i * L + j] * M[i * L + j];
+    double lam = lam_rel * sqrt(fro);
+    if (lam == 0.0) lam = lam_rel;
+    for (int i = 0; i < L; ++i) {
+      for (int j = 0; j < L; ++j) a[i][j] = M[i * L + j] + (i == j ? lam : 0.0);
+      z[i] = 1.0;
+    }
+    // Cholesky of the SPD regularised matrix, then two triangular solves
+    for (int j = 0; j < L; ++j) {
+      double d = a[j][j];
+      for (int k = 0; k < j; ++k) d -= a[j][k] * a[j][k];
+      d = sqrt(d);
+      a[j][j] = d;
+      for (int i = j + 1; i < L; ++i) {
+        double v = a[i][j];
+        for (int k = 0; k < j; ++k) v -= a[i][k] * a[j][k];
+        a[i][j] = v / d;
+      }
+    }
+    for (int i = 0; i < L; ++i) {
+      double v = z[i];
+      for (int k = 0; k < i; ++k) v -= a[i][k] * z[k];
+      z[i] = v / a[i][i];
+    }
+    for (int i = L - 1; i >= 0; --i) {
+      double v = z[i];
+      for (int k = i + 1; k < L; ++k) v -= a[k][i] * z[k];
+      z[i] = v / a[i][i];
+    }
+    double sz = 0.0;
+    for (int i = 0; i < L; ++i) sz += z[i];
+    for (int i = 0; i < L; ++i) c[i] = z[i] / sz;
+    if (blockIdx.x == 0 && coef)
+      for (int i = 0; i < L; ++i) coef[i] = c[i];
+  }
+  __syncthreads();
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n_rows; r += gridDim.x * blockDim.x) {
+    double x = 0.0;
+    for (int i = 0; i < L; ++i) x += c[i] * hs.h[i][r];
+    x_out[r] = x;
+    B[(size_t)r * ldb + row0 + r] = gdiag[row0 + r] + x;
+  }
+}
+
+int rna_blocks(int n_rows) { return std::max(1, std::min(128, (n_rows + 255) / 256)); }
+
+cudaError_t rna_gram_launch(const double* const* hist, int L, int n_rows, double* partials,
+                            int* counter, double* M, cudaStream_t st) {
+  if (L < 1 || L > kRnaMax) return cudaErrorInvalidValue;
+  RnaHist hs{};
+  for (int i = 0; i <= L; ++i) hs.h[i] = hist[i];
+  count_launch();
+  rna_gram_kernel<<<rna_blocks(n_rows), 256, 0, st>>>(hs, L, n_rows, partials, counter, M);
+  return cudaGetLastError();
+}
+
+cudaError_t rna_combine_launch(const double* const* hist, int L, int n_rows, const double* M,
+                               double lam_rel, const double* gdiag, double* x_out, double* B,
+                               int64_t ldb, int row0, double* coef, cudaStream_t st) {
+  RnaHist hs{};
+  for (int i = 0; i <= L; ++i) hs.h[i] = hist[i];
+  count_launch();
+  rna_combine_kernel<<<rna_blocks(n_rows), 256, 0, st>>>(hs, L, n_rows, M, lam_rel, gdiag, x_out,
+                                                         B, ldb, row0, coef);
   return cudaGetLastError();
 }
 

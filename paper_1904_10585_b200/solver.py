@@ -112,6 +112,11 @@ class Solver:
             G = prob["G"]
             self.gdiag = _dev(np.ascontiguousarray(np.diag(G)))
             self.x = _dev((1.0 - np.diag(G))[r0:r1])
+            # extrapolation window (paper §4.3, reading R21): a ring of l + 2 x-buffers IS the
+            # history; pf_nce_step writes the next iterate into the next buffer
+            self.xbuf = [self.x] + [torch.empty_like(self.x) for _ in range(cfg.accel_l + 1)] \
+                if cfg.accel_l > 0 else [self.x]
+            self.win = 1                                             # points in the window
             B0 = G[r0:r1].copy()
             B0[np.arange(nl), r0 + np.arange(nl)] = 1.0           # G_ii + x^0_i = 1
             # even row pitch (16-byte TMA rows, include/pf.h) for any n
@@ -146,7 +151,19 @@ class Solver:
         elif cfg.mode == "pfam":
             ctx.admm_step(self.V, self.f, cfg.t, self.adj, self.deg, self.A, self.obj, st)
         elif cfg.mode == "nce":
-            ctx.nce_step(self.V, self.f, cfg.tau, self.gdiag, self.x, self.A, self.obj, st)
+            if cfg.accel_l > 0:
+                nxt = self.xbuf[self.win]
+                ctx.nce_step(self.V, self.f, cfg.tau, self.gdiag, self.x, nxt, self.A, self.obj, st)
+                self.x = nxt
+                self.win += 1
+                if self.win == cfg.accel_l + 2:                    # every l + 2 iterates
+                    ctx.extrapolate(self.xbuf, cfg.accel_lam, self.gdiag, self.xbuf[0], self.A,
+                                    stream=st)
+                    self.x = self.xbuf[0]
+                    self.win = 1                                     # window restarts at x~
+            else:
+                ctx.nce_step(self.V, self.f, cfg.tau, self.gdiag, self.x, self.x, self.A, self.obj,
+                             st)
         # Warm start the next filter from the Ritz vectors: Range(V) = Range(U), so the method
         # is unchanged (eqn:subspace-update depends on Range(U) only), but the next H = Q^T A Q
         # is then nearly diagonal and the Jacobi solve converges in one or two sweeps.

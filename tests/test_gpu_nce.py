@@ -43,3 +43,36 @@ def test_nce_single_rank_nccl_path():
     for x, y in zip(a, b):
         assert y["objective"] == pytest.approx(x["objective"], rel=1e-13)
         np.testing.assert_allclose(y["x"], x["x"], rtol=1e-13, atol=1e-13)
+
+
+def test_extrapolation_unit_matches_oracle():
+    """pf_extrapolate vs oracle.rna_extrapolate on random histories (l = 1, 5, 7)."""
+    from paper_1904_10585_b200 import Context
+    n = 1001
+    ctx = Context(n, 16, 4)
+    rng = np.random.default_rng(9)
+    gd = rng.standard_normal(n)
+    for l in (1, 5, 7):
+        X = np.cumsum(rng.standard_normal((n, l + 2)), axis=1)
+        ref, cref = O.rna_extrapolate(X, 1e-8)
+        hist = [torch.as_tensor(X[:, i].copy()).cuda() for i in range(l + 2)]
+        B = torch.zeros((n, n + 1), dtype=torch.float64, device="cuda")[:, :n]
+        xo = torch.empty(n, dtype=torch.float64, device="cuda")
+        c = torch.empty(l + 1, dtype=torch.float64, device="cuda")
+        ctx.extrapolate(hist, 1e-8, torch.as_tensor(gd).cuda(), xo, B, c)
+        np.testing.assert_allclose(c.cpu().numpy(), cref, rtol=1e-9, atol=1e-12)
+        np.testing.assert_allclose(xo.cpu().numpy(), ref, rtol=1e-10, atol=1e-10 * np.abs(ref).max())
+        np.testing.assert_allclose(np.diag(B.cpu().numpy()), gd + ref, rtol=1e-10, atol=1e-10)
+
+
+@pytest.mark.parametrize("cfg", [
+    reduced(NEXT_CONFIGS["nce6a"], n=500, p=128, iters=16),
+    reduced(NEXT_CONFIGS["nce7a"], n=650, p=32, iters=16),
+], ids=["ex56_accel", "ex57_accel"])
+def test_nce_accelerated_trajectory(cfg):
+    """Extrapolated PFPG (paper §4.3): iterates x_k and F(x_k) within 1e-10 of the oracle, with
+    two extrapolations (l = 5 -> every 7 iterations) inside the trajectory."""
+    from paper_1904_10585_b200 import run
+    ref = O.run(cfg)["records"]
+    got = run(cfg)["records"]
+    _compare(ref, got, tol=1e-9)

@@ -27,11 +27,13 @@ def main():
     ap.add_argument("--p", type=int, default=64)
     ap.add_argument("--d", type=int, default=8)
     ap.add_argument("--max-iters", type=int, default=600)
+    ap.add_argument("--accel", type=int, default=5,
+                    help="extrapolation window l (paper §4.3; 0 = plain gradient)")
     a = ap.parse_args()
     import torch
     from pfinputs import NEXT_CONFIGS, reduced, nce_problem
     from paper_1904_10585_b200 import Solver
-    cfg = reduced(NEXT_CONFIGS["nce%d" % a.example], n=a.n, p=a.p, d=a.d)
+    cfg = reduced(NEXT_CONFIGS["nce%d" % a.example], n=a.n, p=a.p, d=a.d, accel_l=a.accel)
     prob = nce_problem(cfg)
     st = torch.cuda.Stream()
     with torch.cuda.stream(st):
@@ -56,7 +58,8 @@ def main():
     ref = PAPER.get((a.example, a.n))
     print(json.dumps({
         "problem": f"NCE Example 5.{a.example - 4} (label eg:5.{a.example}), n={a.n}, "
-                   f"p={a.p}, d={a.d}, tau=1, x0 = 1 - diag(G), fp64, 1 B200",
+                   f"p={a.p}, d={a.d}, tau=1, x0 = 1 - diag(G), "
+                   f"extrapolation l={a.accel}, fp64, 1 B200",
         "iterations": it, "time_s": ms / 1e3, "ms_per_iter": ms / it, "objective": F,
         "rel_grad": g / g0, "rank_last": int(s.rank.item()), "status": s.ctx.status(st)["names"],
         "paper_pfpg_cpu": None if ref is None else
