@@ -111,6 +111,16 @@ pf_status pf_interval_psd(pf_ctx ctx, const double* lo_hi, double eta, double* i
 pf_status pf_interval_soft(pf_ctx ctx, double thr, double eta, double* interval,
                            pf_stream stream);
 
+/* Top-r interval: a = lo_hi[0], b = (1 - eta) theta_r + eta a, theta_r the r-th
+ * largest Ritz value of the previous pf_rayleigh_ritz on this context (1 <= r <= p); before any
+ * Rayleigh-Ritz the all-positive rule b = eta a is used (R22).  Writes interval[2]. */
+pf_status pf_interval_top_r(pf_ctx ctx, const double* lo_hi, int32_t r, double eta,
+                            double* interval, pf_stream stream);
+
+/* Chebyshev degree of subsequent pf_filter calls (1 <= degree <= 64), e.g. the thm:conv1
+ * schedule d_k = ceil(c log(k + 2)).  Scratch does not depend on the degree. */
+pf_status pf_set_degree(pf_ctx ctx, int32_t degree);
+
 /* ---------------------------------------------------------------------------- hot path */
 /* U <- orth(rho^q(A) U) with rho(t) = T_d(L(t)), L(t) = (t - (a+b)/2)/((b-a)/2)
  * (eq:cheb P:185-191, eqn:cheb-linear-map P:216-218, eqn:subspace-update P:225-227).

@@ -34,7 +34,7 @@ import numpy as np
 
 from pfinputs import (Config, initial_block, lanczos_start, cfg1_problem, cfg1_noise,
                       pfpg_problem, pfam_problem, unpack_bitmask, cfg5_problem, cfg5_perturb,
-                      nce_problem)
+                      nce_problem, degree_at)
 
 __all__ = [
     "cheb_T", "growth_lower_bound", "interval_map", "interval_psd", "interval_top_r",
@@ -399,10 +399,11 @@ def run(cfg: Config, iters: int | None = None, record_factors: bool = True,
             a, b = interval_psd(lo, cfg.eta)
         else:
             a, b = interval_soft(thr, cfg.eta)
-        plan = rebase_plan(a, b, spread_estimate(theta_prev, lo, hi), cfg.d, cfg.rho_max)
-        # a2/a3
+        dk = degree_at(cfg, k)                                   # NEXT-4 degree schedule
+        plan = rebase_plan(a, b, spread_estimate(theta_prev, lo, hi), dk, cfg.rho_max)
+        # a2/a3 (q applications of the polynomial per filter)
         for _ in range(cfg.warmup if k == 0 else 1):
-            U = filter_update(A, U, a, b, cfg.d, 1, plan)
+            U = filter_update(A, U, a, b, dk, cfg.q, plan)
         # a4/a5
         theta, V = rayleigh_ritz(A, U)
         f = spectral_psd(theta) if psd else spectral_soft(theta, thr)

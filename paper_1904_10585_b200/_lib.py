@@ -44,6 +44,8 @@ def load() -> ctypes.CDLL:
         "pf_lanczos": [P, P, I64, P, I32, P, P],
         "pf_interval_psd": [P, P, D, P, P],
         "pf_interval_soft": [P, D, D, P, P],
+        "pf_interval_top_r": [P, P, I32, D, P, P],
+        "pf_set_degree": [P, I32],
         "pf_filter": [P, P, I64, P, I64, P, I32, D, P],
         "pf_orth": [P, P, I64, P],
         "pf_rayleigh_ritz": [P, P, I64, P, I64, P, I64, P, P],
@@ -188,6 +190,13 @@ class Context:
     def interval_soft(self, thr, eta, interval, stream=None):
         self._check(self.lib.pf_interval_soft(self.h, thr, eta, _ptr(interval), _stream(stream)),
                     "pf_interval_soft")
+
+    def interval_top_r(self, lo_hi, r, eta, interval, stream=None):
+        self._check(self.lib.pf_interval_top_r(self.h, _ptr(lo_hi), r, eta, _ptr(interval),
+                                               _stream(stream)), "pf_interval_top_r")
+
+    def set_degree(self, d: int):
+        self._check(self.lib.pf_set_degree(self.h, d), "pf_set_degree")
 
     def filter(self, A, U, interval, q=1, rho_max=1e6, stream=None):
         self._check(self.lib.pf_filter(self.h, _ptr(A), _ld(A), _ptr(U), _ld(U), _ptr(interval),

@@ -681,6 +681,20 @@ pf_status pf_interval_soft(pf_ctx ctx, double thr, double eta, double* interval,
   return PF_OK;
 }
 
+pf_status pf_interval_top_r(pf_ctx ctx, const double* lo_hi, int32_t r, double eta,
+                            double* interval, pf_stream stream) {
+  if (!ctx || !lo_hi || !interval) return PF_ERR_ARG;
+  if (r < 1 || r > ctx->p || !(eta >= 0.0 && eta < 1.0)) return PF_ERR_ARG;
+  PF_CU(interval_top_r_launch(lo_hi, r, eta, interval, ctx->state, (cudaStream_t)stream));
+  return PF_OK;
+}
+
+pf_status pf_set_degree(pf_ctx ctx, int32_t degree) {
+  if (!ctx || degree < 1 || degree > kMaxDeg) return PF_ERR_ARG;
+  ctx->d = degree;
+  return PF_OK;
+}
+
 pf_status pf_orth(pf_ctx ctx, void* Uv, int64_t ldu, pf_stream stream) {
   if (!ctx || !Uv) return PF_ERR_ARG;
   cudaStream_t st = (cudaStream_t)stream;

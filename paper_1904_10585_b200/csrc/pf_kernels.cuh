@@ -108,6 +108,8 @@ cudaError_t interval_psd_launch(const double* lo_hi, double eta, double* interva
                                 DevState* state, cudaStream_t st);
 cudaError_t interval_soft_launch(double thr, double eta, double* interval, DevState* state,
                                  cudaStream_t st);
+cudaError_t interval_top_r_launch(const double* lo_hi, int r, double eta, double* interval,
+                                  DevState* state, cudaStream_t st);
 cudaError_t copy_theta_launch(const double* theta, int p, DevState* state, cudaStream_t st);
 // Lanczos (pf_lanczos.cu): vectors are local row blocks with pitch ldq; every phase leaves
 // LOCAL sums that the host all-reduces between phases when the context is distributed.

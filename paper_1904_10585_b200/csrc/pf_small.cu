@@ -675,6 +675,29 @@ cudaError_t interval_psd_launch(const double* lo_hi, double eta, double* interva
   return cudaGetLastError();
 }
 
+// top-r interval: a = lo_hi[0], b = (1 - eta) theta_r + eta a with theta_r the r-th
+// largest Ritz value of the previous Rayleigh-Ritz (state->theta, descending); without previous
+// Ritz values the all-positive rule b = eta a is used (reading R22)
+__global__ void interval_top_r_kernel(const double* lo_hi, int r, double eta, double* interval,
+                                      DevState* state) {
+  double a = lo_hi[0];
+  double b = eta * a;
+  if (state->have_theta) b = (1.0 - eta) * state->theta[r - 1] + eta * a;
+  if (!(b > a)) {
+    atomicOr(&state->flags, PF_FLAG_DEGENERATE_INT);
+    b = a + fabs(a) + 1.0;
+  }
+  interval[0] = a;
+  interval[1] = b;
+}
+
+cudaError_t interval_top_r_launch(const double* lo_hi, int r, double eta, double* interval,
+                                  DevState* state, cudaStream_t st) {
+  count_launch();
+  interval_top_r_kernel<<<1, 1, 0, st>>>(lo_hi, r, eta, interval, state);
+  return cudaGetLastError();
+}
+
 __global__ void interval_soft_kernel(double thr, double eta, double* interval) {
   const double beta = (1.0 - eta) * thr;
   interval[0] = -beta;

@@ -11,7 +11,7 @@ import numpy as np
 import torch
 
 from pfinputs import (Config, initial_block, lanczos_start, cfg1_problem, cfg1_noise, pfpg_problem,
-                      pfam_problem, cfg5_problem, nce_problem)
+                      pfam_problem, cfg5_problem, nce_problem, degree_at)
 
 from ._lib import Context, PF_FP64, PF_TF32, PF_OP_PSD, PF_OP_SOFT_THRESHOLD
 
@@ -142,8 +142,10 @@ class Solver:
             ctx.interval_psd(self.lohi, cfg.eta, self.interval, st)
         else:
             ctx.interval_soft(self.thr, cfg.eta, self.interval, st)
+        if cfg.deg_c > 0.0:                                   # thm:conv1 degree schedule (NEXT-4)
+            ctx.set_degree(degree_at(cfg, k))
         for _ in range(cfg.warmup if k == 0 else 1):
-            ctx.filter(self.A, self.U, self.interval, 1, cfg.rho_max, st)
+            ctx.filter(self.A, self.U, self.interval, cfg.q, cfg.rho_max, st)
         ctx.rayleigh_ritz(self.A, self.U, self.V, self.theta, st)
         ctx.spectral_op(self.op, self.thr, self.theta, self.f, self.rank, st)
         if cfg.mode == "pfpg":

@@ -71,6 +71,10 @@ class Config:
     # and lambda = accel_lam * ||U^T U||_2 (SPEC defaults l = 5, 1e-8; reading R21)
     accel_l: int = 0
     accel_lam: float = 1e-8
+    # driver variants (NEXT-4): q applications of the polynomial per iteration, and the
+    # degree schedule d_k = max(d, ceil(deg_c log(k + 2))) of thm:conv1 (0 = constant)
+    q: int = 1
+    deg_c: float = 0.0
     nbig: int = 256           # config 5: eigenvalues drawn from U[5, 50]
     nrefl: int = 64           # config 5: Householder reflectors in the basis
 
@@ -370,3 +374,12 @@ def nce_problem(cfg: Config) -> dict:
     G[(iu[1], iu[0])] = G[iu]
     np.fill_diagonal(G, 1.0)
     return {"G": G}
+
+
+def degree_at(cfg: Config, k: int) -> int:
+    """Chebyshev degree of iteration k: cfg.d, or the thm:conv1 schedule
+    d_k = max(cfg.d, ceil(deg_c * log(k + 2))) when deg_c > 0 (NEXT-4)."""
+    import math
+    if cfg.deg_c <= 0.0:
+        return cfg.d
+    return max(cfg.d, int(math.ceil(cfg.deg_c * math.log(k + 2))))

@@ -1,0 +1,65 @@
+"""Driver variants of the method on the CUDA path vs the oracle:
+q applications of the polynomial per filter, the degree schedule of thm:conv1
+ and the top-r interval."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from pfinputs import CONFIGS, reduced
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a B200")]
+
+
+def _traj(cfg, tol):
+    from paper_1904_10585_b200 import run
+    ref = O.run(cfg)["records"]
+    got = run(cfg)["records"]
+    for r, g in zip(ref, got):
+        assert g["rank"] == r["rank"]
+        den = O.lowrank_fro(r["V"], r["f"])
+        assert O.lowrank_diff_fro(g["V"], g["f"], r["V"], r["f"]) <= tol * den, r["k"]
+        if "objective" in r:
+            assert g["objective"] == pytest.approx(r["objective"], rel=tol)
+
+
+@pytest.mark.parametrize("cfg,tol", [
+    (reduced(CONFIGS[1], iters=6, q=2), 1e-10),
+    (reduced(CONFIGS[3], n=900, iters=6, edge_prob=82 / 900, q=2), 1e-10),
+    (reduced(CONFIGS[5], n=1536, p=64, nbig=24, nrefl=16, iters=3, q=2), 1e-4),
+], ids=["cfg1_q2", "cfg3_q2", "cfg5_tf32_q2"])
+def test_q_repeats(cfg, tol):
+    _traj(cfg, tol)
+
+
+@pytest.mark.parametrize("cfg,tol", [
+    (reduced(CONFIGS[3], n=900, iters=8, d=2, deg_c=3.0, edge_prob=82 / 900), 1e-10),
+    (reduced(CONFIGS[2], n=800, iters=8, d=3, deg_c=2.5), 1e-10),
+], ids=["cfg3_sched", "cfg2_sched"])
+def test_degree_schedule(cfg, tol):
+    _traj(cfg, tol)
+
+
+def test_interval_top_r_matches_oracle():
+    from paper_1904_10585_b200 import Context
+    n, p = 700, 32
+    rng = np.random.default_rng(3)
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    lam = np.concatenate([np.linspace(5, 1, 20), rng.uniform(-2, 0.5, n - 20)])
+    A = (q * lam) @ q.T
+    A = 0.5 * (A + A.T)
+    ctx = Context(n, p, 4)
+    dA = torch.as_tensor(A).cuda()
+    U = torch.as_tensor(O.orth(rng.standard_normal((n, p)))).cuda()
+    V = torch.empty_like(U)
+    th = torch.empty(p, dtype=torch.float64, device="cuda")
+    lohi = torch.tensor([-2.5, 6.0], dtype=torch.float64, device="cuda")
+    iv = torch.zeros(2, dtype=torch.float64, device="cuda")
+    ctx.interval_top_r(lohi, 10, 0.1, iv)       # before any RR: b = eta a
+    np.testing.assert_allclose(iv.cpu().numpy(), O.interval_psd(-2.5, 0.1), rtol=0, atol=0)
+    ctx.rayleigh_ritz(dA, U, V, th)
+    ctx.interval_top_r(lohi, 10, 0.1, iv)
+    theta = th.cpu().numpy()
+    np.testing.assert_allclose(iv.cpu().numpy(), O.interval_top_r(-2.5, theta[9], 0.1),
+                               rtol=1e-15, atol=1e-15)

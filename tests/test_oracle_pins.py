@@ -528,3 +528,32 @@ def test_nce_accelerated_reaches_tolerance_faster():
     assert out["nce6a"][0] is not None and out["nce6a"][0] <= 45
     assert out["nce6"][0] is None or out["nce6"][0] > 2 * out["nce6a"][0]
     assert out["nce6a"][1] == pytest.approx(8.9e3, rel=0.01)
+
+
+# ------------------------------------------------------------------ driver variants (NEXT-4)
+def test_filter_q_repeats_diagonal_closed_form():
+    """q applications of rho = T_d(L(.)): on a diagonal A the filtered block is
+    diag(T_d(L(lambda_i))^q) U exactly (closed form)."""
+    lam = np.array([3.0, 1.2, 0.4, -0.2, -0.9, -1.0])
+    A = np.diag(lam)
+    U = np.random.default_rng(2).standard_normal((6, 3))
+    a, b = -1.0, 0.5
+    c, e = O.interval_map(a, b)
+    for q in (1, 2, 3):
+        Y = U
+        for _ in range(q):
+            Y = O.chebyshev_filter(A, Y, a, b, 4)
+        scale = np.array([O.cheb_T(4, (l - c) / e) for l in lam]) ** q
+        np.testing.assert_allclose(Y, scale[:, None] * U, rtol=1e-12, atol=1e-12)
+        Q = O.filter_update(A, U, a, b, 4, q)
+        np.testing.assert_allclose(np.max(O.sin_theta(O.orth(scale[:, None] * U), Q)), 0, atol=1e-10)
+
+
+def test_degree_schedule_values():
+    """thm:conv1: d_k = ceil(c log(k + 2)), floored at the configured d."""
+    import math
+    from pfinputs import degree_at
+    cfg = reduced(CONFIGS[1], d=2, deg_c=3.0)
+    for k in range(50):
+        assert degree_at(cfg, k) == max(2, math.ceil(3.0 * math.log(k + 2)))
+    assert degree_at(reduced(CONFIGS[1]), 37) == CONFIGS[1].d
