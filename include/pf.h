@@ -60,7 +60,7 @@ typedef enum {
 /* device status word bits (pf_get_device_status) */
 #define PF_FLAG_CHOL_SHIFT 0x1u      /* CholeskyQR fell back to the shifted variant (3 passes) */
 #define PF_FLAG_NONFINITE 0x2u       /* a non-finite value reached the Gram / H matrix */
-#define PF_FLAG_DEGENERATE_INT 0x4u  /* PSD interval needed a < 0 but the estimate was >= 0 */
+#define PF_FLAG_DEGENERATE_INT 0x4u  /* b <= a (e.g. PSD iterate: a >= 0): filter skipped */
 #define PF_FLAG_SATURATED 0x8u       /* rank == p after the spectral operator */
 #define PF_FLAG_JACOBI_MAXSWEEP 0x10u /* Jacobi hit its sweep limit before the tolerance */
 #define PF_FLAG_LANCZOS_BREAK 0x20u  /* Lanczos stopped early (invariant subspace found) */
@@ -103,7 +103,9 @@ pf_status pf_get_device_status(pf_ctx ctx, pf_stream stream, uint32_t* flags, in
 pf_status pf_lanczos(pf_ctx ctx, const void* A, int64_t lda, const double* v0, int32_t m,
                      double* lo_hi, pf_stream stream);
 
-/* PSD / all-positive interval: a = lo_hi[0], b = eta * a.  Writes interval[2]. */
+/* PSD / all-positive interval: a = lo_hi[0], b = eta * a.  Writes interval[2].
+ * If a >= 0 (the iterate is PSD) the interval is the degenerate [a, a]: a pf_filter call
+ * on a degenerate interval skips the filter (returns orth(U)) and sets PF_FLAG_DEGENERATE_INT. */
 pf_status pf_interval_psd(pf_ctx ctx, const double* lo_hi, double eta, double* interval,
                           pf_stream stream);
 

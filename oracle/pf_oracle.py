@@ -395,21 +395,29 @@ def run(cfg: Config, iters: int | None = None, record_factors: bool = True,
         # a1: interval
         if k == 0 or (psd and k % cfg.lanczos_every == 0):
             lo, hi = lanczos_extremes(A, lanczos_start(cfg, k), cfg.lanczos_steps)
-        if psd:
+        # PSD iterate (a >= 0: nothing to damp): degenerate interval, the filter is
+        # skipped this iteration and U_{k-1} is reused (SURVEY §8(c) reading)
+        degenerate = psd and not lo < 0
+        if degenerate:
+            a = b = lo
+        elif psd:
             a, b = interval_psd(lo, cfg.eta)
         else:
             a, b = interval_soft(thr, cfg.eta)
         dk = degree_at(cfg, k)                                   # NEXT-4 degree schedule
-        plan = rebase_plan(a, b, spread_estimate(theta_prev, lo, hi), dk, cfg.rho_max)
-        # a2/a3 (q applications of the polynomial per filter)
-        for _ in range(cfg.warmup if k == 0 else 1):
-            U = filter_update(A, U, a, b, dk, cfg.q, plan)
+        if not degenerate:
+            plan = rebase_plan(a, b, spread_estimate(theta_prev, lo, hi), dk, cfg.rho_max)
+            # a2/a3 (q applications of the polynomial per filter)
+            for _ in range(cfg.warmup if k == 0 else 1):
+                U = filter_update(A, U, a, b, dk, cfg.q, plan)
+        else:
+            plan = []
         # a4/a5
         theta, V = rayleigh_ritz(A, U)
         f = spectral_psd(theta) if psd else spectral_soft(theta, thr)
         keep = f != 0.0
         rec = {"k": k, "a": a, "b": b, "theta": theta, "rank": int(keep.sum()),
-               "saturated": bool(keep.all()), "rebase": plan}
+               "saturated": bool(keep.all()), "rebase": plan, "degenerate": degenerate}
         if record_factors:
             rec["V"], rec["f"] = V[:, keep], f[keep]
         # a6

@@ -609,14 +609,23 @@ cudaError_t spectral_launch(int op, double thr, const double* theta, int p, doub
 __global__ void plan_kernel(const double* __restrict__ interval, int d, double rho_max, int p,
                             DevState* state) {
   if (threadIdx.x != 0) return;
-  double a = interval[0], b = interval[1];
-  if (!(b > a)) {
-    atomicOr(&state->flags, PF_FLAG_DEGENERATE_INT);
-    b = a + 1.0;
-  }
-  const double c = 0.5 * (b + a), e = 0.5 * (b - a);
+  const double a = interval[0], b = interval[1];
   state->interval[0] = a;
   state->interval[1] = b;
+  if (!(b > a)) {
+    // degenerate interval (e.g. a PSD iterate: no eigenvalue to damp), SURVEY §8(c) reading:
+    // the filter is skipped for this call -- identity recurrence Y_{j+1} = Y_j, no re-base --
+    // so pf_filter returns orth(U), i.e. the previous subspace
+    atomicOr(&state->flags, PF_FLAG_DEGENERATE_INT);
+    for (int j = 0; j < d; ++j) {
+      state->coef[j][0] = 0.0;
+      state->coef[j][1] = 1.0;
+      state->coef[j][2] = 0.0;
+      state->rebase[j] = 0;
+    }
+    return;
+  }
+  const double c = 0.5 * (b + a), e = 0.5 * (b - a);
   double spread;
   if (state->have_theta) {
     spread = 0.0;
@@ -659,13 +668,11 @@ cudaError_t plan_launch(const double* interval, int d, double rho_max, int p, De
 
 __global__ void interval_psd_kernel(const double* lo_hi, double eta, double* interval,
                                     DevState* state) {
-  double a = lo_hi[0];
-  if (!(a < 0.0)) {
-    atomicOr(&state->flags, PF_FLAG_DEGENERATE_INT);
-    a = -(fabs(a) + 1.0);
-  }
+  const double a = lo_hi[0];
   interval[0] = a;
-  interval[1] = eta * a;  // b = eta a
+  // b = eta a; a >= 0 (nothing to damp: the iterate is PSD) leaves the
+  // degenerate interval [a, a], on which pf_filter skips the filter (plan_kernel)
+  interval[1] = (a < 0.0) ? eta * a : a;
 }
 
 cudaError_t interval_psd_launch(const double* lo_hi, double eta, double* interval,
@@ -683,12 +690,8 @@ __global__ void interval_top_r_kernel(const double* lo_hi, int r, double eta, do
   double a = lo_hi[0];
   double b = eta * a;
   if (state->have_theta) b = (1.0 - eta) * state->theta[r - 1] + eta * a;
-  if (!(b > a)) {
-    atomicOr(&state->flags, PF_FLAG_DEGENERATE_INT);
-    b = a + fabs(a) + 1.0;
-  }
   interval[0] = a;
-  interval[1] = b;
+  interval[1] = (b > a) ? b : a;  // degenerate -> the filter is skipped (plan_kernel)
 }
 
 cudaError_t interval_top_r_launch(const double* lo_hi, int r, double eta, double* interval,

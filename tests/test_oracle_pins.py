@@ -557,3 +557,23 @@ def test_degree_schedule_values():
     for k in range(50):
         assert degree_at(cfg, k) == max(2, math.ceil(3.0 * math.log(k + 2)))
     assert degree_at(reduced(CONFIGS[1]), 37) == CONFIGS[1].d
+
+
+def test_psd_iterate_skips_filter_compression_closed_form():
+    """Degenerate interval (SURVEY §8(c) reading R23): a PSD iterate has nothing to damp
+    (a = lambda_min >= 0), the filter is skipped and U_{k-1} is reused; with no noise every
+    iterate is then the compression X = P A P, P the orthogonal projector onto span(U_0), and
+    PSD projection leaves it unchanged (the Ritz values of a PSD matrix are >= 0)."""
+    from pfinputs import CONFIGS, reduced, initial_block
+    cfg = reduced(CONFIGS[1], n=64, p=8, iters=3, noise=0.0)
+    rs = np.random.default_rng(11)
+    q, _ = np.linalg.qr(rs.standard_normal((64, 64)))
+    A = (q * rs.uniform(1.0, 10.0, 64)) @ q.T
+    A = 0.5 * (A + A.T)
+    out = O.run(cfg, problem={"A0": A})
+    Q0, _ = np.linalg.qr(initial_block(cfg))
+    X = Q0 @ (Q0.T @ A @ Q0) @ Q0.T
+    for r in out["records"]:
+        assert r["degenerate"] and r["rebase"] == [] and r["a"] == r["b"] > 0
+        Xk = (r["V"] * r["f"]) @ r["V"].T
+        assert np.abs(Xk - X).max() <= 1e-12 * np.abs(X).max()
