@@ -41,7 +41,12 @@ typedef void* pf_stream; /* a cudaStream_t; NULL = legacy default stream */
 typedef enum {
   PF_FP64 = 0, /* fp64 storage + fp64 DMMA tensor cores (mma.sync .f64)                    */
   PF_FP32 = 1, /* reserved (plain fp32 SIMT filter): not built, PF_ERR_UNSUPPORTED          */
-  PF_TF32 = 2  /* fp32 storage, tcgen05 kind::tf32 filter GEMM (3xTF32), fp64 small objects */
+  PF_TF32 = 2, /* fp32 storage, tcgen05 kind::tf32 filter GEMM (3xTF32), fp64 small objects */
+  PF_FP64_I8 = 3 /* fp64 storage and arithmetic; the filter / Rayleigh-Ritz products A Y are
+                    formed from EXACT int8 tensor-core products (tcgen05 kind::i8) of S = 7
+                    signed 7-bit digit slices of A (per-row power-of-two scale) and of Y (per
+                    column), levels combined in fp64 (pf_set_i8_slices; DESIGN.md §4 K1-i8).
+                    Everything else is the PF_FP64 path.  Scratch: 7 n_local n + 7 p n bytes. */
 } pf_dtype;
 
 typedef enum { PF_OP_PSD = 0, PF_OP_SOFT_THRESHOLD = 1 } pf_op;
@@ -230,6 +235,25 @@ pf_status pf_set_tf32_passes(pf_ctx ctx, int32_t passes);
  * 3xTF32.  Errors injected by the cheaper early steps are damped by the exact tail steps
  * (reading R18). */
 pf_status pf_set_tf32_schedule(pf_ctx ctx, int32_t early_passes, int32_t exact_tail);
+
+/* PF_FP64_I8 contexts: digit slices per operand, S in {6, 7} (default 7: operator error
+ * < 2^-48 of the row / column scales), or 0 to run the fp64 DMMA GEMM of PF_FP64 instead (same
+ * context, for comparisons).  PF_ERR_ARG otherwise, PF_ERR_UNSUPPORTED for other dtypes. */
+pf_status pf_set_i8_slices(pf_ctx ctx, int32_t slices);
+
+/* PF_FP64_I8: pf_filter splits A into digit slices on every call; pf_rayleigh_ritz and pf_matmul
+ * reuse the slices of the last split of the same A (pointer, lda) unless a libpf call wrote an
+ * iterate since (pf_prox_step, pf_admm_step, pf_nce_step, pf_extrapolate, pf_perturb).  A caller
+ * that writes A by other means between pf_filter and pf_rayleigh_ritz calls pf_invalidate first.
+ * No-op for other dtypes. */
+pf_status pf_invalidate(pf_ctx ctx);
+
+/* out = A Y with the context's filter GEMM (fp64 dtypes): A local rows (n_local x n, lda as for
+ * pf_filter), Y the local rows of an n x p block (n_local x p, ldy >= p; gathered internally when
+ * distributed), out n_local x p (ldo >= p).  The kernel of every Chebyshev step, exposed for
+ * measurement and tests.  PF_ERR_UNSUPPORTED for PF_TF32. */
+pf_status pf_matmul(pf_ctx ctx, const double* A, int64_t lda, const double* Y, int64_t ldy,
+                    double* out, int64_t ldo, pf_stream stream);
 
 #ifdef __cplusplus
 }

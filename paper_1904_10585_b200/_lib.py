@@ -13,6 +13,7 @@ LIB_PATH = os.path.join(HERE, "libpf.so")
 
 PF_FP64 = 0
 PF_TF32 = 2
+PF_FP64_I8 = 3   # fp64, filter products from exact int8 tensor-core digit products
 PF_OP_PSD = 0
 PF_OP_SOFT_THRESHOLD = 1
 STATUS = {0: "PF_OK", 1: "PF_ERR_ARG", 2: "PF_ERR_DIM", 3: "PF_ERR_INTERVAL", 4: "PF_ERR_CUDA",
@@ -58,6 +59,9 @@ def load() -> ctypes.CDLL:
         "pf_extrapolate": [P, P, I32, D, P, P, P, I64, P, P],
         "pf_set_tf32_passes": [P, I32],
         "pf_set_tf32_schedule": [P, I32, I32],
+        "pf_set_i8_slices": [P, I32],
+        "pf_invalidate": [P],
+        "pf_matmul": [P, P, I64, P, I64, P, I64, P],
         "pf_profile": [P, I32],
         "pf_profile_read": [P, P, ctypes.POINTER(D), ctypes.POINTER(I64)],
         "pf_kernel_launches": [],
@@ -248,6 +252,19 @@ class Context:
 
     def set_tf32_passes(self, passes: int):
         self._check(self.lib.pf_set_tf32_passes(self.h, passes), "pf_set_tf32_passes")
+
+    def set_i8_slices(self, slices: int):
+        """PF_FP64_I8: digit slices per operand (6..8), 0 = the fp64 DMMA GEMM."""
+        self._check(self.lib.pf_set_i8_slices(self.h, slices), "pf_set_i8_slices")
+
+    def invalidate(self):
+        """A was written outside libpf: the next product re-splits it (PF_FP64_I8)."""
+        self._check(self.lib.pf_invalidate(self.h), "pf_invalidate")
+
+    def matmul(self, A, Y, out, stream=None):
+        """out = A Y with the context's filter GEMM (fp64 dtypes; local rows)."""
+        self._check(self.lib.pf_matmul(self.h, _ptr(A), _ld(A), _ptr(Y), _ld(Y), _ptr(out),
+                                       _ld(out), _stream(stream)), "pf_matmul")
 
     def set_tf32_schedule(self, early_passes: int, exact_tail: int):
         self._check(self.lib.pf_set_tf32_schedule(self.h, early_passes, exact_tail),

@@ -94,8 +94,23 @@ struct pf_ctx_s {
   CUtensorMap mapAf, mapApf;
   const float* mapAf_ptr = nullptr;
   int64_t mapAf_lda = 0;
+  // ---- fp64 via exact int8 tensor-core products (dtype PF_FP64_I8, pf_gemm_i8.cu)
+  bool i8 = false;
+  I8Plan i8plan;                               // S = 0: this context runs the DMMA GEMM
+  int8_t* A8 = nullptr;                        // [kI8MaxSlices][n_local][kpad]
+  double* a8_rscale = nullptr;                 // [n_local]
+  int8_t* Y8 = nullptr;                        // [kI8MaxSlices][p][kpad]
+  double* y8_cscale = nullptr;                 // [p]
+  unsigned long long* y8_cmax = nullptr;       // [p]
+  double* i8_acc = nullptr;
+  CUtensorMap mapA8, mapY8, mapA8pf;
+  const double* a8_src = nullptr;              // A whose digit slices A8 holds (pf_filter)
+  int64_t a8_lda = 0;
+  bool a8_valid = false;                       // cleared by every libpf call that writes A
   char err[512] = {0};
 };
+
+static constexpr int kI8MaxSlices = 7;
 
 static pf_status cuda_fail(pf_ctx c, cudaError_t e, const char* where) {
   if (c) snprintf(c->err, sizeof(c->err), "%s: %s", where, cudaGetErrorString(e));
@@ -114,6 +129,7 @@ static pf_status cuda_fail(pf_ctx c, cudaError_t e, const char* where) {
 
 static bool p_supported(int p, pf_dtype dt) {
   if (dt == PF_TF32) return p == 64 || p == 128 || p == 256 || p == 512;
+  // PF_FP64 and PF_FP64_I8
   return p == 16 || p == 32 || p == 64 || p == 128;
 }
 static bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }
@@ -178,6 +194,15 @@ static pf_status alloc_all(pf_ctx ctx) {
     ok &= A((void**)&ctx->Wbuf, (size_t)nl * p * 8);
     ok &= A((void**)&ctx->VFbuf, (size_t)nl * p * 8);
   }
+  if (ctx->i8) {
+    const I8Plan& ip = ctx->i8plan;
+    ok &= A((void**)&ctx->A8, (size_t)kI8MaxSlices * nl * ip.kpad);
+    ok &= A((void**)&ctx->a8_rscale, (size_t)nl * 8);
+    ok &= A((void**)&ctx->Y8, (size_t)kI8MaxSlices * p * ip.kpad);
+    ok &= A((void**)&ctx->y8_cscale, (size_t)p * 8);
+    ok &= A((void**)&ctx->y8_cmax, (size_t)p * 8);
+    ok &= A((void**)&ctx->i8_acc, ip.acc_doubles * 8);
+  }
   if (ctx->dist) {
     ok &= A((void**)&ctx->Yfull, (size_t)n * p * 8);
     ok &= A((void**)&ctx->Vfull, (size_t)n * p * 8);
@@ -239,6 +264,11 @@ static pf_status alloc_all(pf_ctx ctx) {
     snprintf(ctx->err, sizeof(ctx->err), "cuTensorMapEncodeTiled(B) failed");
     return PF_ERR_CUDA;
   }
+  if (ctx->i8 && (!i8_encode_A(&ctx->mapA8, &ctx->mapA8pf, ctx->A8, ctx->i8plan) ||
+                  !i8_encode_B(&ctx->mapY8, ctx->Y8, ctx->i8plan))) {
+    snprintf(ctx->err, sizeof(ctx->err), "cuTensorMapEncodeTiled(int8 slices) failed");
+    return PF_ERR_CUDA;
+  }
   PF_CU(cudaDeviceSynchronize());
   return PF_OK;
 }
@@ -247,7 +277,7 @@ static pf_status create_common(int64_t n, int32_t p, int32_t degree, pf_dtype dt
                                int world, const void* nccl_id, pf_ctx* out) {
   if (!out) return PF_ERR_ARG;
   *out = nullptr;
-  if (dtype != PF_FP64 && dtype != PF_TF32) return PF_ERR_UNSUPPORTED;
+  if (dtype != PF_FP64 && dtype != PF_TF32 && dtype != PF_FP64_I8) return PF_ERR_UNSUPPORTED;
   // fp32 path, distributed: equal row blocks with n_local % 16 == 0 (a 16-wide TMA K box never
   // straddles two ranks' slabs of the gathered block)
   if (dtype == PF_TF32 && nccl_id != nullptr && (n % (16 * (int64_t)world)) != 0)
@@ -278,6 +308,10 @@ static pf_status create_common(int64_t n, int32_t p, int32_t degree, pf_dtype dt
   }
   if (dtype == PF_TF32) ctx->tplan = tf32_plan(p, (int)ctx->n_local, (int)n, ctx->num_sms);
   else ctx->plan = cheb_gemm_plan(p, (int)ctx->n_local, (int)n, ctx->num_sms);
+  if (dtype == PF_FP64_I8) {
+    ctx->i8 = true;
+    ctx->i8plan = i8_plan(p, (int)ctx->n_local, (int)n, 7, ctx->num_sms);  // S = 7
+  }
   pf_status s = alloc_all(ctx);
   if (s == PF_OK && ctx->dist) {
     ncclUniqueId id;
@@ -357,7 +391,9 @@ pf_status pf_destroy(pf_ctx ctx) {
                   ctx->lz_theta, ctx->lz_S,   ctx->rb_part,   ctx->rb_cnt,  ctx->shift_flag,
                   ctx->Yf[0],  ctx->Yf[1],    ctx->Yf[2],     ctx->Wf,      ctx->g32_part,
                   ctx->chol_W, ctx->chol_D,   ctx->jac_H,     ctx->jac_V,   ctx->jac_red,
-                  ctx->jac_cnt, ctx->tf_ws,   ctx->tf_cnt,    ctx->tf_acc,  ctx->Yfull32};
+                  ctx->jac_cnt, ctx->tf_ws,   ctx->tf_cnt,    ctx->tf_acc,  ctx->Yfull32,
+                  ctx->A8,     ctx->a8_rscale, ctx->Y8,       ctx->y8_cscale, ctx->y8_cmax,
+                  ctx->i8_acc};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete ctx;
@@ -431,20 +467,49 @@ static pf_status allreduce(pf_ctx ctx, double* buf, size_t count, cudaStream_t s
 }
 
 // One Chebyshev step / plain product: out = coef * (A B) + ..., B = Y[bidx] (all rows).
+static bool use_i8(pf_ctx ctx) { return ctx->i8 && ctx->i8plan.S > 0; }
+
+// PF_FP64_I8: digit slices of A for the products that follow (pf_gemm_i8.cu).  pf_filter always
+// re-splits (A may have changed since the last iteration); pf_rayleigh_ritz / pf_matmul reuse
+// the slices when they were made from the same A and no libpf call wrote an iterate since.
+static pf_status split_A(pf_ctx ctx, const double* A, int64_t lda, bool reuse, cudaStream_t st) {
+  if (!use_i8(ctx)) return PF_OK;
+  if (reuse && ctx->a8_valid && ctx->a8_src == A && ctx->a8_lda == lda) return PF_OK;
+  PF_CU(i8_split_A_launch(A, lda, ctx->i8plan, ctx->A8, ctx->a8_rscale, ctx->num_sms, st));
+  ctx->a8_src = A;
+  ctx->a8_lda = lda;
+  ctx->a8_valid = true;
+  return PF_OK;
+}
+static void iterate_written(pf_ctx ctx) { ctx->a8_valid = false; }
+
+static bool is_fp64(pf_ctx ctx) { return ctx->dtype == PF_FP64 || ctx->dtype == PF_FP64_I8; }
+
 static pf_status gemm_step(pf_ctx ctx, int bidx, const double* ycur, const double* yprev,
                            double* out, const double* coef, cudaStream_t st) {
   const CUtensorMap* mb;
+  const double* bsrc;
   if (!ctx->dist) {
     mb = &ctx->mapB[bidx];
+    bsrc = ctx->Y[bidx];
   } else {
     PF_TRY(gather(ctx, ctx->Y[bidx], ctx->Yfull, ctx->p, st));
     mb = &ctx->mapBfull;
+    bsrc = ctx->Yfull;
   }
+  if (use_i8(ctx))
+    PF_CU(i8_split_Y_launch(bsrc, ctx->p, ctx->i8plan, ctx->y8_cmax, ctx->Y8, ctx->y8_cscale,
+                            ctx->num_sms, st));
   const bool rec = ctx->prof && ctx->ev_used + 2 <= ctx->ev.size();
   if (ctx->prof && !rec) ++ctx->prof_dropped;
   if (rec) PF_CU(cudaEventRecord(ctx->ev[ctx->ev_used], st));
-  PF_CU(cheb_gemm_launch(ctx->plan, ctx->mapA, *mb, ycur, yprev, out, coef, ctx->cheb_ws,
-                         ctx->cheb_cnt, st));
+  if (use_i8(ctx))
+    PF_CU(i8_gemm_launch(ctx->i8plan, ctx->mapA8, ctx->mapY8, ctx->mapA8pf, ctx->a8_rscale,
+                         ctx->y8_cscale,
+                         ycur, yprev, out, ctx->p, coef, ctx->i8_acc, st));
+  else
+    PF_CU(cheb_gemm_launch(ctx->plan, ctx->mapA, *mb, ycur, yprev, out, coef, ctx->cheb_ws,
+                           ctx->cheb_cnt, st));
   if (rec) {
     PF_CU(cudaEventRecord(ctx->ev[ctx->ev_used + 1], st));
     ctx->ev_used += 2;
@@ -727,6 +792,7 @@ pf_status pf_filter(pf_ctx ctx, const void* Av, int64_t lda, void* Uv, int64_t l
   PF_TRY(check_A(ctx, A, lda));
   PF_TRY(map_A(ctx, A, lda));
   cudaStream_t st = (cudaStream_t)stream;
+  PF_TRY(split_A(ctx, A, lda, false, st));
   const int p = ctx->p, d = ctx->d;
   const int nl = (int)ctx->n_local;
   const size_t row = (size_t)p * 8;
@@ -770,6 +836,7 @@ pf_status pf_rayleigh_ritz(pf_ctx ctx, const void* Av, int64_t lda, const void* 
   PF_TRY(check_A(ctx, A, lda));
   PF_TRY(map_A(ctx, A, lda));
   cudaStream_t st = (cudaStream_t)stream;
+  PF_TRY(split_A(ctx, A, lda, true, st));
   const int p = ctx->p, nl = (int)ctx->n_local;
   const size_t row = (size_t)p * 8;
   PF_CU(cudaMemcpy2DAsync(ctx->Y[0], row, U, ldu * 8, row, nl, cudaMemcpyDeviceToDevice, st));
@@ -818,12 +885,13 @@ pf_status pf_prox_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f
                        int32_t r, double* A_out, int64_t lda_out, double* obj,
                        pf_stream stream) {
   if (!ctx || !V || !f || !omega || !A_out || !obj) return PF_ERR_ARG;
-  if (ctx->dtype != PF_FP64) return PF_ERR_UNSUPPORTED;
+  if (!is_fp64(ctx)) return PF_ERR_UNSUPPORTED;
   if (r < 0 || r > 64 || (r > 0 && !W)) return PF_ERR_ARG;
   if (ldv < ctx->p || (ldv & 1) || !aligned16(V) || ldo < (ctx->n + 31) / 32 ||
       lda_out < ctx->n || (r > 0 && ldw < r))
     return PF_ERR_DIM;
   cudaStream_t st = (cudaStream_t)stream;
+  iterate_written(ctx);
   const double* Vf;
   int64_t ldf;
   PF_TRY(full_V(ctx, V, ldv, &Vf, &ldf, st));
@@ -838,10 +906,11 @@ pf_status pf_admm_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f
                        const uint32_t* adj, int64_t ldadj, const double* deg, double* Z,
                        int64_t ldz, double* obj, pf_stream stream) {
   if (!ctx || !V || !f || !adj || !deg || !Z || !obj) return PF_ERR_ARG;
-  if (ctx->dtype != PF_FP64) return PF_ERR_UNSUPPORTED;
+  if (!is_fp64(ctx)) return PF_ERR_UNSUPPORTED;
   if (ldv < ctx->p || (ldv & 1) || !aligned16(V) || ldadj < (ctx->n + 31) / 32 || ldz < ctx->n)
     return PF_ERR_DIM;
   cudaStream_t st = (cudaStream_t)stream;
+  iterate_written(ctx);
   const double* Vf;
   int64_t ldf;
   PF_TRY(full_V(ctx, V, ldv, &Vf, &ldf, st));
@@ -860,10 +929,11 @@ pf_status pf_nce_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f,
                       const double* gdiag, const double* x_in, double* x_out, double* B,
                       int64_t ldb, double* obj, pf_stream stream) {
   if (!ctx || !V || !f || !gdiag || !x_in || !x_out || !B || !obj) return PF_ERR_ARG;
-  if (ctx->dtype != PF_FP64) return PF_ERR_UNSUPPORTED;
+  if (!is_fp64(ctx)) return PF_ERR_UNSUPPORTED;
   if (ldv < ctx->p || ldb < ctx->n) return PF_ERR_DIM;
   if (!(tau > 0.0)) return PF_ERR_ARG;
   cudaStream_t st = (cudaStream_t)stream;
+  iterate_written(ctx);
   PF_CU(nce_launch(V, ldv, f, ctx->p, tau, gdiag, x_in, x_out, B, ldb, (int)ctx->n_local,
                    (int)ctx->row0, ctx->rb_part, ctx->rb_cnt, obj, st));
   PF_TRY(allreduce(ctx, obj, 2, st));  // raw sums over the row blocks
@@ -875,12 +945,13 @@ pf_status pf_extrapolate(pf_ctx ctx, const double* const* hist, int32_t l, doubl
                          const double* gdiag, double* x_out, double* B, int64_t ldb, double* coef,
                          pf_stream stream) {
   if (!ctx || !hist || !gdiag || !x_out || !B) return PF_ERR_ARG;
-  if (ctx->dtype != PF_FP64) return PF_ERR_UNSUPPORTED;
+  if (!is_fp64(ctx)) return PF_ERR_UNSUPPORTED;
   if (l < 0 || l + 1 > 8 || !(lam_rel > 0.0)) return PF_ERR_ARG;
   if (ldb < ctx->n) return PF_ERR_DIM;
   for (int i = 0; i <= l + 1; ++i)
     if (!hist[i]) return PF_ERR_ARG;
   cudaStream_t st = (cudaStream_t)stream;
+  iterate_written(ctx);
   const int L = l + 1;
   // partials: rna_blocks * L(L+1)/2 <= 128 * 36 doubles fit the rebuild partials buffer
   PF_CU(rna_gram_launch(hist, L, (int)ctx->n_local, ctx->rb_part, ctx->rb_cnt, ctx->G, st));
@@ -893,8 +964,9 @@ pf_status pf_extrapolate(pf_ctx ctx, const double* const* hist, int32_t l, doubl
 pf_status pf_perturb(pf_ctx ctx, double* A, int64_t lda, const double* E, int64_t lde,
                      pf_stream stream) {
   if (!ctx || !A || !E) return PF_ERR_ARG;
-  if (ctx->dtype != PF_FP64) return PF_ERR_UNSUPPORTED;
+  if (!is_fp64(ctx)) return PF_ERR_UNSUPPORTED;
   if (lda < ctx->n || lde < ctx->n) return PF_ERR_DIM;
+  iterate_written(ctx);
   PF_CU(perturb_launch(A, lda, E, lde, (int)ctx->n_local, (int)ctx->n, (cudaStream_t)stream));
   return PF_OK;
 }
@@ -915,6 +987,47 @@ pf_status pf_set_tf32_passes(pf_ctx ctx, int32_t passes) {
   ctx->tf_early = passes;
   ctx->tf_tail = 0;
   ctx->tf_rr = passes;
+  return PF_OK;
+}
+
+pf_status pf_set_i8_slices(pf_ctx ctx, int32_t slices) {
+  if (!ctx) return PF_ERR_ARG;
+  if (ctx->dtype != PF_FP64_I8) return PF_ERR_UNSUPPORTED;
+  if (slices != 0 && (slices < 6 || slices > kI8MaxSlices)) return PF_ERR_ARG;
+  if (slices > 0) {
+    ctx->i8plan = i8_plan(ctx->p, (int)ctx->n_local, (int)ctx->n, slices, ctx->num_sms);
+    if (!i8_encode_A(&ctx->mapA8, &ctx->mapA8pf, ctx->A8, ctx->i8plan) ||
+        !i8_encode_B(&ctx->mapY8, ctx->Y8, ctx->i8plan)) {
+      snprintf(ctx->err, sizeof(ctx->err), "cuTensorMapEncodeTiled(int8 slices) failed");
+      return PF_ERR_CUDA;
+    }
+  } else {
+    ctx->i8plan.S = 0;
+  }
+  ctx->a8_valid = false;
+  return PF_OK;
+}
+
+pf_status pf_invalidate(pf_ctx ctx) {
+  if (!ctx) return PF_ERR_ARG;
+  iterate_written(ctx);
+  return PF_OK;
+}
+
+pf_status pf_matmul(pf_ctx ctx, const double* A, int64_t lda, const double* Y, int64_t ldy,
+                    double* out, int64_t ldo, pf_stream stream) {
+  if (!ctx || !A || !Y || !out) return PF_ERR_ARG;
+  if (!is_fp64(ctx)) return PF_ERR_UNSUPPORTED;
+  if (ldy < ctx->p || ldo < ctx->p) return PF_ERR_DIM;
+  PF_TRY(check_A(ctx, A, lda));
+  PF_TRY(map_A(ctx, A, lda));
+  cudaStream_t st = (cudaStream_t)stream;
+  PF_TRY(split_A(ctx, A, lda, true, st));
+  const int p = ctx->p, nl = (int)ctx->n_local;
+  const size_t row = (size_t)p * 8;
+  PF_CU(cudaMemcpy2DAsync(ctx->Y[0], row, Y, ldy * 8, row, nl, cudaMemcpyDeviceToDevice, st));
+  PF_TRY(gemm_step(ctx, 0, ctx->Y[0], ctx->Y[0], ctx->Wbuf, &ctx->state->coef_rr[0], st));
+  PF_CU(cudaMemcpy2DAsync(out, ldo * 8, ctx->Wbuf, row, row, nl, cudaMemcpyDeviceToDevice, st));
   return PF_OK;
 }
 

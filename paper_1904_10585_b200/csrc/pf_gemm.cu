@@ -337,6 +337,22 @@ bool encode_map_f32(CUtensorMap* map, const float* base, int64_t pitch, int rows
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// int8 digit slices [slices][rows][cols] (pitch bytes per row, slice_pitch bytes per slice),
+// SWIZZLE_64B boxes {64 bytes, box_rows, box_slices}; out-of-range K reads as zero digits.
+bool encode_map_i8_3d(CUtensorMap* map, const int8_t* base, int64_t pitch, int64_t slice_pitch,
+                      int cols, int rows, int slices, int box_rows, int box_slices, bool swizzle) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)slices};
+  cuuint64_t strides[2] = {(cuuint64_t)pitch, (cuuint64_t)slice_pitch};
+  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, (cuuint32_t)box_slices};
+  cuuint32_t es[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides, box,
+             es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             swizzle ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // Rank-major all-gather of p-major blocks: [world][p][n_local] contiguous (n_local % 16 == 0).
 bool tf32_encode_B_dist(CUtensorMap* map, const float* Yg, int p, int n_local, int world) {
   PFN_encodeTiled enc = get_encode();

@@ -1,0 +1,632 @@
+// pf_gemm_i8.cu -- the fp64 Chebyshev-step filter GEMM computed from EXACT int8 tensor-core
+// products (dtype PF_FP64_I8; DESIGN.md §4 K1-i8):
+//
+//     out = s1 * (A B) + s2 * Ycur + s3 * Yprev        (eq:cheb, eqn:cheb-linear-map)
+//
+// B200's fp64 tensor pipe (DMMA) peaks at ~37 TF/s while its int8 tensor cores (tcgen05.mma
+// kind::i8, s32 accumulation) run ~4.5 POPS dense.  An fp64 operand is split into S signed 7-bit
+// digits relative to a power-of-two scale (one per row of A, one per column of B):
+//
+//     x = 2^E * sum_{s=1..S} d_s 128^-s  +  r,   d_s = trunc(128 r_{s-1}) in [-127, 127],
+//     |r| < 2^(E - 7S)                                        (r_0 = x 2^-E, r_s = 128 r_{s-1} - d_s)
+//
+// every step exact in fp64.  Then (A B)_ic = 2^(E_i + F_c) sum_l 128^-l D_l[i, c] with the level
+// sums D_l = sum_{s+t=l} A_s B_t (l = 2..S+1; products below level S+1 are dropped, < 2^-7S
+// relative), each an integer matrix product computed EXACTLY by the tensor core in int32 (the
+// K range per accumulation is bounded so that (l-1) K 127^2 < 2^31).  The levels are combined in
+// fp64 in the epilogue, smallest first.  With S = 7 the operator error is ~2^-48 of the row / column
+// scales -- the same order as an fp64 GEMM's own rounding bound (n u |A| |B|).
+//
+// Kernel structure (one CTA per SM, persistent over (128-row tile, column group) items):
+//  * warp 0: TMA producer.  A slices live as [S][n_rows][kpad] int8: each A stage is ONE slice's
+//    128 x 64-byte box (8 KB) -- small stages so the ring is deep (TMA latency), A tagged L2
+//    evict_first.  B = the digit slices of Y stored K-major [S][p][kpad]: one 3-D box
+//    {64 B, NC columns, S slices} per k-block, L2 evict_last (re-read by every tile).
+//  * warp 1 (one lane): MMA issuer, tcgen05.mma.cta_group::1.kind::i8, M = 128.  The S slices of
+//    B sit stacked in shared memory, so A_s times [B_1 .. B_{S+1-s}] is ONE MMA of N = NC (S+1-s)
+//    (split at 256) whose output columns land exactly on the TMEM regions of levels s+1 .. S+1:
+//    TMEM holds S level accumulators of NC int32 columns side by side (S NC <= 512).
+//  * warps 4..7: epilogue, tcgen05.ld of every level, fp64 combination, row / column scales,
+//    the Chebyshev scale-shift-subtract, fp64 stores.  K ranges longer than the int32 bound are
+//    folded into an fp64 workspace (deterministic order).
+#include <algorithm>
+#include <cstdlib>
+
+#include "pf_kernels.cuh"
+#include "pf_tc.cuh"
+
+namespace pf {
+
+namespace i8 {
+
+PF_DEV void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {  // one full warp
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                   smem_u32(dst_smem)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+}
+PF_DEV void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "r"(ncols)
+               : "memory");
+}
+// Instruction descriptor: D s32, A/B signed int8, both K-major, N, M (kind::i8).
+PF_DEV uint32_t idesc_i8(int M, int N) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
+}
+PF_DEV void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                   uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+PF_DEV void mma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+// 32 lanes x 16 consecutive 32-bit columns
+PF_DEV void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+// exact power of two 2^k as a double (|k| <= 1022)
+PF_DEV double pow2(int k) { return __longlong_as_double((long long)(1023 + k) << 52); }
+// scale exponent E of a row / column with max |x| = m: |x| 2^-E < 1 (frexp), 0 for m == 0
+PF_DEV int scale_exp(double m) {
+  if (!(m > 0.0)) return 0;
+  int e;
+  frexp(m, &e);
+  return max(-1000, min(1000, e));
+}
+// S signed base-128 digits of x 2^-E (|x| 2^-E < 1), truncating: d_s = trunc(128 r), r <- 128 r - d_s.
+// Equivalently d_s = sign(x) ((U >> 7(S-s)) & 127) with U = floor(|x| 2^(7S-E)) -- computed here
+// from the fp64 bit pattern with integer shifts only (exact; no fp64 arithmetic).  Returns the S
+// digits as two's-complement bytes, most significant first, in out[s].
+template <int S>
+PF_DEV void digits(double x, int E, uint32_t (&out)[S]) {
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
+  const int be = (int)((bits >> 52) & 0x7ff);
+  unsigned long long m = bits & 0xFFFFFFFFFFFFFull;
+  int ex = -1074;                       // x = m 2^ex (subnormal / zero)
+  if (be != 0) {
+    m |= 1ull << 52;
+    ex = be - 1075;
+  }
+  const int sh = (E - 7 * S) - ex;      // U = m >> sh (m << -sh: S = 8 keeps 56 > 53 bits)
+  const unsigned long long U = (sh >= 64) ? 0ull : (sh >= 0 ? (m >> sh) : (m << (-sh)));
+  const bool neg = (bits >> 63) != 0;
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const uint32_t d = (uint32_t)(U >> (7 * (S - 1 - s))) & 127u;
+    out[s] = (neg ? (0u - d) : d) & 0xffu;
+  }
+}
+
+}  // namespace i8
+
+// ------------------------------------------------------------------------------ A splitting
+// A (n_rows x n_k fp64, lda) -> A8[s][row][kpad] int8 digit slices, rscale[row] = 2^E_row.
+// One CTA per row at a time: pass 1 the row max (HBM), pass 2 re-reads the row (L2) and writes
+// the S slices, 8 digits (8 bytes) per thread per slice.
+template <int S>
+__global__ void __launch_bounds__(512) a_split_kernel(const double* __restrict__ A, int64_t lda,
+                                                      int n_rows, int n_k, int8_t* __restrict__ A8,
+                                                      int64_t kpad, double* __restrict__ rscale) {
+  __shared__ double red[32];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int64_t slice = (int64_t)n_rows * kpad;
+  for (int row = blockIdx.x; row < n_rows; row += gridDim.x) {
+    const double* a = A + (int64_t)row * lda;
+    double m = 0.0;
+    const int n2 = n_k >> 1;
+#pragma unroll 4
+    for (int j = tid; j < n2; j += nt) {
+      const double2 v = reinterpret_cast<const double2*>(a)[j];  // stays in L2 for pass 2
+      m = fmax(m, fmax(fabs(v.x), fabs(v.y)));
+    }
+    if ((n_k & 1) && tid == 0) m = fmax(m, fabs(a[n_k - 1]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    __syncthreads();
+    if ((tid & 31) == 0) red[tid >> 5] = m;
+    __syncthreads();
+    if (tid < 32) {
+      double v = tid < (nt >> 5) ? red[tid] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+      if (tid == 0) red[0] = v;
+    }
+    __syncthreads();
+    const int E = i8::scale_exp(red[0]);
+    if (tid == 0) rscale[row] = i8::pow2(E);
+    int8_t* o = A8 + (int64_t)row * kpad;
+    for (int j0 = tid * 8; j0 < n_k; j0 += nt * 8) {
+      if (j0 + 8 <= n_k) {
+        uint32_t lo[S], hi[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) lo[s] = hi[s] = 0u;
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const double2 v = __ldcs(reinterpret_cast<const double2*>(a + j0) + h);
+          uint32_t d0[S], d1[S];
+          i8::digits<S>(v.x, E, d0);
+          i8::digits<S>(v.y, E, d1);
+#pragma unroll
+          for (int s = 0; s < S; ++s) {
+            const uint32_t pair = d0[s] | (d1[s] << 8);
+            if (h < 2) lo[s] |= pair << (16 * h);
+            else hi[s] |= pair << (16 * (h - 2));
+          }
+        }
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+          __stcs(reinterpret_cast<uint2*>(o + s * slice + j0), make_uint2(lo[s], hi[s]));
+      } else {
+        for (int j = j0; j < n_k; ++j) {
+          uint32_t d[S];
+          i8::digits<S>(a[j], E, d);
+#pragma unroll
+          for (int s = 0; s < S; ++s) o[s * slice + j] = (int8_t)d[s];
+        }
+      }
+    }
+    __syncthreads();  // red[] reuse
+  }
+}
+
+// ------------------------------------------------------------------------------ Y splitting
+// column max of Y (n_k x p row-major, ldy) into cmax[p] (uint64 bit patterns of |y| >= 0: their
+// integer order is the fp64 order).  cmax zeroed before.
+__global__ void y_colmax_kernel(const double* __restrict__ Y, int64_t ldy, int n_k, int p,
+                                unsigned long long* __restrict__ cmax) {
+  __shared__ double sm[256];
+  const int c = threadIdx.x % p, r0 = threadIdx.x / p, rstep = blockDim.x / p;
+  double m = 0.0;
+  for (int r = blockIdx.x * rstep + r0; r < n_k; r += gridDim.x * rstep)
+    m = fmax(m, fabs(Y[(int64_t)r * ldy + c]));
+  sm[threadIdx.x] = m;
+  __syncthreads();
+  if (threadIdx.x < p) {
+    for (int k = 1; k < rstep; ++k) m = fmax(m, sm[k * p + threadIdx.x]);
+    if (m > 0.0) atomicMax(cmax + c, (unsigned long long)__double_as_longlong(m));
+  }
+}
+
+// Y -> Y8[s][c][kpad] (K-major digit slices), cscale[c] = 2^F_c.  One CTA per 64-row chunk:
+// the 64 x p block is staged in shared memory, each thread emits 8 consecutive digits (8 bytes)
+// of one column per slice.
+template <int S>
+__global__ void __launch_bounds__(256) y_split_kernel(const double* __restrict__ Y, int64_t ldy,
+                                                      int n_k, int p,
+                                                      const unsigned long long* __restrict__ cmax,
+                                                      int8_t* __restrict__ Y8, int64_t kpad,
+                                                      double* __restrict__ cscale) {
+  __shared__ double tile[64 * 65];
+  const int k0 = blockIdx.x * 64;
+  for (int cb = 0; cb < p; cb += 64) {
+    const int pc = min(64, p - cb);
+    __syncthreads();
+    for (int i = threadIdx.x; i < 64 * pc; i += blockDim.x) {
+      const int r = i / pc, c = i % pc;
+      tile[r * 65 + c] = (k0 + r < n_k) ? Y[(int64_t)(k0 + r) * ldy + cb + c] : 0.0;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < pc * 8; i += blockDim.x) {
+      const int c = i / 8, g = i % 8;  // column, 8-row group
+      const int E = i8::scale_exp(__longlong_as_double((long long)cmax[cb + c]));
+      if (blockIdx.x == 0 && g == 0) cscale[cb + c] = i8::pow2(E);
+      uint32_t lo[S], hi[S];
+#pragma unroll
+      for (int s = 0; s < S; ++s) lo[s] = hi[s] = 0u;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        uint32_t d[S];
+        i8::digits<S>(tile[(g * 8 + e) * 65 + c], E, d);
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          if (e < 4) lo[s] |= d[s] << (8 * e);
+          else hi[s] |= d[s] << (8 * (e - 4));
+        }
+      }
+      const int k = k0 + g * 8;
+      if (k < n_k) {
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+          *reinterpret_cast<uint2*>(Y8 + ((int64_t)s * p + cb + c) * kpad + k) = make_uint2(lo[s], hi[s]);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------ GEMM
+template <int S, int NC>
+struct I8Cfg {
+  static constexpr int BK = 64;                  // K bytes per k-block (SWIZZLE_64B rows)
+  static constexpr int BM = 128;                 // rows per tile (M of the MMA)
+  static constexpr int A_TILE = BM * BK;         // one slice of one k-block: 8 KB
+  // A_s x [B_0 .. B_{S-1-s}] as few MMAs as possible (N up to 256): with operands that change
+  // from one MMA to the next, an MMA costs ~100 cycles of M-side (A) operand fetch plus ~0.33
+  // cycle per N column (tools/probe/i8_pattern.cu: 1524 cycles per K = 32 step for this
+  // sequence vs 1951 for uniform N = 128 windows and 2866 for one N = 64 MMA per slice pair),
+  // so the fewest A fetches win.
+  static constexpr int CMAX = 256 / NC;          // B slices per MMA
+  static constexpr int B_LOAD = S * NC * BK;     // TMA bytes per B k-block
+  static constexpr int B_STAGE = B_LOAD;
+  static constexpr int NB = B_STAGE <= 8192 ? 4 : 2;  // B comes from L2 (short latency)
+  static constexpr int BUDGET = 216 * 1024;
+  static constexpr int NA0 = (BUDGET - NB * B_STAGE) / A_TILE;
+  static constexpr int NA = NA0 > 24 ? 24 : NA0;
+  static constexpr int COLS = S * NC;            // TMEM columns used (level-major)
+  static constexpr int TMEM_COLS = COLS <= 32 ? 32 : COLS <= 64 ? 64 : COLS <= 128 ? 128
+                                   : COLS <= 256 ? 256 : 512;
+  static constexpr int CW = NC < 32 ? NC : 32;   // epilogue column chunk
+  static constexpr int THREADS = 256;            // w0 TMA, w1 MMA, w2 TMEM alloc, w4..7 epilogue
+  static constexpr int BAR_BYTES = 8 * (2 * NA + 2 * NB + 2) + 16;
+  static constexpr int SMEM = NA * A_TILE + NB * B_STAGE + 1024 + BAR_BYTES;
+  static_assert(COLS <= 512, "TMEM");
+  static_assert(NC % 16 == 0 && NC <= 64, "NC");
+  static_assert(NA >= 6, "A ring");
+  static_assert(SMEM <= 227 * 1024, "smem");
+};
+
+struct I8Args {
+  int pf_dist;           // L2 prefetch distance of the A k-blocks (0: off)
+  const double* ycur;
+  const double* yprev;
+  double* out;
+  int64_t ldy;
+  const double* coef;    // {s1, s2, s3} (device)
+  const double* rscale;  // [n_rows]
+  const double* cscale;  // [p]
+  double* acc;           // fold workspace [grid][NC][128]
+  int n_rows, kblocks, mtiles, ngroups, chunk_kb;
+};
+
+struct RingI {
+  int n, s;
+  uint32_t ph;
+  __device__ RingI(int n_) : n(n_), s(0), ph(0) {}
+  __device__ void next() {
+    if (++s == n) {
+      s = 0;
+      ph ^= 1u;
+    }
+  }
+};
+
+template <int S, int NC>
+__global__ void __launch_bounds__(I8Cfg<S, NC>::THREADS, 1)
+    cheb_gemm_i8_kernel(const __grid_constant__ CUtensorMap mapA8,
+                        const __grid_constant__ CUtensorMap mapY8,
+                        const __grid_constant__ CUtensorMap mapA8pf, I8Args args) {
+  using C = I8Cfg<S, NC>;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  unsigned char* ring_a = smem;                              // NA x [128][64] int8
+  unsigned char* ring_b = smem + C::NA * C::A_TILE;          // NB x [S][NC][64] int8
+  uint64_t* afull = reinterpret_cast<uint64_t*>(ring_b + C::NB * C::B_STAGE);
+  uint64_t* aempty = afull + C::NA;
+  uint64_t* bfull = aempty + C::NA;
+  uint64_t* bempty = bfull + C::NB;
+  uint64_t* tfull = bempty + C::NB;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::NA; ++s) {
+      mbar_init(&afull[s], 1);
+      mbar_init(&aempty[s], 1);
+    }
+    for (int s = 0; s < C::NB; ++s) {
+      mbar_init(&bfull[s], 1);
+      mbar_init(&bempty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 4);
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&mapA8);
+    tma_prefetch_desc(&mapY8);
+    tma_prefetch_desc(&mapA8pf);
+  }
+  if (warp == 2) i8::tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+
+  const int KB = args.kblocks;
+  const int nitems = args.mtiles * args.ngroups;
+  const int kch = args.chunk_kb;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (one lane)
+    if (lane == 0) {
+      RingI ra(C::NA), rb(C::NB);
+      const uint64_t pol_a = tc::policy_evict_first(), pol_b = tc::policy_evict_last();
+      for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+        const int tile = it / args.ngroups, cg = it - tile * args.ngroups;
+        if (args.pf_dist > 0)  // warm the first k-blocks of the tile into L2
+          for (int kb = 0; kb < min(KB, args.pf_dist); ++kb)
+            tc::tma_prefetch_3d(&mapA8pf, kb * C::BK, tile * C::BM, 0, pol_a);
+        for (int kb = 0; kb < KB; ++kb) {
+          // A streams from HBM once: every slice of k-block kb + pf_dist into L2 ahead of its load
+          if (args.pf_dist > 0 && kb + args.pf_dist < KB)
+            tc::tma_prefetch_3d(&mapA8pf, (kb + args.pf_dist) * C::BK, tile * C::BM, 0, pol_a);
+          mbar_wait(&bempty[rb.s], rb.ph ^ 1u);
+          mbar_arrive_expect_tx(&bfull[rb.s], C::B_LOAD);
+          tc::tma_load_3d_hint(ring_b + rb.s * C::B_STAGE, &mapY8, &bfull[rb.s], kb * C::BK,
+                               cg * NC, 0, pol_b);
+          rb.next();
+#pragma unroll 1
+          for (int s = 0; s < S; ++s, ra.next()) {
+            mbar_wait(&aempty[ra.s], ra.ph ^ 1u);
+            mbar_arrive_expect_tx(&afull[ra.s], C::A_TILE);
+            tc::tma_load_3d_hint(ring_a + ra.s * C::A_TILE, &mapA8, &afull[ra.s], kb * C::BK,
+                                 tile * C::BM, s, pol_a);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (one lane)
+    if (lane == 0) {
+      RingI ra(C::NA), rb(C::NB);
+      uint32_t tph = 0;
+      for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+        for (int k0 = 0; k0 < KB; k0 += kch) {
+          const int k1 = min(KB, k0 + kch);
+          mbar_wait(tempty, tph ^ 1u);  // the epilogue drained the accumulators
+          tc::fence_after_sync();
+          for (int kb = k0; kb < k1; ++kb) {
+            mbar_wait(&bfull[rb.s], rb.ph);
+            const uint32_t b0 = smem_u32(ring_b + rb.s * C::B_STAGE);
+#pragma unroll 1
+            for (int s = 0; s < S; ++s, ra.next()) {
+              mbar_wait(&afull[ra.s], ra.ph);
+              tc::fence_after_sync();
+              const uint32_t a0 = smem_u32(ring_a + ra.s * C::A_TILE);
+#pragma unroll
+              for (int ks = 0; ks < 2; ++ks) {
+                const uint32_t acc = (kb == k0 && s == 0 && ks == 0) ? 0u : 1u;
+                const uint64_t ad = tc::sdesc_k_sw64(a0 + ks * 32);
+                // A_s x [B_0 .. B_{S-1-s}] -> levels s .. S-1 (0-based), chunks of <= CMAX slices;
+                // s = 0 initialises every level
+                for (int t0 = 0; t0 < S - s; t0 += C::CMAX) {
+                  const int c = min(C::CMAX, S - s - t0);
+                  i8::mma_i8(tmem + (uint32_t)((s + t0) * NC), ad,
+                             tc::sdesc_k_sw64(b0 + t0 * NC * C::BK + ks * 32),
+                             i8::idesc_i8(C::BM, c * NC), acc);
+                }
+              }
+              i8::mma_commit(&aempty[ra.s]);  // A slice stage free once these MMAs complete
+            }
+            i8::mma_commit(&bempty[rb.s]);
+            rb.next();
+          }
+          i8::mma_commit(tfull);
+          tph ^= 1u;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue (4 warps)
+    const int q = warp & 3;
+    const int et = 32 * q + lane;  // row within the tile = TMEM lane
+    const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16);
+    const double s1 = args.coef[0], s2 = args.coef[1], s3 = args.coef[2];
+    double* accp = args.acc + (size_t)blockIdx.x * (NC * 128) + et;
+    uint32_t tph = 0;
+    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+      const int tile = it / args.ngroups, cg = it - tile * args.ngroups;
+      const int row = tile * C::BM + et;
+      const bool row_ok = row < args.n_rows;
+      const double rs = row_ok ? args.rscale[row] : 0.0;
+      for (int k0 = 0; k0 < KB; k0 += kch) {
+        const bool first = (k0 == 0), last = (k0 + kch >= KB);
+        mbar_wait(tfull, tph);
+        tph ^= 1u;
+        tc::fence_after_sync();
+#pragma unroll 1
+        for (int c0 = 0; c0 < NC; c0 += C::CW) {
+          double v[C::CW];
+#pragma unroll
+          for (int j = 0; j < C::CW; ++j) v[j] = 0.0;
+          // smallest level first: level L (0-based) carries weight 128^-(L+2)
+#pragma unroll 1
+          for (int L = S - 1; L >= 0; --L) {
+            const double w = i8::pow2(-7 * (L + 2));
+#pragma unroll
+            for (int h = 0; h < C::CW; h += 16) {
+              uint32_t r[16];
+              i8::tmem_ld16(taddr + (uint32_t)(L * NC + c0 + h), r);
+#pragma unroll
+              for (int j = 0; j < 16; ++j) v[h + j] = fma((double)(int)r[j], w, v[h + j]);
+            }
+          }
+          if (!first) {
+#pragma unroll
+            for (int j = 0; j < C::CW; ++j) v[j] += __ldcg(accp + (size_t)(c0 + j) * 128);
+          }
+          if (!last) {
+#pragma unroll
+            for (int j = 0; j < C::CW; ++j) __stcg(accp + (size_t)(c0 + j) * 128, v[j]);
+          } else if (row_ok) {
+            const int cbase = cg * NC + c0;
+            const size_t o = (size_t)row * args.ldy + cbase;
+#pragma unroll
+            for (int j = 0; j < C::CW; ++j) {
+              double y = s1 * (v[j] * rs * __ldg(args.cscale + cbase + j));
+              if (s2 != 0.0) y = fma(s2, args.ycur[o + j], y);
+              if (s3 != 0.0) y = fma(s3, args.yprev[o + j], y);
+              args.out[o + j] = y;
+            }
+          }
+        }
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty);
+      }
+    }
+  }
+
+  __syncwarp();
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 2) {
+    tc::fence_after_sync();
+    i8::tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+// ------------------------------------------------------------------------------ host side
+bool encode_map_i8_3d(CUtensorMap* map, const int8_t* base, int64_t pitch, int64_t slice_pitch,
+                      int cols, int rows, int slices, int box_rows, int box_slices,
+                      bool swizzle = true);
+
+I8Plan i8_plan(int p, int n_rows, int n_k, int slices, int num_sms) {
+  I8Plan pl;
+  pl.p = p;
+  pl.S = slices;
+  pl.n_rows = n_rows;
+  pl.n_k = n_k;
+  pl.NC = std::min(p, 64);
+  pl.ngroups = p / pl.NC;
+  pl.mtiles = (n_rows + 127) / 128;
+  pl.kblocks = (n_k + 63) / 64;
+  pl.kpad = ((int64_t)n_k + 15) / 16 * 16;
+  // exact int32 level sums: (S) K 127^2 < 2^31 for the deepest level (S products)
+  const long long kmax = 2147483647LL / ((long long)slices * 127 * 127);
+  pl.chunk_kb = (int)std::max(1LL, kmax / 64);
+  const int items = pl.mtiles * pl.ngroups;
+  pl.grid = std::min(items, num_sms);
+  pl.acc_doubles = (size_t)pl.grid * pl.NC * 128;
+  pl.pf_dist = 0;
+  if (const char* e = getenv("PF_I8_PFDIST")) pl.pf_dist = atoi(e);  // development knob
+  return pl;
+}
+
+bool i8_encode_A(CUtensorMap* map, CUtensorMap* map_pf, const int8_t* A8, const I8Plan& pl) {
+  return encode_map_i8_3d(map, A8, pl.kpad, pl.kpad * pl.n_rows, pl.n_k, pl.n_rows, pl.S, 128, 1) &&
+         encode_map_i8_3d(map_pf, A8, pl.kpad, pl.kpad * pl.n_rows, pl.n_k, pl.n_rows, pl.S, 128,
+                          pl.S, false);
+}
+bool i8_encode_B(CUtensorMap* map, const int8_t* Y8, const I8Plan& pl) {
+  return encode_map_i8_3d(map, Y8, pl.kpad, pl.kpad * pl.p, pl.n_k, pl.p, pl.S, pl.NC, pl.S);
+}
+
+template <int S>
+static cudaError_t a_split_s(const double* A, int64_t lda, const I8Plan& pl, int8_t* A8,
+                             double* rscale, int num_sms, cudaStream_t st) {
+  count_launch();
+  a_split_kernel<S><<<std::min(pl.n_rows, 2 * num_sms), 512, 0, st>>>(A, lda, pl.n_rows, pl.n_k,
+                                                                      A8, pl.kpad, rscale);
+  return cudaGetLastError();
+}
+cudaError_t i8_split_A_launch(const double* A, int64_t lda, const I8Plan& pl, int8_t* A8,
+                              double* rscale, int num_sms, cudaStream_t st) {
+  switch (pl.S) {
+    case 6: return a_split_s<6>(A, lda, pl, A8, rscale, num_sms, st);
+    case 7: return a_split_s<7>(A, lda, pl, A8, rscale, num_sms, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <int S>
+static cudaError_t y_split_s(const double* Y, int64_t ldy, const I8Plan& pl,
+                             unsigned long long* cmax, int8_t* Y8, double* cscale,
+                             int num_sms, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(cmax, 0, sizeof(unsigned long long) * pl.p, st);
+  if (e != cudaSuccess) return e;
+  const int rstep = 256 / pl.p;
+  const int gmax = (pl.n_k + rstep - 1) / rstep;
+  count_launch();
+  y_colmax_kernel<<<std::max(1, std::min(gmax, 2 * num_sms)), 256, 0, st>>>(Y, ldy, pl.n_k, pl.p,
+                                                                              cmax);
+  count_launch();
+  y_split_kernel<S><<<(pl.n_k + 63) / 64, 256, 0, st>>>(Y, ldy, pl.n_k, pl.p, cmax, Y8, pl.kpad,
+                                                         cscale);
+  return cudaGetLastError();
+}
+cudaError_t i8_split_Y_launch(const double* Y, int64_t ldy, const I8Plan& pl,
+                              unsigned long long* cmax, int8_t* Y8, double* cscale, int num_sms,
+                              cudaStream_t st) {
+  switch (pl.S) {
+    case 6: return y_split_s<6>(Y, ldy, pl, cmax, Y8, cscale, num_sms, st);
+    case 7: return y_split_s<7>(Y, ldy, pl, cmax, Y8, cscale, num_sms, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <int S, int NC>
+static cudaError_t i8_launch_t(const I8Plan& pl, const CUtensorMap& mapA8,
+                               const CUtensorMap& mapY8, const CUtensorMap& mapA8pf,
+                               const I8Args& a, cudaStream_t st) {
+  using C = I8Cfg<S, NC>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(cheb_gemm_i8_kernel<S, NC>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  count_launch();
+  cheb_gemm_i8_kernel<S, NC><<<pl.grid, C::THREADS, C::SMEM, st>>>(mapA8, mapY8, mapA8pf, a);
+  return cudaGetLastError();
+}
+
+template <int S>
+static cudaError_t i8_launch_s(const I8Plan& pl, const CUtensorMap& mapA8,
+                               const CUtensorMap& mapY8, const CUtensorMap& mapA8pf,
+                               const I8Args& a, cudaStream_t st) {
+  switch (pl.NC) {
+    case 16: return i8_launch_t<S, 16>(pl, mapA8, mapY8, mapA8pf, a, st);
+    case 32: return i8_launch_t<S, 32>(pl, mapA8, mapY8, mapA8pf, a, st);
+    case 64: return i8_launch_t<S, 64>(pl, mapA8, mapY8, mapA8pf, a, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t i8_gemm_launch(const I8Plan& pl, const CUtensorMap& mapA8, const CUtensorMap& mapY8,
+                           const CUtensorMap& mapA8pf, const double* rscale, const double* cscale, const double* ycur,
+                           const double* yprev, double* out, int64_t ldy, const double* coef,
+                           double* acc, cudaStream_t st) {
+  I8Args a;
+  a.ycur = ycur;
+  a.yprev = yprev;
+  a.out = out;
+  a.ldy = ldy;
+  a.coef = coef;
+  a.rscale = rscale;
+  a.cscale = cscale;
+  a.acc = acc;
+  a.n_rows = pl.n_rows;
+  a.kblocks = pl.kblocks;
+  a.mtiles = pl.mtiles;
+  a.ngroups = pl.ngroups;
+  a.chunk_kb = pl.chunk_kb;
+  a.pf_dist = pl.pf_dist;
+  switch (pl.S) {
+    case 6: return i8_launch_s<6>(pl, mapA8, mapY8, mapA8pf, a, st);
+    case 7: return i8_launch_s<7>(pl, mapA8, mapY8, mapA8pf, a, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace pf

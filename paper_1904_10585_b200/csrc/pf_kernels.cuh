@@ -56,6 +56,32 @@ cudaError_t tf32_gemm_launch(const Tf32Plan& pl, const CUtensorMap& mapA, const 
                              const double* coef, float* ws, float* acc, int* counters,
                              int npass, cudaStream_t st, int bdist_kb = 0);
 
+// ---- fp64 filter GEMM from exact int8 tensor-core products of S-digit splits (pf_gemm_i8.cu).
+// A8: [S][n_rows][kpad] int8 digit slices of A (row scales rscale), Y8: [S][p][kpad] K-major
+// slices of the B block (column scales cscale).
+struct I8Plan {
+  int p, S, NC, ngroups;  // NC = columns per work item (<= 64), ngroups = p / NC
+  int n_rows, n_k;
+  int mtiles, kblocks;    // 128-row tiles, 64-byte k-blocks
+  int64_t kpad;           // slice pitch (bytes), n_k rounded up to 16
+  int chunk_kb;           // k-blocks per exact int32 accumulation
+  int grid;               // persistent CTAs
+  size_t acc_doubles;     // fold workspace
+  int pf_dist;            // L2 prefetch distance of A (k-blocks, 0 = off)
+};
+I8Plan i8_plan(int p, int n_rows, int n_k, int slices, int num_sms);
+bool i8_encode_A(CUtensorMap* map, CUtensorMap* map_pf, const int8_t* A8, const I8Plan& pl);
+bool i8_encode_B(CUtensorMap* map, const int8_t* Y8, const I8Plan& pl);
+cudaError_t i8_split_A_launch(const double* A, int64_t lda, const I8Plan& pl, int8_t* A8,
+                              double* rscale, int num_sms, cudaStream_t st);
+cudaError_t i8_split_Y_launch(const double* Y, int64_t ldy, const I8Plan& pl,
+                              unsigned long long* cmax, int8_t* Y8, double* cscale, int num_sms,
+                              cudaStream_t st);
+cudaError_t i8_gemm_launch(const I8Plan& pl, const CUtensorMap& mapA8, const CUtensorMap& mapY8,
+                           const CUtensorMap& mapA8pf, const double* rscale, const double* cscale, const double* ycur,
+                           const double* yprev, double* out, int64_t ldy, const double* coef,
+                           double* acc, cudaStream_t st);
+
 // ---- fp32-path kernels (pf_f32.cu); blocks fp32 p-major, p x p objects fp64 row-major
 int gram32_slices(int n_rows, int p, int num_sms);
 // G = X Y^T over the n_rows columns of the p-major blocks; partials: nslices * p * p doubles

@@ -104,6 +104,14 @@ PF_DEV void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1, uint64_t pol
       : "memory");
 }
 
+PF_DEV void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.prefetch.tensor.3d.L2.global.tile.L2::cache_hint [%0, {%1, %2, %3}], %4;\n" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(c0), "r"(c1), "r"(c2), "l"(policy)
+      : "memory");
+}
+
 // ------------------------------------------------------------------------------ TMEM
 template <int NCOLS>
 PF_DEV void tmem_alloc_pair(uint32_t* dst_smem) {  // one full warp of EACH CTA of the pair

@@ -13,7 +13,7 @@ import torch
 from pfinputs import (Config, initial_block, lanczos_start, cfg1_problem, cfg1_noise, pfpg_problem,
                       pfam_problem, cfg5_problem, nce_problem, degree_at)
 
-from ._lib import Context, PF_FP64, PF_TF32, PF_OP_PSD, PF_OP_SOFT_THRESHOLD
+from ._lib import Context, PF_FP64, PF_FP64_I8, PF_TF32, PF_OP_PSD, PF_OP_SOFT_THRESHOLD
 
 
 def _dev(x, dtype=torch.float64):
@@ -36,13 +36,24 @@ class Solver:
     A/Z, U, V and of the row-wise masks; small objects are replicated (include/pf.h)."""
 
     def __init__(self, cfg: Config, problem: dict | None = None, stream=None,
-                 nccl_id: bytes | None = None, rank: int = 0, world: int = 1):
+                 nccl_id: bytes | None = None, rank: int = 0, world: int = 1,
+                 graphs: bool = False):
         self.cfg = cfg
+        # CUDA graphs: iterations k >= 1 replay one captured graph of the iteration body
+        # (interval -> filter -> RR -> f -> update); the Lanczos refresh stays an eager launch
+        # in front of it.  Iterations with a host-side change (degree schedule, extrapolation
+        # window) are not graphed.
+        self.graphs = graphs and cfg.deg_c <= 0.0 and not (cfg.mode == "nce" and cfg.accel_l > 0)
+        self._graph = {}
+        self.graph_launches = {}
         n, p, d = cfg.n, cfg.p, cfg.d
         self.stream = stream
+        if self.graphs and (stream is None or stream.cuda_stream == 0):
+            raise ValueError("graphs=True needs a non-default stream (stream capture)")
         self.f32 = cfg.dtype == "tf32"   # fp32 storage, TF32 tensor-core filter (config 5)
         self.ctx = Context(n, p, d, nccl_id=nccl_id, rank=rank, world=world,
-                           dtype=PF_TF32 if self.f32 else PF_FP64)
+                           dtype=PF_TF32 if self.f32 else
+                           PF_FP64_I8 if cfg.dtype == "f64i8" else PF_FP64)
         if self.f32:
             self.ctx.set_tf32_schedule(cfg.tf32_early, cfg.tf32_tail)
         r0, r1 = rows_of(n, rank, world) if nccl_id is not None else (0, n)
@@ -138,6 +149,36 @@ class Solver:
         cfg, ctx, st, k = self.cfg, self.ctx, self.stream, self.k
         if k == 0 or (self.psd and k % cfg.lanczos_every == 0):
             ctx.lanczos(self.A, self.lanczos_vector(k), cfg.lanczos_steps, self.lohi, st)
+        if self.graphs and k >= 1:
+            self._replay()
+        else:
+            self._body(k)
+        # Warm start the next filter from the Ritz vectors: Range(V) = Range(U), so the method
+        # is unchanged (eqn:subspace-update depends on Range(U) only), but the next H = Q^T A Q
+        # is then nearly diagonal and the Jacobi solve converges in one or two sweeps.
+        self.ritz = self.V
+        self.U, self.V = self.V, self.U
+        self.k += 1
+
+    def _replay(self):
+        """Replay the captured body for the current (U, V) buffer pair (two graphs: the pair
+        swaps every iteration); the first use captures it and then replays it."""
+        from ._lib import kernel_launches
+        key = self.U.data_ptr()
+        g = self._graph.get(key)
+        if g is None:
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            l0 = kernel_launches()
+            with torch.cuda.graph(g, stream=self.stream):
+                self._body(1)
+            self.graph_launches[key] = kernel_launches() - l0
+            self._graph[key] = g
+        with torch.cuda.stream(self.stream):
+            g.replay()
+
+    def _body(self, k: int):
+        cfg, ctx, st = self.cfg, self.ctx, self.stream
         if self.psd:
             ctx.interval_psd(self.lohi, cfg.eta, self.interval, st)
         else:
@@ -166,12 +207,6 @@ class Solver:
             else:
                 ctx.nce_step(self.V, self.f, cfg.tau, self.gdiag, self.x, self.x, self.A, self.obj,
                              st)
-        # Warm start the next filter from the Ritz vectors: Range(V) = Range(U), so the method
-        # is unchanged (eqn:subspace-update depends on Range(U) only), but the next H = Q^T A Q
-        # is then nearly diagonal and the Jacobi solve converges in one or two sweeps.
-        self.ritz = self.V
-        self.U, self.V = self.V, self.U
-        self.k += 1
 
     def perturb(self, E: torch.Tensor):
         self.ctx.perturb(self.A, E, self.stream)
@@ -196,10 +231,19 @@ class Solver:
 
 
 def run(cfg: Config, iters: int | None = None, record: bool = True, problem=None,
-        nccl_id: bytes | None = None, rank: int = 0, world: int = 1) -> dict:
+        nccl_id: bytes | None = None, rank: int = 0, world: int = 1, graphs: bool = False) -> dict:
     """Run K iterations on the GPU, recording per-iteration factors (local rows) / objectives."""
     K = cfg.iters if iters is None else iters
-    s = Solver(cfg, problem, nccl_id=nccl_id, rank=rank, world=world)
+    if graphs:                      # capture needs a non-default stream; make it the current one
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            return _run(cfg, K, record, problem, nccl_id, rank, world, st, True)
+    return _run(cfg, K, record, problem, nccl_id, rank, world, None, False)
+
+
+def _run(cfg, K, record, problem, nccl_id, rank, world, stream, graphs):
+    s = Solver(cfg, problem, stream=stream, nccl_id=nccl_id, rank=rank, world=world,
+               graphs=graphs)
     recs = []
     for k in range(K):
         s.step()

@@ -40,7 +40,7 @@ class Config:
     d: int
     iters: int
     mode: str                 # "sweep_psd" | "pfpg" | "pfam" | "sweep_soft"
-    dtype: str = "f64"
+    dtype: str = "f64"        # "f64" | "f64i8" (fp64 via exact int8 products) | "tf32"
     seed: int = 0
     # interval / filter knobs (readings R4-R7)
     eta: float = 0.1

@@ -34,7 +34,8 @@ def test_argument_errors_are_synchronous_without_gpu():
     assert lib.pf_create(100, 24, 4, 0, ctypes.byref(h)) == 2      # p not supported -> DIM
     assert lib.pf_create(10, 16, 4, 0, ctypes.byref(h)) == 2       # n < p -> DIM
     assert lib.pf_create(100, 16, 0, 0, ctypes.byref(h)) == 1      # degree < 1 -> ARG
-    assert lib.pf_create(100, 16, 4, 3, ctypes.byref(h)) == 7      # dtype -> UNSUPPORTED
+    assert lib.pf_create(100, 16, 4, 4, ctypes.byref(h)) == 7      # dtype -> UNSUPPORTED
+    assert lib.pf_create(100, 24, 4, 3, ctypes.byref(h)) == 2      # PF_FP64_I8: fp64's p set
     assert lib.pf_create(100, 16, 4, 1, ctypes.byref(h)) == 7      # PF_FP32 reserved
     # PF_TF32 (config 5): p in {64, 128, 256, 512}
     assert lib.pf_create(1000, 16, 4, 2, ctypes.byref(h)) == 2
@@ -45,6 +46,9 @@ def test_argument_errors_are_synchronous_without_gpu():
     assert lib.pf_create_dist(1000, 64, 4, 2, nid, 0, 1, ctypes.byref(h)) == 2
     assert lib.pf_set_tf32_passes(None, 3) == 1
     assert lib.pf_set_tf32_schedule(None, 1, 3) == 1
+    assert lib.pf_set_i8_slices(None, 7) == 1
+    assert lib.pf_invalidate(None) == 1
+    assert lib.pf_matmul(None, None, 0, None, 0, None, 0, None) == 1
     assert lib.pf_status_string(3) == b"PF_ERR_INTERVAL"
 
 

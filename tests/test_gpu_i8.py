@@ -1,0 +1,136 @@
+"""PF_FP64_I8: the fp64 filter GEMM formed from exact int8 tensor-core products of 7-bit digit
+slices (pf_gemm_i8.cu, DESIGN.md §4 K1-i8).
+
+  * integer operands with few digits: every product is exact on both sides -> bit-equal to numpy;
+  * random fp64 operands with wide per-row / per-column scales, ragged n, zero rows / columns:
+    within the splitting bound K 2^(E_i + F_c) (S + 2) 2^-7S of the exact product;
+  * trajectories of configs 1-3 (reduced) and NCE against the oracle at the fp64 bar (1e-10),
+    and bit-identical CUDA-graph replay."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from pfinputs import CONFIGS, NEXT_CONFIGS, reduced
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a B200")]
+
+
+def _ctx(n, p, slices=7):
+    from paper_1904_10585_b200._lib import Context, PF_FP64_I8
+    c = Context(n, p, 4, dtype=PF_FP64_I8)
+    c.set_i8_slices(slices)
+    return c
+
+
+def _dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def _pitched(A):
+    n = A.shape[1]
+    buf = torch.zeros((A.shape[0], (n + 1) // 2 * 2), dtype=torch.float64, device="cuda")
+    buf[:, :n].copy_(torch.from_numpy(A))
+    return buf[:, :n]
+
+
+@pytest.mark.parametrize("n,p", [(64, 16), (1000, 32), (1333, 64), (700, 128), (16384, 64)])
+def test_integer_operands_exact(n, p):
+    """|a|, |y| < 2^k with few digits: the digit expansion is exact and so is every level sum."""
+    rs = np.random.default_rng(n + p)
+    A = rs.integers(-100, 101, (n, n)).astype(np.float64)
+    A[3] = 0.0                                        # zero row (scale exponent 0)
+    Y = rs.integers(-50, 51, (n, p)).astype(np.float64)
+    Y[:, 1] = 0.0                                     # zero column
+    ref = A @ Y                                       # exact (integers < 2^53)
+    c = _ctx(n, p)
+    out = torch.empty((n, p), dtype=torch.float64, device="cuda")
+    c.matmul(_pitched(A), _dev(Y), out)
+    assert np.array_equal(out.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("slices", [6, 7])
+@pytest.mark.parametrize("n,p", [(1000, 32), (1333, 64), (2049, 128), (300, 16)])
+def test_random_operands_within_split_bound(n, p, slices):
+    rs = np.random.default_rng(7 * n + p)
+    A = rs.standard_normal((n, n)) * np.exp2(rs.integers(-30, 30, n))[:, None]
+    A[:, rs.integers(0, n, 5)] *= 1e6                 # a few large columns (row scales move)
+    Y = rs.standard_normal((n, p)) * np.exp2(rs.integers(-20, 20, p))[None, :]
+    Y[rs.integers(0, n, 3)] *= 1e-9
+    c = _ctx(n, p, slices)
+    out = torch.empty((n, p), dtype=torch.float64, device="cuda")
+    c.matmul(_pitched(A), _dev(Y), out)
+    got = out.cpu().numpy()
+    ref = A @ Y
+    _, ea = np.frexp(np.abs(A).max(axis=1))
+    _, ey = np.frexp(np.abs(Y).max(axis=0))
+    bound = n * np.exp2(ea[:, None] + ey[None, :]) * (slices + 2) * 2.0 ** (-7 * slices)
+    bound += 4 * n * np.finfo(float).eps * (np.abs(A) @ np.abs(Y))   # numpy's own rounding
+    err = np.abs(got - ref)
+    assert (err <= bound).all(), float((err / bound).max())
+
+
+@pytest.mark.parametrize("n,p", [(1333, 64), (4096, 32)])
+def test_gaussian_operands_fp64_grade(n, p):
+    """Operands without wide in-row dynamic range (the iterates of configs 1-4): the S = 7 product
+    is as accurate as the fp64 DMMA GEMM's (same context, pf_set_i8_slices(0))."""
+    rs = np.random.default_rng(n)
+    A = rs.standard_normal((n, n))
+    A = A + A.T
+    Y = rs.standard_normal((n, p))
+    ref = A @ Y
+    c = _ctx(n, p)
+    out = torch.empty((n, p), dtype=torch.float64, device="cuda")
+    c.matmul(_pitched(A), _dev(Y), out)
+    err = np.abs(out.cpu().numpy() - ref).max()
+    c.set_i8_slices(0)
+    c.matmul(_pitched(A), _dev(Y), out)
+    dm = np.abs(out.cpu().numpy() - ref).max()
+    scale = np.abs(A).max() * np.abs(Y).max() * n
+    assert err <= 2.0 ** -47 * scale and err <= 16 * max(dm, 1e-16 * scale), (err, dm)
+
+
+def test_slices_reused_only_while_valid():
+    """pf_rayleigh_ritz / pf_matmul reuse the slices of the same A; pf_invalidate forces a split."""
+    n, p = 512, 32
+    rs = np.random.default_rng(3)
+    A = rs.standard_normal((n, n))
+    Y = rs.standard_normal((n, p))
+    c = _ctx(n, p)
+    Ad = _pitched(A)
+    out = torch.empty((n, p), dtype=torch.float64, device="cuda")
+    c.matmul(Ad, _dev(Y), out)
+    Ad.mul_(2.0)                                        # written outside libpf
+    c.invalidate()
+    c.matmul(Ad, _dev(Y), out)
+    np.testing.assert_allclose(out.cpu().numpy(), 2 * A @ Y, rtol=0, atol=1e-10)
+
+
+CFGS = [reduced(CONFIGS[1], dtype="f64i8"),
+        reduced(CONFIGS[2], n=1000, iters=8, dtype="f64i8"),
+        reduced(CONFIGS[3], n=1500, iters=8, edge_prob=82 / 1500, dtype="f64i8"),
+        reduced(CONFIGS[4], n=1200, p=128, iters=4, dtype="f64i8"),
+        reduced(NEXT_CONFIGS["nce7"], n=600, iters=10, dtype="f64i8")]
+IDS = ["sweep", "pfpg", "pfam", "pfpg_p128", "nce"]
+
+
+@pytest.mark.parametrize("cfg", CFGS, ids=IDS)
+def test_trajectory_matches_oracle(cfg):
+    from paper_1904_10585_b200 import run
+    ref = O.run(cfg)["records"]
+    out = run(cfg)["records"]
+    for x, y in zip(ref, out):
+        den = max(O.lowrank_fro(x["V"], x["f"]), 1e-300)
+        assert O.lowrank_diff_fro(x["V"], x["f"], y["V"], y["f"]) <= 1e-10 * den
+        if "objective" in x:
+            assert y["objective"] == pytest.approx(x["objective"], rel=1e-10)
+
+
+@pytest.mark.parametrize("cfg", CFGS[1:3], ids=IDS[1:3])
+def test_graph_replay_bit_identical(cfg):
+    from paper_1904_10585_b200 import run
+    a = run(cfg)["records"]
+    b = run(cfg, graphs=True)["records"]
+    for x, y in zip(a, b):
+        assert np.array_equal(x["V"], y["V"]) and np.array_equal(x["f"], y["f"])
