@@ -108,11 +108,17 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     cfg = bench_cfg(args.config)
     if world > 1:
         cfg = reduced(cfg, seed=cfg.seed + rank)          # independent replica per rank
+    if args.path == "i8":
+        cfg = reduced(cfg, dtype="f64i8")                 # fp64 via exact int8 products (K1-i8)
     n, p, d = cfg.n, cfg.p, cfg.d
     stream = torch.cuda.Stream()
+    from pfinputs import pfam_problem
+    prob = pfam_problem(cfg)                              # host data, shared with the DMMA leg
     with torch.cuda.stream(stream):
-        s = Solver(cfg, stream=stream)
-        for _ in range(args.warmup):
+        # iterations k >= 1 replay a captured CUDA graph of the iteration body (both buffer
+        # parities are captured during the warm-up, W >= 3)
+        s = Solver(cfg, problem=prob, stream=stream, graphs=True)
+        for _ in range(max(3, args.warmup)):
             s.step()
         # pre-stage the Lanczos start vectors the timed steps will use (host->device, untimed)
         for k in range(s.k, s.k + args.steps):
@@ -126,8 +132,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     time.sleep(0.3)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    s.ctx.profile(True)
     l0 = kernel_launches()
+    r0 = s.replayed_launches
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -137,18 +143,33 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
             s.step()
         e1.record(stream)
     torch.cuda.synchronize()
-    launches = kernel_launches() - l0
+    launches = kernel_launches() - l0 + s.replayed_launches - r0
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)
-    gemm_ms, gemm_n = s.ctx.profile_read(stream)
-    s.ctx.profile(False)
     clk = clocks.stop()
+    # per-launch time of the dominant kernel: the graphs hold no profiling events, so a few eager
+    # steps (the same kernels) run with pf_profile on, after the timed region
+    s.graphs = False
+    s.ctx.profile(True)
+    ep0, ep1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        ep0.record(stream)
+        for _ in range(5):
+            s.step()
+        ep1.record(stream)
+    torch.cuda.synchronize()
+    gemm_ms, gemm_n = s.ctx.profile_read(stream)
+    gemm_share = gemm_ms / ep0.elapsed_time(ep1)
+    s.ctx.profile(False)
+    s.graphs = True
     status = s.ctx.status(stream)
     obj = s.objective()
 
     # ---------------------------------------------------------------- end to end
     e2e = run_e2e(cfg, args, stream)
+    # the same workload on the fp64 DMMA filter GEMM (PF_FP64), for comparison
+    dmma = run_dmma(cfg, prob, args, stream) if args.path == "i8" else None
 
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -169,12 +190,40 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         peak_src = "measured on this pool by tools/probe/peaks.cu (profiles/r01_probe_peaks.log): " \
                    "fp64 DMMA m16n8k4 37.1 TF/s at 1965 MHz; MEASURED_PEAKS.json has no fp64 entry"
     traffic = None
+    tfile = "i8_gemm_traffic.json" if args.path == "i8" else "gemm_traffic.json"
     try:
-        tr = json.load(open(os.path.join(ROOT, "profiles", "gemm_traffic.json")))
+        tr = json.load(open(os.path.join(ROOT, "profiles", tfile)))
         if tr.get("n") == n and tr.get("p") == p:
             traffic = tr["dram_bytes_per_launch"]
     except Exception:
         pass
+    if args.path == "i8":
+        # K1-i8: S = 7 digit slices, S (S + 1) / 2 = 28 exact int8 slice products per Chebyshev
+        # step; peak = measured dense bf16 x 2 (int8 : bf16 = 2 : 1 nominal, B200_PROFILING.md)
+        S = 7
+        ops = 2.0 * n * n * p * S * (S + 1) / 2
+        i8_peak = 2.0 * pk.get("bf16_tflops", 1618.6)
+        roof = {"bound": "tensor", "kernel": "cheb_gemm_i8_kernel<7,64> (tcgen05 kind::i8, exact "
+                "digit products, fp64 level combination)",
+                "achieved": ops / (gemm_avg_ms / 1e3) / 1e12, "peak": i8_peak, "unit": "TOPS",
+                "frac": ops / (gemm_avg_ms / 1e3) / 1e12 / i8_peak, "traffic": traffic,
+                "peak_source": "MEASURED_PEAKS.json bf16_tflops x 2 (nominal int8:bf16); the "
+                               "burst int8 rate measured by tools/probe/mma_i8_rate.cu is "
+                               "16372 ops/clk/SM = 4.76 POPS at 1965 MHz",
+                "algorithmic_per_launch": {"int8_ops": ops, "fp64_flops": flops_gemm,
+                                           "bytes": 7.0 * n * n},
+                "hbm_frac": 7.0 * n * n / (gemm_avg_ms / 1e3) / 1e9 / pk.get("hbm_gbs", 6550.4),
+                "fp64_equivalent_tflops": achieved,
+                "fp64_equivalent_vs_dmma_peak": achieved / fp64_peak,
+                "avg_launch_ms": gemm_avg_ms, "launches": gemm_n, "share_of_step": gemm_share}
+    else:
+        roof = {"bound": "tensor", "kernel": "cheb_gemm_kernel<64> (fp64 DMMA)",
+                "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                "frac": achieved / fp64_peak, "traffic": traffic,
+                "peak_source": peak_src,
+                "algorithmic_per_launch": {"flops": flops_gemm, "bytes": 8.0 * n * n},
+                "avg_launch_ms": gemm_avg_ms, "launches": gemm_n,
+                "share_of_step": gemm_share}
     filter_flops_per_step = 2.0 * d * n * n * p
     cpu = cpu_baseline(cfg, args) if (world == 1 and not args.no_cpu) else None
     out = {
@@ -192,24 +241,53 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         "data": "synthetic (BASELINE configs[2] recipe, DESIGN.md §3)",
         "config": {"workload": f"config 3: PFAM max-cut SDP, n={n}, p={p}, d={d}, G(n,{cfg.edge_prob})",
                    "n": n, "p": p, "d": d, "lanczos_every": cfg.lanczos_every,
+                   "filter_gemm": "fp64 from exact int8 tensor-core products of 7-bit digit "
+                                  "slices (PF_FP64_I8, S=7)" if args.path == "i8" else
+                                  "fp64 DMMA (PF_FP64)",
+                   "cuda_graphs": "iteration body replayed (k >= 1)",
                    "l2": "inputs larger than L2 (2 GiB fp64 iterate re-read every pass)",
                    "parallelism": "replicas" if world > 1 else "1 GPU"},
         "filter_tflops": world * filter_flops_per_step * args.steps / (ms_max / 1e3) / 1e12,
-        "roofline": {"bound": "tensor", "kernel": "cheb_gemm_kernel<64> (fp64 DMMA)",
-                     "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
-                     "frac": achieved / fp64_peak, "traffic": traffic,
-                     "peak_source": peak_src,
-                     "algorithmic_per_launch": {"flops": flops_gemm, "bytes": 8.0 * n * n},
-                     "avg_launch_ms": gemm_avg_ms, "launches": gemm_n,
-                     "share_of_step": gemm_ms / ms},
+        "roofline": roof,
         "clocks": clk,
         "gpu_launches": launches,
         "e2e": e2e,
         "device_status": status["names"],
         "objective_last": obj,
     }
+    if dmma is not None:
+        out["fp64_dmma_path"] = dmma
     if cpu is not None:
         out["cpu_baseline"] = cpu
+    return out
+
+
+def run_dmma(cfg, prob, args, stream) -> dict:
+    """The same timed loop on the fp64 DMMA filter GEMM (dtype PF_FP64), same problem data."""
+    import torch
+    from pfinputs import reduced
+    from paper_1904_10585_b200 import Solver
+    c64 = reduced(cfg, dtype="f64")
+    with torch.cuda.stream(stream):
+        s = Solver(c64, problem=prob, stream=stream, graphs=True)
+        for _ in range(max(3, args.warmup)):
+            s.step()
+        for k in range(s.k, s.k + args.steps):
+            if k % c64.lanczos_every == 0:
+                s.lanczos_vector(k)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(args.steps):
+            s.step()
+        e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    out = {"value": args.steps / (ms / 1e3), "unit": "it/s", "ms_per_step": ms / args.steps,
+           "what": "same workload and timing, filter GEMM on fp64 DMMA (PF_FP64)"}
+    del s
+    torch.cuda.empty_cache()
     return out
 
 
@@ -238,7 +316,7 @@ def run_e2e(cfg, args, stream) -> dict:
         dev = {k: v.cuda(non_blocking=True) for k, v in host.items()}
         h2d += sum(v.numel() * v.element_size() for v in host.values())
         s = Solver(cfg, problem={"adj_bits": None, "deg": None, "t": cfg.t, "_dev": dev},
-                   stream=stream)
+                   stream=stream, graphs=True)
         for k in range(K):
             if k in v0:
                 s._v0[k] = v0[k].cuda(non_blocking=True)
@@ -310,6 +388,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--path", default="i8", choices=["i8", "dmma"],
+                    help="filter GEMM: fp64 via exact int8 products (default) or fp64 DMMA")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -103,6 +103,8 @@ struct pf_ctx_s {
   double* y8_cscale = nullptr;                 // [p]
   unsigned long long* y8_cmax = nullptr;       // [p]
   double* i8_acc = nullptr;
+  double* i8_part = nullptr;                   // stream-K partials
+  int* i8_cnt = nullptr;                       // [items], self-resetting
   CUtensorMap mapA8, mapY8, mapA8pf;
   const double* a8_src = nullptr;              // A whose digit slices A8 holds (pf_filter)
   int64_t a8_lda = 0;
@@ -202,6 +204,9 @@ static pf_status alloc_all(pf_ctx ctx) {
     ok &= A((void**)&ctx->y8_cscale, (size_t)p * 8);
     ok &= A((void**)&ctx->y8_cmax, (size_t)p * 8);
     ok &= A((void**)&ctx->i8_acc, ip.acc_doubles * 8);
+    // sized for the largest plan of any slice count (the split does not depend on S)
+    ok &= A((void**)&ctx->i8_part, ip.part_doubles * 8);
+    ok &= A((void**)&ctx->i8_cnt, (size_t)ip.items * 4);
   }
   if (ctx->dist) {
     ok &= A((void**)&ctx->Yfull, (size_t)n * p * 8);
@@ -264,6 +269,7 @@ static pf_status alloc_all(pf_ctx ctx) {
     snprintf(ctx->err, sizeof(ctx->err), "cuTensorMapEncodeTiled(B) failed");
     return PF_ERR_CUDA;
   }
+  if (ctx->i8) PF_CU(cudaMemset(ctx->i8_cnt, 0, (size_t)ctx->i8plan.items * 4));
   if (ctx->i8 && (!i8_encode_A(&ctx->mapA8, &ctx->mapA8pf, ctx->A8, ctx->i8plan) ||
                   !i8_encode_B(&ctx->mapY8, ctx->Y8, ctx->i8plan))) {
     snprintf(ctx->err, sizeof(ctx->err), "cuTensorMapEncodeTiled(int8 slices) failed");
@@ -393,7 +399,7 @@ pf_status pf_destroy(pf_ctx ctx) {
                   ctx->chol_W, ctx->chol_D,   ctx->jac_H,     ctx->jac_V,   ctx->jac_red,
                   ctx->jac_cnt, ctx->tf_ws,   ctx->tf_cnt,    ctx->tf_acc,  ctx->Yfull32,
                   ctx->A8,     ctx->a8_rscale, ctx->Y8,       ctx->y8_cscale, ctx->y8_cmax,
-                  ctx->i8_acc};
+                  ctx->i8_acc, ctx->i8_part, ctx->i8_cnt};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete ctx;
@@ -506,7 +512,8 @@ static pf_status gemm_step(pf_ctx ctx, int bidx, const double* ycur, const doubl
   if (use_i8(ctx))
     PF_CU(i8_gemm_launch(ctx->i8plan, ctx->mapA8, ctx->mapY8, ctx->mapA8pf, ctx->a8_rscale,
                          ctx->y8_cscale,
-                         ycur, yprev, out, ctx->p, coef, ctx->i8_acc, st));
+                         ycur, yprev, out, ctx->p, coef, ctx->i8_acc, ctx->i8_part, ctx->i8_cnt,
+                         st));
   else
     PF_CU(cheb_gemm_launch(ctx->plan, ctx->mapA, *mb, ycur, yprev, out, coef, ctx->cheb_ws,
                            ctx->cheb_cnt, st));

@@ -4,16 +4,18 @@
 //     out = s1 * (A B) + s2 * Ycur + s3 * Yprev        (eq:cheb, eqn:cheb-linear-map)
 //
 // B200's fp64 tensor pipe (DMMA) peaks at ~37 TF/s while its int8 tensor cores (tcgen05.mma
-// kind::i8, s32 accumulation) run ~4.5 POPS dense.  An fp64 operand is split into S signed 7-bit
-// digits relative to a power-of-two scale (one per row of A, one per column of B):
+// kind::i8, s32 accumulation) run ~4.8 POPS dense (tools/probe/mma_i8_rate.cu: 16.4k int8
+// ops/clk/SM).  An fp64 operand is split into S base-128 digits relative to a power-of-two scale
+// (one per row of A, one per column of B): with V = trunc(x 2^(7S-E)) (exact, |V| < 2^7S),
 //
-//     x = 2^E * sum_{s=1..S} d_s 128^-s  +  r,   d_s = trunc(128 r_{s-1}) in [-127, 127],
-//     |r| < 2^(E - 7S)                                        (r_0 = x 2^-E, r_s = 128 r_{s-1} - d_s)
+//     x = 2^E * sum_{s=1..S} d_s 128^-s  +  r,   |r| < 2^(E - 7S),
+//     V = d_1 128^(S-1) + ... + d_S,  d_1 in [-128, 127], d_s in [0, 127] (s > 1)
 //
-// every step exact in fp64.  Then (A B)_ic = 2^(E_i + F_c) sum_l 128^-l D_l[i, c] with the level
-// sums D_l = sum_{s+t=l} A_s B_t (l = 2..S+1; products below level S+1 are dropped, < 2^-7S
-// relative), each an integer matrix product computed EXACTLY by the tensor core in int32 (the
-// K range per accumulation is bounded so that (l-1) K 127^2 < 2^31).  The levels are combined in
+// (two's-complement floor digits of V, extracted with integer shifts and byte permutes).  Then
+// (A B)_ic = 2^(E_i + F_c) sum_l 128^-l D_l[i, c] with the level sums D_l = sum_{s+t=l} A_s B_t
+// (l = 2..S+1; products below level S+1 are dropped, < 2^-7S relative), each an integer matrix
+// product computed EXACTLY by the tensor core in int32 (the K range per accumulation is bounded so
+// that (l-1) K 128^2 < 2^31).  The levels are combined in
 // fp64 in the epilogue, smallest first.  With S = 7 the operator error is ~2^-48 of the row / column
 // scales -- the same order as an fp64 GEMM's own rounding bound (n u |A| |B|).
 //
@@ -92,12 +94,17 @@ PF_DEV int scale_exp(double m) {
   frexp(m, &e);
   return max(-1000, min(1000, e));
 }
-// S signed base-128 digits of x 2^-E (|x| 2^-E < 1), truncating: d_s = trunc(128 r), r <- 128 r - d_s.
-// Equivalently d_s = sign(x) ((U >> 7(S-s)) & 127) with U = floor(|x| 2^(7S-E)) -- computed here
-// from the fp64 bit pattern with integer shifts only (exact; no fp64 arithmetic).  Returns the S
-// digits as two's-complement bytes, most significant first, in out[s].
+// Digits of x relative to the scale 2^E (|x| < 2^E): U = floor(|x| 2^(7S-E)) (U < 2^7S, exact from
+// the fp64 bit pattern with integer shifts) in base 128, every digit carrying the sign of x:
+// d_s = sign(x) ((U >> 7(S-1-s)) & 127) in [-127, 127], so x = 2^E sum_s d_s 128^-(s+1) + r with
+// |r| < 2^(E-7S) -- the truncating digit expansion d_s = trunc(128 r), r <- 128 r - d_s.
+// Sign-symmetric digits keep the dropped low-order products (levels > S+1) unbiased; floor digits
+// (all low digits >= 0) bias every dropped term the same way, an error growing like K instead of
+// sqrt(K) (measured 1000x larger on Gaussian data).  Packed as bytes:
+// wlo = (d_{S-1}, d_{S-2}, d_{S-3}, d_{S-4}), whi = (d_{S-5}, ..., d_0) (S - 4 bytes).
 template <int S>
-PF_DEV void digits(double x, int E, uint32_t (&out)[S]) {
+PF_DEV void digit_words(double x, int E, uint32_t& wlo, uint32_t& whi) {
+  static_assert(S == 6 || S == 7, "S");
   const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
   const int be = (int)((bits >> 52) & 0x7ff);
   unsigned long long m = bits & 0xFFFFFFFFFFFFFull;
@@ -106,14 +113,48 @@ PF_DEV void digits(double x, int E, uint32_t (&out)[S]) {
     m |= 1ull << 52;
     ex = be - 1075;
   }
-  const int sh = (E - 7 * S) - ex;      // U = m >> sh (m << -sh: S = 8 keeps 56 > 53 bits)
-  const unsigned long long U = (sh >= 64) ? 0ull : (sh >= 0 ? (m >> sh) : (m << (-sh)));
-  const bool neg = (bits >> 63) != 0;
-#pragma unroll
-  for (int s = 0; s < S; ++s) {
-    const uint32_t d = (uint32_t)(U >> (7 * (S - 1 - s))) & 127u;
-    out[s] = (neg ? (0u - d) : d) & 0xffu;
+  const int sh = (E - 7 * S) - ex;      // >= 4 since |x| < 2^E and 7S <= 49
+  const unsigned long long U = (sh >= 64) ? 0ull : (m >> sh);
+  const uint32_t lo = (uint32_t)U & 0x0FFFFFFFu;
+  wlo = (lo & 0x7Fu) | ((lo << 1) & 0x7F00u) | ((lo << 2) & 0x7F0000u) | ((lo << 3) & 0x7F000000u);
+  const uint32_t h = (uint32_t)(U >> 28);
+  whi = (h & 0x7Fu) | ((h << 1) & 0x7F00u) | ((h << 2) & 0x7F0000u);
+  if (bits >> 63) {  // negate every byte (no borrow between bytes)
+    wlo = __vneg4(wlo);
+    whi = __vneg4(whi);
   }
+}
+// 4 x 4 byte transpose: t[b] = (byte b of w0, w1, w2, w3)
+PF_DEV void transpose4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3, uint32_t (&t)[4]) {
+  const uint32_t a = __byte_perm(w0, w1, 0x5140), b = __byte_perm(w2, w3, 0x5140);
+  const uint32_t c = __byte_perm(w0, w1, 0x7362), d = __byte_perm(w2, w3, 0x7362);
+  t[0] = __byte_perm(a, b, 0x5410);
+  t[1] = __byte_perm(a, b, 0x7632);
+  t[2] = __byte_perm(c, d, 0x5410);
+  t[3] = __byte_perm(c, d, 0x7632);
+}
+// digit slices of 4 consecutive values: out[s] = bytes (d_s(x0), d_s(x1), d_s(x2), d_s(x3))
+template <int S>
+PF_DEV void slices4(double x0, double x1, double x2, double x3, int E, uint32_t (&out)[S]) {
+  uint32_t l[4], h[4], tl[4], th[4];
+  digit_words<S>(x0, E, l[0], h[0]);
+  digit_words<S>(x1, E, l[1], h[1]);
+  digit_words<S>(x2, E, l[2], h[2]);
+  digit_words<S>(x3, E, l[3], h[3]);
+  transpose4(l[0], l[1], l[2], l[3], tl);
+  transpose4(h[0], h[1], h[2], h[3], th);
+#pragma unroll
+  for (int b = 0; b < 4; ++b) out[S - 1 - b] = tl[b];
+#pragma unroll
+  for (int b = 0; b < S - 4; ++b) out[S - 5 - b] = th[b];
+}
+// one value's digits (ragged tails)
+template <int S>
+PF_DEV int8_t digit(double x, int E, int s) {
+  uint32_t lo, hi;
+  digit_words<S>(x, E, lo, hi);
+  const uint32_t w = (s >= S - 4) ? (lo >> (8 * (S - 1 - s))) : (hi >> (8 * (S - 5 - s)));
+  return (int8_t)(w & 0xffu);
 }
 
 }  // namespace i8
@@ -156,32 +197,20 @@ __global__ void __launch_bounds__(512) a_split_kernel(const double* __restrict__
     int8_t* o = A8 + (int64_t)row * kpad;
     for (int j0 = tid * 8; j0 < n_k; j0 += nt * 8) {
       if (j0 + 8 <= n_k) {
+        const double2 v0 = __ldcs(reinterpret_cast<const double2*>(a + j0));
+        const double2 v1 = __ldcs(reinterpret_cast<const double2*>(a + j0) + 1);
+        const double2 v2 = __ldcs(reinterpret_cast<const double2*>(a + j0) + 2);
+        const double2 v3 = __ldcs(reinterpret_cast<const double2*>(a + j0) + 3);
         uint32_t lo[S], hi[S];
-#pragma unroll
-        for (int s = 0; s < S; ++s) lo[s] = hi[s] = 0u;
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          const double2 v = __ldcs(reinterpret_cast<const double2*>(a + j0) + h);
-          uint32_t d0[S], d1[S];
-          i8::digits<S>(v.x, E, d0);
-          i8::digits<S>(v.y, E, d1);
-#pragma unroll
-          for (int s = 0; s < S; ++s) {
-            const uint32_t pair = d0[s] | (d1[s] << 8);
-            if (h < 2) lo[s] |= pair << (16 * h);
-            else hi[s] |= pair << (16 * (h - 2));
-          }
-        }
+        i8::slices4<S>(v0.x, v0.y, v1.x, v1.y, E, lo);
+        i8::slices4<S>(v2.x, v2.y, v3.x, v3.y, E, hi);
 #pragma unroll
         for (int s = 0; s < S; ++s)
           __stcs(reinterpret_cast<uint2*>(o + s * slice + j0), make_uint2(lo[s], hi[s]));
       } else {
-        for (int j = j0; j < n_k; ++j) {
-          uint32_t d[S];
-          i8::digits<S>(a[j], E, d);
+        for (int j = j0; j < n_k; ++j)
 #pragma unroll
-          for (int s = 0; s < S; ++s) o[s * slice + j] = (int8_t)d[s];
-        }
+          for (int s = 0; s < S; ++s) o[s * slice + j] = i8::digit<S>(a[j], E, s);
       }
     }
     __syncthreads();  // red[] reuse
@@ -230,18 +259,9 @@ __global__ void __launch_bounds__(256) y_split_kernel(const double* __restrict__
       const int E = i8::scale_exp(__longlong_as_double((long long)cmax[cb + c]));
       if (blockIdx.x == 0 && g == 0) cscale[cb + c] = i8::pow2(E);
       uint32_t lo[S], hi[S];
-#pragma unroll
-      for (int s = 0; s < S; ++s) lo[s] = hi[s] = 0u;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        uint32_t d[S];
-        i8::digits<S>(tile[(g * 8 + e) * 65 + c], E, d);
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-          if (e < 4) lo[s] |= d[s] << (8 * e);
-          else hi[s] |= d[s] << (8 * (e - 4));
-        }
-      }
+      const double* tc0 = tile + (g * 8) * 65 + c;
+      i8::slices4<S>(tc0[0], tc0[65], tc0[130], tc0[195], E, lo);
+      i8::slices4<S>(tc0[260], tc0[325], tc0[390], tc0[455], E, hi);
       const int k = k0 + g * 8;
       if (k < n_k) {
 #pragma unroll
@@ -293,8 +313,38 @@ struct I8Args {
   const double* rscale;  // [n_rows]
   const double* cscale;  // [p]
   double* acc;           // fold workspace [grid][NC][128]
+  double* part;          // stream-K partial tiles [items][maxp][NC][128]
+  int* counters;         // [items], zero between launches
+  int maxp;
   int n_rows, kblocks, mtiles, ngroups, chunk_kb;
 };
+
+// Stream-K work split: the items x kblocks (tile, k-block) units are cut into gridDim.x equal
+// contiguous ranges, so every SM gets the same share of the tensor work; an item cut between
+// CTAs is finished by the last contributor, which sums the fp64 partials in k order.
+struct SegIter {
+  long long u, u1;
+  int KB;
+  __device__ SegIter(long long U, int G, int b, int KB_) : KB(KB_) {
+    u = U * b / G;
+    u1 = U * (b + 1) / G;
+  }
+  __device__ bool next(int& item, int& kb0, int& kb1) {
+    if (u >= u1) return false;
+    item = (int)(u / KB);
+    kb0 = (int)(u - (long long)item * KB);
+    kb1 = (int)min((long long)KB, kb0 + (u1 - u));
+    u += kb1 - kb0;
+    return true;
+  }
+};
+// CTA owning unit u
+__device__ __forceinline__ int seg_owner(long long u, long long U, int G) {
+  int b = (int)(u * G / U);
+  while (b + 1 < G && U * (b + 1) / G <= u) ++b;
+  while (b > 0 && U * b / G > u) --b;
+  return b;
+}
 
 struct RingI {
   int n, s;
@@ -325,6 +375,7 @@ __global__ void __launch_bounds__(I8Cfg<S, NC>::THREADS, 1)
   uint64_t* tfull = bempty + C::NB;
   uint64_t* tempty = tfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  volatile int* sflag = reinterpret_cast<volatile int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -354,20 +405,24 @@ __global__ void __launch_bounds__(I8Cfg<S, NC>::THREADS, 1)
   const int KB = args.kblocks;
   const int nitems = args.mtiles * args.ngroups;
   const int kch = args.chunk_kb;
+  const long long U = (long long)nitems * KB;
+  const int G = gridDim.x;
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (one lane)
     if (lane == 0) {
       RingI ra(C::NA), rb(C::NB);
       const uint64_t pol_a = tc::policy_evict_first(), pol_b = tc::policy_evict_last();
-      for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+      SegIter si(U, G, blockIdx.x, KB);
+      int it, kbs, kbe;
+      while (si.next(it, kbs, kbe)) {
         const int tile = it / args.ngroups, cg = it - tile * args.ngroups;
-        if (args.pf_dist > 0)  // warm the first k-blocks of the tile into L2
-          for (int kb = 0; kb < min(KB, args.pf_dist); ++kb)
+        if (args.pf_dist > 0)  // warm the first k-blocks of the segment into L2
+          for (int kb = kbs; kb < min(kbe, kbs + args.pf_dist); ++kb)
             tc::tma_prefetch_3d(&mapA8pf, kb * C::BK, tile * C::BM, 0, pol_a);
-        for (int kb = 0; kb < KB; ++kb) {
+        for (int kb = kbs; kb < kbe; ++kb) {
           // A streams from HBM once: every slice of k-block kb + pf_dist into L2 ahead of its load
-          if (args.pf_dist > 0 && kb + args.pf_dist < KB)
+          if (args.pf_dist > 0 && kb + args.pf_dist < kbe)
             tc::tma_prefetch_3d(&mapA8pf, (kb + args.pf_dist) * C::BK, tile * C::BM, 0, pol_a);
           mbar_wait(&bempty[rb.s], rb.ph ^ 1u);
           mbar_arrive_expect_tx(&bfull[rb.s], C::B_LOAD);
@@ -389,9 +444,11 @@ __global__ void __launch_bounds__(I8Cfg<S, NC>::THREADS, 1)
     if (lane == 0) {
       RingI ra(C::NA), rb(C::NB);
       uint32_t tph = 0;
-      for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
-        for (int k0 = 0; k0 < KB; k0 += kch) {
-          const int k1 = min(KB, k0 + kch);
+      SegIter si(U, G, blockIdx.x, KB);
+      int it, kbs, kbe;
+      while (si.next(it, kbs, kbe)) {
+        for (int k0 = kbs; k0 < kbe; k0 += kch) {
+          const int k1 = min(kbe, k0 + kch);
           mbar_wait(tempty, tph ^ 1u);  // the epilogue drained the accumulators
           tc::fence_after_sync();
           for (int kb = k0; kb < k1; ++kb) {
@@ -433,13 +490,23 @@ __global__ void __launch_bounds__(I8Cfg<S, NC>::THREADS, 1)
     const double s1 = args.coef[0], s2 = args.coef[1], s3 = args.coef[2];
     double* accp = args.acc + (size_t)blockIdx.x * (NC * 128) + et;
     uint32_t tph = 0;
-    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+    SegIter si(U, G, blockIdx.x, KB);
+    int it, kbs, kbe;
+    while (si.next(it, kbs, kbe)) {
       const int tile = it / args.ngroups, cg = it - tile * args.ngroups;
       const int row = tile * C::BM + et;
       const bool row_ok = row < args.n_rows;
       const double rs = row_ok ? args.rscale[row] : 0.0;
-      for (int k0 = 0; k0 < KB; k0 += kch) {
-        const bool first = (k0 == 0), last = (k0 + kch >= KB);
+      const bool whole = (kbs == 0 && kbe == KB);
+      int part = 0, nparts = 1;
+      if (!whole) {
+        const int f = seg_owner((long long)it * KB, U, G);
+        part = blockIdx.x - f;
+        nparts = seg_owner((long long)it * KB + KB - 1, U, G) - f + 1;
+      }
+      double* mypart = args.part + ((size_t)it * args.maxp + part) * (NC * 128) + et;
+      for (int k0 = kbs; k0 < kbe; k0 += kch) {
+        const bool first = (k0 == kbs), last = (k0 + kch >= kbe);
         mbar_wait(tfull, tph);
         tph ^= 1u;
         tc::fence_after_sync();
@@ -467,6 +534,9 @@ __global__ void __launch_bounds__(I8Cfg<S, NC>::THREADS, 1)
           if (!last) {
 #pragma unroll
             for (int j = 0; j < C::CW; ++j) __stcg(accp + (size_t)(c0 + j) * 128, v[j]);
+          } else if (!whole) {  // partial of a split item
+#pragma unroll
+            for (int j = 0; j < C::CW; ++j) __stcg(mypart + (size_t)(c0 + j) * 128, v[j]);
           } else if (row_ok) {
             const int cbase = cg * NC + c0;
             const size_t o = (size_t)row * args.ldy + cbase;
@@ -482,6 +552,46 @@ __global__ void __launch_bounds__(I8Cfg<S, NC>::THREADS, 1)
         tc::fence_before_sync();
         __syncwarp();
         if (lane == 0) mbar_arrive(tempty);
+      }
+      if (!whole) {
+        // ------------------------------------------------ stream-K fixup (last contributor)
+        __threadfence();
+        named_bar_sync(1, 128);
+        if (et == 0) {
+          const int prev = atomicAdd(&args.counters[it], 1);
+          *sflag = (prev + 1 == nparts) ? 1 : 0;
+        }
+        named_bar_sync(1, 128);
+        const bool lastc = (*sflag != 0);
+        named_bar_sync(1, 128);
+        if (lastc) {
+          __threadfence();
+          const double* p0 = args.part + (size_t)it * args.maxp * (NC * 128) + et;
+#pragma unroll 1
+          for (int c0 = 0; c0 < NC; c0 += C::CW) {
+            double v[C::CW];
+#pragma unroll
+            for (int j = 0; j < C::CW; ++j) v[j] = 0.0;
+#pragma unroll 1
+            for (int q2 = 0; q2 < nparts; ++q2) {
+#pragma unroll
+              for (int j = 0; j < C::CW; ++j)
+                v[j] += __ldcg(p0 + (size_t)q2 * (NC * 128) + (size_t)(c0 + j) * 128);
+            }
+            if (row_ok) {
+              const int cbase = cg * NC + c0;
+              const size_t o = (size_t)row * args.ldy + cbase;
+#pragma unroll
+              for (int j = 0; j < C::CW; ++j) {
+                double y = s1 * (v[j] * rs * __ldg(args.cscale + cbase + j));
+                if (s2 != 0.0) y = fma(s2, args.ycur[o + j], y);
+                if (s3 != 0.0) y = fma(s3, args.yprev[o + j], y);
+                args.out[o + j] = y;
+              }
+            }
+          }
+          if (et == 0) args.counters[it] = 0;  // ready for the next launch
+        }
       }
     }
   }
@@ -511,12 +621,18 @@ I8Plan i8_plan(int p, int n_rows, int n_k, int slices, int num_sms) {
   pl.mtiles = (n_rows + 127) / 128;
   pl.kblocks = (n_k + 63) / 64;
   pl.kpad = ((int64_t)n_k + 15) / 16 * 16;
-  // exact int32 level sums: (S) K 127^2 < 2^31 for the deepest level (S products)
-  const long long kmax = 2147483647LL / ((long long)slices * 127 * 127);
+  // exact int32 level sums: S K 128^2 < 2^31 for the deepest level (S products)
+  const long long kmax = 2147483647LL / ((long long)slices * 128 * 128);  // |d| <= 128
   pl.chunk_kb = (int)std::max(1LL, kmax / 64);
-  const int items = pl.mtiles * pl.ngroups;
-  pl.grid = std::min(items, num_sms);
+  const long long items = (long long)pl.mtiles * pl.ngroups;
+  const long long U = items * pl.kblocks;
+  // stream-K: every SM gets an equal share of the (tile, k-block) units, at least 8 k-blocks
+  pl.grid = (int)std::max(1LL, std::min<long long>(num_sms, U / 8));
+  const long long per = U / pl.grid;  // fewest units a CTA owns
+  pl.maxp = (int)std::min<long long>(pl.grid, (pl.kblocks + per - 1) / per + 1);
+  pl.items = (int)items;
   pl.acc_doubles = (size_t)pl.grid * pl.NC * 128;
+  pl.part_doubles = (size_t)items * pl.maxp * pl.NC * 128;
   pl.pf_dist = 0;
   if (const char* e = getenv("PF_I8_PFDIST")) pl.pf_dist = atoi(e);  // development knob
   return pl;
@@ -606,8 +722,11 @@ static cudaError_t i8_launch_s(const I8Plan& pl, const CUtensorMap& mapA8,
 cudaError_t i8_gemm_launch(const I8Plan& pl, const CUtensorMap& mapA8, const CUtensorMap& mapY8,
                            const CUtensorMap& mapA8pf, const double* rscale, const double* cscale, const double* ycur,
                            const double* yprev, double* out, int64_t ldy, const double* coef,
-                           double* acc, cudaStream_t st) {
+                           double* acc, double* part, int* counters, cudaStream_t st) {
   I8Args a;
+  a.part = part;
+  a.counters = counters;
+  a.maxp = pl.maxp;
   a.ycur = ycur;
   a.yprev = yprev;
   a.out = out;

@@ -68,6 +68,9 @@ struct I8Plan {
   int grid;               // persistent CTAs
   size_t acc_doubles;     // fold workspace
   int pf_dist;            // L2 prefetch distance of A (k-blocks, 0 = off)
+  int items;              // mtiles * ngroups
+  int maxp;               // most CTAs sharing one item (stream-K)
+  size_t part_doubles;    // stream-K partial workspace
 };
 I8Plan i8_plan(int p, int n_rows, int n_k, int slices, int num_sms);
 bool i8_encode_A(CUtensorMap* map, CUtensorMap* map_pf, const int8_t* A8, const I8Plan& pl);
@@ -80,7 +83,7 @@ cudaError_t i8_split_Y_launch(const double* Y, int64_t ldy, const I8Plan& pl,
 cudaError_t i8_gemm_launch(const I8Plan& pl, const CUtensorMap& mapA8, const CUtensorMap& mapY8,
                            const CUtensorMap& mapA8pf, const double* rscale, const double* cscale, const double* ycur,
                            const double* yprev, double* out, int64_t ldy, const double* coef,
-                           double* acc, cudaStream_t st);
+                           double* acc, double* part, int* counters, cudaStream_t st);
 
 // ---- fp32-path kernels (pf_f32.cu); blocks fp32 p-major, p x p objects fp64 row-major
 int gram32_slices(int n_rows, int p, int num_sms);

@@ -46,6 +46,7 @@ class Solver:
         self.graphs = graphs and cfg.deg_c <= 0.0 and not (cfg.mode == "nce" and cfg.accel_l > 0)
         self._graph = {}
         self.graph_launches = {}
+        self.replayed_launches = 0   # kernels launched by graph replays (not seen by the counter)
         n, p, d = cfg.n, cfg.p, cfg.d
         self.stream = stream
         if self.graphs and (stream is None or stream.cuda_stream == 0):
@@ -176,6 +177,7 @@ class Solver:
             self._graph[key] = g
         with torch.cuda.stream(self.stream):
             g.replay()
+        self.replayed_launches += self.graph_launches[key]
 
     def _body(self, k: int):
         cfg, ctx, st = self.cfg, self.ctx, self.stream

@@ -74,6 +74,19 @@ __global__ void pattern(int ksteps, int mode, int sw, long long* out) {
             mma(tmem + ((s + t0) % 4) * 64, ad, sdesc(b0 + t0 * bt + ko, sw), idesc_i8(128, 256));
             ++nmma;
           }
+        } else if (mode == 4) {        // A changes per MMA, B fixed: N = 256
+          mma(tmem + (s % 2) * 256, ad, sdesc(b0 + ko, sw), idesc_i8(128, 256));
+          ++nmma;
+        } else if (mode == 5) {        // A fixed, B window changes: N = 256
+          mma(tmem + (s % 2) * 256, sdesc(a0 + ko, sw), sdesc(b0 + (s % 4) * bt + ko, sw),
+              idesc_i8(128, 256));
+          ++nmma;
+        } else if (mode == 6) {        // both fixed: N = 256
+          mma(tmem + (s % 2) * 256, sdesc(a0 + ko, sw), sdesc(b0 + ko, sw), idesc_i8(128, 256));
+          ++nmma;
+        } else if (mode == 7) {        // A changes, B fixed, same TMEM region
+          mma(tmem, ad, sdesc(b0 + ko, sw), idesc_i8(128, 256));
+          ++nmma;
         } else {
           for (int t = 0; t < S - s; ++t) {
             mma(tmem + (s + t) * 64, ad, sdesc(b0 + t * bt + ko, sw), idesc_i8(128, 64));
@@ -102,9 +115,11 @@ int main() {
   cudaMalloc(&d, sizeof(long long) * 512);
   const int smem = 7 * 16384 + 10 * 8192 + 2048;
   cudaFuncSetAttribute(pattern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  const char* names[4] = {"mixed N (stacked, <=256)", "uniform N=128", "uniform N=256", "N=64 per pair"};
-  for (int sw : {64, 128})
-    for (int mode = 0; mode < 4; ++mode) {
+  const char* names[8] = {"mixed N (stacked, <=256)", "uniform N=128", "uniform N=256", "N=64 per pair",
+                          "A changes, B fixed N=256", "A fixed, B changes N=256", "both fixed N=256",
+                          "A changes, 1 TMEM region"};
+  for (int sw : {64})
+    for (int mode = 0; mode < 8; ++mode) {
       const int grid = 148;
       const int ksteps = 512;
       pattern<<<grid, 128, smem>>>(ksteps, mode, sw, d);
