@@ -788,9 +788,74 @@ __global__ void perturb_hash32_kernel(float* A, int64_t lda, int rows, int cols,
   *a = __fadd_rn(*a, __double2float_rn(e));
 }
 
+__device__ __forceinline__ float hash_noise(unsigned long long i, unsigned long long jj,
+                                            unsigned long long key, double noise) {
+  const unsigned long long lo = i < jj ? i : jj, hi = i < jj ? jj : i;
+  const unsigned long long z1 = mix64(((lo << 32) | hi) ^ key);
+  const unsigned long long z2 = mix64(z1);
+  const double u1 = __dmul_rn((double)((z1 >> 11) + 1ull), 1.1102230246251565e-16);
+  const double u2 = __dmul_rn((double)(z2 >> 11), 1.1102230246251565e-16);
+  // cos(2 pi u2) as cospi(2 u2) (2 u2 exact): no general argument reduction; differs from the
+  // host's cos(fl(2 pi) u2) in the last fp64 bits only, which the fp32 rounding below almost
+  // always absorbs (tests/test_gpu_tf32.py: < 1e-4 of entries differ, by one fp32 ulp)
+  const double g = __dmul_rn(sqrt(__dmul_rn(-2.0, log(u1))), cospi(2.0 * u2));
+  double e = __dmul_rn(noise, g);
+  if (lo != hi) e = __dmul_rn(e, 0.7071067811865476);
+  return __double2float_rn(e);
+}
+
+// Square local block (one GPU): E is symmetric, so each unordered pair's Gaussian is drawn once
+// -- 64 x 64 tile pairs (I <= J): the tile (I, J) is updated directly and its noise, staged in
+// shared memory, is added transposed to tile (J, I) (coalesced both ways).  Same values as the
+// elementwise kernel (hash_noise of the unordered pair), half the transcendental work.
+__global__ void __launch_bounds__(256) perturb_hash32_sym_kernel(float* A, int64_t lda, int n,
+                                                                 unsigned long long key,
+                                                                 double noise) {
+  __shared__ float e[64][65];
+  // tile pair index -> (I, J), I <= J, row-major over the upper triangle of the tile grid
+  // closed form: rows I hold T - I tiles, row I starts at S(I) = I T - I (I - 1) / 2
+  const long long T = (n + 63) / 64;
+  const long long b = blockIdx.x;
+  const double tt = (double)(2 * T + 1);
+  int I = (int)((tt - sqrt(tt * tt - 8.0 * (double)b)) * 0.5);
+  auto start = [&](long long r) { return r * T - r * (r - 1) / 2; };
+  while (I > 0 && start(I) > b) --I;           // guard the floating-point estimate
+  while (start(I + 1) <= b) ++I;
+  const int J = I + (int)(b - start(I));
+  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 64 columns x 4 rows per pass
+  const int j = J * 64 + tx;
+  for (int r = ty; r < 64; r += 4) {
+    const int i = I * 64 + r;
+    float v = 0.f;
+    if (i < n && j < n) {
+      v = hash_noise((unsigned long long)i, (unsigned long long)j, key, noise);
+      float* a = A + (size_t)i * lda + j;
+      *a = __fadd_rn(*a, v);
+    }
+    e[r][tx] = v;
+  }
+  if (I == J) return;  // the diagonal tile held both (i, j) and (j, i)
+  __syncthreads();
+  const int jt = I * 64 + tx;  // column in tile (J, I)
+  for (int r = ty; r < 64; r += 4) {
+    const int i = J * 64 + r;
+    if (i < n && jt < n) {
+      float* a = A + (size_t)i * lda + jt;
+      *a = __fadd_rn(*a, e[tx][r]);
+    }
+  }
+}
+
 cudaError_t perturb_hash32_launch(float* A, int64_t lda, int rows, int cols, int row0,
                                   unsigned long long seed, int k, double noise, cudaStream_t st) {
   const unsigned long long key = mix64(seed * (1ull << 32) + (unsigned long long)k);
+  if (row0 == 0 && rows == cols) {
+    const long long T = (cols + 63) / 64;
+    count_launch();
+    perturb_hash32_sym_kernel<<<(unsigned)(T * (T + 1) / 2), 256, 0, st>>>(A, lda, cols, key,
+                                                                         noise);
+    return cudaGetLastError();
+  }
   dim3 grid(rows, (cols + 255) / 256);
   count_launch();
   perturb_hash32_kernel<<<grid, 256, 0, st>>>(A, lda, rows, cols, row0, key, noise);

@@ -61,6 +61,13 @@ def test_perturb_hash_matches_host_generator():
     assert diff.mean() < 1e-4, diff.sum()
     np.testing.assert_allclose(got, ref, rtol=2 ** -22, atol=0)
     assert (got == got.T).all()
+    # additive on a non-zero iterate, every entry updated exactly once (both triangles of the
+    # symmetric tile-pair kernel), fp32 add rounded to nearest
+    A1 = np.random.default_rng(1).standard_normal((777, 780)).astype(np.float32)
+    dA1 = _f32(A1)
+    ctx.perturb_hash(dA1[:, :777], cfg.seed, 5, cfg.noise)
+    want = (A1[:, :777] + ref).astype(np.float32)
+    assert (dA1.cpu().numpy()[:, :777] != want).mean() < 1e-4
 
 
 # ------------------------------------------------------------------ orthonormalisation
