@@ -5,3 +5,4 @@ legs may import this package.  The product (`paper_1904_10585_b200`) never impor
 shares no code with it; the only common dependency is the seeded input module `pfinputs`.
 """
 from .pf_oracle import *  # noqa: F401,F403
+from .pf_svt import *  # noqa: F401,F403,E402

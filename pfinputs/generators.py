@@ -77,6 +77,13 @@ class Config:
     deg_c: float = 0.0
     nbig: int = 256           # config 5: eigenvalues drawn from U[5, 50]
     nrefl: int = 64           # config 5: Householder reflectors in the basis
+    # PFSVT matrix completion (mode "svt", NEXT-3, paper §5.2 Example eg:MC, tab:SVT-MKL):
+    # m = n, rank r, sampling ratio sr; SVT parameters (reading R24): threshold
+    # svt_tau * sqrt(m n), step svt_delta / sr, stop at ||P_Omega(X - M)|| <= svt_tol ||P_Omega(M)||
+    sr: float = 0.0
+    svt_tau: float = 5.0
+    svt_delta: float = 1.2
+    svt_tol: float = 1e-4
 
 
 CONFIGS = {
@@ -103,6 +110,18 @@ NEXT_CONFIGS = {
     "nce6a": Config("nce_ex56_n2000_accel", n=2000, p=128, d=8, iters=200, mode="nce",
                     nce_example=6, accel_l=5),
 }
+
+
+# NEXT-3: polynomial-filtered SVT on the matrix completion problems of tab:SVT-MKL;
+# d = 1 as in the paper, p = r + guard columns
+NEXT_CONFIGS.update({
+    "svt1k": Config("svt_mc_n1000_sr20_r10", n=1000, p=16, d=1, iters=300, mode="svt", r=10,
+                    sr=0.20),
+    "svt5k": Config("svt_mc_n5000_sr10_r50", n=5000, p=64, d=1, iters=300, mode="svt", r=50,
+                    sr=0.10),
+    "svt10k": Config("svt_mc_n10000_sr15_r50", n=10000, p=64, d=1, iters=300, mode="svt", r=50,
+                     sr=0.15),
+})
 
 
 def config(i: int) -> Config:
@@ -374,6 +393,36 @@ def nce_problem(cfg: Config) -> dict:
     G[(iu[1], iu[0])] = G[iu]
     np.fill_diagonal(G, 1.0)
     return {"G": G}
+
+
+def svt_problem(cfg: Config) -> dict:
+    """Example eg:MC: M = M_L M_R^T with M_L, M_R iid N(0, 1) (n x r), Omega = a
+    uniformly sampled set of round(sr n^2) index pairs (without replacement), b = P_Omega(M).
+    Omega is delivered sorted row-major (CSR order: rows I, columns J, row pointer) plus its
+    column-major view (CSC pointer, rows, and perm: CSC position -> CSR position).  norm2 =
+    ||P_Omega(M)||_2 (ARPACK, setup for the SVT kick k0 = ceil(tau / (delta norm2)), reading R24)."""
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as sla
+    n, r = cfg.n, cfg.r
+    rs = _rng(cfg.seed, 11)
+    ML = rs.standard_normal((n, r))
+    MR = rs.standard_normal((n, r))
+    nnz = int(round(cfg.sr * n * n))
+    lin = np.sort(_rng(cfg.seed, 12).choice(n * n, nnz, replace=False))
+    I = (lin // n).astype(np.int32)
+    J = (lin % n).astype(np.int32)
+    b = np.einsum("ij,ij->i", ML[I], MR[J])
+    row_ptr = np.zeros(n + 1, dtype=np.int32)
+    np.cumsum(np.bincount(I, minlength=n), out=row_ptr[1:])
+    perm = np.lexsort((I, J)).astype(np.int32)        # CSC order: by column, then row
+    col_ptr = np.zeros(n + 1, dtype=np.int32)
+    np.cumsum(np.bincount(J, minlength=n), out=col_ptr[1:])
+    S = sp.csr_matrix((b, J, row_ptr), shape=(n, n))
+    norm2 = float(sla.svds(S, k=1, v0=_rng(cfg.seed, 13).standard_normal(n), tol=1e-12,
+                           return_singular_vectors=False)[0])
+    return {"ML": ML, "MR": MR, "I": I, "J": J, "b": b, "row_ptr": row_ptr, "col_ptr": col_ptr,
+            "perm": perm, "rows_csc": I[perm], "norm2": norm2,
+            "tau": cfg.svt_tau * n, "delta": cfg.svt_delta / cfg.sr}
 
 
 def degree_at(cfg: Config, k: int) -> int:
