@@ -255,6 +255,39 @@ pf_status pf_invalidate(pf_ctx ctx);
 pf_status pf_matmul(pf_ctx ctx, const double* A, int64_t lda, const double* Y, int64_t ldy,
                     double* out, int64_t ldo, pf_stream stream);
 
+/* ---------------------------------------------------------------- PFSVT (NEXT-3, paper §5.2)
+ * Polynomial-filtered SVT for matrix completion (eqn:svt P:1098-1104, Example eg:MC): the dual
+ * iterate Y = A*(x) is an n x n sparse matrix with the values x on the sampled set Omega
+ * (|Omega| = nnz), given in compressed-row form: ptr[n + 1], idx[nnz] (int32, device), values
+ * val[nnz] in the same order.  The CSC view of Omega (column pointer, row indices, and
+ * perm: CSC position -> CSR position) addresses the SAME values for Y^T.  fp64 contexts only
+ * (PF_FP64 / PF_FP64_I8), one GPU (PF_ERR_UNSUPPORTED when distributed); blocks are n x p
+ * row-major; p in {16, 32, 64, 128}. */
+
+/* out = s1 * (S X) + s2 * Ycur + s3 * Yprev with S = (ptr, idx, val[vperm[e] or e]) -- one
+ * Chebyshev step of the filter on Y^T Y is pf_spmm(CSR, X = Y_j) into a temporary T followed by
+ * pf_spmm(CSC with perm, X = T, coefficients of eq:cheb).  Deterministic (each row's nonzeros
+ * in storage order).  Ycur / Yprev may be NULL when their coefficient is 0. */
+pf_status pf_spmm(pf_ctx ctx, const int32_t* ptr, const int32_t* idx, const double* val,
+                  const int32_t* vperm, const double* X, int64_t ldx, double s1, double s2,
+                  double s3, const double* Ycur, int64_t ldc, const double* Yprev, int64_t ldp,
+                  double* out, int64_t ldo, pf_stream stream);
+
+/* Singular triplets of Y on span(Q) (Q orthonormal, n x p): B = Y Q, B^T B = W diag(lambda) W^T
+ * by Jacobi (descending), sigma = sqrt(max(lambda, 0)) (device, p), V = Q W, U = B W / sigma
+ * (columns with sigma = 0 are zero), the shrink s = (sigma - mu)_+ (device, p) and
+ * *svp = #{s > 0} (device int). */
+pf_status pf_svt_ritz(pf_ctx ctx, const int32_t* ptr, const int32_t* idx, const double* val,
+                      const double* Q, int64_t ldq, double mu, double* U, int64_t ldu, double* V,
+                      int64_t ldv, double* sigma, double* s, int32_t* svp, pf_stream stream);
+
+/* SVT dual step on Omega (CSR order): w_e = sum_l U_{i_e l} s_l V_{j_e l} (the sampled entries of
+ * W = U diag(s) V^T), x_e <- x_e + delta (b_e - w_e), *rss = sum_e (b_e - w_e)^2 (device double,
+ * fixed-order reduction). */
+pf_status pf_svt_update(pf_ctx ctx, const int32_t* ptr, const int32_t* idx, const double* b,
+                        double* x, const double* U, int64_t ldu, const double* V, int64_t ldv,
+                        const double* s, double delta, double* rss, pf_stream stream);
+
 #ifdef __cplusplus
 }
 #endif

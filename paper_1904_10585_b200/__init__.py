@@ -7,3 +7,4 @@ is missing.  There is no CPU fallback in this package.
 from ._lib import (Context, PFError, PF_FP64, PF_TF32, PF_OP_PSD, PF_OP_SOFT_THRESHOLD,  # noqa: F401
                    load)
 from .solver import Solver, run  # noqa: F401
+from .svt import SVTSolver, run_svt  # noqa: F401

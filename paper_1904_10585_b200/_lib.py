@@ -62,6 +62,9 @@ def load() -> ctypes.CDLL:
         "pf_set_i8_slices": [P, I32],
         "pf_invalidate": [P],
         "pf_matmul": [P, P, I64, P, I64, P, I64, P],
+        "pf_spmm": [P, P, P, P, P, P, I64, D, D, D, P, I64, P, I64, P, I64, P],
+        "pf_svt_ritz": [P, P, P, P, P, I64, D, P, I64, P, I64, P, P, P, P],
+        "pf_svt_update": [P, P, P, P, P, P, I64, P, I64, P, D, P, P],
         "pf_profile": [P, I32],
         "pf_profile_read": [P, P, ctypes.POINTER(D), ctypes.POINTER(I64)],
         "pf_kernel_launches": [],
@@ -265,6 +268,27 @@ class Context:
         """out = A Y with the context's filter GEMM (fp64 dtypes; local rows)."""
         self._check(self.lib.pf_matmul(self.h, _ptr(A), _ld(A), _ptr(Y), _ld(Y), _ptr(out),
                                        _ld(out), _stream(stream)), "pf_matmul")
+
+    # ---- PFSVT (NEXT-3): sparse operators in compressed-row form (torch int32 / fp64 tensors)
+    def spmm(self, ptr, idx, val, X, out, coef=(1.0, 0.0, 0.0), ycur=None, yprev=None,
+             vperm=None, stream=None):
+        """out = s1 (S X) + s2 ycur + s3 yprev, S = (ptr, idx, val[vperm])."""
+        self._check(self.lib.pf_spmm(
+            self.h, _ptr(ptr), _ptr(idx), _ptr(val), _ptr(vperm), _ptr(X), _ld(X),
+            float(coef[0]), float(coef[1]), float(coef[2]), _ptr(ycur),
+            _ld(ycur) if ycur is not None else 0, _ptr(yprev),
+            _ld(yprev) if yprev is not None else 0, _ptr(out), _ld(out), _stream(stream)),
+            "pf_spmm")
+
+    def svt_ritz(self, ptr, idx, val, Q, mu, U, V, sigma, s, svp, stream=None):
+        self._check(self.lib.pf_svt_ritz(self.h, _ptr(ptr), _ptr(idx), _ptr(val), _ptr(Q), _ld(Q),
+                                         float(mu), _ptr(U), _ld(U), _ptr(V), _ld(V), _ptr(sigma),
+                                         _ptr(s), _ptr(svp), _stream(stream)), "pf_svt_ritz")
+
+    def svt_update(self, ptr, idx, b, x, U, V, s, delta, rss, stream=None):
+        self._check(self.lib.pf_svt_update(self.h, _ptr(ptr), _ptr(idx), _ptr(b), _ptr(x), _ptr(U),
+                                           _ld(U), _ptr(V), _ld(V), _ptr(s), float(delta),
+                                           _ptr(rss), _stream(stream)), "pf_svt_update")
 
     def set_tf32_schedule(self, early_passes: int, exact_tail: int):
         self._check(self.lib.pf_set_tf32_schedule(self.h, early_passes, exact_tail),

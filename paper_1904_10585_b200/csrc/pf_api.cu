@@ -109,6 +109,9 @@ struct pf_ctx_s {
   const double* a8_src = nullptr;              // A whose digit slices A8 holds (pf_filter)
   int64_t a8_lda = 0;
   bool a8_valid = false;                       // cleared by every libpf call that writes A
+  // ---- PFSVT (pf_svt.cu)
+  double* svt_part = nullptr;                  // residual partials (one per 8 rows)
+  int* svt_cnt = nullptr;
   char err[512] = {0};
 };
 
@@ -234,6 +237,10 @@ static pf_status alloc_all(pf_ctx ctx) {
   ok &= A((void**)&ctx->rb_part,
           std::max<size_t>((size_t)rebuild_blocks((int)nl, (int)n) * 2, 128 * 36) * 8);
   ok &= A((void**)&ctx->rb_cnt, 16);
+  if (!f32) {
+    ok &= A((void**)&ctx->svt_part, (size_t)svt_sample_blocks((int)nl) * 8);
+    ok &= A((void**)&ctx->svt_cnt, 16);
+  }
   ok &= A((void**)&ctx->shift_flag, 16);
   if (!ok) {
     snprintf(ctx->err, sizeof(ctx->err), "cudaMalloc of scratch failed");
@@ -244,6 +251,7 @@ static pf_status alloc_all(pf_ctx ctx) {
   else PF_CU(cudaMemset(ctx->cheb_cnt, 0, (size_t)(ctx->plan.mtiles + 1) * 4));
   PF_CU(cudaMemset(ctx->lz_cnt, 0, 16));
   PF_CU(cudaMemset(ctx->rb_cnt, 0, 16));
+  if (!f32) PF_CU(cudaMemset(ctx->svt_cnt, 0, 16));
   PF_CU(cudaMemset(ctx->shift_flag, 0, 16));
   const double rr[3] = {1.0, 0.0, 0.0};
   PF_CU(cudaMemcpy(&ctx->state->coef_rr[0], rr, sizeof(rr), cudaMemcpyHostToDevice));
@@ -399,7 +407,7 @@ pf_status pf_destroy(pf_ctx ctx) {
                   ctx->chol_W, ctx->chol_D,   ctx->jac_H,     ctx->jac_V,   ctx->jac_red,
                   ctx->jac_cnt, ctx->tf_ws,   ctx->tf_cnt,    ctx->tf_acc,  ctx->Yfull32,
                   ctx->A8,     ctx->a8_rscale, ctx->Y8,       ctx->y8_cscale, ctx->y8_cmax,
-                  ctx->i8_acc, ctx->i8_part, ctx->i8_cnt};
+                  ctx->i8_acc, ctx->i8_part, ctx->i8_cnt, ctx->svt_part, ctx->svt_cnt};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete ctx;
@@ -1035,6 +1043,62 @@ pf_status pf_matmul(pf_ctx ctx, const double* A, int64_t lda, const double* Y, i
   PF_CU(cudaMemcpy2DAsync(ctx->Y[0], row, Y, ldy * 8, row, nl, cudaMemcpyDeviceToDevice, st));
   PF_TRY(gemm_step(ctx, 0, ctx->Y[0], ctx->Y[0], ctx->Wbuf, &ctx->state->coef_rr[0], st));
   PF_CU(cudaMemcpy2DAsync(out, ldo * 8, ctx->Wbuf, row, row, nl, cudaMemcpyDeviceToDevice, st));
+  return PF_OK;
+}
+
+// ------------------------------------------------------------------------------ PFSVT (NEXT-3)
+static pf_status svt_check(pf_ctx ctx) {
+  if (!is_fp64(ctx)) return PF_ERR_UNSUPPORTED;
+  if (ctx->dist) return PF_ERR_UNSUPPORTED;  // one GPU: the sampled set is not row-split
+  return PF_OK;
+}
+
+pf_status pf_spmm(pf_ctx ctx, const int32_t* ptr, const int32_t* idx, const double* val,
+                  const int32_t* vperm, const double* X, int64_t ldx, double s1, double s2,
+                  double s3, const double* Ycur, int64_t ldc, const double* Yprev, int64_t ldp,
+                  double* out, int64_t ldo, pf_stream stream) {
+  if (!ctx || !ptr || !idx || !val || !X || !out) return PF_ERR_ARG;
+  PF_TRY(svt_check(ctx));
+  if ((s2 != 0.0 && !Ycur) || (s3 != 0.0 && !Yprev)) return PF_ERR_ARG;
+  const int p = ctx->p;
+  if (ldx < p || ldo < p || (s2 != 0.0 && ldc < p) || (s3 != 0.0 && ldp < p)) return PF_ERR_DIM;
+  const double coef[3] = {s1, s2, s3};
+  PF_CU(spmm_launch((int)ctx->n, p, ptr, idx, val, vperm, X, ldx, coef, Ycur, ldc, Yprev, ldp,
+                    out, ldo, (cudaStream_t)stream));
+  return PF_OK;
+}
+
+pf_status pf_svt_ritz(pf_ctx ctx, const int32_t* ptr, const int32_t* idx, const double* val,
+                      const double* Q, int64_t ldq, double mu, double* U, int64_t ldu, double* V,
+                      int64_t ldv, double* sigma, double* s, int32_t* svp, pf_stream stream) {
+  if (!ctx || !ptr || !idx || !val || !Q || !U || !V || !sigma || !s || !svp) return PF_ERR_ARG;
+  PF_TRY(svt_check(ctx));
+  const int p = ctx->p, n = (int)ctx->n;
+  if (ldq < p || ldu < p || ldv < p) return PF_ERR_DIM;
+  if (!(mu >= 0.0)) return PF_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const double one[3] = {1.0, 0.0, 0.0};
+  PF_CU(spmm_launch(n, p, ptr, idx, val, nullptr, Q, ldq, one, nullptr, 0, nullptr, 0,
+                    ctx->Wbuf, p, st));                                  // B = Y Q
+  PF_CU(gram_launch(ctx->Wbuf, ctx->Wbuf, n, p, ctx->G, ctx->gram_part, nullptr, nullptr, st));
+  PF_CU(jacobi_launch(ctx->G, p, nullptr, sigma, ctx->Yeig, ctx->state,
+                      std::max(1e-15, 1e-16 * p), 40, st));              // B^T B = W L W^T
+  PF_CU(svt_sigma_launch(sigma, p, mu, sigma, s, ctx->Rinv, svp, st));  // sigma, shrink, 1/sigma
+  PF_CU(rmul_launch(Q, ldq, ctx->Yeig, V, ldv, n, p, nullptr, st));      // V = Q W
+  PF_CU(rmul_launch(ctx->Wbuf, p, ctx->Yeig, U, ldu, n, p, nullptr, st));  // U = B W / sigma
+  PF_CU(scale_cols_inplace_launch(U, ldu, n, p, ctx->Rinv, st));
+  return PF_OK;
+}
+
+pf_status pf_svt_update(pf_ctx ctx, const int32_t* ptr, const int32_t* idx, const double* b,
+                        double* x, const double* U, int64_t ldu, const double* V, int64_t ldv,
+                        const double* s, double delta, double* rss, pf_stream stream) {
+  if (!ctx || !ptr || !idx || !b || !x || !U || !V || !s || !rss) return PF_ERR_ARG;
+  PF_TRY(svt_check(ctx));
+  const int p = ctx->p;
+  if (ldu < p || ldv < p) return PF_ERR_DIM;
+  PF_CU(svt_sample_launch((int)ctx->n, p, ptr, idx, b, x, U, ldu, V, ldv, s, delta, ctx->svt_part,
+                          ctx->svt_cnt, rss, (cudaStream_t)stream));
   return PF_OK;
 }
 

@@ -85,6 +85,21 @@ cudaError_t i8_gemm_launch(const I8Plan& pl, const CUtensorMap& mapA8, const CUt
                            const double* yprev, double* out, int64_t ldy, const double* coef,
                            double* acc, double* part, int* counters, cudaStream_t st);
 
+// ---- PFSVT sparse kernels (pf_svt.cu): S n x n in compressed-row form (CSR, or the CSC view)
+cudaError_t spmm_launch(int rows, int p, const int* ptr, const int* idx, const double* val,
+                        const int* vperm, const double* X, int64_t ldx, const double* coef,
+                        const double* ycur, int64_t ldc, const double* yprev, int64_t ldp,
+                        double* out, int64_t ldo, cudaStream_t st);
+int svt_sample_blocks(int rows);
+cudaError_t svt_sample_launch(int rows, int p, const int* ptr, const int* idx, const double* b,
+                              double* x, const double* U, int64_t ldu, const double* V,
+                              int64_t ldv, const double* s, double delta, double* partials,
+                              int* counter, double* obj, cudaStream_t st);
+cudaError_t svt_sigma_launch(const double* lam, int p, double mu, double* sigma, double* s,
+                             double* inv, int* svp, cudaStream_t st);
+cudaError_t scale_cols_inplace_launch(double* X, int64_t ldx, int rows, int p, const double* d,
+                                      cudaStream_t st);
+
 // ---- fp32-path kernels (pf_f32.cu); blocks fp32 p-major, p x p objects fp64 row-major
 int gram32_slices(int n_rows, int p, int num_sms);
 // G = X Y^T over the n_rows columns of the p-major blocks; partials: nslices * p * p doubles

@@ -1,0 +1,115 @@
+"""GPU driver of polynomial-filtered SVT (PFSVT, NEXT-3; paper §5.2, eqn:svt P:1098-1104) over
+the C ABI: sequences pf_spmm (the filter on Y^T Y), pf_orth, pf_svt_ritz and pf_svt_update.
+Python only moves the problem data to the device and computes the host scalars of the interval
+(reading R24); every step of the iteration runs in libpf kernels."""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from pfinputs import Config, initial_block, svt_problem
+
+from ._lib import Context, PF_FP64, PF_FP64_I8
+
+
+def _i32(a) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).cuda()
+
+
+def _f64(a) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+class SVTSolver:
+    """Device state of one PFSVT run: Omega in CSR + CSC views, b, the dual values x, the block Q
+    (n x p) and the factors U, s, V of W^k = shrink_mu(A*(x^{k-1}))."""
+
+    def __init__(self, cfg: Config, problem: dict | None = None, stream=None):
+        assert cfg.mode == "svt"
+        self.cfg, self.stream = cfg, stream
+        prob = svt_problem(cfg) if problem is None else problem
+        self.prob = prob
+        n, p = cfg.n, cfg.p
+        self.ctx = Context(n, p, max(cfg.d, 1), dtype=PF_FP64_I8 if cfg.dtype == "f64i8" else PF_FP64)
+        self.mu, self.delta = float(prob["tau"]), float(prob["delta"])
+        self.row_ptr, self.col = _i32(prob["row_ptr"]), _i32(prob["J"])
+        self.col_ptr, self.row_csc, self.perm = (_i32(prob["col_ptr"]), _i32(prob["rows_csc"]),
+                                                 _i32(prob["perm"]))
+        self.b = _f64(prob["b"])
+        self.nb = float(np.linalg.norm(prob["b"]))
+        # SVT's kick (reading R24): x^0 = k0 delta b, k0 = ceil(mu / (delta ||P_Omega(M)||_2))
+        k0 = math.ceil(self.mu / (self.delta * prob["norm2"]))
+        self.x = _f64(k0 * self.delta * prob["b"])
+        buf = lambda: torch.empty((n, p), dtype=torch.float64, device="cuda")
+        self.blocks = [buf() for _ in range(4)]   # Q, the recurrence, V (roles rotate)
+        self.T, self.U = buf(), buf()
+        self.Q = self.blocks[0]
+        self.Q.copy_(torch.from_numpy(initial_block(cfg)))
+        self.ctx.orth(self.Q, stream)
+        self.sigma = torch.zeros(p, dtype=torch.float64, device="cuda")
+        self.s = torch.zeros(p, dtype=torch.float64, device="cuda")
+        self.svp = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.rss = torch.zeros(1, dtype=torch.float64, device="cuda")
+        self.k = 0
+
+    def _filter(self):
+        """Q <- orth(T_d(L(Y^T Y)) Q), L(t) = (t - c)/e on [a, b] = [0, (1 - eta) mu^2]."""
+        cfg, ctx, st = self.cfg, self.ctx, self.stream
+        a, b = 0.0, (1.0 - cfg.eta) * self.mu * self.mu
+        c, e = 0.5 * (a + b), 0.5 * (b - a)
+        cur, prev = self.Q, None
+        for j in range(cfg.d):
+            ctx.spmm(self.row_ptr, self.col, self.x, cur, self.T, stream=st)        # T = Y Y_j
+            out = next(y for y in self.blocks if y is not cur and y is not prev)
+            if j == 0:
+                ctx.spmm(self.col_ptr, self.row_csc, self.x, self.T, out, (1.0 / e, -c / e, 0.0),
+                         ycur=cur, vperm=self.perm, stream=st)                     # Y^T T ...
+            else:
+                ctx.spmm(self.col_ptr, self.row_csc, self.x, self.T, out,
+                         (2.0 / e, -2.0 * c / e, -1.0), ycur=cur, yprev=prev,
+                         vperm=self.perm, stream=st)
+            prev, cur = cur, out
+        ctx.orth(cur, st)
+        self.Q = cur
+
+    def step(self):
+        cfg, ctx, st = self.cfg, self.ctx, self.stream
+        for _ in range(cfg.warmup if self.k == 0 else 1):
+            self._filter()
+        V = next(y for y in self.blocks if y is not self.Q)
+        ctx.svt_ritz(self.row_ptr, self.col, self.x, self.Q, self.mu, self.U, V, self.sigma,
+                     self.s, self.svp, st)
+        ctx.svt_update(self.row_ptr, self.col, self.b, self.x, self.U, V, self.s, self.delta,
+                       self.rss, st)
+        self.Q = V            # warm start: span(V) = span(Q)
+        self.k += 1
+
+    def residual(self) -> float:
+        """||P_Omega(W^k) - b|| / ||b|| of the last step (host read)."""
+        return math.sqrt(float(self.rss.item())) / self.nb
+
+    def factors(self):
+        """(U, s, V) of W^k on the host, kept columns only (s > 0)."""
+        s = self.s.cpu().numpy()
+        keep = s > 0.0
+        return (self.U.cpu().numpy()[:, keep], s[keep], self.Q.cpu().numpy()[:, keep])
+
+
+def run_svt(cfg: Config, iters: int | None = None, problem=None, stop: bool = False,
+            record: bool = True) -> dict:
+    """K PFSVT iterations on the GPU (or until the relative residual <= cfg.svt_tol)."""
+    s = SVTSolver(cfg, problem)
+    recs = []
+    for k in range(cfg.iters if iters is None else iters):
+        s.step()
+        rec = {"k": k, "res": s.residual(), "svp": int(s.svp.item())}
+        if record:
+            rec["U"], rec["s"], rec["V"] = s.factors()
+            rec["sigma"] = s.sigma.cpu().numpy()
+        recs.append(rec)
+        if stop and rec["res"] <= cfg.svt_tol:
+            break
+    torch.cuda.synchronize()
+    return {"records": recs, "solver": s}
