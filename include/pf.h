@@ -241,6 +241,13 @@ pf_status pf_set_tf32_schedule(pf_ctx ctx, int32_t early_passes, int32_t exact_t
  * context, for comparisons).  PF_ERR_ARG otherwise, PF_ERR_UNSUPPORTED for other dtypes. */
 pf_status pf_set_i8_slices(pf_ctx ctx, int32_t slices);
 
+/* PF_FP64_I8 precision schedule of pf_filter (reading R25): the first degree -
+ * exact_tail Chebyshev steps multiply only the early_slices (4..S) most significant digit slices
+ * (early_slices (early_slices + 1) / 2 products instead of S (S + 1) / 2), the last exact_tail
+ * steps and the Rayleigh-Ritz product use all S.  The early steps' error off the wanted span is
+ * damped by the later steps.  Default: early_slices = S (no schedule). */
+pf_status pf_set_i8_schedule(pf_ctx ctx, int32_t early_slices, int32_t exact_tail);
+
 /* PF_FP64_I8: pf_filter splits A into digit slices on every call; pf_rayleigh_ritz and pf_matmul
  * reuse the slices of the last split of the same A (pointer, lda) unless a libpf call wrote an
  * iterate since (pf_prox_step, pf_admm_step, pf_nce_step, pf_extrapolate, pf_perturb).  A caller

@@ -60,6 +60,7 @@ def load() -> ctypes.CDLL:
         "pf_set_tf32_passes": [P, I32],
         "pf_set_tf32_schedule": [P, I32, I32],
         "pf_set_i8_slices": [P, I32],
+        "pf_set_i8_schedule": [P, I32, I32],
         "pf_invalidate": [P],
         "pf_matmul": [P, P, I64, P, I64, P, I64, P],
         "pf_spmm": [P, P, P, P, P, P, I64, D, D, D, P, I64, P, I64, P, I64, P],
@@ -259,6 +260,11 @@ class Context:
     def set_i8_slices(self, slices: int):
         """PF_FP64_I8: digit slices per operand (6..8), 0 = the fp64 DMMA GEMM."""
         self._check(self.lib.pf_set_i8_slices(self.h, slices), "pf_set_i8_slices")
+
+    def set_i8_schedule(self, early_slices: int, exact_tail: int):
+        """PF_FP64_I8: early Chebyshev steps on early_slices digits, the last exact_tail on S."""
+        self._check(self.lib.pf_set_i8_schedule(self.h, early_slices, exact_tail),
+                    "pf_set_i8_schedule")
 
     def invalidate(self):
         """A was written outside libpf: the next product re-splits it (PF_FP64_I8)."""

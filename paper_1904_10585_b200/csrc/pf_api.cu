@@ -105,7 +105,10 @@ struct pf_ctx_s {
   double* i8_acc = nullptr;
   double* i8_part = nullptr;                   // stream-K partials
   int* i8_cnt = nullptr;                       // [items], self-resetting
-  CUtensorMap mapA8, mapY8, mapA8pf;
+  CUtensorMap mapA8, mapA8pf;
+  CUtensorMap mapY8[4];                        // B boxes of 4..7 digit slices
+  int i8_early = 7;                            // slices of the Chebyshev steps before the tail
+  int i8_tail = 0;                             // final steps (and RR) at the full slice count
   const double* a8_src = nullptr;              // A whose digit slices A8 holds (pf_filter)
   int64_t a8_lda = 0;
   bool a8_valid = false;                       // cleared by every libpf call that writes A
@@ -165,6 +168,13 @@ pf_status pf_nccl_unique_id(void* out, int32_t bytes) {
   if (ncclGetUniqueId(&id) != ncclSuccess) return PF_ERR_NCCL;
   memcpy(out, &id, sizeof(id));
   return PF_OK;
+}
+
+static bool encode_i8_maps(pf_ctx ctx) {
+  if (!i8_encode_A(&ctx->mapA8, &ctx->mapA8pf, ctx->A8, ctx->i8plan)) return false;
+  for (int su = 4; su <= ctx->i8plan.S; ++su)
+    if (!i8_encode_B(&ctx->mapY8[su - 4], ctx->Y8, ctx->i8plan, su)) return false;
+  return true;
 }
 
 static pf_status alloc_all(pf_ctx ctx) {
@@ -278,8 +288,7 @@ static pf_status alloc_all(pf_ctx ctx) {
     return PF_ERR_CUDA;
   }
   if (ctx->i8) PF_CU(cudaMemset(ctx->i8_cnt, 0, (size_t)ctx->i8plan.items * 4));
-  if (ctx->i8 && (!i8_encode_A(&ctx->mapA8, &ctx->mapA8pf, ctx->A8, ctx->i8plan) ||
-                  !i8_encode_B(&ctx->mapY8, ctx->Y8, ctx->i8plan))) {
+  if (ctx->i8 && !encode_i8_maps(ctx)) {
     snprintf(ctx->err, sizeof(ctx->err), "cuTensorMapEncodeTiled(int8 slices) failed");
     return PF_ERR_CUDA;
   }
@@ -500,7 +509,7 @@ static void iterate_written(pf_ctx ctx) { ctx->a8_valid = false; }
 static bool is_fp64(pf_ctx ctx) { return ctx->dtype == PF_FP64 || ctx->dtype == PF_FP64_I8; }
 
 static pf_status gemm_step(pf_ctx ctx, int bidx, const double* ycur, const double* yprev,
-                           double* out, const double* coef, cudaStream_t st) {
+                           double* out, const double* coef, cudaStream_t st, int su = 0) {
   const CUtensorMap* mb;
   const double* bsrc;
   if (!ctx->dist) {
@@ -517,11 +526,13 @@ static pf_status gemm_step(pf_ctx ctx, int bidx, const double* ycur, const doubl
   const bool rec = ctx->prof && ctx->ev_used + 2 <= ctx->ev.size();
   if (ctx->prof && !rec) ++ctx->prof_dropped;
   if (rec) PF_CU(cudaEventRecord(ctx->ev[ctx->ev_used], st));
-  if (use_i8(ctx))
-    PF_CU(i8_gemm_launch(ctx->i8plan, ctx->mapA8, ctx->mapY8, ctx->mapA8pf, ctx->a8_rscale,
-                         ctx->y8_cscale,
-                         ycur, yprev, out, ctx->p, coef, ctx->i8_acc, ctx->i8_part, ctx->i8_cnt,
-                         st));
+  if (use_i8(ctx)) {
+    const int S = ctx->i8plan.S;
+    su = (su <= 0 || su > S) ? S : su;
+    PF_CU(i8_gemm_launch(ctx->i8plan, ctx->mapA8, ctx->mapY8[su - 4], ctx->mapA8pf,
+                         ctx->a8_rscale, ctx->y8_cscale, ycur, yprev, out, ctx->p, coef,
+                         ctx->i8_acc, ctx->i8_part, ctx->i8_cnt, su, st));
+  }
   else
     PF_CU(cheb_gemm_launch(ctx->plan, ctx->mapA, *mb, ycur, yprev, out, coef, ctx->cheb_ws,
                            ctx->cheb_cnt, st));
@@ -819,8 +830,11 @@ pf_status pf_filter(pf_ctx ctx, const void* Av, int64_t lda, void* Uv, int64_t l
     for (int j = 0; j < d; ++j) {
       const int out = (prev < 0) ? (cur + 1) % 3 : 3 - cur - prev;
       const double* coef = &ctx->state->coef[j][0];
+      // PF_FP64_I8 precision schedule (reading R25): the steps before the last i8_tail use
+      // i8_early digit slices; their error off the wanted span is damped by the steps after
+      const int su = (j < d - ctx->i8_tail) ? ctx->i8_early : 0;
       PF_TRY(gemm_step(ctx, cur, ctx->Y[cur], prev < 0 ? ctx->Y[cur] : ctx->Y[prev], ctx->Y[out],
-                       coef, st));
+                       coef, st, su));
       prev = cur;
       cur = out;
       if (j + 1 < d) {
@@ -1011,8 +1025,8 @@ pf_status pf_set_i8_slices(pf_ctx ctx, int32_t slices) {
   if (slices != 0 && (slices < 6 || slices > kI8MaxSlices)) return PF_ERR_ARG;
   if (slices > 0) {
     ctx->i8plan = i8_plan(ctx->p, (int)ctx->n_local, (int)ctx->n, slices, ctx->num_sms);
-    if (!i8_encode_A(&ctx->mapA8, &ctx->mapA8pf, ctx->A8, ctx->i8plan) ||
-        !i8_encode_B(&ctx->mapY8, ctx->Y8, ctx->i8plan)) {
+    ctx->i8_early = std::min(ctx->i8_early, slices);
+    if (!encode_i8_maps(ctx)) {
       snprintf(ctx->err, sizeof(ctx->err), "cuTensorMapEncodeTiled(int8 slices) failed");
       return PF_ERR_CUDA;
     }
@@ -1020,6 +1034,15 @@ pf_status pf_set_i8_slices(pf_ctx ctx, int32_t slices) {
     ctx->i8plan.S = 0;
   }
   ctx->a8_valid = false;
+  return PF_OK;
+}
+
+pf_status pf_set_i8_schedule(pf_ctx ctx, int32_t early_slices, int32_t exact_tail) {
+  if (!ctx) return PF_ERR_ARG;
+  if (ctx->dtype != PF_FP64_I8) return PF_ERR_UNSUPPORTED;
+  if (early_slices < 4 || early_slices > kI8MaxSlices || exact_tail < 0) return PF_ERR_ARG;
+  ctx->i8_early = std::min<int>(early_slices, ctx->i8plan.S > 0 ? ctx->i8plan.S : kI8MaxSlices);
+  ctx->i8_tail = exact_tail;
   return PF_OK;
 }
 

@@ -643,8 +643,8 @@ bool i8_encode_A(CUtensorMap* map, CUtensorMap* map_pf, const int8_t* A8, const 
          encode_map_i8_3d(map_pf, A8, pl.kpad, pl.kpad * pl.n_rows, pl.n_k, pl.n_rows, pl.S, 128,
                           pl.S, false);
 }
-bool i8_encode_B(CUtensorMap* map, const int8_t* Y8, const I8Plan& pl) {
-  return encode_map_i8_3d(map, Y8, pl.kpad, pl.kpad * pl.p, pl.n_k, pl.p, pl.S, pl.NC, pl.S);
+bool i8_encode_B(CUtensorMap* map, const int8_t* Y8, const I8Plan& pl, int su) {
+  return encode_map_i8_3d(map, Y8, pl.kpad, pl.kpad * pl.p, pl.n_k, pl.p, pl.S, pl.NC, su);
 }
 
 template <int S>
@@ -722,7 +722,10 @@ static cudaError_t i8_launch_s(const I8Plan& pl, const CUtensorMap& mapA8,
 cudaError_t i8_gemm_launch(const I8Plan& pl, const CUtensorMap& mapA8, const CUtensorMap& mapY8,
                            const CUtensorMap& mapA8pf, const double* rscale, const double* cscale, const double* ycur,
                            const double* yprev, double* out, int64_t ldy, const double* coef,
-                           double* acc, double* part, int* counters, cudaStream_t st) {
+                           double* acc, double* part, int* counters, int su, cudaStream_t st) {
+  // su <= pl.S: only the su most significant digit slices of both operands are multiplied --
+  // exactly the su-digit expansion (the digits of a longer truncating expansion start with
+  // those of a shorter one), levels 2..su+1; the B map must have a box of su slices
   I8Args a;
   a.part = part;
   a.counters = counters;
@@ -741,7 +744,10 @@ cudaError_t i8_gemm_launch(const I8Plan& pl, const CUtensorMap& mapA8, const CUt
   a.ngroups = pl.ngroups;
   a.chunk_kb = pl.chunk_kb;
   a.pf_dist = pl.pf_dist;
-  switch (pl.S) {
+  if (su < 4 || su > pl.S) return cudaErrorInvalidValue;
+  switch (su) {
+    case 4: return i8_launch_s<4>(pl, mapA8, mapY8, mapA8pf, a, st);
+    case 5: return i8_launch_s<5>(pl, mapA8, mapY8, mapA8pf, a, st);
     case 6: return i8_launch_s<6>(pl, mapA8, mapY8, mapA8pf, a, st);
     case 7: return i8_launch_s<7>(pl, mapA8, mapY8, mapA8pf, a, st);
     default: return cudaErrorInvalidValue;

@@ -74,7 +74,7 @@ struct I8Plan {
 };
 I8Plan i8_plan(int p, int n_rows, int n_k, int slices, int num_sms);
 bool i8_encode_A(CUtensorMap* map, CUtensorMap* map_pf, const int8_t* A8, const I8Plan& pl);
-bool i8_encode_B(CUtensorMap* map, const int8_t* Y8, const I8Plan& pl);
+bool i8_encode_B(CUtensorMap* map, const int8_t* Y8, const I8Plan& pl, int su);  // box: su slices
 cudaError_t i8_split_A_launch(const double* A, int64_t lda, const I8Plan& pl, int8_t* A8,
                               double* rscale, int num_sms, cudaStream_t st);
 cudaError_t i8_split_Y_launch(const double* Y, int64_t ldy, const I8Plan& pl,
@@ -83,7 +83,7 @@ cudaError_t i8_split_Y_launch(const double* Y, int64_t ldy, const I8Plan& pl,
 cudaError_t i8_gemm_launch(const I8Plan& pl, const CUtensorMap& mapA8, const CUtensorMap& mapY8,
                            const CUtensorMap& mapA8pf, const double* rscale, const double* cscale, const double* ycur,
                            const double* yprev, double* out, int64_t ldy, const double* coef,
-                           double* acc, double* part, int* counters, cudaStream_t st);
+                           double* acc, double* part, int* counters, int su, cudaStream_t st);
 
 // ---- PFSVT sparse kernels (pf_svt.cu): S n x n in compressed-row form (CSR, or the CSC view)
 cudaError_t spmm_launch(int rows, int p, const int* ptr, const int* idx, const double* val,

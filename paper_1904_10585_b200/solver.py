@@ -57,6 +57,8 @@ class Solver:
                            PF_FP64_I8 if cfg.dtype == "f64i8" else PF_FP64)
         if self.f32:
             self.ctx.set_tf32_schedule(cfg.tf32_early, cfg.tf32_tail)
+        if cfg.dtype == "f64i8":
+            self.ctx.set_i8_schedule(cfg.i8_early, cfg.i8_tail)
         r0, r1 = rows_of(n, rank, world) if nccl_id is not None else (0, n)
         self.r0, self.r1, self.n_local = r0, r1, r1 - r0
         assert self.n_local == self.ctx.n_local

@@ -65,6 +65,10 @@ class Config:
     # the first d - tf32_tail Chebyshev steps at tf32_early MMA passes, the rest in 3xTF32
     tf32_early: int = 3
     tf32_tail: int = 0
+    # int8-digit fp64 path (dtype "f64i8", reading R25; the oracle ignores it): Chebyshev steps
+    # before the last i8_tail multiply i8_early digit slices, the tail and RR all 7
+    i8_early: int = 7
+    i8_tail: int = 2
     # nearest correlation estimation (mode "nce"): paper Example eg:5.6 (6) or eg:5.7 (7)
     nce_example: int = 7
     # regularized extrapolation of the iterates (§4.3; NEXT-4): window l (0 = off)
