@@ -6,6 +6,8 @@
 //   spectral operator, interval / re-base plan, Lanczos, perturbation helper.
 #include <algorithm>
 
+#include <cstdlib>
+
 #include "pf_kernels.cuh"
 #include "../../include/pf.h"
 
@@ -428,17 +430,22 @@ __global__ void __launch_bounds__(JacCfg<PE>::THREADS) jacobi_kernel(
       int* pi = pi2 + (r & 1) * C::HALF;
       int* pj = pj2 + (r & 1) * C::HALF;
       if (r > 0 && tid >= 32) {
+        // V is stored transposed (row i of the buffer = column i of V): the rotation of columns
+        // i, j is two contiguous rows, one warp per pair, c / s broadcast, no bank conflicts
         const double* csp = cs2 + ((r - 1) & 1) * 3 * C::HALF;
         const int* pip = pi2 + ((r - 1) & 1) * C::HALF;
         const int* pjp = pj2 + ((r - 1) & 1) * C::HALF;
-        for (int e = tid - 32; e < PE * C::HALF; e += NT - 32) {
-          const int row = e / C::HALF, m = e % C::HALF;
+        const int lane = tid & 31;
+        for (int m = (tid >> 5) - 1; m < C::HALF; m += NT / 32 - 1) {
           const double c = csp[3 * m], s = csp[3 * m + 1];
           if (s != 0.0) {
-            const int i = pip[m], j = pjp[m];
-            const double vi = V[row * PE + i], vj = V[row * PE + j];
-            V[row * PE + i] = c * vi - s * vj;
-            V[row * PE + j] = s * vi + c * vj;
+            double* vi = V + pip[m] * PE;
+            double* vj = V + pjp[m] * PE;
+            for (int k = lane; k < PE; k += 32) {
+              const double a = vi[k], b = vj[k];
+              vi[k] = c * a - s * b;
+              vj[k] = s * a + c * b;
+            }
           }
         }
       }
@@ -545,8 +552,178 @@ __global__ void __launch_bounds__(JacCfg<PE>::THREADS) jacobi_kernel(
       if (lk > li || (lk == li && k < i)) ++rank;
     }
     theta[rank] = li;
-    for (int row = 0; row < p; ++row) Yout[row * p + rank] = V[row * PE + i];
+    for (int row = 0; row < p; ++row) Yout[row * p + rank] = V[i * PE + row];  // V transposed
   }
+}
+
+// Row-owner variant for PE <= 64 (the same two-sided cyclic Jacobi, same rotations and ordering):
+// full H and V^T in shared memory, warp a owns the rows i_a, j_a of its pair in round r.  Phase 1:
+// lane 0 of warp a computes rotation a from its own rows.  Phase 2: lane b of warp a forms block
+// (a, b) of J^T H J -- rows i_a, j_a only, so every warp writes only rows it owns (in place, no
+// mirror stores, conflict-light row accesses) -- and warp a rotates its two rows of V^T.  Each
+// block entry is summed as (P11 b11 + P22 b22) + (P12 b12 + P21 b21) with P = products of the
+// rotation entries and no contraction, which is exactly symmetric under (a, b) -> (b, a), so H
+// stays bit-symmetric.  Two barriers per round.
+template <int PE>
+__global__ void __launch_bounds__(PE * 16) jacobi_rows_kernel(
+    const double* __restrict__ H, int p_static, const int* p_dev, double* __restrict__ theta,
+    double* __restrict__ Yout, DevState* state, double tol, int max_sweeps) {
+  constexpr int HALF = PE / 2, NT = PE * 16;  // HALF warps
+  extern __shared__ double js[];
+  __shared__ double red[32];
+  __shared__ int s_any;
+  __shared__ double s_norm;
+  const int p = p_dev ? *p_dev : p_static;
+  if (p <= 0) return;
+  double* Hs = js;                   // PE x PE, both triangles
+  double* Vt = Hs + PE * PE;         // V transposed
+  double* rc = Vt + PE * PE;         // [HALF] c
+  double* rs = rc + HALF;            // [HALF] s
+  double* rt = rs + HALF;            // [HALF] t
+  int* ri = reinterpret_cast<int*>(rt + HALF);
+  int* rj = ri + HALF;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int e = tid; e < PE * PE; e += NT) {
+    const int i = e / PE, j = e % PE;
+    Vt[e] = (i == j) ? 1.0 : 0.0;
+    Hs[e] = (i < p && j < p) ? 0.5 * (H[i * p + j] + H[j * p + i]) : 0.0;
+  }
+  __syncthreads();
+  int sweep = 0;
+  bool converged = false;
+  for (; sweep < max_sweeps; ++sweep) {
+    double off = 0.0, tot = 0.0;
+    for (int e = tid; e < PE * PE; e += NT) {
+      const double v = Hs[e];
+      tot += v * v;
+      if (e / PE != e % PE) off += v * v;
+    }
+    off = block_sum(off, red);
+    tot = block_sum(tot, red);
+    if (off <= tol * tol * tot || off == 0.0) {
+      converged = true;
+      break;
+    }
+    if (tid == 0) {
+      s_any = 0;
+      s_norm = sqrt(tot);
+    }
+    __syncthreads();
+    for (int r = 0; r < PE - 1; ++r) {
+      const int m = warp;  // this warp's pair
+      int a0, b0;
+      if (m == 0) {
+        a0 = PE - 1;
+        b0 = r;
+      } else {
+        a0 = (r + m) % (PE - 1);
+        b0 = (r - m + (PE - 1)) % (PE - 1);
+      }
+      const int ia = a0 < b0 ? a0 : b0, ja = a0 < b0 ? b0 : a0;
+      if (lane == 0) {
+        double c = 1.0, s = 0.0, t = 0.0;
+        if (ja < p) {
+          const double hij = Hs[ia * PE + ja];
+          if (fabs(hij) > 1e-16 * s_norm) {  // same threshold and schur2 as jacobi_kernel
+            const double hii = Hs[ia * PE + ia], hjj = Hs[ja * PE + ja];
+            const double dd = hjj - hii, ee = 2.0 * hij;
+            const double ir = rsqrt(dd * dd + ee * ee);
+            const double hh = 0.5 + 0.5 * fabs(dd) * ir;
+            const double rcp = rsqrt(hh);
+            c = hh * rcp;
+            s = (dd >= 0.0 ? 0.5 : -0.5) * ee * ir * rcp;
+            t = s * rcp;
+            s_any = 1;
+          }
+        }
+        rc[m] = c;
+        rs[m] = s;
+        rt[m] = t;
+        ri[m] = ia;
+        rj[m] = ja;
+      }
+      __syncthreads();
+      const double ca = rc[m], sa = rs[m];
+      for (int bb = lane; bb < HALF; bb += 32) {
+        const double cb = rc[bb], sb = rs[bb];
+        if (sa == 0.0 && sb == 0.0) continue;
+        const int ib = ri[bb], jb = rj[bb];
+        if (bb == m) {
+          const double ta = rt[m];
+          const double hij = Hs[ia * PE + ja];
+          Hs[ia * PE + ia] -= ta * hij;
+          Hs[ja * PE + ja] += ta * hij;
+          Hs[ia * PE + ja] = 0.0;
+          Hs[ja * PE + ia] = 0.0;
+        } else {
+          const double b11 = Hs[ia * PE + ib], b12 = Hs[ia * PE + jb];
+          const double b21 = Hs[ja * PE + ib], b22 = Hs[ja * PE + jb];
+          // J_a = [[ca, sa], [-sa, ca]] on (ia, ja), J_b likewise; n = J_a^T B J_b
+          const double pcc = __dmul_rn(ca, cb), pcs = __dmul_rn(ca, sb);
+          const double psc = __dmul_rn(sa, cb), pss = __dmul_rn(sa, sb);
+          // n11 = cc b11 - cs b12 - sc b21 + ss b22; n12 = cs b11 + cc b12 - ss b21 - sc b22
+          // n21 = sc b11 - ss b12 + cc b21 - cs b22; n22 = ss b11 + sc b12 + cs b21 + cc b22
+          const double n11 = __dadd_rn(__dadd_rn(__dmul_rn(pcc, b11), __dmul_rn(pss, b22)),
+                                       -__dadd_rn(__dmul_rn(pcs, b12), __dmul_rn(psc, b21)));
+          const double n22 = __dadd_rn(__dadd_rn(__dmul_rn(pss, b11), __dmul_rn(pcc, b22)),
+                                       __dadd_rn(__dmul_rn(psc, b12), __dmul_rn(pcs, b21)));
+          const double n12 = __dadd_rn(__dadd_rn(__dmul_rn(pcs, b11), -__dmul_rn(psc, b22)),
+                                       __dadd_rn(__dmul_rn(pcc, b12), -__dmul_rn(pss, b21)));
+          const double n21 = __dadd_rn(__dadd_rn(__dmul_rn(psc, b11), -__dmul_rn(pcs, b22)),
+                                       __dadd_rn(__dmul_rn(pcc, b21), -__dmul_rn(pss, b12)));
+          Hs[ia * PE + ib] = n11;
+          Hs[ia * PE + jb] = n12;
+          Hs[ja * PE + ib] = n21;
+          Hs[ja * PE + jb] = n22;
+        }
+      }
+      if (sa != 0.0) {  // columns ia, ja of V = rows of V^T
+        double* vi = Vt + ia * PE;
+        double* vj = Vt + ja * PE;
+        for (int k = lane; k < PE; k += 32) {
+          const double x = vi[k], y = vj[k];
+          vi[k] = ca * x - sa * y;
+          vj[k] = sa * x + ca * y;
+        }
+      }
+      __syncthreads();
+    }
+    if (s_any == 0) {
+      converged = true;
+      ++sweep;
+      break;
+    }
+  }
+  if (tid == 0) {
+    state->scratch[1] = (double)sweep;
+    if (!converged) atomicOr(&state->flags, PF_FLAG_JACOBI_MAXSWEEP);
+  }
+  for (int i = tid; i < p; i += NT) {  // sort descending (stable by index) and emit
+    const double li = Hs[i * PE + i];
+    int rank = 0;
+    for (int k = 0; k < p; ++k) {
+      const double lk = Hs[k * PE + k];
+      if (lk > li || (lk == li && k < i)) ++rank;
+    }
+    theta[rank] = li;
+    for (int row = 0; row < p; ++row) Yout[row * p + rank] = Vt[i * PE + row];
+  }
+}
+
+template <int PE>
+static cudaError_t jacobi_rows_pe(const double* H, int p, const int* p_dev, double* theta,
+                                  double* Y, DevState* state, double tol, int max_sweeps,
+                                  cudaStream_t st) {
+  constexpr size_t SMEM = (size_t)(2 * PE * PE + 3 * (PE / 2)) * 8 + (PE / 2) * 8;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(jacobi_rows_kernel<PE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)SMEM);
+    attr = true;
+  }
+  count_launch();
+  jacobi_rows_kernel<PE><<<1, PE * 16, SMEM, st>>>(H, p, p_dev, theta, Y, state, tol, max_sweeps);
+  return cudaGetLastError();
 }
 
 template <int PE>
@@ -567,6 +744,14 @@ static cudaError_t jacobi_pe(const double* H, int p, const int* p_dev, double* t
 // p: order (runtime bound when p_dev != NULL: the kernel reads *p_dev <= p)
 cudaError_t jacobi_launch(const double* H, int p, const int* p_dev, double* theta, double* Y,
                           DevState* state, double tol, int max_sweeps, cudaStream_t st) {
+  static int rows = -1;  // development knob PF_JACOBI_ROWS=0 selects the block-thread kernel
+  if (rows < 0) {
+    const char* e = getenv("PF_JACOBI_ROWS");
+    rows = e ? atoi(e) : 1;
+  }
+  // measured (tools/bench_jacobi.py): 1.74 vs 2.03 us per round at p = 64, no gain at p <= 32
+  if (rows && p > 32 && p <= 64)
+    return jacobi_rows_pe<64>(H, p, p_dev, theta, Y, state, tol, max_sweeps, st);
   if (p <= 16) return jacobi_pe<16>(H, p, p_dev, theta, Y, state, tol, max_sweeps, st);
   if (p <= 32) return jacobi_pe<32>(H, p, p_dev, theta, Y, state, tol, max_sweeps, st);
   if (p <= 64) return jacobi_pe<64>(H, p, p_dev, theta, Y, state, tol, max_sweeps, st);
