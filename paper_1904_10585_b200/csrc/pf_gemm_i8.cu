@@ -321,7 +321,10 @@ struct I8Args {
 
 // Stream-K work split: the items x kblocks (tile, k-block) units are cut into gridDim.x equal
 // contiguous ranges, so every SM gets the same share of the tensor work; an item cut between
-// CTAs is finished by the last contributor, which sums the fp64 partials in k order.
+// CTAs is finished by the last contributor, which sums the fp64 partials in k order.  Items are
+// column-group major (item = cg * mtiles + tile): with p = 128 (two 64-column groups) CTAs b and
+// b + G/2 walk the same A tile over the same k-blocks at the same time, so A's digit slices are
+// read from HBM once and hit in L2 by the other group.
 struct SegIter {
   long long u, u1;
   int KB;
@@ -416,7 +419,7 @@ __global__ void __launch_bounds__(I8Cfg<S, NC>::THREADS, 1)
       SegIter si(U, G, blockIdx.x, KB);
       int it, kbs, kbe;
       while (si.next(it, kbs, kbe)) {
-        const int tile = it / args.ngroups, cg = it - tile * args.ngroups;
+        const int cg = it / args.mtiles, tile = it - cg * args.mtiles;  // column-group major
         if (args.pf_dist > 0)  // warm the first k-blocks of the segment into L2
           for (int kb = kbs; kb < min(kbe, kbs + args.pf_dist); ++kb)
             tc::tma_prefetch_3d(&mapA8pf, kb * C::BK, tile * C::BM, 0, pol_a);
@@ -493,7 +496,7 @@ __global__ void __launch_bounds__(I8Cfg<S, NC>::THREADS, 1)
     SegIter si(U, G, blockIdx.x, KB);
     int it, kbs, kbe;
     while (si.next(it, kbs, kbe)) {
-      const int tile = it / args.ngroups, cg = it - tile * args.ngroups;
+      const int cg = it / args.mtiles, tile = it - cg * args.mtiles;  // column-group major
       const int row = tile * C::BM + et;
       const bool row_ok = row < args.n_rows;
       const double rs = row_ok ? args.rscale[row] : 0.0;
