@@ -166,6 +166,17 @@ __global__ void __launch_bounds__(kRbThreads, 2) rebuild_kernel(const RbArgs a) 
         }
       }
   }
+  // mask words of this thread's 4 rows (one 32-column word covers the warp's 16 columns),
+  // loaded before the MMA so their latency overlaps it
+  uint32_t wbits[2][2];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int li = i0 + wm * 32 + mt * 16 + g8 + 8 * h;
+      wbits[mt][h] = li < a.n_rows ? __ldg(a.bits + (size_t)li * a.ldb + ((j0 + wn * kWn) >> 5))
+                                   : 0u;
+    }
   cp_async_wait_all();
   __syncthreads();
 
@@ -228,7 +239,7 @@ __global__ void __launch_bounds__(kRbThreads, 2) rebuild_kernel(const RbArgs a) 
       const int li = i0 + rt;
       if (li >= a.n_rows) continue;
       const int gi = a.row0 + li;
-      const uint32_t word = __ldg(a.bits + (size_t)li * a.ldb + ((j0 + wn * kWn) >> 5));
+      const uint32_t word = wbits[mt][h];
 #pragma unroll
       for (int nt = 0; nt < kNt; ++nt) {
         const int ct = wn * kWn + nt * 8 + 2 * t4;  // column within tile
