@@ -14,8 +14,10 @@ pytestmark = [pytest.mark.gpu,
 @pytest.mark.parametrize("cfg", [reduced(CONFIGS[3], n=1500, iters=6, edge_prob=82 / 1500),
                                  reduced(CONFIGS[2], n=1000, iters=6),
                                  reduced(CONFIGS[1], iters=4),
-                                 reduced(CONFIGS[5], n=2048, p=128, nbig=40, nrefl=16, iters=3)],
-                         ids=["pfam", "pfpg", "sweep", "tf32_sweep"])
+                                 reduced(CONFIGS[5], n=2048, p=128, nbig=40, nrefl=16, iters=3),
+                                 reduced(CONFIGS[3], n=1500, iters=4, edge_prob=82 / 1500,
+                                         dtype="f64i8")],
+                         ids=["pfam", "pfpg", "sweep", "tf32_sweep", "pfam_i8"])
 def test_single_rank_nccl_path_matches(cfg):
     from paper_1904_10585_b200 import run
     from paper_1904_10585_b200._lib import nccl_unique_id
