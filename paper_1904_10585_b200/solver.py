@@ -37,7 +37,7 @@ class Solver:
 
     def __init__(self, cfg: Config, problem: dict | None = None, stream=None,
                  nccl_id: bytes | None = None, rank: int = 0, world: int = 1,
-                 graphs: bool = False):
+                 graphs: bool = False, ctx: Context | None = None):
         self.cfg = cfg
         # CUDA graphs: iterations k >= 1 replay one captured graph of the iteration body
         # (interval -> filter -> RR -> f -> update); the Lanczos refresh stays an eager launch
@@ -52,9 +52,12 @@ class Solver:
         if self.graphs and (stream is None or stream.cuda_stream == 0):
             raise ValueError("graphs=True needs a non-default stream (stream capture)")
         self.f32 = cfg.dtype == "tf32"   # fp32 storage, TF32 tensor-core filter (config 5)
-        self.ctx = Context(n, p, d, nccl_id=nccl_id, rank=rank, world=world,
-                           dtype=PF_TF32 if self.f32 else
-                           PF_FP64_I8 if cfg.dtype == "f64i8" else PF_FP64)
+        dtype = PF_TF32 if self.f32 else PF_FP64_I8 if cfg.dtype == "f64i8" else PF_FP64
+        if ctx is not None:  # a context created beforehand for this shape (scratch reused)
+            assert (ctx.n, ctx.p, ctx.d, ctx.dtype) == (n, p, d, dtype), "context shape mismatch"
+            self.ctx = ctx
+        else:
+            self.ctx = Context(n, p, d, nccl_id=nccl_id, rank=rank, world=world, dtype=dtype)
         if self.f32:
             self.ctx.set_tf32_schedule(cfg.tf32_early, cfg.tf32_tail)
         if cfg.dtype == "f64i8":
