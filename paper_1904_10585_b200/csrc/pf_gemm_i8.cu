@@ -225,8 +225,9 @@ __global__ void y_colmax_kernel(const double* __restrict__ Y, int64_t ldy, int n
   __shared__ double sm[256];
   const int c = threadIdx.x % p, r0 = threadIdx.x / p, rstep = blockDim.x / p;
   double m = 0.0;
+#pragma unroll 8
   for (int r = blockIdx.x * rstep + r0; r < n_k; r += gridDim.x * rstep)
-    m = fmax(m, fabs(Y[(int64_t)r * ldy + c]));
+    m = fmax(m, fabs(__ldg(Y + (int64_t)r * ldy + c)));
   sm[threadIdx.x] = m;
   __syncthreads();
   if (threadIdx.x < p) {
@@ -235,8 +236,8 @@ __global__ void y_colmax_kernel(const double* __restrict__ Y, int64_t ldy, int n
   }
 }
 
-// Y -> Y8[s][c][kpad] (K-major digit slices), cscale[c] = 2^F_c.  One CTA per 64-row chunk:
-// the 64 x p block is staged in shared memory, each thread emits 8 consecutive digits (8 bytes)
+// Y -> Y8[s][c][kpad] (K-major digit slices), cscale[c] = 2^F_c.  One CTA per 32-row chunk:
+// the 32 x p block is staged in shared memory, each thread emits 8 consecutive digits (8 bytes)
 // of one column per slice.
 template <int S>
 __global__ void __launch_bounds__(256) y_split_kernel(const double* __restrict__ Y, int64_t ldy,
@@ -244,18 +245,20 @@ __global__ void __launch_bounds__(256) y_split_kernel(const double* __restrict__
                                                       const unsigned long long* __restrict__ cmax,
                                                       int8_t* __restrict__ Y8, int64_t kpad,
                                                       double* __restrict__ cscale) {
-  __shared__ double tile[64 * 65];
-  const int k0 = blockIdx.x * 64;
+  constexpr int R = 32;  // rows (K) per CTA: 32-row chunks -> twice the CTAs of 64-row ones
+  __shared__ double tile[R * 65];
+  const int k0 = blockIdx.x * R;
   for (int cb = 0; cb < p; cb += 64) {
     const int pc = min(64, p - cb);
     __syncthreads();
-    for (int i = threadIdx.x; i < 64 * pc; i += blockDim.x) {
+#pragma unroll 8
+    for (int i = threadIdx.x; i < R * pc; i += blockDim.x) {
       const int r = i / pc, c = i % pc;
-      tile[r * 65 + c] = (k0 + r < n_k) ? Y[(int64_t)(k0 + r) * ldy + cb + c] : 0.0;
+      tile[r * 65 + c] = (k0 + r < n_k) ? __ldg(Y + (int64_t)(k0 + r) * ldy + cb + c) : 0.0;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < pc * 8; i += blockDim.x) {
-      const int c = i / 8, g = i % 8;  // column, 8-row group
+    for (int i = threadIdx.x; i < pc * (R / 8); i += blockDim.x) {
+      const int c = i / (R / 8), g = i % (R / 8);  // column, 8-row group
       const int E = i8::scale_exp(__longlong_as_double((long long)cmax[cb + c]));
       if (blockIdx.x == 0 && g == 0) cscale[cb + c] = i8::pow2(E);
       uint32_t lo[S], hi[S];
@@ -676,10 +679,10 @@ static cudaError_t y_split_s(const double* Y, int64_t ldy, const I8Plan& pl,
   const int rstep = 256 / pl.p;
   const int gmax = (pl.n_k + rstep - 1) / rstep;
   count_launch();
-  y_colmax_kernel<<<std::max(1, std::min(gmax, 2 * num_sms)), 256, 0, st>>>(Y, ldy, pl.n_k, pl.p,
+  y_colmax_kernel<<<std::max(1, std::min(gmax, 4 * num_sms)), 256, 0, st>>>(Y, ldy, pl.n_k, pl.p,
                                                                               cmax);
   count_launch();
-  y_split_kernel<S><<<(pl.n_k + 63) / 64, 256, 0, st>>>(Y, ldy, pl.n_k, pl.p, cmax, Y8, pl.kpad,
+  y_split_kernel<S><<<(pl.n_k + 31) / 32, 256, 0, st>>>(Y, ldy, pl.n_k, pl.p, cmax, Y8, pl.kpad,
                                                          cscale);
   return cudaGetLastError();
 }
