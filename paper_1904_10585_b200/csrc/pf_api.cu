@@ -205,6 +205,9 @@ static pf_status alloc_all(pf_ctx ctx) {
     ok &= A((void**)&ctx->tf_acc, ctx->tplan.acc_floats * 4);
     ok &= A((void**)&ctx->tf_cnt, ctx->tplan.counters * 4);
   } else {
+    // panel Cholesky scratch (chol_inv_big, used for p >= 64 on the fp64 path too)
+    ok &= A((void**)&ctx->chol_W, (size_t)p * p * 8);
+    ok &= A((void**)&ctx->chol_D, (size_t)p * 32 * 8);
     for (int i = 0; i < 3; ++i) ok &= A((void**)&ctx->Y[i], (size_t)nl * p * 8);
     ok &= A((void**)&ctx->Wbuf, (size_t)nl * p * 8);
     ok &= A((void**)&ctx->VFbuf, (size_t)nl * p * 8);
@@ -550,11 +553,26 @@ static pf_status gram_all(pf_ctx ctx, const double* X, const double* Y, double* 
   return allreduce(ctx, G, (size_t)ctx->p * ctx->p, st);
 }
 
+// G = R^T R and Rinv = R^{-1} of the p x p Gram: the 32-column panel kernel of the fp32 path for
+// p >= 64 (tools/bench_orth.py: CholeskyQR2 236 vs 259 us at p = 64, 626 vs 853 us at p = 128),
+// the single-CTA column kernel below (PF_CHOL_BIG=0: development knob)
+static cudaError_t chol64(pf_ctx ctx, int* shift_out, const int* cond, cudaStream_t st) {
+  static int big = -1;
+  if (big < 0) {
+    const char* e = getenv("PF_CHOL_BIG");
+    big = e ? atoi(e) : 1;
+  }
+  if (big && ctx->p >= 64)
+    return chol_inv_big_launch(ctx->G, ctx->p, ctx->n, ctx->chol_W, ctx->chol_D, ctx->Rinv,
+                               ctx->state, shift_out, cond, st);
+  return chol_inv_launch(ctx->G, ctx->p, ctx->n, ctx->Rinv, ctx->state, shift_out, cond, st);
+}
+
 // One CholeskyQR pass on Y (in place); cond: only if *cond != 0.
 static pf_status chol_pass(pf_ctx ctx, double* Y, int* shift_out, const int* cond,
                            cudaStream_t st) {
   PF_TRY(gram_all(ctx, Y, Y, ctx->G, cond, st));
-  PF_CU(chol_inv_launch(ctx->G, ctx->p, ctx->n, ctx->Rinv, ctx->state, shift_out, cond, st));
+  PF_CU(chol64(ctx, shift_out, cond, st));
   PF_CU(rmul_launch(Y, ctx->p, ctx->Rinv, Y, ctx->p, (int)ctx->n_local, ctx->p, cond, st));
   return PF_OK;
 }
@@ -841,7 +859,7 @@ pf_status pf_filter(pf_ctx ctx, const void* Av, int64_t lda, void* Uv, int64_t l
         // span-exact re-base of (Y_j, Y_{j-1}) when the plan asks for it (device flag)
         const int* cond = &ctx->state->rebase[j];
         PF_TRY(gram_all(ctx, ctx->Y[cur], ctx->Y[cur], ctx->G, cond, st));
-        PF_CU(chol_inv_launch(ctx->G, p, ctx->n, ctx->Rinv, ctx->state, nullptr, cond, st));
+        PF_CU(chol64(ctx, nullptr, cond, st));
         PF_CU(rmul_launch(ctx->Y[cur], p, ctx->Rinv, ctx->Y[cur], p, nl, p, cond, st));
         PF_CU(rmul_launch(ctx->Y[prev], p, ctx->Rinv, ctx->Y[prev], p, nl, p, cond, st));
       }
