@@ -59,7 +59,8 @@ typedef enum {
   PF_ERR_CUDA = 4,      /* a CUDA runtime call failed (message in pf_last_error) */
   PF_ERR_NOMEM = 5,     /* scratch allocation failed in pf_create */
   PF_ERR_NCCL = 6,      /* NCCL initialisation / collective failed */
-  PF_ERR_UNSUPPORTED = 7
+  PF_ERR_UNSUPPORTED = 7,
+  PF_ERR_BREAKDOWN = 8   /* an iterative step did not converge (pf_rr_ns); nothing was written */
 } pf_status;
 
 /* device status word bits (pf_get_device_status) */
@@ -261,6 +262,18 @@ pf_status pf_invalidate(pf_ctx ctx);
  * measurement and tests.  PF_ERR_UNSUPPORTED for PF_TF32. */
 pf_status pf_matmul(pf_ctx ctx, const double* A, int64_t lda, const double* Y, int64_t ldy,
                     double* out, int64_t ldo, pf_stream stream);
+
+/* Rayleigh-Ritz and the spectral operator without an eigendecomposition (SURVEY NEXT-4,
+ * DESIGN.md reading R26): H = U^T A U as in pf_rayleigh_ritz (same layouts and dtypes), then
+ * F = f(H) (p x p row-major fp64, device) through Newton-Schulz matrix sign iterations
+ * (PSD: f(H) = (H + H sign(H)) / 2; soft threshold thr: f(H) = H + ((H - thr I) sign(H - thr I)
+ * - (H + thr I) sign(H + thr I)) / 2) and *rank = #{f != 0} (device int) from traces, so
+ * X = U F U^T.  *iters (host, may be NULL) = sign iterations used.  Synchronises the stream
+ * (convergence checks) and creates a p x p workspace + cuBLAS handle on its first call.
+ * PF_ERR_BREAKDOWN when an eigenvalue sits so close to the threshold that 100 iterations do not
+ * converge: use pf_rayleigh_ritz + pf_spectral_op for that iteration. */
+pf_status pf_rr_ns(pf_ctx ctx, const void* A, int64_t lda, const void* U, int64_t ldu, pf_op op,
+                   double thr, double* F, int32_t* rank, int32_t* iters, pf_stream stream);
 
 /* ---------------------------------------------------------------- PFSVT (NEXT-3, paper §5.2)
  * Polynomial-filtered SVT for matrix completion (eqn:svt P:1098-1104, Example eg:MC): the dual

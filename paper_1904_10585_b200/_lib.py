@@ -17,7 +17,7 @@ PF_FP64_I8 = 3   # fp64, filter products from exact int8 tensor-core digit produ
 PF_OP_PSD = 0
 PF_OP_SOFT_THRESHOLD = 1
 STATUS = {0: "PF_OK", 1: "PF_ERR_ARG", 2: "PF_ERR_DIM", 3: "PF_ERR_INTERVAL", 4: "PF_ERR_CUDA",
-          5: "PF_ERR_NOMEM", 6: "PF_ERR_NCCL", 7: "PF_ERR_UNSUPPORTED"}
+          5: "PF_ERR_NOMEM", 6: "PF_ERR_NCCL", 7: "PF_ERR_UNSUPPORTED", 8: "PF_ERR_BREAKDOWN"}
 FLAGS = {0x1: "CHOL_SHIFT", 0x2: "NONFINITE", 0x4: "DEGENERATE_INTERVAL", 0x8: "SATURATED",
          0x10: "JACOBI_MAXSWEEP", 0x20: "LANCZOS_BREAK"}
 
@@ -64,6 +64,7 @@ def load() -> ctypes.CDLL:
         "pf_invalidate": [P],
         "pf_matmul": [P, P, I64, P, I64, P, I64, P],
         "pf_spmm": [P, P, P, P, P, P, I64, D, D, D, P, I64, P, I64, P, I64, P],
+        "pf_rr_ns": [P, P, I64, P, I64, I32, D, P, P, ctypes.POINTER(I32), P],
         "pf_svt_ritz": [P, P, P, P, P, I64, D, P, I64, P, I64, P, P, P, P],
         "pf_svt_update": [P, P, P, P, P, P, I64, P, I64, P, D, P, P],
         "pf_profile": [P, I32],
@@ -274,6 +275,16 @@ class Context:
         """out = A Y with the context's filter GEMM (fp64 dtypes; local rows)."""
         self._check(self.lib.pf_matmul(self.h, _ptr(A), _ld(A), _ptr(Y), _ld(Y), _ptr(out),
                                        _ld(out), _stream(stream)), "pf_matmul")
+
+    def rr_ns(self, A, U, op, thr, F, rank, stream=None) -> int:
+        """F = f(U^T A U) by Newton-Schulz (pf_rr_ns); returns the sign iterations used.
+        Raises PFError (PF_ERR_BREAKDOWN) when it does not converge."""
+        it = ctypes.c_int32(0)
+        ldu = _ld(U)
+        self._check(self.lib.pf_rr_ns(self.h, _ptr(A), _ld(A), _ptr(U), ldu, int(op), float(thr),
+                                      _ptr(F), _ptr(rank), ctypes.byref(it), _stream(stream)),
+                    "pf_rr_ns")
+        return int(it.value)
 
     # ---- PFSVT (NEXT-3): sparse operators in compressed-row form (torch int32 / fp64 tensors)
     def spmm(self, ptr, idx, val, X, out, coef=(1.0, 0.0, 0.0), ycur=None, yprev=None,

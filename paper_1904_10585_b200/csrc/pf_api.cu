@@ -112,6 +112,7 @@ struct pf_ctx_s {
   const double* a8_src = nullptr;              // A whose digit slices A8 holds (pf_filter)
   int64_t a8_lda = 0;
   bool a8_valid = false;                       // cleared by every libpf call that writes A
+  NsWork* ns = nullptr;                        // pf_rr_ns workspace (created on first use)
   // ---- PFSVT (pf_svt.cu)
   double* svt_part = nullptr;                  // residual partials (one per 8 rows)
   int* svt_cnt = nullptr;
@@ -154,6 +155,7 @@ const char* pf_status_string(pf_status s) {
     case PF_ERR_NOMEM: return "PF_ERR_NOMEM";
     case PF_ERR_NCCL: return "PF_ERR_NCCL";
     case PF_ERR_UNSUPPORTED: return "PF_ERR_UNSUPPORTED";
+    case PF_ERR_BREAKDOWN: return "PF_ERR_BREAKDOWN";
   }
   return "PF_ERR_UNKNOWN";
 }
@@ -408,6 +410,7 @@ pf_status pf_profile_read(pf_ctx ctx, pf_stream stream, double* gemm_ms, int64_t
 
 pf_status pf_destroy(pf_ctx ctx) {
   if (!ctx) return PF_ERR_ARG;
+  ns_destroy(ctx->ns);
   for (auto e : ctx->ev) cudaEventDestroy(e);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   void* ptrs[] = {ctx->state,  ctx->Y[0],     ctx->Y[1],      ctx->Y[2],    ctx->Yfull,
@@ -1084,6 +1087,55 @@ pf_status pf_matmul(pf_ctx ctx, const double* A, int64_t lda, const double* Y, i
   PF_CU(cudaMemcpy2DAsync(ctx->Y[0], row, Y, ldy * 8, row, nl, cudaMemcpyDeviceToDevice, st));
   PF_TRY(gemm_step(ctx, 0, ctx->Y[0], ctx->Y[0], ctx->Wbuf, &ctx->state->coef_rr[0], st));
   PF_CU(cudaMemcpy2DAsync(out, ldo * 8, ctx->Wbuf, row, row, nl, cudaMemcpyDeviceToDevice, st));
+  return PF_OK;
+}
+
+// ------------------------------------------------------------------------------ Newton-Schulz RR
+pf_status pf_rr_ns(pf_ctx ctx, const void* Av, int64_t lda, const void* Uv, int64_t ldu,
+                   pf_op op, double thr, double* F, int32_t* rank, int32_t* iters,
+                   pf_stream stream) {
+  if (!ctx || !Uv || !F || !rank) return PF_ERR_ARG;
+  if (op != PF_OP_PSD && op != PF_OP_SOFT_THRESHOLD) return PF_ERR_ARG;
+  if (op == PF_OP_SOFT_THRESHOLD && !(thr > 0.0)) return PF_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int p = ctx->p;
+  if (ctx->dtype == PF_TF32) {
+    const float* A = static_cast<const float*>(Av);
+    if (ldu < ctx->n_local) return PF_ERR_DIM;
+    PF_TRY(check_A32(ctx, A, lda));
+    PF_TRY(map_A32(ctx, A, lda));
+    PF_TRY(copy_block32(ctx, ctx->Yf[0], ctx->ldy32, static_cast<const float*>(Uv), ldu, st));
+    PF_TRY(gemm_step32(ctx, 0, ctx->Yf[0], ctx->Yf[0], ctx->Wf, &ctx->state->coef_rr[0],
+                       ctx->tf_rr, st));
+    PF_TRY(gram32_all(ctx, ctx->Yf[0], ctx->Wf, ctx->G, nullptr, st));  // H = Q^T (A Q)
+  } else {
+    const double* A = static_cast<const double*>(Av);
+    if (ldu < p) return PF_ERR_DIM;
+    PF_TRY(check_A(ctx, A, lda));
+    PF_TRY(map_A(ctx, A, lda));
+    PF_TRY(split_A(ctx, A, lda, true, st));
+    const size_t row = (size_t)p * 8;
+    PF_CU(cudaMemcpy2DAsync(ctx->Y[0], row, Uv, ldu * 8, row, ctx->n_local,
+                            cudaMemcpyDeviceToDevice, st));
+    PF_TRY(gemm_step(ctx, 0, ctx->Y[0], ctx->Y[0], ctx->Wbuf, &ctx->state->coef_rr[0], st));
+    PF_TRY(gram_all(ctx, ctx->Y[0], ctx->Wbuf, ctx->G, nullptr, st));
+  }
+  if (!ctx->ns) {
+    ctx->ns = ns_create(p);
+    if (!ctx->ns) {
+      snprintf(ctx->err, sizeof(ctx->err), "pf_rr_ns: workspace / cuBLAS handle creation failed");
+      return PF_ERR_NOMEM;
+    }
+  }
+  int it = 0;
+  const int r = ns_spectral(ctx->ns, ctx->G, op == PF_OP_SOFT_THRESHOLD ? 1 : 0, thr, F, rank,
+                            &it, st);
+  if (iters) *iters = it;
+  // no Ritz values: the next re-base plan falls back to the Lanczos spread estimate
+  PF_CU(cudaMemsetAsync(&ctx->state->have_theta, 0, sizeof(int), st));
+  ctx->filtered = false;
+  if (r == -1) return PF_ERR_BREAKDOWN;
+  if (r < 0) return cuda_fail(ctx, cudaGetLastError(), "pf_rr_ns (cuBLAS)");
   return PF_OK;
 }
 

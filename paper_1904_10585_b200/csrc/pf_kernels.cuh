@@ -85,6 +85,14 @@ cudaError_t i8_gemm_launch(const I8Plan& pl, const CUtensorMap& mapA8, const CUt
                            const double* yprev, double* out, int64_t ldy, const double* coef,
                            double* acc, double* part, int* counters, int su, cudaStream_t st);
 
+// ---- Newton-Schulz spectral operator (pf_ns.cu): F = f(H) of a p x p symmetric fp64 matrix
+struct NsWork;
+NsWork* ns_create(int p);
+void ns_destroy(NsWork* w);
+// 0 ok, -1 not converged (fall back to Jacobi), -2 cuBLAS / CUDA failure; synchronises `st`
+int ns_spectral(NsWork* w, const double* H, int op_soft, double thr, double* F, int* rank,
+                int* iters, cudaStream_t st);
+
 // ---- PFSVT sparse kernels (pf_svt.cu): S n x n in compressed-row form (CSR, or the CSC view)
 cudaError_t spmm_launch(int rows, int p, const int* ptr, const int* idx, const double* val,
                         const int* vperm, const double* X, int64_t ldx, const double* coef,

@@ -43,7 +43,14 @@ class Solver:
         # (interval -> filter -> RR -> f -> update); the Lanczos refresh stays an eager launch
         # in front of it.  Iterations with a host-side change (degree schedule, extrapolation
         # window) are not graphed.
-        self.graphs = graphs and cfg.deg_c <= 0.0 and not (cfg.mode == "nce" and cfg.accel_l > 0)
+        self.graphs = (graphs and cfg.deg_c <= 0.0 and not (cfg.mode == "nce" and cfg.accel_l > 0)
+                       and not cfg.rr_ns)   # Newton-Schulz checks convergence on the host
+        if cfg.rr_ns and cfg.mode not in ("sweep_psd", "sweep_soft"):
+            raise ValueError("rr_ns: the update kernels take eigen-factors; sweep modes only")
+        self.F = None            # f(H) of the last Newton-Schulz Rayleigh-Ritz (p x p)
+        self.ns_iters = 0
+        self.ns_fallbacks = 0
+        self.last_ns = False     # the last iteration's RR ran as Newton-Schulz
         self._graph = {}
         self.graph_launches = {}
         self.replayed_launches = 0   # kernels launched by graph replays (not seen by the counter)
@@ -162,8 +169,11 @@ class Solver:
         # Warm start the next filter from the Ritz vectors: Range(V) = Range(U), so the method
         # is unchanged (eqn:subspace-update depends on Range(U) only), but the next H = Q^T A Q
         # is then nearly diagonal and the Jacobi solve converges in one or two sweeps.
-        self.ritz = self.V
-        self.U, self.V = self.V, self.U
+        if self.last_ns:
+            self.ritz = self.U       # X = U F U^T: the filtered basis itself is the warm start
+        else:
+            self.ritz = self.V
+            self.U, self.V = self.V, self.U
         self.k += 1
 
     def _replay(self):
@@ -194,8 +204,19 @@ class Solver:
             ctx.set_degree(degree_at(cfg, k))
         for _ in range(cfg.warmup if k == 0 else 1):
             ctx.filter(self.A, self.U, self.interval, cfg.q, cfg.rho_max, st)
+        if cfg.rr_ns:
+            from ._lib import PFError
+            if self.F is None:
+                self.F = torch.empty((cfg.p, cfg.p), dtype=torch.float64, device="cuda")
+            try:
+                self.ns_iters = ctx.rr_ns(self.A, self.U, self.op, self.thr, self.F, self.rank, st)
+                self.last_ns = True
+                return
+            except PFError:            # an eigenvalue at the threshold: Jacobi this iteration
+                self.ns_fallbacks += 1
         ctx.rayleigh_ritz(self.A, self.U, self.V, self.theta, st)
         ctx.spectral_op(self.op, self.thr, self.theta, self.f, self.rank, st)
+        self.last_ns = False
         if cfg.mode == "pfpg":
             ctx.prox_step(self.V, self.f, cfg.tau, self.omega, self.W, self.A, self.obj, st)
         elif cfg.mode == "pfam":
@@ -255,7 +276,12 @@ def _run(cfg, K, record, problem, nccl_id, rank, world, stream, graphs):
     for k in range(K):
         s.step()
         rec = {"k": k}
-        if record:
+        if record and s.last_ns:
+            # X = Q F Q^T: recorded as the factor pair (Q F, Q) with unit weights
+            Q = s.ritz_factors()
+            F = s.F.cpu().numpy()
+            rec.update(rank=int(s.rank.item()), QF=Q @ F, Q=Q, ns_iters=s.ns_iters)
+        elif record:
             f = s.f.cpu().numpy()
             keep = f != 0.0
             rec.update(theta=s.theta.cpu().numpy(), rank=int(s.rank.item()),

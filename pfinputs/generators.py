@@ -69,6 +69,9 @@ class Config:
     # before the last i8_tail multiply i8_early digit slices, the tail and RR all 7
     i8_early: int = 7
     i8_tail: int = 2
+    # sweep modes: Rayleigh-Ritz + spectral operator as F = f(H) by Newton-Schulz sign
+    # iterations instead of a Jacobi EVD (NEXT-4 / reading R26; the oracle ignores it)
+    rr_ns: bool = False
     # nearest correlation estimation (mode "nce"): paper Example eg:5.6 (6) or eg:5.7 (7)
     nce_example: int = 7
     # regularized extrapolation of the iterates (§4.3; NEXT-4): window l (0 = off)

@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--p", type=int, default=512)
     ap.add_argument("--d", type=int, nargs="+", default=[4, 8, 16])
     ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--ns", type=int, default=1,
+                    help="1: Rayleigh-Ritz spectral operator by Newton-Schulz (pf_rr_ns, R26)")
     ap.add_argument("--passes", type=int, default=0,
                     help="uniform TF32 passes (1..3); 0 = the config's schedule (reading R18)")
     args = ap.parse_args()
@@ -43,7 +45,7 @@ def main():
     stream = torch.cuda.Stream()
     Adev = None
     for d in args.d:
-        cfg = reduced(base, d=d)
+        cfg = reduced(base, d=d, rr_ns=bool(args.ns))
         with torch.cuda.stream(stream):
             if Adev is None:
                 buf = torch.empty((cfg.n, (cfg.n + 3) // 4 * 4), dtype=torch.float32, device="cuda")
@@ -84,7 +86,11 @@ def main():
             "config": f"config 5 sweep, n={n}, p={p}, d={d}, fp32 storage, tcgen05 TF32 filter "
                       + (f"{args.passes}xTF32 every pass" if args.passes else
                          f"schedule: {cfg.tf32_early}xTF32 steps 1..{d - cfg.tf32_tail}, "
-                         f"3xTF32 last {cfg.tf32_tail} steps + RR") + ", 1 GPU",
+                         f"3xTF32 last {cfg.tf32_tail} steps + RR") +
+                      (", RR spectral operator by Newton-Schulz" if args.ns else ", RR by Jacobi")
+                      + ", 1 GPU",
+            "ns_iters_last": s.ns_iters if args.ns else None,
+            "ns_fallbacks": s.ns_fallbacks if args.ns else None,
             "it_per_s": 1e3 / ms, "ms_per_step": ms, "step_ms": step_ms,
             "filter_tflops": 2.0 * d * n * n * p / (ms / 1e3) / 1e12,
             "gemm_avg_ms": gemm_avg, "gemm_launches": gemm_n,
