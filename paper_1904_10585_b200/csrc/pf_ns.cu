@@ -108,6 +108,7 @@ struct NsWork {
   unsigned long long* nrm = nullptr;     // device
   double* res_host = nullptr;            // pinned
   int p = 0;
+  int last_it[2] = {0, 0};               // iterations the previous call's signs needed
 };
 
 NsWork* ns_create(int p) {
@@ -149,7 +150,7 @@ static bool dgemm(NsWork* w, const double* A, const double* B, double* C, double
 
 // S = sign(H - shift I); returns the iterations used, -1 if not converged within max_it
 static int ns_sign(NsWork* w, const double* H, double shift, double* S, int max_it, double tol,
-                   cudaStream_t st) {
+                   int slot, cudaStream_t st) {
   const int p = w->p, n = p * p;
   cudaMemsetAsync(w->nrm, 0, 8, st);
   count_launch();
@@ -166,16 +167,20 @@ static int ns_sign(NsWork* w, const double* H, double shift, double* S, int max_
     double* t = X;
     X = Xn;
     Xn = t;
-    // ||X_prev^2 - I|| measured before this step: check every 4 steps (one host sync)
-    if ((it & 3) == 0 || it == max_it) {
+    // ||X_prev^2 - I|| measured before this step.  Each check is a host sync: the first one
+    // comes where the previous call (a nearby H in a sweep) converged, then every 2 steps
+    const int first = w->last_it[slot] > 2 ? w->last_it[slot] - 1 : 8;
+    if ((it >= first && ((it - first) & 1) == 0) || it == max_it) {
       cudaMemcpyAsync(w->res_host, w->res, 8, cudaMemcpyDeviceToHost, st);
       cudaStreamSynchronize(st);
       if (sqrt(*w->res_host) <= tol) {
         if (X != S) cudaMemcpyAsync(S, X, (size_t)n * 8, cudaMemcpyDeviceToDevice, st);
+        w->last_it[slot] = it;
         return it;
       }
     }
   }
+  w->last_it[slot] = 0;
   return -1;
 }
 
@@ -191,9 +196,9 @@ int ns_spectral(NsWork* w, const double* H, int op_soft, double thr, double* F, 
   cublasSetMathMode(w->h, CUBLAS_DEFAULT_MATH);  // fp64 arithmetic, no emulation
   int it1, it2 = 0;
   if (op_soft) {
-    it1 = ns_sign(w, H, thr, w->Sp, max_it, tol, st);
+    it1 = ns_sign(w, H, thr, w->Sp, max_it, tol, 0, st);
     if (it1 < 0) return it1;
-    it2 = ns_sign(w, H, -thr, w->Sm, max_it, tol, st);
+    it2 = ns_sign(w, H, -thr, w->Sm, max_it, tol, 1, st);
     if (it2 < 0) return it2;
     // F = H + ((H - thr I) S+ - (H + thr I) S-) / 2
     cudaMemcpyAsync(F, H, (size_t)p * p * 8, cudaMemcpyDeviceToDevice, st);
@@ -205,7 +210,7 @@ int ns_spectral(NsWork* w, const double* H, int op_soft, double thr, double* F, 
     ns_shift_kernel<<<(p + 7) / 8, 256, 0, st>>>(H, p, -thr, w->M, w->nrm);   // H + thr I
     if (!dgemm(w, w->M, w->Sm, F, -0.5, 1.0)) return -2;
   } else {
-    it1 = ns_sign(w, H, 0.0, w->Sp, max_it, tol, st);
+    it1 = ns_sign(w, H, 0.0, w->Sp, max_it, tol, 0, st);
     if (it1 < 0) return it1;
     // F = (H + H S) / 2
     cudaMemcpyAsync(F, H, (size_t)p * p * 8, cudaMemcpyDeviceToDevice, st);
