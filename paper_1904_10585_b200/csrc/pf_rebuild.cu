@@ -41,6 +41,7 @@ struct RbArgs {
   const double* W;
   int64_t ldw;
   int r, rpad;
+  int w_async;  // W rows 16-byte aligned (even ldw, aligned base): stage W panels with cp.async
   const double* deg;
   double* Out;
   int64_t ldo;
@@ -96,6 +97,9 @@ __global__ void __launch_bounds__(kRbThreads, 2) rebuild_kernel(const RbArgs a) 
   const int tc = (a.n + kRb - 1) / kRb, tr = (a.n_rows + kRb - 1) / kRb;
   const int ntiles = a.sym ? (tc * (tc + 1)) / 2 : tr * tc;
   for (int c = tid; c < P; c += kRbThreads) fs[c] = a.f[c];
+  if (PFPG && a.w_async)  // zero padding columns of both W panels (never written by cp.async)
+    for (int e = tid; e < kRb * ldw_s; e += kRbThreads)
+      if (e % ldw_s >= a.r - (a.r & 1)) Wi[e] = Wj[e] = 0.0;
   double s0 = 0.0, s1 = 0.0;
   // persistent CTAs: each owns a CONTIGUOUS range of tiles (deterministic sums; in the row-major
   // upper-triangle order consecutive tiles share the row block I, so the staged I panel is
@@ -131,7 +135,29 @@ __global__ void __launch_bounds__(kRbThreads, 2) rebuild_kernel(const RbArgs a) 
     if (j0 + rr < a.n) cp_async16(dj, a.V + (size_t)(j0 + rr) * a.ldv + c);
     else *reinterpret_cast<double2*>(dj) = make_double2(0.0, 0.0);
   }
-  if (PFPG) {
+  if (PFPG && a.w_async) {
+    // W panels by cp.async (plain loads + stores stalled every thread on its own loads); the
+    // padding columns r .. ldw_s-1 were zeroed once and are never written
+    const int r2 = a.r >> 1;
+    for (int e = tid; e < kRb * r2; e += kRbThreads) {
+      const int rr = e / r2, c = (e - rr * r2) * 2;
+      if (newI) {
+        double* d = Wi + rr * ldw_s + c;
+        if (i0 + rr < a.n_rows) cp_async16(d, a.W + (size_t)(a.row0 + i0 + rr) * a.ldw + c);
+        else *reinterpret_cast<double2*>(d) = make_double2(0.0, 0.0);
+      }
+      double* d = Wj + rr * ldw_s + c;
+      if (j0 + rr < a.n) cp_async16(d, a.W + (size_t)(j0 + rr) * a.ldw + c);
+      else *reinterpret_cast<double2*>(d) = make_double2(0.0, 0.0);
+    }
+    if (a.r & 1) {  // odd rank: the last column by plain loads
+      const int c = a.r - 1;
+      for (int rr = tid; rr < kRb; rr += kRbThreads) {
+        if (newI) Wi[rr * ldw_s + c] = i0 + rr < a.n_rows ? a.W[(size_t)(a.row0 + i0 + rr) * a.ldw + c] : 0.0;
+        Wj[rr * ldw_s + c] = j0 + rr < a.n ? a.W[(size_t)(j0 + rr) * a.ldw + c] : 0.0;
+      }
+    }
+  } else if (PFPG) {
     for (int e = tid; e < kRb * ldw_s; e += kRbThreads) {
       const int rr = e / ldw_s, c = e % ldw_s;
       if (newI)
@@ -404,7 +430,9 @@ cudaError_t prox_launch(const double* V, int64_t ldv, const double* Vloc, int64_
                         int* counter, double* vf, cudaStream_t st) {
   cudaError_t e = scale_cols(Vloc, ldvl, f, n_rows, p, vf, st);
   if (e != cudaSuccess) return e;
-  RbArgs a{V, ldv, vf, f, tau, omega, ldo, W, ldw, r, 0, nullptr, Aout, lda, n_rows, n, row0,
+  RbArgs a{V, ldv, vf, f, tau, omega, ldo, W, ldw, r, 0,
+           (r > 0 && (ldw & 1) == 0 && (reinterpret_cast<uintptr_t>(W) & 15) == 0) ? 1 : 0,
+           nullptr, Aout, lda, n_rows, n, row0,
            0, 0, 0, partials, counter, obj};
   return rb_dispatch<true>(p, a, st);
 }
@@ -416,7 +444,7 @@ cudaError_t admm_launch(const double* V, int64_t ldv, const double* Vloc, int64_
                         cudaStream_t st) {
   cudaError_t e = scale_cols(Vloc, ldvl, f, n_rows, p, vf, st);
   if (e != cudaSuccess) return e;
-  RbArgs a{V, ldv, vf, f, t, adj, ldadj, nullptr, 0, 0, 0, deg, Z, ldz, n_rows, n, row0,
+  RbArgs a{V, ldv, vf, f, t, adj, ldadj, nullptr, 0, 0, 0, 0, deg, Z, ldz, n_rows, n, row0,
            0, 0, raw, partials, counter, obj};
   return rb_dispatch<false>(p, a, st);
 }
