@@ -210,8 +210,11 @@ pf_status pf_profile_read(pf_ctx ctx, pf_stream stream, double* gemm_ms, int64_t
 /* Process-wide number of CUDA kernels launched by this library so far. */
 long long pf_kernel_launches(void);
 /* Synchronises `stream`; diag[0] = Jacobi sweeps of the last Rayleigh-Ritz solve,
- * diag[1] = Lanczos steps of the last refresh. */
-pf_status pf_diagnostics(pf_ctx ctx, pf_stream stream, double* diag /* [2] */);
+ * diag[1] = Lanczos steps of the last refresh, diag[2] = the relative gap of eqn:relative-gap
+ * (NEXT-2 diagnostic) G = min over the Ritz values theta_i outside the damped
+ * interval [a, b] of the last pf_filter of |theta_i - (a + b)/2| / ((b - a)/2) - 1, with the
+ * Ritz values standing in for the eigenvalues (+inf when none lies outside). */
+pf_status pf_diagnostics(pf_ctx ctx, pf_stream stream, double* diag /* [3] */);
 
 /* Workload helper (not the method): A <- A + E (config 1 noise, BASELINE configs[0]).
  * PF_FP64 contexts only. */

@@ -38,6 +38,7 @@ from pfinputs import (Config, initial_block, lanczos_start, cfg1_problem, cfg1_n
 
 __all__ = [
     "cheb_T", "growth_lower_bound", "interval_map", "interval_psd", "interval_top_r",
+    "relative_gap",
     "interval_soft", "lanczos_extremes", "rebase_plan", "spread_estimate", "chebyshev_filter",
     "orth", "filter_update", "rayleigh_ritz", "spectral_psd", "spectral_soft", "jacobi_eig",
     "exact_spectral", "maxcut_C", "prox_tG_diag", "pfam_next", "pfpg_next", "nce_next",
@@ -340,6 +341,18 @@ def _threshold(cfg: Config, prob) -> float:
     return cfg.theta
 
 
+def relative_gap(theta: np.ndarray, a: float, b: float) -> float:
+    """eqn:relative-gap: G_k = min over i in I_k of |lambda_i - (a+b)/2| / ((b-a)/2) - 1,
+    I_k the eigenvalues beyond [a, b]; the Ritz values stand in for the eigenvalues (NEXT-2
+    diagnostic; the printed denominator (a_k - b_k)/2 is negative -- read as (b - a)/2, SURVEY
+    §8(c)).  +inf when no Ritz value lies outside, or the interval is degenerate."""
+    if not b > a:
+        return float("inf")
+    c, e = 0.5 * (a + b), 0.5 * (b - a)
+    out = theta[(theta < a) | (theta > b)]
+    return float(np.min(np.abs(out - c) / e - 1.0)) if out.size else float("inf")
+
+
 def run(cfg: Config, iters: int | None = None, record_factors: bool = True,
         problem: dict | None = None, progress=None) -> dict:
     """The PFPG / PFAM / sweep iteration of SURVEY.md §8(c), step by step.
@@ -417,7 +430,8 @@ def run(cfg: Config, iters: int | None = None, record_factors: bool = True,
         f = spectral_psd(theta) if psd else spectral_soft(theta, thr)
         keep = f != 0.0
         rec = {"k": k, "a": a, "b": b, "theta": theta, "rank": int(keep.sum()),
-               "saturated": bool(keep.all()), "rebase": plan, "degenerate": degenerate}
+               "saturated": bool(keep.all()), "rebase": plan, "degenerate": degenerate,
+               "gap": relative_gap(theta, a, b)}
         if record_factors:
             rec["V"], rec["f"] = V[:, keep], f[keep]
         # a6

@@ -378,6 +378,7 @@ pf_status pf_diagnostics(pf_ctx ctx, pf_stream stream, double* diag) {
   PF_CU(cudaMemcpy(&h, ctx->state, sizeof(DevState), cudaMemcpyDeviceToHost));
   diag[0] = h.scratch[1];
   diag[1] = (double)h.lanczos_steps;
+  diag[2] = h.scratch[2];
   return PF_OK;
 }
 

@@ -901,9 +901,27 @@ cudaError_t interval_soft_launch(double thr, double eta, double* interval, DevSt
 }
 
 __global__ void copy_theta_kernel(const double* theta, int p, DevState* state) {
+  __shared__ double red[32];
   const int i = threadIdx.x;
-  if (i < p) state->theta[i] = theta[i];
-  if (i == 0) state->have_theta = 1;
+  // relative gap (eqn:relative-gap) of the Ritz values beyond the damped interval
+  const double a = state->interval[0], b = state->interval[1];
+  const double c = 0.5 * (a + b), e = 0.5 * (b - a);
+  double g = INFINITY;
+  if (i < p) {
+    const double t = theta[i];
+    state->theta[i] = t;
+    if (e > 0.0 && (t < a || t > b)) g = fabs(t - c) / e - 1.0;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) g = fmin(g, __shfl_xor_sync(0xffffffffu, g, o));
+  if ((i & 31) == 0) red[i >> 5] = g;
+  __syncthreads();
+  if (i == 0) {
+    double m = INFINITY;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmin(m, red[w]);
+    state->scratch[2] = m;
+    state->have_theta = 1;
+  }
 }
 
 cudaError_t copy_theta_launch(const double* theta, int p, DevState* state, cudaStream_t st) {

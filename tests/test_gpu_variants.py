@@ -63,3 +63,21 @@ def test_interval_top_r_matches_oracle():
     theta = th.cpu().numpy()
     np.testing.assert_allclose(iv.cpu().numpy(), O.interval_top_r(-2.5, theta[9], 0.1),
                                rtol=1e-15, atol=1e-15)
+
+
+def test_relative_gap_diagnostic_matches_oracle():
+    """pf_diagnostics' relative gap (NEXT-2, eqn:relative-gap) from the device Ritz values and
+    the damped interval equals the oracle's on every iteration of a sweep."""
+    from paper_1904_10585_b200 import Solver
+    import oracle as O
+    cfg = reduced(CONFIGS[1], iters=6)
+    ref = O.run(cfg)["records"]
+    s = Solver(cfg)
+    from pfinputs import cfg1_noise
+    from paper_1904_10585_b200.solver import _dev
+    for k in range(cfg.iters):
+        s.step()
+        g = s.ctx.diagnostics()["relative_gap"]
+        assert g == pytest.approx(ref[k]["gap"], rel=1e-9), (k, g, ref[k]["gap"])
+        if k + 1 < cfg.iters:
+            s.perturb(_dev(cfg1_noise(cfg, k)))

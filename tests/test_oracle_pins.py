@@ -577,3 +577,12 @@ def test_psd_iterate_skips_filter_compression_closed_form():
         assert r["degenerate"] and r["rebase"] == [] and r["a"] == r["b"] > 0
         Xk = (r["V"] * r["f"]) @ r["V"].T
         assert np.abs(Xk - X).max() <= 1e-12 * np.abs(X).max()
+
+
+def test_relative_gap_definition():
+    """eqn:relative-gap on a hand example: [a, b] = [-1, 1] (c = 0, e = 1), Ritz
+    values 3 and -2 beyond it -> min(3 - 1, 2 - 1) = 1; values inside do not count."""
+    assert O.relative_gap(np.array([3.0, 0.5, -2.0, -0.9]), -1.0, 1.0) == pytest.approx(1.0)
+    assert O.relative_gap(np.array([0.5]), -1.0, 1.0) == float("inf")
+    # G_k > 0 <=> every wanted value is strictly beyond the interval edge
+    assert O.relative_gap(np.array([1.0 + 1e-9]), -1.0, 1.0) == pytest.approx(1e-9, rel=1e-6)
