@@ -26,22 +26,26 @@ def _err(g, r):
     return O.lowrank_diff_fro(g["V"], g["f"], r["V"], r["f"]) / den
 
 
-def test_config2_fullsize_trajectory_prefix():
+@pytest.mark.parametrize("dtype", ["f64", "f64i8"])
+def test_config2_fullsize_trajectory_prefix(dtype):
     from paper_1904_10585_b200 import run
-    cfg = CONFIGS[2]
+    cfg = reduced(CONFIGS[2], dtype=dtype)
     K = 12
     ref = O.run(cfg, iters=K)["records"]
-    got = run(cfg, iters=K)["records"]
+    got = run(cfg, iters=K, graphs=True)["records"]
     for r, g in zip(ref, got):
         assert _err(g, r) <= 1e-10, (r["k"], _err(g, r))
         assert abs(g["objective"] - r["objective"]) <= 1e-10 * abs(r["objective"])
 
 
-def test_config3_fullsize_one_step():
+@pytest.mark.parametrize("dtype", ["f64", "f64i8"])   # f64i8 + graphs: the bench's path
+def test_config3_fullsize_one_step(dtype):
     from paper_1904_10585_b200 import Solver
-    cfg = CONFIGS[3]
+    cfg = reduced(CONFIGS[3], dtype=dtype)
     prob = pfam_problem(cfg)
-    s = Solver(cfg, problem=prob)
+    st = torch.cuda.Stream()
+    torch.cuda.set_stream(st)
+    s = Solver(cfg, problem=prob, stream=st, graphs=True)
     for _ in range(3):
         s.step()                                   # k = 0, 1, 2 on the GPU
     k = s.k                                        # next iteration index (3)
@@ -73,6 +77,7 @@ def test_config3_fullsize_one_step():
     idx = rng.integers(0, cfg.n, size=(2000, 2))
     zs = Zg[torch.as_tensor(idx[:, 0]), torch.as_tensor(idx[:, 1])].cpu().numpy()
     np.testing.assert_allclose(zs, Zn[idx[:, 0], idx[:, 1]], rtol=0, atol=1e-10 * np.abs(Zn).max())
+    torch.cuda.set_stream(torch.cuda.default_stream())
 
 
 def test_config4_shape_fullsize_properties():
