@@ -284,8 +284,25 @@ def run_dmma(cfg, prob, args, stream) -> dict:
         e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
+    # its dominant kernel against the fp64 DMMA peak (eager profiled steps, as for the main arm)
+    s.graphs = False
+    s.ctx.profile(True)
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            s.step()
+    torch.cuda.synchronize()
+    gms, gn = s.ctx.profile_read(stream)
+    s.ctx.profile(False)
+    g_avg = gms / max(gn, 1)
+    tflops = 2.0 * c64.n * c64.n * c64.p / (g_avg / 1e3) / 1e12
+    pk = peaks().get("fp64_dmma_tflops", 37.1)
     out = {"value": args.steps / (ms / 1e3), "unit": "it/s", "ms_per_step": ms / args.steps,
-           "what": "same workload and timing, filter GEMM on fp64 DMMA (PF_FP64)"}
+           "what": "same workload and timing, filter GEMM on fp64 DMMA (PF_FP64)",
+           "roofline": {"bound": "tensor", "kernel": "cheb_gemm_kernel<64> (fp64 DMMA)",
+                        "achieved": tflops, "peak": pk, "unit": "TFLOP/s", "frac": tflops / pk,
+                        "avg_launch_ms": g_avg,
+                        "peak_source": "fp64 DMMA m16n8k4 measured on this pool "
+                                       "(profiles/r01_probe_peaks.log)"}}
     del s
     torch.cuda.empty_cache()
     return out
