@@ -26,7 +26,7 @@ import math
 import numpy as np
 import scipy.sparse as sp
 
-from pfinputs import Config, initial_block, svt_problem
+from pfinputs import Config, initial_block, svt_guard_block, svt_problem
 
 __all__ = ["svt_kick", "svt_matrix", "shrink_exact", "svt_exact_run", "svt_filter", "svt_ritz",
            "svt_sample", "pfsvt_run", "lowrank_rect_diff_fro", "lowrank_rect_fro",
@@ -125,12 +125,22 @@ def pfsvt_run(cfg: Config, prob: dict | None = None, iters: int | None = None,
       4. w = A(U diag(s) V^T) on Omega;  x <- x + tau (b - w)  (eqn:svt);
       5. warm start Q <- V.
     Records the factors of W^k = U diag(s) V^T (kept columns), svp and the relative residual
-    ||w - b|| / ||b|| (the SVT stopping quantity; `stop` ends the run below cfg.svt_tol)."""
+    ||w - b|| / ||b|| (the SVT stopping quantity; `stop` ends the run below cfg.svt_tol).
+    cfg.svt_adapt (NEXT-2, paper §4.2 "the number of [wanted] eigenvalues in the previous
+    iteration is used as an estimation ... guard vectors are also added", reading R27): the next
+    block has p_{k+1} = min(p, the smallest of 16/32/64/128 >= svp_k + p_guard) columns -- the
+    leading Ritz vectors, or all of them plus svt_guard_block(cfg, k, .) columns."""
     prob = svt_problem(cfg) if prob is None else prob
     n = cfg.n
     mu, tau = prob["tau"], prob["delta"]
     x = svt_kick(prob)
-    Q = _orth(initial_block(cfg))
+
+    def bucket(m):
+        m = min(m, cfg.p)
+        return next(q for q in (16, 32, 64, 128) if q >= m)
+
+    p_cur = bucket(cfg.p0) if cfg.svt_adapt else cfg.p
+    Q = _orth(initial_block(cfg)[:, :p_cur])
     a, b = 0.0, (1.0 - cfg.eta) * mu * mu
     nb = float(np.linalg.norm(prob["b"]))
     recs = []
@@ -144,12 +154,19 @@ def pfsvt_run(cfg: Config, prob: dict | None = None, iters: int | None = None,
         w = svt_sample(U[:, keep], s[keep], V[:, keep], prob["I"], prob["J"])
         res = float(np.linalg.norm(w - prob["b"])) / nb
         rec = {"k": k, "sigma": sig, "svp": int(keep.sum()), "res": res,
-               "saturated": bool(keep.all())}
+               "saturated": bool(keep.all()), "p": p_cur}
         if record_factors:
             rec.update(U=U[:, keep], s=s[keep], V=V[:, keep])
         recs.append(rec)
         x = x + tau * (prob["b"] - w)
         Q = V
+        if cfg.svt_adapt:
+            p_next = bucket(int(keep.sum()) + cfg.p_guard)
+            if p_next < p_cur:
+                Q = V[:, :p_next]
+            elif p_next > p_cur:
+                Q = np.hstack([V, svt_guard_block(cfg, k, p_next - p_cur)])
+            p_cur = p_next
         if stop and res <= cfg.svt_tol:
             break
     return {"records": recs, "x": x, "prob": prob}

@@ -9,7 +9,7 @@ import math
 import numpy as np
 import torch
 
-from pfinputs import Config, initial_block, svt_problem
+from pfinputs import Config, initial_block, svt_guard_block, svt_problem
 
 from ._lib import Context, PF_FP64, PF_FP64_I8
 
@@ -31,8 +31,11 @@ class SVTSolver:
         self.cfg, self.stream = cfg, stream
         prob = svt_problem(cfg) if problem is None else problem
         self.prob = prob
-        n, p = cfg.n, cfg.p
-        self.ctx = Context(n, p, max(cfg.d, 1), dtype=PF_FP64_I8 if cfg.dtype == "f64i8" else PF_FP64)
+        n = cfg.n
+        # NEXT-2 adaptive block size (reading R27): a context and block buffers per supported p,
+        # created on first use; the sparse data, b and x are shared
+        p = self._bucket(cfg.p0) if cfg.svt_adapt else cfg.p
+        self._per_p = {}
         self.mu, self.delta = float(prob["tau"]), float(prob["delta"])
         self.row_ptr, self.col = _i32(prob["row_ptr"]), _i32(prob["J"])
         self.col_ptr, self.row_csc, self.perm = (_i32(prob["col_ptr"]), _i32(prob["rows_csc"]),
@@ -42,17 +45,37 @@ class SVTSolver:
         # SVT's kick (reading R24): x^0 = k0 delta b, k0 = ceil(mu / (delta ||P_Omega(M)||_2))
         k0 = math.ceil(self.mu / (self.delta * prob["norm2"]))
         self.x = _f64(k0 * self.delta * prob["b"])
-        buf = lambda: torch.empty((n, p), dtype=torch.float64, device="cuda")
-        self.blocks = [buf() for _ in range(4)]   # Q, the recurrence, V (roles rotate)
-        self.T, self.U = buf(), buf()
-        self.Q = self.blocks[0]
-        self.Q.copy_(torch.from_numpy(initial_block(cfg)))
-        self.ctx.orth(self.Q, stream)
-        self.sigma = torch.zeros(p, dtype=torch.float64, device="cuda")
-        self.s = torch.zeros(p, dtype=torch.float64, device="cuda")
         self.svp = torch.zeros(1, dtype=torch.int32, device="cuda")
         self.rss = torch.zeros(1, dtype=torch.float64, device="cuda")
+        self._use(p)
+        self.Q = self.blocks[0]
+        self.Q.copy_(torch.from_numpy(np.ascontiguousarray(initial_block(cfg)[:, :p])))
+        self.ctx.orth(self.Q, stream)
         self.k = 0
+
+    @staticmethod
+    def _bucket_sizes():
+        return (16, 32, 64, 128)
+
+    def _bucket(self, m: int) -> int:
+        m = min(m, self.cfg.p)
+        return next(q for q in self._bucket_sizes() if q >= m)
+
+    def _use(self, p: int):
+        """Switch the context / block buffers to block size p (allocated on first use)."""
+        if p not in self._per_p:
+            n, cfg = self.cfg.n, self.cfg
+            buf = lambda: torch.empty((n, p), dtype=torch.float64, device="cuda")
+            self._per_p[p] = {
+                "ctx": Context(n, p, max(cfg.d, 1),
+                               dtype=PF_FP64_I8 if cfg.dtype == "f64i8" else PF_FP64),
+                "blocks": [buf() for _ in range(4)], "T": buf(), "U": buf(),
+                "sigma": torch.zeros(p, dtype=torch.float64, device="cuda"),
+                "s": torch.zeros(p, dtype=torch.float64, device="cuda")}
+        d = self._per_p[p]
+        self.p = p
+        self.ctx, self.blocks, self.T, self.U = d["ctx"], d["blocks"], d["T"], d["U"]
+        self.sigma, self.s = d["sigma"], d["s"]
 
     def _filter(self):
         """Q <- orth(T_d(L(Y^T Y)) Q), L(t) = (t - c)/e on [a, b] = [0, (1 - eta) mu^2]."""
@@ -84,6 +107,21 @@ class SVTSolver:
         ctx.svt_update(self.row_ptr, self.col, self.b, self.x, self.U, V, self.s, self.delta,
                        self.rss, st)
         self.Q = V            # warm start: span(V) = span(Q)
+        self.last = {"U": self.U, "s": self.s, "V": V, "sigma": self.sigma}  # W^k's factors
+        if self.cfg.svt_adapt:
+            # next block size from this iteration's recovered rank (host read of svp)
+            p_next = self._bucket(int(self.svp.item()) + self.cfg.p_guard)
+            if p_next != self.p:
+                V, p_old, st = self.Q, self.p, self.stream
+                self._use(p_next)
+                Qn = self.blocks[0]
+                if p_next < p_old:
+                    Qn.copy_(V[:, :p_next])                    # leading Ritz vectors
+                else:
+                    Qn[:, :p_old].copy_(V)                     # + seeded guard columns
+                    Qn[:, p_old:].copy_(torch.from_numpy(
+                        svt_guard_block(self.cfg, self.k, p_next - p_old)))
+                self.Q = Qn
         self.k += 1
 
     def residual(self) -> float:
@@ -92,9 +130,10 @@ class SVTSolver:
 
     def factors(self):
         """(U, s, V) of W^k on the host, kept columns only (s > 0)."""
-        s = self.s.cpu().numpy()
+        L = self.last
+        s = L["s"].cpu().numpy()
         keep = s > 0.0
-        return (self.U.cpu().numpy()[:, keep], s[keep], self.Q.cpu().numpy()[:, keep])
+        return (L["U"].cpu().numpy()[:, keep], s[keep], L["V"].cpu().numpy()[:, keep])
 
 
 def run_svt(cfg: Config, iters: int | None = None, problem=None, stop: bool = False,
@@ -107,7 +146,8 @@ def run_svt(cfg: Config, iters: int | None = None, problem=None, stop: bool = Fa
         rec = {"k": k, "res": s.residual(), "svp": int(s.svp.item())}
         if record:
             rec["U"], rec["s"], rec["V"] = s.factors()
-            rec["sigma"] = s.sigma.cpu().numpy()
+            rec["sigma"] = s.last["sigma"].cpu().numpy()
+            rec["p"] = int(s.last["s"].numel())
         recs.append(rec)
         if stop and rec["res"] <= cfg.svt_tol:
             break

@@ -91,6 +91,12 @@ class Config:
     svt_tau: float = 5.0
     svt_delta: float = 1.2
     svt_tol: float = 1e-4
+    # NEXT-2 adaptive block size (paper §4.2, reading R27): p_k = the smallest supported size
+    # >= svp_{k-1} + p_guard (capped at p), starting from p0; grown blocks are completed with
+    # seeded Gaussian guard columns (svt_guard_block)
+    svt_adapt: bool = False
+    p_guard: int = 5
+    p0: int = 16
 
 
 CONFIGS = {
@@ -400,6 +406,11 @@ def nce_problem(cfg: Config) -> dict:
     G[(iu[1], iu[0])] = G[iu]
     np.fill_diagonal(G, 1.0)
     return {"G": G}
+
+
+def svt_guard_block(cfg: Config, k: int, m: int) -> np.ndarray:
+    """m new N(0, 1) columns (n x m) for a block grown after iteration k (NEXT-2, reading R27)."""
+    return _rng(cfg.seed, 14, k).standard_normal((cfg.n, m))
 
 
 def svt_problem(cfg: Config) -> dict:

@@ -119,3 +119,19 @@ def test_pfsvt_converges_like_tab_svt_mkl():
     M = prob["ML"] @ prob["MR"].T
     mse = np.linalg.norm((last["U"] * last["s"]) @ last["V"].T - M) / np.linalg.norm(M)
     assert 0.5e-4 <= mse <= 2.5e-4
+
+
+def test_adaptive_block_size_matches_oracle():
+    """NEXT-2 (reading R27): p_k = the smallest of 16/32/64 >= svp_{k-1} + 5, grown blocks
+    completed with the seeded guard columns; the GPU follows the oracle's block sizes and
+    iterates (r = 20, so the block grows 16 -> 32 during the run)."""
+    from paper_1904_10585_b200 import run_svt
+    cfg = reduced(NEXT_CONFIGS["svt5k"], n=800, r=20, sr=0.3, p=64, iters=14, svt_adapt=True)
+    prob = svt_problem(cfg)
+    ref = O.pfsvt_run(cfg, prob)["records"]
+    got = run_svt(cfg, problem=prob)["records"]
+    assert len({r["p"] for r in ref}) > 1, [r["p"] for r in ref]
+    for x, y in zip(ref, got):
+        assert x["p"] == y["p"] and x["svp"] == y["svp"]
+        den = max(O.lowrank_rect_fro(x["U"], x["s"], x["V"]), 1e-300)
+        assert O.lowrank_rect_diff_fro(x["U"], x["s"], x["V"], y["U"], y["s"], y["V"]) <= 1e-10 * den

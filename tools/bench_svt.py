@@ -19,6 +19,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cases", nargs="+", default=["svt1k", "svt5k", "svt10k"])
+    ap.add_argument("--adapt", type=int, default=0,
+                    help="1: NEXT-2 adaptive block size (p_k from svp_{k-1} + 5, reading R27)")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -27,6 +29,9 @@ def main():
 
     for name in args.cases:
         cfg = NEXT_CONFIGS[name]
+        if args.adapt:
+            from pfinputs import reduced
+            cfg = reduced(cfg, svt_adapt=True)
         t0 = time.time()
         prob = svt_problem(cfg)
         gen_s = time.time() - t0
@@ -48,6 +53,7 @@ def main():
         total_ms = e0.elapsed_time(e1)
         # one CSR filter product timed alone
         ptr, col, x = s.row_ptr, s.col, s.x
+        p_final = s.p
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         with torch.cuda.stream(st):
             for _ in range(3):
@@ -63,11 +69,13 @@ def main():
         M = prob["ML"] @ prob["MR"].T
         mse = float(np.linalg.norm((U * sv) @ V.T - M) / np.linalg.norm(M))
         print(json.dumps({
-            "case": f"{name}: m=n={cfg.n}, SR={cfg.sr}, r={cfg.r}, p={cfg.p}, d={cfg.d}, nnz={nnz}",
+            "case": f"{name}: m=n={cfg.n}, SR={cfg.sr}, r={cfg.r}, p={cfg.p}, d={cfg.d}, nnz={nnz}"
+                    + (", adaptive p (R27)" if args.adapt else ""),
+            "p_final": p_final,
             "iters": it, "svp": int(s.svp.item()), "res": s.residual(), "mse": mse,
             "seconds_to_converge": total_ms / 1e3, "ms_per_iter": total_ms / it,
             "spmm_ms": spmm_ms,
-            "spmm_gather_gbps": nnz * cfg.p * 8 / spmm_ms / 1e6,
+            "spmm_gather_gbps": nnz * p_final * 8 / spmm_ms / 1e6,
             "spmm_stream_gbps": nnz * 12 / spmm_ms / 1e6,
             "host_generation_s": gen_s}), flush=True)
         del s
