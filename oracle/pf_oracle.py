@@ -5,7 +5,7 @@ TEST INFRASTRUCTURE.  Only tests/, __graft_entry__.smoke() and bench.py's cpu_ba
 
 Citations: ``P:n`` = line n of the paper's LaTeX source, with the section /
 equation label.  Readings where the paper is silent, ambiguous or wrong are numbered
-R1..R14 and listed in DESIGN.md §2.
+R1..R27 and listed in DESIGN.md §2 (R23: a PSD iterate skips the filter).
 
 Each function is the paper's definition or algorithm written out step by step in numpy
 fp64; library primitives used as single steps: ``@`` (matmul), ``numpy.linalg.qr``
@@ -23,8 +23,16 @@ Pins (tests/test_oracle_pins.py) -- what fixes each function independently of it
   pfam_next ......... 2-node max-cut optimum; 5-cycle SDP value -(25+5 sqrt 5)/8 (closed form);
                       diag(prox) == 1; fixed point maps to itself
   pfpg_next ......... p = n, tau = 1: objective non-increasing; exact-subspace equivalence
-  run (trajectories of configs 2-5 at full size) -- parity unpinned beyond the invariants
-      above and the p = n special case (no published values exist for these inputs).
+  nce_next .......... 2x2 closed form; constant off-diagonal -> 11^T; p = n exact; objective
+                      values of tab:ncm
+  rna_extrapolate ... trivial windows, the l = 1 closed form, exact recovery of a linear fixed point
+  relative_gap ...... hand example of eqn:relative-gap
+  run ............... config 1 k = 0 == exact P_+; degenerate (PSD) interval == compression P A P;
+                      q repeats on a diagonal A (closed form); the degree schedule of thm:conv1;
+                      trajectories of configs 2-5 at full size -- parity unpinned beyond the
+                      invariants above and the p = n special case (no published values exist
+                      for these inputs).
+  PFSVT (pf_svt.py) . dual-gradient identity, p = n == exact-SVD SVT, tab:SVT-MKL row 1.
 """
 from __future__ import annotations
 
