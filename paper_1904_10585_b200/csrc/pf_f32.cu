@@ -299,6 +299,14 @@ __global__ void __launch_bounds__(CH_NT) chol_inv_big_kernel(const double* __res
                                                             DevState* state, int* shift_flag_out,
                                                             const int* cond) {
   if (cond && *cond == 0) return;
+  // Cooperative grid (reading: same arithmetic as the one-CTA version): CTA 0 factors each
+  // 32-column panel (top block + forward substitution) and writes it back to W; after a grid
+  // barrier every CTA copies the panel into its shared memory and updates its share of the
+  // trailing 64 x 64 blocks; a second barrier closes the panel.  gridDim.x == 1 is the original
+  // single-CTA kernel.
+  cg::grid_group grid = cg::this_grid();
+  const bool lead = blockIdx.x == 0;
+  volatile double* gfail = &state->scratch[3];  // panel breakdown flag, shared by the grid
   CHOL_T(0);
   extern __shared__ double cs[];  // p x CB_LD panel
   __shared__ double red[32];
@@ -330,14 +338,17 @@ __global__ void __launch_bounds__(CH_NT) chol_inv_big_kernel(const double* __res
   int attempt = 0;
   CHOL_T(1);
   for (;;) {
-    for (int e = tid; e < p * p; e += CH_NT) {
+    for (int e = blockIdx.x * CH_NT + tid; e < p * p; e += gridDim.x * CH_NT) {
       const int i = e / p, j = e % p;
       if (j <= i) W[e] = G[e] + ((i == j) ? shift : 0.0);
     }
     if (tid == 0) s_fail = 0;
-    __syncthreads();
+    if (lead && tid == 0) *gfail = 0.0;
+    __threadfence();
+    grid.sync();
     for (int J = 0; J < p; J += CB) {
       const int R = p - J;
+      if (lead) {  // ---------------- panel factorisation (CTA 0)
       for (int e = tid; e < R * CB; e += CH_NT) {
         const int r = e / CB, c = e % CB;
         cs[PNL(r, c)] = (c <= r) ? W[(size_t)(J + r) * p + J + c] : 0.0;
@@ -368,7 +379,7 @@ __global__ void __launch_bounds__(CH_NT) chol_inv_big_kernel(const double* __res
       }
       __syncthreads();
       if (J == 0) CHOL_T(5);
-      if (s_fail) break;
+      if (!s_fail) {
       // (b) rows below the top block: L[r][0:32] = A[r][0:32] L_top^{-T}, forward substitution
       //     in place, one panel row per thread (the top block is read as a broadcast)
       for (int r = CB + tid; r < R; r += CH_NT) {
@@ -391,6 +402,23 @@ __global__ void __launch_bounds__(CH_NT) chol_inv_big_kernel(const double* __res
         const int r = e / CB, c = e % CB;
         if (c <= r) W[(size_t)(J + r) * p + J + c] = cs[PNL(r, c)];
       }
+      }  // !s_fail
+      if (tid == 0 && s_fail) *gfail = 1.0;
+      }  // lead
+      __threadfence();
+      grid.sync();
+      if (*gfail != 0.0) {
+        if (tid == 0) s_fail = 1;
+        __syncthreads();
+        break;
+      }
+      if (!lead) {  // the other CTAs take the finished panel from W
+        for (int e = tid; e < R * CB; e += CH_NT) {
+          const int r = e / CB, c = e % CB;
+          cs[PNL(r, c)] = (c <= r) ? W[(size_t)(J + r) * p + J + c] : 0.0;
+        }
+        __syncthreads();
+      }
       // (c) trailing update of the lower triangle, W[i][k] -= sum_c P[i][c] P[k][c] for
       //     J+32 <= k <= i, on fp64 DMMA (m16n8k4, K = 32 from the panel in smem): 64 x 64 blocks
       //     of the lower block triangle, one 16 x 16 sub-tile per warp
@@ -400,7 +428,7 @@ __global__ void __launch_bounds__(CH_NT) chol_inv_big_kernel(const double* __res
         const int nblk = nb * (nb + 1) / 2;
         const int wr = (warp >> 2) * 16, wc = (warp & 3) * 16;  // warp sub-tile in the block
         const int g8 = lane >> 2, t4 = lane & 3;
-        for (int b = 0; b < nblk; ++b) {
+        for (int b = blockIdx.x; b < nblk; b += gridDim.x) {
           int bi = (int)((sqrt(8.0 * b + 1.0) - 1.0) * 0.5);
           while (bi * (bi + 1) / 2 > b) --bi;
           while ((bi + 1) * (bi + 2) / 2 <= b) ++bi;
@@ -435,6 +463,8 @@ __global__ void __launch_bounds__(CH_NT) chol_inv_big_kernel(const double* __res
       }
       __syncthreads();
       if (J == 0) CHOL_T(7);
+      __threadfence();
+      grid.sync();
     }
     __syncthreads();
     if (!s_fail) break;
@@ -446,6 +476,7 @@ __global__ void __launch_bounds__(CH_NT) chol_inv_big_kernel(const double* __res
     shift = shift_scale * (tr > 0.0 ? tr : 1.0);
     __syncthreads();
   }
+  if (!lead) return;
   if (tid == 0) {
     if (attempt) atomicOr(&state->flags, PF_FLAG_CHOL_SHIFT);
     if (shift_flag_out && attempt) *shift_flag_out = 1;
@@ -524,9 +555,21 @@ cudaError_t chol_inv_big_launch(const double* G, int p, int64_t n_global, double
                          (int)((512 * CB_LD + CB * CB_LD) * sizeof(double)));
     attr = true;
   }
+  // cooperative grid for the trailing updates at p >= 256 (one CTA below: the grid barriers
+  // would cost more than the few trailing blocks)
+  static int coop = -1;
+  if (coop < 0) {
+    const char* e = getenv("PF_CHOL_GRID");  // development knob
+    coop = e ? atoi(e) : 32;
+  }
+  const int grid = (p >= 256) ? std::max(1, coop) : 1;
+  void* args[] = {(void*)&G,     (void*)&p,     (void*)&scale,          (void*)&W,
+                  (void*)&Dinv,  (void*)&Rinv,  (void*)&state,          (void*)&shift_flag_out,
+                  (void*)&cond};
   count_launch();
-  chol_inv_big_kernel<<<1, CH_NT, smem, st>>>(G, p, scale, W, Dinv, Rinv, state, shift_flag_out,
-                                              cond);
+  cudaError_t e1 = cudaLaunchCooperativeKernel((const void*)chol_inv_big_kernel, dim3(grid),
+                                               dim3(CH_NT), args, smem, st);
+  if (e1 != cudaSuccess) return e1;
   count_launch();
   linv_big_kernel<<<p / CB, 1024, smem2, st>>>(W, p, Dinv, Rinv, cond);
   return cudaGetLastError();
