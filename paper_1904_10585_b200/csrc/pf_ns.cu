@@ -87,16 +87,20 @@ __global__ void ns_finish_kernel(double* __restrict__ F, int p, const double* __
                : 0.5 * (1.0 + Sp[(size_t)i * p + i]);
   tr = block_sum(tr, red);
   if (threadIdx.x == 0) *rank = (int)llrint(tr);
-  // F <- (F + F^T) / 2 over the strict upper triangle (pairs written by one thread)
-  for (int e = threadIdx.x; e < p * p; e += blockDim.x) {
-    const int i = e / p, j = e % p;
-    if (i < j) {
-      const double v = 0.5 * (F[(size_t)i * p + j] + F[(size_t)j * p + i]);
-      F[(size_t)i * p + j] = v;
-      F[(size_t)j * p + i] = v;
-    }
-  }
   (void)theta_out;
+  (void)F;
+}
+
+// F <- (F + F^T) / 2: one thread per element pair i < j (grid-wide)
+__global__ void ns_symmetrize_kernel(double* __restrict__ F, int p) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= p * p) return;
+  const int i = e / p, j = e - i * p;
+  if (i < j) {
+    const double v = 0.5 * (F[(size_t)i * p + j] + F[(size_t)j * p + i]);
+    F[(size_t)i * p + j] = v;
+    F[(size_t)j * p + i] = v;
+  }
 }
 
 struct NsWork {
@@ -218,6 +222,8 @@ int ns_spectral(NsWork* w, const double* H, int op_soft, double thr, double* F, 
   }
   count_launch();
   ns_finish_kernel<<<1, 512, 0, st>>>(F, p, w->Sp, w->Sm, op_soft, nullptr, rank);
+  count_launch();
+  ns_symmetrize_kernel<<<(p * p + 255) / 256, 256, 0, st>>>(F, p);
   if (iters) *iters = it1 + it2;
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
