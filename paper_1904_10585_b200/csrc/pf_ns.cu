@@ -76,10 +76,9 @@ __global__ void ns_prep_kernel(double* __restrict__ T, int p, double* __restrict
   }
 }
 
-// F (symmetrised), rank from the traces of the sign matrices
-__global__ void ns_finish_kernel(double* __restrict__ F, int p, const double* __restrict__ Sp,
-                                 const double* __restrict__ Sm, int soft, double* theta_out,
-                                 int* rank) {
+// rank = #{f != 0} from the traces of the sign matrices
+__global__ void ns_rank_kernel(int p, const double* __restrict__ Sp, const double* __restrict__ Sm,
+                               int soft, int* rank) {
   __shared__ double red[32];
   double tr = 0.0;
   for (int i = threadIdx.x; i < p; i += blockDim.x)
@@ -87,8 +86,6 @@ __global__ void ns_finish_kernel(double* __restrict__ F, int p, const double* __
                : 0.5 * (1.0 + Sp[(size_t)i * p + i]);
   tr = block_sum(tr, red);
   if (threadIdx.x == 0) *rank = (int)llrint(tr);
-  (void)theta_out;
-  (void)F;
 }
 
 // F <- (F + F^T) / 2: one thread per element pair i < j (grid-wide)
@@ -221,7 +218,7 @@ int ns_spectral(NsWork* w, const double* H, int op_soft, double thr, double* F, 
     if (!dgemm(w, H, w->Sp, F, 0.5, 0.5)) return -2;
   }
   count_launch();
-  ns_finish_kernel<<<1, 512, 0, st>>>(F, p, w->Sp, w->Sm, op_soft, nullptr, rank);
+  ns_rank_kernel<<<1, 512, 0, st>>>(p, w->Sp, w->Sm, op_soft, rank);
   count_launch();
   ns_symmetrize_kernel<<<(p * p + 255) / 256, 256, 0, st>>>(F, p);
   if (iters) *iters = it1 + it2;
