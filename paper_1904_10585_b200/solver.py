@@ -183,11 +183,17 @@ class Solver:
         key = self.U.data_ptr()
         g = self._graph.get(key)
         if g is None:
-            torch.cuda.synchronize()
+            # capture without a device synchronisation (torch.cuda.graph() would drain the GPU
+            # first): the body allocates nothing, so capturing while earlier work still runs
+            # is safe, and the GPU stays busy during the host-side capture
             g = torch.cuda.CUDAGraph()
             l0 = kernel_launches()
-            with torch.cuda.graph(g, stream=self.stream):
-                self._body(1)
+            with torch.cuda.stream(self.stream):
+                g.capture_begin()
+                try:
+                    self._body(1)
+                finally:
+                    g.capture_end()
             self.graph_launches[key] = kernel_launches() - l0
             self._graph[key] = g
         with torch.cuda.stream(self.stream):
