@@ -109,9 +109,18 @@ struct pf_ctx_s {
   CUtensorMap mapY8[4];                        // B boxes of 4..7 digit slices
   int i8_early = 7;                            // slices of the Chebyshev steps before the tail
   int i8_tail = 0;                             // final steps (and RR) at the full slice count
+  // PF_FUSE_DIGITS=0: the PFAM update does not write digits (pf_filter splits Z itself)
+  bool fuse_digits = [] {
+    const char* e = getenv("PF_FUSE_DIGITS");
+    return !(e && e[0] == '0');
+  }();
   const double* a8_src = nullptr;              // A whose digit slices A8 holds (pf_filter)
   int64_t a8_lda = 0;
   bool a8_valid = false;                       // cleared by every libpf call that writes A
+  bool a8_fused = false;                       // A8 written by pf_admm_step's update (no split)
+  int* a8_E = nullptr;                         // [n_local] row exponents of the fused digits
+  double2* a8_wa = nullptr;                    // [n_local] row-bound scratch
+  unsigned long long* a8_wmax = nullptr;
   NsWork* ns = nullptr;                        // pf_rr_ns workspace (created on first use)
   // ---- PFSVT (pf_svt.cu)
   double* svt_part = nullptr;                  // residual partials (one per 8 rows)
@@ -218,6 +227,9 @@ static pf_status alloc_all(pf_ctx ctx) {
     const I8Plan& ip = ctx->i8plan;
     ok &= A((void**)&ctx->A8, (size_t)kI8MaxSlices * nl * ip.kpad);
     ok &= A((void**)&ctx->a8_rscale, (size_t)nl * 8);
+    ok &= A((void**)&ctx->a8_E, (size_t)nl * 4);
+    ok &= A((void**)&ctx->a8_wa, (size_t)nl * 16);
+    ok &= A((void**)&ctx->a8_wmax, 16);
     ok &= A((void**)&ctx->Y8, (size_t)kI8MaxSlices * p * ip.kpad);
     ok &= A((void**)&ctx->y8_cscale, (size_t)p * 8);
     ok &= A((void**)&ctx->y8_cmax, (size_t)p * 8);
@@ -506,12 +518,13 @@ static pf_status split_A(pf_ctx ctx, const double* A, int64_t lda, bool reuse, c
   if (!use_i8(ctx)) return PF_OK;
   if (reuse && ctx->a8_valid && ctx->a8_src == A && ctx->a8_lda == lda) return PF_OK;
   PF_CU(i8_split_A_launch(A, lda, ctx->i8plan, ctx->A8, ctx->a8_rscale, ctx->num_sms, st));
+  ctx->a8_fused = false;
   ctx->a8_src = A;
   ctx->a8_lda = lda;
   ctx->a8_valid = true;
   return PF_OK;
 }
-static void iterate_written(pf_ctx ctx) { ctx->a8_valid = false; }
+static void iterate_written(pf_ctx ctx) { ctx->a8_valid = ctx->a8_fused = false; }
 
 static bool is_fp64(pf_ctx ctx) { return ctx->dtype == PF_FP64 || ctx->dtype == PF_FP64_I8; }
 
@@ -840,7 +853,8 @@ pf_status pf_filter(pf_ctx ctx, const void* Av, int64_t lda, void* Uv, int64_t l
   PF_TRY(check_A(ctx, A, lda));
   PF_TRY(map_A(ctx, A, lda));
   cudaStream_t st = (cudaStream_t)stream;
-  PF_TRY(split_A(ctx, A, lda, false, st));
+  // the digits pf_admm_step wrote with Z_new are reused; any other A is split afresh
+  PF_TRY(split_A(ctx, A, lda, ctx->a8_fused, st));
   const int p = ctx->p, d = ctx->d;
   const int nl = (int)ctx->n_local;
   const size_t row = (size_t)p * 8;
@@ -965,9 +979,19 @@ pf_status pf_admm_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f
   const double* Vf;
   int64_t ldf;
   PF_TRY(full_V(ctx, V, ldv, &Vf, &ldf, st));
+  // one GPU, int8-digit filter: the update writes Z_new's digit slices for the next pf_filter
+  const bool fuse = use_i8(ctx) && !ctx->dist && ctx->fuse_digits &&
+                    (ctx->i8plan.S == 6 || ctx->i8plan.S == 7);
+  RbDigits dig{ctx->A8, ctx->i8plan.kpad, ctx->i8plan.kpad * ctx->n_local, ctx->i8plan.S,
+               ctx->a8_E, ctx->a8_rscale, ctx->a8_wa, ctx->a8_wmax};
   PF_CU(admm_launch(Vf, ldf, V, ldv, f, t, adj, ldadj, deg, Z, ldz, (int)ctx->n_local,
                     (int)ctx->n, (int)ctx->row0, ctx->p, obj, ctx->rb_part, ctx->rb_cnt,
-                    ctx->dist ? 1 : 0, ctx->VFbuf, st));
+                    ctx->dist ? 1 : 0, ctx->VFbuf, st, fuse ? &dig : nullptr));
+  if (fuse) {
+    ctx->a8_src = Z;
+    ctx->a8_lda = ldz;
+    ctx->a8_valid = ctx->a8_fused = true;
+  }
   if (ctx->dist) {
     // <C, W> and the squared residual are sums over row blocks; sqrt after the reduction
     PF_TRY(allreduce(ctx, obj, 2, st));

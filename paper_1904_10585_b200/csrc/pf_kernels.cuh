@@ -190,11 +190,22 @@ cudaError_t prox_launch(const double* V, int64_t ldv, const double* Vloc, int64_
                         const double* W, int64_t ldw, int r, double* Aout, int64_t lda,
                         int n_rows, int n, int row0, int p, double* obj, double* partials,
                         int* counter, double* vf, cudaStream_t st);
+// PF_FP64_I8 on one GPU: the PFAM update also writes the digit slices of Z_new (pf_gemm_i8.cu
+// layout [S][n][kpad]) and their row scales, so the next filter skips its split pass
+struct RbDigits {
+  int8_t* A8;
+  int64_t kpad, a8_slice;
+  int S;
+  int* E;                   // [n] row exponents
+  double* rscale;           // [n] 2^E
+  double2* wa;              // [n] scratch (W_ii, sum_k |f_k| V_ik^2)
+  unsigned long long* wmax; // scratch
+};
 cudaError_t admm_launch(const double* V, int64_t ldv, const double* Vloc, int64_t ldvl,
                         const double* f, double t, const uint32_t* adj, int64_t ldadj,
                         const double* deg, double* Z, int64_t ldz, int n_rows, int n, int row0,
                         int p, double* obj, double* partials, int* counter, int raw, double* vf,
-                        cudaStream_t st);
+                        cudaStream_t st, const RbDigits* dig = nullptr);
 cudaError_t sqrt_inplace_launch(double* x, cudaStream_t st);
 // NCE dual gradient update (NEXT-1): partials >= 2 * 256 doubles; obj gets raw sums
 cudaError_t nce_launch(const double* V, int64_t ldv, const double* f, int p, double tau,

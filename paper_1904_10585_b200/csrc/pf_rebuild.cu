@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <cmath>
 
+#include "pf_digits.cuh"
 #include "pf_kernels.cuh"
 
 namespace pf {
@@ -51,6 +52,13 @@ struct RbArgs {
   double* partials;
   int* counter;
   double* obj;
+  // PF_FP64_I8 (PFAM, one GPU): the update also writes the S-digit slices of Z_new for the next
+  // filter (A8 != nullptr): row exponents E (row bounds computed before the update), slices
+  // [S][n][kpad] with slice stride a8_slice -- the separate split pass over Z disappears
+  int8_t* A8;
+  int64_t kpad, a8_slice;
+  const int* E;
+  int S;
 };
 
 template <int P, bool PFPG>
@@ -79,6 +87,40 @@ __device__ __forceinline__ void pair_of(int e, int T, int& I, int& J) {
   J = i + (e - (int)((long long)i * T - (long long)i * (i - 1) / 2));
 }
 
+// Z_new tile (64 x 64 in Tz, row pitch 65) -> digit slices: thread t owns row r = t / 4 and 16
+// consecutive columns; the mirror tile (rows j0.., columns i0..) reads Tz transposed
+template <int S>
+__device__ __forceinline__ void rb_digits(const RbArgs& a, const double* Tz, int i0, int j0,
+                                          bool mirror, int tid) {
+  const int r = tid >> 2, cb = (tid & 3) * 16;
+  auto put = [&](int row, int col0, const double (&v)[16]) {
+    const int E = a.E[row];
+    uint32_t w[4][S];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      i8::slices4<S>(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3], E, w[q]);
+    int8_t* dst = a.A8 + (size_t)row * a.kpad + col0;
+#pragma unroll
+    for (int sl = 0; sl < S; ++sl)
+      __stcs(reinterpret_cast<uint4*>(dst + sl * a.a8_slice),
+             make_uint4(w[0][sl], w[1][sl], w[2][sl], w[3][sl]));
+  };
+  // kpad is a multiple of 16, so a chunk starting below n lies inside the row; entries past n
+  // (never read: the GEMM's tensor map ends at n) are written as 0
+  if (i0 + r < a.n_rows && j0 + cb < a.n) {
+    double v[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = j0 + cb + q < a.n ? Tz[r * 65 + cb + q] : 0.0;
+    put(i0 + r, j0 + cb, v);
+  }
+  if (mirror && j0 + r < a.n && i0 + cb < a.n) {
+    double v[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = i0 + cb + q < a.n ? Tz[(cb + q) * 65 + r] : 0.0;
+    put(j0 + r, i0 + cb, v);
+  }
+}
+
 template <int P, bool PFPG>
 __global__ void __launch_bounds__(kRbThreads, 2) rebuild_kernel(const RbArgs a) {
   using C = RbCfg<P, PFPG>;
@@ -91,6 +133,7 @@ __global__ void __launch_bounds__(kRbThreads, 2) rebuild_kernel(const RbArgs a) 
   double* Vj = sm + kRb * C::LD;    // 64 x LD  rows J
   double* Wi = Vj + kRb * C::LD;    // 64 x ldw_s (PFPG)
   double* Wj = Wi + kRb * ldw_s;
+  double* Tz = Vj + kRb * C::LD;    // 64 x 65 staging of Z_new (PFAM digit output)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g8 = lane >> 2, t4 = lane & 3;
   const int wm = warp & 1, wn = warp >> 1;  // 2 (rows) x 4 (cols) warps, 32 x 16 each
@@ -300,6 +343,10 @@ __global__ void __launch_bounds__(kRbThreads, 2) rebuild_kernel(const RbArgs a) 
             o[c] = znew;
           }
         }
+        if (!PFPG && a.A8) {
+          Tz[rt * 65 + ct] = o[0];
+          Tz[rt * 65 + ct + 1] = two ? o[1] : 0.0;
+        }
         double* op = a.Out + (size_t)li * a.ldo + j;
         if (two && ((reinterpret_cast<uintptr_t>(op) & 15) == 0)) {
           __stcs(reinterpret_cast<double2*>(op), make_double2(o[0], o[1]));
@@ -316,6 +363,12 @@ __global__ void __launch_bounds__(kRbThreads, 2) rebuild_kernel(const RbArgs a) 
       }
     }
 
+    if (!PFPG && a.A8) {
+      // ---- digit slices of the Z_new tile (and of its mirror): coalesced 16-byte rows
+      __syncthreads();
+      if (a.S == 7) rb_digits<7>(a, Tz, i0, j0, mirror, tid);
+      else rb_digits<6>(a, Tz, i0, j0, mirror, tid);
+    }
   }  // tile loop
 
   // ---- deterministic reduction: block tree, then the last CTA sums CTA partials in order
@@ -364,13 +417,14 @@ static cudaError_t rb_launch(RbArgs a, cudaStream_t st) {
   using C = RbCfg<P, PFPG>;
   a.rpad = PFPG ? ((a.r + 3) / 4) * 4 : 0;
   const int ldw_s = a.rpad + 4;
-  const size_t panels = (size_t)2 * kRb * C::LD * 8 + (PFPG ? (size_t)2 * kRb * ldw_s * 8 : 0);
+  const size_t panels = (size_t)2 * kRb * C::LD * 8 + (PFPG ? (size_t)2 * kRb * ldw_s * 8 : 0) +
+                        ((!PFPG && a.A8) ? (size_t)kRb * 65 * 8 : 0);
   const size_t stage = (size_t)kRb * C::LDS * 8;
   const size_t smem = std::max(panels, stage);
   static bool attr = false;
   if (!attr) {
-    const size_t mx =
-        std::max((size_t)2 * kRb * C::LD * 8 + (PFPG ? (size_t)2 * kRb * 68 * 8 : 0), stage);
+    const size_t mx = std::max((size_t)2 * kRb * C::LD * 8 +
+                                   (PFPG ? (size_t)2 * kRb * 68 * 8 : (size_t)kRb * 65 * 8), stage);
     cudaFuncSetAttribute(rebuild_kernel<P, PFPG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)mx);
     attr = true;
@@ -433,19 +487,78 @@ cudaError_t prox_launch(const double* V, int64_t ldv, const double* Vloc, int64_
   RbArgs a{V, ldv, vf, f, tau, omega, ldo, W, ldw, r, 0,
            (r > 0 && (ldw & 1) == 0 && (reinterpret_cast<uintptr_t>(W) & 15) == 0) ? 1 : 0,
            nullptr, Aout, lda, n_rows, n, row0,
-           0, 0, 0, partials, counter, obj};
+           0, 0, 0, partials, counter, obj, nullptr, 0, 0, nullptr, 0};
   return rb_dispatch<true>(p, a, st);
+}
+
+// Row bounds of Z_new = offdiag(W - tC) + Diag(1 - W_ii + Z_ii), W = V diag(f) V^T: with
+// a_i = sum_k |f_k| V_ik^2, Cauchy-Schwarz gives |W_ij| <= sqrt(a_i a_j) <= sqrt(a_i) w_max
+// (w_max = max_j sqrt(a_j)); |t C_ij| <= |t| / 4 off the diagonal, so
+// max_j |Z_new_ij| <= B_i = max(sqrt(a_i) w_max + |t|/4, |1 - W_ii + Z_ii|).  Margins: the update's
+// own W_ij is a DMMA sum, within p u a_i of these (p <= 512: relative 1e-12 on the off-diagonal
+// term, absolute 1e-13 (a_i + 1 + |Z_ii|) on the diagonal one).  E_i = the digit-scale exponent
+// of B_i: every |Z_new_ij| < 2^E_i, as the digit expansion requires.
+__global__ void pfam_bound1_kernel(const double* __restrict__ VF, const double* __restrict__ V,
+                                   int64_t ldv, int n, int p, double2* __restrict__ wa,
+                                   unsigned long long* wmax) {
+  const int i = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (i >= n) return;
+  double s = 0.0, sa = 0.0;
+  for (int k = lane; k < p; k += 32) {
+    const double x = VF[(size_t)i * p + k] * V[(size_t)i * ldv + k];
+    s += x;
+    sa += fabs(x);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    sa += __shfl_xor_sync(0xffffffffu, sa, o);
+  }
+  if (lane == 0) {
+    wa[i] = make_double2(s, sa);
+    atomicMax(wmax, (unsigned long long)__double_as_longlong(sqrt(sa)));
+  }
+}
+
+__global__ void pfam_bound2_kernel(const double2* __restrict__ wa,
+                                   const unsigned long long* __restrict__ wmax,
+                                   const double* __restrict__ Z, int64_t ldz, int n, double t,
+                                   int* __restrict__ E, double* __restrict__ rscale) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double wm = __longlong_as_double((long long)*wmax);
+  const double2 w = wa[i];
+  const double zii = Z[(size_t)i * ldz + i];
+  const double off = (sqrt(w.y) * wm + 0.25 * fabs(t)) * (1.0 + 1e-12);
+  const double dg = fabs(1.0 - w.x + zii) + 1e-13 * (w.y + 1.0 + fabs(zii));
+  const int e = i8::scale_exp(fmax(off, dg));
+  E[i] = e;
+  rscale[i] = i8::pow2(e);
 }
 
 cudaError_t admm_launch(const double* V, int64_t ldv, const double* Vloc, int64_t ldvl,
                         const double* f, double t, const uint32_t* adj, int64_t ldadj,
                         const double* deg, double* Z, int64_t ldz, int n_rows, int n, int row0,
                         int p, double* obj, double* partials, int* counter, int raw, double* vf,
-                        cudaStream_t st) {
+                        cudaStream_t st, const RbDigits* dig) {
   cudaError_t e = scale_cols(Vloc, ldvl, f, n_rows, p, vf, st);
   if (e != cudaSuccess) return e;
   RbArgs a{V, ldv, vf, f, t, adj, ldadj, nullptr, 0, 0, 0, 0, deg, Z, ldz, n_rows, n, row0,
-           0, 0, raw, partials, counter, obj};
+           0, 0, raw, partials, counter, obj, nullptr, 0, 0, nullptr, 0};
+  if (dig && dig->A8 && row0 == 0 && n_rows == n) {
+    e = cudaMemsetAsync(dig->wmax, 0, 8, st);
+    if (e != cudaSuccess) return e;
+    count_launch();
+    pfam_bound1_kernel<<<(n + 7) / 8, 256, 0, st>>>(vf, Vloc, ldvl, n, p, dig->wa, dig->wmax);
+    count_launch();
+    pfam_bound2_kernel<<<(n + 255) / 256, 256, 0, st>>>(dig->wa, dig->wmax, Z, ldz, n, t,
+                                                        dig->E, dig->rscale);
+    a.A8 = dig->A8;
+    a.kpad = dig->kpad;
+    a.a8_slice = dig->a8_slice;
+    a.E = dig->E;
+    a.S = dig->S;
+  }
   return rb_dispatch<false>(p, a, st);
 }
 

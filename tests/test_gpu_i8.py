@@ -134,3 +134,48 @@ def test_graph_replay_bit_identical(cfg):
     b = run(cfg, graphs=True)["records"]
     for x, y in zip(a, b):
         assert np.array_equal(x["V"], y["V"]) and np.array_equal(x["f"], y["f"])
+
+
+def test_pfam_update_digits_match_fresh_split(monkeypatch):
+    """PFAM on one GPU: pf_admm_step writes Z_new's digit slices under its row bounds
+    (pf_rebuild.cu, K4 'fused digits'); the next product reuses them.  The product from
+    the fused digits is within the split bound of the exact Z_new Y, and agrees with a fresh split
+    (pf_invalidate) to the same bar; PF_FUSE_DIGITS=0 gives the same trajectory."""
+    from paper_1904_10585_b200 import run
+    from paper_1904_10585_b200._lib import Context, PF_FP64_I8
+    from pfinputs import pfam_problem
+    cfg = reduced(CONFIGS[3], n=1500, iters=3, edge_prob=82 / 1500, dtype="f64i8")
+    n, p = cfg.n, 64
+    prob = pfam_problem(cfg)
+    rs = np.random.default_rng(11)
+    V = np.linalg.qr(rs.standard_normal((n, p)))[0]
+    f = np.abs(rs.standard_normal(p)) * 3.0
+    f[5:9] = 0.0
+    Z0 = rs.standard_normal((n, n)) * 1e-2
+    Z0 = Z0 + Z0.T
+    from paper_1904_10585_b200.solver import _bits
+    c = Context(n, p, 4, dtype=PF_FP64_I8)
+    c.set_i8_slices(7)
+    Z = _pitched(Z0)
+    obj = torch.zeros(2, dtype=torch.float64, device="cuda")
+    c.admm_step(_dev(V), _dev(f), cfg.t, _bits(prob["adj_bits"]), _dev(prob["deg"]), Z, obj)
+    Zn = Z.cpu().numpy()
+    Y = rs.standard_normal((n, p))
+    out = torch.empty((n, p), dtype=torch.float64, device="cuda")
+    c.matmul(Z, _dev(Y), out)                           # reuses the fused digits
+    fused = out.cpu().numpy()
+    c.invalidate()
+    c.matmul(Z, _dev(Y), out)                           # fresh split of Z_new
+    fresh = out.cpu().numpy()
+    ref = Zn @ Y
+    scale = np.abs(Zn).max() * np.abs(Y).max() * n
+    ef, es = np.abs(fused - ref).max(), np.abs(fresh - ref).max()
+    assert ef <= 2.0 ** -44 * scale, (ef, es)
+    assert ef <= 16 * max(es, 1e-16 * scale), (ef, es)
+
+    a = run(cfg)["records"]
+    monkeypatch.setenv("PF_FUSE_DIGITS", "0")
+    b = run(cfg)["records"]
+    for x, y in zip(a, b):
+        den = max(O.lowrank_fro(x["V"], x["f"]), 1e-300)
+        assert O.lowrank_diff_fro(x["V"], x["f"], y["V"], y["f"]) <= 1e-10 * den

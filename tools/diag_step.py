@@ -56,4 +56,6 @@ def main(cfg_id=3, iters=14, **over):
 
 
 if __name__ == "__main__":
-    main(*[int(a) for a in sys.argv[1:3]])
+    # diag_step.py <cfg> <iters> [dtype]  (dtype f64i8 = the bench's int8-digit filter)
+    kw = {"dtype": sys.argv[3]} if len(sys.argv) > 3 else {}
+    main(*[int(a) for a in sys.argv[1:3]], **kw)
