@@ -252,11 +252,13 @@ pf_status pf_set_i8_slices(pf_ctx ctx, int32_t slices);
  * damped by the later steps.  Default: early_slices = S (no schedule). */
 pf_status pf_set_i8_schedule(pf_ctx ctx, int32_t early_slices, int32_t exact_tail);
 
-/* PF_FP64_I8: pf_filter splits A into digit slices on every call; pf_rayleigh_ritz and pf_matmul
- * reuse the slices of the last split of the same A (pointer, lda) unless a libpf call wrote an
- * iterate since (pf_prox_step, pf_admm_step, pf_nce_step, pf_extrapolate, pf_perturb).  A caller
- * that writes A by other means between pf_filter and pf_rayleigh_ritz calls pf_invalidate first.
- * No-op for other dtypes. */
+/* PF_FP64_I8: pf_filter splits A into digit slices, except right after pf_admm_step on one GPU,
+ * whose update writes the slices of Z_new itself (row scales from a bound on |Z_new|, DESIGN.md
+ * §4 "fused digits"; disabled by the environment variable PF_FUSE_DIGITS=0 at pf_create);
+ * pf_rayleigh_ritz and pf_matmul reuse the slices of the last split of the same A (pointer, lda)
+ * unless a libpf call wrote an iterate since (pf_prox_step, pf_nce_step, pf_extrapolate,
+ * pf_perturb; pf_admm_step leaves its own Z_new's slices valid).  A caller that writes A by other
+ * means between libpf calls calls pf_invalidate first.  No-op for other dtypes. */
 pf_status pf_invalidate(pf_ctx ctx);
 
 /* out = A Y with the context's filter GEMM (fp64 dtypes): A local rows (n_local x n, lda as for
