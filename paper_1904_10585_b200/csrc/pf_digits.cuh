@@ -46,6 +46,24 @@ PF_DEV void digit_words(double x, int E, uint32_t& wlo, uint32_t& whi) {
     whi = __vneg4(whi);
   }
 }
+// The same digits with U formed in fp64: |x| 2^(7S-E) < 2^7S is exact (a power-of-two scale sc,
+// no underflow that could reach 1), and adding 2^52 with round-toward-zero leaves trunc of it in
+// the low 52 bits of the sum.  Two fp64 instructions + a funnel shift replace the exponent
+// decode and the 64-bit variable shift.  Byte negation: -b = (0x80 - b) ^ 0x80 for b in [0, 127].
+template <int S>
+PF_DEV void digit_words_sc(double x, double sc, uint32_t& wlo, uint32_t& whi) {
+  const double y = __dadd_rz(fabs(x) * sc, 4503599627370496.0);
+  const unsigned long long b = (unsigned long long)__double_as_longlong(y);
+  const uint32_t l32 = (uint32_t)b, h32 = (uint32_t)(b >> 32);
+  const uint32_t lo = l32 & 0x0FFFFFFFu;
+  const uint32_t h = __funnelshift_r(l32, h32, 28);
+  wlo = (lo & 0x7Fu) | ((lo << 1) & 0x7F00u) | ((lo << 2) & 0x7F0000u) | ((lo << 3) & 0x7F000000u);
+  whi = (h & 0x7Fu) | ((h << 1) & 0x7F00u) | ((h << 2) & 0x7F0000u);
+  if (__double_as_longlong(x) < 0) {
+    wlo = (0x80808080u - wlo) ^ 0x80808080u;
+    whi = (0x80808080u - whi) ^ 0x80808080u;
+  }
+}
 // 4 x 4 byte transpose: t[b] = (byte b of w0, w1, w2, w3)
 PF_DEV void transpose4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3, uint32_t (&t)[4]) {
   const uint32_t a = __byte_perm(w0, w1, 0x5140), b = __byte_perm(w2, w3, 0x5140);
@@ -59,10 +77,18 @@ PF_DEV void transpose4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3, uint3
 template <int S>
 PF_DEV void slices4(double x0, double x1, double x2, double x3, int E, uint32_t (&out)[S]) {
   uint32_t l[4], h[4], tl[4], th[4];
-  digit_words<S>(x0, E, l[0], h[0]);
-  digit_words<S>(x1, E, l[1], h[1]);
-  digit_words<S>(x2, E, l[2], h[2]);
-  digit_words<S>(x3, E, l[3], h[3]);
+  if (E >= 7 * S - 1022) {  // 2^(7S-E) is a normal double: the fp64 form
+    const double sc = pow2(7 * S - E);
+    digit_words_sc<S>(x0, sc, l[0], h[0]);
+    digit_words_sc<S>(x1, sc, l[1], h[1]);
+    digit_words_sc<S>(x2, sc, l[2], h[2]);
+    digit_words_sc<S>(x3, sc, l[3], h[3]);
+  } else {
+    digit_words<S>(x0, E, l[0], h[0]);
+    digit_words<S>(x1, E, l[1], h[1]);
+    digit_words<S>(x2, E, l[2], h[2]);
+    digit_words<S>(x3, E, l[3], h[3]);
+  }
   transpose4(l[0], l[1], l[2], l[3], tl);
   transpose4(h[0], h[1], h[2], h[3], th);
 #pragma unroll

@@ -91,10 +91,9 @@ __device__ __forceinline__ void pair_of(int e, int T, int& I, int& J) {
 // consecutive columns; the mirror tile (rows j0.., columns i0..) reads Tz transposed
 template <int S>
 __device__ __forceinline__ void rb_digits(const RbArgs& a, const double* Tz, int i0, int j0,
-                                          bool mirror, int tid) {
+                                          bool mirror, int tid, int eI, int eJ) {
   const int r = tid >> 2, cb = (tid & 3) * 16;
-  auto put = [&](int row, int col0, const double (&v)[16]) {
-    const int E = a.E[row];
+  auto put = [&](int row, int col0, const double (&v)[16], int E) {
     uint32_t w[4][S];
 #pragma unroll
     for (int q = 0; q < 4; ++q)
@@ -111,13 +110,13 @@ __device__ __forceinline__ void rb_digits(const RbArgs& a, const double* Tz, int
     double v[16];
 #pragma unroll
     for (int q = 0; q < 16; ++q) v[q] = j0 + cb + q < a.n ? Tz[r * 65 + cb + q] : 0.0;
-    put(i0 + r, j0 + cb, v);
+    put(i0 + r, j0 + cb, v, eI);
   }
   if (mirror && j0 + r < a.n && i0 + cb < a.n) {
     double v[16];
 #pragma unroll
     for (int q = 0; q < 16; ++q) v[q] = i0 + cb + q < a.n ? Tz[(cb + q) * 65 + r] : 0.0;
-    put(j0 + r, i0 + cb, v);
+    put(j0 + r, i0 + cb, v, eJ);
   }
 }
 
@@ -151,6 +150,9 @@ __global__ void __launch_bounds__(kRbThreads, 2) rebuild_kernel(const RbArgs a) 
   const int t_begin = (int)(nt_all * blockIdx.x / gridDim.x);
   const int t_end = (int)(nt_all * (blockIdx.x + 1) / gridDim.x);
   int curI = -1;
+  // digits of the previous tile's Z_new (staged in Tz) are written during this tile's panel loads
+  int pv_i0 = -1, pv_j0 = 0, pv_eI = 0, pv_eJ = 0;
+  bool pv_mirror = false;
   for (int tile = t_begin; tile < t_end; ++tile) {
   int I, J;
   if (a.sym) {
@@ -209,6 +211,17 @@ __global__ void __launch_bounds__(kRbThreads, 2) rebuild_kernel(const RbArgs a) 
     }
   }
 
+  if (!PFPG && a.A8 && pv_i0 >= 0) {  // overlaps the cp.async panel loads in flight
+    if (a.S == 7) rb_digits<7>(a, Tz, pv_i0, pv_j0, pv_mirror, tid, pv_eI, pv_eJ);
+    else rb_digits<6>(a, Tz, pv_i0, pv_j0, pv_mirror, tid, pv_eI, pv_eJ);
+  }
+  // row exponents of this tile's digit rows, consumed one tile later (load latency hidden)
+  int eI = 0, eJ = 0;
+  if (!PFPG && a.A8) {
+    const int r = tid >> 2;
+    if (i0 + r < a.n_rows) eI = __ldg(a.E + i0 + r);
+    if (mirror && j0 + r < a.n) eJ = __ldg(a.E + j0 + r);
+  }
   // ---- PFAM: prefetch the old iterate at this thread's fragment positions (overlaps the MMA)
   double zo[2][2][kNt][2];
   if (!PFPG) {
@@ -363,13 +376,17 @@ __global__ void __launch_bounds__(kRbThreads, 2) rebuild_kernel(const RbArgs a) 
       }
     }
 
-    if (!PFPG && a.A8) {
-      // ---- digit slices of the Z_new tile (and of its mirror): coalesced 16-byte rows
-      __syncthreads();
-      if (a.S == 7) rb_digits<7>(a, Tz, i0, j0, mirror, tid);
-      else rb_digits<6>(a, Tz, i0, j0, mirror, tid);
-    }
+    pv_i0 = i0;  // digit slices of this tile: written after the next tile's barrier
+    pv_j0 = j0;
+    pv_mirror = mirror;
+    pv_eI = eI;
+    pv_eJ = eJ;
   }  // tile loop
+  if (!PFPG && a.A8 && pv_i0 >= 0) {
+    __syncthreads();
+    if (a.S == 7) rb_digits<7>(a, Tz, pv_i0, pv_j0, pv_mirror, tid, pv_eI, pv_eJ);
+    else rb_digits<6>(a, Tz, pv_i0, pv_j0, pv_mirror, tid, pv_eI, pv_eJ);
+  }
 
   // ---- deterministic reduction: block tree, then the last CTA sums CTA partials in order
   s0 = block_sum(s0, red);
