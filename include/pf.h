@@ -105,7 +105,9 @@ pf_status pf_get_device_status(pf_ctx ctx, pf_stream stream, uint32_t* flags, in
 /* m-step Lanczos with full re-orthogonalisation on the symmetric A (reading R5):
  * writes lo_hi[0] = theta_min - |r_min|, lo_hi[1] = theta_max + |r_max| (device double[2]),
  * and remembers them in the context.  v0: device start vector (n_local entries, any norm).
- * 1 <= m <= 64. */
+ * 1 <= m <= 64.  fp64 dtypes on one GPU (n <= 18944): only the 64 x 64 tiles on and above the
+ * diagonal of A are read (A must be symmetric, as the method's iterates are; half the HBM
+ * bytes); the environment variable PF_LZ_SYM=0 at pf_create reads all of A. */
 pf_status pf_lanczos(pf_ctx ctx, const void* A, int64_t lda, const double* v0, int32_t m,
                      double* lo_hi, pf_stream stream);
 

@@ -50,6 +50,7 @@ struct pf_ctx_s {
   double* lz_h = nullptr;                      // h1[kMaxLanczos], h2[kMaxLanczos], s[8]
   double* lz_part = nullptr;
   int* lz_cnt = nullptr;
+  double* lz_sym_ws = nullptr;                 // symmetric-GEMV tile partials (fp64, one GPU)
   double* lz_T = nullptr;
   double* lz_theta = nullptr;
   double* lz_S = nullptr;
@@ -257,6 +258,13 @@ static pf_status alloc_all(pf_ctx ctx) {
   ok &= A((void**)&ctx->lz_h, (size_t)(2 * kMaxLanczos + 8) * 8);
   ok &= A((void**)&ctx->lz_part, (size_t)lanczos_blocks((int)nl) * kMaxLanczos * 8);
   ok &= A((void**)&ctx->lz_cnt, 16);
+  // PF_LZ_SYM=0: the Lanczos GEMV reads all of A (else only its upper triangle, fp64 one GPU)
+  {
+    const char* e = getenv("PF_LZ_SYM");
+    const bool sym_ok = !(e && e[0] == '0') && !ctx->dist && !f32 &&
+                        n <= 32LL * lanczos_blocks((int)n);
+    if (sym_ok) ok &= A((void**)&ctx->lz_sym_ws, lz_symv_ws_doubles((int)n) * 8);
+  }
   ok &= A((void**)&ctx->lz_T, (size_t)kMaxLanczos * kMaxLanczos * 8);
   ok &= A((void**)&ctx->lz_theta, (size_t)kMaxLanczos * 8);
   ok &= A((void**)&ctx->lz_S, (size_t)kMaxLanczos * kMaxLanczos * 8);
@@ -774,6 +782,10 @@ pf_status pf_lanczos(pf_ctx ctx, const void* Av, int64_t lda, const double* v0, 
     if (f32)
       PF_CU(lz_gemv_f32_launch(A32, lda, nl, n, qfull, ctx->lz_Q, ctx->lz_ldq, j, ctx->lz_w, h1,
                                ctx->lz_part, ctx->lz_cnt, ctx->state, st));
+    else if (ctx->lz_sym_ws)  // A symmetric: upper triangle only (half the HBM bytes)
+      PF_CU(lz_symv_launch(A, lda, n, qfull, ctx->lz_Q, ctx->lz_ldq, j, ctx->lz_w, h1,
+                           ctx->lz_sym_ws, ctx->lz_part, ctx->lz_cnt, ctx->state, ctx->num_sms,
+                           st));
     else
       PF_CU(lz_gemv_launch(A, lda, nl, n, qfull, ctx->lz_Q, ctx->lz_ldq, j, ctx->lz_w, h1,
                            ctx->lz_part, ctx->lz_cnt, ctx->state, st));

@@ -172,6 +172,13 @@ cudaError_t lz_start_launch(const double* v0, int n_local, double* s, double* q0
 cudaError_t lz_gemv_launch(const double* A, int64_t lda, int n_local, int n, const double* q,
                            const double* Q, int64_t ldq, int j, double* w, double* h,
                            double* partials, int* counter, DevState* state, cudaStream_t st);
+// symmetric Lanczos GEMV (fp64, one GPU, n <= 32 lanczos_blocks(n)): reads only the upper
+// triangle of A; ws = lz_symv_ws_doubles(n) doubles of scratch
+size_t lz_symv_ws_doubles(int n);
+cudaError_t lz_symv_launch(const double* A, int64_t lda, int n, const double* q, const double* Q,
+                           int64_t ldq, int j, double* w, double* h, double* ws,
+                           double* partials, int* counter, DevState* state, int num_sms,
+                           cudaStream_t st);
 cudaError_t lz_orth_launch(int n_local, const double* Q, int64_t ldq, int j, double* w,
                            const double* h, double* out, double* partials, int* counter,
                            DevState* state, int phase, cudaStream_t st);

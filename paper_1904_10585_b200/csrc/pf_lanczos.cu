@@ -156,6 +156,224 @@ __global__ void __launch_bounds__(kLzThreads, 4) lz_gemv_kernel(
   }
 }
 
+// ---- symmetric GEMV (fp64, one GPU): w = A q from the upper triangle only -- half the HBM
+// bytes of lz_gemv_kernel (A is symmetric: the PFPG / PFAM iterates are written with exact
+// mirrors).  Pass 1: persistent CTAs walk contiguous ranges of the 64 x 64 tiles (I <= J) of
+// the upper triangle; tile (I, J) yields A_IJ q_J (rows of I) and, for I < J, A_IJ^T q_I (rows of
+// J), written as 64-vectors to ws (no atomics).  Pass 2 sums, for every row block R, the T
+// contributions in a fixed order, then the partial dots with Q_0..Q_j as lz_gemv_kernel.
+constexpr int kSyT = 64;
+
+__device__ __forceinline__ long long sym_tile_index(int I, int J, int T) {
+  return (long long)I * T - (long long)I * (I - 1) / 2 + (J - I);
+}
+
+__device__ __forceinline__ void sym_pair_of(long long e, int T, int& I, int& J) {
+  const double b = 2.0 * T + 1.0;
+  int i = (int)floor((b - sqrt(b * b - 8.0 * (double)e)) * 0.5);
+  if (i < 0) i = 0;
+  while (i > 0 && sym_tile_index(i, i, T) > e) --i;
+  while (i + 1 < T && sym_tile_index(i + 1, i + 1, T) <= e) ++i;
+  I = i;
+  J = i + (int)(e - sym_tile_index(i, i, T));
+}
+
+// 16-byte cp.async with zero fill past src_bytes (0, 8 or 16)
+__device__ __forceinline__ void lz_cp16(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(src_bytes)
+               : "memory");
+}
+
+// tile (I, J) of A -> smem stage (64 x 64, row-major): 2048 16-byte chunks, 8 per thread,
+// coalesced (a warp copies one 512-byte row); entries past n are zero-filled
+__device__ __forceinline__ void sym_issue(const double* __restrict__ A, int64_t lda, int n, int I,
+                                          int J, double* stage, int tid) {
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int ch = tid + 256 * u, r = ch >> 5, c = (ch & 31) * 2;
+    const int row = I * kSyT + r, col = J * kSyT + c;
+    const int bytes = (row < n) ? max(0, min(2, n - col)) * 8 : 0;
+    const double* src = bytes ? A + (size_t)row * lda + col : A;
+    lz_cp16(stage + r * kSyT + c, src, bytes);
+  }
+}
+
+constexpr int kSyStages = 3;  // tiles in flight per CTA (2 CTAs / SM: 6 x 32 KB per SM)
+
+// thread t: rows 4 (t / 16) .. +3 and columns {2c, 2c + 1, 32 + 2c, 33 + 2c}, c = t % 16
+__global__ void __launch_bounds__(256, 2) lz_symv_tiles_kernel(
+    const double* __restrict__ A, int64_t lda, int n, const double* __restrict__ q,
+    double* __restrict__ ws, DevState* state) {
+  if (state->lanczos_steps >= 0) return;
+  extern __shared__ __align__(16) double sy_smem[];
+  __shared__ double red[8][kSyT];
+  const int T = (n + kSyT - 1) / kSyT;
+  const long long nt = (long long)T * (T + 1) / 2;
+  const long long t0 = nt * blockIdx.x / gridDim.x, t1 = nt * (blockIdx.x + 1) / gridDim.x;
+  const int tid = threadIdx.x, rg = tid >> 4, cc = tid & 15, warp = tid >> 5, lane = tid & 31;
+  if (t0 >= t1) return;
+  // prologue: the first kSyStages - 1 tiles in flight
+  int In, Jn;  // next tile to issue
+  sym_pair_of(t0, T, In, Jn);
+  auto advance = [&](int& I, int& J) {
+    if (++J == T) {
+      ++I;
+      J = I;
+    }
+  };
+  long long issued = t0;
+#pragma unroll
+  for (int s = 0; s < kSyStages - 1; ++s) {
+    if (issued < t1) {
+      sym_issue(A, lda, n, In, Jn, sy_smem + (size_t)(s) * kSyT * kSyT, tid);
+      advance(In, Jn);
+      ++issued;
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
+  int I, J;
+  sym_pair_of(t0, T, I, J);
+  for (long long t = t0; t < t1; ++t) {
+    const int k = (int)((t - t0) % kSyStages);
+    __syncthreads();  // the stage about to be refilled was read by every thread (tile t - 1)
+    if (issued < t1) {
+      sym_issue(A, lda, n, In, Jn,
+                sy_smem + (size_t)((k + kSyStages - 1) % kSyStages) * kSyT * kSyT, tid);
+      advance(In, Jn);
+      ++issued;
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(kSyStages - 1) : "memory");
+    __syncthreads();
+    const double* tl = sy_smem + (size_t)k * kSyT * kSyT;
+    const int i0 = I * kSyT, j0 = J * kSyT;
+    double qc[4], qr[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = j0 + 2 * cc + (u & 1) + 32 * (u >> 1), r = i0 + 4 * rg + u;
+      qc[u] = c < n ? __ldg(q + c) : 0.0;
+      qr[u] = r < n ? __ldg(q + r) : 0.0;
+    }
+    double rs[4], cs[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+      const double* rowp = tl + (4 * rg + rr) * kSyT + 2 * cc;
+      const double2 v0 = *reinterpret_cast<const double2*>(rowp);
+      const double2 v1 = *reinterpret_cast<const double2*>(rowp + 32);
+      rs[rr] = ((v0.x * qc[0] + v0.y * qc[1]) + v1.x * qc[2]) + v1.y * qc[3];
+      cs[0] += v0.x * qr[rr];
+      cs[1] += v0.y * qr[rr];
+      cs[2] += v1.x * qr[rr];
+      cs[3] += v1.y * qr[rr];
+    }
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) rs[rr] += __shfl_xor_sync(0xffffffffu, rs[rr], o);
+    }
+    double* wrow = ws + (size_t)t * (2 * kSyT);
+    if (cc == 0) {
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr) __stcg(wrow + 4 * rg + rr, rs[rr]);
+    }
+    if (I < J) {  // column sums: the two row groups of a warp, then the 8 warps in order
+#pragma unroll
+      for (int u = 0; u < 4; ++u) cs[u] += __shfl_xor_sync(0xffffffffu, cs[u], 16);
+      if (lane < 16) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) red[warp][2 * cc + (u & 1) + 32 * (u >> 1)] = cs[u];
+      }
+      __syncthreads();
+      if (tid < kSyT) {
+        double v = 0.0;
+#pragma unroll
+        for (int w8 = 0; w8 < 8; ++w8) v += red[w8][tid];
+        __stcg(wrow + kSyT + tid, v);
+      }
+      // red is rewritten only after the next tile's two barriers
+    }
+    advance(I, J);
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+// w_i = sum_{J >= R} ws_row[(R, J)]_i + sum_{I < R} ws_col[(I, R)]_i (R = i / 64, fixed order),
+// then the partial dots h_i = Q_i . w as lz_gemv_kernel
+__global__ void __launch_bounds__(kLzThreads) lz_symv_reduce_kernel(
+    int n, const double* __restrict__ ws, const double* __restrict__ Q, int64_t ldq, int j,
+    double* __restrict__ w, double* __restrict__ h, double* __restrict__ partials, int* counter,
+    DevState* state) {
+  if (state->lanczos_steps >= 0) return;
+  __shared__ double part[8][32];
+  __shared__ double wsm[32];
+  __shared__ int s_last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = kLzThreads / 32;
+  const int T = (n + kSyT - 1) / kSyT;
+  const int rows_per = (n + gridDim.x - 1) / gridDim.x;  // <= 32 (lanczos_blocks)
+  const int r0 = blockIdx.x * rows_per, r1 = min(n, r0 + rows_per);
+  const int i = r0 + lane;
+  double s = 0.0;
+  if (lane < rows_per && i < r1) {
+    const int R = i / kSyT, ii = i - R * kSyT;
+#pragma unroll 8
+    for (int K = warp; K < T; K += nw) {  // independent loads, summed in K order
+      const long long t = K >= R ? sym_tile_index(R, K, T) : sym_tile_index(K, R, T);
+      s += __ldcg(ws + (size_t)t * (2 * kSyT) + (K >= R ? 0 : kSyT) + ii);
+    }
+  }
+  part[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0) {
+    double v = 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v += part[u][lane];
+    wsm[lane] = v;
+    if (lane < rows_per && i < r1) w[i] = v;
+  }
+  __syncthreads();
+  for (int k = warp; k <= j; k += nw) {
+    const double* qk = Q + (size_t)k * ldq;
+    double d = (lane < rows_per && i < r1) ? qk[i] * wsm[lane] : 0.0;
+    d = warp_sum(d);
+    if (lane == 0) partials[(size_t)blockIdx.x * kMaxLanczos + k] = d;
+  }
+  if (last_block_done(counter, &s_last)) {
+    __threadfence();
+    for (int k = warp; k <= j; k += nw) {
+      const double v = warp_reduce_partials(partials, (int)gridDim.x, k);
+      if (lane == 0) h[k] = v;
+    }
+    if (threadIdx.x == 0) *counter = 0;
+  }
+}
+
+size_t lz_symv_ws_doubles(int n) {
+  const long long T = (n + kSyT - 1) / kSyT;
+  return (size_t)(T * (T + 1) / 2) * 2 * kSyT;
+}
+
+cudaError_t lz_symv_launch(const double* A, int64_t lda, int n, const double* q, const double* Q,
+                           int64_t ldq, int j, double* w, double* h, double* ws,
+                           double* partials, int* counter, DevState* state, int num_sms,
+                           cudaStream_t st) {
+  const long long T = (n + kSyT - 1) / kSyT, nt = T * (T + 1) / 2;
+  const int grid = (int)std::max(1LL, std::min(nt, 2LL * num_sms));
+  const size_t smem = (size_t)kSyStages * kSyT * kSyT * 8;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(lz_symv_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attr = true;
+  }
+  count_launch();
+  lz_symv_tiles_kernel<<<grid, 256, smem, st>>>(A, lda, n, q, ws, state);
+  count_launch();
+  lz_symv_reduce_kernel<<<lanczos_blocks(n), kLzThreads, 0, st>>>(n, ws, Q, ldq, j, w, h,
+                                                                   partials, counter, state);
+  return cudaGetLastError();
+}
+
 // w -= Q h (local rows); phase 1: local partial dots -> out[0..j]; phase 2: local |w|^2 -> out[0]
 __global__ void __launch_bounds__(kLzThreads) lz_orth_kernel(
     int n_local, const double* __restrict__ Q, int64_t ldq, int j, double* __restrict__ w,
@@ -172,10 +390,28 @@ __global__ void __launch_bounds__(kLzThreads) lz_orth_kernel(
   __syncthreads();
   const int rows_per = (n_local + gridDim.x - 1) / gridDim.x;
   const int r0 = blockIdx.x * rows_per, r1 = min(n_local, r0 + rows_per);
-  for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
-    double v = w[r];
-    for (int i = 0; i <= j; ++i) v -= Q[(size_t)i * ldq + r] * hs[i];
-    w[r] = v;
+  if (rows_per <= 32) {
+    // lane = row, warp = vectors i = warp (mod 8): the j + 1 loads per row run in parallel; the
+    // 8 warp partials are combined in a fixed order
+    __shared__ double pq[kLzThreads / 32][32];
+    const int r = r0 + lane;
+    double v = 0.0;
+    if (r < r1)
+      for (int i = warp; i <= j; i += nw) v += Q[(size_t)i * ldq + r] * hs[i];
+    pq[warp][lane] = v;
+    __syncthreads();
+    if (warp == 0 && r < r1) {
+      double sum = 0.0;
+#pragma unroll
+      for (int u = 0; u < kLzThreads / 32; ++u) sum += pq[u][lane];
+      w[r] -= sum;
+    }
+  } else {
+    for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+      double v = w[r];
+      for (int i = 0; i <= j; ++i) v -= Q[(size_t)i * ldq + r] * hs[i];
+      w[r] = v;
+    }
   }
   __syncthreads();
   if (phase == 1) {
