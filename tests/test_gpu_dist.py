@@ -18,9 +18,13 @@ pytestmark = [pytest.mark.gpu,
                                  reduced(CONFIGS[3], n=1500, iters=4, edge_prob=82 / 1500,
                                          dtype="f64i8")],
                          ids=["pfam", "pfpg", "sweep", "tf32_sweep", "pfam_i8"])
-def test_single_rank_nccl_path_matches(cfg):
+def test_single_rank_nccl_path_matches(cfg, monkeypatch):
     from paper_1904_10585_b200 import run
     from paper_1904_10585_b200._lib import nccl_unique_id
+    # one-GPU-only shortcuts off (upper-triangle Lanczos GEMV, digits written by the PFAM
+    # update): both runs then do the same arithmetic
+    monkeypatch.setenv("PF_LZ_SYM", "0")
+    monkeypatch.setenv("PF_FUSE_DIGITS", "0")
     a = run(cfg)["records"]
     b = run(cfg, nccl_id=nccl_unique_id(), rank=0, world=1)["records"]
     for x, y in zip(a, b):
