@@ -69,6 +69,14 @@ PF_DEV void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t ide
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// one lane of a converged warp (always the same one: the lowest active lane)
+PF_DEV bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n.reg .pred p;\nelect.sync _|p, 0xffffffff;\nselp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
 PF_DEV void mma_commit(uint64_t* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
@@ -375,33 +383,39 @@ __global__ void __launch_bounds__(I8Cfg<S, NC>::THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer (one lane)
-    if (lane == 0) {
-      RingI ra(C::NA), rb(C::NB);
-      uint32_t tph = 0;
-      SegIter si(U, G, blockIdx.x, KB);
-      int it, kbs, kbe;
-      while (si.next(it, kbs, kbe)) {
-        for (int k0 = kbs; k0 < kbe; k0 += kch) {
-          const int k1 = min(kbe, k0 + kch);
-          mbar_wait(tempty, tph ^ 1u);  // the epilogue drained the accumulators
-          tc::fence_after_sync();
-          for (int kb = k0; kb < k1; ++kb) {
-            mbar_wait(&bfull[rb.s], rb.ph);
-            const uint32_t b0 = smem_u32(ring_b + rb.s * C::B_STAGE);
-#pragma unroll 1
-            for (int s = 0; s < S; ++s, ra.next()) {
-              mbar_wait(&afull[ra.s], ra.ph);
-              tc::fence_after_sync();
-              const uint32_t a0 = smem_u32(ring_a + ra.s * C::A_TILE);
+    // ------------------------------------------------------------ MMA issuer (one warp)
+    // The whole warp runs the loop (its values are warp-uniform, so descriptors and TMEM
+    // addresses live in uniform registers) and one elected lane issues: issuing from a lone
+    // thread made every MMA wait for a scalar-to-uniform broadcast of its seven operands
+    // (~100 cycles each, more than the N = 64..256 MMA itself).
+    RingI ra(C::NA), rb(C::NB);
+    uint32_t tph = 0;
+    SegIter si(U, G, blockIdx.x, KB);
+    int it, kbs, kbe;
+    const uint32_t ring_a0 = smem_u32(ring_a), ring_b0 = smem_u32(ring_b);
+    while (si.next(it, kbs, kbe)) {
+      for (int k0 = kbs; k0 < kbe; k0 += kch) {
+        const int k1 = min(kbe, k0 + kch);
+        mbar_wait(tempty, tph ^ 1u);  // the epilogue drained the accumulators
+        tc::fence_after_sync();
+        for (int kb = k0; kb < k1; ++kb) {
+          mbar_wait(&bfull[rb.s], rb.ph);
+          const uint32_t b0 = ring_b0 + rb.s * C::B_STAGE;
+#pragma unroll
+          for (int s = 0; s < S; ++s) {
+            mbar_wait(&afull[ra.s], ra.ph);
+            tc::fence_after_sync();
+            const uint32_t a0 = ring_a0 + ra.s * C::A_TILE;
+            if (i8::elect_one()) {
 #pragma unroll
               for (int ks = 0; ks < 2; ++ks) {
                 const uint32_t acc = (kb == k0 && s == 0 && ks == 0) ? 0u : 1u;
                 const uint64_t ad = tc::sdesc_k_sw64(a0 + ks * 32);
-                // A_s x [B_0 .. B_{S-1-s}] -> levels s .. S-1 (0-based), chunks of <= CMAX slices;
-                // s = 0 initialises every level
+                // A_s x [B_0 .. B_{S-1-s}] -> levels s .. S-1 (0-based), chunks of <= CMAX
+                // slices; s = 0 initialises every level
+#pragma unroll
                 for (int t0 = 0; t0 < S - s; t0 += C::CMAX) {
-                  const int c = min(C::CMAX, S - s - t0);
+                  const int c = (S - s - t0) < C::CMAX ? (S - s - t0) : C::CMAX;
                   i8::mma_i8(tmem + (uint32_t)((s + t0) * NC), ad,
                              tc::sdesc_k_sw64(b0 + t0 * NC * C::BK + ks * 32),
                              i8::idesc_i8(C::BM, c * NC), acc);
@@ -409,12 +423,16 @@ __global__ void __launch_bounds__(I8Cfg<S, NC>::THREADS, 1)
               }
               i8::mma_commit(&aempty[ra.s]);  // A slice stage free once these MMAs complete
             }
-            i8::mma_commit(&bempty[rb.s]);
-            rb.next();
+            __syncwarp();
+            ra.next();
           }
-          i8::mma_commit(tfull);
-          tph ^= 1u;
+          if (i8::elect_one()) i8::mma_commit(&bempty[rb.s]);
+          __syncwarp();
+          rb.next();
         }
+        if (i8::elect_one()) i8::mma_commit(tfull);
+        __syncwarp();
+        tph ^= 1u;
       }
     }
   } else if (warp >= 4) {
