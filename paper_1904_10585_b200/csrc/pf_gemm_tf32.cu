@@ -232,7 +232,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tf32Cfg<P>::THREADS,
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (pair leader)
-    if (crank == 0 && lane == 0) {
+    // the whole warp runs the loop (warp-uniform operands in uniform registers), one elected
+    // lane issues (see pf_gemm_i8.cu)
+    if (crank == 0) {
       const uint32_t idesc = tc::idesc_tf32(256, C::NMMA);
       Ring rt(C::NT), rl(C::NL);
       uint32_t tphase = 0;
@@ -246,13 +248,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tf32Cfg<P>::THREADS,
         tc::fence_after_sync();
         for (int kb = s0; kb < s1; ++kb, rt.next(), rl.next()) {
           // the converters of BOTH CTAs saw this raw stage land and wrote its lo copy
-          TRACE(3, w, kb - kb0);
+          if (lane == 0) TRACE(3, w, kb - kb0);
           tc::mbar_wait_cluster(&ready[rl.s], rl.ph);
           tc::fence_after_sync();
-          TRACE(4, w, kb - kb0);
+          if (lane == 0) TRACE(4, w, kb - kb0);
           const uint32_t a_hi = smem_u32(raw + rt.s * C::STAGE_BYTES);
           const uint32_t a_lo = smem_u32(low + rl.s * C::STAGE_BYTES);
           const uint32_t b_hi = a_hi + C::A_BYTES, b_lo = a_lo + C::A_BYTES;
+          if (tc::elect_one()) {
 #pragma unroll
           for (int ks = 0; ks < C::BK / 8; ++ks) {
 #pragma unroll
@@ -272,8 +275,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Tf32Cfg<P>::THREADS,
           }
           tc::mma_commit_pair(&empty[rt.s]);  // raw stage free in both CTAs
           tc::mma_commit_pair(&lfree[rl.s]);  // lo stage free in both CTAs
+          }
+          __syncwarp();
         }
-        tc::mma_commit_pair(tfull);  // accumulator complete -> both epilogues
+        if (tc::elect_one()) tc::mma_commit_pair(tfull);  // accumulator complete -> epilogues
+        __syncwarp();
         tphase ^= 1u;
         }
       }
