@@ -352,33 +352,41 @@ __global__ void __launch_bounds__(I8Cfg<S, NC>::THREADS, 1)
   const int G = gridDim.x;
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer (one lane)
-    if (lane == 0) {
-      RingI ra(C::NA), rb(C::NB);
-      const uint64_t pol_a = tc::policy_evict_first(), pol_b = tc::policy_evict_last();
-      SegIter si(U, G, blockIdx.x, KB);
-      int it, kbs, kbe;
-      while (si.next(it, kbs, kbe)) {
-        const int cg = it / args.mtiles, tile = it - cg * args.mtiles;  // column-group major
-        if (args.pf_dist > 0)  // warm the first k-blocks of the segment into L2
-          for (int kb = kbs; kb < min(kbe, kbs + args.pf_dist); ++kb)
-            tc::tma_prefetch_3d(&mapA8pf, kb * C::BK, tile * C::BM, 0, pol_a);
-        for (int kb = kbs; kb < kbe; ++kb) {
-          // A streams from HBM once: every slice of k-block kb + pf_dist into L2 ahead of its load
-          if (args.pf_dist > 0 && kb + args.pf_dist < kbe)
-            tc::tma_prefetch_3d(&mapA8pf, (kb + args.pf_dist) * C::BK, tile * C::BM, 0, pol_a);
-          mbar_wait(&bempty[rb.s], rb.ph ^ 1u);
+    // ------------------------------------------------------------ TMA producer (one warp)
+    // warp-uniform loop, one elected lane issues (as the MMA issuer)
+    RingI ra(C::NA), rb(C::NB);
+    const uint64_t pol_a = tc::policy_evict_first(), pol_b = tc::policy_evict_last();
+    SegIter si(U, G, blockIdx.x, KB);
+    int it, kbs, kbe;
+    while (si.next(it, kbs, kbe)) {
+      const int cg = it / args.mtiles, tile = it - cg * args.mtiles;  // column-group major
+      if (args.pf_dist > 0 && i8::elect_one())  // warm the first k-blocks of the segment
+        for (int kb = kbs; kb < min(kbe, kbs + args.pf_dist); ++kb)
+          tc::tma_prefetch_3d(&mapA8pf, kb * C::BK, tile * C::BM, 0, pol_a);
+      __syncwarp();
+      for (int kb = kbs; kb < kbe; ++kb) {
+        // A streams from HBM once: every slice of k-block kb + pf_dist into L2 ahead of its load
+        if (args.pf_dist > 0 && kb + args.pf_dist < kbe && i8::elect_one())
+          tc::tma_prefetch_3d(&mapA8pf, (kb + args.pf_dist) * C::BK, tile * C::BM, 0, pol_a);
+        __syncwarp();
+        mbar_wait(&bempty[rb.s], rb.ph ^ 1u);
+        if (i8::elect_one()) {
           mbar_arrive_expect_tx(&bfull[rb.s], C::B_LOAD);
           tc::tma_load_3d_hint(ring_b + rb.s * C::B_STAGE, &mapY8, &bfull[rb.s], kb * C::BK,
                                cg * NC, 0, pol_b);
-          rb.next();
-#pragma unroll 1
-          for (int s = 0; s < S; ++s, ra.next()) {
-            mbar_wait(&aempty[ra.s], ra.ph ^ 1u);
+        }
+        __syncwarp();
+        rb.next();
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          mbar_wait(&aempty[ra.s], ra.ph ^ 1u);
+          if (i8::elect_one()) {
             mbar_arrive_expect_tx(&afull[ra.s], C::A_TILE);
             tc::tma_load_3d_hint(ring_a + ra.s * C::A_TILE, &mapA8, &afull[ra.s], kb * C::BK,
                                  tile * C::BM, s, pol_a);
           }
+          __syncwarp();
+          ra.next();
         }
       }
     }
