@@ -98,7 +98,7 @@ struct pf_ctx_s {
   // ---- fp64 via exact int8 tensor-core products (dtype PF_FP64_I8, pf_gemm_i8.cu)
   bool i8 = false;
   I8Plan i8plan;                               // S = 0: this context runs the DMMA GEMM
-  int8_t* A8 = nullptr;                        // [kI8MaxSlices][n_local][kpad]
+  int8_t* A8 = nullptr;                        // tiled digit slices (pf_digits.cuh a8_offset)
   double* a8_rscale = nullptr;                 // [n_local]
   int8_t* Y8 = nullptr;                        // [kI8MaxSlices][p][kpad]
   double* y8_cscale = nullptr;                 // [p]
@@ -226,7 +226,8 @@ static pf_status alloc_all(pf_ctx ctx) {
   }
   if (ctx->i8) {
     const I8Plan& ip = ctx->i8plan;
-    ok &= A((void**)&ctx->A8, (size_t)kI8MaxSlices * nl * ip.kpad);
+    // tiled digit slices: (128-row tiles) x (64-byte k-blocks) x S blocks of 8 KB
+    ok &= A((void**)&ctx->A8, (size_t)ip.mtiles * ip.kblocks * kI8MaxSlices * 8192);
     ok &= A((void**)&ctx->a8_rscale, (size_t)nl * 8);
     ok &= A((void**)&ctx->a8_E, (size_t)nl * 4);
     ok &= A((void**)&ctx->a8_wa, (size_t)nl * 16);
@@ -994,8 +995,7 @@ pf_status pf_admm_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f
   // one GPU, int8-digit filter: the update writes Z_new's digit slices for the next pf_filter
   const bool fuse = use_i8(ctx) && !ctx->dist && ctx->fuse_digits &&
                     (ctx->i8plan.S == 6 || ctx->i8plan.S == 7);
-  RbDigits dig{ctx->A8, ctx->i8plan.kpad, ctx->i8plan.kpad * ctx->n_local, ctx->i8plan.S,
-               ctx->a8_E, ctx->a8_rscale, ctx->a8_wa, ctx->a8_wmax};
+  RbDigits dig{ctx->A8, ctx->i8plan.kblocks, ctx->i8plan.S, ctx->a8_E, ctx->a8_rscale, ctx->a8_wa, ctx->a8_wmax};
   PF_CU(admm_launch(Vf, ldf, V, ldv, f, t, adj, ldadj, deg, Z, ldz, (int)ctx->n_local,
                     (int)ctx->n, (int)ctx->row0, ctx->p, obj, ctx->rb_part, ctx->rb_cnt,
                     ctx->dist ? 1 : 0, ctx->VFbuf, st, fuse ? &dig : nullptr));

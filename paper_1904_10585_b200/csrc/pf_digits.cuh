@@ -7,6 +7,12 @@
 namespace pf {
 namespace i8 {
 
+// Byte offset of digit slice s of A(row, col) in the tiled A8 layout the K1-i8 GEMM streams:
+// [tile = row / 128][k-block = col / 64][slice s < S][row % 128][col % 64] -- every TMA box
+// (one slice of one 128 x 64-byte tile) is a contiguous 8 KB block of HBM.
+PF_DEV size_t a8_offset(int row, int col, int s, int KB, int S) {
+  return ((((size_t)(row >> 7) * KB + (col >> 6)) * S + s) << 13) + ((row & 127) << 6) + (col & 63);
+}
 // exact power of two 2^k as a double (|k| <= 1022)
 PF_DEV double pow2(int k) { return __longlong_as_double((long long)(1023 + k) << 52); }
 // scale exponent E of a row / column with max |x| = m: |x| 2^-E < 1 (frexp), 0 for m == 0

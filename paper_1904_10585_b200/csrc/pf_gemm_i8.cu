@@ -20,7 +20,8 @@
 // scales -- the same order as an fp64 GEMM's own rounding bound (n u |A| |B|).
 //
 // Kernel structure (one CTA per SM, persistent over (128-row tile, column group) items):
-//  * warp 0: TMA producer.  A slices live as [S][n_rows][kpad] int8: each A stage is ONE slice's
+//  * warp 0: TMA producer.  A slices live tiled, [128-row tile][k-block][S][128][64] int8
+//    (pf_digits.cuh a8_offset): each A stage is ONE slice's contiguous 8 KB
 //    128 x 64-byte box (8 KB) -- small stages so the ring is deep (TMA latency), A tagged L2
 //    evict_first.  B = the digit slices of Y stored K-major [S][p][kpad]: one 3-D box
 //    {64 B, NC columns, S slices} per k-block, L2 evict_last (re-read by every tile).
@@ -97,16 +98,15 @@ PF_DEV void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 }  // namespace i8
 
 // ------------------------------------------------------------------------------ A splitting
-// A (n_rows x n_k fp64, lda) -> A8[s][row][kpad] int8 digit slices, rscale[row] = 2^E_row.
+// A (n_rows x n_k fp64, lda) -> tiled int8 digit slices A8 (a8_offset), rscale[row] = 2^E_row.
 // One CTA per row at a time: pass 1 the row max (HBM), pass 2 re-reads the row (L2) and writes
 // the S slices, 8 digits (8 bytes) per thread per slice.
 template <int S>
 __global__ void __launch_bounds__(512) a_split_kernel(const double* __restrict__ A, int64_t lda,
                                                       int n_rows, int n_k, int8_t* __restrict__ A8,
-                                                      int64_t kpad, double* __restrict__ rscale) {
+                                                      int KB, double* __restrict__ rscale) {
   __shared__ double red[32];
   const int tid = threadIdx.x, nt = blockDim.x;
-  const int64_t slice = (int64_t)n_rows * kpad;
   for (int row = blockIdx.x; row < n_rows; row += gridDim.x) {
     const double* a = A + (int64_t)row * lda;
     double m = 0.0;
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(512) a_split_kernel(const double* __restrict__
     __syncthreads();
     const int E = i8::scale_exp(red[0]);
     if (tid == 0) rscale[row] = i8::pow2(E);
-    int8_t* o = A8 + (int64_t)row * kpad;
+    int8_t* o = A8 + i8::a8_offset(row, 0, 0, KB, S);  // (row, k-block 0, slice 0)
     for (int j0 = tid * 8; j0 < n_k; j0 += nt * 8) {
       if (j0 + 8 <= n_k) {
         const double2 v0 = __ldcs(reinterpret_cast<const double2*>(a + j0));
@@ -143,11 +143,13 @@ __global__ void __launch_bounds__(512) a_split_kernel(const double* __restrict__
         i8::slices4<S>(v2.x, v2.y, v3.x, v3.y, E, hi);
 #pragma unroll
         for (int s = 0; s < S; ++s)
-          __stcs(reinterpret_cast<uint2*>(o + s * slice + j0), make_uint2(lo[s], hi[s]));
+          __stcs(reinterpret_cast<uint2*>(o + ((size_t)(j0 >> 6) * S + s) * 8192 + (j0 & 63)),
+                 make_uint2(lo[s], hi[s]));
       } else {
         for (int j = j0; j < n_k; ++j)
 #pragma unroll
-          for (int s = 0; s < S; ++s) o[s * slice + j] = i8::digit<S>(a[j], E, s);
+          for (int s = 0; s < S; ++s)
+            o[((size_t)(j >> 6) * S + s) * 8192 + (j & 63)] = i8::digit<S>(a[j], E, s);
       }
     }
     __syncthreads();  // red[] reuse
@@ -245,6 +247,7 @@ struct I8Cfg {
 
 struct I8Args {
   int pf_dist;           // L2 prefetch distance of the A k-blocks (0: off)
+  int lS;                // slices per (tile, k-block) in the A8 layout (the split's S >= S used)
   const double* ycur;
   const double* yprev;
   double* out;
@@ -362,12 +365,12 @@ __global__ void __launch_bounds__(I8Cfg<S, NC>::THREADS, 1)
       const int cg = it / args.mtiles, tile = it - cg * args.mtiles;  // column-group major
       if (args.pf_dist > 0 && i8::elect_one())  // warm the first k-blocks of the segment
         for (int kb = kbs; kb < min(kbe, kbs + args.pf_dist); ++kb)
-          tc::tma_prefetch_3d(&mapA8pf, kb * C::BK, tile * C::BM, 0, pol_a);
+          tc::tma_prefetch_3d(&mapA8pf, 0, 0, (tile * KB + kb) * args.lS, pol_a);
       __syncwarp();
       for (int kb = kbs; kb < kbe; ++kb) {
         // A streams from HBM once: every slice of k-block kb + pf_dist into L2 ahead of its load
         if (args.pf_dist > 0 && kb + args.pf_dist < kbe && i8::elect_one())
-          tc::tma_prefetch_3d(&mapA8pf, (kb + args.pf_dist) * C::BK, tile * C::BM, 0, pol_a);
+          tc::tma_prefetch_3d(&mapA8pf, 0, 0, (tile * KB + kb + args.pf_dist) * args.lS, pol_a);
         __syncwarp();
         mbar_wait(&bempty[rb.s], rb.ph ^ 1u);
         if (i8::elect_one()) {
@@ -382,8 +385,8 @@ __global__ void __launch_bounds__(I8Cfg<S, NC>::THREADS, 1)
           mbar_wait(&aempty[ra.s], ra.ph ^ 1u);
           if (i8::elect_one()) {
             mbar_arrive_expect_tx(&afull[ra.s], C::A_TILE);
-            tc::tma_load_3d_hint(ring_a + ra.s * C::A_TILE, &mapA8, &afull[ra.s], kb * C::BK,
-                                 tile * C::BM, s, pol_a);
+            tc::tma_load_3d_hint(ring_a + ra.s * C::A_TILE, &mapA8, &afull[ra.s], 0, 0,
+                                 (tile * KB + kb) * args.lS + s, pol_a);
           }
           __syncwarp();
           ra.next();
@@ -600,8 +603,10 @@ I8Plan i8_plan(int p, int n_rows, int n_k, int slices, int num_sms) {
 }
 
 bool i8_encode_A(CUtensorMap* map, CUtensorMap* map_pf, const int8_t* A8, const I8Plan& pl) {
-  return encode_map_i8_3d(map, A8, pl.kpad, pl.kpad * pl.n_rows, pl.n_k, pl.n_rows, pl.S, 128, 1) &&
-         encode_map_i8_3d(map_pf, A8, pl.kpad, pl.kpad * pl.n_rows, pl.n_k, pl.n_rows, pl.S, 128,
+  // tiled layout: 8 KB blocks (64 bytes x 128 rows), one per (tile, k-block, slice)
+  const int blocks = pl.mtiles * pl.kblocks * pl.S;
+  return encode_map_i8_3d(map, A8, 64, 8192, 64, 128, blocks, 128, 1) &&
+         encode_map_i8_3d(map_pf, A8, 64, 8192, 64, 128, blocks, 128,
                           pl.S, false);
 }
 bool i8_encode_B(CUtensorMap* map, const int8_t* Y8, const I8Plan& pl, int su) {
@@ -613,7 +618,7 @@ static cudaError_t a_split_s(const double* A, int64_t lda, const I8Plan& pl, int
                              double* rscale, int num_sms, cudaStream_t st) {
   count_launch();
   a_split_kernel<S><<<std::min(pl.n_rows, 2 * num_sms), 512, 0, st>>>(A, lda, pl.n_rows, pl.n_k,
-                                                                      A8, pl.kpad, rscale);
+                                                                      A8, pl.kblocks, rscale);
   return cudaGetLastError();
 }
 cudaError_t i8_split_A_launch(const double* A, int64_t lda, const I8Plan& pl, int8_t* A8,
@@ -705,6 +710,7 @@ cudaError_t i8_gemm_launch(const I8Plan& pl, const CUtensorMap& mapA8, const CUt
   a.ngroups = pl.ngroups;
   a.chunk_kb = pl.chunk_kb;
   a.pf_dist = pl.pf_dist;
+  a.lS = pl.S;
   if (su < 4 || su > pl.S) return cudaErrorInvalidValue;
   switch (su) {
     case 4: return i8_launch_s<4>(pl, mapA8, mapY8, mapA8pf, a, st);

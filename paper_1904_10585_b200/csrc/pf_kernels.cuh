@@ -57,7 +57,8 @@ cudaError_t tf32_gemm_launch(const Tf32Plan& pl, const CUtensorMap& mapA, const 
                              int npass, cudaStream_t st, int bdist_kb = 0);
 
 // ---- fp64 filter GEMM from exact int8 tensor-core products of S-digit splits (pf_gemm_i8.cu).
-// A8: [S][n_rows][kpad] int8 digit slices of A (row scales rscale), Y8: [S][p][kpad] K-major
+// A8: tiled int8 digit slices of A (pf_digits.cuh a8_offset; mtiles x kblocks x S blocks of
+// 8 KB; row scales rscale), Y8: [S][p][kpad] K-major
 // slices of the B block (column scales cscale).
 struct I8Plan {
   int p, S, NC, ngroups;  // NC = columns per work item (<= 64), ngroups = p / NC
@@ -198,10 +199,10 @@ cudaError_t prox_launch(const double* V, int64_t ldv, const double* Vloc, int64_
                         int n_rows, int n, int row0, int p, double* obj, double* partials,
                         int* counter, double* vf, cudaStream_t st);
 // PF_FP64_I8 on one GPU: the PFAM update also writes the digit slices of Z_new (pf_gemm_i8.cu
-// layout [S][n][kpad]) and their row scales, so the next filter skips its split pass
+// tiled layout, a8_offset) and their row scales, so the next filter skips its split pass
 struct RbDigits {
   int8_t* A8;
-  int64_t kpad, a8_slice;
+  int KB;                   // k-blocks of the tiled layout
   int S;
   int* E;                   // [n] row exponents
   double* rscale;           // [n] 2^E

@@ -54,9 +54,10 @@ struct RbArgs {
   double* obj;
   // PF_FP64_I8 (PFAM, one GPU): the update also writes the S-digit slices of Z_new for the next
   // filter (A8 != nullptr): row exponents E (row bounds computed before the update), slices
-  // [S][n][kpad] with slice stride a8_slice -- the separate split pass over Z disappears
+  // in the tiled layout of pf_digits.cuh a8_offset (KB k-blocks) -- the separate split pass over
+  // Z disappears
   int8_t* A8;
-  int64_t kpad, a8_slice;
+  int KB;
   const int* E;
   int S;
 };
@@ -98,13 +99,14 @@ __device__ __forceinline__ void rb_digits(const RbArgs& a, const double* Tz, int
 #pragma unroll
     for (int q = 0; q < 4; ++q)
       i8::slices4<S>(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3], E, w[q]);
-    int8_t* dst = a.A8 + (size_t)row * a.kpad + col0;
+    int8_t* dst = a.A8 + i8::a8_offset(row, col0, 0, a.KB, S);  // 16 bytes inside one k-block
 #pragma unroll
     for (int sl = 0; sl < S; ++sl)
-      __stcs(reinterpret_cast<uint4*>(dst + sl * a.a8_slice),
+      __stcs(reinterpret_cast<uint4*>(dst + sl * 8192),
              make_uint4(w[0][sl], w[1][sl], w[2][sl], w[3][sl]));
   };
-  // kpad is a multiple of 16, so a chunk starting below n lies inside the row; entries past n
+  // a 16-column chunk starting below n lies inside the padded row (KB 64-byte k-blocks); entries
+  // past n
   // (never read: the GEMM's tensor map ends at n) are written as 0
   if (i0 + r < a.n_rows && j0 + cb < a.n) {
     double v[16];
@@ -504,7 +506,7 @@ cudaError_t prox_launch(const double* V, int64_t ldv, const double* Vloc, int64_
   RbArgs a{V, ldv, vf, f, tau, omega, ldo, W, ldw, r, 0,
            (r > 0 && (ldw & 1) == 0 && (reinterpret_cast<uintptr_t>(W) & 15) == 0) ? 1 : 0,
            nullptr, Aout, lda, n_rows, n, row0,
-           0, 0, 0, partials, counter, obj, nullptr, 0, 0, nullptr, 0};
+           0, 0, 0, partials, counter, obj, nullptr, 0, nullptr, 0};
   return rb_dispatch<true>(p, a, st);
 }
 
@@ -561,7 +563,7 @@ cudaError_t admm_launch(const double* V, int64_t ldv, const double* Vloc, int64_
   cudaError_t e = scale_cols(Vloc, ldvl, f, n_rows, p, vf, st);
   if (e != cudaSuccess) return e;
   RbArgs a{V, ldv, vf, f, t, adj, ldadj, nullptr, 0, 0, 0, 0, deg, Z, ldz, n_rows, n, row0,
-           0, 0, raw, partials, counter, obj, nullptr, 0, 0, nullptr, 0};
+           0, 0, raw, partials, counter, obj, nullptr, 0, nullptr, 0};
   if (dig && dig->A8 && row0 == 0 && n_rows == n) {
     e = cudaMemsetAsync(dig->wmax, 0, 8, st);
     if (e != cudaSuccess) return e;
@@ -571,8 +573,7 @@ cudaError_t admm_launch(const double* V, int64_t ldv, const double* Vloc, int64_
     pfam_bound2_kernel<<<(n + 255) / 256, 256, 0, st>>>(dig->wa, dig->wmax, Z, ldz, n, t,
                                                         dig->E, dig->rscale);
     a.A8 = dig->A8;
-    a.kpad = dig->kpad;
-    a.a8_slice = dig->a8_slice;
+    a.KB = dig->KB;
     a.E = dig->E;
     a.S = dig->S;
   }
