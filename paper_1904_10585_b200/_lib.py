@@ -259,7 +259,7 @@ class Context:
         self._check(self.lib.pf_set_tf32_passes(self.h, passes), "pf_set_tf32_passes")
 
     def set_i8_slices(self, slices: int):
-        """PF_FP64_I8: digit slices per operand (6..8), 0 = the fp64 DMMA GEMM."""
+        """PF_FP64_I8: digit slices per operand (6 or 7), 0 = the fp64 DMMA GEMM."""
         self._check(self.lib.pf_set_i8_slices(self.h, slices), "pf_set_i8_slices")
 
     def set_i8_schedule(self, early_slices: int, exact_tail: int):

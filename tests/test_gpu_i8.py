@@ -136,7 +136,8 @@ def test_graph_replay_bit_identical(cfg):
         assert np.array_equal(x["V"], y["V"]) and np.array_equal(x["f"], y["f"])
 
 
-def test_pfam_update_digits_match_fresh_split(monkeypatch):
+@pytest.mark.parametrize("slices", [7, 6])
+def test_pfam_update_digits_match_fresh_split(monkeypatch, slices):
     """PFAM on one GPU: pf_admm_step writes Z_new's digit slices under its row bounds
     (pf_rebuild.cu, K4 'fused digits'); the next product reuses them.  The product from
     the fused digits is within the split bound of the exact Z_new Y, and agrees with a fresh split
@@ -155,7 +156,7 @@ def test_pfam_update_digits_match_fresh_split(monkeypatch):
     Z0 = Z0 + Z0.T
     from paper_1904_10585_b200.solver import _bits
     c = Context(n, p, 4, dtype=PF_FP64_I8)
-    c.set_i8_slices(7)
+    c.set_i8_slices(slices)
     Z = _pitched(Z0)
     obj = torch.zeros(2, dtype=torch.float64, device="cuda")
     c.admm_step(_dev(V), _dev(f), cfg.t, _bits(prob["adj_bits"]), _dev(prob["deg"]), Z, obj)
@@ -170,12 +171,34 @@ def test_pfam_update_digits_match_fresh_split(monkeypatch):
     ref = Zn @ Y
     scale = np.abs(Zn).max() * np.abs(Y).max() * n
     ef, es = np.abs(fused - ref).max(), np.abs(fresh - ref).max()
-    assert ef <= 2.0 ** -44 * scale, (ef, es)
+    assert ef <= 2.0 ** (5 - 7 * slices) * scale, (ef, es)
     assert ef <= 16 * max(es, 1e-16 * scale), (ef, es)
-
+    if slices != 7:
+        return
     a = run(cfg)["records"]
     monkeypatch.setenv("PF_FUSE_DIGITS", "0")
     b = run(cfg)["records"]
     for x, y in zip(a, b):
         den = max(O.lowrank_fro(x["V"], x["f"]), 1e-300)
         assert O.lowrank_diff_fro(x["V"], x["f"], y["V"], y["f"]) <= 1e-10 * den
+
+
+@pytest.mark.parametrize("n,p", [(1333, 64), (700, 128), (300, 16)])
+def test_schedule_uses_leading_slices_of_the_tiled_layout(n, p):
+    """pf_set_i8_schedule(6, 0) on a 7-slice context multiplies the 6 leading digit slices of
+    each (tile, k-block) group of the tiled A layout: the truncating 7-digit expansion starts
+    with the 6-digit one, so the filter equals a 6-slice context's bit for bit."""
+    rs = np.random.default_rng(n + p)
+    A = rs.standard_normal((n, n))
+    A = A + A.T
+    U = np.linalg.qr(rs.standard_normal((n, p)))[0]
+    interval = torch.tensor([-5.0, 5.0], dtype=torch.float64, device="cuda")
+    outs = []
+    for slices, sched in ((7, (6, 0)), (6, None)):
+        c = _ctx(n, p, slices)
+        if sched:
+            c.set_i8_schedule(*sched)
+        Ud = _dev(U)
+        c.filter(_pitched(A), Ud, interval, 1, 1e6)
+        outs.append(Ud.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
