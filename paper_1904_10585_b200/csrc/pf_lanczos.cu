@@ -199,10 +199,10 @@ __device__ __forceinline__ void sym_issue(const double* __restrict__ A, int64_t 
   }
 }
 
-constexpr int kSyStages = 3;  // tiles in flight per CTA (2 CTAs / SM: 6 x 32 KB per SM)
+constexpr int kSyStages = 2;  // tiles in flight per CTA (3 CTAs / SM: 6 x 32 KB per SM)
 
 // thread t: rows 4 (t / 16) .. +3 and columns {2c, 2c + 1, 32 + 2c, 33 + 2c}, c = t % 16
-__global__ void __launch_bounds__(256, 2) lz_symv_tiles_kernel(
+__global__ void __launch_bounds__(256, 3) lz_symv_tiles_kernel(
     const double* __restrict__ A, int64_t lda, int n, const double* __restrict__ q,
     double* __restrict__ ws, DevState* state) {
   if (state->lanczos_steps >= 0) return;
@@ -358,7 +358,7 @@ cudaError_t lz_symv_launch(const double* A, int64_t lda, int n, const double* q,
                            double* partials, int* counter, DevState* state, int num_sms,
                            cudaStream_t st) {
   const long long T = (n + kSyT - 1) / kSyT, nt = T * (T + 1) / 2;
-  const int grid = (int)std::max(1LL, std::min(nt, 2LL * num_sms));
+  const int grid = (int)std::max(1LL, std::min(nt, 3LL * num_sms));
   const size_t smem = (size_t)kSyStages * kSyT * kSyT * 8;
   static bool attr = false;
   if (!attr) {
