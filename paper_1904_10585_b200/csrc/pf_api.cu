@@ -583,11 +583,16 @@ static pf_status gram_all(pf_ctx ctx, const double* X, const double* Y, double* 
 // p >= 64 (tools/bench_orth.py: CholeskyQR2 236 vs 259 us at p = 64, 626 vs 853 us at p = 128),
 // the single-CTA column kernel below (PF_CHOL_BIG=0: development knob)
 static cudaError_t chol64(pf_ctx ctx, int* shift_out, const int* cond, cudaStream_t st) {
-  static int big = -1;
+  static int big = -1, reg = -1;
   if (big < 0) {
     const char* e = getenv("PF_CHOL_BIG");
     big = e ? atoi(e) : 1;
+    const char* r = getenv("PF_CHOL_REG");  // p <= 64: register-blocked kernel (default)
+    reg = r ? atoi(r) : 1;
   }
+  if (reg && ctx->p <= 64)
+    return chol_inv_reg_launch(ctx->G, ctx->p, ctx->n, ctx->Rinv, ctx->state, shift_out, cond,
+                               st);
   if (big && ctx->p >= 64)
     return chol_inv_big_launch(ctx->G, ctx->p, ctx->n, ctx->chol_W, ctx->chol_D, ctx->Rinv,
                                ctx->state, shift_out, cond, st);

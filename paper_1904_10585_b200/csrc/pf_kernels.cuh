@@ -143,6 +143,10 @@ int gram_blocks(int n_rows, int p);
 cudaError_t gram_launch(const double* X, const double* Y, int n_rows, int p, double* G,
                         double* partials, int* counter, const int* cond, cudaStream_t st);
 // Cholesky G = L L^T (shifted on breakdown) and Rinv = L^{-T}; n_global for the shift.
+// p <= 64: the same factorisation with the matrix in registers (one barrier per column)
+cudaError_t chol_inv_reg_launch(const double* G, int p, int64_t n_global, double* Rinv,
+                                DevState* state, int* shift_flag_out, const int* cond,
+                                cudaStream_t st);
 cudaError_t chol_inv_launch(const double* G, int p, int64_t n_global, double* Rinv,
                             DevState* state, int* shift_flag_out, const int* cond,
                             cudaStream_t st);

@@ -248,6 +248,158 @@ cudaError_t chol_inv_launch(const double* G, int p, int64_t n_global, double* Ri
   return cudaGetLastError();
 }
 
+// Same factorisation and inverse as chol_inv_kernel for p <= 64, with the matrix held in
+// registers: 256 threads, thread t owns the 4 x 4 block (rows 4 (t / 16).., cols 4 (t % 16)..)
+// of the 64 x 64 matrix padded with the identity.  Each column step publishes the current
+// column through a double-buffered 64-vector and needs ONE barrier; every thread then updates
+// its 16 entries in registers (chol_inv_kernel keeps M in shared memory and walks rows and
+// columns in loops: ~75 us per call at p = 64 vs ~15 us here).  Arithmetic per entry is the
+// same: M_ik -= (M_ij / d) M_kj, L_ij = M_ij / sqrt(d); X_ic -= (L_ij / L_jj) X_jc with row j
+// unscaled, then row j scaled by 1 / L_jj.
+__global__ void __launch_bounds__(256) chol_inv_reg_kernel(const double* __restrict__ G, int p,
+                                                         double shift_scale,
+                                                         double* __restrict__ Rinv,
+                                                         DevState* state, int* shift_flag_out,
+                                                         const int* cond) {
+  if (cond && *cond == 0) return;
+  constexpr int PC = 64;
+  __shared__ double Ls[PC * (PC + 1)];  // L (lower), then read by the inverse
+  __shared__ double buf[2][PC];
+  __shared__ double red[32];
+  __shared__ double gdiag[PC];
+  const int tid = threadIdx.x, bi = tid >> 4, bj = tid & 15;
+  const int r0 = 4 * bi, c0 = 4 * bj;
+  const bool act = bj <= bi;  // lower-triangle blocks (incl. diagonal)
+
+  double tr = 0.0;
+  int bad = 0;
+  for (int e = tid; e < p * p; e += 256) {
+    const double v = G[e];
+    if (!isfinite(v)) bad = 1;
+    if (e / p == e % p) tr += v;
+  }
+  bad = __syncthreads_or(bad);
+  tr = block_sum(tr, red);
+  if (bad && tid == 0) atomicOr(&state->flags, PF_FLAG_NONFINITE);
+  for (int i = tid; i < PC; i += 256) gdiag[i] = i < p ? G[(size_t)i * p + i] : 1.0;
+
+  double a[4][4];
+  double shift = 0.0;
+  int attempt = 0;
+  for (;;) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int r = r0 + u, c = c0 + v;
+        a[u][v] = (r < p && c < p) ? G[(size_t)r * p + c] + (r == c ? shift : 0.0)
+                                   : (r == c ? 1.0 : 0.0);
+      }
+    __syncthreads();
+    bool fail = false;
+    for (int j = 0; j < PC; ++j) {
+      double* cb = buf[j & 1];
+      if (bj == (j >> 2) && act) {  // owners of column j publish it (rows >= 4 (j / 4))
+        const int jj = j & 3;  // static register indices only (no local-memory arrays)
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          cb[r0 + u] = jj == 0 ? a[u][0] : jj == 1 ? a[u][1] : jj == 2 ? a[u][2] : a[u][3];
+      }
+      __syncthreads();
+      const double d = cb[j];
+      if (!(d > 1e-12 * gdiag[j]) || !(d > 0.0)) {  // uniform
+        fail = true;
+        break;
+      }
+      const double rsd = rsqrt(d);
+      const double inv_d = rsd * rsd;
+      if (tid < PC) Ls[tid * (PC + 1) + j] = tid > j ? cb[tid] * rsd : (tid == j ? d * rsd : 0.0);
+      if (act && r0 + 3 > j) {
+        double li[4], lk[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) li[u] = cb[r0 + u] * inv_d;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) lk[v] = cb[c0 + v];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v)
+            if (r0 + u > j && c0 + v > j && c0 + v <= r0 + u) a[u][v] -= li[u] * lk[v];
+      }
+    }
+    __syncthreads();
+    if (!fail) break;
+    if (attempt == 1) {
+      if (tid == 0) atomicOr(&state->flags, PF_FLAG_NONFINITE);
+      break;
+    }
+    attempt = 1;
+    shift = shift_scale * (tr > 0.0 ? tr : 1.0);
+  }
+  if (tid == 0) {
+    if (attempt) atomicOr(&state->flags, PF_FLAG_CHOL_SHIFT);
+    if (shift_flag_out && attempt) *shift_flag_out = 1;
+  }
+  // X = L^{-1}: x holds rows r0.., cols c0.. of X (identity to start)
+  double x[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) x[u][v] = (r0 + u == c0 + v) ? 1.0 : 0.0;
+  if (tid < PC) gdiag[tid] = 1.0 / Ls[tid * (PC + 1) + tid];
+  __syncthreads();
+  for (int j = 0; j < PC; ++j) {
+    double* rb = buf[j & 1];
+    if (bi == (j >> 2) && act) {  // owners of row j publish it (unscaled), columns <= j
+      const int jj = j & 3;
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        rb[c0 + v] = jj == 0 ? x[0][v] : jj == 1 ? x[1][v] : jj == 2 ? x[2][v] : x[3][v];
+    }
+    __syncthreads();
+    const double inv = gdiag[j];
+    if (act && r0 + 3 > j && c0 <= j) {
+      double lij[4], xj[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) lij[u] = Ls[(r0 + u) * (PC + 1) + j] * inv;
+#pragma unroll
+      for (int v = 0; v < 4; ++v) xj[v] = rb[c0 + v];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+          if (r0 + u > j && c0 + v <= j) x[u][v] -= lij[u] * xj[v];
+    }
+    if (bi == (j >> 2) && act) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+          if (r0 + u == j && c0 + v <= j) x[u][v] *= inv;
+    }
+  }
+  // Rinv = L^{-T}: Rinv[c][i] = X[i][c] (upper triangular), p x p
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int i = r0 + u, c = c0 + v;
+      if (i < p && c < p) Rinv[(size_t)c * p + i] = act ? x[u][v] : 0.0;
+    }
+  // blocks above the diagonal (inactive threads) write the zero lower part of Rinv
+}
+
+cudaError_t chol_inv_reg_launch(const double* G, int p, int64_t n_global, double* Rinv,
+                                DevState* state, int* shift_flag_out, const int* cond,
+                                cudaStream_t st) {
+  if (p > 64) return cudaErrorInvalidValue;
+  const double u = 1.1102230246251565e-16;
+  const double scale = 11.0 * ((double)n_global * p + (double)p * (p + 1)) * u;
+  count_launch();
+  chol_inv_reg_kernel<<<1, 256, 0, st>>>(G, p, scale, Rinv, state, shift_flag_out, cond);
+  return cudaGetLastError();
+}
+
 // =============================================================================== Y R
 template <int P>
 struct RmulCfg {
