@@ -587,10 +587,11 @@ static cudaError_t chol64(pf_ctx ctx, int* shift_out, const int* cond, cudaStrea
   if (big < 0) {
     const char* e = getenv("PF_CHOL_BIG");
     big = e ? atoi(e) : 1;
-    const char* r = getenv("PF_CHOL_REG");  // p <= 64: register-blocked kernel (default)
+    const char* r = getenv("PF_CHOL_REG");  // p = 64: register-blocked kernel (default)
     reg = r ? atoi(r) : 1;
   }
-  if (reg && ctx->p <= 64)
+  // p <= 32 stays on chol_inv (no gain measured: configs 1 / 2 within noise or slower)
+  if (reg && ctx->p > 32 && ctx->p <= 64)
     return chol_inv_reg_launch(ctx->G, ctx->p, ctx->n, ctx->Rinv, ctx->state, shift_out, cond,
                                st);
   if (big && ctx->p >= 64)

@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(256) chol_inv_reg_kernel(const double* __restr
       }
     __syncthreads();
     bool fail = false;
-    for (int j = 0; j < PC; ++j) {
+    for (int j = 0; j < p; ++j) {  // the identity padding past p needs no steps
       double* cb = buf[j & 1];
       if (bj == (j >> 2) && act) {  // owners of column j publish it (rows >= 4 (j / 4))
         const int jj = j & 3;  // static register indices only (no local-memory arrays)
@@ -346,9 +346,9 @@ __global__ void __launch_bounds__(256) chol_inv_reg_kernel(const double* __restr
   for (int u = 0; u < 4; ++u)
 #pragma unroll
     for (int v = 0; v < 4; ++v) x[u][v] = (r0 + u == c0 + v) ? 1.0 : 0.0;
-  if (tid < PC) gdiag[tid] = 1.0 / Ls[tid * (PC + 1) + tid];
+  if (tid < p) gdiag[tid] = 1.0 / Ls[tid * (PC + 1) + tid];
   __syncthreads();
-  for (int j = 0; j < PC; ++j) {
+  for (int j = 0; j < p; ++j) {
     double* rb = buf[j & 1];
     if (bi == (j >> 2) && act) {  // owners of row j publish it (unscaled), columns <= j
       const int jj = j & 3;
