@@ -579,9 +579,10 @@ static pf_status gram_all(pf_ctx ctx, const double* X, const double* Y, double* 
   return allreduce(ctx, G, (size_t)ctx->p * ctx->p, st);
 }
 
-// G = R^T R and Rinv = R^{-1} of the p x p Gram: the 32-column panel kernel of the fp32 path for
-// p >= 64 (tools/bench_orth.py: CholeskyQR2 236 vs 259 us at p = 64, 626 vs 853 us at p = 128),
-// the single-CTA column kernel below (PF_CHOL_BIG=0: development knob)
+// G = R^T R and Rinv = R^{-1} of the p x p Gram: p = 64 the register-blocked kernel (56 vs ~75 us
+// per factorisation, PF_CHOL_REG=0 to disable); p >= 128 the 32-column panel kernel of the fp32
+// path (tools/bench_orth.py: CholeskyQR2 626 vs 853 us at p = 128); p <= 32 (or PF_CHOL_BIG=0)
+// the single-CTA column kernel
 static cudaError_t chol64(pf_ctx ctx, int* shift_out, const int* cond, cudaStream_t st) {
   static int big = -1, reg = -1;
   if (big < 0) {
