@@ -84,6 +84,21 @@ pf_status pf_create(int64_t n, int32_t p, int32_t degree, pf_dtype dtype, pf_ctx
  * world = 1 is allowed (single-rank communicator, same code path). */
 pf_status pf_create_dist(int64_t n, int32_t p, int32_t degree, pf_dtype dtype,
                          const void* nccl_id, int32_t rank, int32_t world, pf_ctx* out);
+/* In-process loopback communicator (a test harness for the row-block split on ONE GPU; the
+ * exchange semantics of pf_create_dist without NCCL): pf_loop_create makes a hub for `world`
+ * ranks (1 <= world <= 16); each rank's context is created with pf_create_loop(..., hub, rank)
+ * and driven by its own host thread on its own stream.  Every collective is a host rendezvous
+ * of the `world` calls followed by stream-ordered device work: an all-gather waits on each
+ * peer's block-ready event and copies the peer slab (cudaMemcpyAsync); an all-reduce sums the
+ * peers' buffers in rank order in one kernel (identical bits on every rank).  A rendezvous that
+ * waits longer than 300 s (environment PF_LOOP_TIMEOUT_S at pf_loop_create), or a failed peer, fails the call with PF_ERR_NCCL (and every later
+ * collective on the hub).  The hub must outlive its contexts; it owns no device memory. */
+typedef struct pf_loop_s* pf_loop;
+pf_status pf_loop_create(int32_t world, pf_loop* out);
+pf_status pf_loop_destroy(pf_loop hub);
+pf_status pf_create_loop(int64_t n, int32_t p, int32_t degree, pf_dtype dtype, pf_loop hub,
+                         int32_t rank, pf_ctx* out);
+
 /* Writes a fresh NCCL unique id (ncclGetUniqueId) into out[0 .. bytes); bytes >= 128. */
 pf_status pf_nccl_unique_id(void* out, int32_t bytes);
 

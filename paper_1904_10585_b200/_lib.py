@@ -72,6 +72,9 @@ def load() -> ctypes.CDLL:
         "pf_kernel_launches": [],
         "pf_diagnostics": [P, P, ctypes.POINTER(D)],
         "pf_nccl_unique_id": [P, I32],
+        "pf_loop_create": [I32, ctypes.POINTER(P)],
+        "pf_loop_destroy": [P],
+        "pf_create_loop": [I64, I32, I32, I32, P, I32, ctypes.POINTER(P)],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -126,6 +129,32 @@ def _stream(stream) -> int | None:
     return stream.cuda_stream
 
 
+class Loopback:
+    """In-process loopback communicator for `world` ranks on one GPU (pf_loop_create): the
+    test harness of the row-block split.  Each rank's Context(loop=hub, rank=r) must be driven by
+    its own host thread on its own stream (every collective is a rendezvous of the W calls)."""
+
+    def __init__(self, world: int):
+        self.lib = load()
+        self.world = world
+        h = ctypes.c_void_p()
+        st = self.lib.pf_loop_create(world, ctypes.byref(h))
+        if st != 0:
+            raise PFError(f"pf_loop_create: {STATUS.get(st, st)}")
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            self.lib.pf_loop_destroy(self.h)
+            self.h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Context:
     """One pf_ctx: scratch for order-n problems with block width p and degree d.
 
@@ -133,11 +162,15 @@ class Context:
     dtype PF_TF32: A is fp32 row-major, blocks are fp32 p-major tensors of shape (p, n_local)."""
 
     def __init__(self, n: int, p: int, d: int, nccl_id: bytes | None = None, rank: int = 0,
-                 world: int = 1, dtype: int = PF_FP64):
+                 world: int = 1, dtype: int = PF_FP64, loop: "Loopback | None" = None):
         self.lib = load()
         self.n, self.p, self.d, self.dtype = n, p, d, dtype
+        self.loop = loop                     # keeps the hub alive as long as the context
         h = ctypes.c_void_p()
-        if nccl_id is None:
+        if loop is not None:
+            assert loop.world == world, "loopback hub world mismatch"
+            st = self.lib.pf_create_loop(n, p, d, dtype, loop.h, rank, ctypes.byref(h))
+        elif nccl_id is None:
             st = self.lib.pf_create(n, p, d, dtype, ctypes.byref(h))
         else:
             buf = ctypes.create_string_buffer(nccl_id, 128)

@@ -2,7 +2,8 @@
 // the hot-path kernels for one PFPG / PFAM iteration.  All work is stream-ordered; nothing here
 // synchronises the host except pf_get_device_status / pf_profile_read / pf_diagnostics.
 //
-// Distributed contexts (pf_create_dist) own an NCCL communicator: rank g holds the row block
+// Distributed contexts (pf_create_dist: NCCL; pf_create_loop: in-process loopback on one GPU,
+// pf_comm.cuh) own a communicator: rank g holds the row block
 // [g n / world, (g + 1) n / world) of A and of every n x p block.  Each Chebyshev step
 // all-gathers Y_j (the B operand), every Gram / H matrix is all-reduced (p x p), the Lanczos
 // vector is all-gathered per step and its dots / norms all-reduced, and the rebuild gathers V.
@@ -19,6 +20,7 @@
 #include <vector>
 
 #include "../../include/pf.h"
+#include "pf_comm.cuh"
 #include "pf_kernels.cuh"
 
 using namespace pf;
@@ -30,7 +32,7 @@ struct pf_ctx_s {
   int64_t n = 0, n_local = 0, row0 = 0;
   int p = 0, d = 0, rank = 0, world = 1, num_sms = 148;
   pf_dtype dtype = PF_FP64;
-  bool dist = false;                           // NCCL communicator present
+  bool dist = false;                           // communicator present (NCCL or loopback)
   DevState* state = nullptr;
   double* Y[3] = {nullptr, nullptr, nullptr};  // n_local x p, ld p
   double* Yfull = nullptr;                     // n x p gathered block (dist)
@@ -63,7 +65,7 @@ struct pf_ctx_s {
   const double* mapA_ptr = nullptr;
   int64_t mapA_lda = 0;
   CUtensorMap mapA;
-  ncclComm_t comm = nullptr;
+  Comm* comm = nullptr;
   // profiling of the dominant kernel: event pairs around every Chebyshev-step GEMM launch
   bool prof = false;
   std::vector<cudaEvent_t> ev;
@@ -130,6 +132,7 @@ struct pf_ctx_s {
 };
 
 static constexpr int kI8MaxSlices = 7;
+static constexpr int kMaxWorld = 64;  // row-block ranks (the loopback hub allows 16)
 
 static pf_status cuda_fail(pf_ctx c, cudaError_t e, const char* where) {
   if (c) snprintf(c->err, sizeof(c->err), "%s: %s", where, cudaGetErrorString(e));
@@ -323,13 +326,15 @@ static pf_status alloc_all(pf_ctx ctx) {
 }
 
 static pf_status create_common(int64_t n, int32_t p, int32_t degree, pf_dtype dtype, int rank,
-                               int world, const void* nccl_id, pf_ctx* out) {
+                               int world, const void* nccl_id, LoopHub* hub, pf_ctx* out) {
   if (!out) return PF_ERR_ARG;
   *out = nullptr;
+  if (world > kMaxWorld) return PF_ERR_ARG;
   if (dtype != PF_FP64 && dtype != PF_TF32 && dtype != PF_FP64_I8) return PF_ERR_UNSUPPORTED;
   // fp32 path, distributed: equal row blocks with n_local % 16 == 0 (a 16-wide TMA K box never
   // straddles two ranks' slabs of the gathered block)
-  if (dtype == PF_TF32 && nccl_id != nullptr && (n % (16 * (int64_t)world)) != 0)
+  const bool dist = nccl_id != nullptr || hub != nullptr;
+  if (dtype == PF_TF32 && dist && (n % (16 * (int64_t)world)) != 0)
     return PF_ERR_DIM;
   if (degree < 1 || degree > kMaxDeg) return PF_ERR_ARG;
   if (world < 1 || rank < 0 || rank >= world) return PF_ERR_ARG;
@@ -343,7 +348,7 @@ static pf_status create_common(int64_t n, int32_t p, int32_t degree, pf_dtype dt
   ctx->dtype = dtype;
   ctx->rank = rank;
   ctx->world = world;
-  ctx->dist = (nccl_id != nullptr);
+  ctx->dist = dist;
   ctx->row0 = (int64_t)rank * n / world;
   ctx->n_local = (int64_t)(rank + 1) * n / world - ctx->row0;
   int dev = 0;
@@ -363,13 +368,12 @@ static pf_status create_common(int64_t n, int32_t p, int32_t degree, pf_dtype dt
   }
   pf_status s = alloc_all(ctx);
   if (s == PF_OK && ctx->dist) {
-    ncclUniqueId id;
-    memcpy(&id, nccl_id, sizeof(id));
-    ncclResult_t r = ncclCommInitRank(&ctx->comm, world, id, rank);
-    if (r != ncclSuccess) {
-      snprintf(ctx->err, sizeof(ctx->err), "ncclCommInitRank: %s", ncclGetErrorString(r));
-      s = PF_ERR_NCCL;
-    }
+    int cs = PF_OK;
+    // largest all-reduce: a p x p Gram / H, the Lanczos coefficients, the extrapolation Gram
+    const size_t max_reduce = std::max<size_t>((size_t)p * p, 2 * kMaxLanczos + 8);
+    ctx->comm = hub ? comm_loop_create(hub, rank, max_reduce, ctx->err, &cs)
+                    : comm_nccl_create(nccl_id, rank, world, ctx->err, &cs);
+    s = (pf_status)cs;
   }
   if (s != PF_OK) {
     fprintf(stderr, "pf_create: %s\n", ctx->err);
@@ -381,13 +385,32 @@ static pf_status create_common(int64_t n, int32_t p, int32_t degree, pf_dtype dt
 }
 
 pf_status pf_create(int64_t n, int32_t p, int32_t degree, pf_dtype dtype, pf_ctx* out) {
-  return create_common(n, p, degree, dtype, 0, 1, nullptr, out);
+  return create_common(n, p, degree, dtype, 0, 1, nullptr, nullptr, out);
 }
 
 pf_status pf_create_dist(int64_t n, int32_t p, int32_t degree, pf_dtype dtype,
                          const void* nccl_id, int32_t rank, int32_t world, pf_ctx* out) {
   if (!nccl_id) return PF_ERR_ARG;
-  return create_common(n, p, degree, dtype, rank, world, nccl_id, out);
+  return create_common(n, p, degree, dtype, rank, world, nccl_id, nullptr, out);
+}
+
+pf_status pf_loop_create(int32_t world, pf_loop* out) {
+  if (!out) return PF_ERR_ARG;
+  *out = reinterpret_cast<pf_loop>(loop_hub_create(world));
+  return *out ? PF_OK : PF_ERR_ARG;
+}
+
+pf_status pf_loop_destroy(pf_loop hub) {
+  if (!hub) return PF_ERR_ARG;
+  loop_hub_destroy(reinterpret_cast<LoopHub*>(hub));
+  return PF_OK;
+}
+
+pf_status pf_create_loop(int64_t n, int32_t p, int32_t degree, pf_dtype dtype, pf_loop hub,
+                         int32_t rank, pf_ctx* out) {
+  if (!hub) return PF_ERR_ARG;
+  LoopHub* h = reinterpret_cast<LoopHub*>(hub);
+  return create_common(n, p, degree, dtype, rank, loop_hub_world(h), nullptr, h, out);
 }
 
 long long pf_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
@@ -434,7 +457,7 @@ pf_status pf_destroy(pf_ctx ctx) {
   if (!ctx) return PF_ERR_ARG;
   ns_destroy(ctx->ns);
   for (auto e : ctx->ev) cudaEventDestroy(e);
-  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  delete ctx->comm;
   void* ptrs[] = {ctx->state,  ctx->Y[0],     ctx->Y[1],      ctx->Y[2],    ctx->Yfull,
                   ctx->Wbuf,   ctx->VFbuf,    ctx->Vfull,    ctx->G,         ctx->Rinv,    ctx->Yeig,
                   ctx->gram_part, ctx->cheb_ws, ctx->cheb_cnt, ctx->lz_Q,   ctx->lz_qfull,
@@ -444,7 +467,8 @@ pf_status pf_destroy(pf_ctx ctx) {
                   ctx->chol_W, ctx->chol_D,   ctx->jac_H,     ctx->jac_V,   ctx->jac_red,
                   ctx->jac_cnt, ctx->tf_ws,   ctx->tf_cnt,    ctx->tf_acc,  ctx->Yfull32,
                   ctx->A8,     ctx->a8_rscale, ctx->Y8,       ctx->y8_cscale, ctx->y8_cmax,
-                  ctx->i8_acc, ctx->i8_part, ctx->i8_cnt, ctx->svt_part, ctx->svt_cnt};
+                  ctx->i8_acc, ctx->i8_part, ctx->i8_cnt, ctx->svt_part, ctx->svt_cnt,
+                  ctx->lz_sym_ws, ctx->a8_E, ctx->a8_wa, ctx->a8_wmax};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete ctx;
@@ -464,8 +488,9 @@ pf_status pf_get_device_status(pf_ctx ctx, pf_stream stream, uint32_t* flags, in
     lanczos_lo_hi[0] = h.lanczos[0];
     lanczos_lo_hi[1] = h.lanczos[1];
   }
-  PF_CU(cudaMemset(&ctx->state->flags, 0, sizeof(unsigned int)));
-  PF_CU(cudaMemset(&ctx->state->rebases, 0, sizeof(int)));
+  // cleared on the caller's stream (ordered before the next libpf kernel on it)
+  PF_CU(cudaMemsetAsync(&ctx->state->flags, 0, sizeof(unsigned int), st));
+  PF_CU(cudaMemsetAsync(&ctx->state->rebases, 0, sizeof(int), st));
   return PF_OK;
 }
 
@@ -488,33 +513,17 @@ static pf_status map_A(pf_ctx ctx, const double* A, int64_t lda) {
   return PF_OK;
 }
 
-static pf_status nccl_fail(pf_ctx ctx, ncclResult_t r, const char* where) {
-  snprintf(ctx->err, sizeof(ctx->err), "%s: %s", where, ncclGetErrorString(r));
-  return PF_ERR_NCCL;
-}
-
-// Gather the local row block `loc` (n_local x cols, contiguous) into `full` (n x cols).
+// Gather the local row block `loc` (n_local x cols doubles, contiguous) into `full` (n x cols).
 static pf_status gather(pf_ctx ctx, const double* loc, double* full, int cols, cudaStream_t st) {
-  const int64_t n = ctx->n;
-  if (n % ctx->world == 0) {
-    ncclResult_t r = ncclAllGather(loc, full, (size_t)ctx->n_local * cols, ncclDouble, ctx->comm, st);
-    return r == ncclSuccess ? PF_OK : nccl_fail(ctx, r, "ncclAllGather");
-  }
-  // ragged row split: one broadcast per owner inside a group
-  ncclGroupStart();
-  for (int g = 0; g < ctx->world; ++g) {
-    const int64_t r0 = (int64_t)g * n / ctx->world, r1 = (int64_t)(g + 1) * n / ctx->world;
-    ncclBroadcast(g == ctx->rank ? loc : full + r0 * cols, full + r0 * cols, (size_t)(r1 - r0) * cols,
-                  ncclDouble, g, ctx->comm, st);
-  }
-  ncclResult_t r = ncclGroupEnd();
-  return r == ncclSuccess ? PF_OK : nccl_fail(ctx, r, "ncclBroadcast group");
+  size_t off[kMaxWorld + 1];
+  for (int g = 0; g <= ctx->world; ++g)
+    off[g] = (size_t)((int64_t)g * ctx->n / ctx->world) * cols * sizeof(double);
+  return (pf_status)ctx->comm->allgatherv(loc, full, off, st);
 }
 
 static pf_status allreduce(pf_ctx ctx, double* buf, size_t count, cudaStream_t st) {
   if (!ctx->dist) return PF_OK;
-  ncclResult_t r = ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, ctx->comm, st);
-  return r == ncclSuccess ? PF_OK : nccl_fail(ctx, r, "ncclAllReduce");
+  return (pf_status)ctx->comm->allreduce_sum(buf, count, st);
 }
 
 // One Chebyshev step / plain product: out = coef * (A B) + ..., B = Y[bidx] (all rows).
@@ -651,10 +660,10 @@ static pf_status gemm_step32(pf_ctx ctx, int bidx, const float* ycur, const floa
   const CUtensorMap* mb = &ctx->mapBf[bidx];
   int bdist_kb = 0;
   if (ctx->dist) {
-    // all-gather the p-major blocks rank-major: [world][p][n_local] (one NCCL call per step)
-    ncclResult_t r = ncclAllGather(ctx->Yf[bidx], ctx->Yfull32, (size_t)ctx->p * ctx->n_local,
-                                   ncclFloat, ctx->comm, st);
-    if (r != ncclSuccess) return nccl_fail(ctx, r, "ncclAllGather(fp32 block)");
+    // all-gather the p-major blocks rank-major: [world][p][n_local] (equal slabs)
+    size_t off[kMaxWorld + 1];
+    for (int g = 0; g <= ctx->world; ++g) off[g] = (size_t)g * ctx->p * ctx->n_local * 4;
+    PF_TRY((pf_status)ctx->comm->allgatherv(ctx->Yf[bidx], ctx->Yfull32, off, st));
     mb = &ctx->mapBfull32;
     bdist_kb = (int)(ctx->n_local / 16);
   }

@@ -9,9 +9,10 @@
 // (one per row of A, one per column of B): with V = trunc(x 2^(7S-E)) (exact, |V| < 2^7S),
 //
 //     x = 2^E * sum_{s=1..S} d_s 128^-s  +  r,   |r| < 2^(E - 7S),
-//     V = d_1 128^(S-1) + ... + d_S,  d_1 in [-128, 127], d_s in [0, 127] (s > 1)
+//     V = d_1 128^(S-1) + ... + d_S,  d_s in [-127, 127], every digit carrying the sign of x
 //
-// (two's-complement floor digits of V, extracted with integer shifts and byte permutes).  Then
+// (sign-symmetric truncating digits of |V| with the sign applied to each, pf_digits.cuh; the
+// int32 bound below assumes |d| <= 128 and is therefore conservative).  Then
 // (A B)_ic = 2^(E_i + F_c) sum_l 128^-l D_l[i, c] with the level sums D_l = sum_{s+t=l} A_s B_t
 // (l = 2..S+1; products below level S+1 are dropped, < 2^-7S relative), each an integer matrix
 // product computed EXACTLY by the tensor core in int32 (the K range per accumulation is bounded so

@@ -253,7 +253,7 @@ cudaError_t chol_inv_launch(const double* G, int p, int64_t n_global, double* Ri
 // of the 64 x 64 matrix padded with the identity.  Each column step publishes the current
 // column through a double-buffered 64-vector and needs ONE barrier; every thread then updates
 // its 16 entries in registers (chol_inv_kernel keeps M in shared memory and walks rows and
-// columns in loops: ~75 us per call at p = 64 vs ~15 us here).  Arithmetic per entry is the
+// columns in loops: ~75 us per active call at p = 64 vs 56 us here, measured).  Arithmetic per entry is the
 // same: M_ik -= (M_ij / d) M_kj, L_ij = M_ij / sqrt(d); X_ic -= (L_ij / L_jj) X_jc with row j
 // unscaled, then row j scaled by 1 / L_jj.
 __global__ void __launch_bounds__(256) chol_inv_reg_kernel(const double* __restrict__ G, int p,

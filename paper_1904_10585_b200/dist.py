@@ -27,3 +27,36 @@ def max_over_ranks(value: float, device=None) -> float:
     t = torch.tensor([value], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def run_loopback(cfg, world: int, iters: int | None = None, problem=None) -> list[dict]:
+    """Run the row-block split with `world` ranks on ONE GPU (pf_create_loop): one host thread
+    and one stream per rank, every exchange through the in-process loopback communicator.
+    Returns each rank's run() result (records hold that rank's local rows of V)."""
+    import threading
+
+    import torch
+
+    from ._lib import Loopback
+    from .solver import run
+
+    hub = Loopback(world)
+    out: list = [None] * world
+    errs: list = [None] * world
+
+    def worker(r: int):
+        try:
+            with torch.cuda.stream(torch.cuda.Stream()):
+                out[r] = run(cfg, iters=iters, problem=problem, rank=r, world=world, loop=hub)
+        except BaseException as e:  # noqa: BLE001  (re-raised in the caller)
+            errs[r] = e
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for e in errs:
+        if e is not None:
+            raise e
+    return out

@@ -24,6 +24,15 @@ def _bits(b: np.ndarray) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(b).view(np.int32)).cuda()
 
 
+def _iterate64(nl: int, n: int, init=None) -> torch.Tensor:
+    """An (nl x n) fp64 iterate with an even row pitch (16-byte TMA rows, include/pf.h) for any n
+    (zeros, or a copy of the host array `init`)."""
+    buf = torch.zeros((nl, (n + 1) // 2 * 2), dtype=torch.float64, device="cuda")
+    if init is not None:
+        buf[:, :n].copy_(torch.from_numpy(np.ascontiguousarray(init)))
+    return buf[:, :n]
+
+
 def rows_of(n: int, rank: int, world: int) -> tuple[int, int]:
     """Row block [r0, r1) owned by `rank` (the C library's split: floor(g n / world))."""
     return rank * n // world, (rank + 1) * n // world
@@ -37,7 +46,7 @@ class Solver:
 
     def __init__(self, cfg: Config, problem: dict | None = None, stream=None,
                  nccl_id: bytes | None = None, rank: int = 0, world: int = 1,
-                 graphs: bool = False, ctx: Context | None = None):
+                 graphs: bool = False, ctx: Context | None = None, loop=None):
         self.cfg = cfg
         # CUDA graphs: iterations k >= 1 replay one captured graph of the iteration body
         # (interval -> filter -> RR -> f -> update); the Lanczos refresh stays an eager launch
@@ -64,12 +73,14 @@ class Solver:
             assert (ctx.n, ctx.p, ctx.d, ctx.dtype) == (n, p, d, dtype), "context shape mismatch"
             self.ctx = ctx
         else:
-            self.ctx = Context(n, p, d, nccl_id=nccl_id, rank=rank, world=world, dtype=dtype)
+            self.ctx = Context(n, p, d, nccl_id=nccl_id, rank=rank, world=world, dtype=dtype,
+                               loop=loop)
         if self.f32:
             self.ctx.set_tf32_schedule(cfg.tf32_early, cfg.tf32_tail)
         if cfg.dtype == "f64i8":
             self.ctx.set_i8_schedule(cfg.i8_early, cfg.i8_tail)
-        r0, r1 = rows_of(n, rank, world) if nccl_id is not None else (0, n)
+        dist = nccl_id is not None or loop is not None
+        r0, r1 = rows_of(n, rank, world) if dist else (0, n)
         self.r0, self.r1, self.n_local = r0, r1, r1 - r0
         assert self.n_local == self.ctx.n_local
         nl = self.n_local
@@ -104,7 +115,7 @@ class Solver:
             self.thr = cfg.theta
         elif cfg.mode in ("sweep_psd", "sweep_soft"):
             A0 = cfg1_problem(cfg) if problem is None else problem["A0"]
-            self.A = _dev(A0[r0:r1])
+            self.A = _iterate64(nl, n, A0[r0:r1])
             self.thr = cfg.theta
         elif cfg.mode == "pfpg":
             prob = pfpg_problem(cfg) if problem is None else problem
@@ -113,7 +124,7 @@ class Solver:
             self.W = _dev(prob["W"])
             self.mu = prob["mu"]
             self.thr = cfg.tau * prob["mu"]
-            self.A = torch.empty((nl, n), dtype=torch.float64, device="cuda")
+            self.A = _iterate64(nl, n)
             # X_0 = 0: A_0 = 0 - tau Omega o (0 - M)  (the update kernel with zero factors)
             self.ctx.prox_step(self.V.zero_(), self.f, cfg.tau, self.omega, self.W, self.A,
                                self.obj, stream)
@@ -125,7 +136,7 @@ class Solver:
                 self.prob = prob
                 self.adj = _bits(prob["adj_bits"][r0:r1])
                 self.deg = _dev(prob["deg"])
-            self.A = torch.zeros((nl, n), dtype=torch.float64, device="cuda")
+            self.A = _iterate64(nl, n)
             # Z_0 = 0 -> Z_1 = prox_tG(0) = offdiag(-tC) + I  (reading R9)
             self.ctx.admm_step(self.V.zero_(), self.f, cfg.t, self.adj, self.deg, self.A,
                                self.obj, stream)
@@ -143,10 +154,7 @@ class Solver:
             self.win = 1                                             # points in the window
             B0 = G[r0:r1].copy()
             B0[np.arange(nl), r0 + np.arange(nl)] = 1.0           # G_ii + x^0_i = 1
-            # even row pitch (16-byte TMA rows, include/pf.h) for any n
-            buf = torch.zeros((nl, (n + 1) // 2 * 2), dtype=torch.float64, device="cuda")
-            buf[:, :n].copy_(torch.from_numpy(B0))
-            self.A = buf[:, :n]
+            self.A = _iterate64(nl, n, B0)
         else:
             raise ValueError(cfg.mode)
         self.ctx.orth(self.U, stream)
@@ -265,19 +273,21 @@ class Solver:
 
 
 def run(cfg: Config, iters: int | None = None, record: bool = True, problem=None,
-        nccl_id: bytes | None = None, rank: int = 0, world: int = 1, graphs: bool = False) -> dict:
-    """Run K iterations on the GPU, recording per-iteration factors (local rows) / objectives."""
+        nccl_id: bytes | None = None, rank: int = 0, world: int = 1, graphs: bool = False,
+        loop=None) -> dict:
+    """Run K iterations on the GPU, recording per-iteration factors (local rows) / objectives.
+    Distributed: nccl_id (one process per GPU) or loop (a Loopback hub; one thread per rank)."""
     K = cfg.iters if iters is None else iters
     if graphs:                      # capture needs a non-default stream; make it the current one
         st = torch.cuda.Stream()
         with torch.cuda.stream(st):
-            return _run(cfg, K, record, problem, nccl_id, rank, world, st, True)
-    return _run(cfg, K, record, problem, nccl_id, rank, world, None, False)
+            return _run(cfg, K, record, problem, nccl_id, rank, world, st, True, loop)
+    return _run(cfg, K, record, problem, nccl_id, rank, world, None, False, loop)
 
 
-def _run(cfg, K, record, problem, nccl_id, rank, world, stream, graphs):
+def _run(cfg, K, record, problem, nccl_id, rank, world, stream, graphs, loop=None):
     s = Solver(cfg, problem, stream=stream, nccl_id=nccl_id, rank=rank, world=world,
-               graphs=graphs)
+               graphs=graphs, loop=loop)
     recs = []
     for k in range(K):
         s.step()

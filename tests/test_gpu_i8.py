@@ -202,3 +202,60 @@ def test_schedule_uses_leading_slices_of_the_tiled_layout(n, p):
         c.filter(_pitched(A), Ud, interval, 1, 1e6)
         outs.append(Ud.cpu().numpy())
     assert np.array_equal(outs[0], outs[1])
+
+
+# ---------------------------------------------------------------- past the exact-int32 K bound
+# i8_plan bounds one exact int32 accumulation to chunk_kb = 292 k-blocks (K = 18688 at S = 7);
+# longer K ranges fold each chunk into the fp64 accumulator in the epilogue (pf_gemm_i8.cu), and
+# at n = 32768 (config 4) the stream-K split cuts items at arbitrary k-blocks, so CTA segments
+# straddle a fold boundary.  Operands are built on the host in int8 (1 GB at n = 32768) and the
+# exact reference is formed in fp64 row blocks (integer sums < 2^53: exact in any order).
+def _int_problem(n, p, seed):
+    rs = np.random.default_rng(seed)
+    A8 = rs.integers(-100, 101, (n, n), dtype=np.int8)
+    A8[5] = 0                                         # zero row (scale exponent 0)
+    Y = rs.integers(-50, 51, (n, p)).astype(np.float64)
+    Y[:, 2] = 0.0                                     # zero column
+    ref = np.empty((n, p))
+    for r0 in range(0, n, 2048):
+        ref[r0:r0 + 2048] = A8[r0:r0 + 2048].astype(np.float64) @ Y
+    A = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    for r0 in range(0, n, 4096):
+        A[r0:r0 + 4096].copy_(torch.from_numpy(A8[r0:r0 + 4096]).cuda().to(torch.float64))
+    return A, Y, ref
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("n,p", [(18752, 16), (20000, 64), (32768, 128)])
+def test_integer_operands_exact_past_fold(n, p):
+    A, Y, ref = _int_problem(n, p, n + p)
+    c = _ctx(n, p)
+    out = torch.empty((n, p), dtype=torch.float64, device="cuda")
+    c.matmul(A, _dev(Y), out)
+    got = out.cpu().numpy()
+    bad = np.argwhere(got != ref)
+    assert bad.size == 0, (bad[:5], got[tuple(bad[0])], ref[tuple(bad[0])])
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("n,p", [(18752, 64), (32768, 128)])
+def test_gaussian_operands_fp64_grade_past_fold(n, p):
+    """Symmetric Gaussian A (the iterates' profile), K past the fold: within 2^-47 of the scale
+    and within 16x the fp64 DMMA GEMM's own error on the same context."""
+    g = torch.Generator(device="cuda").manual_seed(n)
+    A = torch.randn((n, n), dtype=torch.float64, device="cuda", generator=g)
+    A = A + A.T
+    rs = np.random.default_rng(n)
+    Y = rs.standard_normal((n, p))
+    Ah = A.cpu().numpy()
+    ref = Ah @ Y
+    scale = np.abs(Ah).max() * np.abs(Y).max() * n
+    del Ah
+    c = _ctx(n, p)
+    out = torch.empty((n, p), dtype=torch.float64, device="cuda")
+    c.matmul(A, _dev(Y), out)
+    err = np.abs(out.cpu().numpy() - ref).max()
+    c.set_i8_slices(0)
+    c.matmul(A, _dev(Y), out)
+    dm = np.abs(out.cpu().numpy() - ref).max()
+    assert err <= 2.0 ** -47 * scale and err <= 16 * max(dm, 1e-16 * scale), (err, dm)
