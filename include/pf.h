@@ -142,9 +142,15 @@ pf_status pf_interval_soft(pf_ctx ctx, double thr, double eta, double* interval,
 pf_status pf_interval_top_r(pf_ctx ctx, const double* lo_hi, int32_t r, double eta,
                             double* interval, pf_stream stream);
 
-/* Chebyshev degree of subsequent pf_filter calls (1 <= degree <= 64), e.g. the thm:conv1
- * schedule d_k = ceil(c log(k + 2)).  Scratch does not depend on the degree. */
+/* Chebyshev degree of subsequent pf_filter calls (1 <= degree <= 64).  Scratch does not depend
+ * on the degree. */
 pf_status pf_set_degree(pf_ctx ctx, int32_t degree);
+
+/* Degree schedule of thm:conv1 (PFPG converges when d_k = Omega(log k / min{l, 1})):
+ * sets the degree of subsequent pf_filter calls for iteration k >= 0 to
+ * d_k = max(d_0, ceil(c ln(k + 2))), d_0 = the degree given at create (c = 0: d_0), and writes it
+ * to *degree (host, may be NULL).  PF_ERR_ARG if c < 0 or d_k > 64. */
+pf_status pf_schedule_degree(pf_ctx ctx, double c, int32_t k, int32_t* degree);
 
 /* ---------------------------------------------------------------------------- hot path */
 /* U <- orth(rho^q(A) U) with rho(t) = T_d(L(t)), L(t) = (t - (a+b)/2)/((b-a)/2)
@@ -172,14 +178,16 @@ pf_status pf_rayleigh_ritz(pf_ctx ctx, const void* A, int64_t lda, const void* U
 pf_status pf_spectral_op(pf_ctx ctx, pf_op op, double thr, const double* theta, double* f,
                          int32_t* rank, pf_stream stream);
 
-/* PFPG update for F = 1/2 ||P_Omega(X - M)||_F^2, M = W W^T (eq:pfpg1 P:338-341):
+/* PFPG update for F = 1/2 ||P_Omega(X - M)||_F^2, M = W W^T, R = mu ||.||_* (eq:pfpg1 P:338-341):
  * X = V diag(f) V^T, A_out = X - tau * Omega o (X - M)  (n_local x n, lda_out).
  * omega: packed row-major symmetric bitmask, uint32 words, bit (j & 31) of word [i][j >> 5],
  * row pitch ldo words (>= ceil(n/32)), local rows.  W: n x r FULL (all rows), ldw >= r,
- * 0 <= r <= 64.  obj: device double[2] = {1/2 ||P_Omega(X - M)||_F^2, sum_i |f_i|}. */
+ * 0 <= r <= 64.  mu >= 0.  obj: device double[2] = {h(X), 1/2 ||P_Omega(X - M)||_F^2} with the
+ * PFPG objective h(X) = 1/2 ||P_Omega(X - M)||_F^2 + mu sum_i |f_i| (= mu ||X||_* for
+ * orthonormal V), summed over all ranks. */
 pf_status pf_prox_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f, double tau,
-                       const uint32_t* omega, int64_t ldo, const double* W, int64_t ldw,
-                       int32_t r, double* A_out, int64_t lda_out, double* obj,
+                       double mu, const uint32_t* omega, int64_t ldo, const double* W,
+                       int64_t ldw, int32_t r, double* A_out, int64_t lda_out, double* obj,
                        pf_stream stream);
 
 /* PFAM update for the max-cut SDP min <C,X> s.t. diag(X) = 1, X PSD, C = -L/4 (eq:PFAM1 P:389
@@ -314,6 +322,22 @@ pf_status pf_spmm(pf_ctx ctx, const int32_t* ptr, const int32_t* idx, const doub
                   const int32_t* vperm, const double* X, int64_t ldx, double s1, double s2,
                   double s3, const double* Ycur, int64_t ldc, const double* Yprev, int64_t ldp,
                   double* out, int64_t ldo, pf_stream stream);
+
+/* SVT's kick (reading R24): x = k0 delta b on the nnz sampled entries, k0 = ceil(mu / (delta
+ * norm2)) with norm2 = ||P_Omega(M)||_2 (host scalar, computed by the problem's generator).
+ * b, x: device double[nnz]. */
+pf_status pf_svt_kick(pf_ctx ctx, const double* b, int64_t nnz, double mu, double delta,
+                      double norm2, double* x, pf_stream stream);
+
+/* The PFSVT filter ("subspace extraction from A^T A"; reading R24): Q <- orth(
+ * T_d(L(Y^T Y)) Q) with the context's degree d, Y = A*(x) the sparse dual iterate (CSR ptr / idx
+ * and its CSC view cptr / cidx / perm addressing the same values val = x, as for pf_spmm),
+ * damped interval [0, (1 - eta) mu^2] of Y^T Y, L(t) = (t - c)/e (eqn:cheb-linear-map), the
+ * three-term recurrence eq:cheb with each product Y^T (Y Y_j) as two sparse products, then
+ * CholeskyQR2.  Q: n x p row-major (ldq >= p), in place.  mu > 0, 0 <= eta < 1. */
+pf_status pf_svt_filter(pf_ctx ctx, const int32_t* ptr, const int32_t* idx, const int32_t* cptr,
+                        const int32_t* cidx, const int32_t* perm, const double* val, double* Q,
+                        int64_t ldq, double mu, double eta, pf_stream stream);
 
 /* Singular triplets of Y on span(Q) (Q orthonormal, n x p): B = Y Q, B^T B = W diag(lambda) W^T
  * by Jacobi (descending), sigma = sqrt(max(lambda, 0)) (device, p), V = Q W, U = B W / sigma

@@ -27,8 +27,10 @@ Pins (tests/test_oracle_pins.py) -- what fixes each function independently of it
                       values of tab:ncm
   rna_extrapolate ... trivial windows, the l = 1 closed form, exact recovery of a linear fixed point
   relative_gap ...... hand example of eqn:relative-gap
+  degree_schedule ... Theta(log k) growth (thm:conv1's requirement), floor, c = 0 constant; on a
+                      static config-1 matrix it reaches exact P_+ where the fixed d = 1 lags
   run ............... config 1 k = 0 == exact P_+; degenerate (PSD) interval == compression P A P;
-                      q repeats on a diagonal A (closed form); the degree schedule of thm:conv1;
+                      q repeats on a diagonal A (closed form);
                       trajectories of configs 2-5 at full size -- parity unpinned beyond the
                       invariants above and the p = n special case (no published values exist
                       for these inputs).
@@ -42,7 +44,7 @@ import numpy as np
 
 from pfinputs import (Config, initial_block, lanczos_start, cfg1_problem, cfg1_noise,
                       pfpg_problem, pfam_problem, unpack_bitmask, cfg5_problem, cfg5_perturb,
-                      nce_problem, degree_at)
+                      nce_problem)
 
 __all__ = [
     "cheb_T", "growth_lower_bound", "interval_map", "interval_psd", "interval_top_r",
@@ -50,7 +52,7 @@ __all__ = [
     "interval_soft", "lanczos_extremes", "rebase_plan", "spread_estimate", "chebyshev_filter",
     "orth", "filter_update", "rayleigh_ritz", "spectral_psd", "spectral_soft", "jacobi_eig",
     "exact_spectral", "maxcut_C", "prox_tG_diag", "pfam_next", "pfpg_next", "nce_next",
-    "rna_extrapolate", "run",
+    "rna_extrapolate", "run", "degree_schedule",
     "lowrank_diff_fro", "lowrank_fro", "sin_theta",
 ]
 
@@ -343,6 +345,16 @@ def sin_theta(X: np.ndarray, Y: np.ndarray) -> np.ndarray:
 
 
 # ============================================================================ driver
+def degree_schedule(d0: int, c: float, k: int) -> int:
+    """Chebyshev degree of iteration k (thm:conv1): PFPG converges if
+    d_k = Omega(log k / min{l, 1}); the schedule d_k = max(d0, ceil(c ln(k + 2))) (c = 0: the
+    fixed degree d0) grows like c ln k."""
+    if c <= 0.0:
+        return d0
+    return max(d0, int(math.ceil(c * math.log(k + 2))))
+
+
+
 def _threshold(cfg: Config, prob) -> float:
     if cfg.mode == "pfpg":
         return prob["tau"] * prob["mu"]
@@ -425,7 +437,7 @@ def run(cfg: Config, iters: int | None = None, record_factors: bool = True,
             a, b = interval_psd(lo, cfg.eta)
         else:
             a, b = interval_soft(thr, cfg.eta)
-        dk = degree_at(cfg, k)                                   # NEXT-4 degree schedule
+        dk = degree_schedule(cfg.d, cfg.deg_c, k)                # NEXT-4 degree schedule
         if not degenerate:
             plan = rebase_plan(a, b, spread_estimate(theta_prev, lo, hi), dk, cfg.rho_max)
             # a2/a3 (q applications of the polynomial per filter)

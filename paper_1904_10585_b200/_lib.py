@@ -51,7 +51,10 @@ def load() -> ctypes.CDLL:
         "pf_orth": [P, P, I64, P],
         "pf_rayleigh_ritz": [P, P, I64, P, I64, P, I64, P, P],
         "pf_spectral_op": [P, I32, D, P, P, P, P],
-        "pf_prox_step": [P, P, I64, P, D, P, I64, P, I64, I32, P, I64, P, P],
+        "pf_prox_step": [P, P, I64, P, D, D, P, I64, P, I64, I32, P, I64, P, P],
+        "pf_schedule_degree": [P, D, I32, ctypes.POINTER(I32)],
+        "pf_svt_kick": [P, P, I64, D, D, D, P, P],
+        "pf_svt_filter": [P, P, P, P, P, P, P, P, I64, D, D, P],
         "pf_admm_step": [P, P, I64, P, D, P, I64, P, P, I64, P, P],
         "pf_perturb": [P, P, I64, P, I64, P],
         "pf_perturb_hash": [P, P, I64, ctypes.c_uint64, I32, D, P],
@@ -240,6 +243,13 @@ class Context:
     def set_degree(self, d: int):
         self._check(self.lib.pf_set_degree(self.h, d), "pf_set_degree")
 
+    def schedule_degree(self, c: float, k: int) -> int:
+        """thm:conv1 degree schedule for iteration k (pf_schedule_degree); returns d_k."""
+        d = ctypes.c_int32(0)
+        self._check(self.lib.pf_schedule_degree(self.h, float(c), int(k), ctypes.byref(d)),
+                    "pf_schedule_degree")
+        return int(d.value)
+
     def filter(self, A, U, interval, q=1, rho_max=1e6, stream=None):
         self._check(self.lib.pf_filter(self.h, _ptr(A), _ld(A), _ptr(U), _ld(U), _ptr(interval),
                                        q, rho_max, _stream(stream)), "pf_filter")
@@ -256,10 +266,11 @@ class Context:
         self._check(self.lib.pf_spectral_op(self.h, op, thr, _ptr(theta), _ptr(f), _ptr(rank),
                                             _stream(stream)), "pf_spectral_op")
 
-    def prox_step(self, V, f, tau, omega, W, A_out, obj, stream=None):
+    def prox_step(self, V, f, tau, mu, omega, W, A_out, obj, stream=None):
+        """obj <- {h = fit + mu sum|f|, fit} (device)."""
         r = 0 if W is None else W.shape[1]
         ldw = 0 if W is None else _ld(W)
-        self._check(self.lib.pf_prox_step(self.h, _ptr(V), _ld(V), _ptr(f), tau, _ptr(omega),
+        self._check(self.lib.pf_prox_step(self.h, _ptr(V), _ld(V), _ptr(f), tau, mu, _ptr(omega),
                                           _ld(omega), _ptr(W), ldw, r, _ptr(A_out), _ld(A_out),
                                           _ptr(obj), _stream(stream)), "pf_prox_step")
 
@@ -329,6 +340,15 @@ class Context:
             _ld(ycur) if ycur is not None else 0, _ptr(yprev),
             _ld(yprev) if yprev is not None else 0, _ptr(out), _ld(out), _stream(stream)),
             "pf_spmm")
+
+    def svt_kick(self, b, mu, delta, norm2, x, stream=None):
+        self._check(self.lib.pf_svt_kick(self.h, _ptr(b), b.numel(), float(mu), float(delta),
+                                         float(norm2), _ptr(x), _stream(stream)), "pf_svt_kick")
+
+    def svt_filter(self, ptr, idx, cptr, cidx, perm, x, Q, mu, eta, stream=None):
+        self._check(self.lib.pf_svt_filter(self.h, _ptr(ptr), _ptr(idx), _ptr(cptr), _ptr(cidx),
+                                           _ptr(perm), _ptr(x), _ptr(Q), _ld(Q), float(mu),
+                                           float(eta), _stream(stream)), "pf_svt_filter")
 
     def svt_ritz(self, ptr, idx, val, Q, mu, U, V, sigma, s, svp, stream=None):
         self._check(self.lib.pf_svt_ritz(self.h, _ptr(ptr), _ptr(idx), _ptr(val), _ptr(Q), _ld(Q),

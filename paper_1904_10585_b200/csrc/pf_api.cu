@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -30,7 +31,7 @@ void pf::count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 struct pf_ctx_s {
   int64_t n = 0, n_local = 0, row0 = 0;
-  int p = 0, d = 0, rank = 0, world = 1, num_sms = 148;
+  int p = 0, d = 0, d0 = 0, rank = 0, world = 1, num_sms = 148;  // d0: degree at create
   pf_dtype dtype = PF_FP64;
   bool dist = false;                           // communicator present (NCCL or loopback)
   DevState* state = nullptr;
@@ -344,7 +345,7 @@ static pf_status create_common(int64_t n, int32_t p, int32_t degree, pf_dtype dt
   if (!ctx) return PF_ERR_NOMEM;
   ctx->n = n;
   ctx->p = p;
-  ctx->d = degree;
+  ctx->d = ctx->d0 = degree;
   ctx->dtype = dtype;
   ctx->rank = rank;
   ctx->world = world;
@@ -850,6 +851,18 @@ pf_status pf_set_degree(pf_ctx ctx, int32_t degree) {
   return PF_OK;
 }
 
+pf_status pf_schedule_degree(pf_ctx ctx, double c, int32_t k, int32_t* degree) {
+  if (!ctx || k < 0 || !(c >= 0.0)) return PF_ERR_ARG;
+  // thm:conv1: convergence of PFPG needs d_k = Omega(log k / min{l, 1}); the
+  // schedule d_k = max(d_0, ceil(c ln(k + 2))) grows like c ln k (c = 0: the fixed degree d_0)
+  int dk = ctx->d0;
+  if (c > 0.0) dk = std::max(dk, (int)std::ceil(c * std::log((double)k + 2.0)));
+  if (dk > kMaxDeg) return PF_ERR_ARG;
+  ctx->d = dk;
+  if (degree) *degree = dk;
+  return PF_OK;
+}
+
 pf_status pf_orth(pf_ctx ctx, void* Uv, int64_t ldu, pf_stream stream) {
   if (!ctx || !Uv) return PF_ERR_ARG;
   cudaStream_t st = (cudaStream_t)stream;
@@ -975,10 +988,11 @@ static pf_status full_V(pf_ctx ctx, const double* V, int64_t ldv, const double**
 }
 
 pf_status pf_prox_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f, double tau,
-                       const uint32_t* omega, int64_t ldo, const double* W, int64_t ldw,
-                       int32_t r, double* A_out, int64_t lda_out, double* obj,
+                       double mu, const uint32_t* omega, int64_t ldo, const double* W,
+                       int64_t ldw, int32_t r, double* A_out, int64_t lda_out, double* obj,
                        pf_stream stream) {
   if (!ctx || !V || !f || !omega || !A_out || !obj) return PF_ERR_ARG;
+  if (!(mu >= 0.0)) return PF_ERR_ARG;
   if (!is_fp64(ctx)) return PF_ERR_UNSUPPORTED;
   if (r < 0 || r > 64 || (r > 0 && !W)) return PF_ERR_ARG;
   if (ldv < ctx->p || (ldv & 1) || !aligned16(V) || ldo < (ctx->n + 31) / 32 ||
@@ -992,8 +1006,10 @@ pf_status pf_prox_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f
   PF_CU(prox_launch(Vf, ldf, V, ldv, f, tau, omega, ldo, W, ldw, r, A_out, lda_out,
                     (int)ctx->n_local, (int)ctx->n, (int)ctx->row0, ctx->p, obj, ctx->rb_part,
                     ctx->rb_cnt, ctx->VFbuf, st));
-  // obj[0] is a sum over row blocks; obj[1] = sum |f| is replicated
-  return allreduce(ctx, obj, 1, st);
+  // obj[0] (the fit) is a sum over row blocks; obj[1] = sum |f| is replicated
+  PF_TRY(allreduce(ctx, obj, 1, st));
+  PF_CU(pfpg_obj_finish_launch(obj, mu, st));
+  return PF_OK;
 }
 
 pf_status pf_admm_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f, double t,
@@ -1211,6 +1227,51 @@ pf_status pf_spmm(pf_ctx ctx, const int32_t* ptr, const int32_t* idx, const doub
   const double coef[3] = {s1, s2, s3};
   PF_CU(spmm_launch((int)ctx->n, p, ptr, idx, val, vperm, X, ldx, coef, Ycur, ldc, Yprev, ldp,
                     out, ldo, (cudaStream_t)stream));
+  return PF_OK;
+}
+
+pf_status pf_svt_kick(pf_ctx ctx, const double* b, int64_t nnz, double mu, double delta,
+                      double norm2, double* x, pf_stream stream) {
+  if (!ctx || !b || !x || nnz < 0) return PF_ERR_ARG;
+  PF_TRY(svt_check(ctx));
+  if (!(mu > 0.0) || !(delta > 0.0) || !(norm2 > 0.0)) return PF_ERR_ARG;
+  // SVT's kicking (reading R24): x^0 = k0 delta b, k0 = ceil(mu / (delta ||P_Omega(M)||_2))
+  const double k0 = std::ceil(mu / (delta * norm2));
+  PF_CU(svt_kick_launch(x, b, k0 * delta, nnz, (cudaStream_t)stream));
+  return PF_OK;
+}
+
+pf_status pf_svt_filter(pf_ctx ctx, const int32_t* ptr, const int32_t* idx, const int32_t* cptr,
+                        const int32_t* cidx, const int32_t* perm, const double* val, double* Q,
+                        int64_t ldq, double mu, double eta, pf_stream stream) {
+  if (!ctx || !ptr || !idx || !cptr || !cidx || !perm || !val || !Q) return PF_ERR_ARG;
+  PF_TRY(svt_check(ctx));
+  const int p = ctx->p, n = (int)ctx->n, d = ctx->d;
+  if (ldq < p) return PF_ERR_DIM;
+  if (!(mu > 0.0) || !(eta >= 0.0 && eta < 1.0)) return PF_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  // damped interval of Y^T Y: [a, b] = [0, (1 - eta) mu^2] (singular values below the threshold,
+  // reading R24); L(t) = (t - c) / e (eqn:cheb-linear-map P:216-218)
+  const double a = 0.0, bb = (1.0 - eta) * mu * mu;
+  const double c = 0.5 * (a + bb), e = 0.5 * (bb - a);
+  const size_t row = (size_t)p * 8;
+  PF_CU(cudaMemcpy2DAsync(ctx->Y[0], row, Q, ldq * 8, row, n, cudaMemcpyDeviceToDevice, st));
+  int cur = 0, prev = -1;
+  for (int j = 0; j < d; ++j) {
+    // T = Y Y_j (CSR), then Y_{j+1} = s1 Y^T T + s2 Y_j + s3 Y_{j-1} (CSC view, eq:cheb)
+    const double one[3] = {1.0, 0.0, 0.0};
+    PF_CU(spmm_launch(n, p, ptr, idx, val, nullptr, ctx->Y[cur], p, one, nullptr, 0, nullptr, 0,
+                      ctx->Wbuf, p, st));
+    const int out = (prev < 0) ? (cur + 1) % 3 : 3 - cur - prev;
+    const double first[3] = {1.0 / e, -c / e, 0.0};
+    const double next[3] = {2.0 / e, -2.0 * c / e, -1.0};
+    PF_CU(spmm_launch(n, p, cptr, cidx, val, perm, ctx->Wbuf, p, j == 0 ? first : next,
+                      ctx->Y[cur], p, prev < 0 ? nullptr : ctx->Y[prev], p, ctx->Y[out], p, st));
+    prev = cur;
+    cur = out;
+  }
+  PF_TRY(orth_internal(ctx, ctx->Y[cur], st));
+  PF_CU(cudaMemcpy2DAsync(Q, ldq * 8, ctx->Y[cur], row, row, n, cudaMemcpyDeviceToDevice, st));
   return PF_OK;
 }
 

@@ -95,6 +95,8 @@ int ns_spectral(NsWork* w, const double* H, int op_soft, double thr, double* F, 
                 int* iters, cudaStream_t st);
 
 // ---- PFSVT sparse kernels (pf_svt.cu): S n x n in compressed-row form (CSR, or the CSC view)
+cudaError_t svt_kick_launch(double* x, const double* b, double alpha, int64_t nnz,
+                            cudaStream_t st);
 cudaError_t spmm_launch(int rows, int p, const int* ptr, const int* idx, const double* val,
                         const int* vperm, const double* X, int64_t ldx, const double* coef,
                         const double* ycur, int64_t ldc, const double* yprev, int64_t ldp,
@@ -202,6 +204,7 @@ cudaError_t prox_launch(const double* V, int64_t ldv, const double* Vloc, int64_
                         const double* W, int64_t ldw, int r, double* Aout, int64_t lda,
                         int n_rows, int n, int row0, int p, double* obj, double* partials,
                         int* counter, double* vf, cudaStream_t st);
+cudaError_t pfpg_obj_finish_launch(double* obj, double mu, cudaStream_t st);
 // PF_FP64_I8 on one GPU: the PFAM update also writes the digit slices of Z_new (pf_gemm_i8.cu
 // tiled layout, a8_offset) and their row scales, so the next filter skips its split pass
 struct RbDigits {

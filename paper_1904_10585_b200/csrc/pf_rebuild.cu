@@ -671,6 +671,22 @@ cudaError_t nce_launch(const double* V, int64_t ldv, const double* f, int p, dou
   return cudaGetLastError();
 }
 
+// PFPG objective h = 1/2 ||P_Omega(X - M)||_F^2 + mu sum |f| (eq:pfpg1 P:338-341 with
+// R = mu ||.||_*, whose value at X = V diag(f) V^T, V orthonormal, is mu sum_i |f_i|):
+// obj {fit, sum |f|} -> {fit + mu sum |f|, fit}
+__global__ void pfpg_obj_finish_kernel(double* obj, double mu) {
+  if (threadIdx.x != 0) return;
+  const double fit = obj[0];
+  obj[0] = fit + mu * obj[1];
+  obj[1] = fit;
+}
+
+cudaError_t pfpg_obj_finish_launch(double* obj, double mu, cudaStream_t st) {
+  count_launch();
+  pfpg_obj_finish_kernel<<<1, 32, 0, st>>>(obj, mu);
+  return cudaGetLastError();
+}
+
 cudaError_t nce_finish_launch(const double* f, int p, double* obj, cudaStream_t st) {
   count_launch();
   nce_finish_kernel<<<1, 32, 0, st>>>(f, p, obj);

@@ -13,6 +13,8 @@
 //     partials per block, summed in block order by the last block (deterministic).
 //   * svt_sigma_kernel: sigma = sqrt(max(lambda, 0)) of the Rayleigh-Ritz eigenvalues, shrink
 //     s = (sigma - mu)_+, svp = #{s > 0}, 1 / sigma for the left vectors.
+#include <algorithm>
+
 #include "pf_kernels.cuh"
 
 namespace pf {
@@ -207,6 +209,23 @@ cudaError_t scale_cols_inplace_launch(double* X, int64_t ldx, int rows, int p, c
   const long long t = (long long)rows * p;
   count_launch();
   scale_cols_inplace_kernel<<<(unsigned)((t + 255) / 256), 256, 0, st>>>(X, ldx, rows, p, d);
+  return cudaGetLastError();
+}
+
+// x = alpha b (SVT's kick, pf_svt_kick)
+__global__ void svt_kick_kernel(double* __restrict__ x, const double* __restrict__ b, double alpha,
+                                int64_t nnz) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x)
+    x[e] = alpha * b[e];
+}
+
+cudaError_t svt_kick_launch(double* x, const double* b, double alpha, int64_t nnz,
+                            cudaStream_t st) {
+  if (nnz == 0) return cudaSuccess;
+  count_launch();
+  const int grid = (int)std::min<int64_t>((nnz + 255) / 256, 4096);
+  svt_kick_kernel<<<grid, 256, 0, st>>>(x, b, alpha, nnz);
   return cudaGetLastError();
 }
 

@@ -11,7 +11,7 @@ import numpy as np
 import torch
 
 from pfinputs import (Config, initial_block, lanczos_start, cfg1_problem, cfg1_noise, pfpg_problem,
-                      pfam_problem, cfg5_problem, nce_problem, degree_at)
+                      pfam_problem, cfg5_problem, nce_problem)
 
 from ._lib import Context, PF_FP64, PF_FP64_I8, PF_TF32, PF_OP_PSD, PF_OP_SOFT_THRESHOLD
 
@@ -126,8 +126,8 @@ class Solver:
             self.thr = cfg.tau * prob["mu"]
             self.A = _iterate64(nl, n)
             # X_0 = 0: A_0 = 0 - tau Omega o (0 - M)  (the update kernel with zero factors)
-            self.ctx.prox_step(self.V.zero_(), self.f, cfg.tau, self.omega, self.W, self.A,
-                               self.obj, stream)
+            self.ctx.prox_step(self.V.zero_(), self.f, cfg.tau, self.mu, self.omega, self.W,
+                               self.A, self.obj, stream)
         elif cfg.mode == "pfam":
             if "adj_bits" in devp:
                 self.adj, self.deg = devp["adj_bits"], devp["deg"]
@@ -215,7 +215,7 @@ class Solver:
         else:
             ctx.interval_soft(self.thr, cfg.eta, self.interval, st)
         if cfg.deg_c > 0.0:                                   # thm:conv1 degree schedule (NEXT-4)
-            ctx.set_degree(degree_at(cfg, k))
+            ctx.schedule_degree(cfg.deg_c, k)
         for _ in range(cfg.warmup if k == 0 else 1):
             ctx.filter(self.A, self.U, self.interval, cfg.q, cfg.rho_max, st)
         if cfg.rr_ns:
@@ -232,7 +232,8 @@ class Solver:
         ctx.spectral_op(self.op, self.thr, self.theta, self.f, self.rank, st)
         self.last_ns = False
         if cfg.mode == "pfpg":
-            ctx.prox_step(self.V, self.f, cfg.tau, self.omega, self.W, self.A, self.obj, st)
+            ctx.prox_step(self.V, self.f, cfg.tau, self.mu, self.omega, self.W, self.A, self.obj,
+                          st)
         elif cfg.mode == "pfam":
             ctx.admm_step(self.V, self.f, cfg.t, self.adj, self.deg, self.A, self.obj, st)
         elif cfg.mode == "nce":
@@ -263,10 +264,9 @@ class Solver:
         return (v.T if self.f32 else v).astype(np.float64)
 
     def objective(self) -> tuple[float, float]:
-        """(objective, aux) on the host: PFPG (fit + mu sum|f|, fit); PFAM (<C,W>, ||dZ||_F)."""
+        """(objective, aux) on the host, as the library wrote them: PFPG (h = fit + mu sum|f|,
+        fit); PFAM (<C,W>, ||dZ||_F); NCE (F(x), ||grad F||)."""
         o = self.obj.cpu().numpy()
-        if self.cfg.mode == "pfpg":
-            return float(o[0] + self.mu * o[1]), float(o[0])
         if self.cfg.mode == "nce":
             return float(o[0]), float(o[1])            # F(x_k), ||grad F(x_k)||
         return float(o[0]), float(o[1])

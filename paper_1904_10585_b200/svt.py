@@ -1,7 +1,9 @@
 """GPU driver of polynomial-filtered SVT (PFSVT, NEXT-3; paper §5.2, eqn:svt P:1098-1104) over
-the C ABI: sequences pf_spmm (the filter on Y^T Y), pf_orth, pf_svt_ritz and pf_svt_update.
-Python only moves the problem data to the device and computes the host scalars of the interval
-(reading R24); every step of the iteration runs in libpf kernels."""
+the C ABI: sequences pf_svt_kick, pf_svt_filter (the filter on Y^T Y), pf_svt_ritz and
+pf_svt_update.
+Python only moves the problem data to the device and sequences the calls: the kick, the filter
+(interval, recurrence coefficients, sparse products, orthonormalisation; reading R24), the
+singular-triplet Rayleigh-Ritz and the dual step all run behind the C ABI."""
 from __future__ import annotations
 
 import math
@@ -42,12 +44,12 @@ class SVTSolver:
                                                  _i32(prob["perm"]))
         self.b = _f64(prob["b"])
         self.nb = float(np.linalg.norm(prob["b"]))
-        # SVT's kick (reading R24): x^0 = k0 delta b, k0 = ceil(mu / (delta ||P_Omega(M)||_2))
-        k0 = math.ceil(self.mu / (self.delta * prob["norm2"]))
-        self.x = _f64(k0 * self.delta * prob["b"])
+        self.x = torch.empty_like(self.b)
         self.svp = torch.zeros(1, dtype=torch.int32, device="cuda")
         self.rss = torch.zeros(1, dtype=torch.float64, device="cuda")
         self._use(p)
+        # SVT's kick x^0 = k0 delta b (reading R24), on the device
+        self.ctx.svt_kick(self.b, self.mu, self.delta, prob["norm2"], self.x, stream)
         self.Q = self.blocks[0]
         self.Q.copy_(torch.from_numpy(np.ascontiguousarray(initial_block(cfg)[:, :p])))
         self.ctx.orth(self.Q, stream)
@@ -69,7 +71,7 @@ class SVTSolver:
             self._per_p[p] = {
                 "ctx": Context(n, p, max(cfg.d, 1),
                                dtype=PF_FP64_I8 if cfg.dtype == "f64i8" else PF_FP64),
-                "blocks": [buf() for _ in range(4)], "T": buf(), "U": buf(),
+                "blocks": [buf() for _ in range(2)], "T": None, "U": buf(),
                 "sigma": torch.zeros(p, dtype=torch.float64, device="cuda"),
                 "s": torch.zeros(p, dtype=torch.float64, device="cuda")}
         d = self._per_p[p]
@@ -78,24 +80,9 @@ class SVTSolver:
         self.sigma, self.s = d["sigma"], d["s"]
 
     def _filter(self):
-        """Q <- orth(T_d(L(Y^T Y)) Q), L(t) = (t - c)/e on [a, b] = [0, (1 - eta) mu^2]."""
-        cfg, ctx, st = self.cfg, self.ctx, self.stream
-        a, b = 0.0, (1.0 - cfg.eta) * self.mu * self.mu
-        c, e = 0.5 * (a + b), 0.5 * (b - a)
-        cur, prev = self.Q, None
-        for j in range(cfg.d):
-            ctx.spmm(self.row_ptr, self.col, self.x, cur, self.T, stream=st)        # T = Y Y_j
-            out = next(y for y in self.blocks if y is not cur and y is not prev)
-            if j == 0:
-                ctx.spmm(self.col_ptr, self.row_csc, self.x, self.T, out, (1.0 / e, -c / e, 0.0),
-                         ycur=cur, vperm=self.perm, stream=st)                     # Y^T T ...
-            else:
-                ctx.spmm(self.col_ptr, self.row_csc, self.x, self.T, out,
-                         (2.0 / e, -2.0 * c / e, -1.0), ycur=cur, yprev=prev,
-                         vperm=self.perm, stream=st)
-            prev, cur = cur, out
-        ctx.orth(cur, st)
-        self.Q = cur
+        """Q <- orth(T_d(L(Y^T Y)) Q) on [0, (1 - eta) mu^2] (pf_svt_filter)."""
+        self.ctx.svt_filter(self.row_ptr, self.col, self.col_ptr, self.row_csc, self.perm, self.x,
+                            self.Q, self.mu, self.cfg.eta, self.stream)
 
     def step(self):
         cfg, ctx, st = self.cfg, self.ctx, self.stream

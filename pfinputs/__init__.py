@@ -10,6 +10,6 @@ from .generators import (  # noqa: F401
     initial_block, lanczos_start, cfg1_problem, cfg1_noise,
     pfpg_problem, pfam_problem, sym_bernoulli_bitmask, unpack_bitmask,
     bitmask_words, cfg5_spectrum, cfg5_reflectors, cfg5_basis_columns, Cfg5Matrix, cfg5_problem,
-    hash_gauss, cfg5_noise_rows, cfg5_perturb, NEXT_CONFIGS, nce_problem, degree_at,
+    hash_gauss, cfg5_noise_rows, cfg5_perturb, NEXT_CONFIGS, nce_problem,
     svt_problem, svt_guard_block,
 )

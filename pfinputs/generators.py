@@ -385,11 +385,38 @@ def cfg5_noise_rows(cfg: Config, k: int, i0: int, i1: int) -> np.ndarray:
     return e.astype(np.float32)
 
 
-def cfg5_perturb(cfg: Config, A32: np.ndarray, k: int, chunk: int = 1024) -> None:
-    """In place: A_{k+1} = fl32(A_k + E_k) (fp32 add, round to nearest) on an fp32 array."""
-    for i0 in range(0, cfg.n, chunk):
-        i1 = min(cfg.n, i0 + chunk)
-        A32[i0:i1] += cfg5_noise_rows(cfg, k, i0, i1)
+def cfg5_perturb(cfg: Config, A32: np.ndarray, k: int, chunk: int = 256,
+                 threads: int | None = None) -> None:
+    """In place: A_{k+1} = fl32(A_k + E_k) (fp32 add, round to nearest) on an fp32 array.
+
+    E_k is symmetric entry by entry (the hash keys on the unordered pair), so each row chunk
+    [i0, i1) draws only its upper part E[i0:i1, i0:] and adds it to both A[i0:i1, i0:] and the
+    mirrored A[i1:, i0:i1] -- the same values cfg5_noise_rows gives row by row.  Chunks touch
+    disjoint entries, so they run on a thread pool (numpy releases the GIL in the element-wise
+    kernels); the result does not depend on the thread count."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
+    n = cfg.n
+
+    def one(i0):
+        i1 = min(n, i0 + chunk)
+        rows = np.arange(i0, i1)[:, None]
+        cols = np.arange(i0, n)[None, :]
+        e = cfg.noise * hash_gauss(cfg.seed, k, rows, cols)
+        e = np.where(rows == cols, e, e * 0.7071067811865476).astype(np.float32)
+        A32[i0:i1, i0:] += e
+        if i1 < n:
+            A32[i1:, i0:i1] += e[:, i1 - i0:].T
+
+    starts = range(0, n, chunk)
+    nt = threads or len(os.sched_getaffinity(0))
+    if nt <= 1 or n <= chunk:
+        for i0 in starts:
+            one(i0)
+        return
+    with ThreadPoolExecutor(max_workers=nt) as ex:
+        list(ex.map(one, starts))
 
 
 # ----------------------------------------------------------------------------- NCE (NEXT-1)
@@ -441,12 +468,3 @@ def svt_problem(cfg: Config) -> dict:
     return {"ML": ML, "MR": MR, "I": I, "J": J, "b": b, "row_ptr": row_ptr, "col_ptr": col_ptr,
             "perm": perm, "rows_csc": I[perm], "norm2": norm2,
             "tau": cfg.svt_tau * n, "delta": cfg.svt_delta / cfg.sr}
-
-
-def degree_at(cfg: Config, k: int) -> int:
-    """Chebyshev degree of iteration k: cfg.d, or the thm:conv1 schedule
-    d_k = max(cfg.d, ceil(deg_c * log(k + 2))) when deg_c > 0 (NEXT-4)."""
-    import math
-    if cfg.deg_c <= 0.0:
-        return cfg.d
-    return max(cfg.d, int(math.ceil(cfg.deg_c * math.log(k + 2))))

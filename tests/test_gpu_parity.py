@@ -49,8 +49,9 @@ def test_orth_span_and_orthonormality(p):
     assert np.max(O.sin_theta(O.orth(Y), Q)) < 1e-11
 
 
-def test_orth_shifted_fallback_on_ill_conditioned_block():
-    n, p = 900, 32
+@pytest.mark.parametrize("p", [32, 64, 128])   # chol_inv, chol_inv_reg (p = 64), chol_inv_big
+def test_orth_shifted_fallback_on_ill_conditioned_block(p):
+    n = 900
     rng = np.random.default_rng(3)
     # kappa(Y) = 1e11 > u^-1/2 with mixed singular directions (column scaling alone would not
     # hurt Cholesky, which is invariant to diagonal scaling)
@@ -170,13 +171,15 @@ def test_prox_step_matches_oracle(p, r):
     ctx = _ctx(n, p)
     A = torch.full((n, n), 7.0, dtype=torch.float64, device="cuda")
     obj = torch.zeros(2, dtype=torch.float64, device="cuda")
-    ctx.prox_step(_dev(V), _dev(f), 1.0, torch.from_numpy(bits.view(np.int32)).cuda(), _dev(W), A, obj)
+    mu = 0.37
+    ctx.prox_step(_dev(V), _dev(f), 1.0, mu, torch.from_numpy(bits.view(np.int32)).cuda(), _dev(W),
+                  A, obj)
     A = A.cpu().numpy()
     scale = np.abs(A_ref).max()
     assert np.max(np.abs(A - A_ref)) < 1e-13 * scale * max(p, r)
     o = obj.cpu().numpy()
-    assert o[0] == pytest.approx(fit_ref, rel=1e-12)
-    assert o[1] == pytest.approx(np.abs(f).sum(), rel=1e-14)
+    assert o[0] == pytest.approx(fit_ref + mu * np.abs(f).sum(), rel=1e-12)   # h(X)
+    assert o[1] == pytest.approx(fit_ref, rel=1e-12)
 
 
 @pytest.mark.parametrize("p", [16, 64, 128])

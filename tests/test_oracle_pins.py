@@ -549,14 +549,45 @@ def test_filter_q_repeats_diagonal_closed_form():
         np.testing.assert_allclose(np.max(O.sin_theta(O.orth(scale[:, None] * U), Q)), 0, atol=1e-10)
 
 
-def test_degree_schedule_values():
-    """thm:conv1: d_k = ceil(c log(k + 2)), floored at the configured d."""
+def test_degree_schedule_grows_like_log_k():
+    """thm:conv1 asks for d_k = Omega(log k / min{l, 1}): the schedule is floored at the
+    configured degree, non-decreasing, unbounded, and d_k / ln k stays within [c, c + 1/ln k]
+    (Theta(log k): it neither stalls nor grows faster than the theorem needs)."""
     import math
-    from pfinputs import degree_at
-    cfg = reduced(CONFIGS[1], d=2, deg_c=3.0)
-    for k in range(50):
-        assert degree_at(cfg, k) == max(2, math.ceil(3.0 * math.log(k + 2)))
-    assert degree_at(reduced(CONFIGS[1]), 37) == CONFIGS[1].d
+    c = 2.5
+    ks = [0, 1, 2, 5, 10, 100, 10**3, 10**4, 10**6, 10**9]
+    ds = [O.degree_schedule(3, c, k) for k in ks]
+    assert all(d >= 3 for d in ds) and ds == sorted(ds)
+    assert O.degree_schedule(3, c, 0) == 3                  # c ln 2 < 3: the floor
+    for k in ks[5:]:
+        r = O.degree_schedule(1, c, k) / math.log(k + 2)
+        assert c <= r <= c + 1.0 / math.log(k + 2), (k, r)
+    assert O.degree_schedule(1, c, 10**9) > O.degree_schedule(1, c, 10**4) + 20
+    assert all(O.degree_schedule(4, 0.0, k) == 4 for k in ks)       # c = 0: fixed degree
+
+
+def test_degree_schedule_converges_where_fixed_degree_lags():
+    """What the schedule is for (thm:conv1): on a static config-1 matrix (8 positive eigenvalues
+    of a Haar basis, gap to the damped negative bulk) the warm-started filtered projection with a
+    growing degree reaches the exact P_+(A) to rounding, while the fixed linear polynomial
+    (d = 1, plain subspace iteration on L(A)) still lags after the same number of iterations."""
+    cfg0 = reduced(CONFIGS[1], n=160, p=12, d=1, warmup=1, iters=8, noise=0.0)
+    A = O.run(cfg0, iters=1)["final_A"]
+    Xe = O.exact_spectral(A, "psd")
+    nrm = np.linalg.norm(Xe)
+
+    def errs(cfg):
+        out = []
+        for r in O.run(cfg)["records"]:
+            X = (r["V"] * r["f"]) @ r["V"].T
+            out.append(np.linalg.norm(X - Xe) / nrm)
+        return np.array(out)
+
+    fixed = errs(cfg0)
+    sched = errs(reduced(cfg0, deg_c=3.0))
+    assert sched[-1] <= 1e-12, sched
+    assert fixed[-1] >= 1e3 * max(sched[-1], 1e-16), (fixed[-1], sched[-1])
+    assert np.all(sched <= fixed * (1 + 1e-9) + 1e-14)      # never worse than the fixed degree
 
 
 def test_psd_iterate_skips_filter_compression_closed_form():

@@ -40,7 +40,7 @@ def main(cfg_id=3, iters=14, **over):
             ctx.spectral_op(s.op, s.thr, s.theta, s.f, s.rank, st)
             ev[5].record(st)
             if cfg.mode == "pfpg":
-                ctx.prox_step(s.V, s.f, cfg.tau, s.omega, s.W, s.A, s.obj, st)
+                ctx.prox_step(s.V, s.f, cfg.tau, s.mu, s.omega, s.W, s.A, s.obj, st)
             elif cfg.mode == "pfam":
                 ctx.admm_step(s.V, s.f, cfg.t, s.adj, s.deg, s.A, s.obj, st)
             ev[6].record(st)
