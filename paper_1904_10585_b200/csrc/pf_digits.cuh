@@ -61,10 +61,14 @@ PF_DEV void digit_words_sc(double x, double sc, uint32_t& wlo, uint32_t& whi) {
   const double y = __dadd_rz(fabs(x) * sc, 4503599627370496.0);
   const unsigned long long b = (unsigned long long)__double_as_longlong(y);
   const uint32_t l32 = (uint32_t)b, h32 = (uint32_t)(b >> 32);
-  const uint32_t lo = l32 & 0x0FFFFFFFu;
+  // U bits 28..48 (bits 52.. of b hold y's exponent: masked below)
   const uint32_t h = __funnelshift_r(l32, h32, 28);
-  wlo = (lo & 0x7Fu) | ((lo << 1) & 0x7F00u) | ((lo << 2) & 0x7F0000u) | ((lo << 3) & 0x7F000000u);
-  whi = (h & 0x7Fu) | ((h << 1) & 0x7F00u) | ((h << 2) & 0x7F0000u);
+  // 7-bit groups to bytes in two steps: 14-bit halves to the two 16-bit lanes, then 7-bit
+  // groups to the bytes of each lane (shift + LOP3 each; the same bytes as one mask per byte)
+  const uint32_t tl = (l32 & 0x3FFFu) | ((l32 << 2) & 0x3FFF0000u);
+  wlo = (tl & 0x007F007Fu) | ((tl << 1) & 0x7F007F00u);
+  const uint32_t th = (h & 0x3FFFu) | ((h << 2) & 0x007F0000u);
+  whi = (th & 0x007F007Fu) | ((th << 1) & 0x00007F00u);
   if (__double_as_longlong(x) < 0) {
     wlo = (0x80808080u - wlo) ^ 0x80808080u;
     whi = (0x80808080u - whi) ^ 0x80808080u;

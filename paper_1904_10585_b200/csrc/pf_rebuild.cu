@@ -18,6 +18,7 @@
 //    MMA loop so its HBM latency overlaps the math; masks (Omega / adjacency) are packed bits.
 //  * reductions are deterministic: per-CTA partials summed in CTA order by the last CTA.
 #include <algorithm>
+#include <climits>
 #include <cmath>
 
 #include "pf_digits.cuh"
@@ -58,8 +59,9 @@ struct RbArgs {
   // Z disappears
   int8_t* A8;
   int KB;
-  const int* E;
+  const int* E;     // the digit scale exponent Eg (one int, pfam_bound2_kernel)
   int S;
+  double* rscale;   // row scales of the digit slices (all 2^Eg), written by the update
 };
 
 template <int P, bool PFPG>
@@ -88,38 +90,81 @@ __device__ __forceinline__ void pair_of(int e, int T, int& I, int& J) {
   J = i + (e - (int)((long long)i * T - (long long)i * (i - 1) / 2));
 }
 
-// Z_new tile (64 x 64 in Tz, row pitch 65) -> digit slices: thread t owns row r = t / 4 and 16
-// consecutive columns; the mirror tile (rows j0.., columns i0..) reads Tz transposed
-template <int S>
-__device__ __forceinline__ void rb_digits(const RbArgs& a, const double* Tz, int i0, int j0,
-                                          bool mirror, int tid, int eI, int eJ) {
-  const int r = tid >> 2, cb = (tid & 3) * 16;
-  auto put = [&](int row, int col0, const double (&v)[16], int E) {
-    uint32_t w[4][S];
+// Z_new staging for the digit output: 4 x 4 blocks stored column-block-major, 16 doubles + 2 pad
+// per block (lanes reading 16-byte chunks of consecutive blocks hit distinct bank groups)
+constexpr int kTzBlk = 18;
+__device__ __forceinline__ int tz4(int r, int c) {
+  return ((c >> 2) * (kRb / 4) + (r >> 2)) * kTzBlk + (r & 3) * 4 + (c & 3);
+}
+constexpr int kDgPitch = 80;  // bytes per staged digit row (64 + 16: 16-byte rows, few conflicts)
+static_assert(7 * kRb * kDgPitch <= (kRb / 4) * (kRb / 4) * kTzBlk * 8, "digit staging fits");
+
+// Z_new tile (64 x 64, staged in Tz4) -> digit slices of the tile AND of its mirror.  The fused
+// digits use ONE scale 2^E for the whole matrix (E = the max of the row-bound exponents), so the
+// mirror tile's digits are the byte transpose of the tile's: thread t owns the 4 x 4 block
+// (rows 4 (t % 16).., cols 4 (t / 16)..) and forms its digit words once (4 rows x S slices, a
+// word = 4 consecutive columns).  Mirror rows: the 4 x 4 byte transpose of each slice's words,
+// stored directly (16 consecutive lanes = one 64-byte mirror row).  Tile rows: staged through
+// shared memory (the same buffer, after every thread has read its values) and stored as 16-byte
+// row pieces.  Entries outside the matrix are written as 0.
+template <int S, bool FULL>
+__device__ __forceinline__ void rb_digits(const RbArgs& a, double* Tz, int i0, int j0,
+                                          bool mirror, int tid, int E) {
+  // FULL: the tile and its mirror lie inside the matrix (no bounds checks; constant offsets)
+  const int rb = (tid & 15) * 4, cb = (tid >> 4) * 4;
+  uint32_t w[4][S];
+  const double* blk = Tz + ((cb >> 2) * (kRb / 4) + (rb >> 2)) * kTzBlk;
+  const int c = j0 + cb;
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      i8::slices4<S>(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3], E, w[q]);
-    int8_t* dst = a.A8 + i8::a8_offset(row, col0, 0, a.KB, S);  // 16 bytes inside one k-block
+  for (int i = 0; i < 4; ++i) {
+    const double2 v01 = *reinterpret_cast<const double2*>(blk + i * 4);
+    const double2 v23 = *reinterpret_cast<const double2*>(blk + i * 4 + 2);
+    if (FULL) {
+      i8::slices4<S>(v01.x, v01.y, v23.x, v23.y, E, w[i]);
+    } else {
+      const bool rok = i0 + rb + i < a.n_rows;
+      i8::slices4<S>(rok && c < a.n ? v01.x : 0.0, rok && c + 1 < a.n ? v01.y : 0.0,
+                     rok && c + 2 < a.n ? v23.x : 0.0, rok && c + 3 < a.n ? v23.y : 0.0, E,
+                     w[i]);
+    }
+  }
+  if (mirror && (FULL || i0 + rb < a.n)) {
+    // rows c .. c+3 of the mirror share one 128-row tile: slice s, row c + j at + s 8 KB + 64 j
+    int8_t* base = a.A8 + i8::a8_offset(c, i0 + rb, 0, a.KB, S);
+#pragma unroll
+    for (int sl = 0; sl < S; ++sl) {
+      uint32_t t[4];
+      i8::transpose4(w[0][sl], w[1][sl], w[2][sl], w[3][sl], t);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (FULL || c + j < a.n)
+          __stcs(reinterpret_cast<uint32_t*>(base + sl * 8192 + j * 64), t[j]);
+    }
+  }
+  __syncthreads();  // every thread has read its values: the staging becomes the digit buffer
+  uint8_t* dg = reinterpret_cast<uint8_t*>(Tz);  // [S][64 rows][kDgPitch]
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int sl = 0; sl < S; ++sl)
-      __stcs(reinterpret_cast<uint4*>(dst + sl * 8192),
-             make_uint4(w[0][sl], w[1][sl], w[2][sl], w[3][sl]));
-  };
-  // a 16-column chunk starting below n lies inside the padded row (KB 64-byte k-blocks); entries
-  // past n
-  // (never read: the GEMM's tensor map ends at n) are written as 0
-  if (i0 + r < a.n_rows && j0 + cb < a.n) {
-    double v[16];
+      *reinterpret_cast<uint32_t*>(dg + (sl * kRb + rb + i) * kDgPitch + cb) = w[i][sl];
+  __syncthreads();
+  // tile rows: thread t stores the 16-byte piece q = t % 4 of row t / 4 of every slice
+  const int row = tid >> 2, q = tid & 3;
+  if (FULL || (j0 < a.n && i0 + row < a.n_rows)) {
+    int8_t* base = a.A8 + i8::a8_offset(i0 + row, j0 + 16 * q, 0, a.KB, S);
 #pragma unroll
-    for (int q = 0; q < 16; ++q) v[q] = j0 + cb + q < a.n ? Tz[r * 65 + cb + q] : 0.0;
-    put(i0 + r, j0 + cb, v, eI);
+    for (int sl = 0; sl < S; ++sl)
+      __stcs(reinterpret_cast<uint4*>(base + sl * 8192),
+             *reinterpret_cast<const uint4*>(dg + (sl * kRb + row) * kDgPitch + 16 * q));
   }
-  if (mirror && j0 + r < a.n && i0 + cb < a.n) {
-    double v[16];
-#pragma unroll
-    for (int q = 0; q < 16; ++q) v[q] = i0 + cb + q < a.n ? Tz[(cb + q) * 65 + r] : 0.0;
-    put(j0 + r, i0 + cb, v, eJ);
-  }
+}
+
+template <int S>
+__device__ __forceinline__ void rb_digits_any(const RbArgs& a, double* Tz, int i0, int j0,
+                                              bool mirror, int tid, int E, bool full) {
+  if (full) rb_digits<S, true>(a, Tz, i0, j0, mirror, tid, E);
+  else rb_digits<S, false>(a, Tz, i0, j0, mirror, tid, E);
 }
 
 template <int P, bool PFPG>
@@ -127,20 +172,20 @@ __global__ void __launch_bounds__(kRbThreads, 2) rebuild_kernel(const RbArgs a) 
   using C = RbCfg<P, PFPG>;
   extern __shared__ __align__(16) double sm[];
   __shared__ double red[32];
-  __shared__ double fs[P];
   __shared__ int s_last;
   const int ldw_s = a.rpad + 4;
   double* Vi = sm;                  // 64 x LD  rows I (local row block)
   double* Vj = sm + kRb * C::LD;    // 64 x LD  rows J
   double* Wi = Vj + kRb * C::LD;    // 64 x ldw_s (PFPG)
   double* Wj = Wi + kRb * ldw_s;
-  double* Tz = Vj + kRb * C::LD;    // 64 x 65 staging of Z_new (PFAM digit output)
+  double* Tz = Vj + kRb * C::LD;    // block-major staging of Z_new (PFAM digit output, tz4)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g8 = lane >> 2, t4 = lane & 3;
   const int wm = warp & 1, wn = warp >> 1;  // 2 (rows) x 4 (cols) warps, 32 x 16 each
   const int tc = (a.n + kRb - 1) / kRb, tr = (a.n_rows + kRb - 1) / kRb;
   const int ntiles = a.sym ? (tc * (tc + 1)) / 2 : tr * tc;
-  for (int c = tid; c < P; c += kRbThreads) fs[c] = a.f[c];
+  // 16-byte stores of row pairs need an aligned base and an even pitch
+  const bool al = ((reinterpret_cast<uintptr_t>(a.Out) & 15) == 0) && ((a.ldo & 1) == 0);
   if (PFPG && a.w_async)  // zero padding columns of both W panels (never written by cp.async)
     for (int e = tid; e < kRb * ldw_s; e += kRbThreads)
       if (e % ldw_s >= a.r - (a.r & 1)) Wi[e] = Wj[e] = 0.0;
@@ -153,8 +198,17 @@ __global__ void __launch_bounds__(kRbThreads, 2) rebuild_kernel(const RbArgs a) 
   const int t_end = (int)(nt_all * (blockIdx.x + 1) / gridDim.x);
   int curI = -1;
   // digits of the previous tile's Z_new (staged in Tz) are written during this tile's panel loads
-  int pv_i0 = -1, pv_j0 = 0, pv_eI = 0, pv_eJ = 0;
-  bool pv_mirror = false;
+  int pv_i0 = -1, pv_j0 = 0;
+  bool pv_mirror = false, pv_full = false;
+  // one digit scale 2^Eg for the whole matrix (pfam_bound2_kernel); the row scales the next
+  // product reads are all 2^Eg
+  int Eg = 0;
+  if (!PFPG && a.A8) {
+    Eg = *a.E;
+    const double sc = i8::pow2(Eg);
+    for (int i = blockIdx.x * kRbThreads + tid; i < a.n_rows; i += gridDim.x * kRbThreads)
+      a.rscale[i] = sc;
+  }
   for (int tile = t_begin; tile < t_end; ++tile) {
   int I, J;
   if (a.sym) {
@@ -168,6 +222,11 @@ __global__ void __launch_bounds__(kRbThreads, 2) rebuild_kernel(const RbArgs a) 
   const double wgt = mirror ? 2.0 : 1.0;
   const bool newI = (I != curI);
   curI = I;
+  // fast tile: inside the matrix, off the global diagonal, aligned rows -- the epilogue runs
+  // without bounds, diagonal or alignment checks
+  const int gi0 = a.row0 + i0;
+  const bool full = i0 + kRb <= a.n_rows && j0 + kRb <= a.n;
+  const bool fast = full && al && !(gi0 < j0 + kRb && j0 < gi0 + kRb);
   __syncthreads();  // the previous tile's readers of the panels are done
 
   // ---- stage V panels (cp.async 16 B), f, W panels; the I panel only when I changed
@@ -214,15 +273,8 @@ __global__ void __launch_bounds__(kRbThreads, 2) rebuild_kernel(const RbArgs a) 
   }
 
   if (!PFPG && a.A8 && pv_i0 >= 0) {  // overlaps the cp.async panel loads in flight
-    if (a.S == 7) rb_digits<7>(a, Tz, pv_i0, pv_j0, pv_mirror, tid, pv_eI, pv_eJ);
-    else rb_digits<6>(a, Tz, pv_i0, pv_j0, pv_mirror, tid, pv_eI, pv_eJ);
-  }
-  // row exponents of this tile's digit rows, consumed one tile later (load latency hidden)
-  int eI = 0, eJ = 0;
-  if (!PFPG && a.A8) {
-    const int r = tid >> 2;
-    if (i0 + r < a.n_rows) eI = __ldg(a.E + i0 + r);
-    if (mirror && j0 + r < a.n) eJ = __ldg(a.E + j0 + r);
+    if (a.S == 7) rb_digits_any<7>(a, Tz, pv_i0, pv_j0, pv_mirror, tid, Eg, pv_full);
+    else rb_digits_any<6>(a, Tz, pv_i0, pv_j0, pv_mirror, tid, Eg, pv_full);
   }
   // ---- PFAM: prefetch the old iterate at this thread's fragment positions (overlaps the MMA)
   double zo[2][2][kNt][2];
@@ -232,12 +284,19 @@ __global__ void __launch_bounds__(kRbThreads, 2) rebuild_kernel(const RbArgs a) 
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int li = i0 + wm * 32 + mt * 16 + g8 + 8 * h;
+        const double* zrow = a.Out + (size_t)li * a.ldo + j0 + wn * kWn + 2 * t4;
 #pragma unroll
         for (int nt = 0; nt < kNt; ++nt) {
           const int j = j0 + wn * kWn + nt * 8 + 2 * t4;
+          if (fast) {
+            const double2 z2 = __ldcs(reinterpret_cast<const double2*>(zrow + nt * 8));
+            zo[mt][h][nt][0] = z2.x;
+            zo[mt][h][nt][1] = z2.y;
+            continue;
+          }
           zo[mt][h][nt][0] = zo[mt][h][nt][1] = 0.0;
           if (li < a.n_rows && j < a.n) {
-            const double* zp = a.Out + (size_t)li * a.ldo + j;
+            const double* zp = zrow + nt * 8;
             if (j + 1 < a.n && ((reinterpret_cast<uintptr_t>(zp) & 15) == 0)) {
               const double2 z2 = __ldcs(reinterpret_cast<const double2*>(zp));
               zo[mt][h][nt][0] = z2.x;
@@ -264,7 +323,7 @@ __global__ void __launch_bounds__(kRbThreads, 2) rebuild_kernel(const RbArgs a) 
   cp_async_wait_all();
   __syncthreads();
 
-  // ---- X tile = (V_I diag(f)) V_J^T on DMMA
+  // ---- X tile = (V_I diag(f)) V_J^T on DMMA (fragment loads at constant offsets)
   double acc[2][kNt][4];
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
@@ -272,21 +331,24 @@ __global__ void __launch_bounds__(kRbThreads, 2) rebuild_kernel(const RbArgs a) 
     for (int nt = 0; nt < kNt; ++nt)
 #pragma unroll
       for (int k = 0; k < 4; ++k) acc[mt][nt][k] = 0.0;
-#pragma unroll 4
-  for (int ks = 0; ks < P / 4; ++ks) {
-    const int k = ks * 4 + t4;
-    double a0[2], a1[2], b0[kNt];
+  {
+    const double* pa = Vi + (wm * 32 + g8) * C::LD + t4;
+    const double* pb = Vj + (wn * kWn + g8) * C::LD + t4;
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt) {
-      a0[mt] = Vi[(wm * 32 + mt * 16 + g8) * C::LD + k];
-      a1[mt] = Vi[(wm * 32 + mt * 16 + g8 + 8) * C::LD + k];
+    for (int ks = 0; ks < P / 4; ++ks) {
+      double a0[2], a1[2], b0[kNt];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        a0[mt] = pa[(mt * 16) * C::LD + ks * 4];
+        a1[mt] = pa[(mt * 16 + 8) * C::LD + ks * 4];
+      }
+#pragma unroll
+      for (int nt = 0; nt < kNt; ++nt) b0[nt] = pb[(nt * 8) * C::LD + ks * 4];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < kNt; ++nt) dmma16884(acc[mt][nt], a0[mt], a1[mt], b0[nt]);
     }
-#pragma unroll
-    for (int nt = 0; nt < kNt; ++nt) b0[nt] = Vj[(wn * kWn + nt * 8 + g8) * C::LD + k];
-#pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < kNt; ++nt) dmma16884(acc[mt][nt], a0[mt], a1[mt], b0[nt]);
   }
   double accm[PFPG ? 2 : 1][PFPG ? kNt : 1][4];
   if (PFPG) {
@@ -315,6 +377,53 @@ __global__ void __launch_bounds__(kRbThreads, 2) rebuild_kernel(const RbArgs a) 
   }
 
   // ---- elementwise update + reductions
+  if (fast) {
+    // interior off-diagonal tile: no bounds / diagonal / alignment branches; the tile's sums are
+    // accumulated unweighted and folded in once
+    double ts0 = 0.0, ts1 = 0.0;
+    const double qt = 0.25 * a.tt;
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int rt = wm * 32 + mt * 16 + g8 + 8 * h;
+        const int li = i0 + rt;
+        const uint32_t word = wbits[mt][h];
+        double* rowp = a.Out + (size_t)li * a.ldo + j0;
+#pragma unroll
+        for (int nt = 0; nt < kNt; ++nt) {
+          const int ct = wn * kWn + nt * 8 + 2 * t4;
+          const bool b0 = (word >> (ct & 31)) & 1u, b1 = (word >> ((ct + 1) & 31)) & 1u;
+          const double x0 = acc[mt][nt][2 * h], x1 = acc[mt][nt][2 * h + 1];
+          double o0, o1;
+          if (PFPG) {
+            const double d0 = x0 - accm[PFPG ? mt : 0][PFPG ? nt : 0][2 * h];
+            const double d1 = x1 - accm[PFPG ? mt : 0][PFPG ? nt : 0][2 * h + 1];
+            o0 = b0 ? x0 - a.tt * d0 : x0;
+            o1 = b1 ? x1 - a.tt * d1 : x1;
+            ts0 += (b0 ? d0 * d0 : 0.0) + (b1 ? d1 * d1 : 0.0);
+          } else {
+            o0 = b0 ? x0 - qt : x0;                 // W_ij - t C_ij, C_ij = adj_ij / 4
+            o1 = b1 ? x1 - qt : x1;
+            ts0 += (b0 ? x0 : 0.0) + (b1 ? x1 : 0.0);
+            const double e0 = o0 - zo[mt][h][nt][0], e1 = o1 - zo[mt][h][nt][1];
+            ts1 = fma(e0, e0, fma(e1, e1, ts1));
+            if (a.A8) *reinterpret_cast<double2*>(Tz + tz4(rt, ct)) = make_double2(o0, o1);
+          }
+          __stcs(reinterpret_cast<double2*>(rowp + ct), make_double2(o0, o1));
+          if (mirror) {
+            __stcs(a.Out + (size_t)(j0 + ct) * a.ldo + li, o0);
+            __stcs(a.Out + (size_t)(j0 + ct + 1) * a.ldo + li, o1);
+          }
+        }
+      }
+    if (PFPG) {
+      s0 += wgt * ts0;
+    } else {
+      s0 += wgt * 0.25 * ts0;
+      s1 += wgt * ts1;
+    }
+  } else {
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -358,10 +467,8 @@ __global__ void __launch_bounds__(kRbThreads, 2) rebuild_kernel(const RbArgs a) 
             o[c] = znew;
           }
         }
-        if (!PFPG && a.A8) {
-          Tz[rt * 65 + ct] = o[0];
-          Tz[rt * 65 + ct + 1] = two ? o[1] : 0.0;
-        }
+        if (!PFPG && a.A8)
+          *reinterpret_cast<double2*>(Tz + tz4(rt, ct)) = make_double2(o[0], two ? o[1] : 0.0);
         double* op = a.Out + (size_t)li * a.ldo + j;
         if (two && ((reinterpret_cast<uintptr_t>(op) & 15) == 0)) {
           __stcs(reinterpret_cast<double2*>(op), make_double2(o[0], o[1]));
@@ -377,17 +484,17 @@ __global__ void __launch_bounds__(kRbThreads, 2) rebuild_kernel(const RbArgs a) 
         }
       }
     }
+  }
 
     pv_i0 = i0;  // digit slices of this tile: written after the next tile's barrier
     pv_j0 = j0;
     pv_mirror = mirror;
-    pv_eI = eI;
-    pv_eJ = eJ;
+    pv_full = full;
   }  // tile loop
   if (!PFPG && a.A8 && pv_i0 >= 0) {
     __syncthreads();
-    if (a.S == 7) rb_digits<7>(a, Tz, pv_i0, pv_j0, pv_mirror, tid, pv_eI, pv_eJ);
-    else rb_digits<6>(a, Tz, pv_i0, pv_j0, pv_mirror, tid, pv_eI, pv_eJ);
+    if (a.S == 7) rb_digits_any<7>(a, Tz, pv_i0, pv_j0, pv_mirror, tid, Eg, pv_full);
+    else rb_digits_any<6>(a, Tz, pv_i0, pv_j0, pv_mirror, tid, Eg, pv_full);
   }
 
   // ---- deterministic reduction: block tree, then the last CTA sums CTA partials in order
@@ -437,13 +544,14 @@ static cudaError_t rb_launch(RbArgs a, cudaStream_t st) {
   a.rpad = PFPG ? ((a.r + 3) / 4) * 4 : 0;
   const int ldw_s = a.rpad + 4;
   const size_t panels = (size_t)2 * kRb * C::LD * 8 + (PFPG ? (size_t)2 * kRb * ldw_s * 8 : 0) +
-                        ((!PFPG && a.A8) ? (size_t)kRb * 65 * 8 : 0);
+                        ((!PFPG && a.A8) ? (size_t)(kRb / 4) * (kRb / 4) * kTzBlk * 8 : 0);
   const size_t stage = (size_t)kRb * C::LDS * 8;
   const size_t smem = std::max(panels, stage);
   static bool attr = false;
   if (!attr) {
     const size_t mx = std::max((size_t)2 * kRb * C::LD * 8 +
-                                   (PFPG ? (size_t)2 * kRb * 68 * 8 : (size_t)kRb * 65 * 8), stage);
+                                   (PFPG ? (size_t)2 * kRb * 68 * 8
+                                         : (size_t)(kRb / 4) * (kRb / 4) * kTzBlk * 8), stage);
     cudaFuncSetAttribute(rebuild_kernel<P, PFPG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)mx);
     attr = true;
@@ -506,7 +614,7 @@ cudaError_t prox_launch(const double* V, int64_t ldv, const double* Vloc, int64_
   RbArgs a{V, ldv, vf, f, tau, omega, ldo, W, ldw, r, 0,
            (r > 0 && (ldw & 1) == 0 && (reinterpret_cast<uintptr_t>(W) & 15) == 0) ? 1 : 0,
            nullptr, Aout, lda, n_rows, n, row0,
-           0, 0, 0, partials, counter, obj, nullptr, 0, nullptr, 0};
+           0, 0, 0, partials, counter, obj, nullptr, 0, nullptr, 0, nullptr};
   return rb_dispatch<true>(p, a, st);
 }
 
@@ -516,7 +624,11 @@ cudaError_t prox_launch(const double* V, int64_t ldv, const double* Vloc, int64_
 // max_j |Z_new_ij| <= B_i = max(sqrt(a_i) w_max + |t|/4, |1 - W_ii + Z_ii|).  Margins: the update's
 // own W_ij is a DMMA sum, within p u a_i of these (p <= 512: relative 1e-12 on the off-diagonal
 // term, absolute 1e-13 (a_i + 1 + |Z_ii|) on the diagonal one).  E_i = the digit-scale exponent
-// of B_i: every |Z_new_ij| < 2^E_i, as the digit expansion requires.
+// of B_i: every |Z_new_ij| < 2^E_i, as the digit expansion requires.  The fused digits use the
+// single exponent Eg = max_i E_i (one scale for the matrix: the mirror tile's digits are then the
+// byte transpose of the tile's, DESIGN.md §4 "fused digits"); a row whose own bound is below
+// 2^Eg loses Eg - E_i bits of the 49-bit expansion (measured spread on the config-3 iterates:
+// <= 3 bits).
 __global__ void pfam_bound1_kernel(const double* __restrict__ VF, const double* __restrict__ V,
                                    int64_t ldv, int n, int p, double2* __restrict__ wa,
                                    unsigned long long* wmax) {
@@ -542,17 +654,20 @@ __global__ void pfam_bound1_kernel(const double* __restrict__ VF, const double* 
 __global__ void pfam_bound2_kernel(const double2* __restrict__ wa,
                                    const unsigned long long* __restrict__ wmax,
                                    const double* __restrict__ Z, int64_t ldz, int n, double t,
-                                   int* __restrict__ E, double* __restrict__ rscale) {
+                                   int* __restrict__ Eg) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const double wm = __longlong_as_double((long long)*wmax);
-  const double2 w = wa[i];
-  const double zii = Z[(size_t)i * ldz + i];
-  const double off = (sqrt(w.y) * wm + 0.25 * fabs(t)) * (1.0 + 1e-12);
-  const double dg = fabs(1.0 - w.x + zii) + 1e-13 * (w.y + 1.0 + fabs(zii));
-  const int e = i8::scale_exp(fmax(off, dg));
-  E[i] = e;
-  rscale[i] = i8::pow2(e);
+  int e = INT_MIN;
+  if (i < n) {
+    const double wm = __longlong_as_double((long long)*wmax);
+    const double2 w = wa[i];
+    const double zii = Z[(size_t)i * ldz + i];
+    const double off = (sqrt(w.y) * wm + 0.25 * fabs(t)) * (1.0 + 1e-12);
+    const double dg = fabs(1.0 - w.x + zii) + 1e-13 * (w.y + 1.0 + fabs(zii));
+    e = i8::scale_exp(fmax(off, dg));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) e = max(e, __shfl_xor_sync(0xffffffffu, e, o));
+  if ((threadIdx.x & 31) == 0 && e != INT_MIN) atomicMax(Eg, e);
 }
 
 cudaError_t admm_launch(const double* V, int64_t ldv, const double* Vloc, int64_t ldvl,
@@ -563,19 +678,21 @@ cudaError_t admm_launch(const double* V, int64_t ldv, const double* Vloc, int64_
   cudaError_t e = scale_cols(Vloc, ldvl, f, n_rows, p, vf, st);
   if (e != cudaSuccess) return e;
   RbArgs a{V, ldv, vf, f, t, adj, ldadj, nullptr, 0, 0, 0, 0, deg, Z, ldz, n_rows, n, row0,
-           0, 0, raw, partials, counter, obj, nullptr, 0, nullptr, 0};
+           0, 0, raw, partials, counter, obj, nullptr, 0, nullptr, 0, nullptr};
   if (dig && dig->A8 && row0 == 0 && n_rows == n) {
     e = cudaMemsetAsync(dig->wmax, 0, 8, st);
     if (e != cudaSuccess) return e;
     count_launch();
     pfam_bound1_kernel<<<(n + 7) / 8, 256, 0, st>>>(vf, Vloc, ldvl, n, p, dig->wa, dig->wmax);
+    e = cudaMemsetAsync(dig->E, 0x80, sizeof(int), st);  // INT_MIN-ish start for atomicMax
+    if (e != cudaSuccess) return e;
     count_launch();
-    pfam_bound2_kernel<<<(n + 255) / 256, 256, 0, st>>>(dig->wa, dig->wmax, Z, ldz, n, t,
-                                                        dig->E, dig->rscale);
+    pfam_bound2_kernel<<<(n + 255) / 256, 256, 0, st>>>(dig->wa, dig->wmax, Z, ldz, n, t, dig->E);
     a.A8 = dig->A8;
     a.KB = dig->KB;
     a.E = dig->E;
     a.S = dig->S;
+    a.rscale = dig->rscale;
   }
   return rb_dispatch<false>(p, a, st);
 }
