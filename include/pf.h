@@ -70,6 +70,7 @@ typedef enum {
 #define PF_FLAG_SATURATED 0x8u       /* rank == p after the spectral operator */
 #define PF_FLAG_JACOBI_MAXSWEEP 0x10u /* Jacobi hit its sweep limit before the tolerance */
 #define PF_FLAG_LANCZOS_BREAK 0x20u  /* Lanczos stopped early (invariant subspace found) */
+#define PF_FLAG_NS_FALLBACK 0x40u    /* pf_rr_ns: Newton-Schulz did not converge; Jacobi used */
 
 /* ---------------------------------------------------------------------------- lifetime */
 /* Create a single-GPU context for order-n problems with block width p and Chebyshev degree
@@ -298,10 +299,13 @@ pf_status pf_matmul(pf_ctx ctx, const double* A, int64_t lda, const double* Y, i
  * F = f(H) (p x p row-major fp64, device) through Newton-Schulz matrix sign iterations
  * (PSD: f(H) = (H + H sign(H)) / 2; soft threshold thr: f(H) = H + ((H - thr I) sign(H - thr I)
  * - (H + thr I) sign(H + thr I)) / 2) and *rank = #{f != 0} (device int) from traces, so
- * X = U F U^T.  *iters (host, may be NULL) = sign iterations used.  Synchronises the stream
- * (convergence checks) and creates a p x p workspace + cuBLAS handle on its first call.
- * PF_ERR_BREAKDOWN when an eigenvalue sits so close to the threshold that 100 iterations do not
- * converge: use pf_rayleigh_ritz + pf_spectral_op for that iteration. */
+ * X = U F U^T.  The whole iteration runs in one cooperative kernel (hand-written fp64 DMMA
+ * products, device-side convergence test ||X^2 - I||_F <= 1e-12 sqrt(p), at most 100 steps): no
+ * host synchronisation, capturable in a CUDA graph.  If a sign does not converge (an eigenvalue
+ * at the threshold) the same call falls back on the device to the Jacobi eigensolver
+ * (F = Y diag(f(theta)) Y^T) and sets PF_FLAG_NS_FALLBACK.  iters: DEVICE int (may be NULL) =
+ * sign iterations used, -1 after a fallback.  Scratch (7 p^2 doubles) is allocated on the first
+ * call of a context. */
 pf_status pf_rr_ns(pf_ctx ctx, const void* A, int64_t lda, const void* U, int64_t ldu, pf_op op,
                    double thr, double* F, int32_t* rank, int32_t* iters, pf_stream stream);
 

@@ -19,7 +19,7 @@ PF_OP_SOFT_THRESHOLD = 1
 STATUS = {0: "PF_OK", 1: "PF_ERR_ARG", 2: "PF_ERR_DIM", 3: "PF_ERR_INTERVAL", 4: "PF_ERR_CUDA",
           5: "PF_ERR_NOMEM", 6: "PF_ERR_NCCL", 7: "PF_ERR_UNSUPPORTED", 8: "PF_ERR_BREAKDOWN"}
 FLAGS = {0x1: "CHOL_SHIFT", 0x2: "NONFINITE", 0x4: "DEGENERATE_INTERVAL", 0x8: "SATURATED",
-         0x10: "JACOBI_MAXSWEEP", 0x20: "LANCZOS_BREAK"}
+         0x10: "JACOBI_MAXSWEEP", 0x20: "LANCZOS_BREAK", 0x40: "NS_FALLBACK"}
 
 _lib = None
 
@@ -67,7 +67,7 @@ def load() -> ctypes.CDLL:
         "pf_invalidate": [P],
         "pf_matmul": [P, P, I64, P, I64, P, I64, P],
         "pf_spmm": [P, P, P, P, P, P, I64, D, D, D, P, I64, P, I64, P, I64, P],
-        "pf_rr_ns": [P, P, I64, P, I64, I32, D, P, P, ctypes.POINTER(I32), P],
+        "pf_rr_ns": [P, P, I64, P, I64, I32, D, P, P, P, P],
         "pf_svt_ritz": [P, P, P, P, P, I64, D, P, I64, P, I64, P, P, P, P],
         "pf_svt_update": [P, P, P, P, P, P, I64, P, I64, P, D, P, P],
         "pf_profile": [P, I32],
@@ -320,15 +320,12 @@ class Context:
         self._check(self.lib.pf_matmul(self.h, _ptr(A), _ld(A), _ptr(Y), _ld(Y), _ptr(out),
                                        _ld(out), _stream(stream)), "pf_matmul")
 
-    def rr_ns(self, A, U, op, thr, F, rank, stream=None) -> int:
-        """F = f(U^T A U) by Newton-Schulz (pf_rr_ns); returns the sign iterations used.
-        Raises PFError (PF_ERR_BREAKDOWN) when it does not converge."""
-        it = ctypes.c_int32(0)
-        ldu = _ld(U)
-        self._check(self.lib.pf_rr_ns(self.h, _ptr(A), _ld(A), _ptr(U), ldu, int(op), float(thr),
-                                      _ptr(F), _ptr(rank), ctypes.byref(it), _stream(stream)),
-                    "pf_rr_ns")
-        return int(it.value)
+    def rr_ns(self, A, U, op, thr, F, rank, iters=None, stream=None):
+        """F = f(U^T A U) by Newton-Schulz in one device-side kernel (pf_rr_ns); iters: optional
+        device int32 tensor <- sign iterations used (-1 after the device-side Jacobi fallback)."""
+        self._check(self.lib.pf_rr_ns(self.h, _ptr(A), _ld(A), _ptr(U), _ld(U), int(op),
+                                      float(thr), _ptr(F), _ptr(rank), _ptr(iters),
+                                      _stream(stream)), "pf_rr_ns")
 
     # ---- PFSVT (NEXT-3): sparse operators in compressed-row form (torch int32 / fp64 tensors)
     def spmm(self, ptr, idx, val, X, out, coef=(1.0, 0.0, 0.0), ycur=None, yprev=None,

@@ -60,7 +60,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
     if failed:
         raise RuntimeError("nvcc failed building libpf.so")
     cmd = [nvcc, *ARCH, "-shared", "-o", OUT, *objs, f"-L{nccl}/lib", "-l:libnccl.so.2",
-           f"-Xlinker=-rpath={nccl}/lib", "-lcublas"]
+           f"-Xlinker=-rpath={nccl}/lib"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

@@ -86,6 +86,7 @@ struct pf_ctx_s {
   double* jac_V = nullptr;                     // p x p
   double* jac_red = nullptr;
   int* jac_cnt = nullptr;
+  double* jac_theta = nullptr;                 // p (Newton-Schulz fallback)
   float* tf_ws = nullptr;
   float* tf_acc = nullptr;
   int* tf_cnt = nullptr;
@@ -213,10 +214,6 @@ static pf_status alloc_all(pf_ctx ctx) {
     ok &= A((void**)&ctx->g32_part, (size_t)ctx->g32_slices * p * p * 8);
     ok &= A((void**)&ctx->chol_W, (size_t)p * p * 8);
     ok &= A((void**)&ctx->chol_D, (size_t)p * 32 * 8);
-    ok &= A((void**)&ctx->jac_H, (size_t)2 * p * p * 8);
-    ok &= A((void**)&ctx->jac_V, (size_t)p * p * 8);
-    ok &= A((void**)&ctx->jac_red, (size_t)2 * jacobi_big_grid() * 8);
-    ok &= A((void**)&ctx->jac_cnt, 16);
     ok &= A((void**)&ctx->tf_ws, ctx->tplan.ws_floats * 4);
     ok &= A((void**)&ctx->tf_acc, ctx->tplan.acc_floats * 4);
     ok &= A((void**)&ctx->tf_cnt, ctx->tplan.counters * 4);
@@ -250,6 +247,12 @@ static pf_status alloc_all(pf_ctx ctx) {
     ok &= A((void**)&ctx->lz_qfull, (size_t)n * 8);
   }
   ok &= A((void**)&ctx->G, (size_t)p * p * 8);
+  // cooperative Jacobi scratch (TF32 Rayleigh-Ritz; the Newton-Schulz fallback on every dtype)
+  ok &= A((void**)&ctx->jac_H, (size_t)2 * p * p * 8);
+  ok &= A((void**)&ctx->jac_V, (size_t)p * p * 8);
+  ok &= A((void**)&ctx->jac_red, (size_t)2 * jacobi_big_grid() * 8);
+  ok &= A((void**)&ctx->jac_cnt, 16);
+  ok &= A((void**)&ctx->jac_theta, (size_t)p * 8);
   ok &= A((void**)&ctx->Rinv, (size_t)p * p * 8);
   ok &= A((void**)&ctx->Yeig, (size_t)p * p * 8);
   if (!f32) {
@@ -469,7 +472,7 @@ pf_status pf_destroy(pf_ctx ctx) {
                   ctx->jac_cnt, ctx->tf_ws,   ctx->tf_cnt,    ctx->tf_acc,  ctx->Yfull32,
                   ctx->A8,     ctx->a8_rscale, ctx->Y8,       ctx->y8_cscale, ctx->y8_cmax,
                   ctx->i8_acc, ctx->i8_part, ctx->i8_cnt, ctx->svt_part, ctx->svt_cnt,
-                  ctx->lz_sym_ws, ctx->a8_E, ctx->a8_wa, ctx->a8_wmax};
+                  ctx->lz_sym_ws, ctx->a8_E, ctx->a8_wa, ctx->a8_wmax, ctx->jac_theta};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete ctx;
@@ -1192,19 +1195,25 @@ pf_status pf_rr_ns(pf_ctx ctx, const void* Av, int64_t lda, const void* Uv, int6
   if (!ctx->ns) {
     ctx->ns = ns_create(p);
     if (!ctx->ns) {
-      snprintf(ctx->err, sizeof(ctx->err), "pf_rr_ns: workspace / cuBLAS handle creation failed");
+      snprintf(ctx->err, sizeof(ctx->err), "pf_rr_ns: workspace allocation failed");
       return PF_ERR_NOMEM;
     }
   }
-  int it = 0;
-  const int r = ns_spectral(ctx->ns, ctx->G, op == PF_OP_SOFT_THRESHOLD ? 1 : 0, thr, F, rank,
-                            &it, st);
-  if (iters) *iters = it;
+  const int soft = op == PF_OP_SOFT_THRESHOLD ? 1 : 0;
+  PF_CU(ns_spectral(ctx->ns, ctx->G, soft, thr, F, rank, iters, ctx->state, st));
+  // device-side fallback (no host decision): Jacobi on the same H, then F = Y f(theta) Y^T;
+  // both launches return at once unless the Newton-Schulz kernel raised its fail flag
+  const int* fail = ns_fail_flag(ctx->ns);
+  if (p <= 128)  // single-CTA Jacobi (the cooperative one needs p >= 64 pairs of lanes)
+    PF_CU(jacobi_launch(ctx->G, p, nullptr, ctx->jac_theta, ctx->Yeig, ctx->state,
+                        std::max(1e-15, 1e-16 * p), 40, st, fail));
+  else
+    PF_CU(jacobi_big_launch(ctx->G, p, ctx->jac_theta, ctx->Yeig, ctx->jac_H, ctx->jac_V,
+                            ctx->jac_red, ctx->jac_cnt, ctx->state, 1e-13, 40, nullptr, st, fail));
+  PF_CU(ns_fallback_launch(fail, soft, thr, ctx->jac_theta, ctx->Yeig, p, F, rank, st));
   // no Ritz values: the next re-base plan falls back to the Lanczos spread estimate
   PF_CU(cudaMemsetAsync(&ctx->state->have_theta, 0, sizeof(int), st));
   ctx->filtered = false;
-  if (r == -1) return PF_ERR_BREAKDOWN;
-  if (r < 0) return cuda_fail(ctx, cudaGetLastError(), "pf_rr_ns (cuBLAS)");
   return PF_OK;
 }
 

@@ -600,7 +600,8 @@ __device__ __forceinline__ void jb_decode(int e, int half, int& a, int& b) {
 __global__ void __launch_bounds__(JB_THREADS) jacobi_big_kernel(
     const double* __restrict__ Hin, int p, double* __restrict__ theta, double* __restrict__ Yout,
     double* H0, double* Vt_, double* red_ws, int* cnt_ws, DevState* state, double tol,
-    int max_sweeps, const double* damped) {
+    int max_sweeps, const double* damped, const int* cond) {
+  if (cond && *cond == 0) return;  // conditional launch (uniform over the grid)
   cg::grid_group grid = cg::this_grid();
   __shared__ double csv[3 * 256];
   __shared__ int pii[256], pjj[256];
@@ -793,10 +794,12 @@ int jacobi_big_grid() {
 // Hw: 2 p^2 doubles, Vw: p^2, red_ws: 2 * jacobi_big_grid() doubles, cnt_ws: 4 ints
 cudaError_t jacobi_big_launch(const double* H, int p, double* theta, double* Y, double* Hw,
                               double* Vw, double* red_ws, int* cnt_ws, DevState* state, double tol,
-                              int max_sweeps, const double* damped, cudaStream_t st) {
+                              int max_sweeps, const double* damped, cudaStream_t st,
+                              const int* cond) {
   void* args[] = {(void*)&H,      (void*)&p,     (void*)&theta,  (void*)&Y,
                   (void*)&Hw,     (void*)&Vw,    (void*)&red_ws, (void*)&cnt_ws,
-                  (void*)&state,  (void*)&tol,   (void*)&max_sweeps, (void*)&damped};
+                  (void*)&state,  (void*)&tol,   (void*)&max_sweeps, (void*)&damped,
+                  (void*)&cond};
   count_launch();
   return cudaLaunchCooperativeKernel((const void*)jacobi_big_kernel, dim3(jacobi_big_grid()),
                                      dim3(JB_THREADS), args, 0, st);

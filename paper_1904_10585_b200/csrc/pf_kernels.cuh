@@ -90,9 +90,14 @@ cudaError_t i8_gemm_launch(const I8Plan& pl, const CUtensorMap& mapA8, const CUt
 struct NsWork;
 NsWork* ns_create(int p);
 void ns_destroy(NsWork* w);
-// 0 ok, -1 not converged (fall back to Jacobi), -2 cuBLAS / CUDA failure; synchronises `st`
-int ns_spectral(NsWork* w, const double* H, int op_soft, double thr, double* F, int* rank,
-                int* iters, cudaStream_t st);
+// F = f(H) by Newton-Schulz sign iterations in one cooperative kernel (pf_ns.cu); on
+// non-convergence the fail flag (ns_fail_flag) is set and F is left for the Jacobi fallback
+cudaError_t ns_spectral(NsWork* w, const double* H, int op_soft, double thr, double* F, int* rank,
+                        int* iters_dev, DevState* state, cudaStream_t st);
+const int* ns_fail_flag(const NsWork* w);
+// if *fail: f(theta), F = Y diag(f) Y^T, rank (Y, theta from a Jacobi solve)
+cudaError_t ns_fallback_launch(const int* fail, int op_soft, double thr, const double* theta,
+                               const double* Y, int p, double* F, int* rank, cudaStream_t st);
 
 // ---- PFSVT sparse kernels (pf_svt.cu): S n x n in compressed-row form (CSR, or the CSC view)
 cudaError_t svt_kick_launch(double* x, const double* b, double alpha, int64_t nnz,
@@ -129,7 +134,8 @@ int jacobi_big_grid();
 // (a, b) are not rotated (their eigenpairs have f = 0)
 cudaError_t jacobi_big_launch(const double* H, int p, double* theta, double* Y, double* Hw,
                               double* Vw, double* red_ws, int* cnt_ws, DevState* state, double tol,
-                              int max_sweeps, const double* damped, cudaStream_t st);
+                              int max_sweeps, const double* damped, cudaStream_t st,
+                              const int* cond = nullptr);
 cudaError_t perturb_hash32_launch(float* A, int64_t lda, int rows, int cols, int row0,
                                   unsigned long long seed, int k, double noise, cudaStream_t st);
 // Lanczos GEMV on an fp32 iterate (fp64 accumulation), same contract as lz_gemv_launch
@@ -157,7 +163,8 @@ cudaError_t rmul_launch(const double* in, int64_t ldi, const double* R, double* 
                         int n_rows, int p, const int* cond, cudaStream_t st);
 // two-sided parallel cyclic Jacobi: H (p x p symmetric, only read) -> theta desc, Y (p x p)
 cudaError_t jacobi_launch(const double* H, int p, const int* p_dev, double* theta, double* Y,
-                          DevState* state, double tol, int max_sweeps, cudaStream_t st);
+                          DevState* state, double tol, int max_sweeps, cudaStream_t st,
+                          const int* cond = nullptr);
 cudaError_t spectral_launch(int op, double thr, const double* theta, int p, double* f,
                             int* rank, DevState* state, cudaStream_t st);
 // plan kernel: interval -> per-step coefficients + re-base flags

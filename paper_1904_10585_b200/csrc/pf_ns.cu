@@ -10,120 +10,268 @@
 //                                          S+ = sign(H - theta I), S- = sign(H + theta I)
 // and rank = #{f != 0} = tr(I + S+)/2 + tr(I - S-)/2 (PSD: tr(I + S)/2).  sign(M) by the
 // Newton-Schulz iteration X <- X (3 I - X^2) / 2 from X_0 = M / ||M||_inf (all eigenvalues in
-// [-1, 1]), stopped when ||X^2 - I||_F <= tol; each step is two p x p fp64 GEMMs (cuBLAS DGEMM:
-// plain library GEMMs) and one elementwise kernel.  The iteration count grows like
-// log(||M|| / min |lambda(M)|): eigenvalues close to the threshold are slow, so the host loop
-// caps it and the caller falls back to Jacobi (PF_ERR_BREAKDOWN) when it does not converge.
-#include <cublas_v2.h>
+// [-1, 1]), stopped when ||X^2 - I||_F <= tol.
+//
+// B200 design: ONE cooperative kernel runs the whole iteration on the device (no host sync, so
+// a Rayleigh-Ritz step can be captured in a CUDA graph).  Every iterate is a polynomial in the
+// symmetric M, so it is kept EXACTLY symmetric: each product is formed on the upper 32 x 32 tiles
+// only (fp64 DMMA, both operands row panels: C = A B^T) and mirrored, which also halves the work.
+// For the soft threshold the two signs iterate side by side (two halves of the grid).  Per step:
+// T = X X^T with the residual ||T - I||_F^2 as per-CTA partials, grid barrier, every CTA sums the
+// partials in the same order (a uniform convergence decision), X <- X (3 I - T) / 2, barrier.
+// A sign that has not converged after max_it steps sets the fail flag; the caller then runs the
+// cooperative Jacobi eigensolver on the same H (a conditional launch: no host decision).
+#include <cooperative_groups.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 
+#include "../../include/pf.h"
 #include "pf_kernels.cuh"
 
 namespace pf {
+namespace cg = cooperative_groups;
 
-// X = (H - shift I), and the max absolute row sum of it into *nrm (one block per 32 rows)
-__global__ void ns_shift_kernel(const double* __restrict__ H, int p, double shift,
-                                double* __restrict__ X, unsigned long long* nrm_bits) {
-  const int r = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (r >= p) return;
-  double s = 0.0;
-  for (int c = lane; c < p; c += 32) {
-    const double v = H[(size_t)r * p + c] - (r == c ? shift : 0.0);
-    X[(size_t)r * p + c] = v;
-    s += fabs(v);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) atomicMax(nrm_bits, (unsigned long long)__double_as_longlong(s));
-}
-
-__global__ void ns_scale_kernel(double* __restrict__ X, int n, const unsigned long long* nrm_bits) {
-  const double nrm = __longlong_as_double((long long)*nrm_bits);
-  const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    X[i] *= inv;
-}
-
-// T <- 3 I - T (T = X^2), and res = ||X^2 - I||_F^2 (fixed-order: per-block partials, last block)
-__global__ void ns_prep_kernel(double* __restrict__ T, int p, double* __restrict__ part,
-                               int* counter, double* res) {
-  __shared__ double red[32];
-  __shared__ bool last;
-  double s = 0.0;
-  const int n = p * p;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const bool diag = (i / p) == (i % p);
-    const double t = T[i];
-    const double d = t - (diag ? 1.0 : 0.0);
-    s += d * d;
-    T[i] = (diag ? 3.0 : 0.0) - t;
-  }
-  s = block_sum(s, red);
-  if (threadIdx.x == 0) {
-    part[blockIdx.x] = s;
-    __threadfence();
-    last = (atomicAdd(counter, 1) == (int)gridDim.x - 1);
-  }
-  __syncthreads();
-  if (last && threadIdx.x == 0) {
-    __threadfence();
-    double t = 0.0;
-    for (int b = 0; b < (int)gridDim.x; ++b) t += __ldcg(part + b);
-    *res = t;
-    *counter = 0;
-  }
-}
-
-// rank = #{f != 0} from the traces of the sign matrices
-__global__ void ns_rank_kernel(int p, const double* __restrict__ Sp, const double* __restrict__ Sm,
-                               int soft, int* rank) {
-  __shared__ double red[32];
-  double tr = 0.0;
-  for (int i = threadIdx.x; i < p; i += blockDim.x)
-    tr += soft ? 0.5 * (1.0 + Sp[(size_t)i * p + i]) + 0.5 * (1.0 - Sm[(size_t)i * p + i])
-               : 0.5 * (1.0 + Sp[(size_t)i * p + i]);
-  tr = block_sum(tr, red);
-  if (threadIdx.x == 0) *rank = (int)llrint(tr);
-}
-
-// F <- (F + F^T) / 2: one thread per element pair i < j (grid-wide)
-__global__ void ns_symmetrize_kernel(double* __restrict__ F, int p) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= p * p) return;
-  const int i = e / p, j = e - i * p;
-  if (i < j) {
-    const double v = 0.5 * (F[(size_t)i * p + j] + F[(size_t)j * p + i]);
-    F[(size_t)i * p + j] = v;
-    F[(size_t)j * p + i] = v;
-  }
-}
+constexpr int kNsT = 32;         // tile edge
+constexpr int kNsK = 32;         // K chunk (doubles)
+constexpr int kNsLd = kNsK + 4;  // smem row pitch
+constexpr int kNsThreads = 128;  // 4 warps, warp tile 16 x 16
 
 struct NsWork {
-  cublasHandle_t h = nullptr;
-  double *X = nullptr, *T = nullptr, *Y = nullptr, *Sp = nullptr, *Sm = nullptr, *M = nullptr;
-  double* part = nullptr;
-  int* cnt = nullptr;
-  double* res = nullptr;                 // device
-  unsigned long long* nrm = nullptr;     // device
-  double* res_host = nullptr;            // pinned
-  int p = 0;
-  int last_it[2] = {0, 0};               // iterations the previous call's signs needed
+  int p = 0, tt = 0, nup = 0;  // tiles per dimension, upper tiles (I <= J)
+  double* buf = nullptr;       // per sign: 3 rotating p x p buffers; shared: Hs (p x p)
+  double* part = nullptr;      // per CTA residual partials
+  int* ctrl = nullptr;         // [0] fail, [1] iterations, [2..3] final buffer per sign
+  unsigned long long* nrm = nullptr;  // per sign ||M||_inf bits
 };
+
+struct NsArgs {
+  const double* H;
+  int p, tt, nup, nsign, max_it;
+  double shift[2];  // M_s = Hs - shift[s] I
+  double tol;
+  int soft;
+  double* Hs;
+  double* X[2][3];  // per sign: three rotating p x p buffers
+  double* F;
+  int* rank;
+  double* part;
+  int* ctrl;
+  unsigned long long* nrm;
+  int* iters_out;  // device, may be NULL
+  DevState* state;
+};
+
+__device__ __forceinline__ void ns_cp16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem)
+               : "memory");
+}
+
+// upper tile e (0 <= e < tt (tt + 1) / 2) -> (I, J), I <= J, row-major over the upper triangle
+__device__ __forceinline__ void ns_tile(int e, int tt, int& I, int& J) {
+  int i = 0;
+  while ((i + 1) * tt - (i + 1) * i / 2 <= e) ++i;
+  I = i;
+  J = i + (e - (i * tt - i * (i - 1) / 2));
+}
+
+// acc (warp tile 16 x 16 at (wr, wc) inside the 32 x 32 tile) = A[rows I] B[rows J]^T over K = p
+// (row-major p x p operands, rows / columns >= p read as 0)
+__device__ __forceinline__ void ns_tile_mma(const double* __restrict__ A, const double* __restrict__ B,
+                                            int p, int I, int J, double* sm, double (&acc)[2][4]) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+  const int wr = (warp & 1) * 16, wc = (warp >> 1) * 16;
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc[nt][k] = 0.0;
+  const int nchunk = (p + kNsK - 1) / kNsK;
+  auto stage = [&](int c, int buf) {
+    double* sa = sm + buf * 2 * kNsT * kNsLd;
+    double* sb = sa + kNsT * kNsLd;
+    const int k0 = c * kNsK;
+    // 32 rows x 32 doubles per operand = 512 16-byte pieces, 4 per thread and operand
+    for (int e = tid; e < kNsT * (kNsK / 2); e += kNsThreads) {
+      const int r = e / (kNsK / 2), k = (e % (kNsK / 2)) * 2;
+      const int ra = I * kNsT + r, rb = J * kNsT + r, kk = k0 + k;
+      if (ra < p && kk < p) ns_cp16(sa + r * kNsLd + k, A + (size_t)ra * p + kk);
+      else *reinterpret_cast<double2*>(sa + r * kNsLd + k) = make_double2(0.0, 0.0);
+      if (rb < p && kk < p) ns_cp16(sb + r * kNsLd + k, B + (size_t)rb * p + kk);
+      else *reinterpret_cast<double2*>(sb + r * kNsLd + k) = make_double2(0.0, 0.0);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  stage(0, 0);
+  for (int c = 0; c < nchunk; ++c) {
+    if (c + 1 < nchunk) {
+      stage(c + 1, (c + 1) & 1);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();
+    const double* sa = sm + (c & 1) * 2 * kNsT * kNsLd + (wr + g) * kNsLd + t;
+    const double* sb = sm + (c & 1) * 2 * kNsT * kNsLd + kNsT * kNsLd + (wc + g) * kNsLd + t;
+#pragma unroll
+    for (int ks = 0; ks < kNsK / 4; ++ks) {
+      const double a0 = sa[ks * 4], a1 = sa[8 * kNsLd + ks * 4];
+      const double b0 = sb[ks * 4], b1 = sb[8 * kNsLd + ks * 4];
+      dmma16884(acc[0], a0, a1, b0);
+      dmma16884(acc[1], a0, a1, b1);
+    }
+    __syncthreads();  // the buffer is refilled two chunks later
+  }
+}
+
+// store the warp tile of C (tile (I, J), upper) and its mirror; value(i, j, acc) transforms
+template <typename Fn>
+__device__ __forceinline__ void ns_store(double* __restrict__ C, int p, int I, int J,
+                                         const double (&acc)[2][4], Fn value) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+  const int wr = (warp & 1) * 16, wc = (warp >> 1) * 16;
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int i = I * kNsT + wr + g + 8 * h, j = J * kNsT + wc + nt * 8 + 2 * t + c;
+        if (i < p && j < p && (I < J || i <= j)) {
+          const double v = value(i, j, acc[nt][2 * h + c]);
+          C[(size_t)i * p + j] = v;
+          C[(size_t)j * p + i] = v;
+        }
+      }
+}
+
+__global__ void __launch_bounds__(kNsThreads) ns_kernel(const NsArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double red[32];
+  const int p = a.p, tid = threadIdx.x;
+  const int sg = blockIdx.x / a.nup, e = blockIdx.x % a.nup;
+  int I, J;
+  ns_tile(e, a.tt, I, J);
+  const int gtid = blockIdx.x * kNsThreads + tid, gthreads = gridDim.x * kNsThreads;
+  const int sthreads = a.nup * kNsThreads, stid = e * kNsThreads + tid;  // within the sign group
+  // ---- Hs = (H + H^T) / 2 and ||M_s||_inf per sign
+  if (gtid == 0) a.ctrl[0] = 0;
+  for (int x = gtid; x < p * p; x += gthreads) {
+    const int i = x / p, j = x - i * p;
+    a.Hs[x] = 0.5 * (a.H[(size_t)i * p + j] + a.H[(size_t)j * p + i]);
+  }
+  grid.sync();
+  for (int r = stid >> 5; r < p; r += sthreads >> 5) {  // a warp per row
+    double s = 0.0;
+    for (int c = tid & 31; c < p; c += 32) s += fabs(a.Hs[(size_t)r * p + c] - (r == c ? a.shift[sg] : 0.0));
+    s = warp_sum(s);
+    if ((tid & 31) == 0) atomicMax(a.nrm + sg, (unsigned long long)__double_as_longlong(s));
+  }
+  grid.sync();
+  {
+    const double nrm = __longlong_as_double((long long)a.nrm[sg]);
+    const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
+    for (int x = stid; x < p * p; x += sthreads) {
+      const int i = x / p, j = x - i * p;
+      a.X[sg][0][x] = (a.Hs[x] - (i == j ? a.shift[sg] : 0.0)) * inv;
+    }
+  }
+  grid.sync();
+  // ---- Newton-Schulz iterations.  Three buffers per sign rotate: X (current), T' = 3 I - X^2,
+  // the next X; every buffer is rewritten only after two grid barriers since its last reader.
+  int cur[2] = {0, 0};
+  bool conv[2] = {a.nsign < 1, a.nsign < 2};
+  int its[2] = {0, 0};
+  double acc[2][4];
+  for (int it = 0; it < a.max_it; ++it) {
+    if (!conv[sg]) {  // T = X X^T (= X^2: X is symmetric); T' = 3 I - T
+      const double* X = a.X[sg][cur[sg]];
+      double* T = a.X[sg][(cur[sg] + 1) % 3];
+      ns_tile_mma(X, X, p, I, J, sm, acc);
+      double r = 0.0;
+      ns_store(T, p, I, J, acc, [&](int i, int j, double v) {
+        const double d = v - (i == j ? 1.0 : 0.0);
+        r += (i == j ? 1.0 : 2.0) * d * d;
+        return (i == j ? 3.0 : 0.0) - v;
+      });
+      r = block_sum(r, red);
+      if (tid == 0) a.part[blockIdx.x] = r;
+    }
+    grid.sync();
+    // uniform convergence decision: every CTA sums each group's partials in the same order
+    bool all = true;
+    for (int s = 0; s < a.nsign; ++s) {
+      if (!conv[s]) {
+        double res = 0.0;
+        for (int q = 0; q < a.nup; ++q) res += __ldcg(a.part + s * a.nup + q);
+        if (sqrt(res) <= a.tol) {
+          conv[s] = true;  // the current X is the sign
+          its[s] = it;
+        }
+      }
+      all = all && conv[s];
+    }
+    if (all) break;
+    if (!conv[sg])  // X <- X T' / 2 (T' symmetric: row panels of both)
+      ns_tile_mma(a.X[sg][cur[sg]], a.X[sg][(cur[sg] + 1) % 3], p, I, J, sm, acc),
+          ns_store(a.X[sg][(cur[sg] + 2) % 3], p, I, J, acc, [](int, int, double v) { return 0.5 * v; });
+    grid.sync();
+    for (int s = 0; s < a.nsign; ++s)
+      if (!conv[s]) cur[s] = (cur[s] + 2) % 3;
+  }
+  bool ok = true;
+  for (int s = 0; s < a.nsign; ++s) ok = ok && conv[s];
+  if (!ok) {
+    if (gtid == 0) {
+      a.ctrl[0] = 1;  // fall back to the Jacobi eigensolver (conditional launches follow)
+      a.ctrl[1] = a.max_it * a.nsign;
+      if (a.iters_out) *a.iters_out = -1;
+      atomicOr(&a.state->flags, PF_FLAG_NS_FALLBACK);
+    }
+    return;
+  }
+  // ---- F: G_s = M_s S_s = Hs S_s - shift_s S_s (upper tiles + mirror; symmetric in exact
+  // arithmetic), into the free T' buffer; then F elementwise (exactly symmetric)
+  double* G[2] = {a.X[0][(cur[0] + 1) % 3], a.X[1][(cur[1] + 1) % 3]};
+  {
+    const double* S = a.X[sg][cur[sg]];
+    ns_tile_mma(a.Hs, S, p, I, J, sm, acc);
+    const double sh = a.shift[sg];
+    ns_store(G[sg], p, I, J, acc,
+             [&](int i, int j, double v) { return v - sh * S[(size_t)i * p + j]; });
+  }
+  grid.sync();
+  for (int x = gtid; x < p * p; x += gthreads) {
+    const double h = a.Hs[x];
+    a.F[x] = a.soft ? h + 0.5 * (G[0][x] - G[1][x]) : 0.5 * (h + G[0][x]);
+  }
+  if (blockIdx.x == 0) {
+    double tr = 0.0;
+    for (int i = tid; i < p; i += kNsThreads) {
+      const double sp = a.X[0][cur[0]][(size_t)i * p + i];
+      tr += a.soft ? 0.5 * (1.0 + sp) + 0.5 * (1.0 - a.X[1][cur[1]][(size_t)i * p + i])
+                   : 0.5 * (1.0 + sp);
+    }
+    tr = block_sum(tr, red);
+    if (tid == 0) {
+      *a.rank = (int)llrint(tr);
+      a.ctrl[1] = its[0] + its[1];
+      if (a.iters_out) *a.iters_out = its[0] + its[1];
+    }
+  }
+}
 
 NsWork* ns_create(int p) {
   NsWork* w = new NsWork();
   w->p = p;
+  w->tt = (p + kNsT - 1) / kNsT;
+  w->nup = w->tt * (w->tt + 1) / 2;
   const size_t mb = (size_t)p * p * 8;
-  bool ok = cublasCreate(&w->h) == CUBLAS_STATUS_SUCCESS;
-  ok = ok && cudaMalloc(&w->X, mb) == cudaSuccess && cudaMalloc(&w->T, mb) == cudaSuccess &&
-       cudaMalloc(&w->Y, mb) == cudaSuccess && cudaMalloc(&w->Sp, mb) == cudaSuccess &&
-       cudaMalloc(&w->Sm, mb) == cudaSuccess && cudaMalloc(&w->M, mb) == cudaSuccess &&
-       cudaMalloc(&w->part, 64 * 8) == cudaSuccess && cudaMalloc(&w->cnt, 16) == cudaSuccess &&
-       cudaMalloc(&w->res, 8) == cudaSuccess && cudaMalloc(&w->nrm, 8) == cudaSuccess &&
-       cudaMallocHost(&w->res_host, 8) == cudaSuccess &&
-       cudaMemset(w->cnt, 0, 16) == cudaSuccess;
+  bool ok = cudaMalloc(&w->buf, 7 * mb) == cudaSuccess &&
+            cudaMalloc(&w->part, (size_t)2 * w->nup * 8) == cudaSuccess &&
+            cudaMalloc(&w->ctrl, 16) == cudaSuccess && cudaMalloc(&w->nrm, 16) == cudaSuccess &&
+            cudaMemset(w->ctrl, 0, 16) == cudaSuccess;
   if (!ok) {
     ns_destroy(w);
     return nullptr;
@@ -133,96 +281,90 @@ NsWork* ns_create(int p) {
 
 void ns_destroy(NsWork* w) {
   if (!w) return;
-  if (w->h) cublasDestroy(w->h);
-  for (void* q : {(void*)w->X, (void*)w->T, (void*)w->Y, (void*)w->Sp, (void*)w->Sm, (void*)w->M,
-                  (void*)w->part, (void*)w->cnt, (void*)w->res, (void*)w->nrm})
+  for (void* q : {(void*)w->buf, (void*)w->part, (void*)w->ctrl, (void*)w->nrm})
     if (q) cudaFree(q);
-  if (w->res_host) cudaFreeHost(w->res_host);
   delete w;
 }
 
-// row-major C = alpha A B + beta C (p x p) with column-major cuBLAS: C^T = alpha B^T A^T + beta C^T
-static bool dgemm(NsWork* w, const double* A, const double* B, double* C, double alpha,
-                  double beta) {
+const int* ns_fail_flag(const NsWork* w) { return w->ctrl; }
+
+cudaError_t ns_spectral(NsWork* w, const double* H, int op_soft, double thr, double* F, int* rank,
+                        int* iters_dev, DevState* state, cudaStream_t st) {
   const int p = w->p;
-  return cublasDgemm(w->h, CUBLAS_OP_N, CUBLAS_OP_N, p, p, p, &alpha, B, p, A, p, &beta, C, p) ==
-         CUBLAS_STATUS_SUCCESS;
+  static int max_it = -1;
+  if (max_it < 0) {
+    const char* e = getenv("PF_NS_MAXIT");  // development / test knob
+    max_it = e ? atoi(e) : 100;
+  }
+  NsArgs a{};
+  a.H = H;
+  a.p = p;
+  a.tt = w->tt;
+  a.nup = w->nup;
+  a.nsign = op_soft ? 2 : 1;
+  a.max_it = max_it;
+  a.shift[0] = op_soft ? thr : 0.0;
+  a.shift[1] = -thr;
+  a.tol = 1e-12 * sqrt((double)p);
+  a.soft = op_soft;
+  const size_t pp = (size_t)p * p;
+  a.Hs = w->buf + 6 * pp;
+  for (int s = 0; s < 2; ++s)
+    for (int b = 0; b < 3; ++b) a.X[s][b] = w->buf + (3 * s + b) * pp;
+  a.F = F;
+  a.rank = rank;
+  a.part = w->part;
+  a.ctrl = w->ctrl;
+  a.nrm = w->nrm;
+  a.iters_out = iters_dev;
+  a.state = state;
+  cudaError_t e = cudaMemsetAsync(w->nrm, 0, 16, st);
+  if (e != cudaSuccess) return e;
+  const size_t smem = (size_t)2 * 2 * kNsT * kNsLd * 8;
+  static bool attr = false;
+  if (!attr) {
+    e = cudaFuncSetAttribute(ns_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  void* args[] = {(void*)&a};
+  count_launch();
+  return cudaLaunchCooperativeKernel((const void*)ns_kernel, dim3(a.nup * a.nsign),
+                                     dim3(kNsThreads), args, smem, st);
 }
 
-// S = sign(H - shift I); returns the iterations used, -1 if not converged within max_it
-static int ns_sign(NsWork* w, const double* H, double shift, double* S, int max_it, double tol,
-                   int slot, cudaStream_t st) {
-  const int p = w->p, n = p * p;
-  cudaMemsetAsync(w->nrm, 0, 8, st);
-  count_launch();
-  ns_shift_kernel<<<(p + 7) / 8, 256, 0, st>>>(H, p, shift, w->X, w->nrm);
-  count_launch();
-  ns_scale_kernel<<<64, 256, 0, st>>>(w->X, n, w->nrm);
-  double* X = w->X;
-  double* Xn = S;
-  for (int it = 1; it <= max_it; ++it) {
-    if (!dgemm(w, X, X, w->T, 1.0, 0.0)) return -2;  // T = X^2
-    count_launch();
-    ns_prep_kernel<<<64, 256, 0, st>>>(w->T, p, w->part, w->cnt, w->res);  // T = 3I - X^2
-    if (!dgemm(w, X, w->T, Xn, 0.5, 0.0)) return -2;  // X <- X (3I - X^2) / 2
-    double* t = X;
-    X = Xn;
-    Xn = t;
-    // ||X_prev^2 - I|| measured before this step.  Each check is a host sync: the first one
-    // comes where the previous call (a nearby H in a sweep) converged, then every 2 steps
-    const int first = w->last_it[slot] > 2 ? w->last_it[slot] - 1 : 8;
-    if ((it >= first && ((it - first) & 1) == 0) || it == max_it) {
-      cudaMemcpyAsync(w->res_host, w->res, 8, cudaMemcpyDeviceToHost, st);
-      cudaStreamSynchronize(st);
-      if (sqrt(*w->res_host) <= tol) {
-        if (X != S) cudaMemcpyAsync(S, X, (size_t)n * 8, cudaMemcpyDeviceToDevice, st);
-        w->last_it[slot] = it;
-        return it;
-      }
-    }
+// ---- Jacobi fallback (the NS iteration did not converge): f(theta), F = Y diag(f) Y^T, rank
+__global__ void ns_fallback_kernel(const int* fail, int op_soft, double thr,
+                                   const double* __restrict__ theta, const double* __restrict__ Y,
+                                   int p, double* __restrict__ F, int* rank) {
+  if (*fail == 0) return;
+  extern __shared__ double fv[];
+  for (int k = threadIdx.x; k < p; k += blockDim.x) {
+    const double t = theta[k];
+    fv[k] = op_soft ? (t > thr ? t - thr : (t < -thr ? t + thr : 0.0)) : (t > 0.0 ? t : 0.0);
   }
-  w->last_it[slot] = 0;
-  return -1;
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    int r = 0;
+    for (int k = 0; k < p; ++k) r += fv[k] != 0.0;
+    *rank = r;
+  }
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < p * p; x += gridDim.x * blockDim.x) {
+    const int i = x / p, j = x - i * p;
+    if (j < i) continue;
+    double s = 0.0;
+    for (int k = 0; k < p; ++k) s += Y[(size_t)i * p + k] * fv[k] * Y[(size_t)j * p + k];
+    F[(size_t)i * p + j] = s;
+    F[(size_t)j * p + i] = s;
+  }
 }
 
-// F = f(H) (row-major p x p, ld p), rank (device int); iterations (host) for diagnostics.
-// Returns 0, -1 (not converged: use Jacobi), -2 (cuBLAS failure)
-int ns_spectral(NsWork* w, const double* H, int op_soft, double thr, double* F, int* rank,
-                int* iters, cudaStream_t st) {
-  const int p = w->p;
-  int max_it = 100;
-  if (const char* e = getenv("PF_NS_MAXIT")) max_it = atoi(e);  // development / test knob
-  const double tol = 1e-12 * sqrt((double)p);
-  if (cublasSetStream(w->h, st) != CUBLAS_STATUS_SUCCESS) return -2;
-  cublasSetMathMode(w->h, CUBLAS_DEFAULT_MATH);  // fp64 arithmetic, no emulation
-  int it1, it2 = 0;
-  if (op_soft) {
-    it1 = ns_sign(w, H, thr, w->Sp, max_it, tol, 0, st);
-    if (it1 < 0) return it1;
-    it2 = ns_sign(w, H, -thr, w->Sm, max_it, tol, 1, st);
-    if (it2 < 0) return it2;
-    // F = H + ((H - thr I) S+ - (H + thr I) S-) / 2
-    cudaMemcpyAsync(F, H, (size_t)p * p * 8, cudaMemcpyDeviceToDevice, st);
-    cudaMemsetAsync(w->nrm, 0, 8, st);
-    count_launch();
-    ns_shift_kernel<<<(p + 7) / 8, 256, 0, st>>>(H, p, thr, w->M, w->nrm);    // H - thr I
-    if (!dgemm(w, w->M, w->Sp, F, 0.5, 1.0)) return -2;
-    count_launch();
-    ns_shift_kernel<<<(p + 7) / 8, 256, 0, st>>>(H, p, -thr, w->M, w->nrm);   // H + thr I
-    if (!dgemm(w, w->M, w->Sm, F, -0.5, 1.0)) return -2;
-  } else {
-    it1 = ns_sign(w, H, 0.0, w->Sp, max_it, tol, 0, st);
-    if (it1 < 0) return it1;
-    // F = (H + H S) / 2
-    cudaMemcpyAsync(F, H, (size_t)p * p * 8, cudaMemcpyDeviceToDevice, st);
-    if (!dgemm(w, H, w->Sp, F, 0.5, 0.5)) return -2;
-  }
+cudaError_t ns_fallback_launch(const int* fail, int op_soft, double thr, const double* theta,
+                               const double* Y, int p, double* F, int* rank, cudaStream_t st) {
   count_launch();
-  ns_rank_kernel<<<1, 512, 0, st>>>(p, w->Sp, w->Sm, op_soft, rank);
-  count_launch();
-  ns_symmetrize_kernel<<<(p * p + 255) / 256, 256, 0, st>>>(F, p);
-  if (iters) *iters = it1 + it2;
-  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+  ns_fallback_kernel<<<std::max(1, (p * p + 255) / 256), 256, p * sizeof(double), st>>>(
+      fail, op_soft, thr, theta, Y, p, F, rank);
+  return cudaGetLastError();
 }
 
 }  // namespace pf

@@ -521,7 +521,8 @@ __device__ __forceinline__ int hix(int i, int j) {
 template <int PE>
 __global__ void __launch_bounds__(JacCfg<PE>::THREADS) jacobi_kernel(
     const double* __restrict__ H, int p_static, const int* p_dev, double* __restrict__ theta,
-    double* __restrict__ Yout, DevState* state, double tol, int max_sweeps) {
+    double* __restrict__ Yout, DevState* state, double tol, int max_sweeps, const int* cond) {
+  if (cond && *cond == 0) return;  // conditional launch
   using C = JacCfg<PE>;
   extern __shared__ double js[];
   __shared__ double red[32];
@@ -719,7 +720,8 @@ __global__ void __launch_bounds__(JacCfg<PE>::THREADS) jacobi_kernel(
 template <int PE>
 __global__ void __launch_bounds__(PE * 16) jacobi_rows_kernel(
     const double* __restrict__ H, int p_static, const int* p_dev, double* __restrict__ theta,
-    double* __restrict__ Yout, DevState* state, double tol, int max_sweeps) {
+    double* __restrict__ Yout, DevState* state, double tol, int max_sweeps, const int* cond) {
+  if (cond && *cond == 0) return;  // conditional launch
   constexpr int HALF = PE / 2, NT = PE * 16;  // HALF warps
   extern __shared__ double js[];
   __shared__ double red[32];
@@ -865,7 +867,7 @@ __global__ void __launch_bounds__(PE * 16) jacobi_rows_kernel(
 template <int PE>
 static cudaError_t jacobi_rows_pe(const double* H, int p, const int* p_dev, double* theta,
                                   double* Y, DevState* state, double tol, int max_sweeps,
-                                  cudaStream_t st) {
+                                  cudaStream_t st, const int* cond) {
   constexpr size_t SMEM = (size_t)(2 * PE * PE + 3 * (PE / 2)) * 8 + (PE / 2) * 8;
   static bool attr = false;
   if (!attr) {
@@ -874,13 +876,15 @@ static cudaError_t jacobi_rows_pe(const double* H, int p, const int* p_dev, doub
     attr = true;
   }
   count_launch();
-  jacobi_rows_kernel<PE><<<1, PE * 16, SMEM, st>>>(H, p, p_dev, theta, Y, state, tol, max_sweeps);
+  jacobi_rows_kernel<PE><<<1, PE * 16, SMEM, st>>>(H, p, p_dev, theta, Y, state, tol, max_sweeps,
+                                                   cond);
   return cudaGetLastError();
 }
 
 template <int PE>
 static cudaError_t jacobi_pe(const double* H, int p, const int* p_dev, double* theta, double* Y,
-                             DevState* state, double tol, int max_sweeps, cudaStream_t st) {
+                             DevState* state, double tol, int max_sweeps, cudaStream_t st,
+                             const int* cond) {
   using C = JacCfg<PE>;
   static bool attr = false;
   if (!attr) {
@@ -889,13 +893,15 @@ static cudaError_t jacobi_pe(const double* H, int p, const int* p_dev, double* t
     attr = true;
   }
   count_launch();
-  jacobi_kernel<PE><<<1, C::THREADS, C::SMEM, st>>>(H, p, p_dev, theta, Y, state, tol, max_sweeps);
+  jacobi_kernel<PE><<<1, C::THREADS, C::SMEM, st>>>(H, p, p_dev, theta, Y, state, tol, max_sweeps,
+                                                    cond);
   return cudaGetLastError();
 }
 
 // p: order (runtime bound when p_dev != NULL: the kernel reads *p_dev <= p)
 cudaError_t jacobi_launch(const double* H, int p, const int* p_dev, double* theta, double* Y,
-                          DevState* state, double tol, int max_sweeps, cudaStream_t st) {
+                          DevState* state, double tol, int max_sweeps, cudaStream_t st,
+                          const int* cond) {
   static int rows = -1;  // development knob PF_JACOBI_ROWS=0 selects the block-thread kernel
   if (rows < 0) {
     const char* e = getenv("PF_JACOBI_ROWS");
@@ -903,11 +909,11 @@ cudaError_t jacobi_launch(const double* H, int p, const int* p_dev, double* thet
   }
   // measured (tools/bench_jacobi.py): 1.74 vs 2.03 us per round at p = 64, no gain at p <= 32
   if (rows && p > 32 && p <= 64)
-    return jacobi_rows_pe<64>(H, p, p_dev, theta, Y, state, tol, max_sweeps, st);
-  if (p <= 16) return jacobi_pe<16>(H, p, p_dev, theta, Y, state, tol, max_sweeps, st);
-  if (p <= 32) return jacobi_pe<32>(H, p, p_dev, theta, Y, state, tol, max_sweeps, st);
-  if (p <= 64) return jacobi_pe<64>(H, p, p_dev, theta, Y, state, tol, max_sweeps, st);
-  if (p <= 128) return jacobi_pe<128>(H, p, p_dev, theta, Y, state, tol, max_sweeps, st);
+    return jacobi_rows_pe<64>(H, p, p_dev, theta, Y, state, tol, max_sweeps, st, cond);
+  if (p <= 16) return jacobi_pe<16>(H, p, p_dev, theta, Y, state, tol, max_sweeps, st, cond);
+  if (p <= 32) return jacobi_pe<32>(H, p, p_dev, theta, Y, state, tol, max_sweeps, st, cond);
+  if (p <= 64) return jacobi_pe<64>(H, p, p_dev, theta, Y, state, tol, max_sweeps, st, cond);
+  if (p <= 128) return jacobi_pe<128>(H, p, p_dev, theta, Y, state, tol, max_sweeps, st, cond);
   return cudaErrorInvalidValue;
 }
 

@@ -52,13 +52,11 @@ class Solver:
         # (interval -> filter -> RR -> f -> update); the Lanczos refresh stays an eager launch
         # in front of it.  Iterations with a host-side change (degree schedule, extrapolation
         # window) are not graphed.
-        self.graphs = (graphs and cfg.deg_c <= 0.0 and not (cfg.mode == "nce" and cfg.accel_l > 0)
-                       and not cfg.rr_ns)   # Newton-Schulz checks convergence on the host
+        self.graphs = (graphs and cfg.deg_c <= 0.0 and not (cfg.mode == "nce" and cfg.accel_l > 0))
         if cfg.rr_ns and cfg.mode not in ("sweep_psd", "sweep_soft"):
             raise ValueError("rr_ns: the update kernels take eigen-factors; sweep modes only")
         self.F = None            # f(H) of the last Newton-Schulz Rayleigh-Ritz (p x p)
-        self.ns_iters = 0
-        self.ns_fallbacks = 0
+        self.ns_it = None        # device int: sign iterations of the last pf_rr_ns (-1: fallback)
         self.last_ns = False     # the last iteration's RR ran as Newton-Schulz
         self._graph = {}
         self.graph_launches = {}
@@ -219,15 +217,14 @@ class Solver:
         for _ in range(cfg.warmup if k == 0 else 1):
             ctx.filter(self.A, self.U, self.interval, cfg.q, cfg.rho_max, st)
         if cfg.rr_ns:
-            from ._lib import PFError
+            # Newton-Schulz f(H) on the device; an eigenvalue at the threshold (no convergence)
+            # falls back to Jacobi inside the same call (PF_FLAG_NS_FALLBACK)
             if self.F is None:
                 self.F = torch.empty((cfg.p, cfg.p), dtype=torch.float64, device="cuda")
-            try:
-                self.ns_iters = ctx.rr_ns(self.A, self.U, self.op, self.thr, self.F, self.rank, st)
-                self.last_ns = True
-                return
-            except PFError:            # an eigenvalue at the threshold: Jacobi this iteration
-                self.ns_fallbacks += 1
+                self.ns_it = torch.zeros(1, dtype=torch.int32, device="cuda")
+            ctx.rr_ns(self.A, self.U, self.op, self.thr, self.F, self.rank, self.ns_it, st)
+            self.last_ns = True
+            return
         ctx.rayleigh_ritz(self.A, self.U, self.V, self.theta, st)
         ctx.spectral_op(self.op, self.thr, self.theta, self.f, self.rank, st)
         self.last_ns = False
@@ -296,7 +293,7 @@ def _run(cfg, K, record, problem, nccl_id, rank, world, stream, graphs, loop=Non
             # X = Q F Q^T: recorded as the factor pair (Q F, Q) with unit weights
             Q = s.ritz_factors()
             F = s.F.cpu().numpy()
-            rec.update(rank=int(s.rank.item()), QF=Q @ F, Q=Q, ns_iters=s.ns_iters)
+            rec.update(rank=int(s.rank.item()), QF=Q @ F, Q=Q, ns_iters=int(s.ns_it.item()))
         elif record:
             f = s.f.cpu().numpy()
             keep = f != 0.0

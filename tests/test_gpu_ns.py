@@ -1,6 +1,7 @@
 """Rayleigh-Ritz + spectral operator by Newton-Schulz sign iterations (pf_rr_ns, NEXT-4, reading
 R26): F = f(U^T A U) against numpy's eigendecomposition, for both spectral operators and both
-storage paths; sweep trajectories against the oracle; the breakdown fallback."""
+storage paths; sweep trajectories against the oracle (also replayed as CUDA graphs: the iteration
+runs on the device, no host synchronisation); the device-side Jacobi fallback."""
 import numpy as np
 import pytest
 import torch
@@ -32,9 +33,11 @@ def test_rr_ns_fp64(op):
     F = torch.empty((p, p), dtype=torch.float64, device="cuda")
     rank = torch.zeros(1, dtype=torch.int32, device="cuda")
     thr = 1.0
-    it = ctx.rr_ns(torch.from_numpy(A).cuda(), torch.from_numpy(U).cuda(), op, thr, F, rank)
+    it = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ctx.rr_ns(torch.from_numpy(A).cuda(), torch.from_numpy(U).cuda(), op, thr, F, rank, it)
     want, r = _f(U.T @ A @ U, op, thr)
-    assert it > 0
+    assert it.item() > 0
+    assert "NS_FALLBACK" not in ctx.status()["names"]
     np.testing.assert_allclose(F.cpu().numpy(), want, rtol=0, atol=1e-11 * np.abs(want).max())
     assert int(rank.item()) == r
 
@@ -59,14 +62,52 @@ def test_rr_ns_tf32_matches_eigh():
     assert int(rank.item()) == r
 
 
-@pytest.mark.parametrize("cfg,tol", [
-    (reduced(CONFIGS[1], rr_ns=True), 1e-10),
-    (reduced(CONFIGS[5], n=2048, p=128, nbig=40, nrefl=16, iters=4, rr_ns=True), 1e-4)],
-    ids=["sweep_psd_fp64", "sweep_soft_tf32"])
-def test_ns_trajectory_matches_oracle(cfg, tol):
+@pytest.mark.parametrize("p,tf32", [(16, False), (32, False), (128, False), (256, True),
+                                    (512, True)])
+def test_rr_ns_sizes_and_symmetry(p, tf32):
+    """Tile edges (p < 32 is padded inside the kernel), the two-sign soft threshold at every
+    block width, and the exact symmetry of F (every product is formed on upper tiles and
+    mirrored)."""
+    from paper_1904_10585_b200._lib import Context, PF_TF32
+    n = max(3 * p, 600)
+    rs = np.random.default_rng(p)
+    q, _ = np.linalg.qr(rs.standard_normal((n, n)))
+    lam = np.concatenate([rs.uniform(2, 9, p // 3), rs.uniform(-1.5, 1.5, n - p // 3)])
+    A = (q * lam) @ q.T
+    A = 0.5 * (A + A.T)
+    U, _ = np.linalg.qr(rs.standard_normal((n, p)))
+    if tf32:
+        ctx = Context(n, p, 4, dtype=PF_TF32)
+        A32 = A.astype(np.float32)
+        A32 = np.triu(A32) + np.triu(A32, 1).T
+        U32 = np.ascontiguousarray(U.T.astype(np.float32))
+        Ad, Ud = torch.from_numpy(A32).cuda(), torch.from_numpy(U32).cuda()
+        Uf = U32.T.astype(np.float64)
+        H, tol = Uf.T @ A32.astype(np.float64) @ Uf, 1e-5
+    else:
+        ctx = Context(n, p, 4)
+        Ad, Ud = torch.from_numpy(A).cuda(), torch.from_numpy(U).cuda()
+        H, tol = U.T @ A @ U, 1e-11
+    F = torch.empty((p, p), dtype=torch.float64, device="cuda")
+    rank = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ctx.rr_ns(Ad, Ud, 1, 1.0, F, rank)
+    Fh = F.cpu().numpy()
+    assert np.array_equal(Fh, Fh.T)
+    want, r = _f(H, 1, 1.0)
+    np.testing.assert_allclose(Fh, want, rtol=0, atol=tol * np.abs(H).max())
+    assert int(rank.item()) == r
+
+
+@pytest.mark.parametrize("cfg,tol,graphs", [
+    (reduced(CONFIGS[1], rr_ns=True), 1e-10, False),
+    (reduced(CONFIGS[1], rr_ns=True), 1e-10, True),
+    (reduced(CONFIGS[5], n=2048, p=128, nbig=40, nrefl=16, iters=4, rr_ns=True), 1e-4, False),
+    (reduced(CONFIGS[5], n=2048, p=512, nbig=40, nrefl=16, iters=3, rr_ns=True), 1e-4, True)],
+    ids=["sweep_psd_fp64", "sweep_psd_fp64_graphs", "sweep_soft_tf32", "sweep_soft_tf32_p512_graphs"])
+def test_ns_trajectory_matches_oracle(cfg, tol, graphs):
     from paper_1904_10585_b200 import run
     ref = O.run(reduced(cfg, rr_ns=False))["records"]
-    got = run(cfg)["records"]
+    got = run(cfg, graphs=graphs)["records"]
     for x, y in zip(ref, got):
         den = O.lowrank_fro(x["V"], x["f"])
         if "QF" in y:
@@ -81,24 +122,63 @@ def test_ns_trajectory_matches_oracle(cfg, tol):
 
 def test_ns_breakdown_falls_back_to_jacobi(monkeypatch):
     """When the sign iterations do not converge (forced here by capping them at 3 with the
-    PF_NS_MAXIT knob) pf_rr_ns returns PF_ERR_BREAKDOWN and the solver runs Jacobi for that
-    iteration: the trajectory still matches the oracle."""
-    from paper_1904_10585_b200 import run
-    from paper_1904_10585_b200._lib import Context, PFError
-    monkeypatch.setenv("PF_NS_MAXIT", "3")
-    n, p = 200, 16
-    rs = np.random.default_rng(3)
-    A = rs.standard_normal((n, n))
-    A = A + A.T
-    U, _ = np.linalg.qr(rs.standard_normal((n, p)))
-    ctx = Context(n, p, 4)
-    F = torch.empty((p, p), dtype=torch.float64, device="cuda")
-    rank = torch.zeros(1, dtype=torch.int32, device="cuda")
-    with pytest.raises(PFError, match="BREAKDOWN"):
-        ctx.rr_ns(torch.from_numpy(A).cuda(), torch.from_numpy(U).cuda(), 0, 0.0, F, rank)
-    cfg = reduced(CONFIGS[1], iters=4, rr_ns=True)
-    out = run(cfg)
-    assert out["solver"].ns_fallbacks == 4
-    ref = O.run(reduced(cfg, rr_ns=False))["records"]
-    for x, y in zip(ref, out["records"]):
-        assert O.lowrank_diff_fro(x["V"], x["f"], y["V"], y["f"]) <= 1e-10 * O.lowrank_fro(x["V"], x["f"])
+    PF_NS_MAXIT knob, read once per process -- so this test runs in a subprocess) the same
+    pf_rr_ns call runs the cooperative Jacobi solver on the device and forms F = Y f(theta) Y^T;
+    PF_FLAG_NS_FALLBACK is set and the trajectory still matches the oracle."""
+    import subprocess
+    import sys
+    import textwrap
+    code = textwrap.dedent("""
+        import numpy as np, torch, oracle as O
+        from pfinputs import CONFIGS, reduced
+        from paper_1904_10585_b200 import run
+        from paper_1904_10585_b200._lib import Context
+        n, p = 200, 16
+        rs = np.random.default_rng(3)
+        A = rs.standard_normal((n, n)); A = A + A.T
+        U, _ = np.linalg.qr(rs.standard_normal((n, p)))
+        ctx = Context(n, p, 4)
+        F = torch.empty((p, p), dtype=torch.float64, device="cuda")
+        rank = torch.zeros(1, dtype=torch.int32, device="cuda")
+        it = torch.zeros(1, dtype=torch.int32, device="cuda")
+        ctx.rr_ns(torch.from_numpy(A).cuda(), torch.from_numpy(U).cuda(), 0, 0.0, F, rank, it)
+        assert it.item() == -1 and "NS_FALLBACK" in ctx.status()["names"]
+        lam, W = np.linalg.eigh(U.T @ A @ U)
+        want = (W * np.maximum(lam, 0)) @ W.T
+        assert np.abs(F.cpu().numpy() - want).max() <= 1e-11 * np.abs(want).max()
+        assert rank.item() == int((lam > 0).sum())
+        # p = 256 (TF32 context): the cooperative Jacobi fallback
+        from paper_1904_10585_b200._lib import PF_TF32
+        n, p = 1024, 256
+        q, _ = np.linalg.qr(rs.standard_normal((n, n)))
+        lam0 = np.concatenate([rs.uniform(5, 50, 40), rs.uniform(-1, 1, n - 40)])
+        A32 = ((q * lam0) @ q.T).astype(np.float32)
+        A32 = np.triu(A32) + np.triu(A32, 1).T
+        U32 = np.ascontiguousarray(np.linalg.qr(rs.standard_normal((n, p)))[0].T.astype(np.float32))
+        c32 = Context(n, p, 4, dtype=PF_TF32)
+        F = torch.empty((p, p), dtype=torch.float64, device="cuda")
+        c32.rr_ns(torch.from_numpy(A32).cuda(), torch.from_numpy(U32).cuda(), 1, 3.0, F, rank, it)
+        assert it.item() == -1 and "NS_FALLBACK" in c32.status()["names"]
+        Uf = U32.T.astype(np.float64)
+        lam, W = np.linalg.eigh(Uf.T @ A32.astype(np.float64) @ Uf)
+        fl = np.sign(lam) * np.maximum(np.abs(lam) - 3.0, 0.0)
+        want = (W * fl) @ W.T
+        assert np.abs(F.cpu().numpy() - want).max() <= 1e-5 * np.abs(want).max()
+        assert rank.item() == int((fl != 0).sum())
+        cfg = reduced(CONFIGS[1], iters=4, rr_ns=True)
+        out = run(cfg, graphs=True)
+        ref = O.run(reduced(cfg, rr_ns=False))["records"]
+        for x, y in zip(ref, out["records"]):
+            one = np.ones(y["Q"].shape[1])
+            err = O.lowrank_rect_diff_fro(x["V"] * x["f"], np.ones(x["f"].size), x["V"],
+                                          y["QF"], one, y["Q"])
+            assert err <= 1e-10 * O.lowrank_fro(x["V"], x["f"]), (x["k"], err)
+            assert y["ns_iters"] == -1
+        print("fallback ok")
+    """)
+    import os
+    env = dict(os.environ, PF_NS_MAXIT="3")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "fallback ok" in r.stdout, r.stdout + r.stderr

@@ -89,8 +89,7 @@ def main():
                          f"3xTF32 last {cfg.tf32_tail} steps + RR") +
                       (", RR spectral operator by Newton-Schulz" if args.ns else ", RR by Jacobi")
                       + ", 1 GPU",
-            "ns_iters_last": s.ns_iters if args.ns else None,
-            "ns_fallbacks": s.ns_fallbacks if args.ns else None,
+            "ns_iters_last": int(s.ns_it.item()) if args.ns else None,
             "it_per_s": 1e3 / ms, "ms_per_step": ms, "step_ms": step_ms,
             "filter_tflops": 2.0 * d * n * n * p / (ms / 1e3) / 1e12,
             "gemm_avg_ms": gemm_avg, "gemm_launches": gemm_n,
