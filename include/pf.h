@@ -233,6 +233,13 @@ pf_status pf_profile(pf_ctx ctx, int32_t enable);
 /* Synchronises `stream`; returns the summed GEMM time (ms) and the number of timed launches
  * since pf_profile, then clears the record.  PF_ERR_ARG if launches were dropped. */
 pf_status pf_profile_read(pf_ctx ctx, pf_stream stream, double* gemm_ms, int64_t* gemm_launches);
+/* Overlapped all-gather (PF_TF32, world > 1; environment PF_OVERLAP=0 at create turns it off):
+ * the timeline of the last overlapped GEMM step recorded while pf_profile is on.  Synchronises
+ * `stream`; writes 3 world values (ms from the step start): ms[s] = arrival of the s-th slab in
+ * consumption order (rank, rank - 1, ...), ms[world + s] / ms[2 world + s] = begin / end of its
+ * slab GEMM.  *count = 0 when no overlapped step was recorded.  cap >= 3 world. */
+pf_status pf_overlap_timeline(pf_ctx ctx, pf_stream stream, double* ms, int32_t cap,
+                              int32_t* count);
 /* Process-wide number of CUDA kernels launched by this library so far. */
 long long pf_kernel_launches(void);
 /* Synchronises `stream`; diag[0] = Jacobi sweeps of the last Rayleigh-Ritz solve,

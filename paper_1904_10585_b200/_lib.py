@@ -76,6 +76,7 @@ def load() -> ctypes.CDLL:
         "pf_diagnostics": [P, P, ctypes.POINTER(D)],
         "pf_nccl_unique_id": [P, I32],
         "pf_loop_create": [I32, ctypes.POINTER(P)],
+        "pf_overlap_timeline": [P, P, P, I32, ctypes.POINTER(I32)],
         "pf_loop_destroy": [P],
         "pf_create_loop": [I64, I32, I32, I32, P, I32, ctypes.POINTER(P)],
     }
@@ -223,6 +224,14 @@ class Context:
         self._check(self.lib.pf_profile_read(self.h, _stream(stream), ctypes.byref(ms),
                                              ctypes.byref(n)), "pf_profile_read")
         return ms.value, n.value
+
+    def overlap_timeline(self, stream=None) -> list[float]:
+        """Last overlapped step (pf_profile on): [arrival x W, gemm begin x W, gemm end x W] ms."""
+        buf = (ctypes.c_double * 192)()
+        cnt = ctypes.c_int32(0)
+        self._check(self.lib.pf_overlap_timeline(self.h, _stream(stream), buf, 192,
+                                                 ctypes.byref(cnt)), "pf_overlap_timeline")
+        return [buf[i] for i in range(cnt.value)]
 
     def lanczos(self, A, v0, m, lo_hi, stream=None):
         self._check(self.lib.pf_lanczos(self.h, _ptr(A), _ld(A), _ptr(v0), m, _ptr(lo_hi),

@@ -97,6 +97,18 @@ struct pf_ctx_s {
   Tf32Plan tplan;
   CUtensorMap mapBf[3];
   CUtensorMap mapAf, mapApf;
+  // overlapped all-gather (TF32, world > 1): the GEMM runs slab by slab
+  // (K range of rank g's rows) as each peer slab lands, on SMs left free for the transfers
+  bool overlap = false;
+  int comm_sms = 16;                           // SMs not used by the slab GEMMs (NCCL kernels)
+  cudaStream_t comm_st = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_comm_done = nullptr;
+  std::vector<cudaEvent_t> ev_slab;
+  Tf32Plan tplan_s;                            // one slab: n_local x n_local
+  std::vector<CUtensorMap> mapA_s, mapApf_s, mapB_s;
+  double* coef_acc = nullptr;                  // {s1, 1, 0} of the current step
+  std::vector<cudaEvent_t> ev_tl;              // timeline of the last overlapped step (pf_profile)
+  bool tl_valid = false;
   const float* mapAf_ptr = nullptr;
   int64_t mapAf_lda = 0;
   // ---- fp64 via exact int8 tensor-core products (dtype PF_FP64_I8, pf_gemm_i8.cu)
@@ -329,6 +341,26 @@ static pf_status alloc_all(pf_ctx ctx) {
   return PF_OK;
 }
 
+static pf_status setup_overlap(pf_ctx ctx) {
+  const int W = ctx->world, nl = (int)ctx->n_local, p = ctx->p;
+  PF_CU(cudaStreamCreateWithFlags(&ctx->comm_st, cudaStreamNonBlocking));
+  PF_CU(cudaEventCreateWithFlags(&ctx->ev_start, cudaEventDisableTiming));
+  PF_CU(cudaEventCreateWithFlags(&ctx->ev_comm_done, cudaEventDisableTiming));
+  ctx->ev_slab.assign(W, nullptr);
+  for (auto& e : ctx->ev_slab) PF_CU(cudaEventCreate(&e));  // timed: pf_overlap_timeline
+  PF_CU(cudaMalloc(&ctx->coef_acc, 4 * sizeof(double)));
+  ctx->tplan_s = tf32_plan(p, nl, nl, std::max(2, ctx->num_sms - ctx->comm_sms));
+  ctx->mapA_s.resize(W);
+  ctx->mapApf_s.resize(W);
+  ctx->mapB_s.resize(W);
+  for (int g = 0; g < W; ++g)
+    if (!tf32_encode_B(&ctx->mapB_s[g], ctx->Yfull32 + (size_t)g * p * nl, nl, p, nl)) {
+      snprintf(ctx->err, sizeof(ctx->err), "cuTensorMapEncodeTiled(B slab, fp32) failed");
+      return PF_ERR_CUDA;
+    }
+  return PF_OK;
+}
+
 static pf_status create_common(int64_t n, int32_t p, int32_t degree, pf_dtype dtype, int rank,
                                int world, const void* nccl_id, LoopHub* hub, pf_ctx* out) {
   if (!out) return PF_ERR_ARG;
@@ -379,6 +411,12 @@ static pf_status create_common(int64_t n, int32_t p, int32_t degree, pf_dtype dt
                     : comm_nccl_create(nccl_id, rank, world, ctx->err, &cs);
     s = (pf_status)cs;
   }
+  if (s == PF_OK && ctx->dist && dtype == PF_TF32 && world > 1) {
+    const char* e = getenv("PF_OVERLAP");  // 0: one all-gather, then one GEMM (measurement)
+    ctx->overlap = !(e && e[0] == '0');
+    if (const char* c = getenv("PF_COMM_SMS")) ctx->comm_sms = std::max(0, atoi(c));
+  }
+  if (s == PF_OK && ctx->overlap) s = setup_overlap(ctx);
   if (s != PF_OK) {
     fprintf(stderr, "pf_create: %s\n", ctx->err);
     pf_destroy(ctx);
@@ -457,11 +495,40 @@ pf_status pf_profile_read(pf_ctx ctx, pf_stream stream, double* gemm_ms, int64_t
   return ctx->prof_dropped ? PF_ERR_ARG : PF_OK;
 }
 
+pf_status pf_overlap_timeline(pf_ctx ctx, pf_stream stream, double* ms, int32_t cap,
+                              int32_t* count) {
+  if (!ctx || !ms || !count) return PF_ERR_ARG;
+  *count = 0;
+  if (!ctx->overlap || !ctx->tl_valid) return PF_OK;
+  const int W = ctx->world;
+  if (cap < 3 * W) return PF_ERR_DIM;
+  PF_CU(cudaStreamSynchronize((cudaStream_t)stream));
+  PF_CU(cudaStreamSynchronize(ctx->comm_st));
+  // ms[s]: arrival of the s-th slab in consumption order (g = rank - s); ms[W + s] / ms[2W + s]:
+  // begin / end of its GEMM; all relative to the step start
+  for (int i = 0; i < 3 * W; ++i) {
+    float t = 0.f;
+    cudaEvent_t e = i < W ? ctx->ev_slab[(ctx->rank - i + W) % W] : ctx->ev_tl[1 + i];
+    PF_CU(cudaEventElapsedTime(&t, ctx->ev_tl[0], e));
+    ms[i] = t;
+  }
+  *count = 3 * W;
+  return PF_OK;
+}
+
 pf_status pf_destroy(pf_ctx ctx) {
   if (!ctx) return PF_ERR_ARG;
   ns_destroy(ctx->ns);
   for (auto e : ctx->ev) cudaEventDestroy(e);
   delete ctx->comm;
+  if (ctx->comm_st) cudaStreamDestroy(ctx->comm_st);
+  if (ctx->ev_start) cudaEventDestroy(ctx->ev_start);
+  if (ctx->ev_comm_done) cudaEventDestroy(ctx->ev_comm_done);
+  for (auto e : ctx->ev_slab)
+    if (e) cudaEventDestroy(e);
+  if (ctx->coef_acc) cudaFree(ctx->coef_acc);
+  for (auto e : ctx->ev_tl)
+    if (e) cudaEventDestroy(e);
   void* ptrs[] = {ctx->state,  ctx->Y[0],     ctx->Y[1],      ctx->Y[2],    ctx->Yfull,
                   ctx->Wbuf,   ctx->VFbuf,    ctx->Vfull,    ctx->G,         ctx->Rinv,    ctx->Yeig,
                   ctx->gram_part, ctx->cheb_ws, ctx->cheb_cnt, ctx->lz_Q,   ctx->lz_qfull,
@@ -645,6 +712,12 @@ static pf_status map_A32(pf_ctx ctx, const float* A, int64_t lda) {
       snprintf(ctx->err, sizeof(ctx->err), "cuTensorMapEncodeTiled(A, fp32) failed");
       return PF_ERR_CUDA;
     }
+    const int nl = (int)ctx->n_local;
+    for (int g = 0; ctx->overlap && g < ctx->world; ++g)  // columns of rank g's rows
+      if (!tf32_encode_A(&ctx->mapA_s[g], &ctx->mapApf_s[g], A + (size_t)g * nl, lda, nl, nl)) {
+        snprintf(ctx->err, sizeof(ctx->err), "cuTensorMapEncodeTiled(A slab, fp32) failed");
+        return PF_ERR_CUDA;
+      }
     ctx->mapAf_ptr = A;
     ctx->mapAf_lda = lda;
   }
@@ -659,8 +732,54 @@ static pf_status copy_block32(pf_ctx ctx, float* dst, int64_t ldd, const float* 
   return PF_OK;
 }
 
+// Overlapped step (the gather of Y_j "must overlap" the GEMM): the communication
+// stream gathers the slabs one by one (Comm::allgather_slabs: own slab, then rank - 1, rank - 2,
+// ...), and the compute stream runs the product slab by slab in that order, each launch waiting
+// only for its own slab: the first writes s1 (A_g Y_g) + s2 Ycur + s3 Yprev, the others add
+// s1 (A_g Y_g) in place.  The slab GEMMs use num_sms - comm_sms SMs, so the NCCL kernels of the
+// next slabs run beside them.
+static pf_status gemm_step32_overlap(pf_ctx ctx, int bidx, const float* ycur, const float* yprev,
+                                     float* out, const double* coef, int npass, cudaStream_t st) {
+  const int W = ctx->world, nl = (int)ctx->n_local;
+  PF_CU(cudaEventRecord(ctx->ev_start, st));  // Y_j is ready
+  PF_CU(cudaStreamWaitEvent(ctx->comm_st, ctx->ev_start, 0));
+  const bool tl = ctx->prof;  // timeline: step start, slab arrivals, slab GEMM begin / end
+  if (tl && ctx->ev_tl.empty()) {
+    ctx->ev_tl.assign(1 + 3 * W, nullptr);
+    for (auto& e : ctx->ev_tl) PF_CU(cudaEventCreate(&e));
+  }
+  if (tl) PF_CU(cudaEventRecord(ctx->ev_tl[0], st));
+  PF_TRY((pf_status)ctx->comm->allgather_slabs(ctx->Yf[bidx], ctx->Yfull32,
+                                                (size_t)ctx->p * nl * 4, ctx->comm_st,
+                                                ctx->ev_slab.data()));
+
+  PF_CU(cudaEventRecord(ctx->ev_comm_done, ctx->comm_st));
+  PF_CU(coef_acc_launch(coef, ctx->coef_acc, st));
+  const bool rec = ctx->prof && ctx->ev_used + 2 <= ctx->ev.size();
+  if (ctx->prof && !rec) ++ctx->prof_dropped;
+  if (rec) PF_CU(cudaEventRecord(ctx->ev[ctx->ev_used], st));
+  for (int s = 0; s < W; ++s) {
+    const int g = (ctx->rank - s + W) % W;
+    PF_CU(cudaStreamWaitEvent(st, ctx->ev_slab[g], 0));
+    if (tl) PF_CU(cudaEventRecord(ctx->ev_tl[1 + W + s], st));
+    PF_CU(tf32_gemm_launch(ctx->tplan_s, ctx->mapA_s[g], ctx->mapB_s[g], ctx->mapApf_s[g],
+                           s == 0 ? ycur : out, s == 0 ? yprev : nullptr, out, ctx->ldy32,
+                           s == 0 ? coef : ctx->coef_acc, ctx->tf_ws, ctx->tf_acc, ctx->tf_cnt,
+                           npass, st, 0));
+    if (tl) PF_CU(cudaEventRecord(ctx->ev_tl[1 + 2 * W + s], st));
+  }
+  ctx->tl_valid = tl;
+  if (rec) {
+    PF_CU(cudaEventRecord(ctx->ev[ctx->ev_used + 1], st));
+    ctx->ev_used += 2;
+  }
+  PF_CU(cudaStreamWaitEvent(st, ctx->ev_comm_done, 0));  // Yf[bidx] / Yfull32 reusable after
+  return PF_OK;
+}
+
 static pf_status gemm_step32(pf_ctx ctx, int bidx, const float* ycur, const float* yprev,
                              float* out, const double* coef, int npass, cudaStream_t st) {
+  if (ctx->overlap) return gemm_step32_overlap(ctx, bidx, ycur, yprev, out, coef, npass, st);
   const CUtensorMap* mb = &ctx->mapBf[bidx];
   int bdist_kb = 0;
   if (ctx->dist) {

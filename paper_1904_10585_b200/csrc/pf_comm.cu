@@ -49,6 +49,31 @@ struct NcclComm final : Comm {
     ncclResult_t r = ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, c, st);
     return r == ncclSuccess ? PF_OK : fail(r, "ncclAllReduce");
   }
+  // ring of point-to-point steps: at step s every rank sends its slab to rank + s and receives
+  // rank - s's, so slab rank - s arrives at step s (one NCCL launch per step, event after it)
+  int allgather_slabs(const void* loc, void* full, size_t bytes, cudaStream_t st,
+                      cudaEvent_t* arrived) override {
+    char* f = static_cast<char*>(full);
+    if (cudaMemcpyAsync(f + (size_t)rank * bytes, loc, bytes, cudaMemcpyDeviceToDevice, st) !=
+            cudaSuccess ||
+        cudaEventRecord(arrived[rank], st) != cudaSuccess) {
+      snprintf(err, 512, "allgather_slabs: local slab copy failed");
+      return PF_ERR_CUDA;
+    }
+    for (int s = 1; s < world; ++s) {
+      const int to = (rank + s) % world, from = (rank - s + world) % world;
+      ncclGroupStart();
+      ncclSend(loc, bytes, ncclChar, to, c, st);
+      ncclRecv(f + (size_t)from * bytes, bytes, ncclChar, from, c, st);
+      ncclResult_t r = ncclGroupEnd();
+      if (r != ncclSuccess) return fail(r, "ncclSend/ncclRecv");
+      if (cudaEventRecord(arrived[from], st) != cudaSuccess) {
+        snprintf(err, 512, "allgather_slabs: cudaEventRecord failed");
+        return PF_ERR_CUDA;
+      }
+    }
+    return PF_OK;
+  }
 };
 
 Comm* comm_nccl_create(const void* nccl_id, int rank, int world, char* err, int* status) {
@@ -200,6 +225,28 @@ struct LoopComm final : Comm {
         r = cuda(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st), "cudaMemcpyAsync");
         if (r != PF_OK) return r;
       }
+    }
+    return finish(st);
+  }
+
+  int allgather_slabs(const void* loc, void* full, size_t bytes, cudaStream_t st,
+                      cudaEvent_t* arrived) override {
+    int r = cuda(cudaEventRecord(ready, st), "cudaEventRecord");
+    if (r != PF_OK) return r;
+    if (!rendezvous(loc, ready)) return fail("collective timed out or a peer failed");
+    char* f = static_cast<char*>(full);
+    for (int s = 0; s < world; ++s) {  // the NCCL ring's arrival order
+      const int g = (rank - s + world) % world;
+      const void* src = g == rank ? loc : peer(g).src;
+      if (g != rank) {
+        r = cuda(cudaStreamWaitEvent(st, peer(g).ev, 0), "cudaStreamWaitEvent");
+        if (r != PF_OK) return r;
+      }
+      r = cuda(cudaMemcpyAsync(f + (size_t)g * bytes, src, bytes, cudaMemcpyDeviceToDevice, st),
+               "cudaMemcpyAsync");
+      if (r != PF_OK) return r;
+      r = cuda(cudaEventRecord(arrived[g], st), "cudaEventRecord");
+      if (r != PF_OK) return r;
     }
     return finish(st);
   }

@@ -28,6 +28,12 @@ struct Comm {
   virtual int allgatherv(const void* loc, void* full, const size_t* off, cudaStream_t st) = 0;
   // buf <- sum over ranks (fp64); identical bits on every rank
   virtual int allreduce_sum(double* buf, size_t count, cudaStream_t st) = 0;
+  // Equal slabs, one at a time, for a consumer that overlaps them: rank
+  // g's `loc` (bytes) lands at full + g bytes; enqueued on `st` (the communication stream) in the
+  // fixed order g = rank, rank - 1, ..., rank - W + 1 (mod W), and arrived[g] is recorded on `st`
+  // right after slab g landed.  The caller orders its reuse of `loc` and `full` after `st`.
+  virtual int allgather_slabs(const void* loc, void* full, size_t bytes, cudaStream_t st,
+                              cudaEvent_t* arrived) = 0;
 };
 
 // the return value of the methods is a pf_status (PF_OK = 0)

@@ -229,6 +229,8 @@ cudaError_t admm_launch(const double* V, int64_t ldv, const double* Vloc, int64_
                         int p, double* obj, double* partials, int* counter, int raw, double* vf,
                         cudaStream_t st, const RbDigits* dig = nullptr);
 cudaError_t sqrt_inplace_launch(double* x, cudaStream_t st);
+// d = {c[0], 1, 0}: the coefficients that ADD s1 (A_g Y_g) to an output in place (slab GEMMs)
+cudaError_t coef_acc_launch(const double* c, double* d, cudaStream_t st);
 // NCE dual gradient update (NEXT-1): partials >= 2 * 256 doubles; obj gets raw sums
 cudaError_t nce_launch(const double* V, int64_t ldv, const double* f, int p, double tau,
                        const double* gdiag, const double* x_in, double* x_out, double* B,

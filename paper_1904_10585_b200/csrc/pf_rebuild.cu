@@ -699,6 +699,18 @@ cudaError_t admm_launch(const double* V, int64_t ldv, const double* Vloc, int64_
 
 __global__ void sqrt_inplace_kernel(double* x) { x[0] = sqrt(x[0]); }
 
+__global__ void coef_acc_kernel(const double* c, double* d) {
+  d[0] = c[0];
+  d[1] = 1.0;
+  d[2] = 0.0;
+}
+
+cudaError_t coef_acc_launch(const double* c, double* d, cudaStream_t st) {
+  count_launch();
+  coef_acc_kernel<<<1, 1, 0, st>>>(c, d);
+  return cudaGetLastError();
+}
+
 cudaError_t sqrt_inplace_launch(double* x, cudaStream_t st) {
   count_launch();
   sqrt_inplace_kernel<<<1, 1, 0, st>>>(x);

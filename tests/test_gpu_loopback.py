@@ -116,3 +116,28 @@ def test_loopback_missing_peer_times_out(monkeypatch):
     with pytest.raises(PFError, match="PF_ERR_NCCL"):
         c.orth(U)
     assert time.time() - t0 < 1.0
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_overlapped_gather_matches_single_gather(world, monkeypatch):
+    """TF32 row-block split, the config-5 path: the slab-by-slab GEMM overlapped with the
+    slab-by-slab gather (PF_OVERLAP=1, the default) against one all-gather then one GEMM
+    (PF_OVERLAP=0).  The slab sums regroup the fp32 accumulation, so the two agree to fp32
+    rounding (not bit for bit); both match the oracle at the TF32 bar."""
+    from paper_1904_10585_b200.dist import run_loopback
+    cfg = reduced(CONFIGS[5], n=2048, p=128, nbig=40, nrefl=16, iters=3)
+    ref = O.run(cfg)["records"]
+    outs = {}
+    for ov in ("1", "0"):
+        monkeypatch.setenv("PF_OVERLAP", ov)
+        outs[ov] = run_loopback(cfg, world)
+    for k, r in enumerate(ref):
+        Vs = {}
+        for ov, out in outs.items():
+            per = [o["records"][k] for o in out]
+            V = np.concatenate([g["V"] for g in per], axis=0)
+            Vs[ov] = (V, per[0]["f"])
+            den = O.lowrank_fro(r["V"], r["f"])
+            assert O.lowrank_diff_fro(V, per[0]["f"], r["V"], r["f"]) <= 1e-4 * den, (ov, k)
+        d = O.lowrank_diff_fro(*Vs["1"], *Vs["0"]) / O.lowrank_fro(*Vs["0"])
+        assert d <= 1e-5, (k, d)
