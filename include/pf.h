@@ -120,8 +120,10 @@ pf_status pf_get_device_status(pf_ctx ctx, pf_stream stream, uint32_t* flags, in
 
 /* m-step Lanczos with full re-orthogonalisation on the symmetric A (reading R5):
  * writes lo_hi[0] = theta_min - |r_min|, lo_hi[1] = theta_max + |r_max| (device double[2]),
- * and remembers them in the context.  v0: device start vector (n_local entries, any norm).
- * 1 <= m <= 64.  fp64 dtypes on one GPU (n <= 18944): only the 64 x 64 tiles on and above the
+ * and remembers them in the context.  v0: device start vector (n_local entries, any norm), or
+ * NULL to start from the Ritz vector of the smallest Ritz value of this context's previous
+ * pf_lanczos (lambda_min tracking across refreshes, NEXT-2, reading R29; PF_ERR_ARG if there was
+ * none).  1 <= m <= 64.  fp64 dtypes on one GPU (n <= 18944): only the 64 x 64 tiles on and above the
  * diagonal of A are read (A must be symmetric, as the method's iterates are; half the HBM
  * bytes); the environment variable PF_LZ_SYM=0 at pf_create reads all of A. */
 pf_status pf_lanczos(pf_ctx ctx, const void* A, int64_t lda, const double* v0, int32_t m,
@@ -246,8 +248,12 @@ long long pf_kernel_launches(void);
  * diag[1] = Lanczos steps of the last refresh, diag[2] = the relative gap of eqn:relative-gap
  * (NEXT-2 diagnostic) G = min over the Ritz values theta_i outside the damped
  * interval [a, b] of the last pf_filter of |theta_i - (a + b)/2| / ((b - a)/2) - 1, with the
- * Ritz values standing in for the eigenvalues (+inf when none lies outside). */
-pf_status pf_diagnostics(pf_ctx ctx, pf_stream stream, double* diag /* [3] */);
+ * Ritz values standing in for the eigenvalues (+inf when none lies outside), diag[3] = the
+ * eta_k estimate of eqn:etak (reading R28) for the wanted values of the last filter:
+ * (1 / T_d(1 + G))^q, the bound that holds when a guard Ritz value lies inside [a, b]; NaN when
+ * every Ritz value lies beyond [a, b] (saturated block) or no pf_filter preceded, 0 when none
+ * does. */
+pf_status pf_diagnostics(pf_ctx ctx, pf_stream stream, double* diag /* [4] */);
 
 /* Workload helper (not the method): A <- A + E (config 1 noise, BASELINE configs[0]).
  * PF_FP64 contexts only. */

@@ -27,6 +27,8 @@ Pins (tests/test_oracle_pins.py) -- what fixes each function independently of it
                       values of tab:ncm
   rna_extrapolate ... trivial windows, the l = 1 closed form, exact recovery of a linear fixed point
   relative_gap ...... hand example of eqn:relative-gap
+  eta_k / eta_bound . hand example (T_3(2) = 26); the bound equals the definition when
+                      lambda_{s_{p+1}} sits at the interval edge, dominates it otherwise
   degree_schedule ... Theta(log k) growth (thm:conv1's requirement), floor, c = 0 constant; on a
                       static config-1 matrix it reaches exact P_+ where the fixed d = 1 lags
   run ............... config 1 k = 0 == exact P_+; degenerate (PSD) interval == compression P A P;
@@ -52,7 +54,7 @@ __all__ = [
     "interval_soft", "lanczos_extremes", "rebase_plan", "spread_estimate", "chebyshev_filter",
     "orth", "filter_update", "rayleigh_ritz", "spectral_psd", "spectral_soft", "jacobi_eig",
     "exact_spectral", "maxcut_C", "prox_tG_diag", "pfam_next", "pfpg_next", "nce_next",
-    "rna_extrapolate", "run", "degree_schedule",
+    "rna_extrapolate", "run", "degree_schedule", "eta_k", "eta_bound",
     "lowrank_diff_fro", "lowrank_fro", "sin_theta",
 ]
 
@@ -103,11 +105,13 @@ def interval_soft(thr: float, eta: float) -> tuple[float, float]:
 
 
 # ============================================================================ Lanczos
-def lanczos_extremes(A: np.ndarray, v0: np.ndarray, m: int) -> tuple[float, float]:
+def lanczos_extremes(A: np.ndarray, v0: np.ndarray, m: int, ritz_vector: bool = False):
     """m-step Lanczos with full re-orthogonalisation (the paper's `eigs` for lambda_n,
     P:855-859; reading R5).  Returns (theta_min - |r_min|, theta_max + |r_max|), where
     theta are the Ritz values of the tridiagonal T_m and r the Ritz residual norms
-    |beta_m s_{m,i}|.  Stops early on breakdown (beta_j <= 1e-12 * max|alpha|)."""
+    |beta_m s_{m,i}|.  Stops early on breakdown (beta_j <= 1e-12 * max|alpha|).
+    ritz_vector: also return Q_m s_min, the Ritz vector of theta_min (the warm start of the next
+    refresh when lambda_min is tracked, reading R29)."""
     n = A.shape[0]
     m = min(m, n)
     Q = np.zeros((n, m))
@@ -131,6 +135,8 @@ def lanczos_extremes(A: np.ndarray, v0: np.ndarray, m: int) -> tuple[float, floa
     theta, S = np.linalg.eigh(T)
     r_min = abs(beta[steps - 1] * S[steps - 1, 0])
     r_max = abs(beta[steps - 1] * S[steps - 1, -1])
+    if ritz_vector:
+        return float(theta[0] - r_min), float(theta[-1] + r_max), Q[:, :steps] @ S[:, 0]
     return float(theta[0] - r_min), float(theta[-1] + r_max)
 
 
@@ -373,6 +379,35 @@ def relative_gap(theta: np.ndarray, a: float, b: float) -> float:
     return float(np.min(np.abs(out - c) / e - 1.0)) if out.size else float("inf")
 
 
+def eta_k(eigs: np.ndarray, a: float, b: float, d: int, p: int, q: int = 1) -> float:
+    """eqn:etak, the definition: with rho = T_d(L(.))^q and the eigenvalues ordered by
+    |rho| decreasing (lambda_{s_1}, lambda_{s_2}, ...), eta_k = |rho(lambda_{s_{p+1}})| /
+    |rho(lambda_{s_p})| (needs the whole spectrum: pins only)."""
+    c, e = interval_map(a, b)
+    r = np.sort(np.array([abs(cheb_T(d, (x - c) / e)) ** q for x in eigs]))[::-1]
+    return float(r[p] / r[p - 1])
+
+
+def eta_bound(theta: np.ndarray, a: float, b: float, d: int, q: int = 1) -> float:
+    """NEXT-2 diagnostic (reading R28): eta_k of the wanted values, estimated from the
+    Rayleigh-Ritz values of the block.  With r Ritz values beyond the damped interval [a, b] and
+    at least one inside (a guard direction, so the block holds every eigenvalue beyond [a, b]),
+    lambda_{s_{r+1}} lies in [a, b] where |rho| <= 1 and |rho(lambda_{s_r})| >= T_d(1 + G)^q with
+    G the relative gap (eqn:relative-gap), so eta_k <= (1 / T_d(1 + G))^q -- the bound behind
+    the paper's "eta_k < 1 since G_k >= l > 0".  The Ritz values stand in for the
+    eigenvalues (as for G); nan when every Ritz value lies beyond [a, b] (the block may be
+    saturated: nothing bounds lambda_{s_{p+1}}), 0 when none does (G = +inf)."""
+    if not b > a:
+        return float("nan")
+    outside = (theta < a) | (theta > b)
+    if outside.all():
+        return float("nan")
+    g = relative_gap(theta, a, b)
+    if math.isinf(g):
+        return 0.0
+    return float((1.0 / cheb_T(d, 1.0 + g)) ** q)
+
+
 def run(cfg: Config, iters: int | None = None, record_factors: bool = True,
         problem: dict | None = None, progress=None) -> dict:
     """The PFPG / PFAM / sweep iteration of SURVEY.md §8(c), step by step.
@@ -427,7 +462,11 @@ def run(cfg: Config, iters: int | None = None, record_factors: bool = True,
     for k in range(K):
         # a1: interval
         if k == 0 or (psd and k % cfg.lanczos_every == 0):
-            lo, hi = lanczos_extremes(A, lanczos_start(cfg, k), cfg.lanczos_steps)
+            if cfg.lanczos_warm > 0 and k > 0:     # lambda_min tracking (NEXT-2, reading R29)
+                lo, hi, v_bot = lanczos_extremes(A, v_bot, cfg.lanczos_warm, ritz_vector=True)
+            else:
+                lo, hi, v_bot = lanczos_extremes(A, lanczos_start(cfg, k), cfg.lanczos_steps,
+                                                 ritz_vector=True)
         # PSD iterate (a >= 0: nothing to damp): degenerate interval, the filter is
         # skipped this iteration and U_{k-1} is reused (SURVEY §8(c) reading)
         degenerate = psd and not lo < 0
@@ -451,7 +490,8 @@ def run(cfg: Config, iters: int | None = None, record_factors: bool = True,
         keep = f != 0.0
         rec = {"k": k, "a": a, "b": b, "theta": theta, "rank": int(keep.sum()),
                "saturated": bool(keep.all()), "rebase": plan, "degenerate": degenerate,
-               "gap": relative_gap(theta, a, b)}
+               "gap": relative_gap(theta, a, b),
+               "eta": eta_bound(theta, a, b, dk, cfg.q) if not degenerate else float("nan")}
         if record_factors:
             rec["V"], rec["f"] = V[:, keep], f[keep]
         # a6

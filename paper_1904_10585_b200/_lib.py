@@ -211,9 +211,10 @@ class Context:
         return {"flags": fl.value, "names": names, "rebases": rb.value, "lanczos": (lohi[0], lohi[1])}
 
     def diagnostics(self, stream=None) -> dict:
-        d = (ctypes.c_double * 3)()
+        d = (ctypes.c_double * 4)()
         self._check(self.lib.pf_diagnostics(self.h, _stream(stream), d), "pf_diagnostics")
-        return {"jacobi_sweeps": int(d[0]), "lanczos_steps": int(d[1]), "relative_gap": d[2]}
+        return {"jacobi_sweeps": int(d[0]), "lanczos_steps": int(d[1]), "relative_gap": d[2],
+                "eta": d[3]}
 
     def profile(self, enable: bool):
         self._check(self.lib.pf_profile(self.h, 1 if enable else 0), "pf_profile")

@@ -57,6 +57,8 @@ struct pf_ctx_s {
   double* lz_T = nullptr;
   double* lz_theta = nullptr;
   double* lz_S = nullptr;
+  double* lz_v0 = nullptr;                     // bottom Ritz vector of the last refresh (n_local)
+  bool lz_have_v0 = false;
   double* rb_part = nullptr;
   int* rb_cnt = nullptr;
   int* shift_flag = nullptr;
@@ -94,6 +96,7 @@ struct pf_ctx_s {
   int tf_tail = 0;   // number of final Chebyshev steps run in 3xTF32
   int tf_rr = 3;     // passes of the Rayleigh-Ritz product A Q
   bool filtered = false;  // a pf_filter ran: state->interval holds its damped interval
+  int last_d = 0, last_q = 1;  // degree and repeats of the last pf_filter (eta_k diagnostic)
   Tf32Plan tplan;
   CUtensorMap mapBf[3];
   CUtensorMap mapAf, mapApf;
@@ -288,6 +291,7 @@ static pf_status alloc_all(pf_ctx ctx) {
   ok &= A((void**)&ctx->lz_T, (size_t)kMaxLanczos * kMaxLanczos * 8);
   ok &= A((void**)&ctx->lz_theta, (size_t)kMaxLanczos * 8);
   ok &= A((void**)&ctx->lz_S, (size_t)kMaxLanczos * kMaxLanczos * 8);
+  ok &= A((void**)&ctx->lz_v0, (size_t)nl * 8);
   // shared by the rebuild (2 per tile CTA), NCE (2 x 256) and extrapolation (128 x 36) reductions
   ok &= A((void**)&ctx->rb_part,
           std::max<size_t>((size_t)rebuild_blocks((int)nl, (int)n) * 2, 128 * 36) * 8);
@@ -465,6 +469,7 @@ pf_status pf_diagnostics(pf_ctx ctx, pf_stream stream, double* diag) {
   diag[0] = h.scratch[1];
   diag[1] = (double)h.lanczos_steps;
   diag[2] = h.scratch[2];
+  diag[3] = h.scratch[4];
   return PF_OK;
 }
 
@@ -539,7 +544,8 @@ pf_status pf_destroy(pf_ctx ctx) {
                   ctx->jac_cnt, ctx->tf_ws,   ctx->tf_cnt,    ctx->tf_acc,  ctx->Yfull32,
                   ctx->A8,     ctx->a8_rscale, ctx->Y8,       ctx->y8_cscale, ctx->y8_cmax,
                   ctx->i8_acc, ctx->i8_part, ctx->i8_cnt, ctx->svt_part, ctx->svt_cnt,
-                  ctx->lz_sym_ws, ctx->a8_E, ctx->a8_wa, ctx->a8_wmax, ctx->jac_theta};
+                  ctx->lz_sym_ws, ctx->a8_E, ctx->a8_wa, ctx->a8_wmax, ctx->jac_theta,
+                  ctx->lz_v0};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete ctx;
@@ -841,6 +847,8 @@ static pf_status filter32(pf_ctx ctx, const float* A, int64_t lda, float* U, int
   const int p = ctx->p, d = ctx->d, nl = (int)ctx->n_local;
   PF_CU(plan_launch(interval, d, rho_max, p, ctx->state, st));
   ctx->filtered = true;
+  ctx->last_d = d;
+  ctx->last_q = q;
   PF_TRY(copy_block32(ctx, ctx->Yf[0], ctx->ldy32, U, ldu, st));
   int cur = 0, prev = -1;
   for (int rep = 0; rep < q; ++rep) {
@@ -888,7 +896,7 @@ static pf_status rayleigh_ritz32(pf_ctx ctx, const float* A, int64_t lda, const 
   PF_CU(jacobi_big_launch(ctx->G, p, theta, ctx->Yeig, ctx->jac_H, ctx->jac_V, ctx->jac_red,
                           ctx->jac_cnt, ctx->state, 1e-12, 40,
                           ctx->filtered ? &ctx->state->interval[0] : nullptr, st));
-  PF_CU(copy_theta_launch(theta, p, ctx->state, st));
+  PF_CU(copy_theta_launch(theta, p, ctx->state, st, ctx->last_d, ctx->last_q));
   PF_CU(rmul32_launch(ctx->Yf[0], ctx->ldy32, ctx->Yeig, V, ldv, nl, p, nullptr, st));
   return PF_OK;
 }
@@ -896,8 +904,10 @@ static pf_status rayleigh_ritz32(pf_ctx ctx, const float* A, int64_t lda, const 
 // ------------------------------------------------------------------------------ ABI
 pf_status pf_lanczos(pf_ctx ctx, const void* Av, int64_t lda, const double* v0, int32_t m,
                      double* lo_hi, pf_stream stream) {
-  if (!ctx || !v0 || !lo_hi) return PF_ERR_ARG;
+  if (!ctx || !lo_hi) return PF_ERR_ARG;
+  if (!v0 && !ctx->lz_have_v0) return PF_ERR_ARG;  // warm start needs a previous refresh
   if (m < 1 || m > kMaxLanczos) return PF_ERR_ARG;
+  if (!v0) v0 = ctx->lz_v0;  // lambda_min tracking: start from the last bottom Ritz vector
   const bool f32 = ctx->dtype == PF_TF32;
   const double* A = static_cast<const double*>(Av);
   const float* A32 = static_cast<const float*>(Av);
@@ -939,6 +949,8 @@ pf_status pf_lanczos(pf_ctx ctx, const void* Av, int64_t lda, const double* v0, 
     PF_CU(lz_next_launch(nl, ctx->lz_Q, ctx->lz_ldq, j, ctx->lz_w, s, ctx->state, st));
   }
   PF_CU(lanczos_finish_launch(m, ctx->lz_T, ctx->lz_theta, ctx->lz_S, lo_hi, ctx->state, st));
+  PF_CU(lz_ritz_vector_launch(ctx->lz_Q, ctx->lz_ldq, nl, ctx->lz_S, ctx->state, ctx->lz_v0, st));
+  ctx->lz_have_v0 = true;
   return PF_OK;
 }
 
@@ -1023,6 +1035,8 @@ pf_status pf_filter(pf_ctx ctx, const void* Av, int64_t lda, void* Uv, int64_t l
   const int nl = (int)ctx->n_local;
   const size_t row = (size_t)p * 8;
   PF_CU(plan_launch(interval, d, rho_max, p, ctx->state, st));
+  ctx->last_d = d;
+  ctx->last_q = q;
   PF_CU(cudaMemcpy2DAsync(ctx->Y[0], row, U, ldu * 8, row, nl, cudaMemcpyDeviceToDevice, st));
   int cur = 0, prev = -1;
   for (int rep = 0; rep < q; ++rep) {
@@ -1081,7 +1095,7 @@ pf_status pf_rayleigh_ritz(pf_ctx ctx, const void* Av, int64_t lda, const void* 
   }
   PF_CU(jacobi_launch(ctx->G, p, nullptr, theta, ctx->Yeig, ctx->state,
                       jtol > 0.0 ? jtol : std::max(1e-15, 1e-16 * p), 40, st));
-  PF_CU(copy_theta_launch(theta, p, ctx->state, st));
+  PF_CU(copy_theta_launch(theta, p, ctx->state, st, ctx->last_d, ctx->last_q));
   PF_CU(rmul_launch(ctx->Y[0], p, ctx->Yeig, V, ldv, nl, p, nullptr, st));
   return PF_OK;
 }

@@ -176,7 +176,10 @@ cudaError_t interval_soft_launch(double thr, double eta, double* interval, DevSt
                                  cudaStream_t st);
 cudaError_t interval_top_r_launch(const double* lo_hi, int r, double eta, double* interval,
                                   DevState* state, cudaStream_t st);
-cudaError_t copy_theta_launch(const double* theta, int p, DevState* state, cudaStream_t st);
+// theta -> state (re-base plan), relative gap and the eta_k estimate of the last filter (degree d,
+// q repeats; d = 0: no filter since -> nan)
+cudaError_t copy_theta_launch(const double* theta, int p, DevState* state, cudaStream_t st,
+                              int d = 0, int q = 1);
 // Lanczos (pf_lanczos.cu): vectors are local row blocks with pitch ldq; every phase leaves
 // LOCAL sums that the host all-reduces between phases when the context is distributed.
 int lanczos_blocks(int n_rows);
@@ -198,6 +201,8 @@ cudaError_t lz_orth_launch(int n_local, const double* Q, int64_t ldq, int j, dou
                            DevState* state, int phase, cudaStream_t st);
 cudaError_t lz_next_launch(int n_local, double* Q, int64_t ldq, int j, const double* w,
                            const double* s, DevState* state, cudaStream_t st);
+cudaError_t lz_ritz_vector_launch(const double* Q, int64_t ldq, int n_local, const double* S,
+                                  const DevState* state, double* v, cudaStream_t st);
 cudaError_t lanczos_finish_launch(int m, double* T, double* theta, double* S, double* lo_hi,
                                   DevState* state, cudaStream_t st);
 cudaError_t perturb_launch(double* A, int64_t lda, const double* E, int64_t lde, int rows,

@@ -545,6 +545,28 @@ __global__ void lanczos_extremes_kernel(const double* theta, const double* S, co
   state->lanczos_steps = me;
 }
 
+// v = Q_me s_min: the Ritz vector of the smallest Ritz value (the warm start of the next refresh,
+// NEXT-2 lambda_min tracking); S row-major me x me, columns by descending theta
+__global__ void lz_ritz_vector_kernel(const double* __restrict__ Q, int64_t ldq, int n_local,
+                                      const double* __restrict__ S, const int* m_dev,
+                                      double* __restrict__ v) {
+  const int me = *m_dev;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_local; i += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < me; ++j) s += Q[(size_t)j * ldq + i] * S[j * me + me - 1];
+    v[i] = s;
+  }
+}
+
+cudaError_t lz_ritz_vector_launch(const double* Q, int64_t ldq, int n_local, const double* S,
+                                  const DevState* state, double* v, cudaStream_t st) {
+  const int* m_dev = reinterpret_cast<const int*>(&state->scratch[0]);
+  count_launch();
+  lz_ritz_vector_kernel<<<std::max(1, std::min(296, (n_local + 255) / 256)), 256, 0, st>>>(
+      Q, ldq, n_local, S, m_dev, v);
+  return cudaGetLastError();
+}
+
 cudaError_t lanczos_finish_launch(int m, double* T, double* theta, double* S, double* lo_hi,
                                   DevState* state, cudaStream_t st) {
   int* m_dev = reinterpret_cast<int*>(&state->scratch[0]);

@@ -1058,9 +1058,12 @@ cudaError_t interval_soft_launch(double thr, double eta, double* interval, DevSt
   return cudaGetLastError();
 }
 
-__global__ void copy_theta_kernel(const double* theta, int p, DevState* state) {
+__global__ void copy_theta_kernel(const double* theta, int p, DevState* state, int d, int q) {
   __shared__ double red[32];
+  __shared__ int n_out;
   const int i = threadIdx.x;
+  if (i == 0) n_out = 0;
+  __syncthreads();
   // relative gap (eqn:relative-gap) of the Ritz values beyond the damped interval
   const double a = state->interval[0], b = state->interval[1];
   const double c = 0.5 * (a + b), e = 0.5 * (b - a);
@@ -1068,7 +1071,10 @@ __global__ void copy_theta_kernel(const double* theta, int p, DevState* state) {
   if (i < p) {
     const double t = theta[i];
     state->theta[i] = t;
-    if (e > 0.0 && (t < a || t > b)) g = fabs(t - c) / e - 1.0;
+    if (e > 0.0 && (t < a || t > b)) {
+      g = fabs(t - c) / e - 1.0;
+      atomicAdd(&n_out, 1);
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) g = fmin(g, __shfl_xor_sync(0xffffffffu, g, o));
@@ -1078,13 +1084,19 @@ __global__ void copy_theta_kernel(const double* theta, int p, DevState* state) {
     double m = INFINITY;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmin(m, red[w]);
     state->scratch[2] = m;
+    // eta_k of the wanted values (eqn:etak P:613-616, reading R28): (1 / T_d(1 + G))^q when a
+    // guard Ritz value lies inside [a, b]; T_d(x) = cosh(d acosh x) for x >= 1
+    double eta = NAN;
+    if (d > 0 && e > 0.0 && n_out < p) eta = isinf(m) ? 0.0 : exp(-(double)q * d * acosh(1.0 + m));
+    state->scratch[4] = eta;
     state->have_theta = 1;
   }
 }
 
-cudaError_t copy_theta_launch(const double* theta, int p, DevState* state, cudaStream_t st) {
+cudaError_t copy_theta_launch(const double* theta, int p, DevState* state, cudaStream_t st,
+                              int d, int q) {
   count_launch();
-  copy_theta_kernel<<<1, kMaxP, 0, st>>>(theta, p, state);
+  copy_theta_kernel<<<1, kMaxP, 0, st>>>(theta, p, state, d, q);
   return cudaGetLastError();
 }
 

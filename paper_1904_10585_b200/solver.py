@@ -167,7 +167,10 @@ class Solver:
         """One iteration k: interval -> filter (+warm-up at k = 0) -> RR -> f -> update."""
         cfg, ctx, st, k = self.cfg, self.ctx, self.stream, self.k
         if k == 0 or (self.psd and k % cfg.lanczos_every == 0):
-            ctx.lanczos(self.A, self.lanczos_vector(k), cfg.lanczos_steps, self.lohi, st)
+            if cfg.lanczos_warm > 0 and k > 0:   # lambda_min tracking (NEXT-2, reading R29)
+                ctx.lanczos(self.A, None, cfg.lanczos_warm, self.lohi, st)
+            else:
+                ctx.lanczos(self.A, self.lanczos_vector(k), cfg.lanczos_steps, self.lohi, st)
         if self.graphs and k >= 1:
             self._replay()
         else:

@@ -47,6 +47,9 @@ class Config:
     warmup: int = 4
     lanczos_steps: int = 20
     lanczos_every: int = 10
+    # NEXT-2 lambda_min tracking (reading R29): > 0 -> every refresh after the first runs this
+    # many Lanczos steps from the bottom Ritz vector of the previous refresh (0 = seeded restarts)
+    lanczos_warm: int = 0
     rho_max: float = 1e6      # re-base threshold on the predicted amplification
     # config-1/5 sweep
     noise: float = 1e-3

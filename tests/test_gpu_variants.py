@@ -65,19 +65,44 @@ def test_interval_top_r_matches_oracle():
                                rtol=1e-15, atol=1e-15)
 
 
-def test_relative_gap_diagnostic_matches_oracle():
-    """pf_diagnostics' relative gap (NEXT-2, eqn:relative-gap) from the device Ritz values and
-    the damped interval equals the oracle's on every iteration of a sweep."""
+@pytest.mark.parametrize("q", [1, 2])
+def test_relative_gap_and_eta_diagnostics_match_oracle(q):
+    """pf_diagnostics' relative gap (NEXT-2, eqn:relative-gap) and eta_k estimate (eqn:etak,
+    reading R28) from the device Ritz values and the damped interval equal the oracle's on every
+    iteration of a sweep (q = 2: the polynomial applied twice per filter)."""
     from paper_1904_10585_b200 import Solver
     import oracle as O
-    cfg = reduced(CONFIGS[1], iters=6)
+    cfg = reduced(CONFIGS[1], iters=6, q=q)
     ref = O.run(cfg)["records"]
     s = Solver(cfg)
     from pfinputs import cfg1_noise
     from paper_1904_10585_b200.solver import _dev
     for k in range(cfg.iters):
         s.step()
-        g = s.ctx.diagnostics()["relative_gap"]
-        assert g == pytest.approx(ref[k]["gap"], rel=1e-9), (k, g, ref[k]["gap"])
+        dg = s.ctx.diagnostics()
+        g = dg["relative_gap"]
+        # q = 2: the gap is set by a guard Ritz value just beyond the interval edge, fixed only
+        # to ~1e-6 by the (twice damped) unconverged direction -- looser bar
+        rel = 1e-9 if q == 1 else 1e-5
+        assert g == pytest.approx(ref[k]["gap"], rel=rel), (k, g, ref[k]["gap"])
+        assert np.isnan(ref[k]["eta"]) == np.isnan(dg["eta"])
+        if not np.isnan(ref[k]["eta"]):
+            assert dg["eta"] == pytest.approx(ref[k]["eta"], rel=100 * rel, abs=1e-300), k
+            assert 0.0 <= dg["eta"] < 1.0
+            # the device value is the bound of its own gap: (1 / T_d(1 + G))^q
+            assert dg["eta"] == pytest.approx((1.0 / O.cheb_T(cfg.d, 1.0 + g)) ** q, rel=1e-12)
         if k + 1 < cfg.iters:
             s.perturb(_dev(cfg1_noise(cfg, k)))
+
+
+@pytest.mark.parametrize("cfg,tol", [
+    (reduced(CONFIGS[1], iters=12, lanczos_every=3, lanczos_warm=8), 1e-10),
+    (reduced(CONFIGS[3], n=900, iters=12, edge_prob=82 / 900, lanczos_every=3, lanczos_warm=8),
+     1e-10),
+    (reduced(CONFIGS[3], n=1100, iters=12, edge_prob=0.07, lanczos_every=3, lanczos_warm=8,
+             dtype="f64i8"), 1e-10),
+], ids=["cfg1_warm", "cfg3_warm", "cfg3_i8_warm"])
+def test_lanczos_warm_start_trajectory(cfg, tol):
+    """NEXT-2 lambda_min tracking (reading R29): refreshes after the first restart a short
+    Lanczos from the previous bottom Ritz vector (pf_lanczos with v0 = NULL) on both sides."""
+    _traj(cfg, tol)

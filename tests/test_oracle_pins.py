@@ -617,3 +617,52 @@ def test_relative_gap_definition():
     assert O.relative_gap(np.array([0.5]), -1.0, 1.0) == float("inf")
     # G_k > 0 <=> every wanted value is strictly beyond the interval edge
     assert O.relative_gap(np.array([1.0 + 1e-9]), -1.0, 1.0) == pytest.approx(1e-9, rel=1e-6)
+
+
+def test_eta_bound_hand_example_and_definition():
+    """eqn:etak and reading R28.  Hand example: theta = (5, 2, -0.5) on [-1, 1]
+    (c = 0, e = 1): G = min(5, 2) - 1 = 1, T_3(2) = 4*8 - 3*2 = 26, so the bound is 1/26 (q = 2:
+    1/676).  Against the definition on a full spectrum: with lambda_{s_{p+1}} exactly at the
+    interval edge b (|rho| = 1) and a block holding the p eigenvalues beyond [a, b] plus a guard
+    direction inside, the bound IS eta_k (of the p wanted values); with the (p+1)-th strictly
+    inside the interval it is an upper bound."""
+    th = np.array([5.0, 2.0, -0.5])
+    assert O.eta_bound(th, -1.0, 1.0, 3) == pytest.approx(1.0 / 26.0, rel=1e-15)
+    assert O.eta_bound(th, -1.0, 1.0, 3, q=2) == pytest.approx(1.0 / 676.0, rel=1e-14)
+    assert np.isnan(O.eta_bound(np.array([3.0, -4.0]), -1.0, 1.0, 3))      # all beyond
+    assert O.eta_bound(np.array([0.1, -0.2]), -1.0, 1.0, 3) == 0.0          # none beyond
+    a, b, d, p = -2.0, 1.0, 5, 4
+    out = np.array([7.0, 4.5, 3.0, -3.1])                 # p eigenvalues beyond [a, b]
+    edge = np.concatenate([out, [b], np.linspace(-1.9, 0.9, 30)])
+    block = np.concatenate([out, [0.3]])                  # + one guard Ritz value inside
+    assert O.eta_bound(block, a, b, d) == pytest.approx(O.eta_k(edge, a, b, d, p), rel=1e-13)
+    rs = np.random.default_rng(5)
+    for _ in range(20):
+        inside = rs.uniform(a, b, 40)
+        e_true = O.eta_k(np.concatenate([out, inside]), a, b, d, p)
+        assert e_true <= O.eta_bound(block, a, b, d) * (1 + 1e-13)
+
+
+def test_lanczos_warm_start_tracks_lambda_min():
+    """NEXT-2 lambda_min tracking ("kept up to date periodically"; reading R29):
+    restarting m-step Lanczos from the previous refresh's bottom Ritz vector.  The start vector's
+    Rayleigh quotient is the previous theta_min and lies in the new Krylov space, so theta_min is
+    non-increasing over the restarts; on a fixed matrix with a known spectrum it converges to
+    lambda_min, the estimate lo = theta_min - |r| stays at or below lambda_min (+ rounding) once
+    theta_min is the closest Ritz value to it, and the Ritz vector converges to the eigenvector."""
+    rs = np.random.default_rng(11)
+    n = 300
+    lam = np.sort(np.concatenate([[-3.0, -2.7], rs.uniform(-2.5, 4.0, n - 2)]))
+    q, _ = np.linalg.qr(rs.standard_normal((n, n)))
+    A = (q * lam) @ q.T
+    A = 0.5 * (A + A.T)
+    lo, hi, v = O.lanczos_extremes(A, rs.standard_normal(n), 6, ritz_vector=True)
+    th_prev = v @ A @ v / (v @ v)
+    for _ in range(12):
+        lo, hi, v = O.lanczos_extremes(A, v, 6, ritz_vector=True)
+        th = v @ A @ v / (v @ v)
+        assert th <= th_prev + 1e-12
+        th_prev = th
+    assert th == pytest.approx(-3.0, abs=1e-9)
+    assert lo <= -3.0 + 1e-12
+    assert abs(abs(v @ q[:, 0]) / np.linalg.norm(v) - 1.0) < 1e-8

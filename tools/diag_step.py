@@ -25,7 +25,10 @@ def main(cfg_id=3, iters=14, **over):
         with torch.cuda.stream(st):
             ev[0].record(st)
             if k == 0 or (s.psd and k % cfg.lanczos_every == 0):
-                ctx.lanczos(s.A, s.lanczos_vector(k), cfg.lanczos_steps, s.lohi, st)
+                if cfg.lanczos_warm > 0 and k > 0:
+                    ctx.lanczos(s.A, None, cfg.lanczos_warm, s.lohi, st)
+                else:
+                    ctx.lanczos(s.A, s.lanczos_vector(k), cfg.lanczos_steps, s.lohi, st)
             ev[1].record(st)
             if s.psd:
                 ctx.interval_psd(s.lohi, cfg.eta, s.interval, st)
@@ -57,5 +60,9 @@ def main(cfg_id=3, iters=14, **over):
 
 if __name__ == "__main__":
     # diag_step.py <cfg> <iters> [dtype]  (dtype f64i8 = the bench's int8-digit filter)
+    # diag_step.py <cfg> <iters> [dtype] [field=value ...] (Config overrides, e.g. lanczos_warm=8)
     kw = {"dtype": sys.argv[3]} if len(sys.argv) > 3 else {}
+    for a in sys.argv[4:]:
+        k, v = a.split("=")
+        kw[k] = type(getattr(CONFIGS[int(sys.argv[1])], k))(v)
     main(*[int(a) for a in sys.argv[1:3]], **kw)
