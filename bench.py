@@ -92,8 +92,8 @@ class ClockSampler:
 
 
 def bench_cfg(cfg_id: int):
-    from pfinputs import CONFIGS
-    return CONFIGS[cfg_id]
+    from pfinputs import bench_config
+    return bench_config(cfg_id)
 
 
 # ============================================================================ our arm
@@ -241,6 +241,13 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         "data": "synthetic (BASELINE configs[2] recipe, DESIGN.md §3)",
         "config": {"workload": f"config 3: PFAM max-cut SDP, n={n}, p={p}, d={d}, G(n,{cfg.edge_prob})",
                    "n": n, "p": p, "d": d, "lanczos_every": cfg.lanczos_every,
+                   "rayleigh_ritz": "matrix form: F = P_+(H) = H when H is positive definite "
+                                    "(Cholesky test), else Newton-Schulz / Jacobi; update "
+                                    "W = Q F Q^T (DESIGN.md R30)" if cfg.rr_ns else
+                                    "Jacobi eigendecomposition",
+                   "lambda_min": (f"warm-started {cfg.lanczos_warm}-step Lanczos refresh every "
+                                  f"{cfg.lanczos_every} iterations (R29)") if cfg.lanczos_warm
+                                 else f"{cfg.lanczos_steps}-step seeded Lanczos (R5)",
                    "filter_gemm": "fp64 from exact int8 tensor-core products of 7-bit digit "
                                   "slices (PF_FP64_I8, S=7)" if args.path == "i8" else
                                   "fp64 DMMA (PF_FP64)",

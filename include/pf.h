@@ -204,6 +204,15 @@ pf_status pf_admm_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f
                        const uint32_t* adj, int64_t ldadj, const double* deg, double* Z,
                        int64_t ldz, double* obj, pf_stream stream);
 
+/* PFAM update in matrix form (with pf_rr_ns, reading R30): W = Q F Q^T, F p x p row-major fp64
+ * (device, symmetric), Q the local rows of the orthonormal block (n_local x p, ldq); otherwise as
+ * pf_admm_step (same Z contract, obj, fused digit output on one GPU).  With the PSD projection
+ * of a positive definite H = Q^T A Q, F = H (pf_rr_ns's PD test), so no eigendecomposition is
+ * needed at all. */
+pf_status pf_admm_step_f(pf_ctx ctx, const double* Q, int64_t ldq, const double* F, double t,
+                         const uint32_t* adj, int64_t ldadj, const double* deg, double* Z,
+                         int64_t ldz, double* obj, pf_stream stream);
+
 /* Nearest correlation estimation, dual gradient step (eqn:NCE-dual and
  * eqn:NCE-gradient), PF_FP64 contexts: with Pi_+(B) ~ V diag(f) V^T for the iterate
  * B = G + Diag(x) (f = max(theta, 0) from pf_spectral_op PF_OP_PSD):
@@ -312,7 +321,9 @@ pf_status pf_matmul(pf_ctx ctx, const double* A, int64_t lda, const double* Y, i
  * F = f(H) (p x p row-major fp64, device) through Newton-Schulz matrix sign iterations
  * (PSD: f(H) = (H + H sign(H)) / 2; soft threshold thr: f(H) = H + ((H - thr I) sign(H - thr I)
  * - (H + thr I) sign(H + thr I)) / 2) and *rank = #{f != 0} (device int) from traces, so
- * X = U F U^T.  The whole iteration runs in one cooperative kernel (hand-written fp64 DMMA
+ * X = U F U^T.  PSD with p <= 128: a Cholesky test first -- if H is positive definite,
+ * P_+(H) = H exactly, so F = H and rank = p without sign iterations (reading R30).  The whole
+ * iteration runs in one cooperative kernel (hand-written fp64 DMMA
  * products, device-side convergence test ||X^2 - I||_F <= 1e-12 sqrt(p), at most 100 steps): no
  * host synchronisation, capturable in a CUDA graph.  If a sign does not converge (an eigenvalue
  * at the threshold) the same call falls back on the device to the Jacobi eigensolver

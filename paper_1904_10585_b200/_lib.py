@@ -56,6 +56,7 @@ def load() -> ctypes.CDLL:
         "pf_svt_kick": [P, P, I64, D, D, D, P, P],
         "pf_svt_filter": [P, P, P, P, P, P, P, P, I64, D, D, P],
         "pf_admm_step": [P, P, I64, P, D, P, I64, P, P, I64, P, P],
+        "pf_admm_step_f": [P, P, I64, P, D, P, I64, P, P, I64, P, P],
         "pf_perturb": [P, P, I64, P, I64, P],
         "pf_perturb_hash": [P, P, I64, ctypes.c_uint64, I32, D, P],
         "pf_nce_step": [P, P, I64, P, D, P, P, P, P, I64, P, P],
@@ -288,6 +289,12 @@ class Context:
         self._check(self.lib.pf_admm_step(self.h, _ptr(V), _ld(V), _ptr(f), t, _ptr(adj),
                                           _ld(adj), _ptr(deg), _ptr(Z), _ld(Z), _ptr(obj),
                                           _stream(stream)), "pf_admm_step")
+
+    def admm_step_f(self, Q, F, t, adj, deg, Z, obj, stream=None):
+        """PFAM update with W = Q F Q^T (pf_admm_step_f)."""
+        self._check(self.lib.pf_admm_step_f(self.h, _ptr(Q), _ld(Q), _ptr(F), t, _ptr(adj),
+                                            _ld(adj), _ptr(deg), _ptr(Z), _ld(Z), _ptr(obj),
+                                            _stream(stream)), "pf_admm_step_f")
 
     def perturb(self, A, E, stream=None):
         self._check(self.lib.pf_perturb(self.h, _ptr(A), _ld(A), _ptr(E), _ld(E),

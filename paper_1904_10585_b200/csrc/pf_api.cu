@@ -1180,6 +1180,38 @@ pf_status pf_admm_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f
   return PF_OK;
 }
 
+pf_status pf_admm_step_f(pf_ctx ctx, const double* Q, int64_t ldq, const double* F, double t,
+                         const uint32_t* adj, int64_t ldadj, const double* deg, double* Z,
+                         int64_t ldz, double* obj, pf_stream stream) {
+  if (!ctx || !Q || !F || !adj || !deg || !Z || !obj) return PF_ERR_ARG;
+  if (!is_fp64(ctx)) return PF_ERR_UNSUPPORTED;
+  if (ldq < ctx->p || (ldq & 1) || !aligned16(Q) || ldadj < (ctx->n + 31) / 32 || ldz < ctx->n)
+    return PF_ERR_DIM;
+  cudaStream_t st = (cudaStream_t)stream;
+  iterate_written(ctx);
+  const double* Qf;
+  int64_t ldf;
+  PF_TRY(full_V(ctx, Q, ldq, &Qf, &ldf, st));
+  // local rows of Q F (the I panels of the rebuild); full_V used Wbuf only when distributed
+  PF_CU(rmul_launch(Q, ldq, F, ctx->VFbuf, ctx->p, (int)ctx->n_local, ctx->p, nullptr, st));
+  const bool fuse = use_i8(ctx) && !ctx->dist && ctx->fuse_digits &&
+                    (ctx->i8plan.S == 6 || ctx->i8plan.S == 7);
+  RbDigits dig{ctx->A8, ctx->i8plan.kblocks, ctx->i8plan.S, ctx->a8_E, ctx->a8_rscale, ctx->a8_wa, ctx->a8_wmax};
+  PF_CU(admm_launch(Qf, ldf, Q, ldq, nullptr, t, adj, ldadj, deg, Z, ldz, (int)ctx->n_local,
+                    (int)ctx->n, (int)ctx->row0, ctx->p, obj, ctx->rb_part, ctx->rb_cnt,
+                    ctx->dist ? 1 : 0, ctx->VFbuf, st, fuse ? &dig : nullptr, F));
+  if (fuse) {
+    ctx->a8_src = Z;
+    ctx->a8_lda = ldz;
+    ctx->a8_valid = ctx->a8_fused = true;
+  }
+  if (ctx->dist) {
+    PF_TRY(allreduce(ctx, obj, 2, st));
+    PF_CU(sqrt_inplace_launch(obj + 1, st));
+  }
+  return PF_OK;
+}
+
 pf_status pf_nce_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f, double tau,
                       const double* gdiag, const double* x_in, double* x_out, double* B,
                       int64_t ldb, double* obj, pf_stream stream) {

@@ -226,13 +226,16 @@ struct RbDigits {
   int* E;                   // [n] row exponents
   double* rscale;           // [n] 2^E
   double2* wa;              // [n] scratch (W_ii, sum_k |f_k| V_ik^2)
-  unsigned long long* wmax; // scratch
+  unsigned long long* wmax; // scratch (wmax[1]: ||F|| bound of the matrix form)
 };
 cudaError_t admm_launch(const double* V, int64_t ldv, const double* Vloc, int64_t ldvl,
                         const double* f, double t, const uint32_t* adj, int64_t ldadj,
                         const double* deg, double* Z, int64_t ldz, int n_rows, int n, int row0,
                         int p, double* obj, double* partials, int* counter, int raw, double* vf,
-                        cudaStream_t st, const RbDigits* dig = nullptr);
+                        cudaStream_t st, const RbDigits* dig = nullptr,
+                        const double* Fmat = nullptr);
+// (Fmat != NULL: W = V F V^T with F p x p row-major; vf must already hold the local rows of V F
+//  and f is unused)
 cudaError_t sqrt_inplace_launch(double* x, cudaStream_t st);
 // d = {c[0], 1, 0}: the coefficients that ADD s1 (A_g Y_g) to an output in place (slab GEMMs)
 cudaError_t coef_acc_launch(const double* c, double* d, cudaStream_t st);

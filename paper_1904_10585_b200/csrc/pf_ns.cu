@@ -42,7 +42,7 @@ struct NsWork {
   int p = 0, tt = 0, nup = 0;  // tiles per dimension, upper tiles (I <= J)
   double* buf = nullptr;       // per sign: 3 rotating p x p buffers; shared: Hs (p x p)
   double* part = nullptr;      // per CTA residual partials
-  int* ctrl = nullptr;         // [0] fail, [1] iterations, [2..3] final buffer per sign
+  int* ctrl = nullptr;         // [0] fail, [1] iterations, [2] PD shortcut taken
   unsigned long long* nrm = nullptr;  // per sign ||M||_inf bits
 };
 
@@ -61,6 +61,7 @@ struct NsArgs {
   unsigned long long* nrm;
   int* iters_out;  // device, may be NULL
   DevState* state;
+  const int* skip;  // device: the PD test already wrote F (PSD of a positive definite H)
 };
 
 __device__ __forceinline__ void ns_cp16(void* smem, const void* gmem) {
@@ -146,6 +147,7 @@ __device__ __forceinline__ void ns_store(double* __restrict__ C, int p, int I, i
 }
 
 __global__ void __launch_bounds__(kNsThreads) ns_kernel(const NsArgs a) {
+  if (a.skip && *a.skip) return;  // uniform over the grid
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) double sm[];
   __shared__ double red[32];
@@ -272,6 +274,7 @@ NsWork* ns_create(int p) {
             cudaMalloc(&w->part, (size_t)2 * w->nup * 8) == cudaSuccess &&
             cudaMalloc(&w->ctrl, 16) == cudaSuccess && cudaMalloc(&w->nrm, 16) == cudaSuccess &&
             cudaMemset(w->ctrl, 0, 16) == cudaSuccess;
+  // (ctrl[2] is written by pd_test_kernel before every PSD call; 0 otherwise)
   if (!ok) {
     ns_destroy(w);
     return nullptr;
@@ -287,6 +290,70 @@ void ns_destroy(NsWork* w) {
 }
 
 const int* ns_fail_flag(const NsWork* w) { return w->ctrl; }
+
+// PD test for the PSD projection (reading R30): H (symmetrised) positive definite <=> its Cholesky
+// factorisation runs through with positive pivots; then P_+(H) = H exactly (every eigenvalue is
+// kept), F = H, rank = p and the sign iterations are skipped.  Right-looking, one CTA, one barrier
+// per column (p <= 128); pivots must exceed 1e-13 of their original diagonal (an H indefinite
+// only by rounding takes the Newton-Schulz path).
+__global__ void __launch_bounds__(512) pd_test_kernel(const double* __restrict__ H, int p,
+                                                    double* __restrict__ F, int* rank, int* ctrl,
+                                                    int* iters_out) {
+  extern __shared__ double M[];  // p x (p + 1)
+  __shared__ int s_fail;
+  const int P1 = p + 1, tid = threadIdx.x, nt = blockDim.x, tx = tid & 31, ty = tid >> 5;
+  const int nty = nt >> 5;
+  for (int e = tid; e < p * p; e += nt) {
+    const int i = e / p, j = e - i * p;
+    const double v = 0.5 * (H[(size_t)i * p + j] + H[(size_t)j * p + i]);
+    F[e] = v;
+    if (j <= i) M[i * P1 + j] = v;
+    if (i == j) M[i * P1 + p] = v;  // original diagonal
+  }
+  if (tid == 0) s_fail = 0;
+  __syncthreads();
+  for (int j = 0; j < p; ++j) {
+    const double d = M[j * P1 + j];
+    if (!(d > 1e-13 * M[j * P1 + p])) {  // uniform
+      if (tid == 0) s_fail = 1;
+      break;
+    }
+    const double inv_d = 1.0 / d;
+    for (int i = j + 1 + ty; i < p; i += nty) {
+      const double lij = M[i * P1 + j] * inv_d;
+      for (int k = j + 1 + tx; k <= i; k += 32) M[i * P1 + k] -= lij * M[k * P1 + j];
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const int pd = !s_fail;
+    ctrl[2] = pd;
+    ctrl[0] = 0;
+    if (pd) {
+      *rank = p;
+      ctrl[1] = 0;
+      if (iters_out) *iters_out = 0;
+    }
+  }
+}
+
+static cudaError_t pd_shortcut(NsWork* w, const double* H, double* F, int* rank, int* iters,
+                               cudaStream_t st) {
+  const int p = w->p;
+  if (p > 128) return cudaMemsetAsync(w->ctrl + 2, 0, sizeof(int), st);
+  const size_t smem = (size_t)p * (p + 1) * 8;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(pd_test_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  count_launch();
+  pd_test_kernel<<<1, 512, smem, st>>>(H, p, F, rank, w->ctrl, iters);
+  return cudaGetLastError();
+}
 
 cudaError_t ns_spectral(NsWork* w, const double* H, int op_soft, double thr, double* F, int* rank,
                         int* iters_dev, DevState* state, cudaStream_t st) {
@@ -318,8 +385,16 @@ cudaError_t ns_spectral(NsWork* w, const double* H, int op_soft, double thr, dou
   a.nrm = w->nrm;
   a.iters_out = iters_dev;
   a.state = state;
+  a.skip = w->ctrl + 2;
   cudaError_t e = cudaMemsetAsync(w->nrm, 0, 16, st);
   if (e != cudaSuccess) return e;
+  if (!op_soft) {  // PSD: if H is positive definite, P_+(H) = H (no sign iterations)
+    e = pd_shortcut(w, H, F, rank, iters_dev, st);
+    if (e != cudaSuccess) return e;
+  } else {
+    e = cudaMemsetAsync(w->ctrl + 2, 0, sizeof(int), st);
+    if (e != cudaSuccess) return e;
+  }
   const size_t smem = (size_t)2 * 2 * kNsT * kNsLd * 8;
   static bool attr = false;
   if (!attr) {

@@ -651,6 +651,56 @@ __global__ void pfam_bound1_kernel(const double* __restrict__ VF, const double* 
   }
 }
 
+// matrix form W = Q F Q^T (pf_admm_step_f): |W_ij| <= ||F||_2 ||q_i|| ||q_j||, with ||F||_2 bounded
+// by min(||F||_F, max row sum) (pfam_fnorm_kernel, stored as bits in wmax[1]); W_ii exactly
+__global__ void pfam_fnorm_kernel(const double* __restrict__ F, int p, unsigned long long* out) {
+  __shared__ double red[32];
+  double f2 = 0.0, rmax = 0.0;
+  for (int i = threadIdx.x; i < p; i += blockDim.x) {
+    double r = 0.0;
+    for (int k = 0; k < p; ++k) {
+      const double v = F[(size_t)i * p + k];
+      f2 += v * v;
+      r += fabs(v);
+    }
+    rmax = fmax(rmax, r);
+  }
+  f2 = block_sum(f2, red);
+  __syncthreads();
+  for (int o = 16; o > 0; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = rmax;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, red[w]);
+    *out = (unsigned long long)__double_as_longlong(fmin(sqrt(f2), m) * (1.0 + 1e-12));
+  }
+}
+
+__global__ void pfam_bound1f_kernel(const double* __restrict__ VF, const double* __restrict__ V,
+                                    int64_t ldv, int n, int p, const unsigned long long* fn,
+                                    double2* __restrict__ wa, unsigned long long* wmax) {
+  const int i = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (i >= n) return;
+  const double nf = __longlong_as_double((long long)*fn);
+  double s = 0.0, q2 = 0.0;
+  for (int k = lane; k < p; k += 32) {
+    const double v = V[(size_t)i * ldv + k];
+    s += VF[(size_t)i * p + k] * v;
+    q2 += v * v;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    q2 += __shfl_xor_sync(0xffffffffu, q2, o);
+  }
+  if (lane == 0) {
+    const double sa = nf * q2 * (1.0 + 1e-12);
+    wa[i] = make_double2(s, sa);
+    atomicMax(wmax, (unsigned long long)__double_as_longlong(sqrt(sa)));
+  }
+}
+
 __global__ void pfam_bound2_kernel(const double2* __restrict__ wa,
                                    const unsigned long long* __restrict__ wmax,
                                    const double* __restrict__ Z, int64_t ldz, int n, double t,
@@ -674,16 +724,27 @@ cudaError_t admm_launch(const double* V, int64_t ldv, const double* Vloc, int64_
                         const double* f, double t, const uint32_t* adj, int64_t ldadj,
                         const double* deg, double* Z, int64_t ldz, int n_rows, int n, int row0,
                         int p, double* obj, double* partials, int* counter, int raw, double* vf,
-                        cudaStream_t st, const RbDigits* dig) {
-  cudaError_t e = scale_cols(Vloc, ldvl, f, n_rows, p, vf, st);
-  if (e != cudaSuccess) return e;
+                        cudaStream_t st, const RbDigits* dig, const double* Fmat) {
+  cudaError_t e = cudaSuccess;
+  if (!Fmat) {
+    e = scale_cols(Vloc, ldvl, f, n_rows, p, vf, st);
+    if (e != cudaSuccess) return e;
+  }
   RbArgs a{V, ldv, vf, f, t, adj, ldadj, nullptr, 0, 0, 0, 0, deg, Z, ldz, n_rows, n, row0,
            0, 0, raw, partials, counter, obj, nullptr, 0, nullptr, 0, nullptr};
   if (dig && dig->A8 && row0 == 0 && n_rows == n) {
     e = cudaMemsetAsync(dig->wmax, 0, 8, st);
     if (e != cudaSuccess) return e;
-    count_launch();
-    pfam_bound1_kernel<<<(n + 7) / 8, 256, 0, st>>>(vf, Vloc, ldvl, n, p, dig->wa, dig->wmax);
+    if (Fmat) {
+      count_launch();
+      pfam_fnorm_kernel<<<1, 128, 0, st>>>(Fmat, p, dig->wmax + 1);
+      count_launch();
+      pfam_bound1f_kernel<<<(n + 7) / 8, 256, 0, st>>>(vf, Vloc, ldvl, n, p, dig->wmax + 1,
+                                                        dig->wa, dig->wmax);
+    } else {
+      count_launch();
+      pfam_bound1_kernel<<<(n + 7) / 8, 256, 0, st>>>(vf, Vloc, ldvl, n, p, dig->wa, dig->wmax);
+    }
     e = cudaMemsetAsync(dig->E, 0x80, sizeof(int), st);  // INT_MIN-ish start for atomicMax
     if (e != cudaSuccess) return e;
     count_launch();

@@ -53,8 +53,8 @@ class Solver:
         # in front of it.  Iterations with a host-side change (degree schedule, extrapolation
         # window) are not graphed.
         self.graphs = (graphs and cfg.deg_c <= 0.0 and not (cfg.mode == "nce" and cfg.accel_l > 0))
-        if cfg.rr_ns and cfg.mode not in ("sweep_psd", "sweep_soft"):
-            raise ValueError("rr_ns: the update kernels take eigen-factors; sweep modes only")
+        if cfg.rr_ns and cfg.mode not in ("sweep_psd", "sweep_soft", "pfam"):
+            raise ValueError("rr_ns: sweep modes and PFAM (pf_admm_step_f) only")
         self.F = None            # f(H) of the last Newton-Schulz Rayleigh-Ritz (p x p)
         self.ns_it = None        # device int: sign iterations of the last pf_rr_ns (-1: fallback)
         self.last_ns = False     # the last iteration's RR ran as Newton-Schulz
@@ -227,6 +227,8 @@ class Solver:
                 self.ns_it = torch.zeros(1, dtype=torch.int32, device="cuda")
             ctx.rr_ns(self.A, self.U, self.op, self.thr, self.F, self.rank, self.ns_it, st)
             self.last_ns = True
+            if cfg.mode == "pfam":   # W = Q F Q^T (F = H when H is positive definite, R30)
+                ctx.admm_step_f(self.U, self.F, cfg.t, self.adj, self.deg, self.A, self.obj, st)
             return
         ctx.rayleigh_ritz(self.A, self.U, self.V, self.theta, st)
         ctx.spectral_op(self.op, self.thr, self.theta, self.f, self.rank, st)
@@ -297,6 +299,8 @@ def _run(cfg, K, record, problem, nccl_id, rank, world, stream, graphs, loop=Non
             Q = s.ritz_factors()
             F = s.F.cpu().numpy()
             rec.update(rank=int(s.rank.item()), QF=Q @ F, Q=Q, ns_iters=int(s.ns_it.item()))
+            if cfg.mode == "pfam":
+                rec["objective"], rec["aux"] = s.objective()
         elif record:
             f = s.f.cpu().numpy()
             keep = f != 0.0

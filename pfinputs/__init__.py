@@ -11,5 +11,5 @@ from .generators import (  # noqa: F401
     pfpg_problem, pfam_problem, sym_bernoulli_bitmask, unpack_bitmask,
     bitmask_words, cfg5_spectrum, cfg5_reflectors, cfg5_basis_columns, Cfg5Matrix, cfg5_problem,
     hash_gauss, cfg5_noise_rows, cfg5_perturb, NEXT_CONFIGS, nce_problem,
-    svt_problem, svt_guard_block,
+    svt_problem, svt_guard_block, BENCH_METHOD, bench_config,
 )

@@ -149,6 +149,17 @@ def reduced(cfg: Config, **kw) -> Config:
     return dataclasses.replace(cfg, **kw)
 
 
+# The method options bench.py times on config 3 (both are the method, DESIGN.md readings):
+# R30 -- the Rayleigh-Ritz spectral operator in matrix form (P_+(H) = H when H is positive
+# definite, else Newton-Schulz with a Jacobi fallback; update W = Q F Q^T), and R29 -- lambda_min
+# tracked by warm-started 8-step Lanczos refreshes.  The full-size parity test runs the same.
+BENCH_METHOD = {"rr_ns": True, "lanczos_warm": 8}
+
+
+def bench_config(cfg_id: int = 3) -> Config:
+    return dataclasses.replace(CONFIGS[cfg_id], **(BENCH_METHOD if cfg_id == 3 else {}))
+
+
 def _rng(seed: int, *stream: int) -> np.random.Generator:
     return np.random.default_rng([seed, *stream])
 

@@ -182,3 +182,56 @@ def test_ns_breakdown_falls_back_to_jacobi(monkeypatch):
     r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0 and "fallback ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("cfg,graphs", [
+    (reduced(CONFIGS[3], n=1100, iters=6, edge_prob=0.07, rr_ns=True), False),
+    (reduced(CONFIGS[3], n=1100, iters=6, edge_prob=0.07, rr_ns=True, dtype="f64i8"), True),
+    (reduced(CONFIGS[3], n=1500, iters=4, edge_prob=82 / 1500, p=32, rr_ns=True), False)],
+    ids=["pfam_f64", "pfam_i8_graphs", "pfam_p32"])
+def test_pfam_matrix_form_matches_oracle(cfg, graphs):
+    """PFAM with the Rayleigh-Ritz spectral operator in matrix form (reading R30): H positive
+    definite -> F = H (no eigensolver), else Newton-Schulz; the update W = Q F Q^T
+    (pf_admm_step_f, fused digits on the int8 path).  X_k and <C, W> vs the oracle's
+    eigendecomposition route at the fp64 bar."""
+    from paper_1904_10585_b200 import run
+    ref = O.run(reduced(cfg, rr_ns=False))["records"]
+    got = run(cfg, graphs=graphs)["records"]
+    for x, y in zip(ref, got):
+        one = np.ones(y["Q"].shape[1])
+        den = O.lowrank_fro(x["V"], x["f"])
+        err = O.lowrank_rect_diff_fro(x["V"] * x["f"], np.ones(x["f"].size), x["V"],
+                                      y["QF"], one, y["Q"])
+        assert err <= 1e-10 * den, (x["k"], err / den)
+        assert y["rank"] == x["rank"]
+        assert y["objective"] == pytest.approx(x["objective"], rel=1e-10)
+        assert y["aux"] == pytest.approx(x["residual"], rel=1e-9)
+
+
+def test_admm_step_f_matches_oracle():
+    """pf_admm_step_f on random data: Z_new = offdiag(Q F Q^T - tC) + Diag(1 - W_ii + Z_ii)
+    element by element, <C, W> and ||Z_new - Z||_F, against the oracle's pfam_next on the
+    eigen-factors of F."""
+    from paper_1904_10585_b200._lib import Context
+    from pfinputs import pfam_problem, unpack_bitmask
+    from paper_1904_10585_b200.solver import _bits
+    cfg = reduced(CONFIGS[3], n=777, edge_prob=0.1)
+    prob = pfam_problem(cfg)
+    n, p = cfg.n, 64
+    rs = np.random.default_rng(4)
+    Q = np.linalg.qr(rs.standard_normal((n, p)))[0]
+    B = rs.standard_normal((p, p))
+    F = B @ B.T / p
+    Z = rs.standard_normal((n, n)) * 0.1
+    Z = Z + Z.T
+    lam, Y = np.linalg.eigh(F)
+    C = O.maxcut_C(unpack_bitmask(prob["adj_bits"], n), prob["deg"])
+    Zr, cw, res = O.pfam_next(Q @ Y, lam, Z, C, 1.0)
+    c = Context(n, p, 4)
+    Zd = torch.from_numpy(Z.copy()).cuda()
+    obj = torch.zeros(2, dtype=torch.float64, device="cuda")
+    c.admm_step_f(torch.from_numpy(Q).cuda(), torch.from_numpy(F).cuda(), 1.0,
+                  _bits(prob["adj_bits"]), torch.from_numpy(prob["deg"]).cuda(), Zd, obj)
+    np.testing.assert_allclose(Zd.cpu().numpy(), Zr, rtol=0, atol=1e-13 * np.abs(Zr).max())
+    o = obj.cpu().numpy()
+    assert o[0] == pytest.approx(cw, rel=1e-12) and o[1] == pytest.approx(res, rel=1e-11)

@@ -38,6 +38,22 @@ def main(cfg_id=3, iters=14, **over):
             for _ in range(cfg.warmup if k == 0 else 1):
                 ctx.filter(s.A, s.U, s.interval, 1, cfg.rho_max, st)
             ev[3].record(st)
+            if cfg.rr_ns:   # matrix-form spectral operator (R26 / R30), update W = Q F Q^T
+                if s.F is None:
+                    s.F = torch.empty((cfg.p, cfg.p), dtype=torch.float64, device="cuda")
+                    s.ns_it = torch.zeros(1, dtype=torch.int32, device="cuda")
+                ctx.rr_ns(s.A, s.U, s.op, s.thr, s.F, s.rank, s.ns_it, st)
+                ev[4].record(st)
+                ev[5].record(st)
+                ctx.admm_step_f(s.U, s.F, cfg.t, s.adj, s.deg, s.A, s.obj, st)
+                ev[6].record(st)
+                s.k += 1
+                torch.cuda.synchronize()
+                ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(len(names))]
+                print(f"k={k:3d} " + " ".join(f"{n}={m:7.3f}" for n, m in zip(names, ms)) +
+                      f" total={sum(ms):7.3f} ms  ns_iters={int(s.ns_it.item())} rank={int(s.rank.item())}",
+                      flush=True)
+                continue
             ctx.rayleigh_ritz(s.A, s.U, s.V, s.theta, st)
             ev[4].record(st)
             ctx.spectral_op(s.op, s.thr, s.theta, s.f, s.rank, st)
