@@ -1365,6 +1365,9 @@ pf_status pf_rr_ns(pf_ctx ctx, const void* Av, int64_t lda, const void* Uv, int6
     }
   }
   const int soft = op == PF_OP_SOFT_THRESHOLD ? 1 : 0;
+  // no Ritz values: the next re-base plan falls back to the Lanczos spread estimate, unless the
+  // PD test below records its norm bound of H
+  PF_CU(cudaMemsetAsync(&ctx->state->have_theta, 0, sizeof(int), st));
   PF_CU(ns_spectral(ctx->ns, ctx->G, soft, thr, F, rank, iters, ctx->state, st));
   // device-side fallback (no host decision): Jacobi on the same H, then F = Y f(theta) Y^T;
   // both launches return at once unless the Newton-Schulz kernel raised its fail flag
@@ -1376,8 +1379,6 @@ pf_status pf_rr_ns(pf_ctx ctx, const void* Av, int64_t lda, const void* Uv, int6
     PF_CU(jacobi_big_launch(ctx->G, p, ctx->jac_theta, ctx->Yeig, ctx->jac_H, ctx->jac_V,
                             ctx->jac_red, ctx->jac_cnt, ctx->state, 1e-13, 40, nullptr, st, fail));
   PF_CU(ns_fallback_launch(fail, soft, thr, ctx->jac_theta, ctx->Yeig, p, F, rank, st));
-  // no Ritz values: the next re-base plan falls back to the Lanczos spread estimate
-  PF_CU(cudaMemsetAsync(&ctx->state->have_theta, 0, sizeof(int), st));
   ctx->filtered = false;
   return PF_OK;
 }

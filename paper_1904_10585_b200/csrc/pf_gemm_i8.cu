@@ -33,6 +33,8 @@
 //  * warps 4..7: epilogue, tcgen05.ld of every level, fp64 combination, row / column scales,
 //    the Chebyshev scale-shift-subtract, fp64 stores.  K ranges longer than the int32 bound are
 //    folded into an fp64 workspace (deterministic order).
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cstdlib>
 
@@ -158,58 +160,62 @@ __global__ void __launch_bounds__(512) a_split_kernel(const double* __restrict__
 }
 
 // ------------------------------------------------------------------------------ Y splitting
-// column max of Y (n_k x p row-major, ldy) into cmax[p] (uint64 bit patterns of |y| >= 0: their
-// integer order is the fp64 order).  cmax zeroed before.
-__global__ void y_colmax_kernel(const double* __restrict__ Y, int64_t ldy, int n_k, int p,
-                                unsigned long long* __restrict__ cmax) {
-  __shared__ double sm[256];
-  const int c = threadIdx.x % p, r0 = threadIdx.x / p, rstep = blockDim.x / p;
-  double m = 0.0;
-#pragma unroll 8
-  for (int r = blockIdx.x * rstep + r0; r < n_k; r += gridDim.x * rstep)
-    m = fmax(m, fabs(__ldg(Y + (int64_t)r * ldy + c)));
-  sm[threadIdx.x] = m;
-  __syncthreads();
-  if (threadIdx.x < p) {
-    for (int k = 1; k < rstep; ++k) m = fmax(m, sm[k * p + threadIdx.x]);
-    if (m > 0.0) atomicMax(cmax + c, (unsigned long long)__double_as_longlong(m));
-  }
-}
-
-// Y -> Y8[s][c][kpad] (K-major digit slices), cscale[c] = 2^F_c.  One CTA per 32-row chunk:
-// the 32 x p block is staged in shared memory, each thread emits 8 consecutive digits (8 bytes)
-// of one column per slice.
+// One cooperative launch for the B operand split: the column maxima of Y (n_k x p row-major, ldy;
+// grid-stride, atomicMax of the fp64 bit patterns of |y| >= 0, whose integer order is the fp64
+// order; the accumulator zeroed by CTA 0 before a first grid barrier), a second grid barrier,
+// then the digit split of each CTA's 32-row chunks (rows re-read from L2): Y -> Y8[s][c][kpad]
+// (K-major digit slices), cscale[c] = 2^F_c.
 template <int S>
-__global__ void __launch_bounds__(256) y_split_kernel(const double* __restrict__ Y, int64_t ldy,
-                                                      int n_k, int p,
-                                                      const unsigned long long* __restrict__ cmax,
-                                                      int8_t* __restrict__ Y8, int64_t kpad,
-                                                      double* __restrict__ cscale) {
-  constexpr int R = 32;  // rows (K) per CTA: 32-row chunks -> twice the CTAs of 64-row ones
+__global__ void __launch_bounds__(256) y_colmax_split_kernel(const double* __restrict__ Y,
+                                                            int64_t ldy, int n_k, int p,
+                                                            unsigned long long* cmax,
+                                                            int8_t* __restrict__ Y8, int64_t kpad,
+                                                            double* __restrict__ cscale) {
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  constexpr int R = 32;
   __shared__ double tile[R * 65];
-  const int k0 = blockIdx.x * R;
-  for (int cb = 0; cb < p; cb += 64) {
-    const int pc = min(64, p - cb);
+  if (blockIdx.x == 0)
+    for (int c = threadIdx.x; c < p; c += blockDim.x) cmax[c] = 0ull;
+  grid.sync();
+  {
+    double* smx = tile;  // 256 doubles
+    const int c = threadIdx.x % p, r0 = threadIdx.x / p, rstep = blockDim.x / p;
+    double m = 0.0;
+    for (int r = blockIdx.x * rstep + r0; r < n_k; r += gridDim.x * rstep)
+      m = fmax(m, fabs(__ldg(Y + (int64_t)r * ldy + c)));
+    smx[threadIdx.x] = m;
     __syncthreads();
-#pragma unroll 8
-    for (int i = threadIdx.x; i < R * pc; i += blockDim.x) {
-      const int r = i / pc, c = i % pc;
-      tile[r * 65 + c] = (k0 + r < n_k) ? __ldg(Y + (int64_t)(k0 + r) * ldy + cb + c) : 0.0;
+    if (threadIdx.x < p) {
+      for (int k = 1; k < rstep; ++k) m = fmax(m, smx[k * p + threadIdx.x]);
+      if (m > 0.0) atomicMax(cmax + c, (unsigned long long)__double_as_longlong(m));
     }
-    __syncthreads();
-    for (int i = threadIdx.x; i < pc * (R / 8); i += blockDim.x) {
-      const int c = i / (R / 8), g = i % (R / 8);  // column, 8-row group
-      const int E = i8::scale_exp(__longlong_as_double((long long)cmax[cb + c]));
-      if (blockIdx.x == 0 && g == 0) cscale[cb + c] = i8::pow2(E);
-      uint32_t lo[S], hi[S];
-      const double* tc0 = tile + (g * 8) * 65 + c;
-      i8::slices4<S>(tc0[0], tc0[65], tc0[130], tc0[195], E, lo);
-      i8::slices4<S>(tc0[260], tc0[325], tc0[390], tc0[455], E, hi);
-      const int k = k0 + g * 8;
-      if (k < n_k) {
+  }
+  grid.sync();
+  for (int chunk = blockIdx.x; chunk * R < n_k; chunk += gridDim.x) {
+    const int k0 = chunk * R;
+    for (int cb = 0; cb < p; cb += 64) {
+      const int pc = min(64, p - cb);
+      __syncthreads();
+      for (int i = threadIdx.x; i < R * pc; i += blockDim.x) {
+        const int r = i / pc, c = i % pc;
+        tile[r * 65 + c] = (k0 + r < n_k) ? Y[(int64_t)(k0 + r) * ldy + cb + c] : 0.0;
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < pc * (R / 8); i += blockDim.x) {
+        const int c = i / (R / 8), g = i % (R / 8);  // column, 8-row group
+        const int E = i8::scale_exp(__longlong_as_double((long long)__ldcg(cmax + cb + c)));
+        if (chunk == 0 && g == 0) cscale[cb + c] = i8::pow2(E);
+        uint32_t lo[S], hi[S];
+        const double* tc0 = tile + (g * 8) * 65 + c;
+        i8::slices4<S>(tc0[0], tc0[65], tc0[130], tc0[195], E, lo);
+        i8::slices4<S>(tc0[260], tc0[325], tc0[390], tc0[455], E, hi);
+        const int k = k0 + g * 8;
+        if (k < n_k) {
 #pragma unroll
-        for (int s = 0; s < S; ++s)
-          *reinterpret_cast<uint2*>(Y8 + ((int64_t)s * p + cb + c) * kpad + k) = make_uint2(lo[s], hi[s]);
+          for (int s = 0; s < S; ++s)
+            *reinterpret_cast<uint2*>(Y8 + ((int64_t)s * p + cb + c) * kpad + k) =
+                make_uint2(lo[s], hi[s]);
+        }
       }
     }
   }
@@ -635,17 +641,20 @@ template <int S>
 static cudaError_t y_split_s(const double* Y, int64_t ldy, const I8Plan& pl,
                              unsigned long long* cmax, int8_t* Y8, double* cscale,
                              int num_sms, cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(cmax, 0, sizeof(unsigned long long) * pl.p, st);
-  if (e != cudaSuccess) return e;
-  const int rstep = 256 / pl.p;
-  const int gmax = (pl.n_k + rstep - 1) / rstep;
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, y_colmax_split_kernel<S>, 256, 0);
+    per_sm = std::max(1, std::min(per_sm, 4));
+  }
+  const int chunks = (pl.n_k + 31) / 32;
+  const int grid = std::max(1, std::min(chunks, per_sm * num_sms));
+  int n_k = pl.n_k, p = pl.p;
+  int64_t kpad = pl.kpad;
+  void* args[] = {(void*)&Y, (void*)&ldy, (void*)&n_k, (void*)&p, (void*)&cmax, (void*)&Y8,
+                  (void*)&kpad, (void*)&cscale};
   count_launch();
-  y_colmax_kernel<<<std::max(1, std::min(gmax, 4 * num_sms)), 256, 0, st>>>(Y, ldy, pl.n_k, pl.p,
-                                                                              cmax);
-  count_launch();
-  y_split_kernel<S><<<(pl.n_k + 31) / 32, 256, 0, st>>>(Y, ldy, pl.n_k, pl.p, cmax, Y8, pl.kpad,
-                                                         cscale);
-  return cudaGetLastError();
+  return cudaLaunchCooperativeKernel((const void*)y_colmax_split_kernel<S>, dim3(grid), dim3(256),
+                                     args, 0, st);
 }
 cudaError_t i8_split_Y_launch(const double* Y, int64_t ldy, const I8Plan& pl,
                               unsigned long long* cmax, int8_t* Y8, double* cscale, int num_sms,

@@ -298,9 +298,10 @@ const int* ns_fail_flag(const NsWork* w) { return w->ctrl; }
 // only by rounding takes the Newton-Schulz path).
 __global__ void __launch_bounds__(512) pd_test_kernel(const double* __restrict__ H, int p,
                                                     double* __restrict__ F, int* rank, int* ctrl,
-                                                    int* iters_out) {
+                                                    int* iters_out, DevState* state) {
   extern __shared__ double M[];  // p x (p + 1)
   __shared__ int s_fail;
+  __shared__ double s_inf, s_fro;
   const int P1 = p + 1, tid = threadIdx.x, nt = blockDim.x, tx = tid & 31, ty = tid >> 5;
   const int nty = nt >> 5;
   for (int e = tid; e < p * p; e += nt) {
@@ -310,7 +311,24 @@ __global__ void __launch_bounds__(512) pd_test_kernel(const double* __restrict__
     if (j <= i) M[i * P1 + j] = v;
     if (i == j) M[i * P1 + p] = v;  // original diagonal
   }
-  if (tid == 0) s_fail = 0;
+  if (tid == 0) {
+    s_fail = 0;
+    s_inf = 0.0;
+    s_fro = 0.0;
+  }
+  __syncthreads();
+  // ||H||_inf and ||H||_F: a bound on the spread max |theta| of the Ritz values for the next
+  // re-base plan (the PD path computes no Ritz values)
+  for (int i = tid; i < p; i += nt) {
+    double r = 0.0, f = 0.0;
+    for (int k = 0; k < p; ++k) {
+      const double v = F[(size_t)i * p + k];
+      r += fabs(v);
+      f += v * v;
+    }
+    atomicMax(reinterpret_cast<unsigned long long*>(&s_inf), (unsigned long long)__double_as_longlong(r));
+    atomicAdd(&s_fro, f);
+  }
   __syncthreads();
   for (int j = 0; j < p; ++j) {
     const double d = M[j * P1 + j];
@@ -334,12 +352,16 @@ __global__ void __launch_bounds__(512) pd_test_kernel(const double* __restrict__
       *rank = p;
       ctrl[1] = 0;
       if (iters_out) *iters_out = 0;
+      // theta_max <= min(||H||_inf, ||H||_F) (all Ritz values are positive): the plan's spread
+      state->theta[0] = fmin(s_inf, sqrt(s_fro));
+      for (int k = 1; k < p; ++k) state->theta[k] = 0.0;
+      state->have_theta = 1;
     }
   }
 }
 
 static cudaError_t pd_shortcut(NsWork* w, const double* H, double* F, int* rank, int* iters,
-                               cudaStream_t st) {
+                               DevState* state, cudaStream_t st) {
   const int p = w->p;
   if (p > 128) return cudaMemsetAsync(w->ctrl + 2, 0, sizeof(int), st);
   const size_t smem = (size_t)p * (p + 1) * 8;
@@ -351,7 +373,7 @@ static cudaError_t pd_shortcut(NsWork* w, const double* H, double* F, int* rank,
     attr = true;
   }
   count_launch();
-  pd_test_kernel<<<1, 512, smem, st>>>(H, p, F, rank, w->ctrl, iters);
+  pd_test_kernel<<<1, 512, smem, st>>>(H, p, F, rank, w->ctrl, iters, state);
   return cudaGetLastError();
 }
 
@@ -389,7 +411,7 @@ cudaError_t ns_spectral(NsWork* w, const double* H, int op_soft, double thr, dou
   cudaError_t e = cudaMemsetAsync(w->nrm, 0, 16, st);
   if (e != cudaSuccess) return e;
   if (!op_soft) {  // PSD: if H is positive definite, P_+(H) = H (no sign iterations)
-    e = pd_shortcut(w, H, F, rank, iters_dev, st);
+    e = pd_shortcut(w, H, F, rank, iters_dev, state, st);
     if (e != cudaSuccess) return e;
   } else {
     e = cudaMemsetAsync(w->ctrl + 2, 0, sizeof(int), st);

@@ -4,6 +4,8 @@
 //   right multiplication Y <- Y R (fp64 DMMA): Q = Y R^-1, V = Q Y_eig, re-basing
 //   two-sided parallel cyclic Jacobi eigensolver (single CTA)                  (eqn:RR)
 //   spectral operator, interval / re-base plan, Lanczos, perturbation helper.
+#include <cooperative_groups.h>
+
 #include <algorithm>
 
 #include <cstdlib>
@@ -28,14 +30,17 @@ struct GramCfg {
   static constexpr int R = P >= 128 ? 16 : 32;       // rows per smem sub-chunk (static smem)
 };
 
+// One cooperative launch: per-CTA partial products, a grid barrier, then every CTA sums a slice
+// of the p x p entries over the partials in CTA order (deterministic; the same order as a
+// separate reduction kernel, one launch fewer per Gram).
 template <int P>
 __global__ void __launch_bounds__(256) gram_partial_kernel(const double* __restrict__ X,
                                                           const double* __restrict__ Y,
                                                           int n_rows, int rows_per_block,
                                                           double* __restrict__ partials,
-                                                          const int* cond) {
+                                                          const int* cond, double* G) {
   using C = GramCfg<P>;
-  if (cond && *cond == 0) return;
+  if (cond && *cond == 0) return;  // uniform over the grid
   __shared__ __align__(16) double Xs[C::R * C::LD];
   __shared__ __align__(16) double Ys[C::R * C::LD];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g8 = lane >> 2, t4 = lane & 3;
@@ -96,16 +101,13 @@ __global__ void __launch_bounds__(256) gram_partial_kernel(const double* __restr
         }
     }
   }
-}
-
-__global__ void gram_reduce_kernel(const double* __restrict__ partials, int nblk, int pp,
-                                   double* __restrict__ G, const int* cond) {
-  if (cond && *cond == 0) return;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= pp) return;
-  double s = 0.0;
-  for (int b = 0; b < nblk; ++b) s += partials[(size_t)b * pp + i];
-  G[i] = s;
+  cooperative_groups::this_grid().sync();
+  const int nb = gridDim.x;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < P * P; e += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += __ldcg(partials + (size_t)b * P * P + e);
+    G[e] = s;
+  }
 }
 
 static int gram_rows_per_block(int n_rows) {
@@ -121,23 +123,28 @@ int gram_blocks(int n_rows, int p) {
   return std::max(1, (n_rows + rpb - 1) / rpb);
 }
 
+template <int P>
+static cudaError_t gram_coop(const double* X, const double* Y, int n_rows, int rpb, int nb,
+                             double* partials, const int* cond, double* G, cudaStream_t st) {
+  void* args[] = {(void*)&X, (void*)&Y, (void*)&n_rows, (void*)&rpb, (void*)&partials,
+                  (void*)&cond, (void*)&G};
+  return cudaLaunchCooperativeKernel((const void*)gram_partial_kernel<P>, dim3(nb), dim3(256),
+                                     args, 0, st);
+}
+
 cudaError_t gram_launch(const double* X, const double* Y, int n_rows, int p, double* G,
                         double* partials, int* counter, const int* cond, cudaStream_t st) {
   (void)counter;
   const int rpb = gram_rows_per_block(n_rows);
-  const int nb = std::max(1, (n_rows + rpb - 1) / rpb);
+  const int nb = std::max(1, (n_rows + rpb - 1) / rpb);  // <= 148: one CTA per SM fits
   count_launch();
   switch (p) {
-    case 16: gram_partial_kernel<16><<<nb, 256, 0, st>>>(X, Y, n_rows, rpb, partials, cond); break;
-    case 32: gram_partial_kernel<32><<<nb, 256, 0, st>>>(X, Y, n_rows, rpb, partials, cond); break;
-    case 64: gram_partial_kernel<64><<<nb, 256, 0, st>>>(X, Y, n_rows, rpb, partials, cond); break;
-    case 128: gram_partial_kernel<128><<<nb, 256, 0, st>>>(X, Y, n_rows, rpb, partials, cond); break;
+    case 16: return gram_coop<16>(X, Y, n_rows, rpb, nb, partials, cond, G, st);
+    case 32: return gram_coop<32>(X, Y, n_rows, rpb, nb, partials, cond, G, st);
+    case 64: return gram_coop<64>(X, Y, n_rows, rpb, nb, partials, cond, G, st);
+    case 128: return gram_coop<128>(X, Y, n_rows, rpb, nb, partials, cond, G, st);
     default: return cudaErrorInvalidValue;
   }
-  const int pp = p * p;
-  count_launch();
-  gram_reduce_kernel<<<(pp + 255) / 256, 256, 0, st>>>(partials, nb, pp, G, cond);
-  return cudaGetLastError();
 }
 
 // =============================================================================== Cholesky
