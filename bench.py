@@ -237,7 +237,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "f64",
+        "dtype": "f64 (int8-digit emulation, S=7)" if args.path == "i8" else "f64",
         "data": "synthetic (BASELINE configs[2] recipe, DESIGN.md §3)",
         "config": {"workload": f"config 3: PFAM max-cut SDP, n={n}, p={p}, d={d}, G(n,{cfg.edge_prob})",
                    "n": n, "p": p, "d": d, "lanczos_every": cfg.lanczos_every,
@@ -330,8 +330,9 @@ def run_e2e(cfg, args, stream) -> dict:
             "deg": torch.from_numpy(prob["deg"]).pin_memory(),
             "U0": torch.from_numpy(initial_block(cfg)).pin_memory()}
     K = args.steps + args.warmup
+    # seeded Lanczos start vectors the run uses (only k = 0 when refreshes are warm-started, R29)
     v0 = {k: torch.from_numpy(lanczos_start(cfg, k)).pin_memory()
-          for k in range(K) if k % cfg.lanczos_every == 0}
+          for k in range(K) if k % cfg.lanczos_every == 0 and (k == 0 or cfg.lanczos_warm <= 0)}
     obj_host = torch.empty((K, 2), dtype=torch.float64).pin_memory()
     from paper_1904_10585_b200._lib import Context, PF_FP64, PF_FP64_I8
     ctx = Context(cfg.n, cfg.p, cfg.d, dtype=PF_FP64_I8 if cfg.dtype == "f64i8" else PF_FP64)
@@ -353,7 +354,8 @@ def run_e2e(cfg, args, stream) -> dict:
             obj_host[k].copy_(s.obj, non_blocking=True)
             d2h += 16
         Vh = s.ritz.to("cpu", non_blocking=True)
-        fh = s.f.to("cpu", non_blocking=True)
+        # the factors of X_k: (V, f), or (Q, F) for the matrix-form Rayleigh-Ritz (R30)
+        fh = (s.F if s.last_ns else s.f).to("cpu", non_blocking=True)
         d2h += Vh.numel() * 8 + fh.numel() * 8
         e1.record(stream)
     torch.cuda.synchronize()
