@@ -632,23 +632,29 @@ cudaError_t prox_launch(const double* V, int64_t ldv, const double* Vloc, int64_
 __global__ void pfam_bound1_kernel(const double* __restrict__ VF, const double* __restrict__ V,
                                    int64_t ldv, int n, int p, double2* __restrict__ wa,
                                    unsigned long long* wmax) {
+  __shared__ unsigned long long bmax;
   const int i = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (i >= n) return;
-  double s = 0.0, sa = 0.0;
-  for (int k = lane; k < p; k += 32) {
-    const double x = VF[(size_t)i * p + k] * V[(size_t)i * ldv + k];
-    s += x;
-    sa += fabs(x);
-  }
+  if (threadIdx.x == 0) bmax = 0ull;
+  __syncthreads();
+  if (i < n) {
+    double s = 0.0, sa = 0.0;
+    for (int k = lane; k < p; k += 32) {
+      const double x = VF[(size_t)i * p + k] * V[(size_t)i * ldv + k];
+      s += x;
+      sa += fabs(x);
+    }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    s += __shfl_xor_sync(0xffffffffu, s, o);
-    sa += __shfl_xor_sync(0xffffffffu, sa, o);
+    for (int o = 16; o > 0; o >>= 1) {
+      s += __shfl_xor_sync(0xffffffffu, s, o);
+      sa += __shfl_xor_sync(0xffffffffu, sa, o);
+    }
+    if (lane == 0) {
+      wa[i] = make_double2(s, sa);
+      atomicMax(&bmax, (unsigned long long)__double_as_longlong(sqrt(sa)));
+    }
   }
-  if (lane == 0) {
-    wa[i] = make_double2(s, sa);
-    atomicMax(wmax, (unsigned long long)__double_as_longlong(sqrt(sa)));
-  }
+  __syncthreads();  // one global atomic per block instead of one per row
+  if (threadIdx.x == 0 && bmax) atomicMax(wmax, bmax);
 }
 
 // matrix form W = Q F Q^T (pf_admm_step_f): |W_ij| <= ||F||_2 ||q_i|| ||q_j||, with ||F||_2 bounded
@@ -680,25 +686,31 @@ __global__ void pfam_fnorm_kernel(const double* __restrict__ F, int p, unsigned 
 __global__ void pfam_bound1f_kernel(const double* __restrict__ VF, const double* __restrict__ V,
                                     int64_t ldv, int n, int p, const unsigned long long* fn,
                                     double2* __restrict__ wa, unsigned long long* wmax) {
+  __shared__ unsigned long long bmax;
   const int i = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (i >= n) return;
-  const double nf = __longlong_as_double((long long)*fn);
-  double s = 0.0, q2 = 0.0;
-  for (int k = lane; k < p; k += 32) {
-    const double v = V[(size_t)i * ldv + k];
-    s += VF[(size_t)i * p + k] * v;
-    q2 += v * v;
-  }
+  if (threadIdx.x == 0) bmax = 0ull;
+  __syncthreads();
+  if (i < n) {
+    const double nf = __longlong_as_double((long long)*fn);
+    double s = 0.0, q2 = 0.0;
+    for (int k = lane; k < p; k += 32) {
+      const double v = V[(size_t)i * ldv + k];
+      s += VF[(size_t)i * p + k] * v;
+      q2 += v * v;
+    }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    s += __shfl_xor_sync(0xffffffffu, s, o);
-    q2 += __shfl_xor_sync(0xffffffffu, q2, o);
+    for (int o = 16; o > 0; o >>= 1) {
+      s += __shfl_xor_sync(0xffffffffu, s, o);
+      q2 += __shfl_xor_sync(0xffffffffu, q2, o);
+    }
+    if (lane == 0) {
+      const double sa = nf * q2 * (1.0 + 1e-12);
+      wa[i] = make_double2(s, sa);
+      atomicMax(&bmax, (unsigned long long)__double_as_longlong(sqrt(sa)));
+    }
   }
-  if (lane == 0) {
-    const double sa = nf * q2 * (1.0 + 1e-12);
-    wa[i] = make_double2(s, sa);
-    atomicMax(wmax, (unsigned long long)__double_as_longlong(sqrt(sa)));
-  }
+  __syncthreads();
+  if (threadIdx.x == 0 && bmax) atomicMax(wmax, bmax);
 }
 
 __global__ void pfam_bound2_kernel(const double2* __restrict__ wa,

@@ -958,6 +958,12 @@ cudaError_t spectral_launch(int op, double thr, const double* theta, int p, doub
 // Per pf_filter call: coefficients of the recurrence and the re-base schedule (reading R7).
 __global__ void plan_kernel(const double* __restrict__ interval, int d, double rho_max, int p,
                             DevState* state) {
+  // the spread max |theta_prev| by one warp (a serial loop of dependent global loads took ~15 us)
+  double sp = 0.0;
+  if (state->have_theta)
+    for (int i = threadIdx.x; i < p; i += 32) sp = fmax(sp, fabs(state->theta[i]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sp = fmax(sp, __shfl_xor_sync(0xffffffffu, sp, o));
   if (threadIdx.x != 0) return;
   const double a = interval[0], b = interval[1];
   state->interval[0] = a;
@@ -978,8 +984,7 @@ __global__ void plan_kernel(const double* __restrict__ interval, int d, double r
   const double c = 0.5 * (b + a), e = 0.5 * (b - a);
   double spread;
   if (state->have_theta) {
-    spread = 0.0;
-    for (int i = 0; i < p; ++i) spread = fmax(spread, fabs(state->theta[i]));
+    spread = sp;
   } else if (state->have_lanczos) {
     spread = fmax(fabs(state->lanczos[0]), fabs(state->lanczos[1]));
   } else {
@@ -997,10 +1002,16 @@ __global__ void plan_kernel(const double* __restrict__ interval, int d, double r
       state->coef[j][2] = -1.0;
     }
   }
+  // T_0 .. T_d at t_hat by the three-term recurrence (t_hat >= 1: all positive, increasing);
+  // the closed form's two fp64 pow() per value cost ~15 us on one thread
+  double Tj[kMaxDeg + 1];
+  Tj[0] = 1.0;
+  Tj[1] = that;
+  for (int j = 2; j <= d; ++j) Tj[j] = 2.0 * that * Tj[j - 1] - Tj[j - 2];
   int base = 0;
   for (int j = 1; j <= d; ++j) {
     int rb = 0;
-    if (j < d && cheb_T(j, that) / cheb_T(base, that) > rho_max) {
+    if (j < d && Tj[j] / Tj[base] > rho_max) {
       rb = 1;
       base = j;
     }
