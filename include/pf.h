@@ -181,11 +181,19 @@ pf_status pf_rayleigh_ritz(pf_ctx ctx, const void* A, int64_t lda, const void* U
 pf_status pf_spectral_op(pf_ctx ctx, pf_op op, double thr, const double* theta, double* f,
                          int32_t* rank, pf_stream stream);
 
+/* The rank-p rebuild alone (§8(b)'s optional dense output of the spectral operator): X = V diag(f)
+ * V^T, written to X (n_local x n, ldx >= n; every entry).  V: local rows (n_local x p, ldv even,
+ * 16-byte aligned), f: device double[p] (e.g. from pf_spectral_op).  fp64 dtypes; DMMA on
+ * symmetric tile pairs (the PFPG update kernel with no mask and tau = 0). */
+pf_status pf_rebuild(pf_ctx ctx, const double* V, int64_t ldv, const double* f, double* X,
+                     int64_t ldx, pf_stream stream);
+
 /* PFPG update for F = 1/2 ||P_Omega(X - M)||_F^2, M = W W^T, R = mu ||.||_* (eq:pfpg1 P:338-341):
  * X = V diag(f) V^T, A_out = X - tau * Omega o (X - M)  (n_local x n, lda_out).
  * omega: packed row-major symmetric bitmask, uint32 words, bit (j & 31) of word [i][j >> 5],
  * row pitch ldo words (>= ceil(n/32)), local rows.  W: n x r FULL (all rows), ldw >= r,
- * 0 <= r <= 64.  mu >= 0.  obj: device double[2] = {h(X), 1/2 ||P_Omega(X - M)||_F^2} with the
+ * 0 <= r <= 64 (the low-rank factor of M is staged in shared memory next to the V panels; the
+ * BASELINE configs use r = 10 / 50).  mu >= 0.  obj: device double[2] = {h(X), 1/2 ||P_Omega(X - M)||_F^2} with the
  * PFPG objective h(X) = 1/2 ||P_Omega(X - M)||_F^2 + mu sum_i |f_i| (= mu ||X||_* for
  * orthonormal V), summed over all ranks. */
 pf_status pf_prox_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f, double tau,

@@ -57,6 +57,7 @@ def load() -> ctypes.CDLL:
         "pf_svt_filter": [P, P, P, P, P, P, P, P, I64, D, D, P],
         "pf_admm_step": [P, P, I64, P, D, P, I64, P, P, I64, P, P],
         "pf_admm_step_f": [P, P, I64, P, D, P, I64, P, P, I64, P, P],
+        "pf_rebuild": [P, P, I64, P, P, I64, P],
         "pf_perturb": [P, P, I64, P, I64, P],
         "pf_perturb_hash": [P, P, I64, ctypes.c_uint64, I32, D, P],
         "pf_nce_step": [P, P, I64, P, D, P, P, P, P, I64, P, P],
@@ -289,6 +290,11 @@ class Context:
         self._check(self.lib.pf_admm_step(self.h, _ptr(V), _ld(V), _ptr(f), t, _ptr(adj),
                                           _ld(adj), _ptr(deg), _ptr(Z), _ld(Z), _ptr(obj),
                                           _stream(stream)), "pf_admm_step")
+
+    def rebuild(self, V, f, X, stream=None):
+        """X = V diag(f) V^T (dense, local rows; pf_rebuild)."""
+        self._check(self.lib.pf_rebuild(self.h, _ptr(V), _ld(V), _ptr(f), _ptr(X), _ld(X),
+                                        _stream(stream)), "pf_rebuild")
 
     def admm_step_f(self, Q, F, t, adj, deg, Z, obj, stream=None):
         """PFAM update with W = Q F Q^T (pf_admm_step_f)."""

@@ -60,6 +60,7 @@ struct pf_ctx_s {
   double* lz_v0 = nullptr;                     // bottom Ritz vector of the last refresh (n_local)
   bool lz_have_v0 = false;
   double* rb_part = nullptr;
+  double* rb_obj = nullptr;                    // [2] objective scratch of pf_rebuild
   int* rb_cnt = nullptr;
   int* shift_flag = nullptr;
   ChebGemmPlan plan;
@@ -296,6 +297,7 @@ static pf_status alloc_all(pf_ctx ctx) {
   ok &= A((void**)&ctx->rb_part,
           std::max<size_t>((size_t)rebuild_blocks((int)nl, (int)n) * 2, 128 * 36) * 8);
   ok &= A((void**)&ctx->rb_cnt, 16);
+  ok &= A((void**)&ctx->rb_obj, 16);
   if (!f32) {
     ok &= A((void**)&ctx->svt_part, (size_t)svt_sample_blocks((int)nl) * 8);
     ok &= A((void**)&ctx->svt_cnt, 16);
@@ -545,7 +547,7 @@ pf_status pf_destroy(pf_ctx ctx) {
                   ctx->A8,     ctx->a8_rscale, ctx->Y8,       ctx->y8_cscale, ctx->y8_cmax,
                   ctx->i8_acc, ctx->i8_part, ctx->i8_cnt, ctx->svt_part, ctx->svt_cnt,
                   ctx->lz_sym_ws, ctx->a8_E, ctx->a8_wa, ctx->a8_wmax, ctx->jac_theta,
-                  ctx->lz_v0};
+                  ctx->lz_v0, ctx->rb_obj};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete ctx;
@@ -1145,6 +1147,24 @@ pf_status pf_prox_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f
   // obj[0] (the fit) is a sum over row blocks; obj[1] = sum |f| is replicated
   PF_TRY(allreduce(ctx, obj, 1, st));
   PF_CU(pfpg_obj_finish_launch(obj, mu, st));
+  return PF_OK;
+}
+
+pf_status pf_rebuild(pf_ctx ctx, const double* V, int64_t ldv, const double* f, double* X,
+                     int64_t ldx, pf_stream stream) {
+  if (!ctx || !V || !f || !X) return PF_ERR_ARG;
+  if (!is_fp64(ctx)) return PF_ERR_UNSUPPORTED;
+  if (ldv < ctx->p || (ldv & 1) || !aligned16(V) || ldx < ctx->n) return PF_ERR_DIM;
+  cudaStream_t st = (cudaStream_t)stream;
+  const double* Vf;
+  int64_t ldf;
+  PF_TRY(full_V(ctx, V, ldv, &Vf, &ldf, st));
+  // the PFPG update kernel with no mask and tau = 0: X - 0 * Omega o (X - M) = X (its objective
+  // partials land in scratch)
+  PF_CU(prox_launch(Vf, ldf, V, ldv, f, 0.0, nullptr, 0, nullptr, 0, 0, X, ldx, (int)ctx->n_local,
+                    (int)ctx->n, (int)ctx->row0, ctx->p, ctx->rb_obj, ctx->rb_part, ctx->rb_cnt,
+                    ctx->VFbuf, st));
+  if (X == ctx->a8_src) iterate_written(ctx);
   return PF_OK;
 }
 

@@ -317,7 +317,8 @@ __global__ void __launch_bounds__(kRbThreads, 2) rebuild_kernel(const RbArgs a) 
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int li = i0 + wm * 32 + mt * 16 + g8 + 8 * h;
-      wbits[mt][h] = li < a.n_rows ? __ldg(a.bits + (size_t)li * a.ldb + ((j0 + wn * kWn) >> 5))
+      wbits[mt][h] = (li < a.n_rows && a.bits)  // no mask (pf_rebuild): every bit 0
+                         ? __ldg(a.bits + (size_t)li * a.ldb + ((j0 + wn * kWn) >> 5))
                                    : 0u;
     }
   cp_async_wait_all();

@@ -264,3 +264,18 @@ def test_trajectory_config3_reduced():
 
 def test_trajectory_config4_shape_reduced():
     _traj(reduced(CONFIGS[4], n=1200, iters=8, omega_prob=0.1))
+
+
+@pytest.mark.parametrize("n,p", [(777, 32), (1000, 64), (650, 128), (300, 16)])
+def test_rebuild_dense_matches_definition(n, p):
+    """pf_rebuild (SURVEY §8(b)'s optional dense output of the spectral operator): X = V diag(f)
+    V^T element by element, both triangles, ragged n."""
+    rng = np.random.default_rng(n + p)
+    V = rng.standard_normal((n, p))
+    f = rng.standard_normal(p) * (rng.random(p) > 0.3)
+    ctx = _ctx(n, p)
+    X = torch.full((n, n + 6), 7.0, dtype=torch.float64, device="cuda")[:, :n]   # ldx > n
+    ctx.rebuild(_dev(V), _dev(f), X)
+    ref = (V * f) @ V.T
+    got = X.cpu().numpy()
+    assert np.max(np.abs(got - ref)) <= 1e-13 * np.abs(ref).max() * p
