@@ -50,6 +50,21 @@ def test_argument_errors_are_synchronous_without_gpu():
     assert lib.pf_invalidate(None) == 1
     assert lib.pf_matmul(None, None, 0, None, 0, None, 0, None) == 1
     assert lib.pf_status_string(3) == b"PF_ERR_INTERVAL"
+    # round-2 entries: null contexts / invalid arguments fail before any device work
+    loop = ctypes.c_void_p()
+    assert lib.pf_loop_create(0, ctypes.byref(loop)) == 1            # world < 1
+    assert lib.pf_loop_create(17, ctypes.byref(loop)) == 1           # world > 16
+    assert lib.pf_create_loop(100, 16, 4, 0, None, 0, ctypes.byref(h)) == 1  # no hub
+    assert lib.pf_loop_destroy(None) == 1
+    d = ctypes.c_int32(0)
+    assert lib.pf_schedule_degree(None, 1.0, 0, ctypes.byref(d)) == 1
+    assert lib.pf_svt_kick(None, None, 0, 1.0, 1.0, 1.0, None, None) == 1
+    assert lib.pf_svt_filter(None, None, None, None, None, None, None, None, 0, 1.0, 0.1,
+                             None) == 1
+    assert lib.pf_rebuild(None, None, 0, None, None, 0, None) == 1
+    assert lib.pf_admm_step_f(None, None, 0, None, 1.0, None, 0, None, None, 0, None, None) == 1
+    cnt = ctypes.c_int32(0)
+    assert lib.pf_overlap_timeline(None, None, None, 0, ctypes.byref(cnt)) == 1
 
 
 def test_product_does_not_import_oracle():

@@ -106,3 +106,17 @@ def test_lanczos_warm_start_trajectory(cfg, tol):
     """NEXT-2 lambda_min tracking (reading R29): refreshes after the first restart a short
     Lanczos from the previous bottom Ritz vector (pf_lanczos with v0 = NULL) on both sides."""
     _traj(cfg, tol)
+
+
+def test_schedule_degree_matches_oracle_and_rejects_bad_arguments():
+    """pf_schedule_degree (thm:conv1 schedule in the library) against the oracle's own
+    degree_schedule for a range of k, and its synchronous argument errors."""
+    from paper_1904_10585_b200._lib import Context, PFError
+    c = Context(256, 16, 3)
+    for cc in (0.0, 1.5, 3.0):
+        for k in (0, 1, 5, 40, 1000, 10**6):
+            assert c.schedule_degree(cc, k) == O.degree_schedule(3, cc, k), (cc, k)
+    with pytest.raises(PFError, match="PF_ERR_ARG"):
+        c.schedule_degree(-1.0, 3)
+    with pytest.raises(PFError, match="PF_ERR_ARG"):
+        c.schedule_degree(30.0, 10**9)          # d_k > 64

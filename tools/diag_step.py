@@ -45,7 +45,8 @@ def main(cfg_id=3, iters=14, **over):
                 ctx.rr_ns(s.A, s.U, s.op, s.thr, s.F, s.rank, s.ns_it, st)
                 ev[4].record(st)
                 ev[5].record(st)
-                ctx.admm_step_f(s.U, s.F, cfg.t, s.adj, s.deg, s.A, s.obj, st)
+                if cfg.mode == "pfam":
+                    ctx.admm_step_f(s.U, s.F, cfg.t, s.adj, s.deg, s.A, s.obj, st)
                 ev[6].record(st)
                 s.k += 1
                 torch.cuda.synchronize()
