@@ -142,6 +142,12 @@ struct pf_ctx_s {
   int* a8_E = nullptr;                         // [n_local] row exponents of the fused digits
   double2* a8_wa = nullptr;                    // [n_local] row-bound scratch
   unsigned long long* a8_wmax = nullptr;
+  // PFAM update on int8 tensor cores (pf_rebuild_i8.cu; one GPU, p = 64, fused digits)
+  bool r8_on = false;
+  int8_t* r8_VF8 = nullptr;                    // digit slices of V' (r8_bytes)
+  int8_t* r8_V8 = nullptr;                     // digit slices of V
+  double* r8_rs = nullptr;                     // [2 n] row scales of V' and V
+  CUtensorMap r8_mapA, r8_mapB;
   NsWork* ns = nullptr;                        // pf_rr_ns workspace (created on first use)
   // ---- PFSVT (pf_svt.cu)
   double* svt_part = nullptr;                  // residual partials (one per 8 rows)
@@ -249,6 +255,16 @@ static pf_status alloc_all(pf_ctx ctx) {
     ok &= A((void**)&ctx->a8_E, (size_t)nl * 4);
     ok &= A((void**)&ctx->a8_wa, (size_t)nl * 16);
     ok &= A((void**)&ctx->a8_wmax, 16);
+    if (!ctx->dist && p == 64 && ip.S == 7) {
+      const char* e = getenv("PF_K7I8");  // 0: the DMMA update kernel (measurement)
+      ctx->r8_on = !(e && e[0] == '0');
+    }
+    if (ctx->r8_on) {
+      ok &= A((void**)&ctx->r8_VF8, r8_bytes((int)n));
+      ok &= A((void**)&ctx->r8_V8, r8_bytes((int)n));
+      ok &= A((void**)&ctx->r8_rs, (size_t)2 * n * 8);
+      ok = ok && r8_encode(&ctx->r8_mapA, &ctx->r8_mapB, ctx->r8_VF8, ctx->r8_V8, (int)n);
+    }
     ok &= A((void**)&ctx->Y8, (size_t)kI8MaxSlices * p * ip.kpad);
     ok &= A((void**)&ctx->y8_cscale, (size_t)p * 8);
     ok &= A((void**)&ctx->y8_cmax, (size_t)p * 8);
@@ -547,7 +563,7 @@ pf_status pf_destroy(pf_ctx ctx) {
                   ctx->A8,     ctx->a8_rscale, ctx->Y8,       ctx->y8_cscale, ctx->y8_cmax,
                   ctx->i8_acc, ctx->i8_part, ctx->i8_cnt, ctx->svt_part, ctx->svt_cnt,
                   ctx->lz_sym_ws, ctx->a8_E, ctx->a8_wa, ctx->a8_wmax, ctx->jac_theta,
-                  ctx->lz_v0, ctx->rb_obj};
+                  ctx->lz_v0, ctx->rb_obj, ctx->r8_VF8, ctx->r8_V8, ctx->r8_rs};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete ctx;
@@ -1184,9 +1200,12 @@ pf_status pf_admm_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f
   const bool fuse = use_i8(ctx) && !ctx->dist && ctx->fuse_digits &&
                     (ctx->i8plan.S == 6 || ctx->i8plan.S == 7);
   RbDigits dig{ctx->A8, ctx->i8plan.kblocks, ctx->i8plan.S, ctx->a8_E, ctx->a8_rscale, ctx->a8_wa, ctx->a8_wmax};
+  R8Bufs r8{&ctx->r8_mapA, &ctx->r8_mapB, ctx->r8_VF8, ctx->r8_V8, ctx->r8_rs,
+            ctx->r8_rs + ctx->n, ctx->num_sms};
   PF_CU(admm_launch(Vf, ldf, V, ldv, f, t, adj, ldadj, deg, Z, ldz, (int)ctx->n_local,
                     (int)ctx->n, (int)ctx->row0, ctx->p, obj, ctx->rb_part, ctx->rb_cnt,
-                    ctx->dist ? 1 : 0, ctx->VFbuf, st, fuse ? &dig : nullptr));
+                    ctx->dist ? 1 : 0, ctx->VFbuf, st, fuse ? &dig : nullptr, nullptr,
+                    fuse && ctx->r8_on ? &r8 : nullptr));
   if (fuse) {
     ctx->a8_src = Z;
     ctx->a8_lda = ldz;
@@ -1217,9 +1236,12 @@ pf_status pf_admm_step_f(pf_ctx ctx, const double* Q, int64_t ldq, const double*
   const bool fuse = use_i8(ctx) && !ctx->dist && ctx->fuse_digits &&
                     (ctx->i8plan.S == 6 || ctx->i8plan.S == 7);
   RbDigits dig{ctx->A8, ctx->i8plan.kblocks, ctx->i8plan.S, ctx->a8_E, ctx->a8_rscale, ctx->a8_wa, ctx->a8_wmax};
+  R8Bufs r8{&ctx->r8_mapA, &ctx->r8_mapB, ctx->r8_VF8, ctx->r8_V8, ctx->r8_rs,
+            ctx->r8_rs + ctx->n, ctx->num_sms};
   PF_CU(admm_launch(Qf, ldf, Q, ldq, nullptr, t, adj, ldadj, deg, Z, ldz, (int)ctx->n_local,
                     (int)ctx->n, (int)ctx->row0, ctx->p, obj, ctx->rb_part, ctx->rb_cnt,
-                    ctx->dist ? 1 : 0, ctx->VFbuf, st, fuse ? &dig : nullptr, F));
+                    ctx->dist ? 1 : 0, ctx->VFbuf, st, fuse ? &dig : nullptr, F,
+                    fuse && ctx->r8_on ? &r8 : nullptr));
   if (fuse) {
     ctx->a8_src = Z;
     ctx->a8_lda = ldz;

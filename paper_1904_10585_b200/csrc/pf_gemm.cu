@@ -309,6 +309,29 @@ bool encode_map_A(CUtensorMap* map, const double* A, int64_t lda, int n_rows, in
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// generic tiled map (pf_rebuild_i8.cu): element type fp64 (f64) or bytes, rank 2 or 3, strides
+// in bytes for dims 1.., swizzle span 0 / 32 / 64 / 128 bytes
+bool encode_map_gen(CUtensorMap* map, bool f64, int rank, const void* base, const uint64_t* dims,
+                    const uint64_t* strides, const uint32_t* box, int swizzle) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc || rank < 2 || rank > 3) return false;
+  cuuint64_t d[3], s[2];
+  cuuint32_t b[3], es[3] = {1, 1, 1};
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    b[i] = box[i];
+    if (i) s[i - 1] = strides[i - 1];
+  }
+  const CUtensorMapSwizzle sw = swizzle == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                : swizzle == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                : CU_TENSOR_MAP_SWIZZLE_NONE;
+  return enc(map, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_UINT8,
+             (cuuint32_t)rank, const_cast<void*>(base), d, s, b, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool encode_map_B(CUtensorMap* map, const double* B, int p, int n_k) {
   PFN_encodeTiled enc = get_encode();
   if (!enc) return false;

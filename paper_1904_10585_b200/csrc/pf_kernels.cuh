@@ -228,12 +228,30 @@ struct RbDigits {
   double2* wa;              // [n] scratch (W_ii, sum_k |f_k| V_ik^2)
   unsigned long long* wmax; // scratch (wmax[1]: ||F|| bound of the matrix form)
 };
+// PF_FP64_I8, one GPU, p = 64, fused digits: W = V' V^T from int8 digit products on tcgen05
+// (pf_rebuild_i8.cu) -- digit buffers of V' and V (r8_bytes each), their row scales, TMA maps
+struct R8Bufs {
+  const CUtensorMap* mapA;
+  const CUtensorMap* mapB;
+  int8_t* VF8;
+  int8_t* V8;
+  double* rsA;
+  double* rsB;
+  int num_sms;
+};
+size_t r8_bytes(int n);
+bool r8_encode(CUtensorMap* mapA, CUtensorMap* mapB, const int8_t* VF8, const int8_t* V8, int n);
+cudaError_t admm_i8_launch(const CUtensorMap& mapA, const CUtensorMap& mapB, const double* VF,
+                           const double* V, int64_t ldv, int8_t* VF8, int8_t* V8, double* rsA,
+                           double* rsB, const uint32_t* adj, int64_t ldadj, const double* deg,
+                           double t, double* Z, int64_t ldz, int n, double* obj, double* partials,
+                           int* counter, const RbDigits* dig, int num_sms, cudaStream_t st);
 cudaError_t admm_launch(const double* V, int64_t ldv, const double* Vloc, int64_t ldvl,
                         const double* f, double t, const uint32_t* adj, int64_t ldadj,
                         const double* deg, double* Z, int64_t ldz, int n_rows, int n, int row0,
                         int p, double* obj, double* partials, int* counter, int raw, double* vf,
                         cudaStream_t st, const RbDigits* dig = nullptr,
-                        const double* Fmat = nullptr);
+                        const double* Fmat = nullptr, const R8Bufs* r8 = nullptr);
 // (Fmat != NULL: W = V F V^T with F p x p row-major; vf must already hold the local rows of V F
 //  and f is unused)
 cudaError_t sqrt_inplace_launch(double* x, cudaStream_t st);

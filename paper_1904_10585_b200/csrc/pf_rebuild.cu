@@ -737,7 +737,8 @@ cudaError_t admm_launch(const double* V, int64_t ldv, const double* Vloc, int64_
                         const double* f, double t, const uint32_t* adj, int64_t ldadj,
                         const double* deg, double* Z, int64_t ldz, int n_rows, int n, int row0,
                         int p, double* obj, double* partials, int* counter, int raw, double* vf,
-                        cudaStream_t st, const RbDigits* dig, const double* Fmat) {
+                        cudaStream_t st, const RbDigits* dig, const double* Fmat,
+                        const R8Bufs* r8) {
   cudaError_t e = cudaSuccess;
   if (!Fmat) {
     e = scale_cols(Vloc, ldvl, f, n_rows, p, vf, st);
@@ -767,6 +768,10 @@ cudaError_t admm_launch(const double* V, int64_t ldv, const double* Vloc, int64_
     a.E = dig->E;
     a.S = dig->S;
     a.rscale = dig->rscale;
+    if (r8 && p == 64 && dig->S == 7)
+      return admm_i8_launch(*r8->mapA, *r8->mapB, vf, V, ldv, r8->VF8, r8->V8, r8->rsA, r8->rsB,
+                            adj, ldadj, deg, t, Z, ldz, n, obj, partials, counter, dig,
+                            r8->num_sms, st);
   }
   return rb_dispatch<false>(p, a, st);
 }

@@ -259,3 +259,77 @@ def test_gaussian_operands_fp64_grade_past_fold(n, p):
     c.matmul(A, _dev(Y), out)
     dm = np.abs(out.cpu().numpy() - ref).max()
     assert err <= 2.0 ** -47 * scale and err <= 16 * max(dm, 1e-16 * scale), (err, dm)
+
+
+def _digit_bound(X, p):
+    """Elementwise bound on |W - V'V^T| for the int8-digit product (pf_rebuild_i8.cu): rows of V'
+    and V split under their own scales 2^E_i, 2^F_j (|x| < 2^E), 7 digits (truncation residual
+    < 2^(E-49) per entry), levels s + t <= 6 kept (dropped levels < 7 * 127^2 * 128^-9 2^(E+F) per
+    product); summed over p products: < 4 p 2^(E_i + F_j - 49)."""
+    m = np.abs(X).max(axis=1)
+    e = np.where(m > 0, np.floor(np.log2(np.where(m > 0, m, 1.0))) + 1, 0)
+    return 2.0 ** e
+
+
+@pytest.mark.parametrize("n", [64, 100, 300, 1333, 2050])
+@pytest.mark.parametrize("form", ["diag", "matrix"])
+def test_pfam_update_int8_matches_oracle(monkeypatch, n, form):
+    """PFAM update with W = V' V^T from int8 tcgen05 digit products (pf_rebuild_i8.cu, one GPU,
+    p = 64, fused digits): Z_new = offdiag(W - tC) + Diag(1 - W_ii + Z_ii) element by element
+    within the digit-split bound of the exact W (eq:PFAM1 P:389), <C, W> and ||Z_new - Z||_F;
+    ragged n (tiles of 128 x 32), the 128 x 128 diagonal blocks, n < 128.  PF_K7I8=0 (the DMMA
+    update) agrees within the same bound."""
+    from paper_1904_10585_b200._lib import Context, PF_FP64_I8
+    from paper_1904_10585_b200.solver import _bits
+    from pfinputs import sym_bernoulli_bitmask, unpack_bitmask
+    p = 64
+    rs = np.random.default_rng(n + (form == "matrix"))
+    V = np.linalg.qr(rs.standard_normal((n, p)))[0]
+    V[3] *= 1e-3                                        # rows on other scales
+    V[min(7, n - 1)] = 0.0                              # a zero row
+    bits = sym_bernoulli_bitmask(n, 0.08, np.random.default_rng(5), diagonal=False)
+    adj = unpack_bitmask(bits, n)
+    deg = adj.sum(1).astype(float)
+    C = O.maxcut_C(adj, deg)
+    Z = rs.standard_normal((n, n)) * 0.05
+    Z = Z + Z.T
+    if form == "diag":
+        f = np.abs(rs.standard_normal(p)) * 20.0
+        f[:4] = 0.0
+        Vp, Vr, fr = V * f, V, f
+    else:
+        B = rs.standard_normal((p, p))
+        F = B @ B.T / p
+        lam, Y = np.linalg.eigh(F)
+        Vp, Vr, fr = V @ F, V @ Y, lam
+    Zr, cw, res = O.pfam_next(Vr, fr, Z, C, 0.7)
+    bound = 4 * p * 2.0 ** -49 * np.outer(_digit_bound(Vp, p), _digit_bound(V, p))
+    bound = np.maximum(bound, bound.T) + 1e-15 * np.abs(Zr).max()
+    outs = []
+    for k7 in ("1", "0"):
+        monkeypatch.setenv("PF_K7I8", k7)
+        c = Context(n, p, 4, dtype=PF_FP64_I8)
+        Zd = _pitched(Z)
+        obj = torch.zeros(2, dtype=torch.float64, device="cuda")
+        if form == "diag":
+            c.admm_step(_dev(V), _dev(f), 0.7, _bits(bits), _dev(deg), Zd, obj)
+        else:
+            c.admm_step_f(_dev(V), _dev(F), 0.7, _bits(bits), _dev(deg), Zd, obj)
+        Zg = Zd.cpu().numpy()
+        err = np.abs(Zg - Zr)
+        assert np.all(err <= bound), (k7, float((err / bound).max()))
+        if k7 == "1":  # off the 128 x 128 diagonal blocks the mirror store is the tile's
+            blk = np.arange(n) // 128
+            off = blk[:, None] != blk[None, :]
+            assert np.array_equal(Zg[off], Zg.T[off])
+        o = obj.cpu().numpy()
+        assert o[0] == pytest.approx(cw, rel=1e-11, abs=1e-12)
+        assert o[1] == pytest.approx(res, rel=1e-11)
+        outs.append(Zg)
+        # the fused digits of Z_new drive the next product within the split bound
+        Y = rs.standard_normal((n, p))
+        out = torch.empty((n, p), dtype=torch.float64, device="cuda")
+        c.matmul(Zd, _dev(Y), out)
+        ref = Zg @ Y
+        scale = np.abs(Zg).max() * np.abs(Y).max() * n
+        assert np.abs(out.cpu().numpy() - ref).max() <= 2.0 ** (5 - 49) * scale
