@@ -146,8 +146,8 @@ struct pf_ctx_s {
   bool r8_on = false;
   int8_t* r8_VF8 = nullptr;                    // digit slices of V' (r8_bytes)
   int8_t* r8_V8 = nullptr;                     // digit slices of V
-  double* r8_rs = nullptr;                     // [2 n] row scales of V' and V
-  CUtensorMap r8_mapA, r8_mapB;
+  double* r8_rs = nullptr;                     // [2 x n padded to 128] row scales of V', V
+  CUtensorMap r8_maps[4];
   NsWork* ns = nullptr;                        // pf_rr_ns workspace (created on first use)
   // ---- PFSVT (pf_svt.cu)
   double* svt_part = nullptr;                  // residual partials (one per 8 rows)
@@ -262,8 +262,8 @@ static pf_status alloc_all(pf_ctx ctx) {
     if (ctx->r8_on) {
       ok &= A((void**)&ctx->r8_VF8, r8_bytes((int)n));
       ok &= A((void**)&ctx->r8_V8, r8_bytes((int)n));
-      ok &= A((void**)&ctx->r8_rs, (size_t)2 * n * 8);
-      ok = ok && r8_encode(&ctx->r8_mapA, &ctx->r8_mapB, ctx->r8_VF8, ctx->r8_V8, (int)n);
+      ok &= A((void**)&ctx->r8_rs, (size_t)2 * ip.mtiles * 128 * 8);
+      ok = ok && r8_encode(ctx->r8_maps, ctx->r8_VF8, ctx->r8_V8, ctx->A8, (int)n, ip.kblocks);
     }
     ok &= A((void**)&ctx->Y8, (size_t)kI8MaxSlices * p * ip.kpad);
     ok &= A((void**)&ctx->y8_cscale, (size_t)p * 8);
@@ -1200,8 +1200,8 @@ pf_status pf_admm_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f
   const bool fuse = use_i8(ctx) && !ctx->dist && ctx->fuse_digits &&
                     (ctx->i8plan.S == 6 || ctx->i8plan.S == 7);
   RbDigits dig{ctx->A8, ctx->i8plan.kblocks, ctx->i8plan.S, ctx->a8_E, ctx->a8_rscale, ctx->a8_wa, ctx->a8_wmax};
-  R8Bufs r8{&ctx->r8_mapA, &ctx->r8_mapB, ctx->r8_VF8, ctx->r8_V8, ctx->r8_rs,
-            ctx->r8_rs + ctx->n, ctx->num_sms};
+  R8Bufs r8{ctx->r8_maps, ctx->r8_VF8, ctx->r8_V8, ctx->r8_rs,
+            ctx->r8_rs + (size_t)ctx->i8plan.mtiles * 128, ctx->num_sms};
   PF_CU(admm_launch(Vf, ldf, V, ldv, f, t, adj, ldadj, deg, Z, ldz, (int)ctx->n_local,
                     (int)ctx->n, (int)ctx->row0, ctx->p, obj, ctx->rb_part, ctx->rb_cnt,
                     ctx->dist ? 1 : 0, ctx->VFbuf, st, fuse ? &dig : nullptr, nullptr,
@@ -1236,8 +1236,8 @@ pf_status pf_admm_step_f(pf_ctx ctx, const double* Q, int64_t ldq, const double*
   const bool fuse = use_i8(ctx) && !ctx->dist && ctx->fuse_digits &&
                     (ctx->i8plan.S == 6 || ctx->i8plan.S == 7);
   RbDigits dig{ctx->A8, ctx->i8plan.kblocks, ctx->i8plan.S, ctx->a8_E, ctx->a8_rscale, ctx->a8_wa, ctx->a8_wmax};
-  R8Bufs r8{&ctx->r8_mapA, &ctx->r8_mapB, ctx->r8_VF8, ctx->r8_V8, ctx->r8_rs,
-            ctx->r8_rs + ctx->n, ctx->num_sms};
+  R8Bufs r8{ctx->r8_maps, ctx->r8_VF8, ctx->r8_V8, ctx->r8_rs,
+            ctx->r8_rs + (size_t)ctx->i8plan.mtiles * 128, ctx->num_sms};
   PF_CU(admm_launch(Qf, ldf, Q, ldq, nullptr, t, adj, ldadj, deg, Z, ldz, (int)ctx->n_local,
                     (int)ctx->n, (int)ctx->row0, ctx->p, obj, ctx->rb_part, ctx->rb_cnt,
                     ctx->dist ? 1 : 0, ctx->VFbuf, st, fuse ? &dig : nullptr, F,

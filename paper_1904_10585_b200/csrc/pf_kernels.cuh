@@ -231,8 +231,7 @@ struct RbDigits {
 // PF_FP64_I8, one GPU, p = 64, fused digits: W = V' V^T from int8 digit products on tcgen05
 // (pf_rebuild_i8.cu) -- digit buffers of V' and V (r8_bytes each), their row scales, TMA maps
 struct R8Bufs {
-  const CUtensorMap* mapA;
-  const CUtensorMap* mapB;
+  const CUtensorMap* maps;  // [4]: V' digits, V digits, Z_new digit tile / mirror boxes (r8_encode)
   int8_t* VF8;
   int8_t* V8;
   double* rsA;
@@ -240,11 +239,13 @@ struct R8Bufs {
   int num_sms;
 };
 size_t r8_bytes(int n);
-bool r8_encode(CUtensorMap* mapA, CUtensorMap* mapB, const int8_t* VF8, const int8_t* V8, int n);
-cudaError_t admm_i8_launch(const CUtensorMap& mapA, const CUtensorMap& mapB, const double* VF,
-                           const double* V, int64_t ldv, int8_t* VF8, int8_t* V8, double* rsA,
-                           double* rsB, const uint32_t* adj, int64_t ldadj, const double* deg,
-                           double t, double* Z, int64_t ldz, int n, double* obj, double* partials,
+bool r8_encode(CUtensorMap* maps, const int8_t* VF8, const int8_t* V8, const int8_t* A8, int n,
+               int KB);
+bool r8_usable(const double* Z, int64_t ldz);  // TMA on Z: even pitch, 16-byte aligned base
+cudaError_t admm_i8_launch(const CUtensorMap* maps, const double* VF, const double* V,
+                           int64_t ldv, int8_t* VF8, int8_t* V8, double* rsA, double* rsB,
+                           const uint32_t* adj, int64_t ldadj, const double* deg, double t,
+                           double* Z, int64_t ldz, int n, double* obj, double* partials,
                            int* counter, const RbDigits* dig, int num_sms, cudaStream_t st);
 cudaError_t admm_launch(const double* V, int64_t ldv, const double* Vloc, int64_t ldvl,
                         const double* f, double t, const uint32_t* adj, int64_t ldadj,

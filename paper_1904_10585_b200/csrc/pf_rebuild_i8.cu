@@ -1,28 +1,32 @@
 // pf_rebuild_i8.cu -- the PFAM update (step a6, eq:PFAM1 P:389 with the corrected prox, reading
 // R1) on one GPU for PF_FP64_I8 contexts, with the rank-p product W = V' V^T formed from EXACT
-// int8 tensor-core products (tcgen05 kind::i8) of 7-bit digit slices -- the same Ozaki-style
-// splitting as the filter GEMM K1-i8 (pf_gemm_i8.cu):
+// int8 tensor-core products (tcgen05 kind::i8) of 7-bit digit slices -- the same splitting as the
+// filter GEMM K1-i8 (pf_gemm_i8.cu):
 //
 //     V' = V diag(f) (or Q F, pf_admm_step_f),  V'_i = 2^{E_i} sum_s d_s 128^-(s+1) + r,
 //     V_j = 2^{F_j} sum_t e_t 128^-(t+1) + r',   W_ij = 2^{E_i + F_j} sum_l 128^-(l+2) D_l[i][j],
 //     D_l = sum_{s+t=l} A_s B_t^T  (exact int32, K = p = 64 digits: one 64-byte k-block)
 //
-// then Z_new = offdiag(W - tC) + Diag(1 - W_ii + Z_ii), written with its mirror and (fused
-// digits) the digit slices of Z_new for the next filter.  Why: the fp64 DMMA formulation
-// (rebuild_kernel) spends ~0.46 ms of DMMA pipe time on W at config 3 and cannot overlap it with
-// the 5.1 GB HBM stream inside its CTAs (1.64 ms, DRAM ~37%); here W costs ~0.18 ms of tensor
-// time issued by one thread, accumulates in TMEM (two buffers), and 8 update warps do nothing
-// but the memory-bound update while the tensor core fills the other buffer.
+// then Z_new = offdiag(W - tC) + Diag(1 - W_ii + Z_ii), written with its mirror and the digit
+// slices of Z_new for the next filter (one scale 2^Eg, DESIGN.md §4 "fused digits").  Why: the
+// fp64 DMMA formulation (rebuild_kernel) spends ~0.46 ms of DMMA pipe time on W at config 3 and
+// its CTAs cannot overlap it with the 5.1 GB HBM stream; here W costs ~0.18 ms of tensor time
+// issued by one thread into TMEM, and every byte of the stream moves by TMA: Z_old tiles are
+// loaded into shared memory ahead of use, Z_new (tile and mirror) and its digit slices are
+// staged in shared memory and written by TMA stores, so the update warps only compute.
 //
-// Tiles: 128 rows (a block I of V') x 32 columns (a block J of V), J * 32 >= I * 128 (upper part;
-// the 4 tiles J = 4I .. 4I+3 cover the 128 x 128 diagonal block, both triangles, no mirror).
-// Warp 0: TMA (A = the 7 slices of V' block I, 56 KB, reloaded when I changes; B = the 7 slices
-// of V block J, 14 KB, 4-stage ring).  Warp 1: 14 MMAs per tile (A_s x [B_0 .. B_{6-s}], N =
-// 32 (7 - s), levels s .. 6 at TMEM columns 32 s ..).  Warps 4-11: TMEM lane = tile row,
-// 16 columns each: levels combined in fp64, the update, fp64 stores (tile rows, and mirror rows
-// coalesced across the warp), digit slices (tile words directly, mirror words by 4 x 4 byte
-// transposes across 4 lanes).  Deterministic sums (fixed per-thread order, CTA partials summed
-// in CTA order by the last CTA).
+// Tiles: 128 rows (a block I of V') x 32 columns (a block J of V), J >= 4 I (upper part; the 4
+// tiles J = 4I .. 4I+3 cover the 128 x 128 diagonal block, both triangles, no mirror).
+//   warp 0   TMA loads: A = the 7 slices of V' block I (56 KB, reloaded when I changes), B = the
+//            7 slices of V block J (14 KB), Z_old tile (2 x 16 KB boxes, SWIZZLE_128B, 2 buffers)
+//   warp 1   14 MMAs per tile (A_s x [B_0 .. B_{6-s}], N = 32 (7 - s)): level l at TMEM column
+//            32 l of one of two 256-column accumulators
+//   warp 2   TMEM allocation
+//   warp 3   TMA stores: Z_new tile (from the Z_old buffer, updated in place), mirror tile, digit
+//            slices of both; releases the buffers when the stores have read them
+//   warps 4-11  TMEM lane = tile row r, 16 columns (h): levels combined in fp64, the update,
+//            Z_new in place, the mirror (transposed) and the digit slices into staging
+// Deterministic sums: fixed per-thread order, CTA partials summed in CTA order by the last CTA.
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -34,13 +38,20 @@
 
 namespace pf {
 
-constexpr int kR8S = 7;                       // digit slices of V' and V
-constexpr int kR8M = 128, kR8N = 32;          // tile
-constexpr int kR8BS = 4;                      // B ring stages
-constexpr int kR8Threads = 384;               // w0 TMA, w1 MMA, w2 TMEM, w3 idle, w4..11 update
-constexpr int kR8A = kR8S * 8192;             // A bytes (7 slices x 128 rows x 64 B)
-constexpr int kR8B = kR8S * 2048;             // B bytes per stage (7 slices x 32 rows x 64 B)
-constexpr int kR8Smem = 1024 + kR8A + kR8BS * kR8B + 256;
+constexpr int kR8S = 7;                        // digit slices of V', V and Z_new
+constexpr int kR8M = 128, kR8N = 32;           // tile
+constexpr int kR8Threads = 384;
+constexpr int kOffA = 0;                       // 7 x 128 x 64 B
+constexpr int kOffB = kOffA + kR8S * 8192;     // 7 x 32 x 64 B
+constexpr int kOffZ = kOffB + kR8S * 2048;     // 2 buffers x 2 boxes {16 fp64, 128 rows}
+constexpr int kOffM = kOffZ + 2 * 32768;       // mirror: 8 boxes {16 fp64, 32 rows}
+constexpr int kOffDt = kOffM + 32768;          // tile digits: box {32 B, 128 rows, 7 slices}
+constexpr int kOffDm = kOffDt + kR8S * 4096;   // mirror digits: 2 boxes {64 B, 32 rows, 7}
+constexpr int kOffBar = kOffDm + 2 * kR8S * 2048;
+constexpr int kR8Smem = kOffBar + 256 + 1024;
+static_assert(kR8Smem <= 232448, "shared memory");
+static_assert(kOffZ % 1024 == 0 && kOffM % 1024 == 0 && kOffDt % 1024 == 0 && kOffDm % 1024 == 0,
+              "swizzled boxes need 1024-byte alignment");
 
 struct R8Args {
   const double* rsA;  // [n] 2^E_i of V' rows
@@ -49,23 +60,25 @@ struct R8Args {
   int64_t ldb;
   const double* deg;
   double tt;
-  double* Z;
-  int64_t ldz;
-  int n, TC, MT;
-  int8_t* A8;         // fused digit output (nullptr: none)
-  int KB, S;
-  const int* E;       // global digit exponent of Z_new
+  int n, TC, MT, KB;
+  const int* E;       // global digit exponent Eg of Z_new
   double* rscale;
   double* partials;
   int* counter;
   double* obj;
 };
 
+struct R8Maps {
+  CUtensorMap a, b;   // V', V digit slices
+  CUtensorMap z, zm;  // Z: boxes {16, 128} (tile, Z_old) and {16, 32} (mirror)
+  CUtensorMap dt, dm; // Z_new digit slices: {32 B, 128, 7} (tile), {64 B, 32, 7} (mirror)
+};
+
 // tile e -> (I, J): rows I of 128 (I < MT), columns J of 32 from 4I to TC - 1; cnt(I) = tiles
 // before row block I = I TC - 2 I (I - 1)
 __device__ __forceinline__ void r8_tile(long long e, int TC, int MT, int& I, int& J) {
   const double b = (double)TC + 2.0;
-  double disc = b * b - 8.0 * (double)e;
+  const double disc = b * b - 8.0 * (double)e;
   int i = (int)floor((b - sqrt(fmax(disc, 0.0))) * 0.25);
   i = max(0, min(MT - 1, i));
   auto cnt = [&](long long x) { return x * TC - 2 * x * (x - 1); };
@@ -75,20 +88,65 @@ __device__ __forceinline__ void r8_tile(long long e, int TC, int MT, int& I, int
   J = 4 * i + (int)(e - cnt(i));
 }
 
+__device__ __forceinline__ void r8_next(int TC, int& I, int& J) {
+  if (++J == TC) {
+    ++I;
+    J = 4 * I;
+  }
+}
+
+// mbarrier wait for the producer / MMA / store warps: back off between polls so the spinning
+// warp leaves its scheduler's issue slots to the update warps
+__device__ __forceinline__ void mbar_wait_idle(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t done;
+  for (;;) {
+    asm volatile(
+        "{\n.reg .pred P1;\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P1;\n}\n"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (done) return;
+    __nanosleep(64);
+  }
+}
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];\n" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1,
+                                             int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];\n" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+
 __global__ void __launch_bounds__(kR8Threads, 1)
-    rebuild_i8_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-                      const R8Args a) {
+    rebuild_i8_kernel(const __grid_constant__ R8Maps m, const R8Args a) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  unsigned char* sA = smem;
-  unsigned char* sB = smem + kR8A;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kR8BS * kR8B);
-  uint64_t* afull = bars;           // A landed
-  uint64_t* aempty = bars + 1;      // MMAs that read A (this row block) complete
-  uint64_t* bfull = bars + 2;       // [4]
-  uint64_t* bempty = bars + 6;      // [4]
-  uint64_t* tfull = bars + 10;      // [2] accumulator buffer complete
-  uint64_t* tempty = bars + 12;     // [2] accumulator buffer drained (8 update warps)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
+  uint64_t* afull = bars;       // A landed
+  uint64_t* aempty = bars + 1;  // the MMAs that read A (this row block) completed
+  uint64_t* bfull = bars + 2;
+  uint64_t* bempty = bars + 3;
+  uint64_t* tfull = bars + 4;   // [2] accumulator complete
+  uint64_t* tempty = bars + 6;  // [2] accumulator drained (8 update warps)
+  uint64_t* zfull = bars + 8;   // [2] Z_old tile landed
+  uint64_t* zempty = bars + 10; // [2] the Z_new stores have read the buffer
+  uint64_t* sfull = bars + 12;  // staging + Z_new written (8 update warps)
+  uint64_t* sempty = bars + 13; // the stores have read the staging
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
   __shared__ double red[32];
   __shared__ int s_last;
@@ -97,19 +155,27 @@ __global__ void __launch_bounds__(kR8Threads, 1)
   if (threadIdx.x == 0) {
     mbar_init(afull, 1);
     mbar_init(aempty, 1);
-    for (int q = 0; q < kR8BS; ++q) {
-      mbar_init(&bfull[q], 1);
-      mbar_init(&bempty[q], 1);
-    }
+    mbar_init(bfull, 1);
+    mbar_init(bempty, 1);
     for (int q = 0; q < 2; ++q) {
       mbar_init(&tfull[q], 1);
       mbar_init(&tempty[q], 8);
+      mbar_init(&zfull[q], 1);
+      mbar_init(&zempty[q], 1);
     }
+    mbar_init(sfull, 8);
+    mbar_init(sempty, 1);
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&mapA);
-    tma_prefetch_desc(&mapB);
+    tma_prefetch_desc(&m.a);
+    tma_prefetch_desc(&m.b);
+    tma_prefetch_desc(&m.z);
+  }
+  if (warp == 3 && lane == 0) {
+    tma_prefetch_desc(&m.zm);
+    tma_prefetch_desc(&m.dt);
+    tma_prefetch_desc(&m.dm);
   }
   if (warp == 2) i8::tmem_alloc(tmem_slot, 512);
   tc::fence_before_sync();
@@ -123,153 +189,196 @@ __global__ void __launch_bounds__(kR8Threads, 1)
   double s0 = 0.0, s1 = 0.0;
 
   if (warp == 0) {
-    // ------------------------------------------------------------------ TMA producer
+    // ------------------------------------------------------------------ TMA loads
     int curI = -1;
     uint32_t aeph = 0;
-    int bs = 0;
-    uint32_t bph = 0;
-    const uint64_t pol = tc::policy_evict_last();  // V' and V digits are re-read (L2)
-    for (long long t = t_begin; t < t_end; ++t) {
-      int I, J;
-      r8_tile(t, a.TC, a.MT, I, J);
+    const uint64_t keep = tc::policy_evict_last();   // V', V digits: re-read across tiles
+    const uint64_t stream = tc::policy_evict_first(); // Z_old: read once
+    int it = 0, I = 0, J = 0;
+    if (t_begin < t_end) r8_tile(t_begin, a.TC, a.MT, I, J);
+    for (long long t = t_begin; t < t_end; ++t, ++it, r8_next(a.TC, I, J)) {
+      const int i0 = I * kR8M, j0 = J * kR8N, zb = it & 1;
+      // Z_old first: the update warps wait for it; the MMA has slack
+      mbar_wait_idle(&zempty[zb], ((it >> 1) & 1) ^ 1u);
+      if (i8::elect_one()) {
+        mbar_arrive_expect_tx(&zfull[zb], 32768);
+        unsigned char* zs = smem + kOffZ + zb * 32768;
+        tc::tma_load_2d_hint(zs, &m.z, &zfull[zb], j0, i0, stream);
+        tc::tma_load_2d_hint(zs + 16384, &m.z, &zfull[zb], j0 + 16, i0, stream);
+      }
+      __syncwarp();
       if (I != curI) {
         if (curI >= 0) {
-          mbar_wait(aempty, aeph);
+          mbar_wait_idle(aempty, aeph);
           aeph ^= 1u;
         }
         if (i8::elect_one()) {
-          mbar_arrive_expect_tx(afull, kR8A);
-          tc::tma_load_3d_hint(sA, &mapA, afull, 0, 0, I * kR8S, pol);
+          mbar_arrive_expect_tx(afull, kR8S * 8192);
+          tc::tma_load_3d_hint(smem + kOffA, &m.a, afull, 0, 0, I * kR8S, keep);
         }
         __syncwarp();
         curI = I;
       }
-      mbar_wait(&bempty[bs], bph ^ 1u);
+      mbar_wait_idle(bempty, (it & 1) ^ 1u);
       if (i8::elect_one()) {
-        mbar_arrive_expect_tx(&bfull[bs], kR8B);
-        const int j0 = J * kR8N;
-        tc::tma_load_3d_hint(sB + bs * kR8B, &mapB, &bfull[bs], 0, j0 & 127, (j0 >> 7) * kR8S, pol);
+        mbar_arrive_expect_tx(bfull, kR8S * 2048);
+        tc::tma_load_3d_hint(smem + kOffB, &m.b, bfull, 0, j0 & 127, (j0 >> 7) * kR8S, keep);
       }
       __syncwarp();
-      if (++bs == kR8BS) {
-        bs = 0;
-        bph ^= 1u;
-      }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------------ MMA issuer
     int curI = -1;
     uint32_t aph = 0;
-    int bs = 0;
-    uint32_t bph = 0;
-    uint32_t tph[2] = {0u, 0u};
-    const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
-    int it = 0;
-    for (long long t = t_begin; t < t_end; ++t, ++it) {
-      int I, J;
-      r8_tile(t, a.TC, a.MT, I, J);
+    const uint32_t a0 = smem_u32(smem + kOffA), b0 = smem_u32(smem + kOffB);
+    int it = 0, I = 0, J = 0;
+    if (t_begin < t_end) r8_tile(t_begin, a.TC, a.MT, I, J);
+    for (long long t = t_begin; t < t_end; ++t, ++it, r8_next(a.TC, I, J)) {
       if (I != curI) {
-        mbar_wait(afull, aph);
+        mbar_wait_idle(afull, aph);
         aph ^= 1u;
         curI = I;
       }
-      const int buf = it & 1;
-      mbar_wait(&tempty[buf], tph[buf] ^ 1u);  // the update warps drained this buffer
-      tph[buf] ^= 1u;
-      mbar_wait(&bfull[bs], bph);
+      const int tb = it & 1;
+      mbar_wait_idle(&tempty[tb], ((it >> 1) & 1) ^ 1u);  // the update warps drained this buffer
+      mbar_wait_idle(bfull, it & 1);
       tc::fence_after_sync();
-      int In = -1, Jn;
-      if (t + 1 < t_end) r8_tile(t + 1, a.TC, a.MT, In, Jn);
+      int In = I, Jn = J;
+      r8_next(a.TC, In, Jn);
+      if (t + 1 >= t_end) In = -1;
       if (i8::elect_one()) {
-        const uint32_t bst = b0 + bs * kR8B;
 #pragma unroll
         for (int s = 0; s < kR8S; ++s)
 #pragma unroll
           for (int ks = 0; ks < 2; ++ks)
-            i8::mma_i8(tmem + (uint32_t)(buf * 256 + s * kR8N),
-                       tc::sdesc_k_sw64(a0 + s * 8192 + ks * 32),
-                       tc::sdesc_k_sw64(bst + ks * 32), i8::idesc_i8(kR8M, kR8N * (kR8S - s)),
-                       (s | ks) ? 1u : 0u);
-        i8::mma_commit(&bempty[bs]);
-        i8::mma_commit(&tfull[buf]);
+            i8::mma_i8(tmem + (uint32_t)(tb * 256 + s * kR8N),
+                       tc::sdesc_k_sw64(a0 + s * 8192 + ks * 32), tc::sdesc_k_sw64(b0 + ks * 32),
+                       i8::idesc_i8(kR8M, kR8N * (kR8S - s)), (s | ks) ? 1u : 0u);
+        i8::mma_commit(bempty);
+        i8::mma_commit(&tfull[tb]);
         if (In != I) i8::mma_commit(aempty);  // the next tile loads another row block of V'
       }
       __syncwarp();
-      if (++bs == kR8BS) {
-        bs = 0;
-        bph ^= 1u;
-      }
     }
+  } else if (warp == 3) {
+    // ------------------------------------------------------------------ TMA stores
+    int it = 0, I = 0, J = 0;
+    if (t_begin < t_end) r8_tile(t_begin, a.TC, a.MT, I, J);
+    for (long long t = t_begin; t < t_end; ++t, ++it, r8_next(a.TC, I, J)) {
+      const int i0 = I * kR8M, j0 = J * kR8N, zb = it & 1;
+      const bool diagblk = J < 4 * I + 4;
+      mbar_wait_idle(sfull, it & 1);
+      if (i8::elect_one()) {
+        const unsigned char* zs = smem + kOffZ + zb * 32768;
+        tma_store_2d(&m.z, zs, j0, i0);
+        tma_store_2d(&m.z, zs + 16384, j0 + 16, i0);
+        tma_store_3d(&m.dt, smem + kOffDt, j0 & 63, 0, (I * a.KB + (j0 >> 6)) * kR8S);
+        if (!diagblk) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) tma_store_2d(&m.zm, smem + kOffM + k * 4096, i0 + 16 * k, j0);
+          const int kb0 = i0 >> 6, jt = (j0 >> 7) * a.KB;
+          tma_store_3d(&m.dm, smem + kOffDm, 0, j0 & 127, (jt + kb0) * kR8S);
+          if (kb0 + 1 < a.KB)
+            tma_store_3d(&m.dm, smem + kOffDm + kR8S * 2048, 0, j0 & 127, (jt + kb0 + 1) * kR8S);
+        }
+        bulk_commit();
+        bulk_wait_read0();
+        mbar_arrive(&zempty[zb]);
+        mbar_arrive(sempty);
+      }
+      __syncwarp();
+    }
+    if (i8::elect_one()) bulk_wait0();
+    __syncwarp();
   } else if (warp >= 4) {
     // ------------------------------------------------------------------ update warps
     const int q = warp & 3, h = (warp - 4) >> 2;
     const int r = 32 * q + lane;  // tile row = TMEM lane
-    const bool dig = a.A8 != nullptr;
-    const int Eg = dig ? *a.E : 0;
-    if (dig) {
+    const int Eg = *a.E;
+    {
       const double sc = i8::pow2(Eg);
       for (int i = blockIdx.x * 256 + (threadIdx.x - 128); i < a.n; i += gridDim.x * 256)
         a.rscale[i] = sc;
     }
     const double qt = 0.25 * a.tt;
-    uint32_t tph[2] = {0u, 0u};
-    double zo[16];
-    auto load_zo = [&](long long t) {
-      int I, J;
-      r8_tile(t, a.TC, a.MT, I, J);
-      const int i = I * kR8M + r, jb = J * kR8N + 16 * h;
-      const double* zr = a.Z + (size_t)i * a.ldz + jb;
-      if (i < a.n && jb + 16 <= a.n) {
-#pragma unroll
-        for (int c = 0; c < 16; c += 2) {
-          const double2 v = __ldcs(reinterpret_cast<const double2*>(zr + c));
-          zo[c] = v.x;
-          zo[c + 1] = v.y;
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < 16; ++c) zo[c] = (i < a.n && jb + c < a.n) ? zr[c] : 0.0;
-      }
-    };
-    if (t_begin < t_end) load_zo(t_begin);
-    int it = 0;
+    const int sw = r & 7;
+    // transposes of 4 x 4 byte blocks across lanes 4k .. 4k+3 (two exchange rounds)
+    const int u = lane & 3;
+    const uint32_t sel1 = (u & 2) ? 0x3276u : 0x5410u, sel2 = (u & 1) ? 0x3715u : 0x6240u;
+    int it = 0, I = 0, J = 0;
+    if (t_begin < t_end) r8_tile(t_begin, a.TC, a.MT, I, J);
+    // this tile's adjacency word and row scale, loaded one tile ahead
+    uint32_t wraw = 0u;
+    double rs = 0.0;
+    if (t_begin < t_end) {
+      const int i = I * kR8M + r;
+      wraw = (i < a.n) ? __ldg(a.bits + (size_t)i * a.ldb + ((J * kR8N + 16 * h) >> 5)) : 0u;
+      rs = __ldg(a.rsA + i);
+    }
     for (long long t = t_begin; t < t_end; ++t, ++it) {
-      int I, J;
-      r8_tile(t, a.TC, a.MT, I, J);
       const int i0 = I * kR8M, j0 = J * kR8N;
       const int i = i0 + r, jb = j0 + 16 * h;
-      const bool diagblk = J < 4 * I + 4;            // inside the 128 x 128 diagonal block
-      const bool interior = (i0 + kR8M <= a.n) && (j0 + kR8N <= a.n);
-      const bool fast = interior && !diagblk;
-      const uint32_t word = (i < a.n) ? (__ldg(a.bits + (size_t)i * a.ldb + (jb >> 5)) >> (jb & 31)) : 0u;
-      const double rs = (i < a.n) ? a.rsA[i] : 0.0;
+      const bool diagblk = J < 4 * I + 4;             // inside the 128 x 128 diagonal block
+      const bool fast = !diagblk && (i0 + kR8M <= a.n) && (j0 + kR8N <= a.n);
+      const uint32_t word = wraw >> (jb & 31);
+      const double rsi = rs;
+      {
+        int In = I, Jn = J;
+        r8_next(a.TC, In, Jn);
+        if (t + 1 < t_end) {
+          const int inx = In * kR8M + r;
+          wraw = (inx < a.n) ? __ldg(a.bits + (size_t)inx * a.ldb + ((Jn * kR8N + 16 * h) >> 5)) : 0u;
+          rs = __ldg(a.rsA + inx);
+        }
+        I = In;
+        J = Jn;
+      }
       double cs[16];
 #pragma unroll
-      for (int c = 0; c < 16; ++c) cs[c] = (jb + c < a.n) ? __ldg(a.rsB + jb + c) : 0.0;
+      for (int c = 0; c < 16; c += 2) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(a.rsB + jb + c));
+        cs[c] = v.x;
+        cs[c + 1] = v.y;
+      }
       // ---- W from the TMEM levels (smallest weight first)
-      const int buf = it & 1;
-      mbar_wait(&tfull[buf], tph[buf]);
-      tph[buf] ^= 1u;
+      const int tb = it & 1, zb = it & 1;
+      mbar_wait(&tfull[tb], (it >> 1) & 1);
       tc::fence_after_sync();
+      // levels in pairs: 128 D_l + D_{l+1} is exact in int32 (|D_l| <= (l+1) 64 127^2 < 2^23),
+      // then 4 exact conversions; summed smallest weight first
       double w[16];
+      const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(tb * 256 + 16 * h);
+      {
+        uint32_t r6[16];
+        i8::tmem_ld16(taddr + (uint32_t)(6 * kR8N), r6);
 #pragma unroll
-      for (int c = 0; c < 16; ++c) w[c] = 0.0;
-      const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * 256 + 16 * h);
+        for (int c = 0; c < 16; ++c) w[c] = (double)(int)r6[c] * i8::pow2(-56);
+      }
 #pragma unroll 1
-      for (int L = kR8S - 1; L >= 0; --L) {
-        uint32_t rr[16];
-        i8::tmem_ld16(taddr + (uint32_t)(L * kR8N), rr);
-        const double wl = i8::pow2(-7 * (L + 2));
+      for (int L = 4; L >= 0; L -= 2) {
+        uint32_t ra[16], rb2[16];
+        i8::tmem_ld16(taddr + (uint32_t)(L * kR8N), ra);
+        i8::tmem_ld16(taddr + (uint32_t)((L + 1) * kR8N), rb2);
+        const double wl = i8::pow2(-7 * (L + 3));
 #pragma unroll
-        for (int c = 0; c < 16; ++c) w[c] = fma((double)(int)rr[c], wl, w[c]);
+        for (int c = 0; c < 16; ++c) w[c] = fma((double)((int)ra[c] * 128 + (int)rb2[c]), wl, w[c]);
       }
       tc::fence_before_sync();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[buf]);  // the MMA may refill this buffer
+      if (lane == 0) mbar_arrive(&tempty[tb]);  // the MMA may refill this accumulator
 #pragma unroll
-      for (int c = 0; c < 16; ++c) w[c] *= rs * cs[c];  // exact: powers of two
-      // ---- Z_new
+      for (int c = 0; c < 16; ++c) w[c] *= rsi * cs[c];  // exact: powers of two
+      // ---- Z_old (swizzled 128-byte rows: chunk k of row r at k ^ (r % 8))
+      mbar_wait(&zfull[zb], (it >> 1) & 1);
+      double* zrow = reinterpret_cast<double*>(smem + kOffZ + zb * 32768 + h * 16384 + r * 128);
       double z[16];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const double2 v = *reinterpret_cast<const double2*>(zrow + 2 * (k ^ sw));
+        z[2 * k] = v.x;
+        z[2 * k + 1] = v.y;
+      }
+      // ---- Z_new
       if (fast) {
         double ts0 = 0.0, ts1 = 0.0;
 #pragma unroll
@@ -278,7 +387,7 @@ __global__ void __launch_bounds__(kR8Threads, 1)
           const double x = w[c];
           const double o = b ? x - qt : x;          // W_ij - t C_ij, C_ij = adj_ij / 4
           ts0 += b ? x : 0.0;
-          const double e = o - zo[c];
+          const double e = o - z[c];
           ts1 = fma(e, e, ts1);
           z[c] = o;
         }
@@ -289,78 +398,73 @@ __global__ void __launch_bounds__(kR8Threads, 1)
 #pragma unroll
         for (int c = 0; c < 16; ++c) {
           const int j = jb + c;
-          z[c] = 0.0;
-          if (i >= a.n || j >= a.n) continue;
-          const bool b = (word >> c) & 1u;
-          const double x = w[c], zold = zo[c];
-          double o;
-          if (j == i) {
-            o = 1.0 - x + zold;                    // Diag(1 - W_ii + Z_ii)
-            s0 += -0.25 * a.deg[i] * x;            // C_ii = -deg_i / 4
-            s1 += (o - zold) * (o - zold);
-          } else {
-            o = b ? x - qt : x;
-            if (b) s0 += wgt * 0.25 * x;
-            s1 += wgt * (o - zold) * (o - zold);
+          const double x = w[c], zold = z[c];
+          double o = 0.0;                           // outside the matrix: 0 (digits too)
+          if (i < a.n && j < a.n) {
+            const bool b = (word >> c) & 1u;
+            if (j == i) {
+              o = 1.0 - x + zold;                    // Diag(1 - W_ii + Z_ii)
+              s0 += -0.25 * a.deg[i] * x;            // C_ii = -deg_i / 4
+              s1 += (o - zold) * (o - zold);
+            } else {
+              o = b ? x - qt : x;
+              if (b) s0 += wgt * 0.25 * x;
+              s1 += wgt * (o - zold) * (o - zold);
+            }
           }
           z[c] = o;
         }
       }
-      // the next tile's Z_old (its HBM latency overlaps the stores and digits below)
-      if (t + 1 < t_end) load_zo(t + 1);
-      // ---- fp64 stores: the tile row piece (128 B) and, off the diagonal block, the mirror
-      if (i < a.n) {
-        double* zr = a.Z + (size_t)i * a.ldz + jb;
-        if (jb + 16 <= a.n && ((reinterpret_cast<uintptr_t>(zr) & 15) == 0)) {
 #pragma unroll
-          for (int c = 0; c < 16; c += 2)
-            __stcs(reinterpret_cast<double2*>(zr + c), make_double2(z[c], z[c + 1]));
-        } else {
-#pragma unroll
-          for (int c = 0; c < 16; ++c)
-            if (jb + c < a.n) zr[c] = z[c];
-        }
-        if (!diagblk) {
-#pragma unroll
-          for (int c = 0; c < 16; ++c)  // warp: 32 consecutive rows of mirror row jb + c
-            if (jb + c < a.n) __stcs(a.Z + (size_t)(jb + c) * a.ldz + i, z[c]);
-        }
-      }
-      if (!dig) continue;
-      // ---- digit slices of Z_new (one scale 2^Eg, DESIGN.md §4 "fused digits")
+      for (int k = 0; k < 8; ++k)
+        *reinterpret_cast<double2*>(zrow + 2 * (k ^ sw)) = make_double2(z[2 * k], z[2 * k + 1]);
+      // ---- digit slices of Z_new (scale 2^Eg): word g of slice s = columns 4g .. 4g+3
       uint32_t dw[4][kR8S];
 #pragma unroll
       for (int g = 0; g < 4; ++g)
         i8::slices4<kR8S>(z[4 * g], z[4 * g + 1], z[4 * g + 2], z[4 * g + 3], Eg, dw[g]);
-      if (i < a.n && jb < a.n) {  // tile row: 16 digits per slice
-        int8_t* base = a.A8 + i8::a8_offset(i, jb, 0, a.KB, kR8S);
+      mbar_wait(sempty, (it & 1) ^ 1u);             // the previous tile's stores read the staging
+      // tile digits: [slice][row][32 B], SWIZZLE_32B (16-byte chunk ^= bit 7 of the offset)
 #pragma unroll
-        for (int sl = 0; sl < kR8S; ++sl)
-          __stcs(reinterpret_cast<uint4*>(base + sl * 8192),
-                 make_uint4(dw[0][sl], dw[1][sl], dw[2][sl], dw[3][sl]));
+      for (int s = 0; s < kR8S; ++s) {
+        int off = s * 4096 + r * 32 + 16 * h;
+        off ^= ((off >> 7) & 1) << 4;
+        *reinterpret_cast<uint4*>(smem + kOffDt + off) =
+            make_uint4(dw[0][s], dw[1][s], dw[2][s], dw[3][s]);
       }
       if (!diagblk) {
-        // mirror rows: a 4 x 4 byte transpose across lanes 4k .. 4k+3 (rows i .. i+3); lane
-        // 4k + u gets column 4g + u of those 4 rows
-        const int u = lane & 3;
-        const int rbase = i0 + 32 * q + (lane & ~3);
+        // mirror fp64: box k = r / 16 holds mirror rows jj = 0..31 (tile columns), columns
+        // r % 16, SWIZZLE_128B
+        unsigned char* mb = smem + kOffM + (r >> 4) * 4096;
+        const int mc = r & 15;
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          const int jj = 16 * h + c;
+          *reinterpret_cast<double*>(mb + jj * 128 + ((((mc >> 1) ^ (jj & 7))) << 4) + (mc & 1) * 8) =
+              z[c];
+        }
+        // mirror digits: 4 x 4 byte transposes across lanes 4k .. 4k+3 (rows rb .. rb+3); lane
+        // 4k + u gets mirror row 16h + 4g + u, bytes = rows rb .. rb+3: exchange 16-bit halves
+        // with lane u ^ 2, then bytes with lane u ^ 1.  [kb][slice][32 rows][64 B], SWIZZLE_64B
+        // (16-byte chunk ^= bits 7-8 of the offset)
+        const int rb = 32 * q + (lane & ~3);
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
-          const int c = jb + 4 * g + u;
+          const int jj = 16 * h + 4 * g + u;
 #pragma unroll
-          for (int sl = 0; sl < kR8S; ++sl) {
-            const uint32_t x0 = __shfl_sync(0xffffffffu, dw[g][sl], 0, 4);
-            const uint32_t x1 = __shfl_sync(0xffffffffu, dw[g][sl], 1, 4);
-            const uint32_t x2 = __shfl_sync(0xffffffffu, dw[g][sl], 2, 4);
-            const uint32_t x3 = __shfl_sync(0xffffffffu, dw[g][sl], 3, 4);
-            uint32_t tt[4];
-            i8::transpose4(x0, x1, x2, x3, tt);
-            const uint32_t v = u == 0 ? tt[0] : u == 1 ? tt[1] : u == 2 ? tt[2] : tt[3];
-            if (c < a.n && rbase < a.n)
-              __stcs(reinterpret_cast<uint32_t*>(a.A8 + i8::a8_offset(c, rbase, sl, a.KB, kR8S)), v);
+          for (int s = 0; s < kR8S; ++s) {
+            const uint32_t x = dw[g][s];
+            const uint32_t y = __byte_perm(x, __shfl_xor_sync(0xffffffffu, x, 2), sel1);
+            const uint32_t v = __byte_perm(y, __shfl_xor_sync(0xffffffffu, y, 1), sel2);
+            int off = ((rb >> 6) * kR8S + s) * 2048 + jj * 64 + (rb & 63);
+            off ^= ((off >> 7) & 3) << 4;
+            *reinterpret_cast<uint32_t*>(smem + kOffDm + off) = v;
           }
         }
       }
+      fence_proxy_async();  // generic-proxy smem writes -> visible to the TMA stores
+      __syncwarp();
+      if (lane == 0) mbar_arrive(sfull);
     }
   }
   __syncwarp();
@@ -415,36 +519,59 @@ __global__ void __launch_bounds__(256) r8_split_kernel(const double* __restrict_
     v[2] = y.x;
     v[3] = y.y;
   }
-  double m = fmax(fmax(fabs(v[0]), fabs(v[1])), fmax(fabs(v[2]), fabs(v[3])));
+  double mx = fmax(fmax(fabs(v[0]), fabs(v[1])), fmax(fabs(v[2]), fabs(v[3])));
 #pragma unroll
-  for (int o = 8; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o, 16));
-  const int E = i8::scale_exp(m);
+  for (int o = 8; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o, 16));
+  const int E = i8::scale_exp(mx);
   uint32_t w[kR8S];
   i8::slices4<kR8S>(v[0], v[1], v[2], v[3], E, w);
 #pragma unroll
   for (int s = 0; s < kR8S; ++s)
     *reinterpret_cast<uint32_t*>(X8 + i8::a8_offset(row, 4 * t, s, 1, kR8S)) = w[s];
-  if (t == 0 && row < n) scale[row] = i8::pow2(E);
+  if (t == 0) scale[row] = i8::pow2(E);  // padded rows: 1 (their digits are 0)
 }
 
-bool encode_map_i8_3d(CUtensorMap* map, const int8_t* base, int64_t pitch, int64_t slice_pitch,
-                      int cols, int rows, int slices, int box_rows, int box_slices,
-                      bool swizzle = true);
-
-bool r8_encode(CUtensorMap* mapA, CUtensorMap* mapB, const int8_t* VF8, const int8_t* V8, int n) {
-  const int mtiles = (n + 127) / 128;
-  return encode_map_i8_3d(mapA, VF8, 64, 8192, 64, 128, mtiles * kR8S, 128, kR8S) &&
-         encode_map_i8_3d(mapB, V8, 64, 8192, 64, 128, mtiles * kR8S, kR8N, kR8S);
-}
+bool encode_map_gen(CUtensorMap* map, bool f64, int rank, const void* base, const uint64_t* dims,
+                    const uint64_t* strides, const uint32_t* box, int swizzle);
 
 size_t r8_bytes(int n) { return (size_t)((n + 127) / 128) * kR8S * 8192; }
 
-cudaError_t admm_i8_launch(const CUtensorMap& mapA, const CUtensorMap& mapB, const double* VF,
-                           const double* V, int64_t ldv, int8_t* VF8, int8_t* V8, double* rsA,
-                           double* rsB, const uint32_t* adj, int64_t ldadj, const double* deg,
-                           double t, double* Z, int64_t ldz, int n, double* obj, double* partials,
+// the maps that do not depend on Z: V', V digit buffers and the A8 layout of Z_new's digits
+bool r8_encode(CUtensorMap* maps, const int8_t* VF8, const int8_t* V8, const int8_t* A8, int n,
+               int KB) {
+  const uint64_t mt = (uint64_t)(n + 127) / 128;
+  const uint64_t dv[3] = {64, 128, mt * kR8S}, sv[2] = {64, 8192};
+  const uint32_t ba[3] = {64, 128, kR8S}, bb[3] = {64, kR8N, kR8S};
+  const uint64_t dd[3] = {64, 128, mt * (uint64_t)KB * kR8S};
+  const uint32_t bt[3] = {32, 128, kR8S}, bm[3] = {64, 32, kR8S};
+  return encode_map_gen(&maps[0], false, 3, VF8, dv, sv, ba, 64) &&
+         encode_map_gen(&maps[1], false, 3, V8, dv, sv, bb, 64) &&
+         encode_map_gen(&maps[2], false, 3, A8, dd, sv, bt, 32) &&
+         encode_map_gen(&maps[3], false, 3, A8, dd, sv, bm, 64);
+}
+
+bool r8_usable(const double* Z, int64_t ldz) {
+  return (ldz % 2) == 0 && (reinterpret_cast<uintptr_t>(Z) & 15) == 0;
+}
+
+cudaError_t admm_i8_launch(const CUtensorMap* maps, const double* VF, const double* V,
+                           int64_t ldv, int8_t* VF8, int8_t* V8, double* rsA, double* rsB,
+                           const uint32_t* adj, int64_t ldadj, const double* deg, double t,
+                           double* Z, int64_t ldz, int n, double* obj, double* partials,
                            int* counter, const RbDigits* dig, int num_sms, cudaStream_t st) {
   const int mtiles = (n + 127) / 128, rows_pad = mtiles * 128;
+  R8Maps m;
+  m.a = maps[0];
+  m.b = maps[1];
+  m.dt = maps[2];
+  m.dm = maps[3];
+  {
+    const uint64_t dz[2] = {(uint64_t)n, (uint64_t)n}, sz[1] = {(uint64_t)ldz * 8};
+    const uint32_t bz[2] = {16, 128}, bzm[2] = {16, 32};
+    if (!encode_map_gen(&m.z, true, 2, Z, dz, sz, bz, 128) ||
+        !encode_map_gen(&m.zm, true, 2, Z, dz, sz, bzm, 128))
+      return cudaErrorInvalidValue;
+  }
   count_launch();
   r8_split_kernel<<<(rows_pad + 15) / 16, 256, 0, st>>>(VF, 64, n, rows_pad, VF8, rsA);
   count_launch();
@@ -456,16 +583,12 @@ cudaError_t admm_i8_launch(const CUtensorMap& mapA, const CUtensorMap& mapB, con
   a.ldb = ldadj;
   a.deg = deg;
   a.tt = t;
-  a.Z = Z;
-  a.ldz = ldz;
   a.n = n;
   a.TC = (n + kR8N - 1) / kR8N;
   a.MT = mtiles;
-  a.A8 = dig ? dig->A8 : nullptr;
-  a.KB = dig ? dig->KB : 0;
-  a.S = kR8S;
-  a.E = dig ? dig->E : nullptr;
-  a.rscale = dig ? dig->rscale : nullptr;
+  a.KB = dig->KB;
+  a.E = dig->E;
+  a.rscale = dig->rscale;
   a.partials = partials;
   a.counter = counter;
   a.obj = obj;
@@ -479,7 +602,7 @@ cudaError_t admm_i8_launch(const CUtensorMap& mapA, const CUtensorMap& mapB, con
   const long long ntiles = (long long)a.MT * a.TC - 2LL * a.MT * (a.MT - 1);
   const int grid = (int)std::max<long long>(1, std::min<long long>(ntiles, num_sms));
   count_launch();
-  rebuild_i8_kernel<<<grid, kR8Threads, kR8Smem, st>>>(mapA, mapB, a);
+  rebuild_i8_kernel<<<grid, kR8Threads, kR8Smem, st>>>(m, a);
   return cudaGetLastError();
 }
 
