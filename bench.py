@@ -160,7 +160,9 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         ep1.record(stream)
     torch.cuda.synchronize()
     gemm_ms, gemm_n = s.ctx.profile_read(stream)
+    upd_ms, upd_n = s.ctx.profile_read_update(stream)
     gemm_share = gemm_ms / ep0.elapsed_time(ep1)
+    upd_share = upd_ms / ep0.elapsed_time(ep1)
     s.ctx.profile(False)
     s.graphs = True
     status = s.ctx.status(stream)
@@ -224,6 +226,31 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
                 "algorithmic_per_launch": {"flops": flops_gemm, "bytes": 8.0 * n * n},
                 "avg_launch_ms": gemm_avg_ms, "launches": gemm_n,
                 "share_of_step": gemm_share}
+    # the PFAM update (pf_admm_step, HBM-bound): Z_old upper triangle read, Z_new written in full,
+    # the digit slices of Z_new (fused, i8 path), V and V' rows, the upper adjacency bits
+    upd_roof = None
+    if upd_n:
+        fused = args.path == "i8" and os.environ.get("PF_FUSE_DIGITS", "1") != "0"
+        k7i8 = fused and p == 64 and os.environ.get("PF_K7I8", "1") != "0"
+        ubytes = 8.0 * n * (n + 1) / 2 + 8.0 * n * n + (7.0 * n * n if fused else 0.0) \
+            + 2 * 8.0 * n * p + n * n / 16.0
+        uavg = upd_ms / upd_n
+        utraffic = None
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", "update_traffic.json")))
+            if tr.get("n") == n and tr.get("p") == p and tr.get("kernel_i8") == k7i8:
+                utraffic = tr["dram_bytes_per_launch"]
+        except Exception:
+            pass
+        upd_roof = {"bound": "hbm",
+                    "kernel": ("rebuild_i8_kernel (W from tcgen05 kind::i8 digit products, "
+                               "TMA-staged update)") if k7i8 else "rebuild_kernel<P> (fp64 DMMA)",
+                    "achieved": ubytes / (uavg / 1e3) / 1e9, "peak": pk.get("hbm_gbs", 6550.4),
+                    "unit": "GB/s",
+                    "frac": ubytes / (uavg / 1e3) / 1e9 / pk.get("hbm_gbs", 6550.4),
+                    "traffic": utraffic, "algorithmic_bytes_per_launch": ubytes,
+                    "avg_launch_ms": uavg, "launches": upd_n, "share_of_step": upd_share,
+                    "timed": "events around pf_admm_step (row bounds + splits + update kernel)"}
     filter_flops_per_step = 2.0 * d * n * n * p
     cpu = cpu_baseline(cfg, args) if (world == 1 and not args.no_cpu) else None
     out = {
@@ -256,6 +283,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
                    "parallelism": "replicas" if world > 1 else "1 GPU"},
         "filter_tflops": world * filter_flops_per_step * args.steps / (ms_max / 1e3) / 1e12,
         "roofline": roof,
+        "update_roofline": upd_roof,
         "clocks": clk,
         "gpu_launches": launches,
         "e2e": e2e,

@@ -252,6 +252,10 @@ pf_status pf_profile(pf_ctx ctx, int32_t enable);
 /* Synchronises `stream`; returns the summed GEMM time (ms) and the number of timed launches
  * since pf_profile, then clears the record.  PF_ERR_ARG if launches were dropped. */
 pf_status pf_profile_read(pf_ctx ctx, pf_stream stream, double* gemm_ms, int64_t* gemm_launches);
+/* Synchronises `stream`; returns the summed time (ms) and count of the PFAM updates
+ * (pf_admm_step / pf_admm_step_f: row bounds, splits and the update kernel, bracketed by events
+ * on their stream) timed since pf_profile, then clears that record (up to 512 updates). */
+pf_status pf_profile_read_update(pf_ctx ctx, pf_stream stream, double* ms, int64_t* launches);
 /* Overlapped all-gather (PF_TF32, world > 1; environment PF_OVERLAP=0 at create turns it off):
  * the timeline of the last overlapped GEMM step recorded while pf_profile is on.  Synchronises
  * `stream`; writes 3 world values (ms from the step start): ms[s] = arrival of the s-th slab in

@@ -74,6 +74,7 @@ def load() -> ctypes.CDLL:
         "pf_svt_update": [P, P, P, P, P, P, I64, P, I64, P, D, P, P],
         "pf_profile": [P, I32],
         "pf_profile_read": [P, P, ctypes.POINTER(D), ctypes.POINTER(I64)],
+        "pf_profile_read_update": [P, P, ctypes.POINTER(D), ctypes.POINTER(I64)],
         "pf_kernel_launches": [],
         "pf_diagnostics": [P, P, ctypes.POINTER(D)],
         "pf_nccl_unique_id": [P, I32],
@@ -226,6 +227,13 @@ class Context:
         ms, n = ctypes.c_double(), ctypes.c_int64()
         self._check(self.lib.pf_profile_read(self.h, _stream(stream), ctypes.byref(ms),
                                              ctypes.byref(n)), "pf_profile_read")
+        return ms.value, n.value
+
+    def profile_read_update(self, stream=None):
+        """(summed ms, count) of the PFAM updates (pf_admm_step*) since profile(True)."""
+        ms, n = ctypes.c_double(), ctypes.c_int64()
+        self._check(self.lib.pf_profile_read_update(self.h, _stream(stream), ctypes.byref(ms),
+                                                    ctypes.byref(n)), "pf_profile_read_update")
         return ms.value, n.value
 
     def overlap_timeline(self, stream=None) -> list[float]:

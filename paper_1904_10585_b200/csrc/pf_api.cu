@@ -74,6 +74,8 @@ struct pf_ctx_s {
   bool prof = false;
   std::vector<cudaEvent_t> ev;
   size_t ev_used = 0;
+  std::vector<cudaEvent_t> evu;               // ... and around every PFAM update (pf_admm_step*)
+  size_t evu_used = 0;
   long long prof_dropped = 0;
   // ---- fp32 storage / TF32 tensor-core path (dtype PF_TF32): p-major fp32 blocks
   int64_t ldy32 = 0;                           // pitch of the internal blocks (>= n_local, %4)
@@ -496,10 +498,28 @@ pf_status pf_profile(pf_ctx ctx, int32_t enable) {
   if (enable && ctx->ev.empty()) {
     ctx->ev.resize(8192);
     for (auto& e : ctx->ev) PF_CU(cudaEventCreate(&e));
+    ctx->evu.resize(1024);
+    for (auto& e : ctx->evu) PF_CU(cudaEventCreate(&e));
   }
   ctx->prof = enable != 0;
   ctx->ev_used = 0;
+  ctx->evu_used = 0;
   ctx->prof_dropped = 0;
+  return PF_OK;
+}
+
+pf_status pf_profile_read_update(pf_ctx ctx, pf_stream stream, double* ms_out, int64_t* launches) {
+  if (!ctx || !ms_out || !launches) return PF_ERR_ARG;
+  PF_CU(cudaStreamSynchronize((cudaStream_t)stream));
+  double tot = 0.0;
+  for (size_t i = 0; i + 1 < ctx->evu_used; i += 2) {
+    float ms = 0.f;
+    PF_CU(cudaEventElapsedTime(&ms, ctx->evu[i], ctx->evu[i + 1]));
+    tot += ms;
+  }
+  *ms_out = tot;
+  *launches = (int64_t)(ctx->evu_used / 2);
+  ctx->evu_used = 0;
   return PF_OK;
 }
 
@@ -543,6 +563,7 @@ pf_status pf_destroy(pf_ctx ctx) {
   if (!ctx) return PF_ERR_ARG;
   ns_destroy(ctx->ns);
   for (auto e : ctx->ev) cudaEventDestroy(e);
+  for (auto e : ctx->evu) cudaEventDestroy(e);
   delete ctx->comm;
   if (ctx->comm_st) cudaStreamDestroy(ctx->comm_st);
   if (ctx->ev_start) cudaEventDestroy(ctx->ev_start);
@@ -1202,10 +1223,16 @@ pf_status pf_admm_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f
   RbDigits dig{ctx->A8, ctx->i8plan.kblocks, ctx->i8plan.S, ctx->a8_E, ctx->a8_rscale, ctx->a8_wa, ctx->a8_wmax};
   R8Bufs r8{ctx->r8_maps, ctx->r8_VF8, ctx->r8_V8, ctx->r8_rs,
             ctx->r8_rs + (size_t)ctx->i8plan.mtiles * 128, ctx->num_sms};
+  const bool urec = ctx->prof && ctx->evu_used + 2 <= ctx->evu.size();
+  if (urec) PF_CU(cudaEventRecord(ctx->evu[ctx->evu_used], st));
   PF_CU(admm_launch(Vf, ldf, V, ldv, f, t, adj, ldadj, deg, Z, ldz, (int)ctx->n_local,
                     (int)ctx->n, (int)ctx->row0, ctx->p, obj, ctx->rb_part, ctx->rb_cnt,
                     ctx->dist ? 1 : 0, ctx->VFbuf, st, fuse ? &dig : nullptr, nullptr,
                     fuse && ctx->r8_on ? &r8 : nullptr));
+  if (urec) {
+    PF_CU(cudaEventRecord(ctx->evu[ctx->evu_used + 1], st));
+    ctx->evu_used += 2;
+  }
   if (fuse) {
     ctx->a8_src = Z;
     ctx->a8_lda = ldz;
@@ -1238,10 +1265,16 @@ pf_status pf_admm_step_f(pf_ctx ctx, const double* Q, int64_t ldq, const double*
   RbDigits dig{ctx->A8, ctx->i8plan.kblocks, ctx->i8plan.S, ctx->a8_E, ctx->a8_rscale, ctx->a8_wa, ctx->a8_wmax};
   R8Bufs r8{ctx->r8_maps, ctx->r8_VF8, ctx->r8_V8, ctx->r8_rs,
             ctx->r8_rs + (size_t)ctx->i8plan.mtiles * 128, ctx->num_sms};
+  const bool urec = ctx->prof && ctx->evu_used + 2 <= ctx->evu.size();
+  if (urec) PF_CU(cudaEventRecord(ctx->evu[ctx->evu_used], st));
   PF_CU(admm_launch(Qf, ldf, Q, ldq, nullptr, t, adj, ldadj, deg, Z, ldz, (int)ctx->n_local,
                     (int)ctx->n, (int)ctx->row0, ctx->p, obj, ctx->rb_part, ctx->rb_cnt,
                     ctx->dist ? 1 : 0, ctx->VFbuf, st, fuse ? &dig : nullptr, F,
                     fuse && ctx->r8_on ? &r8 : nullptr));
+  if (urec) {
+    PF_CU(cudaEventRecord(ctx->evu[ctx->evu_used + 1], st));
+    ctx->evu_used += 2;
+  }
   if (fuse) {
     ctx->a8_src = Z;
     ctx->a8_lda = ldz;
