@@ -129,6 +129,11 @@ struct pf_ctx_s {
   double* i8_part = nullptr;                   // stream-K partials
   int* i8_cnt = nullptr;                       // [items], self-resetting
   CUtensorMap mapA8, mapA8pf;
+  // half-storage symmetric product (K1-i8s, pf_gemm_i8.cu) on fused digits: the stored tiles
+  // (I, J >= I) only; PF_I8SYM=1 at create turns it on
+  bool i8s_ok = false;
+  CUtensorMap mapA8t;                          // 64-row boxes read transposed
+  bool a8_half = false;                        // A8 holds the upper tiles only (no mirror digits)
   CUtensorMap mapY8[4];                        // B boxes of 4..7 digit slices
   int i8_early = 7;                            // slices of the Chebyshev steps before the tail
   int i8_tail = 0;                             // final steps (and RR) at the full slice count
@@ -213,6 +218,7 @@ pf_status pf_nccl_unique_id(void* out, int32_t bytes) {
 
 static bool encode_i8_maps(pf_ctx ctx) {
   if (!i8_encode_A(&ctx->mapA8, &ctx->mapA8pf, ctx->A8, ctx->i8plan)) return false;
+  if (ctx->i8s_ok && !i8s_encode_At(&ctx->mapA8t, ctx->A8, ctx->i8plan)) return false;
   for (int su = 4; su <= ctx->i8plan.S; ++su)
     if (!i8_encode_B(&ctx->mapY8[su - 4], ctx->Y8, ctx->i8plan, su)) return false;
   return true;
@@ -425,6 +431,10 @@ static pf_status create_common(int64_t n, int32_t p, int32_t degree, pf_dtype dt
   if (dtype == PF_FP64_I8) {
     ctx->i8 = true;
     ctx->i8plan = i8_plan(p, (int)ctx->n_local, (int)n, 7, ctx->num_sms);  // S = 7
+    // the half-storage product is opt-in (PF_I8SYM=1): it halves the A-digit reads but runs on
+    // one CTA per 128-row tile (128 of 148 SMs at n = 16384) and measured slower
+    const char* e8 = getenv("PF_I8SYM");
+    ctx->i8s_ok = !dist && (e8 && e8[0] == '1') && i8s_supported(ctx->i8plan, ctx->num_sms);
   }
   pf_status s = alloc_all(ctx);
   if (s == PF_OK && ctx->dist) {
@@ -652,13 +662,13 @@ static pf_status split_A(pf_ctx ctx, const double* A, int64_t lda, bool reuse, c
   if (!use_i8(ctx)) return PF_OK;
   if (reuse && ctx->a8_valid && ctx->a8_src == A && ctx->a8_lda == lda) return PF_OK;
   PF_CU(i8_split_A_launch(A, lda, ctx->i8plan, ctx->A8, ctx->a8_rscale, ctx->num_sms, st));
-  ctx->a8_fused = false;
+  ctx->a8_fused = ctx->a8_half = false;
   ctx->a8_src = A;
   ctx->a8_lda = lda;
   ctx->a8_valid = true;
   return PF_OK;
 }
-static void iterate_written(pf_ctx ctx) { ctx->a8_valid = ctx->a8_fused = false; }
+static void iterate_written(pf_ctx ctx) { ctx->a8_valid = ctx->a8_fused = ctx->a8_half = false; }
 
 static bool is_fp64(pf_ctx ctx) { return ctx->dtype == PF_FP64 || ctx->dtype == PF_FP64_I8; }
 
@@ -683,9 +693,19 @@ static pf_status gemm_step(pf_ctx ctx, int bidx, const double* ycur, const doubl
   if (use_i8(ctx)) {
     const int S = ctx->i8plan.S;
     su = (su <= 0 || su > S) ? S : su;
-    PF_CU(i8_gemm_launch(ctx->i8plan, ctx->mapA8, ctx->mapY8[su - 4], ctx->mapA8pf,
-                         ctx->a8_rscale, ctx->y8_cscale, ycur, yprev, out, ctx->p, coef,
-                         ctx->i8_acc, ctx->i8_part, ctx->i8_cnt, su, st));
+    // fused digits of a symmetric iterate (one scale): the half-storage product
+    const bool sym = ctx->i8s_ok && ctx->a8_fused && su == S && S == 7;
+    if (ctx->a8_half && !sym) {
+      snprintf(ctx->err, sizeof(ctx->err), "upper-tile digits need the full slice count");
+      return PF_ERR_UNSUPPORTED;
+    }
+    if (sym)
+      PF_CU(i8s_gemm_launch(ctx->i8plan, ctx->mapA8, ctx->mapA8t, ctx->mapY8[su - 4],
+                            ctx->a8_rscale, ctx->y8_cscale, ycur, yprev, out, ctx->p, coef, st));
+    else
+      PF_CU(i8_gemm_launch(ctx->i8plan, ctx->mapA8, ctx->mapY8[su - 4], ctx->mapA8pf,
+                           ctx->a8_rscale, ctx->y8_cscale, ycur, yprev, out, ctx->p, coef,
+                           ctx->i8_acc, ctx->i8_part, ctx->i8_cnt, su, st));
   }
   else
     PF_CU(cheb_gemm_launch(ctx->plan, ctx->mapA, *mb, ycur, yprev, out, coef, ctx->cheb_ws,
@@ -1221,8 +1241,11 @@ pf_status pf_admm_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f
   const bool fuse = use_i8(ctx) && !ctx->dist && ctx->fuse_digits &&
                     (ctx->i8plan.S == 6 || ctx->i8plan.S == 7);
   RbDigits dig{ctx->A8, ctx->i8plan.kblocks, ctx->i8plan.S, ctx->a8_E, ctx->a8_rscale, ctx->a8_wa, ctx->a8_wmax};
+  // the half-storage product reads the upper tiles only: no mirror digits (unless a precision
+  // schedule will run products on fewer slices, which the half-storage kernel does not do)
+  const bool half = ctx->i8s_ok && ctx->i8_early >= ctx->i8plan.S;
   R8Bufs r8{ctx->r8_maps, ctx->r8_VF8, ctx->r8_V8, ctx->r8_rs,
-            ctx->r8_rs + (size_t)ctx->i8plan.mtiles * 128, ctx->num_sms};
+            ctx->r8_rs + (size_t)ctx->i8plan.mtiles * 128, ctx->num_sms, half ? 0 : 1};
   const bool urec = ctx->prof && ctx->evu_used + 2 <= ctx->evu.size();
   if (urec) PF_CU(cudaEventRecord(ctx->evu[ctx->evu_used], st));
   PF_CU(admm_launch(Vf, ldf, V, ldv, f, t, adj, ldadj, deg, Z, ldz, (int)ctx->n_local,
@@ -1237,6 +1260,7 @@ pf_status pf_admm_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f
     ctx->a8_src = Z;
     ctx->a8_lda = ldz;
     ctx->a8_valid = ctx->a8_fused = true;
+    ctx->a8_half = half && ctx->r8_on && ctx->i8plan.S == 7 && r8_usable(Z, ldz);
   }
   if (ctx->dist) {
     // <C, W> and the squared residual are sums over row blocks; sqrt after the reduction
@@ -1263,8 +1287,11 @@ pf_status pf_admm_step_f(pf_ctx ctx, const double* Q, int64_t ldq, const double*
   const bool fuse = use_i8(ctx) && !ctx->dist && ctx->fuse_digits &&
                     (ctx->i8plan.S == 6 || ctx->i8plan.S == 7);
   RbDigits dig{ctx->A8, ctx->i8plan.kblocks, ctx->i8plan.S, ctx->a8_E, ctx->a8_rscale, ctx->a8_wa, ctx->a8_wmax};
+  // the half-storage product reads the upper tiles only: no mirror digits (unless a precision
+  // schedule will run products on fewer slices, which the half-storage kernel does not do)
+  const bool half = ctx->i8s_ok && ctx->i8_early >= ctx->i8plan.S;
   R8Bufs r8{ctx->r8_maps, ctx->r8_VF8, ctx->r8_V8, ctx->r8_rs,
-            ctx->r8_rs + (size_t)ctx->i8plan.mtiles * 128, ctx->num_sms};
+            ctx->r8_rs + (size_t)ctx->i8plan.mtiles * 128, ctx->num_sms, half ? 0 : 1};
   const bool urec = ctx->prof && ctx->evu_used + 2 <= ctx->evu.size();
   if (urec) PF_CU(cudaEventRecord(ctx->evu[ctx->evu_used], st));
   PF_CU(admm_launch(Qf, ldf, Q, ldq, nullptr, t, adj, ldadj, deg, Z, ldz, (int)ctx->n_local,
@@ -1279,6 +1306,7 @@ pf_status pf_admm_step_f(pf_ctx ctx, const double* Q, int64_t ldq, const double*
     ctx->a8_src = Z;
     ctx->a8_lda = ldz;
     ctx->a8_valid = ctx->a8_fused = true;
+    ctx->a8_half = half && ctx->r8_on && ctx->i8plan.S == 7 && r8_usable(Z, ldz);
   }
   if (ctx->dist) {
     PF_TRY(allreduce(ctx, obj, 2, st));

@@ -522,6 +522,207 @@ __global__ void __launch_bounds__(I8Cfg<S, NC>::THREADS, 1)
   }
 }
 
+// ------------------------------------------------------------------------------ symmetric A
+// Half-storage filter product for a SYMMETRIC A whose digit slices share one scale (the fused
+// PFAM digits, scale 2^Eg for every row; DESIGN.md §4 "K1-i8s"): only the 128 x 128 tiles
+// (I, J >= I) of the tiled layout are read.  CTA I owns row tile I and walks the column tiles in
+// the order J = (t - I) mod T, t = 0 .. T-1: the lower tiles (J < I) are the stored tiles (J, I)
+// read transposed -- an MN-major A operand (two 64-row boxes of tile J's k-blocks 2I, 2I+1;
+// descriptor LBO = 4096 between the two 64-byte M chunks, SBO = 512 between 8-row K groups,
+// instruction-descriptor transpose-A bit; tools/probe/i8_mn.cu checks it bit-exactly).  Stored
+// tile (a, b) is needed by CTA a and CTA b at the same step t = a + b (mod T), so the second read
+// of every off-diagonal tile is an L2 hit while the CTAs advance together: HBM reads 7n²/2
+// bytes instead of 7n².  One CTA per row tile (T <= SMs), no K split: the whole K range is one
+// exact int32 accumulation (K <= chunk_kb k-blocks), the epilogue runs once.  S = 7, NC = p = 64.
+constexpr int kSymS = 7, kSymNC = 64;
+using SymCfg = I8Cfg<kSymS, kSymNC>;
+
+__global__ void __launch_bounds__(SymCfg::THREADS, 1)
+    cheb_gemm_i8s_kernel(const __grid_constant__ CUtensorMap mapA8,
+                         const __grid_constant__ CUtensorMap mapA8t,
+                         const __grid_constant__ CUtensorMap mapY8, I8Args args) {
+  using C = SymCfg;
+  constexpr int S = kSymS, NC = kSymNC;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  unsigned char* ring_a = smem;                              // NA x 8 KB
+  unsigned char* ring_b = smem + C::NA * C::A_TILE;          // NB x [S][NC][64] int8
+  uint64_t* afull = reinterpret_cast<uint64_t*>(ring_b + C::NB * C::B_STAGE);
+  uint64_t* aempty = afull + C::NA;
+  uint64_t* bfull = aempty + C::NA;
+  uint64_t* bempty = bfull + C::NB;
+  uint64_t* tfull = bempty + C::NB;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::NA; ++s) {
+      mbar_init(&afull[s], 1);
+      mbar_init(&aempty[s], 1);
+    }
+    for (int s = 0; s < C::NB; ++s) {
+      mbar_init(&bfull[s], 1);
+      mbar_init(&bempty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&mapA8);
+    tma_prefetch_desc(&mapA8t);
+    tma_prefetch_desc(&mapY8);
+  }
+  if (warp == 2) i8::tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+
+  const int KB = args.kblocks, T = args.mtiles, I = blockIdx.x;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    RingI ra(C::NA), rb(C::NB);
+    const uint64_t pol_b = tc::policy_evict_last();
+    const uint64_t pol_d = tc::policy_evict_first();  // diagonal tiles: read once
+    for (int t = 0; t < T; ++t) {
+      const int J = (t - I + T) % T;
+      for (int kk = 0; kk < 2; ++kk) {
+        const int kb = 2 * J + kk;
+        if (kb >= KB) break;
+        mbar_wait(&bempty[rb.s], rb.ph ^ 1u);
+        if (i8::elect_one()) {
+          mbar_arrive_expect_tx(&bfull[rb.s], C::B_LOAD);
+          tc::tma_load_3d_hint(ring_b + rb.s * C::B_STAGE, &mapY8, &bfull[rb.s], kb * C::BK, 0,
+                               0, pol_b);
+        }
+        __syncwarp();
+        rb.next();
+#pragma unroll 1
+        for (int s = 0; s < S; ++s) {
+          mbar_wait(&aempty[ra.s], ra.ph ^ 1u);
+          if (i8::elect_one()) {
+            unsigned char* dst = ring_a + ra.s * C::A_TILE;
+            if (J >= I) {  // stored tile (I, J): K-major box of k-block kb
+              mbar_arrive_expect_tx(&afull[ra.s], C::A_TILE);
+              if (J == I)
+                tc::tma_load_3d_hint(dst, &mapA8, &afull[ra.s], 0, 0, (I * KB + kb) * args.lS + s,
+                                     pol_d);
+              else
+                tc::tma_load_3d(dst, &mapA8, &afull[ra.s], 0, 0, (I * KB + kb) * args.lS + s);
+            } else {  // stored tile (J, I) transposed: rows 64 kk.. of its k-blocks 2I, 2I+1
+              const bool two = 2 * I + 1 < KB;
+              mbar_arrive_expect_tx(&afull[ra.s], two ? C::A_TILE : C::A_TILE / 2);
+              tc::tma_load_3d(dst, &mapA8t, &afull[ra.s], 0, 64 * kk,
+                              (J * KB + 2 * I) * args.lS + s);
+              if (two)
+                tc::tma_load_3d(dst + C::A_TILE / 2, &mapA8t, &afull[ra.s], 0, 64 * kk,
+                                (J * KB + 2 * I + 1) * args.lS + s);
+            }
+          }
+          __syncwarp();
+          ra.next();
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    RingI ra(C::NA), rb(C::NB);
+    const uint32_t ring_a0 = smem_u32(ring_a), ring_b0 = smem_u32(ring_b);
+    bool first = true;
+    for (int t = 0; t < T; ++t) {
+      const int J = (t - I + T) % T;
+      const bool tr = J < I;
+      for (int kk = 0; kk < 2; ++kk) {
+        const int kb = 2 * J + kk;
+        if (kb >= KB) break;
+        mbar_wait(&bfull[rb.s], rb.ph);
+        const uint32_t b0 = ring_b0 + rb.s * C::B_STAGE;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          mbar_wait(&afull[ra.s], ra.ph);
+          tc::fence_after_sync();
+          const uint32_t a0 = ring_a0 + ra.s * C::A_TILE;
+          if (i8::elect_one()) {
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) {
+              const uint32_t acc = (first && s == 0 && ks == 0) ? 0u : 1u;
+              // K-major: 32-byte K step inside the 64-byte rows; MN-major: 32 rows of K (2 KB),
+              // the two 64-byte M chunks 4 KB apart
+              const uint64_t ad = tr ? (tc::sdesc_k_sw64(a0 + ks * 2048) & ~(0x3FFFull << 16)) |
+                                           ((uint64_t)(4096 >> 4) << 16)
+                                     : tc::sdesc_k_sw64(a0 + ks * 32);
+              const uint32_t tbit = tr ? (1u << 15) : 0u;
+#pragma unroll
+              for (int t0 = 0; t0 < S - s; t0 += C::CMAX) {
+                const int c = (S - s - t0) < C::CMAX ? (S - s - t0) : C::CMAX;
+                i8::mma_i8(tmem + (uint32_t)((s + t0) * NC), ad,
+                           tc::sdesc_k_sw64(b0 + t0 * NC * C::BK + ks * 32),
+                           i8::idesc_i8(C::BM, c * NC) | tbit, acc);
+              }
+            }
+            i8::mma_commit(&aempty[ra.s]);
+          }
+          __syncwarp();
+          ra.next();
+        }
+        first = false;
+        if (i8::elect_one()) i8::mma_commit(&bempty[rb.s]);
+        __syncwarp();
+        rb.next();
+      }
+    }
+    if (i8::elect_one()) i8::mma_commit(tfull);
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue (4 warps)
+    const int q = warp & 3;
+    const int et = 32 * q + lane;
+    const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16);
+    const double s1 = args.coef[0], s2 = args.coef[1], s3 = args.coef[2];
+    const int row = I * C::BM + et;
+    const bool row_ok = row < args.n_rows;
+    const double rs = row_ok ? args.rscale[row] : 0.0;
+    mbar_wait(tfull, 0);
+    tc::fence_after_sync();
+#pragma unroll 1
+    for (int c0 = 0; c0 < NC; c0 += C::CW) {
+      double v[C::CW];
+#pragma unroll
+      for (int j = 0; j < C::CW; ++j) v[j] = 0.0;
+#pragma unroll 1
+      for (int L = S - 1; L >= 0; --L) {
+        const double w = i8::pow2(-7 * (L + 2));
+#pragma unroll
+        for (int h = 0; h < C::CW; h += 16) {
+          uint32_t r[16];
+          i8::tmem_ld16(taddr + (uint32_t)(L * NC + c0 + h), r);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[h + j] = fma((double)(int)r[j], w, v[h + j]);
+        }
+      }
+      if (row_ok) {
+        const size_t o = (size_t)row * args.ldy + c0;
+#pragma unroll
+        for (int j = 0; j < C::CW; ++j) {
+          double y = s1 * (v[j] * rs * __ldg(args.cscale + c0 + j));
+          if (s2 != 0.0) y = fma(s2, args.ycur[o + j], y);
+          if (s3 != 0.0) y = fma(s3, args.yprev[o + j], y);
+          args.out[o + j] = y;
+        }
+      }
+    }
+  }
+
+  __syncwarp();
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 2) {
+    tc::fence_after_sync();
+    i8::tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
 // ------------------------------------------------------------------------------ host side
 bool encode_map_i8_3d(CUtensorMap* map, const int8_t* base, int64_t pitch, int64_t slice_pitch,
                       int cols, int rows, int slices, int box_rows, int box_slices,
@@ -675,6 +876,44 @@ cudaError_t i8_gemm_launch(const I8Plan& pl, const CUtensorMap& mapA8, const CUt
     case 7: return i8_launch_s<7>(pl, mapA8, mapY8, mapA8pf, a, st);
     default: return cudaErrorInvalidValue;
   }
+}
+
+// the symmetric kernel applies: one GPU's whole matrix, p = 64, S = 7 slices used, one CTA per row
+// tile, one exact accumulation over K
+bool i8s_supported(const I8Plan& pl, int num_sms) {
+  return pl.p == 64 && pl.S == 7 && pl.n_rows == pl.n_k && pl.mtiles <= num_sms &&
+         pl.kblocks <= pl.chunk_kb;
+}
+bool i8s_encode_At(CUtensorMap* map, const int8_t* A8, const I8Plan& pl) {
+  const int blocks = pl.mtiles * pl.kblocks * pl.S;
+  return encode_map_i8_3d(map, A8, 64, 8192, 64, 128, blocks, 64, 1);
+}
+cudaError_t i8s_gemm_launch(const I8Plan& pl, const CUtensorMap& mapA8, const CUtensorMap& mapA8t,
+                            const CUtensorMap& mapY8, const double* rscale, const double* cscale,
+                            const double* ycur, const double* yprev, double* out, int64_t ldy,
+                            const double* coef, cudaStream_t st) {
+  I8Args a = {};
+  a.ycur = ycur;
+  a.yprev = yprev;
+  a.out = out;
+  a.ldy = ldy;
+  a.coef = coef;
+  a.rscale = rscale;
+  a.cscale = cscale;
+  a.n_rows = pl.n_rows;
+  a.kblocks = pl.kblocks;
+  a.mtiles = pl.mtiles;
+  a.lS = pl.S;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(cheb_gemm_i8s_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, SymCfg::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  count_launch();
+  cheb_gemm_i8s_kernel<<<pl.mtiles, SymCfg::THREADS, SymCfg::SMEM, st>>>(mapA8, mapA8t, mapY8, a);
+  return cudaGetLastError();
 }
 
 }  // namespace pf

@@ -81,6 +81,12 @@ cudaError_t i8_split_A_launch(const double* A, int64_t lda, const I8Plan& pl, in
 cudaError_t i8_split_Y_launch(const double* Y, int64_t ldy, const I8Plan& pl,
                               unsigned long long* cmax, int8_t* Y8, double* cscale, int num_sms,
                               cudaStream_t st);
+bool i8s_supported(const I8Plan& pl, int num_sms);
+bool i8s_encode_At(CUtensorMap* map, const int8_t* A8, const I8Plan& pl);
+cudaError_t i8s_gemm_launch(const I8Plan& pl, const CUtensorMap& mapA8, const CUtensorMap& mapA8t,
+                            const CUtensorMap& mapY8, const double* rscale, const double* cscale,
+                            const double* ycur, const double* yprev, double* out, int64_t ldy,
+                            const double* coef, cudaStream_t st);
 cudaError_t i8_gemm_launch(const I8Plan& pl, const CUtensorMap& mapA8, const CUtensorMap& mapY8,
                            const CUtensorMap& mapA8pf, const double* rscale, const double* cscale, const double* ycur,
                            const double* yprev, double* out, int64_t ldy, const double* coef,
@@ -237,6 +243,7 @@ struct R8Bufs {
   double* rsA;
   double* rsB;
   int num_sms;
+  int mirror_dig;           // 0: upper-tile digits only (the half-storage product reads no others)
 };
 size_t r8_bytes(int n);
 bool r8_encode(CUtensorMap* maps, const int8_t* VF8, const int8_t* V8, const int8_t* A8, int n,
@@ -246,7 +253,8 @@ cudaError_t admm_i8_launch(const CUtensorMap* maps, const double* VF, const doub
                            int64_t ldv, int8_t* VF8, int8_t* V8, double* rsA, double* rsB,
                            const uint32_t* adj, int64_t ldadj, const double* deg, double t,
                            double* Z, int64_t ldz, int n, double* obj, double* partials,
-                           int* counter, const RbDigits* dig, int num_sms, cudaStream_t st);
+                           int* counter, const RbDigits* dig, int mirror_dig, int num_sms,
+                           cudaStream_t st);
 cudaError_t admm_launch(const double* V, int64_t ldv, const double* Vloc, int64_t ldvl,
                         const double* f, double t, const uint32_t* adj, int64_t ldadj,
                         const double* deg, double* Z, int64_t ldz, int n_rows, int n, int row0,

@@ -770,7 +770,8 @@ cudaError_t admm_launch(const double* V, int64_t ldv, const double* Vloc, int64_
     a.rscale = dig->rscale;
     if (r8 && p == 64 && dig->S == 7 && r8_usable(Z, ldz))
       return admm_i8_launch(r8->maps, vf, V, ldv, r8->VF8, r8->V8, r8->rsA, r8->rsB, adj, ldadj,
-                            deg, t, Z, ldz, n, obj, partials, counter, dig, r8->num_sms, st);
+                            deg, t, Z, ldz, n, obj, partials, counter, dig, r8->mirror_dig,
+                            r8->num_sms, st);
   }
   return rb_dispatch<false>(p, a, st);
 }

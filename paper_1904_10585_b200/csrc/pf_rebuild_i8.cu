@@ -61,6 +61,7 @@ struct R8Args {
   const double* deg;
   double tt;
   int n, TC, MT, KB;
+  int mirror_dig;     // 0: the digit slices of the upper tiles only (K1-i8s reads no others)
   const int* E;       // global digit exponent Eg of Z_new
   double* rscale;
   double* partials;
@@ -277,9 +278,12 @@ __global__ void __launch_bounds__(kR8Threads, 1)
 #pragma unroll
           for (int k = 0; k < 8; ++k) tma_store_2d(&m.zm, smem + kOffM + k * 4096, i0 + 16 * k, j0);
           const int kb0 = i0 >> 6, jt = (j0 >> 7) * a.KB;
-          tma_store_3d(&m.dm, smem + kOffDm, 0, j0 & 127, (jt + kb0) * kR8S);
-          if (kb0 + 1 < a.KB)
-            tma_store_3d(&m.dm, smem + kOffDm + kR8S * 2048, 0, j0 & 127, (jt + kb0 + 1) * kR8S);
+          if (a.mirror_dig) {
+            tma_store_3d(&m.dm, smem + kOffDm, 0, j0 & 127, (jt + kb0) * kR8S);
+            if (kb0 + 1 < a.KB)
+              tma_store_3d(&m.dm, smem + kOffDm + kR8S * 2048, 0, j0 & 127,
+                           (jt + kb0 + 1) * kR8S);
+          }
         }
         bulk_commit();
         bulk_wait_read0();
@@ -448,6 +452,7 @@ __global__ void __launch_bounds__(kR8Threads, 1)
         // with lane u ^ 2, then bytes with lane u ^ 1.  [kb][slice][32 rows][64 B], SWIZZLE_64B
         // (16-byte chunk ^= bits 7-8 of the offset)
         const int rb = 32 * q + (lane & ~3);
+        if (a.mirror_dig)
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
           const int jj = 16 * h + 4 * g + u;
@@ -558,7 +563,8 @@ cudaError_t admm_i8_launch(const CUtensorMap* maps, const double* VF, const doub
                            int64_t ldv, int8_t* VF8, int8_t* V8, double* rsA, double* rsB,
                            const uint32_t* adj, int64_t ldadj, const double* deg, double t,
                            double* Z, int64_t ldz, int n, double* obj, double* partials,
-                           int* counter, const RbDigits* dig, int num_sms, cudaStream_t st) {
+                           int* counter, const RbDigits* dig, int mirror_dig, int num_sms,
+                           cudaStream_t st) {
   const int mtiles = (n + 127) / 128, rows_pad = mtiles * 128;
   R8Maps m;
   m.a = maps[0];
@@ -587,6 +593,7 @@ cudaError_t admm_i8_launch(const CUtensorMap* maps, const double* VF, const doub
   a.TC = (n + kR8N - 1) / kR8N;
   a.MT = mtiles;
   a.KB = dig->KB;
+  a.mirror_dig = mirror_dig;
   a.E = dig->E;
   a.rscale = dig->rscale;
   a.partials = partials;

@@ -127,6 +127,23 @@ def test_trajectory_matches_oracle(cfg):
             assert y["objective"] == pytest.approx(x["objective"], rel=1e-10)
 
 
+@pytest.mark.parametrize("graphs", [False, True])
+def test_pfam_trajectory_half_storage_filter(monkeypatch, graphs):
+    """PF_I8SYM=1: the PFAM iterate's fused digits are written for the upper tiles only and every
+    product runs the half-storage symmetric kernel (lower tiles = stored upper tiles read
+    transposed, K1-i8s); the trajectory matches the oracle at the fp64 bar."""
+    from paper_1904_10585_b200 import run
+    monkeypatch.setenv("PF_I8SYM", "1")
+    cfg = CFGS[2]
+    ref = O.run(cfg)["records"]
+    out = run(cfg, graphs=graphs)["records"]
+    for x, y in zip(ref, out):
+        den = max(O.lowrank_fro(x["V"], x["f"]), 1e-300)
+        assert O.lowrank_diff_fro(x["V"], x["f"], y["V"], y["f"]) <= 1e-10 * den
+        if "objective" in x:
+            assert y["objective"] == pytest.approx(x["objective"], rel=1e-10)
+
+
 @pytest.mark.parametrize("cfg", CFGS[1:3], ids=IDS[1:3])
 def test_graph_replay_bit_identical(cfg):
     from paper_1904_10585_b200 import run
@@ -273,12 +290,16 @@ def _digit_bound(X, p):
 
 @pytest.mark.parametrize("n", [64, 100, 300, 1333, 2050])
 @pytest.mark.parametrize("form", ["diag", "matrix"])
-def test_pfam_update_int8_matches_oracle(monkeypatch, n, form):
+@pytest.mark.parametrize("sym", ["1", "0"])
+def test_pfam_update_int8_matches_oracle(monkeypatch, n, form, sym):
     """PFAM update with W = V' V^T from int8 tcgen05 digit products (pf_rebuild_i8.cu, one GPU,
     p = 64, fused digits): Z_new = offdiag(W - tC) + Diag(1 - W_ii + Z_ii) element by element
     within the digit-split bound of the exact W (eq:PFAM1 P:389), <C, W> and ||Z_new - Z||_F;
     ragged n (tiles of 128 x 32), the 128 x 128 diagonal blocks, n < 128.  PF_K7I8=0 (the DMMA
-    update) agrees within the same bound."""
+    update) agrees within the same bound.  The next product from the fused digits: the
+    half-storage symmetric kernel (upper tiles only, the lower ones read transposed; K1-i8s) or,
+    PF_I8SYM=0, the full stream-K kernel -- within the split bound of Z_new Y."""
+    monkeypatch.setenv("PF_I8SYM", sym)
     from paper_1904_10585_b200._lib import Context, PF_FP64_I8
     from paper_1904_10585_b200.solver import _bits
     from pfinputs import sym_bernoulli_bitmask, unpack_bitmask
