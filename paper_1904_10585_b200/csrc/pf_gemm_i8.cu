@@ -356,7 +356,8 @@ __global__ void __launch_bounds__(I8Cfg<S, NC>::THREADS, 1)
     uint32_t tph = 0;
     SegIter si(U, G, blockIdx.x, KB);
     int it, kbs, kbe;
-    const uint32_t ring_a0 = smem_u32(ring_a), ring_b0 = smem_u32(ring_b);
+    const uint64_t adesc_ring = tc::sdesc_k_sw64(smem_u32(ring_a));
+    const uint64_t bdesc_ring = tc::sdesc_k_sw64(smem_u32(ring_b));
     while (si.next(it, kbs, kbe)) {
       for (int k0 = kbs; k0 < kbe; k0 += kch) {
         const int k1 = min(kbe, k0 + kch);
@@ -364,24 +365,27 @@ __global__ void __launch_bounds__(I8Cfg<S, NC>::THREADS, 1)
         tc::fence_after_sync();
         for (int kb = k0; kb < k1; ++kb) {
           mbar_wait(&bfull[rb.s], rb.ph);
-          const uint32_t b0 = ring_b0 + rb.s * C::B_STAGE;
+          // descriptors by addition: the start-address field is (addr >> 4) in the low 14 bits
+          // (smem < 256 KB, no carry out), so desc(addr + off) = desc(addr) + off / 16 -- a few
+          // integer adds per MMA instead of rebuilding every descriptor
+          const uint64_t bd0 = bdesc_ring + (uint64_t)(rb.s * (C::B_STAGE >> 4));
 #pragma unroll
           for (int s = 0; s < S; ++s) {
             mbar_wait(&afull[ra.s], ra.ph);
             tc::fence_after_sync();
-            const uint32_t a0 = ring_a0 + ra.s * C::A_TILE;
+            const uint64_t ad0 = adesc_ring + (uint64_t)(ra.s * (C::A_TILE >> 4));
             if (i8::elect_one()) {
 #pragma unroll
               for (int ks = 0; ks < 2; ++ks) {
                 const uint32_t acc = (kb == k0 && s == 0 && ks == 0) ? 0u : 1u;
-                const uint64_t ad = tc::sdesc_k_sw64(a0 + ks * 32);
+                const uint64_t ad = ad0 + (uint64_t)(ks * 2);
                 // A_s x [B_0 .. B_{S-1-s}] -> levels s .. S-1 (0-based), chunks of <= CMAX
                 // slices; s = 0 initialises every level
 #pragma unroll
                 for (int t0 = 0; t0 < S - s; t0 += C::CMAX) {
                   const int c = (S - s - t0) < C::CMAX ? (S - s - t0) : C::CMAX;
                   i8::mma_i8(tmem + (uint32_t)((s + t0) * NC), ad,
-                             tc::sdesc_k_sw64(b0 + t0 * NC * C::BK + ks * 32),
+                             bd0 + (uint64_t)((t0 * NC * C::BK + ks * 32) >> 4),
                              i8::idesc_i8(C::BM, c * NC), acc);
                 }
               }
