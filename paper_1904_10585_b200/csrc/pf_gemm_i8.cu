@@ -245,6 +245,29 @@ __device__ __forceinline__ int seg_owner(long long u, long long U, int G) {
   return b;
 }
 
+// v[j] += sum_L 128^-(L+2) D_L[c0 + j], L = S-1 .. 0 in that order (smallest weight first),
+// one TMEM wait per level (all CW columns of the level in flight)
+template <int S, int NC, int CW>
+__device__ __forceinline__ void i8_combine_levels(uint32_t taddr, int c0, double (&v)[CW]) {
+  static_assert(CW % 16 == 0, "CW");
+  struct R16 {
+    uint32_t x[16];
+  };
+#pragma unroll 1
+  for (int L = S - 1; L >= 0; --L) {
+    R16 a[CW / 16];
+#pragma unroll
+    for (int h = 0; h < CW / 16; ++h)
+      i8::tmem_ld16_nw(taddr + (uint32_t)(L * NC + c0 + 16 * h), a[h].x);
+    i8::tmem_wait_ld();
+    const double w = i8::pow2(-7 * (L + 2));
+#pragma unroll
+    for (int h = 0; h < CW / 16; ++h)
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[16 * h + j] = fma((double)(int)a[h].x[j], w, v[16 * h + j]);
+  }
+}
+
 struct RingI {
   int n, s;
   uint32_t ph;
@@ -426,6 +449,86 @@ __global__ void __launch_bounds__(I8Cfg<S, NC>::THREADS, 1)
         nparts = seg_owner((long long)it * KB + KB - 1, U, G) - f + 1;
       }
       double* mypart = args.part + ((size_t)it * args.maxp + part) * (NC * 128) + et;
+      if (!whole && kbe - kbs <= kch) {
+        // ------------------------------------------------ split item, one accumulation
+        // If every other contributor has already published its partial (the usual case: this
+        // CTA runs the item's long part), the item is finished straight from TMEM without
+        // writing and re-reading this CTA's partial.  Sum order is the general fixup's (parts
+        // in index order, this one in its slot): bit-identical either way.
+        mbar_wait(tfull, tph);
+        tph ^= 1u;
+        tc::fence_after_sync();
+        named_bar_sync(1, 128);
+        if (et == 0) *sflag = (atomicAdd(&args.counters[it], 0) + 1 == nparts) ? 1 : 0;
+        named_bar_sync(1, 128);
+        const bool early = (*sflag != 0);
+        named_bar_sync(1, 128);
+        bool lastc = early;
+        if (!early) {
+#pragma unroll 1
+          for (int c0 = 0; c0 < NC; c0 += C::CW) {
+            double v[C::CW];
+#pragma unroll
+            for (int j = 0; j < C::CW; ++j) v[j] = 0.0;
+            i8_combine_levels<S, NC, C::CW>(taddr, c0, v);
+#pragma unroll
+            for (int j = 0; j < C::CW; ++j) __stcg(mypart + (size_t)(c0 + j) * 128, v[j]);
+          }
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(tempty);
+          __threadfence();
+          named_bar_sync(1, 128);
+          if (et == 0) *sflag = (atomicAdd(&args.counters[it], 1) + 1 == nparts) ? 1 : 0;
+          named_bar_sync(1, 128);
+          lastc = (*sflag != 0);
+          named_bar_sync(1, 128);
+        } else {
+          __threadfence();
+        }
+        if (lastc) {
+          const double* p0 = args.part + (size_t)it * args.maxp * (NC * 128) + et;
+#pragma unroll 1
+          for (int c0 = 0; c0 < NC; c0 += C::CW) {
+            double m[C::CW];  // this CTA's part: from TMEM (early) or its own published partial
+#pragma unroll
+            for (int j = 0; j < C::CW; ++j) m[j] = 0.0;
+            if (early) i8_combine_levels<S, NC, C::CW>(taddr, c0, m);
+            double v[C::CW];
+#pragma unroll
+            for (int j = 0; j < C::CW; ++j) v[j] = 0.0;
+#pragma unroll 1
+            for (int q2 = 0; q2 < nparts; ++q2) {
+              if (q2 == part && early) {
+#pragma unroll
+                for (int j = 0; j < C::CW; ++j) v[j] += m[j];
+              } else {
+#pragma unroll
+                for (int j = 0; j < C::CW; ++j)
+                  v[j] += __ldcg(p0 + (size_t)q2 * (NC * 128) + (size_t)(c0 + j) * 128);
+              }
+            }
+            if (row_ok) {
+              const int cbase = cg * NC + c0;
+              const size_t o = (size_t)row * args.ldy + cbase;
+#pragma unroll
+              for (int j = 0; j < C::CW; ++j) {
+                double y = s1 * (v[j] * rs * __ldg(args.cscale + cbase + j));
+                if (s2 != 0.0) y = fma(s2, args.ycur[o + j], y);
+                if (s3 != 0.0) y = fma(s3, args.yprev[o + j], y);
+                args.out[o + j] = y;
+              }
+            }
+          }
+          if (et == 0) args.counters[it] = 0;  // ready for the next launch
+        }
+        if (early) {
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(tempty);
+        }
+        continue;
+      }
       for (int k0 = kbs; k0 < kbe; k0 += kch) {
         const bool first = (k0 == kbs), last = (k0 + kch >= kbe);
         mbar_wait(tfull, tph);
@@ -437,17 +540,7 @@ __global__ void __launch_bounds__(I8Cfg<S, NC>::THREADS, 1)
 #pragma unroll
           for (int j = 0; j < C::CW; ++j) v[j] = 0.0;
           // smallest level first: level L (0-based) carries weight 128^-(L+2)
-#pragma unroll 1
-          for (int L = S - 1; L >= 0; --L) {
-            const double w = i8::pow2(-7 * (L + 2));
-#pragma unroll
-            for (int h = 0; h < C::CW; h += 16) {
-              uint32_t r[16];
-              i8::tmem_ld16(taddr + (uint32_t)(L * NC + c0 + h), r);
-#pragma unroll
-              for (int j = 0; j < 16; ++j) v[h + j] = fma((double)(int)r[j], w, v[h + j]);
-            }
-          }
+          i8_combine_levels<S, NC, C::CW>(taddr, c0, v);
           if (!first) {
 #pragma unroll
             for (int j = 0; j < C::CW; ++j) v[j] += __ldcg(accp + (size_t)(c0 + j) * 128);
@@ -487,7 +580,7 @@ __global__ void __launch_bounds__(I8Cfg<S, NC>::THREADS, 1)
         named_bar_sync(1, 128);
         if (lastc) {
           __threadfence();
-          const double* p0 = args.part + (size_t)it * args.maxp * (NC * 128) + et;
+            const double* p0 = args.part + (size_t)it * args.maxp * (NC * 128) + et;
 #pragma unroll 1
           for (int c0 = 0; c0 < NC; c0 += C::CW) {
             double v[C::CW];
@@ -694,17 +787,7 @@ __global__ void __launch_bounds__(SymCfg::THREADS, 1)
       double v[C::CW];
 #pragma unroll
       for (int j = 0; j < C::CW; ++j) v[j] = 0.0;
-#pragma unroll 1
-      for (int L = S - 1; L >= 0; --L) {
-        const double w = i8::pow2(-7 * (L + 2));
-#pragma unroll
-        for (int h = 0; h < C::CW; h += 16) {
-          uint32_t r[16];
-          i8::tmem_ld16(taddr + (uint32_t)(L * NC + c0 + h), r);
-#pragma unroll
-          for (int j = 0; j < 16; ++j) v[h + j] = fma((double)(int)r[j], w, v[h + j]);
-        }
-      }
+      i8_combine_levels<S, NC, C::CW>(taddr, c0, v);
       if (row_ok) {
         const size_t o = (size_t)row * args.ldy + c0;
 #pragma unroll
