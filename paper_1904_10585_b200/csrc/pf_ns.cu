@@ -319,10 +319,10 @@ __global__ void __launch_bounds__(512) pd_test_kernel(const double* __restrict__
   __syncthreads();
   // ||H||_inf and ||H||_F: a bound on the spread max |theta| of the Ritz values for the next
   // re-base plan (the PD path computes no Ritz values)
-  for (int i = tid; i < p; i += nt) {
+  for (int i = tid; i < p; i += nt) {  // row i of the symmetric H from the lower triangle in M
     double r = 0.0, f = 0.0;
     for (int k = 0; k < p; ++k) {
-      const double v = F[(size_t)i * p + k];
+      const double v = k <= i ? M[i * P1 + k] : M[k * P1 + i];
       r += fabs(v);
       f += v * v;
     }

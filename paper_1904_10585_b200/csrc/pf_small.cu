@@ -54,19 +54,35 @@ __global__ void __launch_bounds__(256) gram_partial_kernel(const double* __restr
 #pragma unroll
       for (int i = 0; i < 4; ++i) acc[w][nt][i] = 0.0;
 
-  for (int rb = r0; rb < r1; rb += C::R) {
-    for (int e = threadIdx.x; e < C::R * P / 2; e += 256) {
+  // sub-chunk loads staged in registers one chunk ahead: every load of a chunk is in flight at
+  // once, and the next chunk's loads overlap this chunk's DMMAs
+  constexpr int NE = C::R * P / 2 / 256;  // double2 per thread per matrix per chunk
+  static_assert(NE >= 1 && (C::R * P / 2) % 256 == 0, "chunk split");
+  double2 xr[NE], yr[NE];
+  auto load = [&](int rb) {
+#pragma unroll
+    for (int i = 0; i < NE; ++i) {
+      const int e = threadIdx.x + 256 * i;
       const int rr = e / (P / 2), cc = (e % (P / 2)) * 2;
       const int row = rb + rr;
-      double2 x = make_double2(0.0, 0.0), y = make_double2(0.0, 0.0);
+      xr[i] = yr[i] = make_double2(0.0, 0.0);
       if (row < r1) {
-        x = *reinterpret_cast<const double2*>(X + (size_t)row * P + cc);
-        y = *reinterpret_cast<const double2*>(Y + (size_t)row * P + cc);
+        xr[i] = __ldcg(reinterpret_cast<const double2*>(X + (size_t)row * P + cc));
+        yr[i] = __ldcg(reinterpret_cast<const double2*>(Y + (size_t)row * P + cc));
       }
-      *reinterpret_cast<double2*>(Xs + rr * C::LD + cc) = x;
-      *reinterpret_cast<double2*>(Ys + rr * C::LD + cc) = y;
+    }
+  };
+  if (r0 < r1) load(r0);
+  for (int rb = r0; rb < r1; rb += C::R) {
+#pragma unroll
+    for (int i = 0; i < NE; ++i) {
+      const int e = threadIdx.x + 256 * i;
+      const int rr = e / (P / 2), cc = (e % (P / 2)) * 2;
+      *reinterpret_cast<double2*>(Xs + rr * C::LD + cc) = xr[i];
+      *reinterpret_cast<double2*>(Ys + rr * C::LD + cc) = yr[i];
     }
     __syncthreads();
+    if (rb + C::R < r1) load(rb + C::R);
 #pragma unroll
     for (int w = 0; w < C::PER_WARP; ++w) {
       const int wt = warp + 8 * w;
@@ -102,11 +118,23 @@ __global__ void __launch_bounds__(256) gram_partial_kernel(const double* __restr
     }
   }
   cooperative_groups::this_grid().sync();
+  // G[e] = sum over the CTA partials: TPE lanes per entry (a power of two up to 32, as many as the
+  // grid has threads for), each summing every TPE-th partial in order, then a fixed xor tree
+  // (deterministic; 8 lanes per entry at p = 64 instead of one lane walking 128 partials)
   const int nb = gridDim.x;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < P * P; e += gridDim.x * blockDim.x) {
+  const int nthr = gridDim.x * blockDim.x;
+  int tpe = 1;
+  while (tpe < 32 && tpe * 2 * P * P <= nthr) tpe *= 2;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int sub = gt & (tpe - 1);
+  // warp-uniform trip count (the shuffles need every lane): entries e0 = base + lane / tpe
+  for (int base = (gt >> 5) * (32 / tpe); base < P * P; base += nthr / tpe) {
+    const int e0 = base + (threadIdx.x & 31) / tpe;
     double s = 0.0;
-    for (int b = 0; b < nb; ++b) s += __ldcg(partials + (size_t)b * P * P + e);
-    G[e] = s;
+    if (e0 < P * P)
+      for (int b = sub; b < nb; b += tpe) s += __ldcg(partials + (size_t)b * P * P + e0);
+    for (int o = 1; o < tpe; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (sub == 0 && e0 < P * P) G[e0] = s;
   }
 }
 
@@ -428,16 +456,36 @@ __global__ void __launch_bounds__(256) rmul_kernel(const double* in, int64_t ldi
   double* Ys = sm + P * C::LD;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g8 = lane >> 2, t4 = lane & 3;
   const int row0 = blockIdx.x * C::BM;
-  for (int e = threadIdx.x; e < P * P / 2; e += 256) {
+  // all loads into registers first (in / out may alias, so the compiler will not hoist loads
+  // above the shared-memory stores by itself): one memory latency instead of one per element
+  constexpr int NR = (P * P / 2 + 255) / 256, NY = (C::BM * P / 2 + 255) / 256;
+  double2 rv[NR], yv[NY];
+#pragma unroll
+  for (int i = 0; i < NR; ++i) {
+    const int e = threadIdx.x + 256 * i;
     const int r = e / (P / 2), c = (e % (P / 2)) * 2;
-    *reinterpret_cast<double2*>(Rs + r * C::LD + c) =
-        *reinterpret_cast<const double2*>(R + r * P + c);
+    rv[i] = e < P * P / 2 ? __ldg(reinterpret_cast<const double2*>(R + r * P + c))
+                          : make_double2(0.0, 0.0);
   }
-  for (int e = threadIdx.x; e < C::BM * P / 2; e += 256) {
+#pragma unroll
+  for (int i = 0; i < NY; ++i) {
+    const int e = threadIdx.x + 256 * i;
     const int r = e / (P / 2), c = (e % (P / 2)) * 2;
-    double2 v = make_double2(0.0, 0.0);
-    if (row0 + r < n_rows) v = *reinterpret_cast<const double2*>(in + (size_t)(row0 + r) * ldi + c);
-    *reinterpret_cast<double2*>(Ys + r * C::LD + c) = v;
+    yv[i] = make_double2(0.0, 0.0);
+    if (e < C::BM * P / 2 && row0 + r < n_rows)
+      yv[i] = *reinterpret_cast<const double2*>(in + (size_t)(row0 + r) * ldi + c);
+  }
+#pragma unroll
+  for (int i = 0; i < NR; ++i) {
+    const int e = threadIdx.x + 256 * i;
+    const int r = e / (P / 2), c = (e % (P / 2)) * 2;
+    if (e < P * P / 2) *reinterpret_cast<double2*>(Rs + r * C::LD + c) = rv[i];
+  }
+#pragma unroll
+  for (int i = 0; i < NY; ++i) {
+    const int e = threadIdx.x + 256 * i;
+    const int r = e / (P / 2), c = (e % (P / 2)) * 2;
+    if (e < C::BM * P / 2) *reinterpret_cast<double2*>(Ys + r * C::LD + c) = yv[i];
   }
   __syncthreads();
   const int wm = warp & 3, wn = warp >> 2;
