@@ -275,7 +275,7 @@ static pf_status alloc_all(pf_ctx ctx) {
     }
     ok &= A((void**)&ctx->Y8, (size_t)kI8MaxSlices * p * ip.kpad);
     ok &= A((void**)&ctx->y8_cscale, (size_t)p * 8);
-    ok &= A((void**)&ctx->y8_cmax, (size_t)p * 8);
+    ok &= A((void**)&ctx->y8_cmax, (size_t)(2 * p + 1) * 8);  // two halves + selector
     ok &= A((void**)&ctx->i8_acc, ip.acc_doubles * 8);
     // sized for the largest plan of any slice count (the split does not depend on S)
     ok &= A((void**)&ctx->i8_part, ip.part_doubles * 8);
@@ -363,6 +363,7 @@ static pf_status alloc_all(pf_ctx ctx) {
     return PF_ERR_CUDA;
   }
   if (ctx->i8) PF_CU(cudaMemset(ctx->i8_cnt, 0, (size_t)ctx->i8plan.items * 4));
+  if (ctx->i8) PF_CU(cudaMemset(ctx->y8_cmax, 0, (size_t)(2 * ctx->p + 1) * 8));
   if (ctx->i8 && !encode_i8_maps(ctx)) {
     snprintf(ctx->err, sizeof(ctx->err), "cuTensorMapEncodeTiled(int8 slices) failed");
     return PF_ERR_CUDA;

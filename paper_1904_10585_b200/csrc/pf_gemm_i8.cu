@@ -167,6 +167,66 @@ __global__ void __launch_bounds__(256) y_colmax_split_kernel(const double* __res
   }
 }
 
+// The same split in ONE grid barrier when every 32-row chunk has its own CTA (p <= 64): each CTA
+// loads its chunk once into shared memory, publishes the chunk's column maxima (atomicMax), waits
+// at the barrier, and splits the chunk from shared memory -- no second read of Y and no barrier
+// for zeroing the accumulator, which alternates between two halves of cmax (cmax[2p] selects the
+// half; the other half is zeroed for the next call).
+template <int S>
+__global__ void __launch_bounds__(256) y_split_tile_kernel(const double* __restrict__ Y,
+                                                          int64_t ldy, int n_k, int p,
+                                                          unsigned long long* cmax,
+                                                          int8_t* __restrict__ Y8, int64_t kpad,
+                                                          double* __restrict__ cscale) {
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  constexpr int R = 32;
+  __shared__ double tile[R * 65];
+  __shared__ double smx[256];
+  const int sel = (int)__ldcg(cmax + 2 * p);
+  unsigned long long* cm = cmax + (size_t)sel * p;
+  const int k0 = blockIdx.x * R;
+  const int half = p >> 1;
+  for (int i = threadIdx.x; i < R * half; i += blockDim.x) {
+    const int r = i / half, c = (i - r * half) * 2;
+    double2 v = make_double2(0.0, 0.0);
+    if (k0 + r < n_k) v = __ldcg(reinterpret_cast<const double2*>(Y + (int64_t)(k0 + r) * ldy + c));
+    tile[r * 65 + c] = v.x;
+    tile[r * 65 + c + 1] = v.y;
+  }
+  __syncthreads();
+  {
+    const int c = threadIdx.x % p, r0 = threadIdx.x / p, rstep = blockDim.x / p;
+    double m = 0.0;
+    for (int r = r0; r < R; r += rstep) m = fmax(m, fabs(tile[r * 65 + c]));
+    smx[threadIdx.x] = m;
+    __syncthreads();
+    if (threadIdx.x < p) {
+      for (int k = 1; k < rstep; ++k) m = fmax(m, smx[k * p + threadIdx.x]);
+      if (m > 0.0) atomicMax(cm + c, (unsigned long long)__double_as_longlong(m));
+    }
+  }
+  grid.sync();
+  if (blockIdx.x == 0) {
+    for (int c = threadIdx.x; c < p; c += blockDim.x) cmax[(size_t)(1 - sel) * p + c] = 0ull;
+    if (threadIdx.x == 0) cmax[2 * p] = (unsigned long long)(1 - sel);  // every CTA read sel
+  }
+  for (int i = threadIdx.x; i < p * (R / 8); i += blockDim.x) {
+    const int c = i / (R / 8), g = i % (R / 8);  // column, 8-row group
+    const int E = i8::scale_exp(__longlong_as_double((long long)__ldcg(cm + c)));
+    if (blockIdx.x == 0 && g == 0) cscale[c] = i8::pow2(E);
+    uint32_t lo[S], hi[S];
+    const double* tc0 = tile + (g * 8) * 65 + c;
+    i8::slices4<S>(tc0[0], tc0[65], tc0[130], tc0[195], E, lo);
+    i8::slices4<S>(tc0[260], tc0[325], tc0[390], tc0[455], E, hi);
+    const int k = k0 + g * 8;
+    if (k < n_k) {
+#pragma unroll
+      for (int s = 0; s < S; ++s)
+        *reinterpret_cast<uint2*>(Y8 + ((int64_t)s * p + c) * kpad + k) = make_uint2(lo[s], hi[s]);
+    }
+  }
+}
+
 // ------------------------------------------------------------------------------ GEMM
 template <int S, int NC>
 struct I8Cfg {
@@ -881,11 +941,21 @@ static cudaError_t y_split_s(const double* Y, int64_t ldy, const I8Plan& pl,
     per_sm = std::max(1, std::min(per_sm, 4));
   }
   const int chunks = (pl.n_k + 31) / 32;
-  const int grid = std::max(1, std::min(chunks, per_sm * num_sms));
   int n_k = pl.n_k, p = pl.p;
   int64_t kpad = pl.kpad;
   void* args[] = {(void*)&Y, (void*)&ldy, (void*)&n_k, (void*)&p, (void*)&cmax, (void*)&Y8,
                   (void*)&kpad, (void*)&cscale};
+  static int per_sm_t = 0;
+  if (!per_sm_t) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_t, y_split_tile_kernel<S>, 256, 0);
+    per_sm_t = std::max(1, per_sm_t);
+  }
+  if (p <= 64 && (ldy % 2) == 0 && chunks <= per_sm_t * num_sms) {
+    count_launch();
+    return cudaLaunchCooperativeKernel((const void*)y_split_tile_kernel<S>, dim3(chunks),
+                                       dim3(256), args, 0, st);
+  }
+  const int grid = std::max(1, std::min(chunks, per_sm * num_sms));
   count_launch();
   return cudaLaunchCooperativeKernel((const void*)y_colmax_split_kernel<S>, dim3(grid), dim3(256),
                                      args, 0, st);
