@@ -288,7 +288,7 @@ def _digit_bound(X, p):
     return 2.0 ** e
 
 
-@pytest.mark.parametrize("n", [64, 100, 300, 1333, 2050])
+@pytest.mark.parametrize("n", [64, 100, 300, 1333, 2050, 5000])
 @pytest.mark.parametrize("form", ["diag", "matrix"])
 @pytest.mark.parametrize("sym", ["1", "0"])
 def test_pfam_update_int8_matches_oracle(monkeypatch, n, form, sym):
