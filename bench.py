@@ -357,7 +357,10 @@ def run_e2e(cfg, args, stream) -> dict:
     host = {"adj_bits": torch.from_numpy(prob["adj_bits"].view(np.int32)).pin_memory(),
             "deg": torch.from_numpy(prob["deg"]).pin_memory(),
             "U0": torch.from_numpy(initial_block(cfg)).pin_memory()}
-    K = args.steps + args.warmup
+    # the configured job: config 3 is a 100-iteration solve (BASELINE.json configs[2]), so the
+    # fixed costs of a solve (k = 0 with its warm-up sweeps and 20-step Lanczos, graph capture,
+    # uploads) are spread over the job's own length, not over the bench's timed-step count
+    K = max(args.steps + args.warmup, cfg.iters)
     # seeded Lanczos start vectors the run uses (only k = 0 when refreshes are warm-started, R29)
     v0 = {k: torch.from_numpy(lanczos_start(cfg, k)).pin_memory()
           for k in range(K) if k % cfg.lanczos_every == 0 and (k == 0 or cfg.lanczos_warm <= 0)}
@@ -391,9 +394,10 @@ def run_e2e(cfg, args, stream) -> dict:
     return {"value": K / (ms / 1e3),
             "unit": "it/s", "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": d2h / K,
             "iterations": K, "ms_total": ms,
-            "what": "solve from host data on a pre-created context: H2D problem + U0, solver "
-                    "state, W+K iterations (graph capture included), per-iteration objective "
-                    "D2H, final factors D2H"}
+            "what": "the configured solve (cfg.iters iterations, at least warmup + steps) from "
+                    "host data on a pre-created context: H2D problem + U0, solver state, every "
+                    "iteration (graph capture included), per-iteration objective D2H, final "
+                    "factors D2H"}
 
 
 # ============================================================================ CPU oracle
