@@ -249,6 +249,12 @@ size_t r8_bytes(int n);
 bool r8_encode(CUtensorMap* maps, const int8_t* VF8, const int8_t* V8, const int8_t* A8, int n,
                int KB);
 bool r8_usable(const double* Z, int64_t ldz);  // TMA on Z: even pitch, 16-byte aligned base
+// PF_FP64, one GPU, p = 64: the TMA-staged PFAM update with W on DMMA (pf_rebuild_i8.cu)
+bool td_usable(const double* VF, const double* V, int64_t ldv, const double* Z, int64_t ldz);
+cudaError_t admm_tma_launch(const double* VF, const double* V, int64_t ldv, const uint32_t* adj,
+                            int64_t ldadj, const double* deg, double t, double* Z, int64_t ldz,
+                            int n, double* obj, double* partials, int* counter, int num_sms,
+                            cudaStream_t st);
 cudaError_t admm_i8_launch(const CUtensorMap* maps, const double* VF, const double* V,
                            int64_t ldv, int8_t* VF8, int8_t* V8, double* rsA, double* rsB,
                            const uint32_t* adj, int64_t ldadj, const double* deg, double t,

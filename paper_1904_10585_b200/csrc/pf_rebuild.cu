@@ -772,6 +772,19 @@ cudaError_t admm_launch(const double* V, int64_t ldv, const double* Vloc, int64_
       return admm_i8_launch(r8->maps, vf, V, ldv, r8->VF8, r8->V8, r8->rsA, r8->rsB, adj, ldadj,
                             deg, t, Z, ldz, n, obj, partials, counter, dig, r8->mirror_dig,
                             r8->num_sms, st);
+  } else if (p == 64 && row0 == 0 && n_rows == n && !raw && td_usable(vf, V, ldv, Z, ldz)) {
+    // one GPU, no digit output: the TMA-staged update with W on DMMA (PF_K7TMA=0: rebuild_kernel)
+    static int use = -1, sms = 148;
+    if (use < 0) {
+      const char* e = getenv("PF_K7TMA");
+      use = !(e && e[0] == '0');
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    if (use)
+      return admm_tma_launch(vf, V, ldv, adj, ldadj, deg, t, Z, ldz, n, obj, partials, counter,
+                             sms, st);
   }
   return rb_dispatch<false>(p, a, st);
 }

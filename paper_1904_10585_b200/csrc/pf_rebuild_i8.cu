@@ -38,6 +38,9 @@
 
 namespace pf {
 
+bool encode_map_gen(CUtensorMap* map, bool f64, int rank, const void* base, const uint64_t* dims,
+                    const uint64_t* strides, const uint32_t* box, int swizzle);
+
 constexpr int kR8S = 7;                        // digit slices of V', V and Z_new
 constexpr int kR8M = 128, kR8N = 32;           // tile
 constexpr int kR8Threads = 384;
@@ -507,6 +510,332 @@ __global__ void __launch_bounds__(kR8Threads, 1)
   }
 }
 
+// ============================================================================== fp64 variant
+// The same TMA-staged PFAM update for PF_FP64 contexts (no digit output, one GPU, p = 64), with
+// W = V' V^T formed in fp64 on DMMA (mma.sync m16n8k4) by the 8 compute warps from shared-memory
+// panels instead of int8 digit products: V' row block (128 x 64, four SWIZZLE_128B boxes,
+// reloaded when I changes), V column block (32 x 64, two stages), Z_old tiles (two buffers), Z_new
+// written in place and by TMA stores with its mirror.  The DMMA rebuild_kernel (K7) interleaves
+// the product with LSU loads / stores inside each CTA and runs at 0.46 of HBM at config 3.
+//   warp 0   TMA loads          warp 1   TMA stores
+//   warps 2-9  compute: warp w owns rows 16w .. 16w+15 of the tile (all 32 columns, 4 n8 blocks)
+constexpr int kTdThreads = 320;
+constexpr int kTdOffVi = 0;                    // 4 boxes {16 fp64, 128 rows} = 64 KB
+constexpr int kTdOffVj = kTdOffVi + 65536;     // 2 stages x 4 boxes {16, 32} = 2 x 16 KB
+constexpr int kTdOffZ = kTdOffVj + 32768;      // 2 buffers x 2 boxes {16, 128}
+constexpr int kTdOffM = kTdOffZ + 65536;       // mirror: 8 boxes {16, 32}
+constexpr int kTdOffBar = kTdOffM + 32768;
+constexpr int kTdSmem = kTdOffBar + 256 + 1024;
+static_assert(kTdSmem <= 232448, "shared memory");
+
+struct TdMaps {
+  CUtensorMap vi, vj;  // V' rows (box {16, 128}), V rows (box {16, 32})
+  CUtensorMap z, zm;   // Z: {16, 128} (tile, Z_old), {16, 32} (mirror)
+};
+
+// element (r, c) of a SWIZZLE_128B box of 16 fp64 columns (128-byte rows): byte offset
+__device__ __forceinline__ int sw128(int r, int c) {
+  return r * 128 + ((((c >> 1) ^ (r & 7))) << 4) + (c & 1) * 8;
+}
+
+__global__ void __launch_bounds__(kTdThreads, 1)
+    rebuild_tma_kernel(const __grid_constant__ TdMaps m, const R8Args a) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kTdOffBar);
+  uint64_t* vifull = bars;
+  uint64_t* viempty = bars + 1;   // compute warps done with this row block's V' panel
+  uint64_t* vjfull = bars + 2;    // [2]
+  uint64_t* vjempty = bars + 4;   // [2]
+  uint64_t* zfull = bars + 6;     // [2]
+  uint64_t* zempty = bars + 8;    // [2]
+  uint64_t* sfull = bars + 10;
+  uint64_t* sempty = bars + 11;
+  __shared__ double red[32];
+  __shared__ int s_last;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    mbar_init(vifull, 1);
+    mbar_init(viempty, 8);
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&vjfull[q], 1);
+      mbar_init(&vjempty[q], 8);
+      mbar_init(&zfull[q], 1);
+      mbar_init(&zempty[q], 1);
+    }
+    mbar_init(sfull, 8);
+    mbar_init(sempty, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&m.vi);
+    tma_prefetch_desc(&m.vj);
+    tma_prefetch_desc(&m.z);
+  }
+  if (warp == 1 && lane == 0) tma_prefetch_desc(&m.zm);
+  __syncthreads();
+
+  const long long ntiles = (long long)a.MT * a.TC - 2LL * a.MT * (a.MT - 1);
+  const long long t_begin = ntiles * blockIdx.x / gridDim.x;
+  const long long t_end = ntiles * (blockIdx.x + 1) / gridDim.x;
+  double s0 = 0.0, s1 = 0.0;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ TMA loads
+    int curI = -1;
+    uint32_t viph = 0;
+    const uint64_t keep = tc::policy_evict_last();    // V', V panels: re-read across tiles
+    const uint64_t stream = tc::policy_evict_first(); // Z_old: read once
+    int it = 0, I = 0, J = 0;
+    if (t_begin < t_end) r8_tile(t_begin, a.TC, a.MT, I, J);
+    for (long long t = t_begin; t < t_end; ++t, ++it, r8_next(a.TC, I, J)) {
+      const int i0 = I * kR8M, j0 = J * kR8N, b = it & 1;
+      mbar_wait_idle(&zempty[b], ((it >> 1) & 1) ^ 1u);
+      if (i8::elect_one()) {
+        mbar_arrive_expect_tx(&zfull[b], 32768);
+        unsigned char* zs = smem + kTdOffZ + b * 32768;
+        tc::tma_load_2d_hint(zs, &m.z, &zfull[b], j0, i0, stream);
+        tc::tma_load_2d_hint(zs + 16384, &m.z, &zfull[b], j0 + 16, i0, stream);
+      }
+      __syncwarp();
+      if (I != curI) {
+        if (curI >= 0) {
+          mbar_wait_idle(viempty, viph);
+          viph ^= 1u;
+        }
+        if (i8::elect_one()) {
+          mbar_arrive_expect_tx(vifull, 65536);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            tc::tma_load_2d_hint(smem + kTdOffVi + q * 16384, &m.vi, vifull, 16 * q, i0, keep);
+        }
+        __syncwarp();
+        curI = I;
+      }
+      mbar_wait_idle(&vjempty[b], ((it >> 1) & 1) ^ 1u);
+      if (i8::elect_one()) {
+        mbar_arrive_expect_tx(&vjfull[b], 16384);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          tc::tma_load_2d_hint(smem + kTdOffVj + b * 16384 + q * 4096, &m.vj, &vjfull[b], 16 * q,
+                               j0, keep);
+      }
+      __syncwarp();
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ TMA stores
+    int it = 0, I = 0, J = 0;
+    if (t_begin < t_end) r8_tile(t_begin, a.TC, a.MT, I, J);
+    for (long long t = t_begin; t < t_end; ++t, ++it, r8_next(a.TC, I, J)) {
+      const int i0 = I * kR8M, j0 = J * kR8N, b = it & 1;
+      const bool diagblk = J < 4 * I + 4;
+      mbar_wait_idle(sfull, it & 1);
+      if (i8::elect_one()) {
+        const unsigned char* zs = smem + kTdOffZ + b * 32768;
+        tma_store_2d(&m.z, zs, j0, i0);
+        tma_store_2d(&m.z, zs + 16384, j0 + 16, i0);
+        if (!diagblk) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) tma_store_2d(&m.zm, smem + kTdOffM + k * 4096, i0 + 16 * k, j0);
+        }
+        bulk_commit();
+        bulk_wait_read0();
+        mbar_arrive(&zempty[b]);
+        mbar_arrive(sempty);
+      }
+      __syncwarp();
+    }
+    if (i8::elect_one()) bulk_wait0();
+    __syncwarp();
+  } else {
+    // ------------------------------------------------------------------ compute warps
+    const int w = warp - 2, g8 = lane >> 2, t4 = lane & 3;
+    const double qt = 0.25 * a.tt;
+    int curI = -1;
+    uint32_t viph = 0;
+    int it = 0, I = 0, J = 0;
+    if (t_begin < t_end) r8_tile(t_begin, a.TC, a.MT, I, J);
+    const unsigned char* vi = smem + kTdOffVi;
+    for (long long t = t_begin; t < t_end; ++t, ++it) {
+      const int i0 = I * kR8M, j0 = J * kR8N, b = it & 1;
+      const bool diagblk = J < 4 * I + 4;
+      const bool fast = !diagblk && (i0 + kR8M <= a.n) && (j0 + kR8N <= a.n);
+      if (I != curI) {
+        if (curI >= 0) {  // release the previous row block's panel
+          __syncwarp();
+          if (lane == 0) mbar_arrive(viempty);
+        }
+        mbar_wait(vifull, viph);
+        viph ^= 1u;
+        curI = I;
+      }
+      // adjacency words of this thread's two rows (columns j0 .. j0+31: one 32-bit word)
+      const int ra = i0 + 16 * w + g8, rb = ra + 8;
+      const uint32_t wa = ra < a.n ? __ldg(a.bits + (size_t)ra * a.ldb + (j0 >> 5)) : 0u;
+      const uint32_t wb = rb < a.n ? __ldg(a.bits + (size_t)rb * a.ldb + (j0 >> 5)) : 0u;
+      // ---- W = V'_I V_J^T on DMMA: rows 16w + (g8, g8 + 8), columns 8 nt + 2 t4 + (0, 1)
+      mbar_wait(&vjfull[b], (it >> 1) & 1);
+      const unsigned char* vj = smem + kTdOffVj + b * 16384;
+      double acc[4][4];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[nt][q] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < 16; ++ks) {
+        const int k = 4 * ks + t4, kb = k >> 4, kc = k & 15;
+        const double a0 = *reinterpret_cast<const double*>(vi + kb * 16384 + sw128(16 * w + g8, kc));
+        const double a1 =
+            *reinterpret_cast<const double*>(vi + kb * 16384 + sw128(16 * w + g8 + 8, kc));
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+          dmma16884(acc[nt], a0, a1,
+                    *reinterpret_cast<const double*>(vj + kb * 4096 + sw128(8 * nt + g8, kc)));
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&vjempty[b]);
+      // ---- the update against Z_old (swizzled buffer), Z_new in place
+      mbar_wait(&zfull[b], (it >> 1) & 1);
+      unsigned char* zs = smem + kTdOffZ + b * 32768;
+      double z[4][2][2];  // [nt][row h][c]
+      double wgt = diagblk ? 1.0 : 2.0;
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = 16 * w + g8 + 8 * h, cc = 8 * nt + 2 * t4;  // tile coordinates
+          double2* zp = reinterpret_cast<double2*>(zs + (cc >> 4) * 16384 + sw128(r, cc & 15));
+          const double2 zo = *zp;
+          const uint32_t word = h ? wb : wa;
+          const int i = i0 + r;
+          double o[2];
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const int j = j0 + cc + c;
+            const double x = acc[nt][2 * h + c], zold = c ? zo.y : zo.x;
+            const bool bit = (word >> (cc + c)) & 1u;
+            if (fast) {
+              o[c] = bit ? x - qt : x;
+              if (bit) s0 += wgt * 0.25 * x;
+              s1 = fma(wgt * (o[c] - zold), o[c] - zold, s1);
+            } else if (i < a.n && j < a.n) {
+              if (j == i) {
+                o[c] = 1.0 - x + zold;                // Diag(1 - W_ii + Z_ii)
+                s0 += -0.25 * a.deg[i] * x;           // C_ii = -deg_i / 4
+                s1 += (o[c] - zold) * (o[c] - zold);
+              } else {
+                o[c] = bit ? x - qt : x;
+                if (bit) s0 += wgt * 0.25 * x;
+                s1 += wgt * (o[c] - zold) * (o[c] - zold);
+              }
+            } else {
+              o[c] = 0.0;
+            }
+            z[nt][h][c] = o[c];
+          }
+          *zp = make_double2(o[0], o[1]);
+        }
+      // ---- mirror staging (after the previous tile's stores read it)
+      mbar_wait(sempty, (it & 1) ^ 1u);
+      if (!diagblk) {
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              const int r = 16 * w + g8 + 8 * h, jj = 8 * nt + 2 * t4 + c;
+              *reinterpret_cast<double*>(smem + kTdOffM + (r >> 4) * 4096 + sw128(jj, r & 15)) =
+                  z[nt][h][c];
+            }
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(sfull);
+      // next tile
+      r8_next(a.TC, I, J);
+    }
+    if (curI >= 0) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(viempty);
+    }
+  }
+  __syncthreads();
+  // ---- deterministic reduction: block tree, then the last CTA sums CTA partials in order
+  s0 = block_sum(s0, red);
+  s1 = block_sum(s1, red);
+  if (threadIdx.x == 0) {
+    a.partials[2 * (size_t)blockIdx.x] = s0;
+    a.partials[2 * (size_t)blockIdx.x + 1] = s1;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(a.counter, 1) == (int)gridDim.x - 1);
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    double t0 = 0.0, t1 = 0.0;
+    for (int bb = threadIdx.x; bb < (int)gridDim.x; bb += kTdThreads) {
+      t0 += __ldcg(a.partials + 2 * (size_t)bb);
+      t1 += __ldcg(a.partials + 2 * (size_t)bb + 1);
+    }
+    t0 = block_sum(t0, red);
+    t1 = block_sum(t1, red);
+    if (threadIdx.x == 0) {
+      a.obj[0] = t0;
+      a.obj[1] = sqrt(t1);
+      *a.counter = 0;
+    }
+  }
+}
+
+bool td_usable(const double* VF, const double* V, int64_t ldv, const double* Z, int64_t ldz) {
+  return (ldv % 2) == 0 && (ldz % 2) == 0 && (reinterpret_cast<uintptr_t>(VF) & 15) == 0 &&
+         (reinterpret_cast<uintptr_t>(V) & 15) == 0 && (reinterpret_cast<uintptr_t>(Z) & 15) == 0;
+}
+
+cudaError_t admm_tma_launch(const double* VF, const double* V, int64_t ldv, const uint32_t* adj,
+                            int64_t ldadj, const double* deg, double t, double* Z, int64_t ldz,
+                            int n, double* obj, double* partials, int* counter, int num_sms,
+                            cudaStream_t st) {
+  TdMaps m;
+  {
+    const uint64_t dv[2] = {64, (uint64_t)n};
+    const uint64_t svf[1] = {64 * 8}, sv[1] = {(uint64_t)ldv * 8};
+    const uint32_t bi[2] = {16, 128}, bj[2] = {16, 32};
+    const uint64_t dz[2] = {(uint64_t)n, (uint64_t)n}, sz[1] = {(uint64_t)ldz * 8};
+    if (!encode_map_gen(&m.vi, true, 2, VF, dv, svf, bi, 128) ||
+        !encode_map_gen(&m.vj, true, 2, V, dv, sv, bj, 128) ||
+        !encode_map_gen(&m.z, true, 2, Z, dz, sz, bi, 128) ||
+        !encode_map_gen(&m.zm, true, 2, Z, dz, sz, bj, 128))
+      return cudaErrorInvalidValue;
+  }
+  R8Args a = {};
+  a.bits = adj;
+  a.ldb = ldadj;
+  a.deg = deg;
+  a.tt = t;
+  a.n = n;
+  a.TC = (n + kR8N - 1) / kR8N;
+  a.MT = (n + 127) / 128;
+  a.partials = partials;
+  a.counter = counter;
+  a.obj = obj;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(rebuild_tma_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kTdSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const long long ntiles = (long long)a.MT * a.TC - 2LL * a.MT * (a.MT - 1);
+  const int grid = (int)std::max<long long>(1, std::min<long long>(ntiles, num_sms));
+  count_launch();
+  rebuild_tma_kernel<<<grid, kTdThreads, kTdSmem, st>>>(m, a);
+  return cudaGetLastError();
+}
+
 // rows of X (n x 64 fp64, ldx) -> 7 digit slices in the tiled layout [128-row tile][slice][128][64]
 // (a8_offset with KB = 1), scale[row] = 2^E_row; rows n .. up to the tile end are zeros.
 // 16 threads per row, 4 values each.
@@ -536,8 +865,6 @@ __global__ void __launch_bounds__(256) r8_split_kernel(const double* __restrict_
   if (t == 0) scale[row] = i8::pow2(E);  // padded rows: 1 (their digits are 0)
 }
 
-bool encode_map_gen(CUtensorMap* map, bool f64, int rank, const void* base, const uint64_t* dims,
-                    const uint64_t* strides, const uint32_t* box, int swizzle);
 
 size_t r8_bytes(int n) { return (size_t)((n + 127) / 128) * kR8S * 8192; }
 
