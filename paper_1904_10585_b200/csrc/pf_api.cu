@@ -151,6 +151,7 @@ struct pf_ctx_s {
   unsigned long long* a8_wmax = nullptr;
   // PFAM update on int8 tensor cores (pf_rebuild_i8.cu; one GPU, p = 64, fused digits)
   bool r8_on = false;
+  bool k7tma = true;                           // PF_K7TMA=0 at create: rebuild_kernel on PF_FP64
   int8_t* r8_VF8 = nullptr;                    // digit slices of V' (r8_bytes)
   int8_t* r8_V8 = nullptr;                     // digit slices of V
   double* r8_rs = nullptr;                     // [2 x n padded to 128] row scales of V', V
@@ -436,6 +437,10 @@ static pf_status create_common(int64_t n, int32_t p, int32_t degree, pf_dtype dt
     // one CTA per 128-row tile (128 of 148 SMs at n = 16384) and measured slower
     const char* e8 = getenv("PF_I8SYM");
     ctx->i8s_ok = !dist && (e8 && e8[0] == '1') && i8s_supported(ctx->i8plan, ctx->num_sms);
+  }
+  {
+    const char* e = getenv("PF_K7TMA");
+    ctx->k7tma = !(e && e[0] == '0');
   }
   pf_status s = alloc_all(ctx);
   if (s == PF_OK && ctx->dist) {
@@ -1252,7 +1257,7 @@ pf_status pf_admm_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f
   PF_CU(admm_launch(Vf, ldf, V, ldv, f, t, adj, ldadj, deg, Z, ldz, (int)ctx->n_local,
                     (int)ctx->n, (int)ctx->row0, ctx->p, obj, ctx->rb_part, ctx->rb_cnt,
                     ctx->dist ? 1 : 0, ctx->VFbuf, st, fuse ? &dig : nullptr, nullptr,
-                    fuse && ctx->r8_on ? &r8 : nullptr));
+                    fuse && ctx->r8_on ? &r8 : nullptr, ctx->k7tma ? ctx->num_sms : 0));
   if (urec) {
     PF_CU(cudaEventRecord(ctx->evu[ctx->evu_used + 1], st));
     ctx->evu_used += 2;
@@ -1298,7 +1303,7 @@ pf_status pf_admm_step_f(pf_ctx ctx, const double* Q, int64_t ldq, const double*
   PF_CU(admm_launch(Qf, ldf, Q, ldq, nullptr, t, adj, ldadj, deg, Z, ldz, (int)ctx->n_local,
                     (int)ctx->n, (int)ctx->row0, ctx->p, obj, ctx->rb_part, ctx->rb_cnt,
                     ctx->dist ? 1 : 0, ctx->VFbuf, st, fuse ? &dig : nullptr, F,
-                    fuse && ctx->r8_on ? &r8 : nullptr));
+                    fuse && ctx->r8_on ? &r8 : nullptr, ctx->k7tma ? ctx->num_sms : 0));
   if (urec) {
     PF_CU(cudaEventRecord(ctx->evu[ctx->evu_used + 1], st));
     ctx->evu_used += 2;

@@ -266,7 +266,10 @@ cudaError_t admm_launch(const double* V, int64_t ldv, const double* Vloc, int64_
                         const double* deg, double* Z, int64_t ldz, int n_rows, int n, int row0,
                         int p, double* obj, double* partials, int* counter, int raw, double* vf,
                         cudaStream_t st, const RbDigits* dig = nullptr,
-                        const double* Fmat = nullptr, const R8Bufs* r8 = nullptr);
+                        const double* Fmat = nullptr, const R8Bufs* r8 = nullptr,
+                        int tma_sms = 0);
+// (tma_sms > 0: a one-GPU update without digit output may use the TMA-staged kernel with W on
+//  DMMA on that many SMs, pf_rebuild_i8.cu)
 // (Fmat != NULL: W = V F V^T with F p x p row-major; vf must already hold the local rows of V F
 //  and f is unused)
 cudaError_t sqrt_inplace_launch(double* x, cudaStream_t st);

@@ -738,7 +738,7 @@ cudaError_t admm_launch(const double* V, int64_t ldv, const double* Vloc, int64_
                         const double* deg, double* Z, int64_t ldz, int n_rows, int n, int row0,
                         int p, double* obj, double* partials, int* counter, int raw, double* vf,
                         cudaStream_t st, const RbDigits* dig, const double* Fmat,
-                        const R8Bufs* r8) {
+                        const R8Bufs* r8, int tma_sms) {
   cudaError_t e = cudaSuccess;
   if (!Fmat) {
     e = scale_cols(Vloc, ldvl, f, n_rows, p, vf, st);
@@ -772,19 +772,11 @@ cudaError_t admm_launch(const double* V, int64_t ldv, const double* Vloc, int64_
       return admm_i8_launch(r8->maps, vf, V, ldv, r8->VF8, r8->V8, r8->rsA, r8->rsB, adj, ldadj,
                             deg, t, Z, ldz, n, obj, partials, counter, dig, r8->mirror_dig,
                             r8->num_sms, st);
-  } else if (p == 64 && row0 == 0 && n_rows == n && !raw && td_usable(vf, V, ldv, Z, ldz)) {
-    // one GPU, no digit output: the TMA-staged update with W on DMMA (PF_K7TMA=0: rebuild_kernel)
-    static int use = -1, sms = 148;
-    if (use < 0) {
-      const char* e = getenv("PF_K7TMA");
-      use = !(e && e[0] == '0');
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    if (use)
-      return admm_tma_launch(vf, V, ldv, adj, ldadj, deg, t, Z, ldz, n, obj, partials, counter,
-                             sms, st);
+  } else if (tma_sms > 0 && p == 64 && row0 == 0 && n_rows == n && !raw &&
+             td_usable(vf, V, ldv, Z, ldz)) {
+    // one GPU, no digit output: the TMA-staged update with W on DMMA
+    return admm_tma_launch(vf, V, ldv, adj, ldadj, deg, t, Z, ldz, n, obj, partials, counter,
+                           tma_sms, st);
   }
   return rb_dispatch<false>(p, a, st);
 }

@@ -25,6 +25,7 @@ def test_single_rank_nccl_path_matches(cfg, monkeypatch):
     # update): both runs then do the same arithmetic
     monkeypatch.setenv("PF_LZ_SYM", "0")
     monkeypatch.setenv("PF_FUSE_DIGITS", "0")
+    monkeypatch.setenv("PF_K7TMA", "0")
     a = run(cfg)["records"]
     b = run(cfg, nccl_id=nccl_unique_id(), rank=0, world=1)["records"]
     for x, y in zip(a, b):

@@ -89,6 +89,7 @@ def test_loopback_world1_matches_plain_context(monkeypatch):
     from paper_1904_10585_b200.dist import run_loopback
     monkeypatch.setenv("PF_LZ_SYM", "0")
     monkeypatch.setenv("PF_FUSE_DIGITS", "0")
+    monkeypatch.setenv("PF_K7TMA", "0")
     cfg = reduced(CONFIGS[3], n=900, iters=4, edge_prob=0.09)
     a = run(cfg)["records"]
     b = run_loopback(cfg, 1)[0]["records"]

@@ -279,3 +279,50 @@ def test_rebuild_dense_matches_definition(n, p):
     ref = (V * f) @ V.T
     got = X.cpu().numpy()
     assert np.max(np.abs(got - ref)) <= 1e-13 * np.abs(ref).max() * p
+
+
+@pytest.mark.parametrize("n", [64, 100, 300, 1333, 2050])
+@pytest.mark.parametrize("k7tma", ["1", "0"])
+def test_admm_step_tma_kernel_matches_oracle(monkeypatch, n, k7tma):
+    """PF_FP64 PFAM update at p = 64 on one GPU: the TMA-staged kernel with W on DMMA
+    (rebuild_tma_kernel; PF_K7TMA=0: rebuild_kernel) against the oracle's eq:PFAM1 step (P:389,
+    reading R1) element by element -- ragged n, the 128 x 128 diagonal blocks, n < 128 -- plus
+    <C, W> and ||Z_new - Z||_F, in both forms (V diag(f) V^T and Q F Q^T)."""
+    monkeypatch.setenv("PF_K7TMA", k7tma)
+    p = 64
+    rng = np.random.default_rng(n)
+    V = np.linalg.qr(rng.standard_normal((n, max(n, p))))[0][:, :p] if n >= p else None
+    f = np.maximum(rng.standard_normal(p), 0) * 3.0
+    Z = rng.standard_normal((n, n)) * 0.1
+    Z = Z + Z.T
+    bits = sym_bernoulli_bitmask(n, 0.08, np.random.default_rng(9), diagonal=False)
+    adj = unpack_bitmask(bits, n)
+    deg = adj.sum(1).astype(float)
+    C = O.maxcut_C(adj, deg)
+    Z_ref, cw_ref, res_ref = O.pfam_next(V, f, Z, C, 0.9)
+    ctx = _ctx(n, p)
+
+    def pitched(A):  # even pitch: the TMA path needs 16-byte rows (odd n falls back otherwise)
+        buf = torch.zeros((n, (n + 1) // 2 * 2), dtype=torch.float64, device="cuda")
+        buf[:, :n].copy_(torch.from_numpy(A))
+        return buf[:, :n]
+
+    Zd = pitched(Z)
+    obj = torch.zeros(2, dtype=torch.float64, device="cuda")
+    bt = torch.from_numpy(bits.view(np.int32)).cuda()
+    ctx.admm_step(_dev(V), _dev(f), 0.9, bt, _dev(deg), Zd, obj)
+    Zg = Zd.cpu().numpy()
+    assert np.max(np.abs(Zg - Z_ref)) < 1e-13 * np.abs(Z_ref).max() * p
+    o = obj.cpu().numpy()
+    assert o[0] == pytest.approx(cw_ref, rel=1e-11, abs=1e-12)
+    assert o[1] == pytest.approx(res_ref, rel=1e-12)
+    # matrix form: W = Q F Q^T
+    B = rng.standard_normal((p, p))
+    F = B @ B.T / p
+    lam, Y = np.linalg.eigh(F)
+    Zr2, cw2, res2 = O.pfam_next(V @ Y, lam, Z, C, 0.9)
+    Zd = pitched(Z)
+    ctx.admm_step_f(_dev(V), _dev(F), 0.9, bt, _dev(deg), Zd, obj)
+    np.testing.assert_allclose(Zd.cpu().numpy(), Zr2, rtol=0, atol=1e-13 * np.abs(Zr2).max() * p)
+    o = obj.cpu().numpy()
+    assert o[0] == pytest.approx(cw2, rel=1e-11, abs=1e-12) and o[1] == pytest.approx(res2, rel=1e-11)
