@@ -205,8 +205,10 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         S = 7
         ops = 2.0 * n * n * p * S * (S + 1) / 2
         i8_peak = 2.0 * pk.get("bf16_tflops", 1618.6)
-        roof = {"bound": "tensor", "kernel": "cheb_gemm_i8_kernel<7,64> (tcgen05 kind::i8, exact "
-                "digit products, fp64 level combination)",
+        kname = ("cheb_gemm_i8_kernel<7,64> (tcgen05 kind::i8" if os.environ.get("PF_I8PAIR") == "0"
+                 else "cheb_gemm_i8p_kernel (CTA pairs, tcgen05.mma.cta_group::2 kind::i8, M = 256")
+        roof = {"bound": "tensor", "kernel": kname + ", exact digit products, fp64 level "
+                "combination)",
                 "achieved": ops / (gemm_avg_ms / 1e3) / 1e12, "peak": i8_peak, "unit": "TOPS",
                 "frac": ops / (gemm_avg_ms / 1e3) / 1e12 / i8_peak, "traffic": traffic,
                 "peak_source": "MEASURED_PEAKS.json bf16_tflops x 2 (nominal int8:bf16); the "

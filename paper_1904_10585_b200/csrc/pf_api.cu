@@ -135,6 +135,7 @@ struct pf_ctx_s {
   CUtensorMap mapA8t;                          // 64-row boxes read transposed
   bool a8_half = false;                        // A8 holds the upper tiles only (no mirror digits)
   CUtensorMap mapY8[4];                        // B boxes of 4..7 digit slices
+  CUtensorMap mapY8p[2];                       // K1-i8p B boxes (64 / 32 rows of one slice)
   int i8_early = 7;                            // slices of the Chebyshev steps before the tail
   int i8_tail = 0;                             // final steps (and RR) at the full slice count
   // PF_FUSE_DIGITS=0: the PFAM update does not write digits (pf_filter splits Z itself)
@@ -222,6 +223,8 @@ static bool encode_i8_maps(pf_ctx ctx) {
   if (ctx->i8s_ok && !i8s_encode_At(&ctx->mapA8t, ctx->A8, ctx->i8plan)) return false;
   for (int su = 4; su <= ctx->i8plan.S; ++su)
     if (!i8_encode_B(&ctx->mapY8[su - 4], ctx->Y8, ctx->i8plan, su)) return false;
+  if (ctx->i8plan.pair && !i8_encode_B_pair(&ctx->mapY8p[0], &ctx->mapY8p[1], ctx->Y8, ctx->i8plan))
+    return false;
   return true;
 }
 
@@ -711,7 +714,8 @@ static pf_status gemm_step(pf_ctx ctx, int bidx, const double* ycur, const doubl
     else
       PF_CU(i8_gemm_launch(ctx->i8plan, ctx->mapA8, ctx->mapY8[su - 4], ctx->mapA8pf,
                            ctx->a8_rscale, ctx->y8_cscale, ycur, yprev, out, ctx->p, coef,
-                           ctx->i8_acc, ctx->i8_part, ctx->i8_cnt, su, st));
+                           ctx->i8_acc, ctx->i8_part, ctx->i8_cnt, su, st, &ctx->mapY8p[0],
+                           &ctx->mapY8p[1]));
   }
   else
     PF_CU(cheb_gemm_launch(ctx->plan, ctx->mapA, *mb, ycur, yprev, out, coef, ctx->cheb_ws,

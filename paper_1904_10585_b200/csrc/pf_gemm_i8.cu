@@ -679,6 +679,385 @@ __global__ void __launch_bounds__(I8Cfg<S, NC>::THREADS, 1)
   }
 }
 
+// ------------------------------------------------------------------------------ CTA pairs
+// K1-i8p: the same product on CTA pairs -- cluster 2 x 1,
+// tcgen05.mma.cta_group::2.kind::i8, M = 256 (the pair's two 128-row tiles).  Each CTA holds its
+// own tile's A slices and supplies HALF of every MMA's N rows of B, so the tensor core's B reads
+// per SM halve: the K1-i8 MMA sequence reads ~96 KB of operands per 32-byte K step per SM from
+// shared memory (40 KB of A, 56 KB of stacked B) against the ~1792-cycle budget of a k-block
+// at the int8 peak, next to the TMA writes of the ring -- the per-SM operand bandwidth, not the
+// MMA rate, was the limit.  The pair reads 40 + 28 KB per K step per SM.
+//
+// An MMA's N rows are split in halves between the CTAs at ONE shared-memory offset, and its
+// D columns are [first half | second half]; to land every slice product on its level's TMEM
+// columns (level l at 64 l, as in K1-i8) the B block is staged per k-block as 7 regions whose
+// halves differ by rank (512 rows of 64 bytes per CTA, 32 KB):
+//   rows   0..127  Ra  [B0 B1 | B2 B3]      A_0..A_3 x Ra, N = 256, TMEM column 64 s
+//   rows 128..223  Rb  [B4 B5a | B5b B6]    A_0 x Rb, N = 192, column 256
+//   rows 224..287  Rc  [B4 | B5]            A_1 x Rc, N = 128, column 320
+//   rows 288..319  Rd  [B4a | B4b]          A_2 x Rd, N =  64, column 384
+//   rows 320..415  Re  [B0 B1a | B1b B2]    A_4 x Re, N = 192, column 256
+//   rows 416..479  Rf  [B0 | B1]            A_5 x Rf, N = 128, column 320
+//   rows 480..511  Rg  [B0a | B0b]          A_6 x Rg, N =  64, column 384
+// (a / b = columns 0..31 / 32..63 of a slice; "|" separates rank 0's rows from rank 1's).
+// The same 10 MMAs per K step as K1-i8, each twice as tall.  Both CTAs' TMA loads complete on
+// the LEADER's full barriers (cta_group::2 TMA), the leader's MMA commits free the stages of both
+// (multicast), both epilogues drain their own TMEM lanes and arrive on the leader's tempty.
+// Stream-K runs over (pair tile, k-block) units per cluster; each CTA finishes its own rows
+// (partials and counters per CTA).  S = 7, NC = 64 (p a multiple of 64).
+struct I8PCfg {
+  static constexpr int S = 7, NC = 64, BK = 64, BM = 128;
+  static constexpr int A_TILE = BM * BK;               // 8 KB: one slice of one k-block
+  static constexpr int B_ROWS = 512;                   // staged B rows per CTA per k-block
+  static constexpr int B_STAGE = B_ROWS * BK;          // 32 KB
+  static constexpr int NB = 2;
+  static constexpr int NA = (216 * 1024 - NB * B_STAGE) / A_TILE;  // 19
+  static constexpr int TMEM_COLS = 512;                // 448 used
+  static constexpr int CW = 32;
+  static constexpr int THREADS = 256;
+  static constexpr int BAR_BYTES = 8 * (2 * NA + 2 * NB + 2) + 16;
+  static constexpr int SMEM = NA * A_TILE + NB * B_STAGE + 1024 + BAR_BYTES;
+  static_assert(SMEM <= 227 * 1024, "smem");
+};
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8PCfg::THREADS, 1)
+    cheb_gemm_i8p_kernel(const __grid_constant__ CUtensorMap mapA8,
+                         const __grid_constant__ CUtensorMap mapB64,
+                         const __grid_constant__ CUtensorMap mapB32, I8Args args) {
+  using C = I8PCfg;
+  constexpr int S = C::S, NC = C::NC;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  unsigned char* ring_a = smem;                              // NA x [128][64] int8
+  unsigned char* ring_b = smem + C::NA * C::A_TILE;          // NB x [512][64] int8
+  uint64_t* afull = reinterpret_cast<uint64_t*>(ring_b + C::NB * C::B_STAGE);
+  uint64_t* aempty = afull + C::NA;
+  uint64_t* bfull = aempty + C::NA;
+  uint64_t* bempty = bfull + C::NB;
+  uint64_t* tfull = bempty + C::NB;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  volatile int* sflag = reinterpret_cast<volatile int*>(tmem_slot + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = tc::cluster_ctarank();
+  const int G = (int)tc::nclusters_x(), g = (int)tc::cluster_id_x();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::NA; ++s) {
+      mbar_init(&afull[s], 1);
+      mbar_init(&aempty[s], 1);
+    }
+    for (int s = 0; s < C::NB; ++s) {
+      mbar_init(&bfull[s], 1);
+      mbar_init(&bempty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 8);  // 4 epilogue warps x 2 CTAs (the leader's copy is used)
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&mapA8);
+    tma_prefetch_desc(&mapB64);
+    tma_prefetch_desc(&mapB32);
+  }
+  if (warp == 2) tc::tmem_alloc_pair<C::TMEM_COLS>(tmem_slot);
+  tc::fence_before_sync();
+  tc::cluster_sync();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+
+  const int KB = args.kblocks;
+  const int mpairs = (args.mtiles + 1) >> 1;
+  const int nitems = mpairs * args.ngroups;
+  const int kch = args.chunk_kb;
+  const long long U = (long long)nitems * KB;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (both CTAs)
+    RingI ra(C::NA), rb(C::NB);
+    const uint64_t pol_a = tc::policy_evict_first(), pol_b = tc::policy_evict_last();
+    const uint32_t afull_l = tc::mapa(smem_u32(afull), 0), bfull_l = tc::mapa(smem_u32(bfull), 0);
+    // this rank's B boxes per k-block: {smem row, slice, row in slice, 64-row box?}
+    constexpr int T0[10][4] = {{0, 0, 0, 1},   {64, 1, 0, 1},   {128, 4, 0, 1}, {192, 5, 0, 0},
+                               {224, 4, 0, 1}, {288, 4, 0, 0},  {320, 0, 0, 1}, {384, 1, 0, 0},
+                               {416, 0, 0, 1}, {480, 0, 0, 0}};
+    constexpr int T1[10][4] = {{0, 2, 0, 1},    {64, 3, 0, 1},  {128, 5, 32, 0}, {160, 6, 0, 1},
+                               {224, 5, 0, 1},  {288, 4, 32, 0}, {320, 1, 32, 0}, {352, 2, 0, 1},
+                               {416, 1, 0, 1},  {480, 0, 32, 0}};
+    SegIter si(U, G, g, KB);
+    int it, kbs, kbe;
+    while (si.next(it, kbs, kbe)) {
+      const int cg = it / mpairs, pt = it - cg * mpairs;  // column-group major
+      const int tile = 2 * pt + (int)crank;               // past mtiles: zero-filled by TMA
+      for (int kb = kbs; kb < kbe; ++kb) {
+        mbar_wait(&bempty[rb.s], rb.ph ^ 1u);
+        if (i8::elect_one()) {
+          if (crank == 0) mbar_arrive_expect_tx(&bfull[rb.s], 2 * C::B_STAGE);
+          unsigned char* dst = ring_b + rb.s * C::B_STAGE;
+#pragma unroll
+          for (int i = 0; i < 10; ++i) {
+            const int srow = crank ? T1[i][0] : T0[i][0];
+            const int sl = crank ? T1[i][1] : T0[i][1];
+            const int ro = crank ? T1[i][2] : T0[i][2];
+            const bool big = crank ? T1[i][3] : T0[i][3];
+            tc::tma_load_3d_pair(dst + srow * C::BK, big ? &mapB64 : &mapB32,
+                                 bfull_l + 8u * (uint32_t)rb.s, kb * C::BK, cg * NC + ro, sl,
+                                 pol_b);
+          }
+        }
+        __syncwarp();
+        rb.next();
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          mbar_wait(&aempty[ra.s], ra.ph ^ 1u);
+          if (i8::elect_one()) {
+            if (crank == 0) mbar_arrive_expect_tx(&afull[ra.s], 2 * C::A_TILE);
+            tc::tma_load_3d_pair(ring_a + ra.s * C::A_TILE, &mapA8, afull_l + 8u * (uint32_t)ra.s,
+                                 0, 0, (tile * KB + kb) * args.lS + s, pol_a);
+          }
+          __syncwarp();
+          ra.next();
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (pair leader)
+    if (crank == 0) {
+      RingI ra(C::NA), rb(C::NB);
+      uint32_t tph = 0;
+      SegIter si(U, G, g, KB);
+      int it, kbs, kbe;
+      const uint64_t adesc_ring = tc::sdesc_k_sw64(smem_u32(ring_a));
+      const uint64_t bdesc_ring = tc::sdesc_k_sw64(smem_u32(ring_b));
+      // per A slice: up to two MMAs {B region row, N, TMEM column}
+      constexpr int MM[7][2][3] = {{{0, 256, 0}, {128, 192, 256}},  {{0, 256, 64}, {224, 128, 320}},
+                                   {{0, 256, 128}, {288, 64, 384}}, {{0, 256, 192}, {0, 0, 0}},
+                                   {{320, 192, 256}, {0, 0, 0}},    {{416, 128, 320}, {0, 0, 0}},
+                                   {{480, 64, 384}, {0, 0, 0}}};
+      while (si.next(it, kbs, kbe)) {
+        for (int k0 = kbs; k0 < kbe; k0 += kch) {
+          const int k1 = min(kbe, k0 + kch);
+          tc::mbar_wait_cluster(tempty, tph ^ 1u);  // both epilogues drained the accumulators
+          tc::fence_after_sync();
+          for (int kb = k0; kb < k1; ++kb) {
+            tc::mbar_wait_cluster(&bfull[rb.s], rb.ph);
+            const uint64_t bd0 = bdesc_ring + (uint64_t)(rb.s * (C::B_STAGE >> 4));
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+              tc::mbar_wait_cluster(&afull[ra.s], ra.ph);
+              tc::fence_after_sync();
+              const uint64_t ad0 = adesc_ring + (uint64_t)(ra.s * (C::A_TILE >> 4));
+              if (i8::elect_one()) {
+#pragma unroll
+                for (int ks = 0; ks < 2; ++ks) {
+                  const uint32_t acc = (kb == k0 && s == 0 && ks == 0) ? 0u : 1u;
+#pragma unroll
+                  for (int m = 0; m < 2; ++m) {
+                    if (MM[s][m][1] == 0) continue;
+                    i8::mma_i8_pair(tmem + (uint32_t)MM[s][m][2], ad0 + (uint64_t)(ks * 2),
+                                    bd0 + (uint64_t)((MM[s][m][0] * C::BK + ks * 32) >> 4),
+                                    i8::idesc_i8(256, MM[s][m][1]), acc);
+                  }
+                }
+                tc::mma_commit_pair(&aempty[ra.s]);  // the slice stage is free in both CTAs
+              }
+              __syncwarp();
+              ra.next();
+            }
+            if (i8::elect_one()) tc::mma_commit_pair(&bempty[rb.s]);
+            __syncwarp();
+            rb.next();
+          }
+          if (i8::elect_one()) tc::mma_commit_pair(tfull);
+          __syncwarp();
+          tph ^= 1u;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue (4 warps, both CTAs)
+    const int q = warp & 3;
+    const int et = 32 * q + lane;  // row within this CTA's tile = TMEM lane
+    const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16);
+    const uint32_t tempty_l = tc::mapa(smem_u32(tempty), 0);
+    const double s1 = args.coef[0], s2 = args.coef[1], s3 = args.coef[2];
+    double* accp = args.acc + (size_t)blockIdx.x * (NC * 128) + et;
+    uint32_t tph = 0;
+    SegIter si(U, G, g, KB);
+    int it, kbs, kbe;
+    auto drained = [&]() {  // this warp's TMEM reads are done: tell the leader's MMA warp
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive_cluster(tempty_l);
+    };
+    while (si.next(it, kbs, kbe)) {
+      const int cg = it / mpairs, pt = it - cg * mpairs;
+      const int row = (2 * pt + (int)crank) * C::BM + et;
+      const bool row_ok = row < args.n_rows;
+      const double rs = row_ok ? args.rscale[row] : 0.0;
+      const bool whole = (kbs == 0 && kbe == KB);
+      int part = 0, nparts = 1;
+      if (!whole) {
+        const int f = seg_owner((long long)it * KB, U, G);
+        part = g - f;
+        nparts = seg_owner((long long)it * KB + KB - 1, U, G) - f + 1;
+      }
+      const int cit = 2 * it + (int)crank;  // this CTA's counter / partial slot
+      double* mypart = args.part + ((size_t)cit * args.maxp + part) * (NC * 128) + et;
+      if (!whole && kbe - kbs <= kch) {
+        // ------------------------------------------------ split item, one accumulation
+        mbar_wait(tfull, tph);
+        tph ^= 1u;
+        tc::fence_after_sync();
+        named_bar_sync(1, 128);
+        if (et == 0) *sflag = (atomicAdd(&args.counters[cit], 0) + 1 == nparts) ? 1 : 0;
+        named_bar_sync(1, 128);
+        const bool early = (*sflag != 0);
+        named_bar_sync(1, 128);
+        bool lastc = early;
+        if (!early) {
+#pragma unroll 1
+          for (int c0 = 0; c0 < NC; c0 += C::CW) {
+            double v[C::CW];
+#pragma unroll
+            for (int j = 0; j < C::CW; ++j) v[j] = 0.0;
+            i8_combine_levels<S, NC, C::CW>(taddr, c0, v);
+#pragma unroll
+            for (int j = 0; j < C::CW; ++j) __stcg(mypart + (size_t)(c0 + j) * 128, v[j]);
+          }
+          drained();
+          __threadfence();
+          named_bar_sync(1, 128);
+          if (et == 0) *sflag = (atomicAdd(&args.counters[cit], 1) + 1 == nparts) ? 1 : 0;
+          named_bar_sync(1, 128);
+          lastc = (*sflag != 0);
+          named_bar_sync(1, 128);
+        } else {
+          __threadfence();
+        }
+        if (lastc) {
+          const double* p0 = args.part + (size_t)cit * args.maxp * (NC * 128) + et;
+#pragma unroll 1
+          for (int c0 = 0; c0 < NC; c0 += C::CW) {
+            double m[C::CW];
+#pragma unroll
+            for (int j = 0; j < C::CW; ++j) m[j] = 0.0;
+            if (early) i8_combine_levels<S, NC, C::CW>(taddr, c0, m);
+            double v[C::CW];
+#pragma unroll
+            for (int j = 0; j < C::CW; ++j) v[j] = 0.0;
+#pragma unroll 1
+            for (int q2 = 0; q2 < nparts; ++q2) {
+              if (q2 == part && early) {
+#pragma unroll
+                for (int j = 0; j < C::CW; ++j) v[j] += m[j];
+              } else {
+#pragma unroll
+                for (int j = 0; j < C::CW; ++j)
+                  v[j] += __ldcg(p0 + (size_t)q2 * (NC * 128) + (size_t)(c0 + j) * 128);
+              }
+            }
+            if (row_ok) {
+              const int cbase = cg * NC + c0;
+              const size_t o = (size_t)row * args.ldy + cbase;
+#pragma unroll
+              for (int j = 0; j < C::CW; ++j) {
+                double y = s1 * (v[j] * rs * __ldg(args.cscale + cbase + j));
+                if (s2 != 0.0) y = fma(s2, args.ycur[o + j], y);
+                if (s3 != 0.0) y = fma(s3, args.yprev[o + j], y);
+                args.out[o + j] = y;
+              }
+            }
+          }
+          if (et == 0) args.counters[cit] = 0;  // ready for the next launch
+        }
+        if (early) drained();
+        continue;
+      }
+      for (int k0 = kbs; k0 < kbe; k0 += kch) {
+        const bool first = (k0 == kbs), last = (k0 + kch >= kbe);
+        mbar_wait(tfull, tph);
+        tph ^= 1u;
+        tc::fence_after_sync();
+#pragma unroll 1
+        for (int c0 = 0; c0 < NC; c0 += C::CW) {
+          double v[C::CW];
+#pragma unroll
+          for (int j = 0; j < C::CW; ++j) v[j] = 0.0;
+          i8_combine_levels<S, NC, C::CW>(taddr, c0, v);
+          if (!first) {
+#pragma unroll
+            for (int j = 0; j < C::CW; ++j) v[j] += __ldcg(accp + (size_t)(c0 + j) * 128);
+          }
+          if (!last) {
+#pragma unroll
+            for (int j = 0; j < C::CW; ++j) __stcg(accp + (size_t)(c0 + j) * 128, v[j]);
+          } else if (!whole) {
+#pragma unroll
+            for (int j = 0; j < C::CW; ++j) __stcg(mypart + (size_t)(c0 + j) * 128, v[j]);
+          } else if (row_ok) {
+            const int cbase = cg * NC + c0;
+            const size_t o = (size_t)row * args.ldy + cbase;
+#pragma unroll
+            for (int j = 0; j < C::CW; ++j) {
+              double y = s1 * (v[j] * rs * __ldg(args.cscale + cbase + j));
+              if (s2 != 0.0) y = fma(s2, args.ycur[o + j], y);
+              if (s3 != 0.0) y = fma(s3, args.yprev[o + j], y);
+              args.out[o + j] = y;
+            }
+          }
+        }
+        drained();
+      }
+      if (!whole) {
+        // ------------------------------------------------ stream-K fixup (last contributor)
+        __threadfence();
+        named_bar_sync(1, 128);
+        if (et == 0) *sflag = (atomicAdd(&args.counters[cit], 1) + 1 == nparts) ? 1 : 0;
+        named_bar_sync(1, 128);
+        const bool lastc = (*sflag != 0);
+        named_bar_sync(1, 128);
+        if (lastc) {
+          __threadfence();
+          const double* p0 = args.part + (size_t)cit * args.maxp * (NC * 128) + et;
+#pragma unroll 1
+          for (int c0 = 0; c0 < NC; c0 += C::CW) {
+            double v[C::CW];
+#pragma unroll
+            for (int j = 0; j < C::CW; ++j) v[j] = 0.0;
+#pragma unroll 1
+            for (int q2 = 0; q2 < nparts; ++q2) {
+#pragma unroll
+              for (int j = 0; j < C::CW; ++j)
+                v[j] += __ldcg(p0 + (size_t)q2 * (NC * 128) + (size_t)(c0 + j) * 128);
+            }
+            if (row_ok) {
+              const int cbase = cg * NC + c0;
+              const size_t o = (size_t)row * args.ldy + cbase;
+#pragma unroll
+              for (int j = 0; j < C::CW; ++j) {
+                double y = s1 * (v[j] * rs * __ldg(args.cscale + cbase + j));
+                if (s2 != 0.0) y = fma(s2, args.ycur[o + j], y);
+                if (s3 != 0.0) y = fma(s3, args.yprev[o + j], y);
+                args.out[o + j] = y;
+              }
+            }
+          }
+          if (et == 0) args.counters[cit] = 0;
+        }
+      }
+    }
+  }
+
+  __syncwarp();
+  tc::fence_before_sync();
+  tc::cluster_sync();  // the peer's MMAs / TMEM reads are done before the pair's dealloc
+  if (warp == 2) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc_pair<C::TMEM_COLS>(tmem);
+  }
+}
+
 // ------------------------------------------------------------------------------ symmetric A
 // Half-storage filter product for a SYMMETRIC A whose digit slices share one scale (the fused
 // PFAM digits, scale 2^Eg for every row; DESIGN.md §4 "K1-i8s"): only the 128 x 128 tiles
@@ -893,6 +1272,7 @@ I8Plan i8_plan(int p, int n_rows, int n_k, int slices, int num_sms) {
   const long long U = items * pl.kblocks;
   // stream-K: every SM gets an equal share of the (tile, k-block) units, at least 8 k-blocks
   pl.grid = (int)std::max(1LL, std::min<long long>(num_sms, U / 8));
+  if (const char* e = getenv("PF_I8_GRID")) pl.grid = std::max(1, std::min(pl.grid, atoi(e)));  // dev
   const long long per = U / pl.grid;  // fewest units a CTA owns
   pl.maxp = (int)std::min<long long>(pl.grid, (pl.kblocks + per - 1) / per + 1);
   pl.items = (int)items;
@@ -900,6 +1280,23 @@ I8Plan i8_plan(int p, int n_rows, int n_k, int slices, int num_sms) {
   pl.part_doubles = (size_t)items * pl.maxp * pl.NC * 128;
   pl.pf_dist = 0;
   if (const char* e = getenv("PF_I8_PFDIST")) pl.pf_dist = atoi(e);  // development knob
+  // K1-i8p: CTA pairs (PF_I8PAIR=0 keeps the one-CTA kernel); workspaces sized for both
+  pl.pair = 0;
+  pl.pgrid = pl.grid;
+  pl.pmaxp = pl.maxp;
+  const char* ep = getenv("PF_I8PAIR");
+  if (slices == 7 && pl.NC == 64 && num_sms >= 2 && !(ep && ep[0] == '0')) {
+    const long long pit = (long long)((pl.mtiles + 1) / 2) * pl.ngroups;
+    const long long PU = pit * pl.kblocks;
+    const long long G2 = std::max(1LL, std::min<long long>(pl.grid / 2, PU / 8));
+    const long long pper = PU / G2;
+    pl.pair = 1;
+    pl.pgrid = (int)(2 * G2);
+    pl.pmaxp = (int)std::min<long long>(G2, (pl.kblocks + pper - 1) / pper + 1);
+    pl.part_doubles = std::max(pl.part_doubles, (size_t)(pit * pl.pmaxp * 2) * pl.NC * 128);
+    pl.items = std::max<int>(pl.items, (int)(2 * pit));
+    pl.acc_doubles = std::max(pl.acc_doubles, (size_t)pl.pgrid * pl.NC * 128);
+  }
   return pl;
 }
 
@@ -912,6 +1309,11 @@ bool i8_encode_A(CUtensorMap* map, CUtensorMap* map_pf, const int8_t* A8, const 
 }
 bool i8_encode_B(CUtensorMap* map, const int8_t* Y8, const I8Plan& pl, int su) {
   return encode_map_i8_3d(map, Y8, pl.kpad, pl.kpad * pl.p, pl.n_k, pl.p, pl.S, pl.NC, su);
+}
+// K1-i8p B boxes: 64 or 32 rows of one slice
+bool i8_encode_B_pair(CUtensorMap* map64, CUtensorMap* map32, const int8_t* Y8, const I8Plan& pl) {
+  return encode_map_i8_3d(map64, Y8, pl.kpad, pl.kpad * pl.p, pl.n_k, pl.p, pl.S, 64, 1) &&
+         encode_map_i8_3d(map32, Y8, pl.kpad, pl.kpad * pl.p, pl.n_k, pl.p, pl.S, 32, 1);
 }
 
 template <int S>
@@ -1002,7 +1404,8 @@ static cudaError_t i8_launch_s(const I8Plan& pl, const CUtensorMap& mapA8,
 cudaError_t i8_gemm_launch(const I8Plan& pl, const CUtensorMap& mapA8, const CUtensorMap& mapY8,
                            const CUtensorMap& mapA8pf, const double* rscale, const double* cscale, const double* ycur,
                            const double* yprev, double* out, int64_t ldy, const double* coef,
-                           double* acc, double* part, int* counters, int su, cudaStream_t st) {
+                           double* acc, double* part, int* counters, int su, cudaStream_t st,
+                           const CUtensorMap* mapB64, const CUtensorMap* mapB32) {
   // su <= pl.S: only the su most significant digit slices of both operands are multiplied --
   // exactly the su-digit expansion (the digits of a longer truncating expansion start with
   // those of a shorter one), levels 2..su+1; the B map must have a box of su slices
@@ -1026,6 +1429,21 @@ cudaError_t i8_gemm_launch(const I8Plan& pl, const CUtensorMap& mapA8, const CUt
   a.pf_dist = pl.pf_dist;
   a.lS = pl.S;
   if (su < 4 || su > pl.S) return cudaErrorInvalidValue;
+  if (pl.pair && su == 7 && pl.S == 7 && mapB64 && mapB32) {
+    static bool attr_p = false;
+    if (!attr_p) {
+      cudaError_t e = cudaFuncSetAttribute(cheb_gemm_i8p_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           I8PCfg::SMEM);
+      if (e != cudaSuccess) return e;
+      attr_p = true;
+    }
+    a.maxp = pl.pmaxp;
+    count_launch();
+    cheb_gemm_i8p_kernel<<<pl.pgrid, I8PCfg::THREADS, I8PCfg::SMEM, st>>>(mapA8, *mapB64,
+                                                                          *mapB32, a);
+    return cudaGetLastError();
+  }
   switch (su) {
     case 4: return i8_launch_s<4>(pl, mapA8, mapY8, mapA8pf, a, st);
     case 5: return i8_launch_s<5>(pl, mapA8, mapY8, mapA8pf, a, st);

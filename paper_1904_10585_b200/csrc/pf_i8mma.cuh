@@ -33,6 +33,19 @@ PF_DEV void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t ide
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// the same MMA issued by the pair leader for both CTAs (M = 256: A rows 0..127 from this CTA,
+// 128..255 from the peer; N rows of B split in halves between the two at the same offset)
+PF_DEV void mma_i8_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                        uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 // one lane of a converged warp (always the same one: the lowest active lane)
 PF_DEV bool elect_one() {
   uint32_t pred;

@@ -69,6 +69,8 @@ struct I8Plan {
   int grid;               // persistent CTAs
   size_t acc_doubles;     // fold workspace
   int pf_dist;            // L2 prefetch distance of A (k-blocks, 0 = off)
+  int pair;               // K1-i8p (CTA pairs, cta_group::2) for full-precision S = 7, NC = 64
+  int pgrid, pmaxp;       // its CTAs (2 per cluster) and most clusters sharing a pair item
   int items;              // mtiles * ngroups
   int maxp;               // most CTAs sharing one item (stream-K)
   size_t part_doubles;    // stream-K partial workspace
@@ -76,6 +78,7 @@ struct I8Plan {
 I8Plan i8_plan(int p, int n_rows, int n_k, int slices, int num_sms);
 bool i8_encode_A(CUtensorMap* map, CUtensorMap* map_pf, const int8_t* A8, const I8Plan& pl);
 bool i8_encode_B(CUtensorMap* map, const int8_t* Y8, const I8Plan& pl, int su);  // box: su slices
+bool i8_encode_B_pair(CUtensorMap* map64, CUtensorMap* map32, const int8_t* Y8, const I8Plan& pl);
 cudaError_t i8_split_A_launch(const double* A, int64_t lda, const I8Plan& pl, int8_t* A8,
                               double* rscale, int num_sms, cudaStream_t st);
 cudaError_t i8_split_Y_launch(const double* Y, int64_t ldy, const I8Plan& pl,
@@ -90,7 +93,8 @@ cudaError_t i8s_gemm_launch(const I8Plan& pl, const CUtensorMap& mapA8, const CU
 cudaError_t i8_gemm_launch(const I8Plan& pl, const CUtensorMap& mapA8, const CUtensorMap& mapY8,
                            const CUtensorMap& mapA8pf, const double* rscale, const double* cscale, const double* ycur,
                            const double* yprev, double* out, int64_t ldy, const double* coef,
-                           double* acc, double* part, int* counters, int su, cudaStream_t st);
+                           double* acc, double* part, int* counters, int su, cudaStream_t st,
+                           const CUtensorMap* mapB64 = nullptr, const CUtensorMap* mapB32 = nullptr);
 
 // ---- Newton-Schulz spectral operator (pf_ns.cu): F = f(H) of a p x p symmetric fp64 matrix
 struct NsWork;

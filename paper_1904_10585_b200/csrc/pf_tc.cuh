@@ -120,6 +120,19 @@ PF_DEV void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2, uint
       : "memory");
 }
 
+// 3-D tile load into THIS CTA's shared memory whose completion is signalled on the PAIR
+// LEADER's mbarrier (`mbar_cluster`: a shared::cluster address from mapa(.., 0)); the leader
+// expects the bytes of both CTAs' loads (cta_group::2 form)
+PF_DEV void tma_load_3d_pair(void* smem_dst, const CUtensorMap* map, uint32_t mbar_cluster, int c0,
+                             int c1, int c2, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6;\n" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(mbar_cluster), "r"(c0), "r"(c1), "r"(c2),
+      "l"(policy)
+      : "memory");
+}
+
 // ------------------------------------------------------------------------------ TMEM
 template <int NCOLS>
 PF_DEV void tmem_alloc_pair(uint32_t* dst_smem) {  // one full warp of EACH CTA of the pair

@@ -50,6 +50,45 @@ def test_integer_operands_exact(n, p):
     assert np.array_equal(out.cpu().numpy(), ref)
 
 
+@pytest.mark.parametrize("pair", ["0", "1"])
+@pytest.mark.parametrize("n,p", [(64, 64), (129, 64), (1333, 64), (2049, 128), (4160, 64)])
+def test_pair_and_single_cta_kernels_exact(monkeypatch, n, p, pair):
+    """K1-i8p (CTA pairs, cta_group::2, the default at S = 7, p % 64 == 0) and the one-CTA
+    K1-i8 (PF_I8PAIR=0) on integer operands: bit-equal to numpy.  Odd tile counts (n = 64, 1333,
+    4160: a pair whose second tile lies past n, zero-filled by TMA), two column groups (p = 128)
+    and stream-K splits across pair items."""
+    monkeypatch.setenv("PF_I8PAIR", pair)
+    rs = np.random.default_rng(3 * n + p)
+    A = rs.integers(-127, 128, (n, n)).astype(np.float64)
+    Y = rs.integers(-90, 91, (n, p)).astype(np.float64)
+    Y[:, -1] = 0.0
+    ref = A @ Y
+    c = _ctx(n, p)
+    out = torch.empty((n, p), dtype=torch.float64, device="cuda")
+    c.matmul(_pitched(A), _dev(Y), out)
+    assert np.array_equal(out.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("n,p", [(1333, 64), (6000, 128)])
+def test_pair_kernel_matches_single_cta_kernel(monkeypatch, n, p):
+    """Gaussian operands: the two kernels form the same exact level sums; only the stream-K
+    split points (fp64 partial sums) differ, so they agree to the fp64 rounding of the sum."""
+    rs = np.random.default_rng(n + 5)
+    A = rs.standard_normal((n, n))
+    A = A + A.T
+    Y = rs.standard_normal((n, p))
+    outs = []
+    for pair in ("1", "0"):
+        monkeypatch.setenv("PF_I8PAIR", pair)
+        c = _ctx(n, p)
+        out = torch.empty((n, p), dtype=torch.float64, device="cuda")
+        c.matmul(_pitched(A), _dev(Y), out)
+        outs.append(out.cpu().numpy())
+    scale = np.abs(A).max() * np.abs(Y).max() * n
+    assert np.abs(outs[0] - outs[1]).max() <= 2.0 ** -50 * scale
+    assert np.abs(outs[0] - A @ Y).max() <= 2.0 ** -47 * scale
+
+
 @pytest.mark.parametrize("slices", [6, 7])
 @pytest.mark.parametrize("n,p", [(1000, 32), (1333, 64), (2049, 128), (300, 16)])
 def test_random_operands_within_split_bound(n, p, slices):

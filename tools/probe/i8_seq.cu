@@ -98,7 +98,7 @@ __global__ void seq(int steps, int mode, long long* out) {
       }
   }
   const bool tr = mode == 3;
-  if (mode >= 4) {  // mode 0's sequence with the kernel's per-slice (4) / per-k-block (5) sync
+  if (mode >= 4 && mode < 10) {  // mode 0's sequence with the kernel's per-slice (4) / per-k-block (5) sync
     for (int s = 0; s < 7; ++s)
       for (int t0 = 0; t0 < 7 - s; t0 += 4) {
         const int c = min(4, 7 - s - t0);
@@ -109,18 +109,21 @@ __global__ void seq(int steps, int mode, long long* out) {
   if (rank == 0 && warp == 1) {
     const uint32_t a0 = smem_u32(A), b0 = smem_u32(B);
     long long t0 = clock64();
-    if (mode >= 4) {
+    if (mode >= 4 && mode < 10) {
       // per k-block (2 K steps): for each slice s: [wait + fence], MMAs of ks = 0, 1, [commit]
       for (int kb = 0; kb < steps / 2; ++kb) {
-        if (mode == 5) {
+        if (mode == 5 || mode == 9) {
           mbar_wait(done, 0);
-          tc::fence_after_sync();
+          if (mode == 5) tc::fence_after_sync();
         }
 #pragma unroll
         for (int s = 0; s < 7; ++s) {
-          if (mode == 4) {
+          // 4: wait + fence + commit per slice (the kernel); 6: wait + commit per slice, no
+          // fence; 7: wait per slice (no fence), commit per k-block; 8: wait + commit per
+          // slice pair {0,1},{2,3},{4,5},{6}; 9: wait + commit per k-block, no fence
+          if (mode == 4 || mode == 6 || mode == 7 || (mode == 8 && (s & 1) == 0)) {
             mbar_wait(done, 0);
-            tc::fence_after_sync();
+            if (mode == 4) tc::fence_after_sync();
           }
           if (tc::elect_one()) {
 #pragma unroll
@@ -132,13 +135,55 @@ __global__ void seq(int steps, int mode, long long* out) {
                         tc::sdesc_k_sw64(a0 + s * 8192 + ks * 32),
                         tc::sdesc_k_sw64(b0 + 64 * t0 * 64 + ks * 32), idesc_i8(M, 64 * c));
               }
-            if (mode == 4)
+            if (mode == 4 || mode == 6 || (mode == 8 && ((s & 1) == 1 || s == 6)))
               asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(sink)));
           }
           __syncwarp();
         }
-        if (mode == 5 && tc::elect_one())
+        if ((mode == 5 || mode == 7 || mode == 9) && tc::elect_one())
           asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(sink)));
+        __syncwarp();
+      }
+    }
+    if (mode >= 10) {
+      // 10: one wait per k-block, every MMA of the k-block inside ONE elected block (s, ks, t0)
+      // 11: as 10 in the K-step-outer order (ks, s, t0)
+      // 12: per-slice wait + commit by the elected lane alone (no warp sync between slices)
+      for (int kb = 0; kb < steps / 2; ++kb) {
+        if (mode != 12) mbar_wait(done, 0);
+        if (tc::elect_one()) {
+          if (mode == 11) {
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+              for (int s = 0; s < 7; ++s)
+#pragma unroll
+                for (int t0 = 0; t0 < 7 - s; t0 += 4) {
+                  const int c = min(4, 7 - s - t0);
+                  mma<CG>(tmem + (uint32_t)((64 * (s + t0)) % 256),
+                          tc::sdesc_k_sw64(a0 + s * 8192 + ks * 32),
+                          tc::sdesc_k_sw64(b0 + 64 * t0 * 64 + ks * 32), idesc_i8(M, 64 * c));
+                }
+          } else {
+#pragma unroll
+            for (int s = 0; s < 7; ++s) {
+              if (mode == 12) mbar_wait(done, 0);
+#pragma unroll
+              for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+                for (int t0 = 0; t0 < 7 - s; t0 += 4) {
+                  const int c = min(4, 7 - s - t0);
+                  mma<CG>(tmem + (uint32_t)((64 * (s + t0)) % 256),
+                          tc::sdesc_k_sw64(a0 + s * 8192 + ks * 32),
+                          tc::sdesc_k_sw64(b0 + 64 * t0 * 64 + ks * 32), idesc_i8(M, 64 * c));
+                }
+              if (mode == 12)
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(sink)));
+            }
+          }
+          if (mode != 12)
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(sink)));
+        }
         __syncwarp();
       }
     }
@@ -217,7 +262,7 @@ void run(int mode, int clusters) {
 
 int main() {
   run<1>(0, 148);
-  run<1>(4, 148);
-  run<1>(5, 148);
+  for (int m = 4; m <= 12; ++m) run<1>(m, 148);
+  run<2>(1, 74);
   return 0;
 }
