@@ -890,11 +890,78 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8PCfg::THREADS, 1)
       __syncwarp();
       if (lane == 0) tc::mbar_arrive_cluster(tempty_l);
     };
-    while (si.next(it, kbs, kbe)) {
-      const int cg = it / mpairs, pt = it - cg * mpairs;
+    // The CTA's last segment ends with every MMA complete and every ring stage consumed, so its
+    // output tile is staged in the A ring (128 x 64 fp64, pitch 65) and written by rows:
+    // coalesced Y_j / Y_{j-1} reads and out stores instead of one 512-byte row per lane
+    // (the kernel's exposed tail, DESIGN.md §4 K1-i8p)
+    double* stg = reinterpret_cast<double*>(ring_a);
+    bool stage = false;
+    int cg = 0, pt = 0;
+    auto emit = [&](const double (&v)[C::CW], int c0) {
       const int row = (2 * pt + (int)crank) * C::BM + et;
-      const bool row_ok = row < args.n_rows;
-      const double rs = row_ok ? args.rscale[row] : 0.0;
+      if (stage) {
+        fence_proxy_async();  // after the tensor core's reads of the ring (tfull observed)
+#pragma unroll
+        for (int j = 0; j < C::CW; ++j) stg[et * 65 + c0 + j] = v[j];
+        return;
+      }
+      if (row < args.n_rows) {
+        const double rs = args.rscale[row];
+        const int cbase = cg * NC + c0;
+        const size_t o = (size_t)row * args.ldy + cbase;
+#pragma unroll
+        for (int j = 0; j < C::CW; ++j) {
+          double y = s1 * (v[j] * rs * __ldg(args.cscale + cbase + j));
+          if (s2 != 0.0) y = fma(s2, args.ycur[o + j], y);
+          if (s3 != 0.0) y = fma(s3, args.yprev[o + j], y);
+          args.out[o + j] = y;
+        }
+      }
+    };
+    double* srs = stg + C::BM * 65;  // the tile's row scales
+    auto flush = [&]() {  // the staged tile -> out, 64 consecutive columns of a row per 2 warps
+      const int r0 = (2 * pt + (int)crank) * C::BM;
+      srs[et] = (r0 + et < args.n_rows) ? args.rscale[r0 + et] : 0.0;
+      named_bar_sync(1, 128);
+      const int c = et & 63;
+      const double cs = __ldg(args.cscale + cg * NC + c);
+      const int nr = min(C::BM, args.n_rows - r0);
+      if (nr <= 0) return;  // the pair's second tile past n (uniform over the CTA)
+      // 8 rows per batch: the batch's Y_j / Y_{j-1} loads are all in flight together
+#pragma unroll 1
+      for (int rb = 0; rb < C::BM; rb += 16) {
+        double y[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = rb + 2 * i + (et >> 6);
+          y[i] = s1 * (stg[r * 65 + c] * srs[r] * cs);
+        }
+        if (s2 != 0.0 || s3 != 0.0) {
+          double a[8], b[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int r = rb + 2 * i + (et >> 6);
+            const size_t o = (size_t)(r0 + min(r, nr - 1)) * args.ldy + cg * NC + c;
+            a[i] = s2 != 0.0 ? args.ycur[o] : 0.0;
+            b[i] = s3 != 0.0 ? args.yprev[o] : 0.0;
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            if (s2 != 0.0) y[i] = fma(s2, a[i], y[i]);
+            if (s3 != 0.0) y[i] = fma(s3, b[i], y[i]);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = rb + 2 * i + (et >> 6);
+          if (r < nr) args.out[(size_t)(r0 + r) * args.ldy + cg * NC + c] = y[i];
+        }
+      }
+    };
+    while (si.next(it, kbs, kbe)) {
+      cg = it / mpairs;
+      pt = it - cg * mpairs;
+      stage = si.u >= si.u1;  // last segment: the ring is idle once its accumulation completes
       const bool whole = (kbs == 0 && kbe == KB);
       int part = 0, nparts = 1;
       if (!whole) {
@@ -957,18 +1024,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8PCfg::THREADS, 1)
                   v[j] += __ldcg(p0 + (size_t)q2 * (NC * 128) + (size_t)(c0 + j) * 128);
               }
             }
-            if (row_ok) {
-              const int cbase = cg * NC + c0;
-              const size_t o = (size_t)row * args.ldy + cbase;
-#pragma unroll
-              for (int j = 0; j < C::CW; ++j) {
-                double y = s1 * (v[j] * rs * __ldg(args.cscale + cbase + j));
-                if (s2 != 0.0) y = fma(s2, args.ycur[o + j], y);
-                if (s3 != 0.0) y = fma(s3, args.yprev[o + j], y);
-                args.out[o + j] = y;
-              }
-            }
+            emit(v, c0);
           }
+          if (stage) flush();
           if (et == 0) args.counters[cit] = 0;  // ready for the next launch
         }
         if (early) drained();
@@ -995,19 +1053,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8PCfg::THREADS, 1)
           } else if (!whole) {
 #pragma unroll
             for (int j = 0; j < C::CW; ++j) __stcg(mypart + (size_t)(c0 + j) * 128, v[j]);
-          } else if (row_ok) {
-            const int cbase = cg * NC + c0;
-            const size_t o = (size_t)row * args.ldy + cbase;
-#pragma unroll
-            for (int j = 0; j < C::CW; ++j) {
-              double y = s1 * (v[j] * rs * __ldg(args.cscale + cbase + j));
-              if (s2 != 0.0) y = fma(s2, args.ycur[o + j], y);
-              if (s3 != 0.0) y = fma(s3, args.yprev[o + j], y);
-              args.out[o + j] = y;
-            }
+          } else {
+            emit(v, c0);
           }
         }
         drained();
+        if (stage && last && whole) flush();
       }
       if (!whole) {
         // ------------------------------------------------ stream-K fixup (last contributor)
@@ -1031,18 +1082,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8PCfg::THREADS, 1)
               for (int j = 0; j < C::CW; ++j)
                 v[j] += __ldcg(p0 + (size_t)q2 * (NC * 128) + (size_t)(c0 + j) * 128);
             }
-            if (row_ok) {
-              const int cbase = cg * NC + c0;
-              const size_t o = (size_t)row * args.ldy + cbase;
-#pragma unroll
-              for (int j = 0; j < C::CW; ++j) {
-                double y = s1 * (v[j] * rs * __ldg(args.cscale + cbase + j));
-                if (s2 != 0.0) y = fma(s2, args.ycur[o + j], y);
-                if (s3 != 0.0) y = fma(s3, args.yprev[o + j], y);
-                args.out[o + j] = y;
-              }
-            }
+            emit(v, c0);
           }
+          if (stage) flush();
           if (et == 0) args.counters[cit] = 0;
         }
       }
