@@ -392,7 +392,8 @@ __global__ void __launch_bounds__(I8Cfg<S, NC>::THREADS, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (one warp)
-    // warp-uniform loop, one elected lane issues (as the MMA issuer)
+    // warp-uniform loop, one elected lane issues (as the MMA issuer); one B box per k-block
+    // (a separate B producer warp, as in K1-i8p, measured 0.383 vs 0.381 ms: no gain here)
     RingI ra(C::NA), rb(C::NB);
     const uint64_t pol_a = tc::policy_evict_first(), pol_b = tc::policy_evict_last();
     SegIter si(U, G, blockIdx.x, KB);
@@ -711,7 +712,7 @@ struct I8PCfg {
   static constexpr int B_ROWS = 512;                   // staged B rows per CTA per k-block
   static constexpr int B_STAGE = B_ROWS * BK;          // 32 KB
   static constexpr int NB = 2;
-  static constexpr int NA = (216 * 1024 - NB * B_STAGE) / A_TILE;  // 19
+  static constexpr int NA = 20;  // the A ring takes what the B ring and the barriers leave
   static constexpr int TMEM_COLS = 512;                // 448 used
   static constexpr int CW = 32;
   static constexpr int THREADS = 256;
@@ -772,8 +773,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8PCfg::THREADS, 1)
   const int kch = args.chunk_kb;
   const long long U = (long long)nitems * KB;
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer (both CTAs)
+  if (warp == 0 || warp == 3) {
+    // ------------------------------------------------------------ TMA producers (both CTAs)
+    // warp 0 streams the A slices, warp 3 the B regions: two loops, so the A ring runs up to
+    // NA slices ahead whatever the depth of the B ring
+    const bool is_a = (warp == 0);
     RingI ra(C::NA), rb(C::NB);
     const uint64_t pol_a = tc::policy_evict_first(), pol_b = tc::policy_evict_last();
     const uint32_t afull_l = tc::mapa(smem_u32(afull), 0), bfull_l = tc::mapa(smem_u32(bfull), 0);
@@ -790,23 +794,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8PCfg::THREADS, 1)
       const int cg = it / mpairs, pt = it - cg * mpairs;  // column-group major
       const int tile = 2 * pt + (int)crank;               // past mtiles: zero-filled by TMA
       for (int kb = kbs; kb < kbe; ++kb) {
-        mbar_wait(&bempty[rb.s], rb.ph ^ 1u);
-        if (i8::elect_one()) {
-          if (crank == 0) mbar_arrive_expect_tx(&bfull[rb.s], 2 * C::B_STAGE);
-          unsigned char* dst = ring_b + rb.s * C::B_STAGE;
+        if (!is_a) {
+          mbar_wait(&bempty[rb.s], rb.ph ^ 1u);
+          if (i8::elect_one()) {
+            if (crank == 0) mbar_arrive_expect_tx(&bfull[rb.s], 2 * C::B_STAGE);
+            unsigned char* dst = ring_b + rb.s * C::B_STAGE;
 #pragma unroll
-          for (int i = 0; i < 10; ++i) {
-            const int srow = crank ? T1[i][0] : T0[i][0];
-            const int sl = crank ? T1[i][1] : T0[i][1];
-            const int ro = crank ? T1[i][2] : T0[i][2];
-            const bool big = crank ? T1[i][3] : T0[i][3];
-            tc::tma_load_3d_pair(dst + srow * C::BK, big ? &mapB64 : &mapB32,
-                                 bfull_l + 8u * (uint32_t)rb.s, kb * C::BK, cg * NC + ro, sl,
-                                 pol_b);
+            for (int i = 0; i < 10; ++i) {
+              const int srow = crank ? T1[i][0] : T0[i][0];
+              const int sl = crank ? T1[i][1] : T0[i][1];
+              const int ro = crank ? T1[i][2] : T0[i][2];
+              const bool big = crank ? T1[i][3] : T0[i][3];
+              tc::tma_load_3d_pair(dst + srow * C::BK, big ? &mapB64 : &mapB32,
+                                   bfull_l + 8u * (uint32_t)rb.s, kb * C::BK, cg * NC + ro, sl,
+                                   pol_b);
+            }
           }
+          __syncwarp();
+          rb.next();
+          continue;
         }
-        __syncwarp();
-        rb.next();
 #pragma unroll
         for (int s = 0; s < S; ++s) {
           mbar_wait(&aempty[ra.s], ra.ph ^ 1u);
