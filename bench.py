@@ -234,7 +234,11 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
     if upd_n:
         fused = args.path == "i8" and os.environ.get("PF_FUSE_DIGITS", "1") != "0"
         k7i8 = fused and p == 64 and os.environ.get("PF_K7I8", "1") != "0"
-        ubytes = 8.0 * n * (n + 1) / 2 + 8.0 * n * n + (7.0 * n * n if fused else 0.0) \
+        # Z_new written in full, or (upper-block storage, pf_set_z_upper) on and above the
+        # 128 x 128 diagonal blocks only
+        zup = bool(getattr(s, "z_upper", False))
+        zw = 8.0 * n * (n + 128) / 2 if zup else 8.0 * n * n
+        ubytes = 8.0 * n * (n + 1) / 2 + zw + (7.0 * n * n if fused else 0.0) \
             + 2 * 8.0 * n * p + n * n / 16.0
         uavg = upd_ms / upd_n
         utraffic = None
@@ -252,6 +256,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
                     "frac": ubytes / (uavg / 1e3) / 1e9 / pk.get("hbm_gbs", 6550.4),
                     "traffic": utraffic, "algorithmic_bytes_per_launch": ubytes,
                     "avg_launch_ms": uavg, "launches": upd_n, "share_of_step": upd_share,
+                    "z_storage": "upper blocks (pf_set_z_upper)" if zup else "full",
                     "timed": "events around pf_admm_step (row bounds + splits + update kernel)"}
     filter_flops_per_step = 2.0 * d * n * n * p
     cpu = cpu_baseline(cfg, args) if (world == 1 and not args.no_cpu) else None
@@ -280,6 +285,11 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
                    "filter_gemm": "fp64 from exact int8 tensor-core products of 7-bit digit "
                                   "slices (PF_FP64_I8, S=7)" if args.path == "i8" else
                                   "fp64 DMMA (PF_FP64)",
+                   "iterate_storage": ("symmetric Z in upper-block storage: the update writes Z_new "
+                                       "on and above the 128 x 128 diagonal blocks (every reader on "
+                                       "this path reads only those), plus all digit slices "
+                                       "(pf_set_z_upper)") if getattr(s, "z_upper", False)
+                                      else "full symmetric Z",
                    "cuda_graphs": "iteration body replayed (k >= 1)",
                    "l2": "inputs larger than L2 (2 GiB fp64 iterate re-read every pass)",
                    "parallelism": "replicas" if world > 1 else "1 GPU"},

@@ -321,6 +321,19 @@ pf_status pf_set_i8_schedule(pf_ctx ctx, int32_t early_slices, int32_t exact_tai
  * means between libpf calls calls pf_invalidate first.  No-op for other dtypes. */
 pf_status pf_invalidate(pf_ctx ctx);
 
+/* Upper-block storage of the PFAM iterate (DESIGN.md §4 "K7-i8, upper-block storage"): with
+ * upper = 1, pf_admm_step / pf_admm_step_f on this context write Z_new only in the rows' 128 x 128
+ * diagonal blocks and to their right (entries (i, j) with j >= 128 floor(i / 128)), not the exact
+ * mirror below them -- Z is symmetric, and every libpf reader of the iterate on this path reads
+ * only that region: pf_filter / pf_rayleigh_ritz / pf_rr_ns take the update's digit slices
+ * (mirror slices included), pf_lanczos reads the upper 64 x 64 tiles, the next update the upper
+ * tiles.  A fresh digit split of such an iterate (it would read the stale lower part) fails with
+ * PF_ERR_UNSUPPORTED until pf_invalidate (the caller declares the full matrix written) or upper
+ * = 0.  Applies when the int8-digit update runs (one GPU, PF_FP64_I8, p = 64, S = 7, fused digits,
+ * PF_K7I8 not 0) and pf_lanczos uses the symmetric tile GEMV (one GPU, n <= 18944); otherwise
+ * PF_ERR_UNSUPPORTED.  upper = 0 (the default) restores full storage. */
+pf_status pf_set_z_upper(pf_ctx ctx, int32_t upper);
+
 /* out = A Y with the context's filter GEMM (fp64 dtypes): A local rows (n_local x n, lda as for
  * pf_filter), Y the local rows of an n x p block (n_local x p, ldy >= p; gathered internally when
  * distributed), out n_local x p (ldo >= p).  The kernel of every Chebyshev step, exposed for

@@ -67,6 +67,7 @@ def load() -> ctypes.CDLL:
         "pf_set_i8_slices": [P, I32],
         "pf_set_i8_schedule": [P, I32, I32],
         "pf_invalidate": [P],
+        "pf_set_z_upper": [P, I32],
         "pf_matmul": [P, P, I64, P, I64, P, I64, P],
         "pf_spmm": [P, P, P, P, P, P, I64, D, D, D, P, I64, P, I64, P, I64, P],
         "pf_rr_ns": [P, P, I64, P, I64, I32, D, P, P, P, P],
@@ -341,6 +342,10 @@ class Context:
         """PF_FP64_I8: early Chebyshev steps on early_slices digits, the last exact_tail on S."""
         self._check(self.lib.pf_set_i8_schedule(self.h, early_slices, exact_tail),
                     "pf_set_i8_schedule")
+
+    def set_z_upper(self, upper: bool):
+        """PFAM iterate in upper-block storage (pf_set_z_upper): the update skips the fp64 mirror."""
+        self._check(self.lib.pf_set_z_upper(self.h, 1 if upper else 0), "pf_set_z_upper")
 
     def invalidate(self):
         """A was written outside libpf: the next product re-splits it (PF_FP64_I8)."""

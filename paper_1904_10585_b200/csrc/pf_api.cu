@@ -152,6 +152,8 @@ struct pf_ctx_s {
   unsigned long long* a8_wmax = nullptr;
   // PFAM update on int8 tensor cores (pf_rebuild_i8.cu; one GPU, p = 64, fused digits)
   bool r8_on = false;
+  bool z_upper = false;                        // pf_set_z_upper: the update skips the fp64 mirror
+  const void* z_upper_src = nullptr;           // the iterate last written upper-only
   bool k7tma = true;                           // PF_K7TMA=0 at create: rebuild_kernel on PF_FP64
   int8_t* r8_VF8 = nullptr;                    // digit slices of V' (r8_bytes)
   int8_t* r8_V8 = nullptr;                     // digit slices of V
@@ -670,6 +672,11 @@ static bool use_i8(pf_ctx ctx) { return ctx->i8 && ctx->i8plan.S > 0; }
 static pf_status split_A(pf_ctx ctx, const double* A, int64_t lda, bool reuse, cudaStream_t st) {
   if (!use_i8(ctx)) return PF_OK;
   if (reuse && ctx->a8_valid && ctx->a8_src == A && ctx->a8_lda == lda) return PF_OK;
+  if (ctx->z_upper_src == A) {  // its blocks below the diagonal were not written (pf_set_z_upper)
+    snprintf(ctx->err, sizeof(ctx->err),
+             "iterate stored upper-only by pf_admm_step: a fresh digit split needs the full matrix");
+    return PF_ERR_UNSUPPORTED;
+  }
   PF_CU(i8_split_A_launch(A, lda, ctx->i8plan, ctx->A8, ctx->a8_rscale, ctx->num_sms, st));
   ctx->a8_fused = ctx->a8_half = false;
   ctx->a8_src = A;
@@ -1255,7 +1262,8 @@ pf_status pf_admm_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f
   // schedule will run products on fewer slices, which the half-storage kernel does not do)
   const bool half = ctx->i8s_ok && ctx->i8_early >= ctx->i8plan.S;
   R8Bufs r8{ctx->r8_maps, ctx->r8_VF8, ctx->r8_V8, ctx->r8_rs,
-            ctx->r8_rs + (size_t)ctx->i8plan.mtiles * 128, ctx->num_sms, half ? 0 : 1};
+            ctx->r8_rs + (size_t)ctx->i8plan.mtiles * 128, ctx->num_sms, half ? 0 : 1,
+            ctx->z_upper ? 0 : 1};
   const bool urec = ctx->prof && ctx->evu_used + 2 <= ctx->evu.size();
   if (urec) PF_CU(cudaEventRecord(ctx->evu[ctx->evu_used], st));
   PF_CU(admm_launch(Vf, ldf, V, ldv, f, t, adj, ldadj, deg, Z, ldz, (int)ctx->n_local,
@@ -1271,6 +1279,8 @@ pf_status pf_admm_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f
     ctx->a8_lda = ldz;
     ctx->a8_valid = ctx->a8_fused = true;
     ctx->a8_half = half && ctx->r8_on && ctx->i8plan.S == 7 && r8_usable(Z, ldz);
+    if (ctx->z_upper && ctx->r8_on && ctx->p == 64 && ctx->i8plan.S == 7 && r8_usable(Z, ldz))
+      ctx->z_upper_src = Z;
   }
   if (ctx->dist) {
     // <C, W> and the squared residual are sums over row blocks; sqrt after the reduction
@@ -1301,7 +1311,8 @@ pf_status pf_admm_step_f(pf_ctx ctx, const double* Q, int64_t ldq, const double*
   // schedule will run products on fewer slices, which the half-storage kernel does not do)
   const bool half = ctx->i8s_ok && ctx->i8_early >= ctx->i8plan.S;
   R8Bufs r8{ctx->r8_maps, ctx->r8_VF8, ctx->r8_V8, ctx->r8_rs,
-            ctx->r8_rs + (size_t)ctx->i8plan.mtiles * 128, ctx->num_sms, half ? 0 : 1};
+            ctx->r8_rs + (size_t)ctx->i8plan.mtiles * 128, ctx->num_sms, half ? 0 : 1,
+            ctx->z_upper ? 0 : 1};
   const bool urec = ctx->prof && ctx->evu_used + 2 <= ctx->evu.size();
   if (urec) PF_CU(cudaEventRecord(ctx->evu[ctx->evu_used], st));
   PF_CU(admm_launch(Qf, ldf, Q, ldq, nullptr, t, adj, ldadj, deg, Z, ldz, (int)ctx->n_local,
@@ -1317,6 +1328,8 @@ pf_status pf_admm_step_f(pf_ctx ctx, const double* Q, int64_t ldq, const double*
     ctx->a8_lda = ldz;
     ctx->a8_valid = ctx->a8_fused = true;
     ctx->a8_half = half && ctx->r8_on && ctx->i8plan.S == 7 && r8_usable(Z, ldz);
+    if (ctx->z_upper && ctx->r8_on && ctx->p == 64 && ctx->i8plan.S == 7 && r8_usable(Z, ldz))
+      ctx->z_upper_src = Z;
   }
   if (ctx->dist) {
     PF_TRY(allreduce(ctx, obj, 2, st));
@@ -1420,6 +1433,25 @@ pf_status pf_set_i8_schedule(pf_ctx ctx, int32_t early_slices, int32_t exact_tai
 pf_status pf_invalidate(pf_ctx ctx) {
   if (!ctx) return PF_ERR_ARG;
   iterate_written(ctx);
+  ctx->z_upper_src = nullptr;  // the caller wrote the iterate (in full)
+  return PF_OK;
+}
+
+pf_status pf_set_z_upper(pf_ctx ctx, int32_t upper) {
+  if (!ctx || (upper != 0 && upper != 1)) return PF_ERR_ARG;
+  if (!upper) {
+    ctx->z_upper = false;
+    ctx->z_upper_src = nullptr;
+    return PF_OK;
+  }
+  if (!use_i8(ctx) || ctx->dist || !ctx->fuse_digits || !ctx->r8_on || ctx->p != 64 ||
+      ctx->i8plan.S != 7 || !ctx->lz_sym_ws) {
+    snprintf(ctx->err, sizeof(ctx->err),
+             "upper-block storage needs the one-GPU int8-digit update (p = 64, S = 7) and the "
+             "symmetric Lanczos GEMV");
+    return PF_ERR_UNSUPPORTED;
+  }
+  ctx->z_upper = true;
   return PF_OK;
 }
 

@@ -248,6 +248,7 @@ struct R8Bufs {
   double* rsB;
   int num_sms;
   int mirror_dig;           // 0: upper-tile digits only (the half-storage product reads no others)
+  int mirror_z;             // 0: Z_new on and above the 128 x 128 diagonal blocks only
 };
 size_t r8_bytes(int n);
 bool r8_encode(CUtensorMap* maps, const int8_t* VF8, const int8_t* V8, const int8_t* A8, int n,
@@ -263,8 +264,8 @@ cudaError_t admm_i8_launch(const CUtensorMap* maps, const double* VF, const doub
                            int64_t ldv, int8_t* VF8, int8_t* V8, double* rsA, double* rsB,
                            const uint32_t* adj, int64_t ldadj, const double* deg, double t,
                            double* Z, int64_t ldz, int n, double* obj, double* partials,
-                           int* counter, const RbDigits* dig, int mirror_dig, int num_sms,
-                           cudaStream_t st);
+                           int* counter, const RbDigits* dig, int mirror_dig, int mirror_z,
+                           int num_sms, cudaStream_t st);
 cudaError_t admm_launch(const double* V, int64_t ldv, const double* Vloc, int64_t ldvl,
                         const double* f, double t, const uint32_t* adj, int64_t ldadj,
                         const double* deg, double* Z, int64_t ldz, int n_rows, int n, int row0,

@@ -771,7 +771,7 @@ cudaError_t admm_launch(const double* V, int64_t ldv, const double* Vloc, int64_
     if (r8 && p == 64 && dig->S == 7 && r8_usable(Z, ldz))
       return admm_i8_launch(r8->maps, vf, V, ldv, r8->VF8, r8->V8, r8->rsA, r8->rsB, adj, ldadj,
                             deg, t, Z, ldz, n, obj, partials, counter, dig, r8->mirror_dig,
-                            r8->num_sms, st);
+                            r8->mirror_z, r8->num_sms, st);
   } else if (tma_sms > 0 && p == 64 && row0 == 0 && n_rows == n && !raw &&
              td_usable(vf, V, ldv, Z, ldz)) {
     // one GPU, no digit output: the TMA-staged update with W on DMMA

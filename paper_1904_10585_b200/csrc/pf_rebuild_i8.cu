@@ -65,6 +65,7 @@ struct R8Args {
   double tt;
   int n, TC, MT, KB;
   int mirror_dig;     // 0: the digit slices of the upper tiles only (K1-i8s reads no others)
+  int mirror_z;       // 0: Z_new on and above the diagonal blocks only (pf_set_z_upper)
   const int* E;       // global digit exponent Eg of Z_new
   double* rscale;
   double* partials;
@@ -278,8 +279,10 @@ __global__ void __launch_bounds__(kR8Threads, 1)
         tma_store_2d(&m.z, zs + 16384, j0 + 16, i0);
         tma_store_3d(&m.dt, smem + kOffDt, j0 & 63, 0, (I * a.KB + (j0 >> 6)) * kR8S);
         if (!diagblk) {
+          if (a.mirror_z)
 #pragma unroll
-          for (int k = 0; k < 8; ++k) tma_store_2d(&m.zm, smem + kOffM + k * 4096, i0 + 16 * k, j0);
+            for (int k = 0; k < 8; ++k)
+              tma_store_2d(&m.zm, smem + kOffM + k * 4096, i0 + 16 * k, j0);
           const int kb0 = i0 >> 6, jt = (j0 >> 7) * a.KB;
           if (a.mirror_dig) {
             tma_store_3d(&m.dm, smem + kOffDm, 0, j0 & 127, (jt + kb0) * kR8S);
@@ -442,13 +445,15 @@ __global__ void __launch_bounds__(kR8Threads, 1)
       if (!diagblk) {
         // mirror fp64: box k = r / 16 holds mirror rows jj = 0..31 (tile columns), columns
         // r % 16, SWIZZLE_128B
-        unsigned char* mb = smem + kOffM + (r >> 4) * 4096;
-        const int mc = r & 15;
+        if (a.mirror_z) {
+          unsigned char* mb = smem + kOffM + (r >> 4) * 4096;
+          const int mc = r & 15;
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          const int jj = 16 * h + c;
-          *reinterpret_cast<double*>(mb + jj * 128 + ((((mc >> 1) ^ (jj & 7))) << 4) + (mc & 1) * 8) =
-              z[c];
+          for (int c = 0; c < 16; ++c) {
+            const int jj = 16 * h + c;
+            *reinterpret_cast<double*>(mb + jj * 128 + ((((mc >> 1) ^ (jj & 7))) << 4) +
+                                       (mc & 1) * 8) = z[c];
+          }
         }
         // mirror digits: 4 x 4 byte transposes across lanes 4k .. 4k+3 (rows rb .. rb+3); lane
         // 4k + u gets mirror row 16h + 4g + u, bytes = rows rb .. rb+3: exchange 16-bit halves
@@ -890,8 +895,8 @@ cudaError_t admm_i8_launch(const CUtensorMap* maps, const double* VF, const doub
                            int64_t ldv, int8_t* VF8, int8_t* V8, double* rsA, double* rsB,
                            const uint32_t* adj, int64_t ldadj, const double* deg, double t,
                            double* Z, int64_t ldz, int n, double* obj, double* partials,
-                           int* counter, const RbDigits* dig, int mirror_dig, int num_sms,
-                           cudaStream_t st) {
+                           int* counter, const RbDigits* dig, int mirror_dig, int mirror_z,
+                           int num_sms, cudaStream_t st) {
   const int mtiles = (n + 127) / 128, rows_pad = mtiles * 128;
   R8Maps m;
   m.a = maps[0];
@@ -921,6 +926,7 @@ cudaError_t admm_i8_launch(const CUtensorMap* maps, const double* VF, const doub
   a.MT = mtiles;
   a.KB = dig->KB;
   a.mirror_dig = mirror_dig;
+  a.mirror_z = mirror_z;
   a.E = dig->E;
   a.rscale = dig->rscale;
   a.partials = partials;

@@ -78,6 +78,12 @@ class Solver:
         if cfg.dtype == "f64i8":
             self.ctx.set_i8_schedule(cfg.i8_early, cfg.i8_tail)
         dist = nccl_id is not None or loop is not None
+        # upper-block storage of the PFAM iterate where the library supports it (one GPU, int8
+        # digits, p = 64, n <= 18944); elsewhere the iterate stays in full storage
+        self.z_upper = (cfg.z_upper and cfg.mode == "pfam" and cfg.dtype == "f64i8" and not dist
+                        and p == 64 and n <= 18944)
+        if self.z_upper:
+            self.ctx.set_z_upper(True)
         r0, r1 = rows_of(n, rank, world) if dist else (0, n)
         self.r0, self.r1, self.n_local = r0, r1, r1 - r0
         assert self.n_local == self.ctx.n_local
@@ -252,6 +258,17 @@ class Solver:
             else:
                 ctx.nce_step(self.V, self.f, cfg.tau, self.gdiag, self.x, self.x, self.A, self.obj,
                              st)
+
+    def iterate_entries(self, i, j) -> torch.Tensor:
+        """Entries Z[i, j] of the symmetric iterate, read where they are stored: in upper-block
+        storage (pf_set_z_upper) an entry left of row i's 128 x 128 diagonal block is read at
+        (j, i)."""
+        i = torch.as_tensor(i, device=self.A.device)
+        j = torch.as_tensor(j, device=self.A.device)
+        if self.z_upper:
+            low = j < torch.div(i, 128, rounding_mode="floor") * 128
+            i, j = torch.where(low, j, i), torch.where(low, i, j)
+        return self.A[i, j]
 
     def perturb(self, E: torch.Tensor):
         self.ctx.perturb(self.A, E, self.stream)

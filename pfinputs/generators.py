@@ -75,6 +75,9 @@ class Config:
     # sweep modes: Rayleigh-Ritz + spectral operator as F = f(H) by Newton-Schulz sign
     # iterations instead of a Jacobi EVD (NEXT-4 / reading R26; the oracle ignores it)
     rr_ns: bool = False
+    # PFAM on the one-GPU int8-digit path: the iterate in upper-block storage (pf_set_z_upper,
+    # the update skips the fp64 mirror; storage only, the oracle ignores it)
+    z_upper: bool = False
     # nearest correlation estimation (mode "nce"): paper Example eg:5.6 (6) or eg:5.7 (7)
     nce_example: int = 7
     # regularized extrapolation of the iterates (§4.3; NEXT-4): window l (0 = off)
@@ -153,7 +156,7 @@ def reduced(cfg: Config, **kw) -> Config:
 # R30 -- the Rayleigh-Ritz spectral operator in matrix form (P_+(H) = H when H is positive
 # definite, else Newton-Schulz with a Jacobi fallback; update W = Q F Q^T), and R29 -- lambda_min
 # tracked by warm-started 8-step Lanczos refreshes.  The full-size parity test runs the same.
-BENCH_METHOD = {"rr_ns": True, "lanczos_warm": 8}
+BENCH_METHOD = {"rr_ns": True, "lanczos_warm": 8, "z_upper": True}
 
 
 def bench_config(cfg_id: int = 3) -> Config:

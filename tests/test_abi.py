@@ -65,6 +65,7 @@ def test_argument_errors_are_synchronous_without_gpu():
     assert lib.pf_admm_step_f(None, None, 0, None, 1.0, None, 0, None, None, 0, None, None) == 1
     cnt = ctypes.c_int32(0)
     assert lib.pf_overlap_timeline(None, None, None, 0, ctypes.byref(cnt)) == 1
+    assert lib.pf_set_z_upper(None, 1) == 1
 
 
 def test_product_does_not_import_oracle():

@@ -77,10 +77,11 @@ def test_config3_fullsize_trajectory(cfg3_ref, dtype):
     cfg, prob, ref, Zref = cfg3_ref
     out = run(reduced(cfg, dtype=dtype), iters=12, problem=prob, graphs=True)
     _compare_qf(ref, out["records"], 1e-10, 1e-9)
-    Z = out["solver"].A
+    solver = out["solver"]
+    assert solver.z_upper == (dtype == "f64i8")   # the bench's storage (pf_set_z_upper)
     rng = np.random.default_rng(7)
     idx = rng.integers(0, cfg.n, size=(4000, 2))
-    zs = Z[torch.as_tensor(idx[:, 0]), torch.as_tensor(idx[:, 1])].cpu().numpy()
+    zs = solver.iterate_entries(idx[:, 0], idx[:, 1]).cpu().numpy()
     np.testing.assert_allclose(zs, Zref[idx[:, 0], idx[:, 1]], rtol=0,
                                atol=1e-10 * np.abs(Zref).max())
 

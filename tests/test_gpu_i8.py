@@ -393,3 +393,61 @@ def test_pfam_update_int8_matches_oracle(monkeypatch, n, form, sym):
         ref = Zg @ Y
         scale = np.abs(Zg).max() * np.abs(Y).max() * n
         assert np.abs(out.cpu().numpy() - ref).max() <= 2.0 ** (5 - 49) * scale
+
+
+@pytest.mark.parametrize("n", [1100, 2300])
+def test_z_upper_storage_same_trajectory(n):
+    """pf_set_z_upper (the bench's storage): the PFAM update skips the fp64 mirror below the
+    128 x 128 diagonal blocks.  Every reader of the iterate on this path reads the stored part
+    only, so the trajectory (factors, <C, W>, ||Z+ - Z||) and the stored part of Z are
+    bit-identical to full storage; the blocks below keep their stale values."""
+    from pfinputs import bench_config, pfam_problem
+    from paper_1904_10585_b200 import run
+    cfg = reduced(bench_config(3), n=n, p=64, iters=5, edge_prob=0.07, dtype="f64i8",
+                  lanczos_every=2)
+    prob = pfam_problem(cfg)
+    outs = [run(reduced(cfg, z_upper=zu), iters=5, problem=prob, graphs=True) for zu in (True, False)]
+    assert outs[0]["solver"].z_upper and not outs[1]["solver"].z_upper
+    for a, b in zip(outs[0]["records"], outs[1]["records"]):
+        assert a["objective"] == b["objective"] and a["aux"] == b["aux"]
+        assert np.array_equal(a["Q"], b["Q"]) and np.array_equal(a["QF"], b["QF"])
+    Zu, Zf = outs[0]["solver"].A.cpu().numpy(), outs[1]["solver"].A.cpu().numpy()
+    rows = np.arange(n)[:, None]
+    stored = np.arange(n)[None, :] >= (rows // 128) * 128
+    assert np.array_equal(Zu[stored], Zf[stored])
+    i, j = np.nonzero(~stored)
+    if i.size:
+        got = outs[0]["solver"].iterate_entries(i, j).cpu().numpy()
+        assert np.array_equal(got, Zf[i, j])           # read through the mirror
+        assert not np.array_equal(Zu[i, j], Zf[i, j])  # the stale part really is not written
+
+
+def test_z_upper_storage_argument_errors():
+    from paper_1904_10585_b200._lib import Context, PF_FP64, PF_FP64_I8, load
+    lib = load()
+    c = Context(2000, 64, 4, dtype=PF_FP64_I8)
+    assert lib.pf_set_z_upper(c.h, 2) == 1                 # not 0 / 1 -> ARG
+    assert lib.pf_set_z_upper(c.h, 1) == 0 and lib.pf_set_z_upper(c.h, 0) == 0
+    assert lib.pf_set_z_upper(Context(2000, 64, 4, dtype=PF_FP64).h, 1) == 7   # DMMA update
+    assert lib.pf_set_z_upper(Context(2000, 32, 4, dtype=PF_FP64_I8).h, 1) == 7  # p != 64
+    assert lib.pf_set_z_upper(Context(20000, 64, 4, dtype=PF_FP64_I8).h, 1) == 7  # full GEMV
+
+
+def test_z_upper_storage_refuses_a_fresh_split():
+    """After an upper-only update, a digit split of that iterate (it would read the stale lower
+    blocks) fails loudly until pf_invalidate declares the matrix written in full."""
+    from pfinputs import bench_config, pfam_problem
+    from paper_1904_10585_b200 import run
+    from paper_1904_10585_b200._lib import PFError
+    cfg = reduced(bench_config(3), n=700, p=64, iters=2, edge_prob=0.1, dtype="f64i8")
+    out = run(cfg, iters=2, problem=pfam_problem(cfg))
+    s = out["solver"]
+    Z = s.A
+    Y = torch.randn((cfg.n, 64), dtype=torch.float64, device="cuda")
+    o = torch.empty_like(Y)
+    s.ctx.matmul(Z, Y, o)                    # the update's own digits: fine
+    s.ctx.set_i8_slices(7)                   # drops the digits: the next product re-splits Z
+    with pytest.raises(PFError):
+        s.ctx.matmul(Z, Y, o)
+    s.ctx.invalidate()                       # the caller declares Z written in full
+    s.ctx.matmul(Z, Y, o)
