@@ -238,8 +238,13 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
         # 128 x 128 diagonal blocks only
         zup = bool(getattr(s, "z_upper", False))
         zw = 8.0 * n * (n + 128) / 2 if zup else 8.0 * n * n
-        ubytes = 8.0 * n * (n + 1) / 2 + zw + (7.0 * n * n if fused else 0.0) \
-            + 2 * 8.0 * n * p + n * n / 16.0
+        # digit slices of Z_new: every tile, or (the filter reads the lower tiles as the stored
+        # upper ones transposed: PF_I8T / PF_I8SYM) the upper tiles and the
+        # 256 x 256 diagonal super-blocks only
+        half = k7i8 and world == 1 and (os.environ.get("PF_I8T", "1") != "0" or
+                                        os.environ.get("PF_I8SYM") == "1")
+        dw = (7.0 * n * (n + 256) / 2 if half else 7.0 * n * n) if fused else 0.0
+        ubytes = 8.0 * n * (n + 1) / 2 + zw + dw + 2 * 8.0 * n * p + n * n / 16.0
         uavg = upd_ms / upd_n
         utraffic = None
         try:
@@ -257,6 +262,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> dict | None:
                     "traffic": utraffic, "algorithmic_bytes_per_launch": ubytes,
                     "avg_launch_ms": uavg, "launches": upd_n, "share_of_step": upd_share,
                     "z_storage": "upper blocks (pf_set_z_upper)" if zup else "full",
+                    "digit_tiles": "upper tiles + diagonal super-blocks (K1-i8p reads the rest "
+                                   "transposed)" if half else "all",
                     "timed": "events around pf_admm_step (row bounds + splits + update kernel)"}
     filter_flops_per_step = 2.0 * d * n * n * p
     cpu = cpu_baseline(cfg, args) if (world == 1 and not args.no_cpu) else None

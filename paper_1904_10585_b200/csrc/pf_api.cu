@@ -132,6 +132,7 @@ struct pf_ctx_s {
   // half-storage symmetric product (K1-i8s, pf_gemm_i8.cu) on fused digits: the stored tiles
   // (I, J >= I) only; PF_I8SYM=1 at create turns it on
   bool i8s_ok = false;
+  bool i8t_ok = false;                         // K1-i8p reads upper-tile digits (lower transposed)
   CUtensorMap mapA8t;                          // 64-row boxes read transposed
   bool a8_half = false;                        // A8 holds the upper tiles only (no mirror digits)
   CUtensorMap mapY8[4];                        // B boxes of 4..7 digit slices
@@ -222,7 +223,8 @@ pf_status pf_nccl_unique_id(void* out, int32_t bytes) {
 
 static bool encode_i8_maps(pf_ctx ctx) {
   if (!i8_encode_A(&ctx->mapA8, &ctx->mapA8pf, ctx->A8, ctx->i8plan)) return false;
-  if (ctx->i8s_ok && !i8s_encode_At(&ctx->mapA8t, ctx->A8, ctx->i8plan)) return false;
+  if ((ctx->i8s_ok || ctx->i8t_ok) && !i8s_encode_At(&ctx->mapA8t, ctx->A8, ctx->i8plan))
+    return false;
   for (int su = 4; su <= ctx->i8plan.S; ++su)
     if (!i8_encode_B(&ctx->mapY8[su - 4], ctx->Y8, ctx->i8plan, su)) return false;
   if (ctx->i8plan.pair && !i8_encode_B_pair(&ctx->mapY8p[0], &ctx->mapY8p[1], ctx->Y8, ctx->i8plan))
@@ -442,6 +444,9 @@ static pf_status create_common(int64_t n, int32_t p, int32_t degree, pf_dtype dt
     // one CTA per 128-row tile (128 of 148 SMs at n = 16384) and measured slower
     const char* e8 = getenv("PF_I8SYM");
     ctx->i8s_ok = !dist && (e8 && e8[0] == '1') && i8s_supported(ctx->i8plan, ctx->num_sms);
+    // K1-i8p on upper-tile digits (PF_I8T=0: the update writes every mirror digit tile)
+    const char* et = getenv("PF_I8T");
+    ctx->i8t_ok = !dist && !ctx->i8s_ok && !(et && et[0] == '0') && ctx->i8plan.pair;
   }
   {
     const char* e = getenv("PF_K7TMA");
@@ -711,7 +716,10 @@ static pf_status gemm_step(pf_ctx ctx, int bidx, const double* ycur, const doubl
     su = (su <= 0 || su > S) ? S : su;
     // fused digits of a symmetric iterate (one scale): the half-storage product
     const bool sym = ctx->i8s_ok && ctx->a8_fused && su == S && S == 7;
-    if (ctx->a8_half && !sym) {
+    // upper-tile digits (the update skipped the mirror tiles): K1-i8p reads the lower part
+    // transposed
+    const bool lowt = ctx->i8t_ok && ctx->a8_half && su == S && S == 7 && ctx->i8plan.pair;
+    if (ctx->a8_half && !sym && !lowt) {
       snprintf(ctx->err, sizeof(ctx->err), "upper-tile digits need the full slice count");
       return PF_ERR_UNSUPPORTED;
     }
@@ -722,7 +730,7 @@ static pf_status gemm_step(pf_ctx ctx, int bidx, const double* ycur, const doubl
       PF_CU(i8_gemm_launch(ctx->i8plan, ctx->mapA8, ctx->mapY8[su - 4], ctx->mapA8pf,
                            ctx->a8_rscale, ctx->y8_cscale, ycur, yprev, out, ctx->p, coef,
                            ctx->i8_acc, ctx->i8_part, ctx->i8_cnt, su, st, &ctx->mapY8p[0],
-                           &ctx->mapY8p[1]));
+                           &ctx->mapY8p[1], lowt ? &ctx->mapA8t : nullptr));
   }
   else
     PF_CU(cheb_gemm_launch(ctx->plan, ctx->mapA, *mb, ycur, yprev, out, coef, ctx->cheb_ws,
@@ -1260,7 +1268,7 @@ pf_status pf_admm_step(pf_ctx ctx, const double* V, int64_t ldv, const double* f
   RbDigits dig{ctx->A8, ctx->i8plan.kblocks, ctx->i8plan.S, ctx->a8_E, ctx->a8_rscale, ctx->a8_wa, ctx->a8_wmax};
   // the half-storage product reads the upper tiles only: no mirror digits (unless a precision
   // schedule will run products on fewer slices, which the half-storage kernel does not do)
-  const bool half = ctx->i8s_ok && ctx->i8_early >= ctx->i8plan.S;
+  const bool half = (ctx->i8s_ok || ctx->i8t_ok) && ctx->i8_early >= ctx->i8plan.S;
   R8Bufs r8{ctx->r8_maps, ctx->r8_VF8, ctx->r8_V8, ctx->r8_rs,
             ctx->r8_rs + (size_t)ctx->i8plan.mtiles * 128, ctx->num_sms, half ? 0 : 1,
             ctx->z_upper ? 0 : 1};
@@ -1309,7 +1317,7 @@ pf_status pf_admm_step_f(pf_ctx ctx, const double* Q, int64_t ldq, const double*
   RbDigits dig{ctx->A8, ctx->i8plan.kblocks, ctx->i8plan.S, ctx->a8_E, ctx->a8_rscale, ctx->a8_wa, ctx->a8_wmax};
   // the half-storage product reads the upper tiles only: no mirror digits (unless a precision
   // schedule will run products on fewer slices, which the half-storage kernel does not do)
-  const bool half = ctx->i8s_ok && ctx->i8_early >= ctx->i8plan.S;
+  const bool half = (ctx->i8s_ok || ctx->i8t_ok) && ctx->i8_early >= ctx->i8plan.S;
   R8Bufs r8{ctx->r8_maps, ctx->r8_VF8, ctx->r8_V8, ctx->r8_rs,
             ctx->r8_rs + (size_t)ctx->i8plan.mtiles * 128, ctx->num_sms, half ? 0 : 1,
             ctx->z_upper ? 0 : 1};

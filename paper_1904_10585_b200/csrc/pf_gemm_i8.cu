@@ -260,6 +260,8 @@ struct I8Cfg {
 
 struct I8Args {
   int pf_dist;           // L2 prefetch distance of the A k-blocks (0: off)
+  int lower_t;           // K1-i8p: A holds the upper tiles (+ diagonal super-blocks) only; the
+                         // units left of the pair's super-block read the stored upper tile transposed
   int lS;                // slices per (tile, k-block) in the A8 layout (the split's S >= S used)
   const double* ycur;
   const double* yprev;
@@ -724,7 +726,8 @@ struct I8PCfg {
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8PCfg::THREADS, 1)
     cheb_gemm_i8p_kernel(const __grid_constant__ CUtensorMap mapA8,
                          const __grid_constant__ CUtensorMap mapB64,
-                         const __grid_constant__ CUtensorMap mapB32, I8Args args) {
+                         const __grid_constant__ CUtensorMap mapB32,
+                         const __grid_constant__ CUtensorMap mapA8t, I8Args args) {
   using C = I8PCfg;
   constexpr int S = C::S, NC = C::NC;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -760,6 +763,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8PCfg::THREADS, 1)
     tma_prefetch_desc(&mapA8);
     tma_prefetch_desc(&mapB64);
     tma_prefetch_desc(&mapB32);
+    if (args.lower_t) tma_prefetch_desc(&mapA8t);
   }
   if (warp == 2) tc::tmem_alloc_pair<C::TMEM_COLS>(tmem_slot);
   tc::fence_before_sync();
@@ -814,13 +818,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8PCfg::THREADS, 1)
           rb.next();
           continue;
         }
+        // lower-transposed mode: column tile J = kb / 2 left of the pair's 256 x 256 diagonal
+        // super-block -> rows 64 (kb & 1) .. +63 of the stored tile (J, tile)'s k-blocks 2 tile,
+        // 2 tile + 1 (an MN-major operand, two 64-row boxes; K1-i8s reads them the same way)
+        const bool tr = args.lower_t && (kb >> 1) < 2 * pt;
 #pragma unroll
         for (int s = 0; s < S; ++s) {
           mbar_wait(&aempty[ra.s], ra.ph ^ 1u);
           if (i8::elect_one()) {
             if (crank == 0) mbar_arrive_expect_tx(&afull[ra.s], 2 * C::A_TILE);
-            tc::tma_load_3d_pair(ring_a + ra.s * C::A_TILE, &mapA8, afull_l + 8u * (uint32_t)ra.s,
-                                 0, 0, (tile * KB + kb) * args.lS + s, pol_a);
+            unsigned char* dst = ring_a + ra.s * C::A_TILE;
+            const uint32_t bar = afull_l + 8u * (uint32_t)ra.s;
+            if (!tr) {
+              tc::tma_load_3d_pair(dst, &mapA8, bar, 0, 0, (tile * KB + kb) * args.lS + s, pol_a);
+            } else {
+              const int blk = (kb >> 1) * KB + 2 * tile;  // past the tensor: zero-filled
+              tc::tma_load_3d_pair(dst, &mapA8t, bar, 0, 64 * (kb & 1), blk * args.lS + s, pol_a);
+              tc::tma_load_3d_pair(dst + C::A_TILE / 2, &mapA8t, bar, 0, 64 * (kb & 1),
+                                   (blk + 1) * args.lS + s, pol_a);
+            }
           }
           __syncwarp();
           ra.next();
@@ -835,6 +851,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8PCfg::THREADS, 1)
       SegIter si(U, G, g, KB);
       int it, kbs, kbe;
       const uint64_t adesc_ring = tc::sdesc_k_sw64(smem_u32(ring_a));
+      // MN-major A (lower-transposed units): the two 64-byte M chunks 4 KB apart (LBO), a K step
+      // of 32 rows = 2 KB; instruction-descriptor bit 15 = transpose A (tools/probe/i8_mn.cu)
+      const uint64_t adesc_ring_t = (adesc_ring & ~(0x3FFFull << 16)) | ((uint64_t)(4096 >> 4) << 16);
       const uint64_t bdesc_ring = tc::sdesc_k_sw64(smem_u32(ring_b));
       // per A slice: up to two MMAs {B region row, N, TMEM column}
       constexpr int MM[7][2][3] = {{{0, 256, 0}, {128, 192, 256}},  {{0, 256, 64}, {224, 128, 320}},
@@ -842,6 +861,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8PCfg::THREADS, 1)
                                    {{320, 192, 256}, {0, 0, 0}},    {{416, 128, 320}, {0, 0, 0}},
                                    {{480, 64, 384}, {0, 0, 0}}};
       while (si.next(it, kbs, kbe)) {
+        const int pt = it % mpairs;
         for (int k0 = kbs; k0 < kbe; k0 += kch) {
           const int k1 = min(kbe, k0 + kch);
           tc::mbar_wait_cluster(tempty, tph ^ 1u);  // both epilogues drained the accumulators
@@ -849,21 +869,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8PCfg::THREADS, 1)
           for (int kb = k0; kb < k1; ++kb) {
             tc::mbar_wait_cluster(&bfull[rb.s], rb.ph);
             const uint64_t bd0 = bdesc_ring + (uint64_t)(rb.s * (C::B_STAGE >> 4));
+            const bool tr = args.lower_t && (kb >> 1) < 2 * pt;
+            const uint32_t tbit = tr ? (1u << 15) : 0u;
 #pragma unroll
             for (int s = 0; s < S; ++s) {
               tc::mbar_wait_cluster(&afull[ra.s], ra.ph);
               tc::fence_after_sync();
-              const uint64_t ad0 = adesc_ring + (uint64_t)(ra.s * (C::A_TILE >> 4));
+              const uint64_t ad0 = (tr ? adesc_ring_t : adesc_ring) +
+                                   (uint64_t)(ra.s * (C::A_TILE >> 4));
               if (i8::elect_one()) {
 #pragma unroll
                 for (int ks = 0; ks < 2; ++ks) {
                   const uint32_t acc = (kb == k0 && s == 0 && ks == 0) ? 0u : 1u;
+                  const uint64_t ad = ad0 + (uint64_t)(tr ? ks * (2048 >> 4) : ks * 2);
 #pragma unroll
                   for (int m = 0; m < 2; ++m) {
                     if (MM[s][m][1] == 0) continue;
-                    i8::mma_i8_pair(tmem + (uint32_t)MM[s][m][2], ad0 + (uint64_t)(ks * 2),
+                    i8::mma_i8_pair(tmem + (uint32_t)MM[s][m][2], ad,
                                     bd0 + (uint64_t)((MM[s][m][0] * C::BK + ks * 32) >> 4),
-                                    i8::idesc_i8(256, MM[s][m][1]), acc);
+                                    i8::idesc_i8(256, MM[s][m][1]) | tbit, acc);
                   }
                 }
                 tc::mma_commit_pair(&aempty[ra.s]);  // the slice stage is free in both CTAs
@@ -1454,11 +1478,12 @@ cudaError_t i8_gemm_launch(const I8Plan& pl, const CUtensorMap& mapA8, const CUt
                            const CUtensorMap& mapA8pf, const double* rscale, const double* cscale, const double* ycur,
                            const double* yprev, double* out, int64_t ldy, const double* coef,
                            double* acc, double* part, int* counters, int su, cudaStream_t st,
-                           const CUtensorMap* mapB64, const CUtensorMap* mapB32) {
+                           const CUtensorMap* mapB64, const CUtensorMap* mapB32,
+                           const CUtensorMap* mapA8t) {
   // su <= pl.S: only the su most significant digit slices of both operands are multiplied --
   // exactly the su-digit expansion (the digits of a longer truncating expansion start with
   // those of a shorter one), levels 2..su+1; the B map must have a box of su slices
-  I8Args a;
+  I8Args a = {};
   a.part = part;
   a.counters = counters;
   a.maxp = pl.maxp;
@@ -1488,9 +1513,10 @@ cudaError_t i8_gemm_launch(const I8Plan& pl, const CUtensorMap& mapA8, const CUt
       attr_p = true;
     }
     a.maxp = pl.pmaxp;
+    a.lower_t = mapA8t ? 1 : 0;
     count_launch();
-    cheb_gemm_i8p_kernel<<<pl.pgrid, I8PCfg::THREADS, I8PCfg::SMEM, st>>>(mapA8, *mapB64,
-                                                                          *mapB32, a);
+    cheb_gemm_i8p_kernel<<<pl.pgrid, I8PCfg::THREADS, I8PCfg::SMEM, st>>>(
+        mapA8, *mapB64, *mapB32, mapA8t ? *mapA8t : mapA8, a);
     return cudaGetLastError();
   }
   switch (su) {

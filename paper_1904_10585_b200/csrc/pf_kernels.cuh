@@ -94,7 +94,8 @@ cudaError_t i8_gemm_launch(const I8Plan& pl, const CUtensorMap& mapA8, const CUt
                            const CUtensorMap& mapA8pf, const double* rscale, const double* cscale, const double* ycur,
                            const double* yprev, double* out, int64_t ldy, const double* coef,
                            double* acc, double* part, int* counters, int su, cudaStream_t st,
-                           const CUtensorMap* mapB64 = nullptr, const CUtensorMap* mapB32 = nullptr);
+                           const CUtensorMap* mapB64 = nullptr, const CUtensorMap* mapB32 = nullptr,
+                           const CUtensorMap* mapA8t = nullptr);  // K1-i8p lower-transposed mode
 
 // ---- Newton-Schulz spectral operator (pf_ns.cu): F = f(H) of a p x p symmetric fp64 matrix
 struct NsWork;

@@ -64,7 +64,9 @@ struct R8Args {
   const double* deg;
   double tt;
   int n, TC, MT, KB;
-  int mirror_dig;     // 0: the digit slices of the upper tiles only (K1-i8s reads no others)
+  int mirror_dig;     // 0: the digit slices of the upper tiles (and of the lower tiles inside the
+                      // 256 x 256 diagonal super-blocks) only: K1-i8s and K1-i8p in lower-
+                      // transposed mode read no others
   int mirror_z;       // 0: Z_new on and above the diagonal blocks only (pf_set_z_upper)
   const int* E;       // global digit exponent Eg of Z_new
   double* rscale;
@@ -272,6 +274,7 @@ __global__ void __launch_bounds__(kR8Threads, 1)
     for (long long t = t_begin; t < t_end; ++t, ++it, r8_next(a.TC, I, J)) {
       const int i0 = I * kR8M, j0 = J * kR8N, zb = it & 1;
       const bool diagblk = J < 4 * I + 4;
+      const bool sblk = (I & 1) == 0 && (J >> 2) == I + 1;
       mbar_wait_idle(sfull, it & 1);
       if (i8::elect_one()) {
         const unsigned char* zs = smem + kOffZ + zb * 32768;
@@ -284,7 +287,7 @@ __global__ void __launch_bounds__(kR8Threads, 1)
             for (int k = 0; k < 8; ++k)
               tma_store_2d(&m.zm, smem + kOffM + k * 4096, i0 + 16 * k, j0);
           const int kb0 = i0 >> 6, jt = (j0 >> 7) * a.KB;
-          if (a.mirror_dig) {
+          if (a.mirror_dig || sblk) {
             tma_store_3d(&m.dm, smem + kOffDm, 0, j0 & 127, (jt + kb0) * kR8S);
             if (kb0 + 1 < a.KB)
               tma_store_3d(&m.dm, smem + kOffDm + kR8S * 2048, 0, j0 & 127,
@@ -329,6 +332,8 @@ __global__ void __launch_bounds__(kR8Threads, 1)
       const int i0 = I * kR8M, j0 = J * kR8N;
       const int i = i0 + r, jb = j0 + 16 * h;
       const bool diagblk = J < 4 * I + 4;             // inside the 128 x 128 diagonal block
+      // mirror inside a 256 x 256 diagonal super-block (written even without mirror_dig)
+      const bool sblk = (I & 1) == 0 && (J >> 2) == I + 1;
       const bool fast = !diagblk && (i0 + kR8M <= a.n) && (j0 + kR8N <= a.n);
       const uint32_t word = wraw >> (jb & 31);
       const double rsi = rs;
@@ -460,7 +465,9 @@ __global__ void __launch_bounds__(kR8Threads, 1)
         // with lane u ^ 2, then bytes with lane u ^ 1.  [kb][slice][32 rows][64 B], SWIZZLE_64B
         // (16-byte chunk ^= bits 7-8 of the offset)
         const int rb = 32 * q + (lane & ~3);
-        if (a.mirror_dig)
+        // (sblk: the mirror lies in a 256 x 256 diagonal super-block, which K1-i8p reads
+        // directly even in lower-transposed mode)
+        if (a.mirror_dig || sblk)
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
           const int jj = 16 * h + 4 * g + u;
@@ -635,6 +642,7 @@ __global__ void __launch_bounds__(kTdThreads, 1)
     for (long long t = t_begin; t < t_end; ++t, ++it, r8_next(a.TC, I, J)) {
       const int i0 = I * kR8M, j0 = J * kR8N, b = it & 1;
       const bool diagblk = J < 4 * I + 4;
+      const bool sblk = (I & 1) == 0 && (J >> 2) == I + 1;
       mbar_wait_idle(sfull, it & 1);
       if (i8::elect_one()) {
         const unsigned char* zs = smem + kTdOffZ + b * 32768;

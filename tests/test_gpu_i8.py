@@ -451,3 +451,24 @@ def test_z_upper_storage_refuses_a_fresh_split():
         s.ctx.matmul(Z, Y, o)
     s.ctx.invalidate()                       # the caller declares Z written in full
     s.ctx.matmul(Z, Y, o)
+
+
+@pytest.mark.parametrize("n", [1100, 1333, 2600])
+def test_lower_transposed_filter_same_trajectory(monkeypatch, n):
+    """K1-i8p in lower-transposed mode (the default, PF_I8T): the update writes the digit slices
+    of the upper tiles and of the 256 x 256 diagonal super-blocks only, and the filter reads every
+    tile left of a pair's super-block as the stored upper tile transposed (MN-major A).  The
+    digits and every exact level sum are the same, so the trajectory is bit-identical to the one
+    with all mirror digits written (PF_I8T=0); odd tile counts and graphs included."""
+    from pfinputs import bench_config, pfam_problem
+    from paper_1904_10585_b200 import run
+    cfg = reduced(bench_config(3), n=n, p=64, iters=4, edge_prob=0.07, dtype="f64i8",
+                  lanczos_every=2)
+    prob = pfam_problem(cfg)
+    outs = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("PF_I8T", flag)
+        outs.append(run(cfg, iters=4, problem=prob, graphs=True))
+    for a, b in zip(outs[0]["records"], outs[1]["records"]):
+        assert a["objective"] == b["objective"] and a["aux"] == b["aux"]
+        assert np.array_equal(a["Q"], b["Q"]) and np.array_equal(a["QF"], b["QF"])
