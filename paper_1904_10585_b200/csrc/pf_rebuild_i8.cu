@@ -150,11 +150,14 @@ __global__ void __launch_bounds__(kR8Threads, 1)
   uint64_t* bempty = bars + 3;
   uint64_t* tfull = bars + 4;   // [2] accumulator complete
   uint64_t* tempty = bars + 6;  // [2] accumulator drained (8 update warps)
-  uint64_t* zfull = bars + 8;   // [2] Z_old tile landed
-  uint64_t* zempty = bars + 10; // [2] the Z_new stores have read the buffer
-  uint64_t* sfull = bars + 12;  // staging + Z_new written (8 update warps)
-  uint64_t* sempty = bars + 13; // the stores have read the staging
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  uint64_t* zfull = bars + 8;   // [nz] Z_old tile landed
+  uint64_t* zempty = bars + 11; // [nz] the Z_new stores have read the buffer
+  uint64_t* sfull = bars + 14;  // staging + Z_new written (8 update warps)
+  uint64_t* sempty = bars + 15; // the stores have read the staging
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  // Z_old / Z_new buffers: 2, or 3 when no fp64 mirror is written (its staging area is free)
+  const int nz = a.mirror_z ? 2 : 3;
+  auto zbuf = [&](int zb) { return smem + (zb < 2 ? kOffZ + zb * 32768 : kOffM); };
   __shared__ double red[32];
   __shared__ int s_last;
 
@@ -167,6 +170,8 @@ __global__ void __launch_bounds__(kR8Threads, 1)
     for (int q = 0; q < 2; ++q) {
       mbar_init(&tfull[q], 1);
       mbar_init(&tempty[q], 8);
+    }
+    for (int q = 0; q < 3; ++q) {
       mbar_init(&zfull[q], 1);
       mbar_init(&zempty[q], 1);
     }
@@ -204,12 +209,13 @@ __global__ void __launch_bounds__(kR8Threads, 1)
     int it = 0, I = 0, J = 0;
     if (t_begin < t_end) r8_tile(t_begin, a.TC, a.MT, I, J);
     for (long long t = t_begin; t < t_end; ++t, ++it, r8_next(a.TC, I, J)) {
-      const int i0 = I * kR8M, j0 = J * kR8N, zb = it & 1;
+      const int i0 = I * kR8M, j0 = J * kR8N, zb = it % nz;
+      const uint32_t zph = (uint32_t)((it / nz) & 1);
       // Z_old first: the update warps wait for it; the MMA has slack
-      mbar_wait_idle(&zempty[zb], ((it >> 1) & 1) ^ 1u);
+      mbar_wait_idle(&zempty[zb], zph ^ 1u);
       if (i8::elect_one()) {
         mbar_arrive_expect_tx(&zfull[zb], 32768);
-        unsigned char* zs = smem + kOffZ + zb * 32768;
+        unsigned char* zs = zbuf(zb);
         tc::tma_load_2d_hint(zs, &m.z, &zfull[zb], j0, i0, stream);
         tc::tma_load_2d_hint(zs + 16384, &m.z, &zfull[zb], j0 + 16, i0, stream);
       }
@@ -272,12 +278,12 @@ __global__ void __launch_bounds__(kR8Threads, 1)
     int it = 0, I = 0, J = 0;
     if (t_begin < t_end) r8_tile(t_begin, a.TC, a.MT, I, J);
     for (long long t = t_begin; t < t_end; ++t, ++it, r8_next(a.TC, I, J)) {
-      const int i0 = I * kR8M, j0 = J * kR8N, zb = it & 1;
+      const int i0 = I * kR8M, j0 = J * kR8N, zb = it % nz;
       const bool diagblk = J < 4 * I + 4;
       const bool sblk = (I & 1) == 0 && (J >> 2) == I + 1;
       mbar_wait_idle(sfull, it & 1);
       if (i8::elect_one()) {
-        const unsigned char* zs = smem + kOffZ + zb * 32768;
+        const unsigned char* zs = zbuf(zb);
         tma_store_2d(&m.z, zs, j0, i0);
         tma_store_2d(&m.z, zs + 16384, j0 + 16, i0);
         tma_store_3d(&m.dt, smem + kOffDt, j0 & 63, 0, (I * a.KB + (j0 >> 6)) * kR8S);
@@ -356,7 +362,7 @@ __global__ void __launch_bounds__(kR8Threads, 1)
         cs[c + 1] = v.y;
       }
       // ---- W from the TMEM levels (smallest weight first)
-      const int tb = it & 1, zb = it & 1;
+      const int tb = it & 1, zb = it % nz;
       mbar_wait(&tfull[tb], (it >> 1) & 1);
       tc::fence_after_sync();
       // levels in pairs: 128 D_l + D_{l+1} is exact in int32 (|D_l| <= (l+1) 64 127^2 < 2^23),
@@ -384,8 +390,8 @@ __global__ void __launch_bounds__(kR8Threads, 1)
 #pragma unroll
       for (int c = 0; c < 16; ++c) w[c] *= rsi * cs[c];  // exact: powers of two
       // ---- Z_old (swizzled 128-byte rows: chunk k of row r at k ^ (r % 8))
-      mbar_wait(&zfull[zb], (it >> 1) & 1);
-      double* zrow = reinterpret_cast<double*>(smem + kOffZ + zb * 32768 + h * 16384 + r * 128);
+      mbar_wait(&zfull[zb], (uint32_t)((it / nz) & 1));
+      double* zrow = reinterpret_cast<double*>(zbuf(zb) + h * 16384 + r * 128);
       double z[16];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
