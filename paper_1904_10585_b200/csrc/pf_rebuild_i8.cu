@@ -137,6 +137,9 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read0() {
   asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
 }
+__device__ __forceinline__ void bulk_wait_read1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+}
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 
 __global__ void __launch_bounds__(kR8Threads, 1)
@@ -284,8 +287,8 @@ __global__ void __launch_bounds__(kR8Threads, 1)
       mbar_wait_idle(sfull, it & 1);
       if (i8::elect_one()) {
         const unsigned char* zs = zbuf(zb);
-        tma_store_2d(&m.z, zs, j0, i0);
-        tma_store_2d(&m.z, zs + 16384, j0 + 16, i0);
+        // two bulk groups: the staging (digits, mirrors) first, released as soon as its stores
+        // have read it (the update warps write the next tile's digits there), then Z_new
         tma_store_3d(&m.dt, smem + kOffDt, j0 & 63, 0, (I * a.KB + (j0 >> 6)) * kR8S);
         if (!diagblk) {
           if (a.mirror_z)
@@ -301,9 +304,13 @@ __global__ void __launch_bounds__(kR8Threads, 1)
           }
         }
         bulk_commit();
+        tma_store_2d(&m.z, zs, j0, i0);
+        tma_store_2d(&m.z, zs + 16384, j0 + 16, i0);
+        bulk_commit();
+        bulk_wait_read1();
+        mbar_arrive(sempty);
         bulk_wait_read0();
         mbar_arrive(&zempty[zb]);
-        mbar_arrive(sempty);
       }
       __syncwarp();
     }
