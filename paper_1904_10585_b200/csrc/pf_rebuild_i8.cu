@@ -43,7 +43,9 @@ bool encode_map_gen(CUtensorMap* map, bool f64, int rank, const void* base, cons
 
 constexpr int kR8S = 7;                        // digit slices of V', V and Z_new
 constexpr int kR8M = 128, kR8N = 32;           // tile
-constexpr int kR8Threads = 384;
+constexpr int kR8UW = 16;                      // update warps (4 per TMEM lane quarter)
+constexpr int kR8C = kR8N / (kR8UW / 4);       // tile columns per update thread
+constexpr int kR8Threads = 128 + 32 * kR8UW;
 constexpr int kOffA = 0;                       // 7 x 128 x 64 B
 constexpr int kOffB = kOffA + kR8S * 8192;     // 7 x 32 x 64 B
 constexpr int kOffZ = kOffB + kR8S * 2048;     // 2 buffers x 2 boxes {16 fp64, 128 rows}
@@ -142,6 +144,21 @@ __device__ __forceinline__ void bulk_wait_read1() {
 }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 
+// 32 lanes x kR8C consecutive 32-bit TMEM columns (then a wait)
+template <int N>
+__device__ __forceinline__ void tmem_ld_c(uint32_t taddr, uint32_t (&r)[N]) {
+  if constexpr (N == 16) {
+    i8::tmem_ld16(taddr, r);
+  } else {
+    static_assert(N == 8, "kR8C");
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                   "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+  }
+}
+
 __global__ void __launch_bounds__(kR8Threads, 1)
     rebuild_i8_kernel(const __grid_constant__ R8Maps m, const R8Args a) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -172,13 +189,13 @@ __global__ void __launch_bounds__(kR8Threads, 1)
     mbar_init(bempty, 1);
     for (int q = 0; q < 2; ++q) {
       mbar_init(&tfull[q], 1);
-      mbar_init(&tempty[q], 8);
+      mbar_init(&tempty[q], kR8UW);
     }
     for (int q = 0; q < 3; ++q) {
       mbar_init(&zfull[q], 1);
       mbar_init(&zempty[q], 1);
     }
-    mbar_init(sfull, 8);
+    mbar_init(sfull, kR8UW);
     mbar_init(sempty, 1);
     fence_mbar_init();
   }
@@ -323,7 +340,8 @@ __global__ void __launch_bounds__(kR8Threads, 1)
     const int Eg = *a.E;
     {
       const double sc = i8::pow2(Eg);
-      for (int i = blockIdx.x * 256 + (threadIdx.x - 128); i < a.n; i += gridDim.x * 256)
+      for (int i = blockIdx.x * (32 * kR8UW) + (threadIdx.x - 128); i < a.n;
+           i += gridDim.x * (32 * kR8UW))
         a.rscale[i] = sc;
     }
     const double qt = 0.25 * a.tt;
@@ -338,12 +356,12 @@ __global__ void __launch_bounds__(kR8Threads, 1)
     double rs = 0.0;
     if (t_begin < t_end) {
       const int i = I * kR8M + r;
-      wraw = (i < a.n) ? __ldg(a.bits + (size_t)i * a.ldb + ((J * kR8N + 16 * h) >> 5)) : 0u;
+      wraw = (i < a.n) ? __ldg(a.bits + (size_t)i * a.ldb + ((J * kR8N + kR8C * h) >> 5)) : 0u;
       rs = __ldg(a.rsA + i);
     }
     for (long long t = t_begin; t < t_end; ++t, ++it) {
       const int i0 = I * kR8M, j0 = J * kR8N;
-      const int i = i0 + r, jb = j0 + 16 * h;
+      const int i = i0 + r, jb = j0 + kR8C * h;
       const bool diagblk = J < 4 * I + 4;             // inside the 128 x 128 diagonal block
       // mirror inside a 256 x 256 diagonal super-block (written even without mirror_dig)
       const bool sblk = (I & 1) == 0 && (J >> 2) == I + 1;
@@ -355,15 +373,15 @@ __global__ void __launch_bounds__(kR8Threads, 1)
         r8_next(a.TC, In, Jn);
         if (t + 1 < t_end) {
           const int inx = In * kR8M + r;
-          wraw = (inx < a.n) ? __ldg(a.bits + (size_t)inx * a.ldb + ((Jn * kR8N + 16 * h) >> 5)) : 0u;
+          wraw = (inx < a.n) ? __ldg(a.bits + (size_t)inx * a.ldb + ((Jn * kR8N + kR8C * h) >> 5)) : 0u;
           rs = __ldg(a.rsA + inx);
         }
         I = In;
         J = Jn;
       }
-      double cs[16];
+      double cs[kR8C];
 #pragma unroll
-      for (int c = 0; c < 16; c += 2) {
+      for (int c = 0; c < kR8C; c += 2) {
         const double2 v = __ldg(reinterpret_cast<const double2*>(a.rsB + jb + c));
         cs[c] = v.x;
         cs[c + 1] = v.y;
@@ -374,35 +392,37 @@ __global__ void __launch_bounds__(kR8Threads, 1)
       tc::fence_after_sync();
       // levels in pairs: 128 D_l + D_{l+1} is exact in int32 (|D_l| <= (l+1) 64 127^2 < 2^23),
       // then 4 exact conversions; summed smallest weight first
-      double w[16];
-      const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(tb * 256 + 16 * h);
+      double w[kR8C];
+      const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(tb * 256 + kR8C * h);
       {
-        uint32_t r6[16];
-        i8::tmem_ld16(taddr + (uint32_t)(6 * kR8N), r6);
+        uint32_t r6[kR8C];
+        tmem_ld_c(taddr + (uint32_t)(6 * kR8N), r6);
 #pragma unroll
-        for (int c = 0; c < 16; ++c) w[c] = (double)(int)r6[c] * i8::pow2(-56);
+        for (int c = 0; c < kR8C; ++c) w[c] = (double)(int)r6[c] * i8::pow2(-56);
       }
 #pragma unroll 1
       for (int L = 4; L >= 0; L -= 2) {
-        uint32_t ra[16], rb2[16];
-        i8::tmem_ld16(taddr + (uint32_t)(L * kR8N), ra);
-        i8::tmem_ld16(taddr + (uint32_t)((L + 1) * kR8N), rb2);
+        uint32_t ra[kR8C], rb2[kR8C];
+        tmem_ld_c(taddr + (uint32_t)(L * kR8N), ra);
+        tmem_ld_c(taddr + (uint32_t)((L + 1) * kR8N), rb2);
         const double wl = i8::pow2(-7 * (L + 3));
 #pragma unroll
-        for (int c = 0; c < 16; ++c) w[c] = fma((double)((int)ra[c] * 128 + (int)rb2[c]), wl, w[c]);
+        for (int c = 0; c < kR8C; ++c) w[c] = fma((double)((int)ra[c] * 128 + (int)rb2[c]), wl, w[c]);
       }
       tc::fence_before_sync();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[tb]);  // the MMA may refill this accumulator
 #pragma unroll
-      for (int c = 0; c < 16; ++c) w[c] *= rsi * cs[c];  // exact: powers of two
+      for (int c = 0; c < kR8C; ++c) w[c] *= rsi * cs[c];  // exact: powers of two
       // ---- Z_old (swizzled 128-byte rows: chunk k of row r at k ^ (r % 8))
       mbar_wait(&zfull[zb], (uint32_t)((it / nz) & 1));
-      double* zrow = reinterpret_cast<double*>(zbuf(zb) + h * 16384 + r * 128);
-      double z[16];
+      // the thread's columns: 16-column box (kR8C h) / 16, its 16-byte chunks k0 .. k0 + kR8C / 2 - 1
+      double* zrow = reinterpret_cast<double*>(zbuf(zb) + ((kR8C * h) >> 4) * 16384 + r * 128);
+      const int k0 = ((kR8C * h) & 15) >> 1;
+      double z[kR8C];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const double2 v = *reinterpret_cast<const double2*>(zrow + 2 * (k ^ sw));
+      for (int k = 0; k < kR8C / 2; ++k) {
+        const double2 v = *reinterpret_cast<const double2*>(zrow + 2 * ((k0 + k) ^ sw));
         z[2 * k] = v.x;
         z[2 * k + 1] = v.y;
       }
@@ -410,7 +430,7 @@ __global__ void __launch_bounds__(kR8Threads, 1)
       if (fast) {
         double ts0 = 0.0, ts1 = 0.0;
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
+        for (int c = 0; c < kR8C; ++c) {
           const bool b = (word >> c) & 1u;
           const double x = w[c];
           const double o = b ? x - qt : x;          // W_ij - t C_ij, C_ij = adj_ij / 4
@@ -424,7 +444,7 @@ __global__ void __launch_bounds__(kR8Threads, 1)
       } else {
         const double wgt = diagblk ? 1.0 : 2.0;
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
+        for (int c = 0; c < kR8C; ++c) {
           const int j = jb + c;
           const double x = w[c], zold = z[c];
           double o = 0.0;                           // outside the matrix: 0 (digits too)
@@ -444,21 +464,24 @@ __global__ void __launch_bounds__(kR8Threads, 1)
         }
       }
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        *reinterpret_cast<double2*>(zrow + 2 * (k ^ sw)) = make_double2(z[2 * k], z[2 * k + 1]);
+      for (int k = 0; k < kR8C / 2; ++k)
+        *reinterpret_cast<double2*>(zrow + 2 * ((k0 + k) ^ sw)) = make_double2(z[2 * k], z[2 * k + 1]);
       // ---- digit slices of Z_new (scale 2^Eg): word g of slice s = columns 4g .. 4g+3
-      uint32_t dw[4][kR8S];
+      uint32_t dw[kR8C / 4][kR8S];
 #pragma unroll
-      for (int g = 0; g < 4; ++g)
+      for (int g = 0; g < kR8C / 4; ++g)
         i8::slices4<kR8S>(z[4 * g], z[4 * g + 1], z[4 * g + 2], z[4 * g + 3], Eg, dw[g]);
       mbar_wait(sempty, (it & 1) ^ 1u);             // the previous tile's stores read the staging
       // tile digits: [slice][row][32 B], SWIZZLE_32B (16-byte chunk ^= bit 7 of the offset)
 #pragma unroll
       for (int s = 0; s < kR8S; ++s) {
-        int off = s * 4096 + r * 32 + 16 * h;
+        int off = s * 4096 + r * 32 + kR8C * h;
         off ^= ((off >> 7) & 1) << 4;
-        *reinterpret_cast<uint4*>(smem + kOffDt + off) =
-            make_uint4(dw[0][s], dw[1][s], dw[2][s], dw[3][s]);
+        if constexpr (kR8C == 16)
+          *reinterpret_cast<uint4*>(smem + kOffDt + off) =
+              make_uint4(dw[0][s], dw[1][s], dw[kR8C / 4 - 2][s], dw[kR8C / 4 - 1][s]);
+        else
+          *reinterpret_cast<uint2*>(smem + kOffDt + off) = make_uint2(dw[0][s], dw[1][s]);
       }
       if (!diagblk) {
         // mirror fp64: box k = r / 16 holds mirror rows jj = 0..31 (tile columns), columns
@@ -467,8 +490,8 @@ __global__ void __launch_bounds__(kR8Threads, 1)
           unsigned char* mb = smem + kOffM + (r >> 4) * 4096;
           const int mc = r & 15;
 #pragma unroll
-          for (int c = 0; c < 16; ++c) {
-            const int jj = 16 * h + c;
+          for (int c = 0; c < kR8C; ++c) {
+            const int jj = kR8C * h + c;
             *reinterpret_cast<double*>(mb + jj * 128 + ((((mc >> 1) ^ (jj & 7))) << 4) +
                                        (mc & 1) * 8) = z[c];
           }
@@ -482,8 +505,8 @@ __global__ void __launch_bounds__(kR8Threads, 1)
         // directly even in lower-transposed mode)
         if (a.mirror_dig || sblk)
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          const int jj = 16 * h + 4 * g + u;
+        for (int g = 0; g < kR8C / 4; ++g) {
+          const int jj = kR8C * h + 4 * g + u;
 #pragma unroll
           for (int s = 0; s < kR8S; ++s) {
             const uint32_t x = dw[g][s];
