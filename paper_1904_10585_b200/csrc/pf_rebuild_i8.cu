@@ -24,8 +24,9 @@
 //   warp 2   TMEM allocation
 //   warp 3   TMA stores: Z_new tile (from the Z_old buffer, updated in place), mirror tile, digit
 //            slices of both; releases the buffers when the stores have read them
-//   warps 4-11  TMEM lane = tile row r, 16 columns (h): levels combined in fp64, the update,
-//            Z_new in place, the mirror (transposed) and the digit slices into staging
+//   warps 4-19  (kR8UW = 16 update warps) TMEM lane = tile row r, kR8C = 8 columns (h = 0..3):
+//            levels combined in fp64, the update, Z_new in place, the mirror (transposed) and
+//            the digit slices into staging
 // Deterministic sums: fixed per-thread order, CTA partials summed in CTA order by the last CTA.
 #include <algorithm>
 #include <cmath>
